@@ -1,0 +1,426 @@
+"""Pins of the CPU oracle against what the paper and mathematics fix (not the
+oracle's own formulas).  Runs on CPU (`-m "not gpu"`).
+
+Each test names the passage it pins.  A plausible mistake anywhere in the
+oracle (a dropped term, a wrong sign, a transposed operand) fails one of them:
+  * exp_spec                  vs libm exp in fp64 (<= 2 ulp), exp(0) = 1
+  * phi-bar, Eq. 6            golden values from tests/golden/phi_bar.txt
+  * Sigma, S*phi, EWA         vs scipy rotation + numerically differentiated
+                              pinhole projection (independent Jacobian)
+  * kernel value              one isotropic particle on the optical axis:
+                              textbook Gaussian at sample pixels, all beta
+  * Eq. 3 compositing         T + sum(w) = 1, empty scene, single splat,
+                              permutation invariance, convexity
+  * keys / lists              numpy brute force on tiny inputs
+  * adjoints                  central finite differences of the all-fp64
+                              pipeline, every parameter group incl. beta
+  * beta chain identity       dL/dbeta = rho (1 - phi/2) sum_k dL/dlog s_k
+  * beta = 2 / rho = 0        bit-identical to the Gaussian path (Fig. 4)
+  * SH basis                  orthonormality by Gauss-Legendre quadrature
+"""
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy.spatial.transform import Rotation
+
+import ges_inputs as gi
+from oracle import oracle as O
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def golden_phi():
+    rows = []
+    with open(os.path.join(GOLDEN, "phi_bar.txt")) as f:
+        for line in f:
+            if line.startswith("#") or line.startswith("gamma"):
+                continue
+            b, r, v = line.split()
+            rows.append((float(b), float(r), float(v)))
+    return rows
+
+
+def one_particle(mean, log_scale, quat=(1, 0, 0, 0), logit=0.0, beta=2.0, sh=None, sh_degree=0):
+    K = (sh_degree + 1) ** 2
+    if sh is None:
+        sh = np.zeros((3 * K, 1))
+        sh[0:3, 0] = 0.5
+    f = lambda a: np.ascontiguousarray(np.asarray(a, np.float64).reshape(-1, 1), np.float32)
+    return gi.Particles(f(mean), f(log_scale), f(quat), np.array([logit], np.float32),
+                        np.ascontiguousarray(sh, np.float32), np.array([beta], np.float32), sh_degree)
+
+
+def cam_identity(W=64, H=64, f=60.0, near=0.2):
+    return gi.Camera(W, H, f, f, W / 2.0, H / 2.0, near, np.eye(3, dtype=np.float32), np.zeros(3, np.float32))
+
+
+# --------------------------------------------------------------------------
+# KEYSPEC exp
+# --------------------------------------------------------------------------
+def test_exp_spec_accuracy_and_exact_zero():
+    x = np.linspace(-87.0, 88.0, 400001, dtype=np.float32)
+    y = O.exp_spec(x).astype(np.float64)
+    ref = np.exp(x.astype(np.float64))
+    ulp = np.spacing(ref.astype(np.float32)).astype(np.float64)
+    err = np.abs(y - ref) / ulp
+    assert err.max() <= 2.0, err.max()
+    assert O.exp_spec(np.array([0.0], np.float32))[0] == np.float32(1.0)
+    # reproducible bit pattern (no hidden state)
+    assert np.array_equal(O.exp_spec(x).view(np.uint32), O.exp_spec(x).view(np.uint32))
+
+
+# --------------------------------------------------------------------------
+# phi-bar (Eq. 6) through the whole S1: one isotropic particle on the axis
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("mode", [O.PHI_SCALE, O.PHI_VARIANCE])
+def test_phi_bar_golden_through_projection(mode):
+    z, s, f = 4.0, 0.05, 60.0
+    cam = cam_identity(f=f)
+    for beta, rho, phi in golden_phi():
+        parts = one_particle([0, 0, z], [math.log(s)] * 3, beta=beta)
+        pre = O.preprocess(parts, cam, O.Settings(rho=rho, phi_mode=mode), "f64")
+        m = phi if mode == O.PHI_SCALE else math.sqrt(phi)
+        s32 = math.exp(float(np.float32(math.log(s))))     # parameters are fp32
+        sigma2 = (f * m * s32 / z) ** 2 + 0.3
+        A, B, Cc = pre["cov2d"][:, 0]
+        # rho enters through the fp32 settings struct (rel. error 1.5e-9 -> ~1e-9 in phi)
+        assert abs(A - sigma2) <= 1e-8 * sigma2 and abs(Cc - sigma2) <= 1e-8 * sigma2 and abs(B) < 1e-15
+        assert pre["uv"][0, 0] == cam.cx and pre["uv"][1, 0] == cam.cy
+
+
+def test_beta2_and_rho0_bit_identical_to_gaussian_path():
+    """PAPER.md:294 and Fig. 4 caption: phi-bar(2) = 1 exactly and
+    rho = 0 reduces GES to Gaussian splatting for any beta."""
+    sc = gi.make_config(0)
+    cam = sc.cameras[0]
+    g = O.preprocess(sc.particles, cam, O.Settings(gaussian_only=1), "f32")
+    p2 = sc.particles.subset(slice(None))
+    p2.beta[:] = 2.0
+    b2 = O.preprocess(p2, cam, O.Settings(), "f32")
+    r0 = O.preprocess(sc.particles, cam, O.Settings(rho=0.0), "f32")
+    for k in ("depth", "uv", "conic", "cov2d", "kappa", "rgb", "radius", "rect", "tiles", "status", "flags"):
+        assert np.array_equal(g[k], b2[k]), k
+        assert np.array_equal(g[k], r0[k]), k
+    # and beta != 2 really changes the footprint (phi-bar > 1 for beta > 2)
+    p8 = sc.particles.subset(slice(None))
+    p8.beta[:] = 8.0
+    b8 = O.preprocess(p8, cam, O.Settings(), "f32")
+    vis = (g["status"] == 0) & (b8["status"] == 0)
+    assert np.all(b8["cov2d"][0, vis] > g["cov2d"][0, vis])
+
+
+# --------------------------------------------------------------------------
+# Sigma = R S S^T R^T (S scaled by phi-bar) and EWA Sigma' = J W Sigma W^T J^T
+# --------------------------------------------------------------------------
+def _numeric_jacobian(tcam, fx, fy):
+    def proj(t):
+        return np.array([fx * t[0] / t[2], fy * t[1] / t[2]])
+    J = np.zeros((2, 3))
+    for k in range(3):
+        h = 1e-6 * max(1.0, abs(tcam[k]))
+        e = np.zeros(3)
+        e[k] = h
+        J[:, k] = (proj(tcam + e) - proj(tcam - e)) / (2 * h)
+    return J
+
+
+@pytest.mark.parametrize("mode", [O.PHI_SCALE, O.PHI_VARIANCE])
+def test_covariance_and_ewa_against_independent_construction(mode):
+    rng = np.random.default_rng(7)
+    cam = gi.make_config(2).cameras[3]
+    P = 64
+    mean = rng.normal(0, 0.3, (3, P))
+    log_scale = rng.normal(-3.0, 0.5, (3, P))
+    quat = rng.standard_normal((4, P))
+    beta = rng.uniform(0.5, 8.0, P)
+    parts = gi.Particles(*(np.ascontiguousarray(a, np.float32) for a in
+                           (mean, log_scale, quat, rng.normal(0, 1, P), rng.normal(0, 0.3, (3, P)), beta)), 0)
+    rho = 0.1
+    pre = O.preprocess(parts, cam, O.Settings(rho=rho, phi_mode=mode), "f64")
+    W = cam.R.astype(np.float64)
+    for i in range(P):
+        if pre["status"][i] != 0:
+            continue
+        q = parts.quat[:, i].astype(np.float64)
+        Rq = Rotation.from_quat([q[1], q[2], q[3], q[0]]).as_matrix()   # scipy: (x, y, z, w)
+        phi = 2.0 / (1.0 + math.exp(-(rho * float(parts.beta[i]) - 2 * rho)))
+        m = phi if mode == O.PHI_SCALE else math.sqrt(phi)
+        S = np.diag(np.exp(parts.log_scale[:, i].astype(np.float64)) * m)
+        Sigma = Rq @ S @ S.T @ Rq.T
+        tcam = W @ parts.mean[:, i].astype(np.float64) + cam.t.astype(np.float64)
+        lim = 1.3 * 0.5 * cam.width / cam.fx
+        if abs(tcam[0] / tcam[2]) > lim or abs(tcam[1] / tcam[2]) > lim:
+            continue
+        J = _numeric_jacobian(tcam, cam.fx, cam.fy)
+        cov = J @ W @ Sigma @ W.T @ J.T + 0.3 * np.eye(2)
+        got = pre["cov2d"][:, i]
+        scale = abs(cov).max()
+        assert np.allclose(got, [cov[0, 0], cov[0, 1], cov[1, 1]], rtol=0, atol=1e-7 * scale), (i, got, cov)
+        inv = np.linalg.inv(cov)
+        assert np.allclose(pre["conic"][:, i], [inv[0, 0], inv[0, 1], inv[1, 1]], rtol=1e-7, atol=0)
+        u = cam.fx * tcam[0] / tcam[2] + cam.cx
+        v = cam.fy * tcam[1] / tcam[2] + cam.cy
+        assert abs(pre["uv"][0, i] - u) < 1e-9 and abs(pre["uv"][1, i] - v) < 1e-9
+        lam = np.linalg.eigvalsh(cov).max()
+        mid = 0.5 * (cov[0, 0] + cov[1, 1])
+        if mid * mid - np.linalg.det(cov) > 0.2:   # away from the 0.1 floor reading (R7)
+            assert pre["radius"][i] == math.ceil(3 * math.sqrt(lam))
+
+
+def test_projection_properties():
+    """SPEC.md:432-450 projection properties: doubling depth halves the std,
+    camera roll leaves an isotropic footprint invariant."""
+    cam = cam_identity(W=256, H=256, f=200.0)
+    st = O.Settings(rho=0.0)
+    s = 0.05
+    a = O.preprocess(one_particle([0, 0, 2.0], [math.log(s)] * 3), cam, st, "f64")
+    b = O.preprocess(one_particle([0, 0, 4.0], [math.log(s)] * 3), cam, st, "f64")
+    va, vb = a["cov2d"][0, 0] - 0.3, b["cov2d"][0, 0] - 0.3
+    assert abs(math.sqrt(va) / math.sqrt(vb) - 2.0) < 1e-12
+    # roll: rotate the camera about its optical axis
+    th = 0.7
+    Rz = np.array([[math.cos(th), -math.sin(th), 0], [math.sin(th), math.cos(th), 0], [0, 0, 1]], np.float32)
+    cam_r = gi.Camera(256, 256, 200.0, 200.0, 128.0, 128.0, 0.2, Rz, np.zeros(3, np.float32))
+    p = one_particle([0.1, -0.05, 3.0], [math.log(s)] * 3)
+    e0 = np.linalg.eigvalsh(_cov(O.preprocess(p, cam, st, "f64")))
+    e1 = np.linalg.eigvalsh(_cov(O.preprocess(p, cam_r, st, "f64")))
+    assert np.allclose(e0, e1, rtol=1e-3)  # EWA is a local linearisation: equal to first order
+
+
+def _cov(pre):
+    A, B, C = pre["cov2d"][:, 0]
+    return np.array([[A, B], [B, C]])
+
+
+# --------------------------------------------------------------------------
+# Kernel value at sample pixels (Eq. 2 at beta = 2 is the textbook Gaussian;
+# other beta enter only through phi-bar, Eq. 4-6)
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("beta", [0.5, 1.0, 2.0, 4.0, 8.0])
+@pytest.mark.parametrize("precision,tol", [("f64", 1e-12), ("f32", 2e-6)])
+def test_kernel_value_isotropic_on_axis(beta, precision, tol):
+    f, z, s, logit = 60.0, 4.0, 0.12, 0.3
+    cam = cam_identity(W=64, H=64, f=f)
+    bg = (0.1, 0.2, 0.3)
+    st = O.Settings(rho=0.1, background=bg)
+    sh0 = np.array([0.2, -0.4, 0.7])
+    sh = sh0.reshape(3, 1)
+    parts = one_particle([0, 0, z], [math.log(s)] * 3, logit=logit, beta=beta, sh=sh)
+    out = O.render(parts, cam, st, precision)
+    r32 = lambda v: float(np.float32(v))          # the particle/settings structs are fp32
+    rho = r32(0.1)
+    phi = 2.0 / (1.0 + math.exp(-(rho * beta - 2 * rho)))
+    sig2 = (f * phi * math.exp(r32(math.log(s))) / z) ** 2 + 0.3
+    kappa = 1.0 / (1.0 + math.exp(-r32(logit)))
+    Y00 = 0.5 / math.sqrt(math.pi)
+    rgb = np.maximum(Y00 * sh0.astype(np.float32).astype(np.float64) + 0.5, 0.0)
+    bgc = np.array([np.float32(c) for c in bg], np.float64)
+    sig = math.sqrt(sig2)
+    for (py, px) in [(32, 32), (32, 35), (29, 31), (33, 38), (36, 36)]:
+        d2 = (px + 0.5 - 32.0) ** 2 + (py + 0.5 - 32.0) ** 2
+        if math.sqrt(d2) > 2.5 * sig:
+            continue
+        alpha = min(0.99, kappa * math.exp(-0.5 * d2 / sig2))
+        expect = alpha * rgb + (1 - alpha) * bgc if alpha >= 1 / 255 else bgc
+        got = out["image"][:, py, px]
+        assert np.allclose(got, expect, rtol=0, atol=tol), (py, px, got, expect)
+
+
+# --------------------------------------------------------------------------
+# Eq. 3 discrete compositing invariants
+# --------------------------------------------------------------------------
+def _white(parts):
+    p = parts.subset(slice(None))
+    p.sh[:] = 0.0
+    p.sh[0:3] = math.sqrt(math.pi)  # Y00 * sh = 0.5 -> rgb = 1 (up to fp32 rounding of sh)
+    return p
+
+
+def test_transmittance_plus_weights_is_one():
+    sc = gi.make_config(0)
+    cam = sc.cameras[0]
+    out = O.render(_white(sc.particles), cam, O.Settings(), "f32")
+    # rgb = const (degree-0 SH, same coefficients), bg = 0  =>  image = rgb * sum_i w_i
+    rgb0 = float(out["pre"]["rgb"][0, out["pre"]["status"] == 0][0])
+    assert abs(rgb0 - 1.0) < 1e-6
+    s = out["image"][0] / rgb0 + out["final_T"]
+    assert np.abs(s - 1.0).max() < 1e-12
+    assert np.all(out["final_T"] <= 1.0) and np.all(out["final_T"] >= 0.0)
+    # early termination keeps T >= 1e-4 (R12)
+    assert out["final_T"].min() >= np.float32(1e-4)
+
+
+def test_empty_scene_and_single_splat_at_center():
+    cam = cam_identity(W=32, H=32, f=30.0)
+    bg = (0.25, 0.5, 0.75)
+    bgc = np.array([np.float32(c) for c in bg], np.float64)
+    far = one_particle([0, 0, 0.1], [-2, -2, -2])  # behind the near plane
+    out = O.render(far, cam, O.Settings(background=bg), "f64")
+    assert np.allclose(out["image"], bgc[:, None, None], atol=0)
+    # splat centred exactly on a pixel centre: d = 0, G = 1, alpha = kappa
+    z = 3.0
+    x = (16.5 - 16.0) * z / 30.0
+    p = one_particle([x, x, z], [-2.5] * 3, logit=0.4)
+    out = O.render(p, cam, O.Settings(background=bg), "f64")
+    kappa = 1 / (1 + math.exp(-0.4))
+    rgb = 0.5 / math.sqrt(math.pi) * 0.5 + 0.5
+    assert np.allclose(out["image"][:, 16, 16], kappa * rgb + (1 - kappa) * bgc, atol=1e-12)
+
+
+def test_permutation_invariance_and_convexity():
+    sc = gi.make_config(0, P=400)
+    cam = sc.cameras[0]
+    a = O.render(sc.particles, cam, O.Settings(), "f64")
+    perm = np.random.default_rng(3).permutation(sc.particles.P)
+    b = O.render(sc.particles.subset(perm), cam, O.Settings(), "f64")
+    assert np.abs(a["image"] - b["image"]).max() < 1e-12
+    assert a["image"].min() >= 0.0 and a["image"].max() <= 1.0
+
+
+# --------------------------------------------------------------------------
+# Keys, sort, lists: numpy brute force on tiny inputs
+# --------------------------------------------------------------------------
+def test_keys_and_lists_bruteforce():
+    sc = gi.make_config(0, P=300)
+    cam = sc.cameras[0]
+    pre = O.preprocess(sc.particles, cam, O.Settings(), "f32")
+    keys, vals = O.pairs_sorted(pre)
+    tx = pre["tiles_x"]
+    db = pre["depth"].view(np.uint32)
+    ek, ev = [], []
+    for i in range(sc.particles.P):
+        if pre["status"][i] != 0:
+            continue
+        x0, y0, x1, y1 = pre["rect"][:, i]
+        for y in range(y0, y1):
+            for x in range(x0, x1):
+                ek.append((int(y * tx + x) << 32) | int(db[i]))
+                ev.append(i)
+    ek, ev = np.array(ek, np.uint64), np.array(ev, np.int32)
+    o = np.lexsort((ev, ek))
+    assert np.array_equal(keys, ek[o]) and np.array_equal(vals, ev[o])
+    offsets, lst = O.tile_lists(pre)
+    tiles = (keys >> np.uint64(32)).astype(np.int64)
+    for t in range(tx * pre["tiles_y"]):
+        sel = vals[tiles == t]
+        assert np.array_equal(lst[offsets[t]:offsets[t + 1]], sel)
+    # ranges by linear scan == offsets
+    ranges = np.searchsorted(tiles, np.arange(tx * pre["tiles_y"] + 1))
+    assert np.array_equal(ranges, offsets)
+
+
+# --------------------------------------------------------------------------
+# Adjoints vs central finite differences (all-fp64 pipeline)
+# --------------------------------------------------------------------------
+def _fd_check(scene, st, n_checks=None, rel=1e-5, seed=0):
+    cam = scene.cameras[0]
+    parts = scene.particles
+    O.set_amb_margin(1e-3)
+    try:
+        base = O.render(parts, cam, st, "f64")
+    finally:
+        O.set_amb_margin(0.0)
+    g = gi.upstream_grad(seed, 0, cam.width, cam.height).astype(np.float64)
+    g[:, base["amb"] != 0] = 0.0   # never straddle a skip/stop/clamp decision
+    pre = base["pre"]
+    g2d = O.render_bwd(pre, cam, st, base["offsets"], base["list"], g)
+    grads = O.backward_particles(parts, cam, st, g2d, pre["status"], pre["flags"])
+    fails = []
+    names = ("mean", "log_scale", "quat", "opacity_logit", "sh", "beta")
+    for n in names:
+        arr = getattr(parts, n)
+        ga = grads[n]
+        for idx in np.ndindex(arr.shape):
+            i = idx[-1]
+            if pre["status"][i] != 0:
+                continue
+            p64 = gi.Particles(*(np.array(getattr(parts, m), np.float64) for m in names[:5]),
+                               np.array(parts.beta, np.float64), parts.sh_degree)
+            x0 = float(getattr(p64, n)[idx])
+            h = 1e-6 * max(1.0, abs(x0))
+            getattr(p64, n)[idx] = x0 + h
+            lp = O.loss_f64(p64, cam, st, g)
+            getattr(p64, n)[idx] = x0 - h
+            lm = O.loss_f64(p64, cam, st, g)
+            fd = (lp - lm) / (2 * h)
+            an = float(ga[idx])
+            if abs(fd - an) > rel * max(abs(fd), abs(an)) + 1e-8:
+                fails.append((n, idx, an, fd))
+    assert not fails, fails[:10]
+    return grads
+
+
+@pytest.mark.parametrize("seed,deg,mode", [(1, 0, O.PHI_SCALE), (2, 1, O.PHI_SCALE), (3, 3, O.PHI_VARIANCE),
+                                           (4, 3, O.PHI_SCALE)])
+def test_gradients_finite_differences(seed, deg, mode):
+    sc = gi.random_small_scene(seed, P=5, W=32, H=32, sh_degree=deg, kappa_max=0.6)
+    st = O.Settings(rho=0.1, phi_mode=mode, background=(0.1, 0.3, 0.2))
+    _fd_check(sc, st)
+
+
+def test_gradients_fd_large_rho_and_off_axis_camera():
+    sc = gi.random_small_scene(11, P=4, W=48, H=32, sh_degree=2, kappa_max=0.6)
+    cam = sc.cameras[0]
+    R, t = gi.look_at((0.4, -0.3, -0.5), target=(0.0, 0.0, 4.0))
+    sc.cameras[0] = gi.Camera(cam.width, cam.height, cam.fx, cam.fy * 1.1, cam.cx + 1.5, cam.cy - 2.0, 0.2, R, t)
+    _fd_check(sc, O.Settings(rho=0.5))
+
+
+def test_beta_gradient_identity_and_zero_cases():
+    """dL/dbeta = rho phi'(beta)/phi ... : with s_eff = s*m(beta),
+    dL/dbeta = (dm/dbeta / m) * sum_k dL/dlog s_k; m = phi (SCALE) gives
+    rho (1 - phi/2), m = sqrt(phi) gives half that (Eq. 6 derivative)."""
+    sc = gi.make_config(0, P=500)
+    cam = sc.cameras[0]
+    g = gi.upstream_grad(sc.seed, 0, cam.width, cam.height)
+    for mode, fac in ((O.PHI_SCALE, 1.0), (O.PHI_VARIANCE, 0.5)):
+        st = O.Settings(rho=0.1, phi_mode=mode)
+        r = O.render_and_grad(sc.particles, cam, st, g)
+        rho = float(np.float32(0.1))   # settings carry fp32 rho
+        phi = 2.0 / (1.0 + np.exp(-(rho * sc.particles.beta.astype(np.float64) - 2 * rho)))
+        expect = fac * rho * (1 - phi / 2) * r["grads"]["log_scale"].sum(axis=0)
+        assert np.allclose(r["grads"]["beta"], expect, rtol=1e-10, atol=1e-14)
+    r0 = O.render_and_grad(sc.particles, cam, O.Settings(rho=0.0), g)
+    assert np.all(r0["grads"]["beta"] == 0.0)
+    rz = O.render_and_grad(sc.particles, cam, O.Settings(), np.zeros_like(g))
+    for v in rz["grads"].values():
+        assert np.all(v == 0.0)
+
+
+def test_sh_gradient_linear_in_upstream():
+    sc = gi.make_config(0, P=300)
+    cam = sc.cameras[0]
+    g = gi.upstream_grad(sc.seed, 0, cam.width, cam.height).astype(np.float64)
+    a = O.render_and_grad(sc.particles, cam, O.Settings(), g)["grads"]["sh"]
+    b = O.render_and_grad(sc.particles, cam, O.Settings(), 2.5 * g)["grads"]["sh"]
+    assert np.allclose(b, 2.5 * a, rtol=1e-12, atol=1e-15)
+
+
+# --------------------------------------------------------------------------
+# SH basis: orthonormal on the sphere (pins constants and polynomials)
+# --------------------------------------------------------------------------
+def test_sh_basis_orthonormal():
+    n = 24
+    xg, wg = np.polynomial.legendre.leggauss(n)        # cos(theta)
+    phis = np.arange(2 * n) * (2 * math.pi / (2 * n))  # exact for trig degree < 2n
+    Gram = np.zeros((16, 16))
+    for ct, w in zip(xg, wg):
+        st_ = math.sqrt(1 - ct * ct)
+        for ph in phis:
+            d = (st_ * math.cos(ph), st_ * math.sin(ph), ct)
+            Y = O.sh_basis(d, 16)
+            Gram += w * (2 * math.pi / (2 * n)) * np.outer(Y, Y)
+    assert np.abs(Gram - np.eye(16)).max() < 1e-12
+    # DC constant 1/(2 sqrt(pi)); fp32 KEYSPEC basis agrees with fp64 to fp32 precision
+    assert abs(O.sh_basis((0, 0, 1), 1)[0] - 0.28209479177387814) < 1e-16
+    d = np.array([0.3, -0.5, 0.8])
+    d /= np.linalg.norm(d)
+    assert np.allclose(O.sh_basis(d.astype(np.float32), 16, "f32"), O.sh_basis(d, 16), rtol=2e-6, atol=1e-7)
+
+
+def test_ambiguity_flags_are_rare_on_config0():
+    sc = gi.make_config(0)
+    out = O.render(sc.particles, sc.cameras[0], O.Settings(), "f32")
+    assert (out["amb"] != 0).mean() < 1e-3
