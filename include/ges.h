@@ -1,0 +1,196 @@
+/* include/ges.h -- C ABI of the B200-native GES tile rasterizer (libges.so).
+ *
+ * GES = Generalized Exponential Splatting, arXiv 2402.10128 (/root/reference/
+ * PAPER.md).  The library implements the data-parallel hot path named by
+ * BASELINE.json:north_star, every stage as hand-written sm_100a CUDA:
+ *
+ *   ges_preprocess  S1  per particle: Sigma = R S S^T R^T with S scaled by
+ *                       phi-bar(beta) (Eq. 4 :268-270;
+ *                       Eq. 6 :291-293), EWA projection Sigma' = J W Sigma W^T J^T
+ *                       (PAPER.md:249-253), SH colour and opacity kappa
+ *                       (PAPER.md:247), screen radius and 16x16-tile rect;
+ *                       compacts the visible particles with their depth keys
+ *                       and builds the per-tile pair histogram.
+ *   ges_sort        S2  depth radix sort of the visible particles, duplication
+ *                       into (tile, particle) pairs in depth order, stable
+ *                       radix sort by tile id; the resulting order of every
+ *                       tile's list is the order of the keys
+ *                       (tile_id << 32 | fp32 bits of depth), ties by index.
+ *                   S3  per-tile ranges [ranges[t], ranges[t+1]).
+ *   ges_render_fwd  S4  per 16x16 tile front-to-back alpha compositing with
+ *                       early termination on transmittance (Eq. 3,
+ *                       PAPER.md:259-266; constants DESIGN.md R7).
+ *   ges_render_bwd  S5  adjoint of S4 per tile, then the per-particle chain
+ *                       to mean, log-scale, quaternion, opacity logit, SH and
+ *                       beta ("optimization ... encompasses the beta parameter
+ *                       as well as position, opacity, covariance, SH",
+ *                       PAPER.md:351).
+ *
+ * Conventions (every entry point):
+ *   - Pointers are DEVICE pointers unless the name says *_host.  The caller
+ *     owns every buffer; the library never allocates or frees and keeps no
+ *     global state (re-entrant across distinct frames).  All work is
+ *     stream-ordered on `stream` (a cudaStream_t passed as void*; NULL = the
+ *     legacy default stream) and CUDA-graph capturable; only ges_counts_get
+ *     synchronises.
+ *   - Particles: planar SoA fp32 [C][P] (plane c of particle i at ptr[c*P+i]):
+ *       mean[3][P]; log_scale[3][P]; quat[4][P] (w,x,y,z; any non-zero norm);
+ *       opacity_logit[P] (kappa = sigmoid); sh[3K][P] (plane 3k+channel,
+ *       K = (sh_degree+1)^2, real SH, Condon-Shortley phase, rgb = sum + 0.5,
+ *       clamped >= 0); beta[P] = the TRUE shape parameter (the paper stores
+ *       beta - 2: a storage shift only).
+ *   - Camera: world->camera rotation R (row-major) and translation t, OpenCV
+ *     axes (x right, y down, z forward), pinhole fx, fy, cx, cy in pixels;
+ *     pixel (row i, col j) samples the point (j+0.5, i+0.5).
+ *   - Images are planar fp32 [3][H][W], linear, unclamped.
+ *   - Errors: argument errors return GES_ERR_INVALID_ARG before any launch;
+ *     launch failures return GES_ERR_CUDA.  A frame whose pair count M
+ *     exceeds its capacity sets counts.overflow; ges_sort then writes no
+ *     pairs and the renders draw nothing: the caller regrows the workspace
+ *     (ges_workspace_bytes with a larger capacity) and re-runs.
+ */
+#ifndef GES_H_
+#define GES_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    GES_OK = 0,
+    GES_ERR_INVALID_ARG = 1,
+    GES_ERR_CAPACITY = 2,
+    GES_ERR_CUDA = 3,
+    GES_ERR_UNSUPPORTED = 4
+} ges_status;
+
+/* DESIGN.md R1: phi-bar scales the 3-D scale vector (SCALE: s_eff = phi s,
+ * following "the scales matrix ... modified by phi") or
+ * the variance (VARIANCE: s_eff = sqrt(phi) s, following Eq. 4's "effective
+ * variance").  Both are the identity at beta = 2. */
+typedef enum { GES_PHI_SCALE = 0, GES_PHI_VARIANCE = 1 } ges_phi_mode;
+
+/* Per-particle status written by ges_preprocess into frame.status. */
+typedef enum { GES_VISIBLE = 0, GES_CULL_NEAR = 1, GES_DEGENERATE = 2, GES_OFFSCREEN = 3 } ges_particle_status;
+
+typedef struct {
+    int64_t P;          /* number of particles, 1 <= P <= 2^31 - 1           */
+    int32_t sh_degree;  /* 0..3                                              */
+    int32_t _pad;
+    const float *mean, *log_scale, *quat, *opacity_logit, *sh, *beta;
+} ges_particles;
+
+typedef struct {
+    int32_t width, height;      /* pixels; tiles_x * tiles_y <= 65536        */
+    float fx, fy, cx, cy;       /* pinhole intrinsics (pixels)               */
+    float near_z;               /* particles with camera z <= near_z culled  */
+    float R[9];                 /* world -> camera rotation, row-major       */
+    float t[3];
+} ges_camera;
+
+typedef struct {
+    float rho;                  /* shape strength of Eq. 6 (paper: 0.1); >= 0 */
+    int32_t phi_mode;           /* ges_phi_mode                                              */
+    int32_t gaussian_only;      /* 1: beta ignored (phi = 1) -- the equivalent Gaussian rasterizer */
+    float background[3];
+} ges_settings;
+
+/* Gradients, planar [C][P] fp32 in the parameter layout.  accumulate = 1 adds
+ * into the buffers (several views before one allreduce), 0 overwrites. */
+typedef struct {
+    float *mean, *log_scale, *quat, *opacity_logit, *sh, *beta;
+    int32_t accumulate;
+    int32_t _pad;
+} ges_grads;
+
+typedef struct {
+    int64_t visible;    /* particles with status GES_VISIBLE                     */
+    int64_t pairs;      /* M = sum over visible particles of tiles touched       */
+    int64_t capacity;   /* pair capacity of the frame                            */
+    int32_t overflow;   /* 1 if pairs > capacity: lists and images are invalid   */
+    int32_t _pad;
+} ges_counts;
+
+/* Counter slots inside frame.counters (uint64). */
+enum { GES_CTR_VISIBLE = 0, GES_CTR_PAIRS = 1, GES_CTR_OVERFLOW = 2, GES_CTR_TILE0 = 3, GES_CTR_N = 16 };
+
+/* A frame: every per-frame device array, carved by ges_frame_init out of ONE
+ * caller-owned device workspace.  The struct lives in caller (host) memory;
+ * its fields are public so that tests can read the intermediate arrays. */
+typedef struct {
+    int64_t P, pair_capacity;
+    int32_t width, height, tiles_x, tiles_y, num_tiles, tile_bits;
+    int32_t sh_degree_max, _pad;
+    /* ---- S1 per-particle state ---- */
+    float *depth;          /* [P] camera-space z                                       */
+    float *pay0;           /* [P][4] (u, v, a, b): projected mean, conic a, b           */
+    float *pay1;           /* [P][4] (c, kappa, r, g): conic c, opacity, colour r, g    */
+    float *pay2;           /* [P]    colour b                                           */
+    int32_t *radius;       /* [P] screen radius (pixels)                                */
+    uint16_t *rect;        /* [P][4] tile rect x0, y0, x1, y1 (exclusive ends)           */
+    uint8_t *status;       /* [P] ges_particle_status                                   */
+    uint8_t *flags;        /* [P] bit0-2 rgb clamped at 0, bit3/4 Jacobian x/y clamped   */
+    /* ---- S2 depth sort of the visible particles ---- */
+    uint32_t *vis_key[2];  /* [P] depth bits, ping-pong                                 */
+    uint32_t *vis_val[2];  /* [P] particle index, ping-pong                             */
+    uint32_t *sorted_vis;  /* [P] visible particles in (depth, index) order (alias)     */
+    /* ---- S2 pairs and S3 ranges ---- */
+    uint32_t *pair_tile[2];/* [cap] tile id, ping-pong                                  */
+    uint32_t *pair_val[2]; /* [cap] particle index, ping-pong                           */
+    uint32_t *list;        /* [cap] final per-tile lists (alias of a pair_val buffer)   */
+    uint32_t *ranges;      /* [T+1] list of tile t = list[ranges[t] .. ranges[t+1])      */
+    int32_t *tile_diff;    /* [(tiles_y+1)*(tiles_x+1)] 2-D difference grid of rects    */
+    uint32_t *hist;        /* [8][256] radix digit histograms -> exclusive offsets      */
+    uint32_t *lookback;    /* decoupled look-back scratch                               */
+    uint64_t *counters;    /* [GES_CTR_N]                                               */
+    size_t lookback_bytes;
+    /* ---- S4 / S5 ---- */
+    float *final_T;        /* [H*W] transmittance after the last composited particle   */
+    uint32_t *n_contrib;   /* [H*W] list position of the last composited particle + 1  */
+    float *grad2d;         /* [9][P] dL/d(u, v, a, b, c, kappa, r, g, b)                 */
+    size_t workspace_bytes;
+} ges_frame;
+
+/* Bytes of device workspace a frame needs (256-byte aligned base). */
+size_t ges_workspace_bytes(int64_t P, int32_t width, int32_t height, int64_t pair_capacity);
+
+/* Carve `frame` out of `workspace` (device, >= ges_workspace_bytes(...) bytes,
+ * 256-byte aligned).  Host-only; no device work. */
+ges_status ges_frame_init(void *workspace, size_t bytes, int64_t P, int32_t width, int32_t height,
+                          int64_t pair_capacity, ges_frame *frame);
+
+/* S1.  Writes the per-particle state, the visible list and the tile
+ * histogram of `frame`.  particles/camera/settings are host structs whose
+ * array pointers are device pointers; camera must match the frame size. */
+ges_status ges_preprocess(const ges_particles *particles, const ges_camera *camera, const ges_settings *settings,
+                          ges_frame *frame, void *stream);
+
+/* S2 + S3.  Depth sort, pair duplication, tile sort, ranges. */
+ges_status ges_sort(ges_frame *frame, void *stream);
+
+/* S4.  image: [3][H][W] fp32 (device).  Also writes frame.final_T and
+ * frame.n_contrib.  n_eval (optional, [H*W] u32, may be NULL) receives the
+ * number of list entries each pixel evaluated (diagnostics / roofline). */
+ges_status ges_render_fwd(ges_frame *frame, const ges_settings *settings, float *image, uint32_t *n_eval,
+                          void *stream);
+
+/* S5.  dL_dimage: [3][H][W] fp32 (device).  Writes frame.grad2d, then the
+ * parameter gradients into `grads`. */
+ges_status ges_render_bwd(const ges_particles *particles, const ges_camera *camera, const ges_settings *settings,
+                          ges_frame *frame, const float *dL_dimage, const ges_grads *grads, void *stream);
+
+/* Copies the frame's counts to host memory.  Synchronises `stream`. */
+ges_status ges_counts_get(const ges_frame *frame, ges_counts *host_out, void *stream);
+
+const char *ges_status_string(ges_status s);
+
+/* Library version / build id (static string). */
+const char *ges_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GES_H_ */

@@ -1,0 +1,115 @@
+"""ctypes binding of the C ABI in include/ges.h (argument marshalling only).
+
+Every step of the path runs in libges.so's CUDA kernels; this module only
+mirrors the C structs.  Importing it on a machine without the built library
+raises immediately -- there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import _build
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libges.so")
+
+GES_OK, GES_ERR_INVALID_ARG, GES_ERR_CAPACITY, GES_ERR_CUDA, GES_ERR_UNSUPPORTED = range(5)
+GES_PHI_SCALE, GES_PHI_VARIANCE = 0, 1
+GES_VISIBLE, GES_CULL_NEAR, GES_DEGENERATE, GES_OFFSCREEN = range(4)
+GES_CTR_VISIBLE, GES_CTR_PAIRS, GES_CTR_OVERFLOW, GES_CTR_TILE0, GES_CTR_N = 0, 1, 2, 3, 16
+
+_fp = C.POINTER(C.c_float)
+_u32p = C.POINTER(C.c_uint32)
+
+
+class ges_particles(C.Structure):
+    _fields_ = [("P", C.c_int64), ("sh_degree", C.c_int32), ("_pad", C.c_int32)] + [
+        (n, C.c_void_p) for n in ("mean", "log_scale", "quat", "opacity_logit", "sh", "beta")]
+
+
+class ges_camera(C.Structure):
+    _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("fx", C.c_float), ("fy", C.c_float),
+                ("cx", C.c_float), ("cy", C.c_float), ("near_z", C.c_float), ("R", C.c_float * 9),
+                ("t", C.c_float * 3)]
+
+
+class ges_settings(C.Structure):
+    _fields_ = [("rho", C.c_float), ("phi_mode", C.c_int32), ("gaussian_only", C.c_int32),
+                ("background", C.c_float * 3)]
+
+
+class ges_grads(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("mean", "log_scale", "quat", "opacity_logit", "sh", "beta")] + [
+        ("accumulate", C.c_int32), ("_pad", C.c_int32)]
+
+
+class ges_counts(C.Structure):
+    _fields_ = [("visible", C.c_int64), ("pairs", C.c_int64), ("capacity", C.c_int64), ("overflow", C.c_int32),
+                ("_pad", C.c_int32)]
+
+
+class ges_frame(C.Structure):
+    _fields_ = [
+        ("P", C.c_int64), ("pair_capacity", C.c_int64),
+        ("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
+        ("num_tiles", C.c_int32), ("tile_bits", C.c_int32), ("sh_degree_max", C.c_int32), ("_pad", C.c_int32),
+        ("depth", C.c_void_p), ("pay0", C.c_void_p), ("pay1", C.c_void_p), ("pay2", C.c_void_p),
+        ("radius", C.c_void_p), ("rect", C.c_void_p), ("status", C.c_void_p), ("flags", C.c_void_p),
+        ("vis_key", C.c_void_p * 2), ("vis_val", C.c_void_p * 2), ("sorted_vis", C.c_void_p),
+        ("pair_tile", C.c_void_p * 2), ("pair_val", C.c_void_p * 2), ("list", C.c_void_p),
+        ("ranges", C.c_void_p), ("tile_diff", C.c_void_p), ("hist", C.c_void_p), ("lookback", C.c_void_p),
+        ("counters", C.c_void_p), ("lookback_bytes", C.c_size_t),
+        ("final_T", C.c_void_p), ("n_contrib", C.c_void_p), ("grad2d", C.c_void_p),
+        ("workspace_bytes", C.c_size_t),
+    ]
+
+
+EXPORTS = ["ges_workspace_bytes", "ges_frame_init", "ges_preprocess", "ges_sort", "ges_render_fwd",
+           "ges_render_bwd", "ges_counts_get", "ges_status_string", "ges_version"]
+
+_lib = None
+
+
+class GESError(RuntimeError):
+    pass
+
+
+def load(build_if_missing: bool = True) -> C.CDLL:
+    """Loads libges.so (building it first if the sources are newer)."""
+    global _lib
+    if _lib is None:
+        if build_if_missing:
+            _build.build()
+        if not os.path.exists(LIB_PATH):
+            raise GESError(f"libges.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        L.ges_workspace_bytes.restype = C.c_size_t
+        L.ges_workspace_bytes.argtypes = [C.c_int64, C.c_int32, C.c_int32, C.c_int64]
+        L.ges_frame_init.restype = C.c_int
+        L.ges_frame_init.argtypes = [C.c_void_p, C.c_size_t, C.c_int64, C.c_int32, C.c_int32, C.c_int64,
+                                     C.POINTER(ges_frame)]
+        L.ges_preprocess.restype = C.c_int
+        L.ges_preprocess.argtypes = [C.POINTER(ges_particles), C.POINTER(ges_camera), C.POINTER(ges_settings),
+                                     C.POINTER(ges_frame), C.c_void_p]
+        L.ges_sort.restype = C.c_int
+        L.ges_sort.argtypes = [C.POINTER(ges_frame), C.c_void_p]
+        L.ges_render_fwd.restype = C.c_int
+        L.ges_render_fwd.argtypes = [C.POINTER(ges_frame), C.POINTER(ges_settings), C.c_void_p, C.c_void_p,
+                                     C.c_void_p]
+        L.ges_render_bwd.restype = C.c_int
+        L.ges_render_bwd.argtypes = [C.POINTER(ges_particles), C.POINTER(ges_camera), C.POINTER(ges_settings),
+                                     C.POINTER(ges_frame), C.c_void_p, C.POINTER(ges_grads), C.c_void_p]
+        L.ges_counts_get.restype = C.c_int
+        L.ges_counts_get.argtypes = [C.POINTER(ges_frame), C.POINTER(ges_counts), C.c_void_p]
+        L.ges_status_string.restype = C.c_char_p
+        L.ges_status_string.argtypes = [C.c_int]
+        L.ges_version.restype = C.c_char_p
+        _lib = L
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    if status != GES_OK:
+        msg = load().ges_status_string(status).decode()
+        raise GESError(f"{what} failed: {msg} ({status})")

@@ -1,0 +1,216 @@
+"""Thin Python binding of the GES C ABI (include/ges.h).
+
+PyTorch is used for device memory, streams and process groups only; every
+step of the rasterizer runs in libges.so's sm_100a kernels.  The four entry
+points keep the C names (ges_preprocess, ges_sort, ges_render_fwd,
+ges_render_bwd); `Renderer` is a convenience owner of one frame workspace.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+from typing import Optional, Sequence
+
+import torch
+
+from . import _lib as L
+
+PARAM_NAMES = ("mean", "log_scale", "quat", "opacity_logit", "sh", "beta")
+
+
+def plane_counts(sh_degree: int):
+    K = (sh_degree + 1) ** 2
+    return {"mean": 3, "log_scale": 3, "quat": 4, "opacity_logit": 1, "sh": 3 * K, "beta": 1}
+
+
+def n_planes(sh_degree: int) -> int:
+    return sum(plane_counts(sh_degree).values())
+
+
+@dataclasses.dataclass
+class Settings:
+    rho: float = 0.1                 # PAPER.md:397 "shape strength ... 0.1"
+    phi_mode: int = L.GES_PHI_SCALE
+    gaussian_only: int = 0
+    background: Sequence[float] = (0.0, 0.0, 0.0)
+
+    def c(self) -> L.ges_settings:
+        s = L.ges_settings()
+        s.rho, s.phi_mode, s.gaussian_only = float(self.rho), int(self.phi_mode), int(self.gaussian_only)
+        for k in range(3):
+            s.background[k] = float(self.background[k])
+        return s
+
+
+class PlanarParams:
+    """Planar SoA fp32 buffer [C][P] (one allocation) with named plane views."""
+
+    def __init__(self, flat: torch.Tensor, P: int, sh_degree: int):
+        assert flat.dtype == torch.float32 and flat.is_contiguous() and flat.shape == (n_planes(sh_degree), P)
+        self.flat, self.P, self.sh_degree = flat, P, sh_degree
+        o = 0
+        for n, c in plane_counts(sh_degree).items():
+            v = flat[o:o + c]
+            setattr(self, n, v[0] if n in ("opacity_logit", "beta") else v)
+            o += c
+
+    @classmethod
+    def empty(cls, P: int, sh_degree: int, device="cuda", pin_memory=False):
+        t = torch.empty((n_planes(sh_degree), P), dtype=torch.float32, device=device, pin_memory=pin_memory)
+        return cls(t, P, sh_degree)
+
+    @classmethod
+    def zeros(cls, P: int, sh_degree: int, device="cuda"):
+        return cls(torch.zeros((n_planes(sh_degree), P), dtype=torch.float32, device=device), P, sh_degree)
+
+    @classmethod
+    def from_inputs(cls, parts, device="cuda", pin_memory=False):
+        """From a ges_inputs.Particles (numpy planes)."""
+        flat = torch.from_numpy(parts.flat())
+        if pin_memory:
+            flat = flat.pin_memory()
+        if device != "cpu":
+            flat = flat.to(device)
+        return cls(flat.contiguous(), parts.P, parts.sh_degree)
+
+    def c_particles(self) -> L.ges_particles:
+        p = L.ges_particles()
+        p.P, p.sh_degree = self.P, self.sh_degree
+        for n in PARAM_NAMES:
+            setattr(p, n, getattr(self, n).data_ptr())
+        return p
+
+    def c_grads(self, accumulate: bool) -> L.ges_grads:
+        g = L.ges_grads()
+        for n in PARAM_NAMES:
+            setattr(g, n, getattr(self, n).data_ptr())
+        g.accumulate = 1 if accumulate else 0
+        return g
+
+
+def c_camera(cam) -> L.ges_camera:
+    """From any object with width, height, fx, fy, cx, cy, near, R (3x3), t (3)."""
+    c = L.ges_camera()
+    c.width, c.height = int(cam.width), int(cam.height)
+    c.fx, c.fy, c.cx, c.cy, c.near_z = cam.fx, cam.fy, cam.cx, cam.cy, cam.near
+    R = [float(x) for x in list(cam.R.reshape(9))]
+    t = [float(x) for x in list(cam.t.reshape(3))]
+    for k in range(9):
+        c.R[k] = R[k]
+    for k in range(3):
+        c.t[k] = t[k]
+    return c
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+class Frame:
+    """One frame workspace (a single torch uint8 allocation) and its C struct."""
+
+    def __init__(self, P: int, width: int, height: int, pair_capacity: int, device="cuda"):
+        lib = L.load()
+        nbytes = lib.ges_workspace_bytes(P, width, height, pair_capacity)
+        if nbytes == 0:
+            raise L.GESError("invalid frame size")
+        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+        base = self.ws.data_ptr()
+        self.offset = (-base) % 256
+        self.c = L.ges_frame()
+        L.check(lib.ges_frame_init(C.c_void_p(base + self.offset), nbytes, P, width, height, pair_capacity,
+                                   C.byref(self.c)), "ges_frame_init")
+        self.P, self.width, self.height, self.pair_capacity = P, width, height, pair_capacity
+
+    # --- typed views into the workspace (tests / diagnostics) ---
+    def view(self, field: str, dtype: torch.dtype, count: int, index: Optional[int] = None) -> torch.Tensor:
+        ptr = getattr(self.c, field)
+        if index is not None:
+            ptr = ptr[index]
+        off = ptr - self.ws.data_ptr()
+        esz = torch.tensor([], dtype=dtype).element_size()
+        return self.ws[off:off + count * esz].view(dtype)
+
+    def counts(self, stream=None) -> L.ges_counts:
+        out = L.ges_counts()
+        L.check(L.load().ges_counts_get(C.byref(self.c), C.byref(out), C.c_void_p(_stream(stream))),
+                "ges_counts_get")
+        return out
+
+    @property
+    def num_tiles(self) -> int:
+        return self.c.num_tiles
+
+    def ranges(self):
+        return self.view("ranges", torch.int32, self.num_tiles + 1)
+
+    def list(self, M: int):
+        return self.view("list", torch.int32, M)
+
+
+# --- the four C entry points, same names ------------------------------------
+def ges_preprocess(particles: PlanarParams, camera, settings: Settings, frame: Frame, stream=None) -> None:
+    p, c, s = particles.c_particles(), c_camera(camera), settings.c()
+    L.check(L.load().ges_preprocess(C.byref(p), C.byref(c), C.byref(s), C.byref(frame.c), C.c_void_p(_stream(stream))),
+            "ges_preprocess")
+
+
+def ges_sort(frame: Frame, stream=None) -> None:
+    L.check(L.load().ges_sort(C.byref(frame.c), C.c_void_p(_stream(stream))), "ges_sort")
+
+
+def ges_render_fwd(frame: Frame, settings: Settings, image: torch.Tensor, n_eval: Optional[torch.Tensor] = None,
+                   stream=None) -> None:
+    assert image.dtype == torch.float32 and image.is_contiguous() and image.numel() == 3 * frame.width * frame.height
+    s = settings.c()
+    ne = C.c_void_p(n_eval.data_ptr()) if n_eval is not None else None
+    L.check(L.load().ges_render_fwd(C.byref(frame.c), C.byref(s), C.c_void_p(image.data_ptr()), ne,
+                                    C.c_void_p(_stream(stream))), "ges_render_fwd")
+
+
+def ges_render_bwd(particles: PlanarParams, camera, settings: Settings, frame: Frame, dL_dimage: torch.Tensor,
+                   grads: PlanarParams, accumulate: bool = False, stream=None) -> None:
+    assert dL_dimage.dtype == torch.float32 and dL_dimage.is_contiguous()
+    p, c, s, g = particles.c_particles(), c_camera(camera), settings.c(), grads.c_grads(accumulate)
+    L.check(L.load().ges_render_bwd(C.byref(p), C.byref(c), C.byref(s), C.byref(frame.c),
+                                    C.c_void_p(dL_dimage.data_ptr()), C.byref(g), C.c_void_p(_stream(stream))),
+            "ges_render_bwd")
+
+
+class Renderer:
+    """Owns a frame workspace sized for (P, W, H) and grows the pair capacity
+    on overflow (one synchronising count read the first time)."""
+
+    def __init__(self, P: int, width: int, height: int, pair_capacity: Optional[int] = None, device="cuda"):
+        self.P, self.width, self.height, self.device = P, width, height, device
+        cap = pair_capacity or max(1 << 16, 16 * P)
+        self.frame = Frame(P, width, height, cap, device)
+
+    def grow(self, M: int) -> None:
+        cap = int(M * 1.25) + 1024
+        self.frame = Frame(self.P, self.width, self.height, cap, self.device)
+
+    def forward(self, particles: PlanarParams, camera, settings: Settings, image: Optional[torch.Tensor] = None,
+                n_eval=None, stream=None, check_overflow: bool = True) -> torch.Tensor:
+        if image is None:
+            image = torch.empty((3, self.height, self.width), dtype=torch.float32, device=self.device)
+        for _ in range(3):
+            ges_preprocess(particles, camera, settings, self.frame, stream)
+            ges_sort(self.frame, stream)
+            ges_render_fwd(self.frame, settings, image, n_eval, stream)
+            if not check_overflow:
+                break
+            cnt = self.frame.counts(stream)
+            if not cnt.overflow:
+                break
+            self.grow(cnt.pairs)
+        return image
+
+    def backward(self, particles: PlanarParams, camera, settings: Settings, dL_dimage: torch.Tensor,
+                 grads: Optional[PlanarParams] = None, accumulate: bool = False, stream=None) -> PlanarParams:
+        if grads is None:
+            grads = PlanarParams.zeros(particles.P, particles.sh_degree, self.device)
+        ges_render_bwd(particles, camera, settings, self.frame, dL_dimage, grads, accumulate, stream)
+        return grads

@@ -1,0 +1,290 @@
+// ges_api.cu -- the C ABI (include/ges.h): workspace layout, argument checks
+// and the launch sequence of each stage.  Host code only; every kernel lives
+// in preprocess.cu / sort.cu / render.cu / particle_bwd.cu.
+#include <cstring>
+
+#include "ges_internal.h"
+#include "ges_scan.cuh"
+
+namespace ges {
+
+int num_sms() {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+namespace {
+
+constexpr size_t kAlign = 256;
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// Lookback scratch: K1 (1 word / tile), 4 depth passes, duplication, 2 tile passes.
+struct LookbackLayout {
+    size_t pre, depth[4], dup, tile[2], total;  // word offsets
+};
+
+LookbackLayout lookback_layout(int64_t P, int64_t cap) {
+    LookbackLayout L;
+    size_t o = 0;
+    L.pre = o; o += (size_t)preprocess_lookback_words(P);
+    for (int d = 0; d < 4; ++d) { L.depth[d] = o; o += (size_t)radix_tiles(P) * kRadixDigits; }
+    L.dup = o; o += (size_t)duplicate_tiles(P);
+    for (int d = 0; d < 2; ++d) { L.tile[d] = o; o += (size_t)radix_tiles(cap) * kRadixDigits; }
+    L.total = o;
+    return L;
+}
+
+int tiles_of(int px) { return (px + kTile - 1) / kTile; }
+
+int bits_for(int64_t n) {
+    int b = 0;
+    while (((int64_t)1 << b) < n) ++b;
+    return b;
+}
+
+// Carves the frame; returns the total size.  base == nullptr => size only.
+size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_frame* f) {
+    const int tx = tiles_of(W), ty = tiles_of(H);
+    const int64_t T = (int64_t)tx * ty;
+    const int64_t HW = (int64_t)W * H;
+    const LookbackLayout L = lookback_layout(P, cap);
+    size_t off = 0;
+    auto take = [&](size_t bytes) -> char* {
+        char* p = base ? base + off : nullptr;
+        off = align_up(off + bytes);
+        return p;
+    };
+    ges_frame g;
+    std::memset(&g, 0, sizeof(g));
+    g.P = P; g.pair_capacity = cap; g.width = W; g.height = H; g.tiles_x = tx; g.tiles_y = ty;
+    g.num_tiles = (int32_t)T; g.tile_bits = bits_for(T); g.sh_degree_max = 3;
+    // --- zero-per-frame region (one memset in ges_preprocess) ---
+    g.counters = (uint64_t*)take(sizeof(uint64_t) * GES_CTR_N);
+    g.hist = (uint32_t*)take(sizeof(uint32_t) * 8 * 256);
+    g.tile_diff = (int32_t*)take(sizeof(int32_t) * (size_t)(tx + 1) * (ty + 1));
+    g.lookback = (uint32_t*)take(sizeof(uint32_t) * L.total);
+    g.lookback_bytes = off;  // bytes of the zero region from the workspace base
+    // --- per particle ---
+    g.depth = (float*)take(sizeof(float) * P);
+    g.pay0 = (float*)take(16 * (size_t)P);
+    g.pay1 = (float*)take(16 * (size_t)P);
+    g.pay2 = (float*)take(sizeof(float) * P);
+    g.radius = (int32_t*)take(sizeof(int32_t) * P);
+    g.rect = (uint16_t*)take(8 * (size_t)P);
+    g.status = (uint8_t*)take((size_t)P);
+    g.flags = (uint8_t*)take((size_t)P);
+    for (int k = 0; k < 2; ++k) {
+        g.vis_key[k] = (uint32_t*)take(sizeof(uint32_t) * P);
+        g.vis_val[k] = (uint32_t*)take(sizeof(uint32_t) * P);
+    }
+    g.sorted_vis = g.vis_val[0];
+    for (int k = 0; k < 2; ++k) {
+        g.pair_tile[k] = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
+        g.pair_val[k] = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
+    }
+    g.list = (g.tile_bits <= 8) ? g.pair_val[1] : g.pair_val[0];
+    g.ranges = (uint32_t*)take(sizeof(uint32_t) * (size_t)(T + 1));
+    g.final_T = (float*)take(sizeof(float) * HW);
+    g.n_contrib = (uint32_t*)take(sizeof(uint32_t) * HW);
+    g.grad2d = (float*)take(sizeof(float) * 9 * (size_t)P);
+    g.workspace_bytes = off;
+    if (f) *f = g;
+    return off;
+}
+
+CamParams cam_params(const ges_camera* c) {
+    CamParams p;
+    p.W = c->width; p.H = c->height;
+    p.tiles_x = tiles_of(c->width); p.tiles_y = tiles_of(c->height);
+    p.fx = c->fx; p.fy = c->fy; p.cx = c->cx; p.cy = c->cy; p.near_z = c->near_z;
+    for (int k = 0; k < 9; ++k) p.R[k] = c->R[k];
+    for (int k = 0; k < 3; ++k) p.t[k] = c->t[k];
+    return p;
+}
+
+bool particles_ok(const ges_particles* p) {
+    return p && p->P >= 1 && p->P <= 0x7fffffff && p->sh_degree >= 0 && p->sh_degree <= 3 && p->mean &&
+           p->log_scale && p->quat && p->opacity_logit && p->sh && p->beta;
+}
+
+bool camera_ok(const ges_camera* c, const ges_frame* f) {
+    return c && c->width == f->width && c->height == f->height && c->near_z > 0.0f && c->fx > 0.0f && c->fy > 0.0f;
+}
+
+ges_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GES_OK : GES_ERR_CUDA; }
+
+}  // namespace
+}  // namespace ges
+
+using namespace ges;
+
+extern "C" {
+
+size_t ges_workspace_bytes(int64_t P, int32_t width, int32_t height, int64_t pair_capacity) {
+    if (P < 1 || width < 1 || height < 1 || pair_capacity < 1) return 0;
+    return layout(nullptr, P, width, height, pair_capacity, nullptr);
+}
+
+ges_status ges_frame_init(void* workspace, size_t bytes, int64_t P, int32_t width, int32_t height,
+                          int64_t pair_capacity, ges_frame* frame) {
+    if (!workspace || !frame || P < 1 || P > 0x7fffffff || width < 1 || height < 1 || pair_capacity < 1 ||
+        pair_capacity >= (int64_t)kValueMask)
+        return GES_ERR_INVALID_ARG;
+    if (((uintptr_t)workspace) % kAlign) return GES_ERR_INVALID_ARG;
+    const int tx = tiles_of(width), ty = tiles_of(height);
+    if ((int64_t)tx * ty > 65536 || ranges_smem_bytes(tx, ty) > 200 * 1024) return GES_ERR_INVALID_ARG;
+    if (bytes < layout(nullptr, P, width, height, pair_capacity, nullptr)) return GES_ERR_CAPACITY;
+    layout((char*)workspace, P, width, height, pair_capacity, frame);
+    return GES_OK;
+}
+
+ges_status ges_preprocess(const ges_particles* particles, const ges_camera* camera, const ges_settings* settings,
+                          ges_frame* frame, void* stream) {
+    if (!frame || !settings || !particles_ok(particles) || !camera_ok(camera, frame) || particles->P != frame->P ||
+        !(settings->rho >= 0.0f) || (settings->phi_mode != GES_PHI_SCALE && settings->phi_mode != GES_PHI_VARIANCE))
+        return GES_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(frame->counters, 0, frame->lookback_bytes, s);
+    if (e != cudaSuccess) return GES_ERR_CUDA;
+    PreprocessArgs a;
+    a.mean = particles->mean; a.log_scale = particles->log_scale; a.quat = particles->quat;
+    a.opacity_logit = particles->opacity_logit; a.sh = particles->sh; a.beta = particles->beta;
+    a.P = (int)particles->P; a.sh_degree = particles->sh_degree;
+    a.rho = settings->rho; a.phi_mode = settings->phi_mode; a.gaussian_only = settings->gaussian_only ? 1 : 0;
+    a.cam = cam_params(camera);
+    a.depth = frame->depth; a.pay0 = (float4*)frame->pay0; a.pay1 = (float4*)frame->pay1; a.pay2 = frame->pay2;
+    a.radius = frame->radius; a.rect = (ushort4*)frame->rect; a.status = frame->status; a.flags = frame->flags;
+    a.vis_key = frame->vis_key[0]; a.vis_val = frame->vis_val[0];
+    a.tile_diff = frame->tile_diff; a.hist = frame->hist;
+    const LookbackLayout L = lookback_layout(frame->P, frame->pair_capacity);
+    a.lookback = frame->lookback + L.pre;
+    a.counters = (unsigned long long*)frame->counters;
+    return cuda_status(launch_preprocess(a, s));
+}
+
+ges_status ges_sort(ges_frame* frame, void* stream) {
+    if (!frame) return GES_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long* ctr = (unsigned long long*)frame->counters;
+    const LookbackLayout L = lookback_layout(frame->P, frame->pair_capacity);
+    RangesArgs r;
+    r.tile_diff = frame->tile_diff; r.tiles_x = frame->tiles_x; r.tiles_y = frame->tiles_y;
+    r.tile_bits = frame->tile_bits; r.ranges = frame->ranges; r.hist = frame->hist; r.counters = ctr;
+    r.capacity = frame->pair_capacity;
+    cudaError_t e = launch_ranges(r, s);
+    if (e != cudaSuccess) return GES_ERR_CUDA;
+    // depth sort of the visible particles: 4 x 8-bit passes, ping-pong 0 -> 1 -> 0 -> 1 -> 0
+    for (int d = 0; d < 4; ++d) {
+        RadixPassArgs p;
+        p.keys_in = frame->vis_key[d & 1]; p.vals_in = frame->vis_val[d & 1];
+        p.keys_out = (d < 3) ? frame->vis_key[(d + 1) & 1] : nullptr;
+        p.vals_out = frame->vis_val[(d + 1) & 1];
+        p.count = ctr + GES_CTR_VISIBLE; p.max_items = frame->P;
+        p.digit_offset = frame->hist + d * 256;
+        p.lookback = frame->lookback + L.depth[d];
+        p.tile_counter = ctr + GES_CTR_TILE0 + 1 + d;
+        p.shift = 8 * d;
+        p.overflow = nullptr;
+        if ((e = launch_radix_pass(p, s)) != cudaSuccess) return GES_ERR_CUDA;
+    }
+    frame->sorted_vis = frame->vis_val[0];
+    DuplicateArgs dp;
+    dp.sorted_vis = frame->sorted_vis; dp.rect = (const ushort4*)frame->rect; dp.counters = ctr;
+    dp.tiles_x = frame->tiles_x; dp.pair_tile = frame->pair_tile[0]; dp.pair_val = frame->pair_val[0];
+    dp.lookback = frame->lookback + L.dup; dp.tile_counter = ctr + GES_CTR_TILE0 + 5; dp.max_items = frame->P;
+    if ((e = launch_duplicate(dp, s)) != cudaSuccess) return GES_ERR_CUDA;
+    // stable sort of the pairs by tile id: 1 or 2 passes
+    const int passes = frame->tile_bits <= 8 ? 1 : 2;
+    for (int d = 0; d < passes; ++d) {
+        RadixPassArgs p;
+        p.keys_in = frame->pair_tile[d]; p.vals_in = frame->pair_val[d];
+        p.keys_out = (d + 1 < passes) ? frame->pair_tile[d + 1] : nullptr;
+        p.vals_out = frame->pair_val[(d + 1) & 1];
+        p.count = ctr + GES_CTR_PAIRS; p.max_items = frame->pair_capacity;
+        p.digit_offset = frame->hist + (4 + d) * 256;
+        p.lookback = frame->lookback + L.tile[d];
+        p.tile_counter = ctr + GES_CTR_TILE0 + 6 + d;
+        p.shift = 8 * d;
+        p.overflow = ctr + GES_CTR_OVERFLOW;
+        if ((e = launch_radix_pass(p, s)) != cudaSuccess) return GES_ERR_CUDA;
+    }
+    frame->list = frame->pair_val[passes & 1];
+    return GES_OK;
+}
+
+ges_status ges_render_fwd(ges_frame* frame, const ges_settings* settings, float* image, uint32_t* n_eval,
+                          void* stream) {
+    if (!frame || !settings || !image) return GES_ERR_INVALID_ARG;
+    RenderFwdArgs a;
+    a.pay0 = (const float4*)frame->pay0; a.pay1 = (const float4*)frame->pay1; a.pay2 = frame->pay2;
+    a.list = frame->list; a.ranges = frame->ranges; a.counters = (const unsigned long long*)frame->counters;
+    a.W = frame->width; a.H = frame->height; a.tiles_x = frame->tiles_x; a.tiles_y = frame->tiles_y;
+    for (int k = 0; k < 3; ++k) a.bg[k] = settings->background[k];
+    a.image = image; a.final_T = frame->final_T; a.n_contrib = frame->n_contrib; a.n_eval = n_eval;
+    return cuda_status(launch_render_fwd(a, (cudaStream_t)stream));
+}
+
+ges_status ges_render_bwd(const ges_particles* particles, const ges_camera* camera, const ges_settings* settings,
+                          ges_frame* frame, const float* dL_dimage, const ges_grads* grads, void* stream) {
+    if (!frame || !settings || !dL_dimage || !grads || !particles_ok(particles) || !camera_ok(camera, frame) ||
+        particles->P != frame->P || !grads->mean || !grads->log_scale || !grads->quat || !grads->opacity_logit ||
+        !grads->sh || !grads->beta)
+        return GES_ERR_INVALID_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemsetAsync(frame->grad2d, 0, sizeof(float) * 9 * (size_t)frame->P, s) != cudaSuccess) return GES_ERR_CUDA;
+    RenderBwdArgs b;
+    b.pay0 = (const float4*)frame->pay0; b.pay1 = (const float4*)frame->pay1; b.pay2 = frame->pay2;
+    b.list = frame->list; b.ranges = frame->ranges; b.counters = (const unsigned long long*)frame->counters;
+    b.W = frame->width; b.H = frame->height; b.tiles_x = frame->tiles_x; b.tiles_y = frame->tiles_y;
+    for (int k = 0; k < 3; ++k) b.bg[k] = settings->background[k];
+    b.final_T = frame->final_T; b.n_contrib = frame->n_contrib; b.dL_dimage = dL_dimage; b.grad2d = frame->grad2d;
+    b.P = (int)frame->P;
+    cudaError_t e = launch_render_bwd(b, s);
+    if (e != cudaSuccess) return GES_ERR_CUDA;
+    ParticleBwdArgs q;
+    q.mean = particles->mean; q.log_scale = particles->log_scale; q.quat = particles->quat;
+    q.opacity_logit = particles->opacity_logit; q.sh = particles->sh; q.beta = particles->beta;
+    q.P = (int)particles->P; q.sh_degree = particles->sh_degree;
+    q.rho = settings->rho; q.phi_mode = settings->phi_mode; q.gaussian_only = settings->gaussian_only ? 1 : 0;
+    q.cam = cam_params(camera);
+    q.status = frame->status; q.flags = frame->flags; q.grad2d = frame->grad2d;
+    q.g_mean = grads->mean; q.g_log_scale = grads->log_scale; q.g_quat = grads->quat;
+    q.g_opacity_logit = grads->opacity_logit; q.g_sh = grads->sh; q.g_beta = grads->beta;
+    q.accumulate = grads->accumulate;
+    return cuda_status(launch_particle_bwd(q, s));
+}
+
+ges_status ges_counts_get(const ges_frame* frame, ges_counts* host_out, void* stream) {
+    if (!frame || !host_out) return GES_ERR_INVALID_ARG;
+    uint64_t c[GES_CTR_N];
+    cudaStream_t s = (cudaStream_t)stream;
+    if (cudaMemcpyAsync(c, frame->counters, sizeof(c), cudaMemcpyDeviceToHost, s) != cudaSuccess) return GES_ERR_CUDA;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return GES_ERR_CUDA;
+    host_out->visible = (int64_t)c[GES_CTR_VISIBLE];
+    host_out->pairs = (int64_t)c[GES_CTR_PAIRS];
+    host_out->capacity = frame->pair_capacity;
+    host_out->overflow = (int32_t)c[GES_CTR_OVERFLOW];
+    host_out->_pad = 0;
+    return GES_OK;
+}
+
+const char* ges_status_string(ges_status st) {
+    switch (st) {
+        case GES_OK: return "ok";
+        case GES_ERR_INVALID_ARG: return "invalid argument";
+        case GES_ERR_CAPACITY: return "workspace or pair capacity too small";
+        case GES_ERR_CUDA: return "CUDA error";
+        case GES_ERR_UNSUPPORTED: return "unsupported";
+    }
+    return "unknown";
+}
+
+const char* ges_version(void) { return "ges-b200 0.1 (sm_100a)"; }
+
+}  // extern "C"

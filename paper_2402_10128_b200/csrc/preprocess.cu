@@ -1,0 +1,270 @@
+// preprocess.cu -- S1: per-particle projection of GES
+// particles, fused with visible-list compaction (decoupled look-back), the
+// depth-key digit histograms of the following radix sort and the 2-D
+// difference grid of the particles' tile rects (-> per-tile pair counts).
+//
+// Paper: Eq. 2 kernel and Sigma; PAPER.md:249-254 EWA
+// Sigma' = J W Sigma W^T J^T with Sigma = R S S^T R^T and S "modified by"
+// phi(beta); Eq. 4 (:268-270) effective variance; Eq. 6 (:291-293)
+// phi-bar_rho(beta) = 2 / (1 + exp(-(rho beta - 2 rho))); PAPER.md:247 opacity
+// and SH colour.  Inherited constants: DESIGN.md R7.  Op order: KEYSPEC
+// -- bit-identical to oracle/ges_geom.inc (REAL=float).
+//
+// HBM-bound: reads 48 B/particle (mean, log-scale, quat, logit, beta) plus 12K
+// bytes of SH for visible particles only; coalesced planar loads (lane i of a
+// warp reads element i of each plane).
+#include "ges_device.cuh"
+#include "ges_internal.h"
+#include "ges_scan.cuh"
+
+namespace ges {
+
+struct PreOut {
+    float depth, u, v, ca, cb, cc, kappa, r, g, b;
+    int radius, x0, y0, x1, y1;
+    uint8_t status, flags;
+};
+
+template <int K>
+__device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const CamDerived& cd, int i) {
+    const int P = a.P;
+    const CamParams& c = a.cam;
+    PreOut o;
+    o.u = o.v = o.ca = o.cb = o.cc = o.kappa = o.r = o.g = o.b = 0.0f;
+    o.radius = o.x0 = o.y0 = o.x1 = o.y1 = 0;
+    o.flags = 0;
+    const float mx = __ldg(a.mean + i), my = __ldg(a.mean + P + i), mz = __ldg(a.mean + 2 * P + i);
+    // camera space t = W mu + t
+    float tx = fmul(c.R[0], mx); tx = ffma(c.R[1], my, tx); tx = ffma(c.R[2], mz, tx); tx = fadd(tx, c.t[0]);
+    float ty = fmul(c.R[3], mx); ty = ffma(c.R[4], my, ty); ty = ffma(c.R[5], mz, ty); ty = fadd(ty, c.t[1]);
+    float tz = fmul(c.R[6], mx); tz = ffma(c.R[7], my, tz); tz = ffma(c.R[8], mz, tz); tz = fadd(tz, c.t[2]);
+    o.depth = tz;
+    if (!(tz > c.near_z)) { o.status = GES_CULL_NEAR; return o; }
+
+    // normalised quaternion -> rotation
+    float qw = __ldg(a.quat + i), qx = __ldg(a.quat + P + i), qy = __ldg(a.quat + 2 * P + i),
+          qz = __ldg(a.quat + 3 * P + i);
+    float n2 = fmul(qw, qw); n2 = ffma(qx, qx, n2); n2 = ffma(qy, qy, n2); n2 = ffma(qz, qz, n2);
+    if (!(n2 > 0.0f) || !isfinite(n2)) { o.status = GES_DEGENERATE; return o; }
+    const float nq = fsqrt(n2);
+    qw = fdiv(qw, nq); qx = fdiv(qx, nq); qy = fdiv(qy, nq); qz = fdiv(qz, nq);
+    const float xx = fmul(qx, qx), yy = fmul(qy, qy), zz = fmul(qz, qz);
+    const float xy = fmul(qx, qy), xz = fmul(qx, qz), yz = fmul(qy, qz);
+    const float wx = fmul(qw, qx), wy = fmul(qw, qy), wz = fmul(qw, qz);
+    float r[3][3];
+    r[0][0] = fsub(1.0f, fmul(2.0f, fadd(yy, zz)));
+    r[0][1] = fmul(2.0f, fsub(xy, wz));
+    r[0][2] = fmul(2.0f, fadd(xz, wy));
+    r[1][0] = fmul(2.0f, fadd(xy, wz));
+    r[1][1] = fsub(1.0f, fmul(2.0f, fadd(xx, zz)));
+    r[1][2] = fmul(2.0f, fsub(yz, wx));
+    r[2][0] = fmul(2.0f, fsub(xz, wy));
+    r[2][1] = fmul(2.0f, fadd(yz, wx));
+    r[2][2] = fsub(1.0f, fmul(2.0f, fadd(xx, yy)));
+
+    // phi-bar (Eq. 6) -> effective scale (R1)
+    float mfac = 1.0f;
+    if (!a.gaussian_only) {
+        const float d = fsub(__ldg(a.beta + i), 2.0f);
+        const float ar = fmul(a.rho, d);
+        const float e = exp_spec(-ar);
+        const float phi = fdiv(2.0f, fadd(1.0f, e));
+        mfac = (a.phi_mode == GES_PHI_VARIANCE) ? fsqrt(phi) : phi;
+    }
+    float se[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) se[k] = fmul(exp_spec(__ldg(a.log_scale + k * P + i)), mfac);
+
+    // Sigma = M M^T, M = R diag(se)
+    float M[3][3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) M[j][k] = fmul(r[j][k], se[k]);
+    float S[3][3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+#pragma unroll
+        for (int l = j; l < 3; ++l) {
+            float p = fmul(M[j][0], M[l][0]); p = ffma(M[j][1], M[l][1], p); p = ffma(M[j][2], M[l][2], p);
+            S[j][l] = p; S[l][j] = p;
+        }
+
+    // EWA Jacobian at the clamped mean; T = J W
+    const float xn = fdiv(tx, tz), yn = fdiv(ty, tz);
+    uint8_t fl = 0;
+    const float xc = fminf(cd.limx, fmaxf(-cd.limx, xn));
+    const float yc = fminf(cd.limy, fmaxf(-cd.limy, yn));
+    if (xn > cd.limx || xn < -cd.limx) fl |= 8;
+    if (yn > cd.limy || yn < -cd.limy) fl |= 16;
+    const float txc = fmul(xc, tz), tyc = fmul(yc, tz);
+    const float tz2 = fmul(tz, tz);
+    const float j00 = fdiv(c.fx, tz), j02 = fdiv(-fmul(c.fx, txc), tz2);
+    const float j11 = fdiv(c.fy, tz), j12 = fdiv(-fmul(c.fy, tyc), tz2);
+    float T[2][3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        T[0][k] = ffma(j02, c.R[6 + k], fmul(j00, c.R[0 + k]));
+        T[1][k] = ffma(j12, c.R[6 + k], fmul(j11, c.R[3 + k]));
+    }
+    float U[2][3];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            float p = fmul(T[j][0], S[0][k]); p = ffma(T[j][1], S[1][k], p); p = ffma(T[j][2], S[2][k], p);
+            U[j][k] = p;
+        }
+    float c00 = fmul(U[0][0], T[0][0]); c00 = ffma(U[0][1], T[0][1], c00); c00 = ffma(U[0][2], T[0][2], c00);
+    float c01 = fmul(U[0][0], T[1][0]); c01 = ffma(U[0][1], T[1][1], c01); c01 = ffma(U[0][2], T[1][2], c01);
+    float c11 = fmul(U[1][0], T[1][0]); c11 = ffma(U[1][1], T[1][1], c11); c11 = ffma(U[1][2], T[1][2], c11);
+    const float A = fadd(c00, kDilation), B = c01, C = fadd(c11, kDilation);
+    const float bb = fmul(B, B);
+    const float det = ffma(A, C, -bb);
+    o.flags = fl;
+    if (!(det > 0.0f) || !isfinite(det)) { o.status = GES_DEGENERATE; return o; }
+    const float ca = fdiv(C, det), cb = fdiv(-B, det), ccn = fdiv(A, det);
+    const float mid = fmul(0.5f, fadd(A, C));
+    float d2 = ffma(mid, mid, -det);
+    d2 = fmaxf(0.1f, d2);
+    const float lam = fadd(mid, fsqrt(d2));
+    const float rad = ceilf(fmul(3.0f, fsqrt(lam)));
+    const float u = ffma(c.fx, xn, c.cx), v = ffma(c.fy, yn, c.cy);
+    if (!isfinite(u) || !isfinite(v) || !isfinite(rad)) { o.status = GES_DEGENERATE; return o; }
+    const float fx0 = floorf(fmul(fsub(u, rad), 0.0625f));
+    const float fx1 = fadd(floorf(fmul(fadd(u, rad), 0.0625f)), 1.0f);
+    const float fy0 = floorf(fmul(fsub(v, rad), 0.0625f));
+    const float fy1 = fadd(floorf(fmul(fadd(v, rad), 0.0625f)), 1.0f);
+    const float ftx = (float)c.tiles_x, fty = (float)c.tiles_y;
+    o.x0 = (int)fminf(fmaxf(fx0, 0.0f), ftx);
+    o.x1 = (int)fminf(fmaxf(fx1, 0.0f), ftx);
+    o.y0 = (int)fminf(fmaxf(fy0, 0.0f), fty);
+    o.y1 = (int)fminf(fmaxf(fy1, 0.0f), fty);
+    o.u = u; o.v = v; o.ca = ca; o.cb = cb; o.cc = ccn;
+    o.radius = (int)rad;
+    if ((o.x1 - o.x0) * (o.y1 - o.y0) == 0) { o.status = GES_OFFSCREEN; return o; }
+
+    // view-dependent colour: rgb = sum_k Y_k(dir) sh_k + 0.5, >= 0
+    const float dx = fsub(mx, cd.c0), dy = fsub(my, cd.c1), dz = fsub(mz, cd.c2);
+    float dn2 = fmul(dx, dx); dn2 = ffma(dy, dy, dn2); dn2 = ffma(dz, dz, dn2);
+    const float dn = fsqrt(dn2);
+    float Y[16];
+    sh_basis<K>(fdiv(dx, dn), fdiv(dy, dn), fdiv(dz, dn), Y);
+    float rgb[3];
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+        float acc = fmul(Y[0], __ldg(a.sh + (size_t)ch * P + i));
+#pragma unroll
+        for (int k = 1; k < K; ++k) acc = ffma(Y[k], __ldg(a.sh + (size_t)(3 * k + ch) * P + i), acc);
+        acc = fadd(acc, 0.5f);
+        if (acc < 0.0f) { acc = 0.0f; fl |= (uint8_t)(1u << ch); }
+        rgb[ch] = acc;
+    }
+    o.r = rgb[0]; o.g = rgb[1]; o.b = rgb[2];
+    o.kappa = fdiv(1.0f, fadd(1.0f, exp_spec(-__ldg(a.opacity_logit + i))));
+    o.flags = fl;
+    o.status = GES_VISIBLE;
+    return o;
+}
+
+constexpr int kPreThreads = 256;
+constexpr int kPreItems = 4;
+constexpr int kPreTile = kPreThreads * kPreItems;
+
+template <int K>
+__global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs a) {
+    __shared__ uint32_t s_hist[4][256];
+    __shared__ uint32_t s_warp[kPreItems][kPreThreads / 32];
+    __shared__ uint32_t s_tile, s_base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int k = tid; k < 4 * 256; k += kPreThreads) (&s_hist[0][0])[k] = 0;
+    if (tid == 0) s_tile = (uint32_t)atomicAdd(&a.counters[GES_CTR_TILE0], 1ull);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    const CamDerived cd = derive_camera(a.cam);
+    const int stride_diff = a.cam.tiles_x + 1;
+
+    bool vis[kPreItems];
+    uint32_t key[kPreItems];
+#pragma unroll
+    for (int j = 0; j < kPreItems; ++j) {
+        const int64_t i64 = (int64_t)tile * kPreTile + j * kPreThreads + tid;
+        vis[j] = false;
+        key[j] = 0;
+        if (i64 >= a.P) continue;
+        const int i = (int)i64;
+        const PreOut o = preprocess_one<K>(a, cd, i);
+        a.depth[i] = o.depth;
+        a.pay0[i] = make_float4(o.u, o.v, o.ca, o.cb);
+        a.pay1[i] = make_float4(o.cc, o.kappa, o.r, o.g);
+        a.pay2[i] = o.b;
+        a.radius[i] = o.radius;
+        a.rect[i] = make_ushort4((uint16_t)o.x0, (uint16_t)o.y0, (uint16_t)o.x1, (uint16_t)o.y1);
+        a.status[i] = o.status;
+        a.flags[i] = o.flags;
+        if (o.status == GES_VISIBLE) {
+            vis[j] = true;
+            key[j] = __float_as_uint(o.depth);
+#pragma unroll
+            for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(key[j] >> (8 * d)) & 255u], 1u);
+            atomicAdd(&a.tile_diff[o.y0 * stride_diff + o.x0], 1);
+            atomicAdd(&a.tile_diff[o.y0 * stride_diff + o.x1], -1);
+            atomicAdd(&a.tile_diff[o.y1 * stride_diff + o.x0], -1);
+            atomicAdd(&a.tile_diff[o.y1 * stride_diff + o.x1], 1);
+        }
+    }
+    // compaction in index order: item (j, warp, lane)
+    uint32_t ball[kPreItems];
+#pragma unroll
+    for (int j = 0; j < kPreItems; ++j) {
+        ball[j] = __ballot_sync(0xffffffffu, vis[j]);
+        if (lane == 0) s_warp[j][warp] = __popc(ball[j]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        // exclusive scan of the kPreItems * 8 warp counts (j-major) in one warp
+        uint32_t v = (lane < kPreItems * 8) ? (&s_warp[0][0])[lane] : 0u;
+        uint32_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += n;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        if (lane < kPreItems * 8) (&s_warp[0][0])[lane] = incl - v;
+        const uint32_t prefix = lookback_warp(a.lookback, tile, total);
+        if (lane == 0) {
+            s_base = prefix;
+            if (total) atomicAdd(&a.counters[GES_CTR_VISIBLE], (unsigned long long)total);
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kPreItems; ++j) {
+        if (!vis[j]) continue;
+        const uint32_t pos = s_base + s_warp[j][warp] + __popc(ball[j] & ((1u << lane) - 1u));
+        a.vis_key[pos] = key[j];
+        a.vis_val[pos] = (uint32_t)((int64_t)tile * kPreTile + j * kPreThreads + tid);
+    }
+    for (int k = tid; k < 4 * 256; k += kPreThreads) {
+        const uint32_t h = (&s_hist[0][0])[k];
+        if (h) atomicAdd(&a.hist[k], h);
+    }
+}
+
+cudaError_t launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {
+    const int64_t tiles = (a.P + kPreTile - 1) / kPreTile;
+    dim3 grid((unsigned)tiles), block(kPreThreads);
+    switch (a.sh_degree) {
+        case 0: preprocess_kernel<1><<<grid, block, 0, stream>>>(a); break;
+        case 1: preprocess_kernel<4><<<grid, block, 0, stream>>>(a); break;
+        case 2: preprocess_kernel<9><<<grid, block, 0, stream>>>(a); break;
+        case 3: preprocess_kernel<16><<<grid, block, 0, stream>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+int64_t preprocess_lookback_words(int64_t P) { return (P + kPreTile - 1) / kPreTile; }
+
+}  // namespace ges

@@ -1,0 +1,103 @@
+"""CPU-side checks of the C ABI: libges.so loads, exports every function that
+include/ges.h declares, the ctypes mirrors have the C layout, and the host-only
+entry points (workspace sizing, frame carving, argument checks) behave."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import pytest
+
+from paper_2402_10128_b200 import _lib as L
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "ges.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ges_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = L.load()
+    names = declared_functions()
+    assert set(names) == set(L.EXPORTS), names
+    for n in names:
+        assert hasattr(lib, n), n
+    out = subprocess.run(["nm", "-D", "--defined-only", L.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r" T (ges_\w+)", out))
+    assert set(names) <= exported
+
+
+def test_ctypes_layout_matches_header(tmp_path):
+    prog = tmp_path / "layout.c"
+    structs = {"ges_particles": L.ges_particles, "ges_camera": L.ges_camera, "ges_settings": L.ges_settings,
+               "ges_grads": L.ges_grads, "ges_counts": L.ges_counts, "ges_frame": L.ges_frame}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', 'int main(void) {']
+    for s, cls in structs.items():
+        lines.append(f'printf("{s} %zu\\n", sizeof({s}));')
+        for f, _ in cls._fields_:
+            lines.append(f'printf("{s}.{f} %zu\\n", offsetof({s}, {f}));')
+    lines.append("return 0; }")
+    prog.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-o", str(exe), str(prog)])
+    out = dict(line.rsplit(" ", 1) for line in subprocess.check_output([str(exe)], text=True).splitlines())
+    for s, cls in structs.items():
+        assert int(out[s]) == C.sizeof(cls), s
+        for f, _ in cls._fields_:
+            assert int(out[f"{s}.{f}"]) == getattr(cls, f).offset, (s, f)
+
+
+def test_workspace_and_frame_carving_host_only():
+    lib = L.load()
+    P, W, H, cap = 1000, 100, 70, 5000
+    nbytes = lib.ges_workspace_bytes(P, W, H, cap)
+    assert nbytes > 0
+    assert lib.ges_workspace_bytes(0, W, H, cap) == 0
+    # ges_frame_init never touches device memory: carve a fake aligned address
+    base = 1 << 40
+    f = L.ges_frame()
+    assert lib.ges_frame_init(C.c_void_p(base), nbytes, P, W, H, cap, C.byref(f)) == L.GES_OK
+    assert (f.tiles_x, f.tiles_y, f.num_tiles) == (7, 5, 35)
+    assert f.tile_bits == 6
+    assert f.workspace_bytes == nbytes
+    ptrs = [f.depth, f.pay0, f.pay1, f.pay2, f.radius, f.rect, f.status, f.flags, f.vis_key[0], f.vis_key[1],
+            f.vis_val[0], f.vis_val[1], f.pair_tile[0], f.pair_tile[1], f.pair_val[0], f.pair_val[1], f.ranges,
+            f.tile_diff, f.hist, f.lookback, f.counters, f.final_T, f.n_contrib, f.grad2d]
+    assert all(base <= p < base + nbytes and p % 256 == 0 for p in ptrs)
+    assert len(set(ptrs)) == len(ptrs)
+    # errors
+    assert lib.ges_frame_init(C.c_void_p(base), nbytes - 1, P, W, H, cap, C.byref(f)) == L.GES_ERR_CAPACITY
+    assert lib.ges_frame_init(C.c_void_p(base + 8), nbytes, P, W, H, cap, C.byref(f)) == L.GES_ERR_INVALID_ARG
+    assert lib.ges_frame_init(None, nbytes, P, W, H, cap, C.byref(f)) == L.GES_ERR_INVALID_ARG
+    assert lib.ges_sort(None, None) == L.GES_ERR_INVALID_ARG
+    assert lib.ges_status_string(L.GES_ERR_CAPACITY).decode().startswith("workspace")
+    assert b"sm_100a" in lib.ges_version()
+
+
+def test_invalid_arguments_rejected_before_launch():
+    lib = L.load()
+    P, W, H, cap = 10, 32, 32, 100
+    nbytes = lib.ges_workspace_bytes(P, W, H, cap)
+    f = L.ges_frame()
+    assert lib.ges_frame_init(C.c_void_p(1 << 40), nbytes, P, W, H, cap, C.byref(f)) == L.GES_OK
+    p = L.ges_particles()
+    p.P, p.sh_degree = P, 5  # bad degree
+    cam = L.ges_camera()
+    cam.width, cam.height, cam.fx, cam.fy, cam.near_z = W, H, 10.0, 10.0, 0.2
+    s = L.ges_settings()
+    assert lib.ges_preprocess(C.byref(p), C.byref(cam), C.byref(s), C.byref(f), None) == L.GES_ERR_INVALID_ARG
+    p.sh_degree = 0  # null pointers
+    assert lib.ges_preprocess(C.byref(p), C.byref(cam), C.byref(s), C.byref(f), None) == L.GES_ERR_INVALID_ARG
+
+
+def test_product_package_does_not_import_oracle():
+    pkg = os.path.join(ROOT, "paper_2402_10128_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cuh", ".h")):
+                txt = open(os.path.join(dirpath, fn)).read()
+                assert "oracle" not in re.sub(r"(#|//).*", "", txt).lower() or fn == "_build.py", fn

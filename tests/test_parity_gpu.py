@@ -1,0 +1,237 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs.  Bars (BASELINE.json north_star):
+  * per-particle S1 state, keys, sort order, ranges: bit-exact
+  * image: <= 1e-4 max abs per channel, except pixels the oracle flags as
+    threshold-ambiguous (R18), which must be rare
+  * gradients: |g_gpu - g_ref| <= max(1e-3 |g_ref|, 1e-6), except particles
+    touching an ambiguous pixel (reported, bounded in number).
+"""
+import numpy as np
+import pytest
+import torch
+
+import ges_inputs as gi
+import paper_2402_10128_b200 as G
+from oracle import oracle as O
+
+from gpu_helpers import (ambiguous_particles, gpu_backward, gpu_forward, gpu_keys, grad_mismatch, settings_pair)
+
+pytestmark = pytest.mark.gpu
+
+PRE_KEYS = ("depth", "uv", "conic", "kappa", "rgb", "radius", "rect", "status", "flags")
+
+
+def compare_preprocess(out, pre):
+    P = pre["status"].size
+    assert np.array_equal(out["status"], pre["status"])
+    vis = pre["status"] == 0
+    assert np.array_equal(out["depth"].view(np.uint32), pre["depth"].view(np.uint32))
+    g_uv = out["pay0"][:, 0:2].T
+    g_conic = np.stack([out["pay0"][:, 2], out["pay0"][:, 3], out["pay1"][:, 0]])
+    g_kappa = out["pay1"][:, 1]
+    g_rgb = np.stack([out["pay1"][:, 2], out["pay1"][:, 3], out["pay2"]])
+    for name, g, o in (("uv", g_uv, pre["uv"]), ("conic", g_conic, pre["conic"]), ("kappa", g_kappa, pre["kappa"]),
+                       ("rgb", g_rgb, pre["rgb"])):
+        gm, om = g[..., vis], o[..., vis]
+        bad = np.nonzero(gm.view(np.uint32) != om.view(np.uint32))
+        assert bad[0].size == 0, (name, bad[0][:5], gm[bad][:5], om[bad][:5])
+    assert np.array_equal(out["radius"][vis], pre["radius"][vis])
+    assert np.array_equal(out["rect"].T[:, vis], pre["rect"][:, vis])
+    assert np.array_equal(out["flags"][vis], pre["flags"][vis])
+
+
+def compare_sort(out, pre):
+    keys, vals = O.pairs_sorted(pre)
+    assert int(out["counts"].pairs) == keys.size
+    assert int(out["counts"].visible) == int((pre["status"] == 0).sum())
+    assert np.array_equal(out["list"], vals.astype(np.int64))
+    assert np.array_equal(gpu_keys(out), keys)
+    offsets, _ = O.tile_lists(pre)
+    assert np.array_equal(out["ranges"], offsets)
+
+
+def compare_image(out, ref, tol=1e-4, max_amb_frac=2e-3):
+    amb = ref["amb"] != 0
+    assert amb.mean() <= max_amb_frac, amb.mean()
+    d = np.abs(out["image"] - ref["image"])
+    d[:, amb] = 0.0
+    assert d.max() <= tol, (d.max(), np.unravel_index(d.argmax(), d.shape))
+    ok = ~amb
+    assert np.array_equal(out["n_contrib"][ok], ref["n_contrib"][ok])
+    assert np.abs(out["final_T"][ok] - ref["final_T"][ok]).max() <= tol
+    if "n_eval" in out:
+        assert np.array_equal(out["n_eval"][ok], ref["n_eval"][ok])
+
+
+def compare_grads(gg, ref, pre, amb, tiles_x, max_bad_frac=1e-3):
+    skip = ambiguous_particles(pre, amb, tiles_x)
+    nbad = 0
+    ntot = 0
+    worst = []
+    for n in G.PARAM_NAMES:
+        a, r = gg[n], ref["grads"][n]
+        m = grad_mismatch(a, r)
+        m[..., skip] = False
+        nbad += int(m.sum())
+        ntot += int(np.prod(a.shape))
+        if m.any():
+            idx = np.argwhere(m)[:3]
+            worst += [(n, tuple(i), float(a[tuple(i)]), float(r[tuple(i)])) for i in idx]
+    assert nbad <= max_bad_frac * ntot, (nbad, ntot, worst[:10])
+    return nbad
+
+
+def run_case(parts, cam, gs, osx, dL=None, grads=True, max_bad_frac=1e-3):
+    out = gpu_forward(parts, cam, gs)
+    assert not out["counts"].overflow
+    pre = O.preprocess(parts, cam, osx, "f32")
+    compare_preprocess(out, pre)
+    compare_sort(out, pre)
+    ref = O.render_fwd(pre, cam, osx, *O.tile_lists(pre))
+    compare_image(out, ref)
+    if grads:
+        if dL is None:
+            dL = gi.upstream_grad(1000, 0, cam.width, cam.height)
+        gg, _ = gpu_backward(out, cam, gs, dL)
+        offsets, lst = O.tile_lists(pre)
+        g2d = O.render_bwd(pre, cam, osx, offsets, lst, dL)
+        rg = {"grads": O.backward_particles(parts, cam, osx, g2d, pre["status"], pre["flags"])}
+        compare_grads(gg, rg, pre, ref["amb"], pre["tiles_x"], max_bad_frac)
+    return out, pre
+
+
+def test_config0_full_parity():
+    sc = gi.make_config(0)
+    gs, osx = settings_pair()
+    dL = gi.upstream_grad(sc.seed, 0, 256, 256)
+    run_case(sc.particles, sc.cameras[0], gs, osx, dL)
+
+
+@pytest.mark.parametrize("beta", [0.5, 1.0, 2.0, 4.0, 8.0])
+def test_config1_beta_sweep(beta):
+    sc = gi.make_config(1, beta_value=beta)
+    gs, osx = settings_pair()
+    dL = gi.upstream_grad(sc.seed, 0, 512, 512)
+    run_case(sc.particles, sc.cameras[0], gs, osx, dL)
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_phi_modes_and_background(mode):
+    sc = gi.make_config(0, P=1500)
+    gs, osx = settings_pair(rho=0.3, phi_mode=mode, background=(0.2, 0.5, 0.9))
+    run_case(sc.particles, sc.cameras[0], gs, osx)
+
+
+def test_config2_view_sh3():
+    sc = gi.make_config(2, P=60000)
+    cam = sc.cameras[2]
+    gs, osx = settings_pair()
+    run_case(sc.particles, cam, gs, osx, gi.upstream_grad(sc.seed, 2, cam.width, cam.height))
+
+
+def test_beta2_bitwise_equals_gaussian_path():
+    sc = gi.make_config(1, beta_value=2.0, P=20000)
+    cam = sc.cameras[0]
+    a = gpu_forward(sc.particles, cam, G.Settings(rho=0.1))
+    b = gpu_forward(sc.particles, cam, G.Settings(rho=0.1, gaussian_only=1))
+    for k in ("image", "list", "ranges", "pay0", "pay1", "pay2", "final_T", "n_contrib"):
+        assert np.array_equal(a[k].view(np.uint8), b[k].view(np.uint8)), k
+
+
+def test_forward_deterministic():
+    sc = gi.make_config(0)
+    a = gpu_forward(sc.particles, sc.cameras[0], G.Settings())
+    b = gpu_forward(sc.particles, sc.cameras[0], G.Settings())
+    for k in ("image", "list", "ranges", "final_T", "n_contrib"):
+        assert np.array_equal(a[k].view(np.uint8), b[k].view(np.uint8)), k
+
+
+def test_ragged_image_and_tiny_counts():
+    # W, H not multiples of 16; P = 1 and P = 37
+    for P in (1, 37):
+        sc = gi.make_config(0, P=P)
+        cam = sc.cameras[0]
+        cam = gi.Camera(71, 45, 120.0, 120.0, 35.5, 22.5, 0.2, cam.R, cam.t)
+        gs, osx = settings_pair(background=(0.1, 0.1, 0.1))
+        run_case(sc.particles, cam, gs, osx, gi.upstream_grad(5, P, 71, 45))
+
+
+def test_everything_culled():
+    sc = gi.make_config(0, P=100)
+    parts = sc.particles.subset(slice(None))
+    parts.mean[2] = -5.0  # behind the camera
+    cam = sc.cameras[0]
+    gs, osx = settings_pair(background=(0.3, 0.6, 0.9))
+    out = gpu_forward(parts, cam, gs)
+    assert out["counts"].visible == 0 and out["counts"].pairs == 0
+    bg = np.array([0.3, 0.6, 0.9], np.float32)[:, None, None]
+    assert np.array_equal(out["image"], np.broadcast_to(bg, out["image"].shape))
+    gg, _ = gpu_backward(out, cam, gs, np.ones((3, 256, 256), np.float32))
+    assert all(np.all(v == 0) for v in gg.values())
+
+
+def test_degenerate_particles():
+    sc = gi.make_config(0, P=500)
+    parts = sc.particles.subset(slice(None))
+    parts.quat[:, :20] = 0.0            # zero quaternion
+    parts.log_scale[:, 20:40] = -30.0   # vanishing scale
+    parts.log_scale[:, 40:60] = 3.0     # huge: covers the whole screen
+    parts.mean[2, 60:80] = 0.2          # exactly on the near plane
+    gs, osx = settings_pair()
+    run_case(parts, sc.cameras[0], gs, osx)
+
+
+def test_overflow_regrow():
+    sc = gi.make_config(0)
+    cam = sc.cameras[0]
+    out = gpu_forward(sc.particles, cam, G.Settings(), pair_capacity=1000)
+    assert not out["counts"].overflow and out["counts"].capacity >= out["counts"].pairs > 1000
+    pre = O.preprocess(sc.particles, cam, O.Settings(), "f32")
+    compare_sort(out, pre)
+
+
+def test_gradient_accumulate():
+    sc = gi.make_config(0, P=800)
+    cam = sc.cameras[0]
+    gs, _ = settings_pair()
+    out = gpu_forward(sc.particles, cam, gs)
+    dL = gi.upstream_grad(3, 0, 256, 256)
+    g1, grads = gpu_backward(out, cam, gs, dL)
+    g2, _ = gpu_backward(out, cam, gs, dL, accumulate=True, grads=grads)
+    for n in G.PARAM_NAMES:
+        assert np.allclose(g2[n], 2 * g1[n], rtol=1e-6, atol=1e-12)
+
+
+def test_full_size_config3_sampled():
+    """BASELINE config 3 at full size (1.5M particles, 1297x840, SH3) in the
+    launch configuration bench.py times: S1 bit-exact for every particle,
+    per-tile lists / image / transmittance exact on sampled tiles."""
+    sc = gi.make_config(3)
+    cam = sc.cameras[0]
+    gs, osx = settings_pair()
+    out = gpu_forward(sc.particles, cam, gs)
+    pre = O.preprocess(sc.particles, cam, osx, "f32")
+    compare_preprocess(out, pre)
+    T = pre["tiles_x"] * pre["tiles_y"]
+    rng = np.random.default_rng(0)
+    mask = np.zeros(T, np.uint8)
+    mask[rng.choice(T, 48, replace=False)] = 1
+    # the densest tiles too
+    counts = np.diff(out["ranges"])
+    mask[np.argsort(counts)[-4:]] = 1
+    offsets, lst = O.tile_lists(pre, mask)
+    for t in np.nonzero(mask)[0]:
+        assert np.array_equal(out["list"][out["ranges"][t]:out["ranges"][t + 1]], lst[offsets[t]:offsets[t + 1]])
+    assert int(out["counts"].pairs) == O.count_pairs(pre)
+    ref = O.render_fwd(pre, cam, osx, offsets, lst, mask)
+    pix_mask = np.zeros((cam.height, cam.width), bool)
+    tx = pre["tiles_x"]
+    for t in np.nonzero(mask)[0]:
+        y, x = divmod(int(t), tx)
+        pix_mask[y * 16:(y + 1) * 16, x * 16:(x + 1) * 16] = True
+    amb = (ref["amb"] != 0) & pix_mask
+    sel = pix_mask & ~amb
+    assert amb.sum() <= 0.01 * pix_mask.sum()
+    d = np.abs(out["image"][:, sel] - ref["image"][:, sel])
+    assert d.max() <= 1e-4, d.max()
+    assert np.array_equal(out["n_contrib"][sel], ref["n_contrib"][sel])
