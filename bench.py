@@ -1,0 +1,457 @@
+"""Benchmark of the GES tile rasterizer (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step is one pass of the whole hot path (S1 preprocess,
+S2 sort, S3 ranges, S4 forward compositing, S5 backward) over one camera view
+of the config-3 scene (1.5M particles, 1297x840, SH degree 3) per rank; with
+N > 1 ranks (torchrun, NCCL) every rank renders its own view and the particle
+gradients are summed by an NCCL allreduce (view data parallelism, weak
+scaling).  Rank 0 prints ONE JSON line.
+
+value        whole-job Mpixel-frames/s of fwd+bwd steps, inputs resident in HBM,
+             CUDA events on the launching stream, L2 flushed between steps,
+             max over ranks.
+e2e          the same through the public API with pinned HOST buffers: the
+             particles and dL/dimage are copied in and the image copied out
+             every step, inside the timed region.
+roofline     the dominant kernel against its bound.
+cpu_baseline the oracle (oracle/, as it stands) on a bounded sample of the
+             same workload on this host's cores.
+--impl reference  times that oracle as the reference arm (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Mpixel-frames/s fwd and fwd+bwd iters/s at 1/2/4/8 B200 vs roofline"
+WORKLOAD_CFG = 3
+L2_FLUSH_BYTES = 256 << 20
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# oracle (cpu_baseline / reference arm): bounded sample of the same workload
+# ---------------------------------------------------------------------------
+def oracle_sample(scene, cam_index: int, n_tiles: int = 24, seed: int = 0) -> dict:
+    """S1 over all particles, S2/S3 membership lists (all pairs counted), S4+S5a
+    on n_tiles sampled tiles, S5b over all particles; per-frame time is
+    extrapolated to every tile."""
+    from oracle import oracle as O
+    import ges_inputs as gi
+    cam = scene.cameras[cam_index]
+    st = O.Settings(rho=scene.rho)
+    t0 = time.perf_counter()
+    pre = O.preprocess(scene.particles, cam, st, "f32")
+    t1 = time.perf_counter()
+    T = pre["tiles_x"] * pre["tiles_y"]
+    rng = np.random.default_rng(seed)
+    mask = np.zeros(T, np.uint8)
+    mask[rng.choice(T, min(n_tiles, T), replace=False)] = 1
+    offsets, lst = O.tile_lists(pre, mask)
+    t2 = time.perf_counter()
+    dL = gi.upstream_grad(scene.seed, cam_index, cam.width, cam.height)
+    O.render_fwd(pre, cam, st, offsets, lst, mask)
+    g2d = O.render_bwd(pre, cam, st, offsets, lst, dL, mask)
+    t3 = time.perf_counter()
+    O.backward_particles(scene.particles, cam, st, g2d, pre["status"], pre["flags"])
+    t4 = time.perf_counter()
+    per_tile = (t3 - t2) / max(1, int(mask.sum()))
+    frame_s = (t1 - t0) + (t2 - t1) + per_tile * T + (t4 - t3)
+    return {"frame_s": frame_s, "threads": O.num_threads(), "tiles": int(mask.sum()), "T": T,
+            "t_pre": t1 - t0, "t_lists": t2 - t1, "t_tiles": t3 - t2, "t_s5b": t4 - t3}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import ges_inputs as gi
+    scene = gi.make_config(WORKLOAD_CFG)
+    cam = scene.cameras[0]
+    n_tiles = args.ref_tiles
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        pass
+    times = []
+    info = None
+    for k in range(args.steps):
+        info = oracle_sample(scene, 0, n_tiles=n_tiles, seed=k)
+        times.append(info["frame_s"])
+    ms = 1e3 * statistics.mean(times)
+    value = cam.width * cam.height / (ms / 1e3) / 1e6
+    sample = (f"S1+S5b over all {scene.particles.P} particles, S4+S5a on {info['tiles']} of {info['T']} "
+              f"tiles per step, per-frame time extrapolated to all tiles")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Mpixel-frames/s (fwd+bwd)",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (fp32 S1)",
+        "data": "synthetic", "config": workload_config(scene, cam, args.gpus),
+        "cpu_baseline": {"kind": "oracle", "value": value, "unit": "Mpixel-frames/s (fwd+bwd)",
+                         "cores": info["threads"], "sample": sample},
+        "e2e": {"value": value, "unit": "Mpixel-frames/s (fwd+bwd)", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(scene, cam, n):
+    return {"workload": scene.name, "particles": scene.particles.P, "sh_degree": scene.particles.sh_degree,
+            "width": cam.width, "height": cam.height, "tiles": ((cam.width + 15) // 16) * ((cam.height + 15) // 16),
+            "rho": scene.rho, "phi_mode": "scale", "views_per_rank": 1,
+            "step": "S1-S5 fwd+bwd of one view per rank (+NCCL allreduce of particle grads if N>1)",
+            "parallelism": f"dp{n} (camera-view data parallel)",
+            "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MB write); inputs 360 MB > L2"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    import ges_inputs as gi
+    import paper_2402_10128_b200 as G
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.current_stream()
+
+    scene = gi.make_config(WORKLOAD_CFG)
+    cam = scene.cameras[rank % len(scene.cameras)]
+    W, H, P = cam.width, cam.height, scene.particles.P
+    st = G.Settings(rho=scene.rho)
+    params = G.PlanarParams.from_inputs(scene.particles, device=dev)
+    grads = G.PlanarParams.zeros(P, scene.particles.sh_degree, dev)
+    dL = torch.from_numpy(gi.upstream_grad(scene.seed, rank, W, H)).to(dev)
+    image = torch.empty((3, H, W), dtype=torch.float32, device=dev)
+    n_eval = torch.zeros(W * H, dtype=torch.int32, device=dev)
+    r = G.Renderer(P, W, H, device=dev)
+    r.forward(params, cam, st, image)               # sizes the pair buffer (one sync)
+    cnt = r.frame.counts()
+    r.grow(int(cnt.pairs))                          # capacity = 1.25 M, fixed from here on
+    frame = r.frame
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    stage_names = ("preprocess", "sort", "render_fwd", "render_bwd", "allreduce")
+
+    def step(timers=None):
+        def mark(i):
+            if timers is not None:
+                timers[i].record(stream)
+        mark(0)
+        G.ges_preprocess(params, cam, st, frame, stream)
+        mark(1)
+        G.ges_sort(frame, stream)
+        mark(2)
+        G.ges_render_fwd(frame, st, image, None, stream)
+        mark(3)
+        G.ges_render_bwd(params, cam, st, frame, dL, grads, False, stream)
+        mark(4)
+        if world > 1:
+            dist.all_reduce(grads.flat)
+        mark(5)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    cnt = frame.counts()
+    assert not cnt.overflow
+
+    # ---- timed region ----
+    stage_ms = np.zeros(len(stage_names))
+    step_ms = []
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            timers = [ev() for _ in range(6)]
+            step(timers)
+            timers[-1].synchronize()
+            step_ms.append(timers[0].elapsed_time(timers[5]))
+            for i in range(5):
+                stage_ms[i] += timers[i].elapsed_time(timers[i + 1])
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    total_ms = float(sum(step_ms))
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    stage_ms /= args.steps
+    value = world * W * H / (ms_per_step / 1e3) / 1e6
+
+    # ---- forward-only throughput and the equivalent-Gaussian comparator (untimed above) ----
+    fwd_ms = time_forward(G, params, cam, st, frame, image, flush, stream, args.steps)
+    gauss = gaussian_equivalent(G, scene, cam, dev)
+    g_frame = G.Renderer(P, W, H, pair_capacity=frame.pair_capacity, device=dev).frame
+    g_ms = time_forward(G, gauss, cam, G.Settings(rho=scene.rho, gaussian_only=1), g_frame, image, flush, stream,
+                        args.steps)
+
+    # ---- algorithmic work for the roofline ----
+    G.ges_preprocess(params, cam, st, frame, stream)
+    G.ges_sort(frame, stream)
+    G.ges_render_fwd(frame, st, image, n_eval, stream)
+    torch.cuda.synchronize()
+    e_fwd = int(n_eval.to(torch.int64).sum().item())
+    e_bwd = int(frame.view("n_contrib", torch.int32, W * H).to(torch.int64).sum().item())
+    peaks, peak_src = measured_peaks()
+    clocks = clk.summary()
+    sm_mhz = clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    alu_peak = sms * 128 * sm_mhz * 1e6 / 1e12  # T thread-instr/s
+    rows = {
+        "render_bwd": ("alu", e_bwd * BWD_OPS / (stage_ms[3] / 1e3) / 1e12, alu_peak, "Tinstr/s"),
+        "render_fwd": ("alu", e_fwd * FWD_OPS / (stage_ms[2] / 1e3) / 1e12, alu_peak, "Tinstr/s"),
+    }
+    pre_bytes = preprocess_bytes(P, int(cnt.visible), scene.particles.sh_degree)
+    rows["preprocess"] = ("hbm", pre_bytes / (stage_ms[0] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s")
+    sort_bytes = sort_algorithmic_bytes(P, int(cnt.visible), int(cnt.pairs), frame.c.tile_bits)
+    rows["sort"] = ("hbm", sort_bytes / (stage_ms[1] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s")
+    dom = max(range(4), key=lambda i: stage_ms[i])
+    dname = stage_names[dom]
+    bound, achieved, peak, unit = rows[dname]
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(G, scene, cam, st, frame, dL, dev, stream, args.steps, world)
+    if rank == 0:
+        cpu = None if args.no_cpu else cpu_baseline(scene)
+        line = {
+            "metric": METRIC, "value": value, "unit": "Mpixel-frames/s (fwd+bwd)", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, DESIGN.md recipe)",
+            "config": workload_config(scene, cam, world),
+            "iters_per_s": 1e3 / ms_per_step,
+            "fwd_only": {"value": W * H / (fwd_ms / 1e3) / 1e6 * world, "unit": "Mpixel-frames/s",
+                         "ms": fwd_ms, "fps_per_gpu": 1e3 / fwd_ms},
+            "vs_gaussian_equivalent": {"ges_fwd_ms": fwd_ms, "gaussian_fwd_ms": g_ms, "ratio": g_ms / fwd_ms,
+                                       "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
+            "stages_ms": {n: float(stage_ms[i]) for i, n in enumerate(stage_names)},
+            "counts": {"visible": int(cnt.visible), "pairs": int(cnt.pairs), "evals_fwd": e_fwd, "evals_bwd": e_bwd},
+            "roofline": {"kernel": dname, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+                         "frac": achieved / peak, "traffic": None,
+                         "peak_source": peak_src if bound == "hbm" else
+                         f"derived: {sms} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (median SM clock under load)",
+                         "all": {k: {"bound": v[0], "achieved": v[1], "peak": v[2], "unit": v[3],
+                                     "frac": v[1] / v[2]} for k, v in rows.items()}},
+            "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": LAUNCHES_PER_STEP * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+# algorithmic FP32-pipe thread-instructions per pixel-entry evaluation
+FWD_OPS = 19
+BWD_OPS = 45
+LAUNCHES_PER_STEP = 12  # K1, ranges, 4 depth passes, duplicate, 2 tile passes, K6, K7, K8
+
+
+def preprocess_bytes(P, V, deg):
+    K = (deg + 1) ** 2
+    # reads: 14 floats/particle (mean, log-scale, quat, logit, beta) for all, SH 3K floats for visible;
+    # writes: depth 4 + payload 36 + radius 4 + rect 8 + status/flags 2 = 54 B/particle, visible list 8 B/visible
+    return P * (4 * 12 + 54) + V * (4 * 3 * K + 8)
+
+
+def sort_algorithmic_bytes(P, V, M, tile_bits):
+    depth = 4 * V * 16                      # 4 LSD passes, key+value read+write
+    dup = V * (4 + 8) + M * 8               # read ids + rects, write (tile, id)
+    tile_passes = 1 if tile_bits <= 8 else 2
+    tiles = (tile_passes - 1) * M * 16 + M * 12   # last pass writes values only
+    return depth + dup + tiles
+
+
+def time_forward(G, params, cam, st, frame, image, flush, stream, steps):
+    import torch
+    ms = []
+    for _ in range(2):
+        G.ges_preprocess(params, cam, st, frame, stream)
+        G.ges_sort(frame, stream)
+        G.ges_render_fwd(frame, st, image, None, stream)
+    for _ in range(steps):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        G.ges_preprocess(params, cam, st, frame, stream)
+        G.ges_sort(frame, stream)
+        G.ges_render_fwd(frame, st, image, None, stream)
+        b.record(stream)
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    return float(statistics.mean(ms))
+
+
+def gaussian_equivalent(G, scene, cam, dev):
+    """The equivalent Gaussian rasterizer's input: same particles with the
+    phi-bar factor folded into the log-scales (SCALE mode) so that footprints
+    and pair counts are identical; rendered with gaussian_only = 1."""
+    import torch
+    p = scene.particles
+    beta = p.beta.astype(np.float64)
+    phi = 2.0 / (1.0 + np.exp(-(scene.rho * beta - 2 * scene.rho)))
+    q = p.subset(slice(None))
+    q.log_scale = (p.log_scale.astype(np.float64) + np.log(phi)[None, :]).astype(np.float32)
+    return G.PlanarParams.from_inputs(q, device=dev)
+
+
+def run_e2e(G, scene, cam, st, frame, dL_dev, dev, stream, steps, world):
+    """Public-API step with HOST inputs: pinned particles + dL/dimage copied in,
+    image copied out, every step, inside the timed region."""
+    import torch
+    P, deg = scene.particles.P, scene.particles.sh_degree
+    host_params = G.PlanarParams.from_inputs(scene.particles, device="cpu", pin_memory=True)
+    host_dL = dL_dev.cpu().pin_memory()
+    host_img = torch.empty((3, cam.height, cam.width), dtype=torch.float32).pin_memory()
+    dparams = G.PlanarParams.empty(P, deg, dev)
+    ddL = torch.empty_like(dL_dev)
+    img = torch.empty((3, cam.height, cam.width), dtype=torch.float32, device=dev)
+    grads = G.PlanarParams.zeros(P, deg, dev)
+
+    def one():
+        dparams.flat.copy_(host_params.flat, non_blocking=True)
+        ddL.copy_(host_dL, non_blocking=True)
+        G.ges_preprocess(dparams, cam, st, frame, stream)
+        G.ges_sort(frame, stream)
+        G.ges_render_fwd(frame, st, img, None, stream)
+        G.ges_render_bwd(dparams, cam, st, frame, ddL, grads, False, stream)
+        host_img.copy_(img, non_blocking=True)
+
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        one()
+    b.record(stream)
+    b.synchronize()
+    ms = a.elapsed_time(b) / steps
+    h2d = host_params.flat.numel() * 4 + host_dL.numel() * 4
+    d2h = host_img.numel() * 4
+    return {"value": world * cam.width * cam.height / (ms / 1e3) / 1e6, "unit": "Mpixel-frames/s (fwd+bwd)",
+            "ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "path": "pinned host -> device copy, ges_preprocess/sort/render_fwd/render_bwd, image -> host"}
+
+
+def cpu_baseline(scene):
+    info = oracle_sample(scene, 0, n_tiles=24)
+    cam = scene.cameras[0]
+    value = cam.width * cam.height / info["frame_s"] / 1e6
+    return {"value": value, "unit": "Mpixel-frames/s (fwd+bwd)", "cores": info["threads"], "kind": "oracle",
+            "sample": (f"S1+S5b over all {scene.particles.P} particles, S4+S5a on {info['tiles']} of "
+                       f"{info['T']} tiles, per-frame time extrapolated"),
+            "frame_s": info["frame_s"]}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-tiles", type=int, default=16)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

