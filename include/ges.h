@@ -9,13 +9,13 @@
  *                       Eq. 6 :291-293), EWA projection Sigma' = J W Sigma W^T J^T
  *                       (PAPER.md:249-253), SH colour and opacity kappa
  *                       (PAPER.md:247), screen radius and 16x16-tile rect;
- *                       compacts the visible particles with their depth keys
- *                       and builds the per-tile pair histogram.
- *   ges_sort        S2  depth radix sort of the visible particles, duplication
- *                       into (tile, particle) pairs in depth order, stable
- *                       radix sort by tile id; the resulting order of every
- *                       tile's list is the order of the keys
- *                       (tile_id << 32 | fp32 bits of depth), ties by index.
+ *                       depth keys, digit histograms and the per-tile pair
+ *                       counts (2-D difference grid of the rects).
+ *   ges_sort        S2  depth radix sort of the visible particles (pass 0
+ *                       compacts them), then every (tile, particle) pair is
+ *                       written once into its tile's list; each list is in
+ *                       the order of the keys (tile_id << 32 | fp32 bits of
+ *                       depth), ties by particle index.
  *                   S3  per-tile ranges [ranges[t], ranges[t+1]).
  *   ges_render_fwd  S4  per 16x16 tile front-to-back alpha compositing with
  *                       early termination on transmittance (Eq. 3,
@@ -84,7 +84,7 @@ typedef struct {
 } ges_particles;
 
 typedef struct {
-    int32_t width, height;      /* pixels; tiles_x * tiles_y <= 65536        */
+    int32_t width, height;      /* pixels; 16x16 tiles: tiles_x * tiles_y <= 65536 */
     float fx, fy, cx, cy;       /* pinhole intrinsics (pixels)               */
     float near_z;               /* particles with camera z <= near_z culled  */
     float R[9];                 /* world -> camera rotation, row-major       */
@@ -134,23 +134,30 @@ typedef struct {
     uint8_t *status;       /* [P] ges_particle_status                                   */
     uint8_t *flags;        /* [P] bit0-2 rgb clamped at 0, bit3/4 Jacobian x/y clamped   */
     /* ---- S2 depth sort of the visible particles ---- */
-    uint32_t *vis_key[2];  /* [P] depth bits, ping-pong                                 */
-    uint32_t *vis_val[2];  /* [P] particle index, ping-pong                             */
-    uint32_t *sorted_vis;  /* [P] visible particles in (depth, index) order (alias)     */
+    uint32_t *vis_key[2];  /* [P] depth bits (0xffffffff = not visible), ping-pong */
+    uint32_t *vis_val[2];  /* [P] particle index, ping-pong                      */
+    uint32_t *sorted_vis;  /* [V] visible particles in (depth, index) order (alias) */
+    /* ---- S2 radix scratch ---- */
+    uint32_t *radix_hist;  /* [256][max(P,cap)/4096] per-tile digit counts -> offsets (digit-major) */
+    uint32_t *radix_total; /* [256] digit totals of the current pass               */
     /* ---- S2 pairs and S3 ranges ---- */
-    uint32_t *pair_tile[2];/* [cap] tile id, ping-pong                                  */
-    uint32_t *pair_val[2]; /* [cap] particle index, ping-pong                           */
-    uint32_t *list;        /* [cap] final per-tile lists (alias of a pair_val buffer)   */
-    uint32_t *ranges;      /* [T+1] list of tile t = list[ranges[t] .. ranges[t+1])      */
-    int32_t *tile_diff;    /* [(tiles_y+1)*(tiles_x+1)] 2-D difference grid of rects    */
-    uint32_t *hist;        /* [8][256] radix digit histograms -> exclusive offsets      */
-    uint32_t *lookback;    /* decoupled look-back scratch                               */
-    uint64_t *counters;    /* [GES_CTR_N]                                               */
-    size_t lookback_bytes;
+    uint32_t *item_offset; /* [P] first pair slot of each depth-sorted visible particle */
+    uint32_t *tile_first;  /* [cap/4096+2] sorted particle holding slot 4096*j        */
+    uint32_t *pair_tile;   /* [cap] tile ids after the first tile-digit pass          */
+    uint32_t *pair_val;    /* [cap] particle ids after the first tile-digit pass      */
+    uint32_t *list;        /* [cap] per-tile lists: tile t = list[ranges[t] .. ranges[t+1]) */
+    uint32_t *ranges;      /* [T+1]                                               */
+    int32_t *tile_diff;    /* [(tiles_y+1)*(tiles_x+1)] 2-D difference grid of rects */
+    uint32_t *hist;        /* [8][256] radix digit histograms -> exclusive offsets  */
+    uint32_t *lookback;    /* decoupled look-back scratch                         */
+    uint64_t *counters;    /* [GES_CTR_N]                                         */
+    size_t zero_bytes;     /* bytes from `counters` zeroed at the start of a frame */
     /* ---- S4 / S5 ---- */
     float *final_T;        /* [H*W] transmittance after the last composited particle   */
     uint32_t *n_contrib;   /* [H*W] list position of the last composited particle + 1  */
-    float *grad2d;         /* [9][P] dL/d(u, v, a, b, c, kappa, r, g, b)                 */
+    float *grad2d;         /* [P][12] per-particle 2-D gradient record (du, dv, dA, dB |
+                              dC, dkappa, dr, dg | db, 0, 0, 0), A..C = the log2-scaled
+                              conic; kept all-zero between backward passes            */
     size_t workspace_bytes;
 } ges_frame;
 
@@ -158,7 +165,9 @@ typedef struct {
 size_t ges_workspace_bytes(int64_t P, int32_t width, int32_t height, int64_t pair_capacity);
 
 /* Carve `frame` out of `workspace` (device, >= ges_workspace_bytes(...) bytes,
- * 256-byte aligned).  Host-only; no device work. */
+ * 256-byte aligned).  Host-only; no device work.  The workspace must be
+ * zero-filled once before the frame's first ges_render_bwd (the backward
+ * keeps frame.grad2d zero between calls instead of clearing it per frame). */
 ges_status ges_frame_init(void *workspace, size_t bytes, int64_t P, int32_t width, int32_t height,
                           int64_t pair_capacity, ges_frame *frame);
 

@@ -57,9 +57,10 @@ class ges_frame(C.Structure):
         ("depth", C.c_void_p), ("pay0", C.c_void_p), ("pay1", C.c_void_p), ("pay2", C.c_void_p),
         ("radius", C.c_void_p), ("rect", C.c_void_p), ("status", C.c_void_p), ("flags", C.c_void_p),
         ("vis_key", C.c_void_p * 2), ("vis_val", C.c_void_p * 2), ("sorted_vis", C.c_void_p),
-        ("pair_tile", C.c_void_p * 2), ("pair_val", C.c_void_p * 2), ("list", C.c_void_p),
+        ("radix_hist", C.c_void_p), ("radix_total", C.c_void_p), ("item_offset", C.c_void_p), ("tile_first", C.c_void_p), ("pair_tile", C.c_void_p),
+        ("pair_val", C.c_void_p), ("list", C.c_void_p),
         ("ranges", C.c_void_p), ("tile_diff", C.c_void_p), ("hist", C.c_void_p), ("lookback", C.c_void_p),
-        ("counters", C.c_void_p), ("lookback_bytes", C.c_size_t),
+        ("counters", C.c_void_p), ("zero_bytes", C.c_size_t),
         ("final_T", C.c_void_p), ("n_contrib", C.c_void_p), ("grad2d", C.c_void_p),
         ("workspace_bytes", C.c_size_t),
     ]

@@ -116,7 +116,7 @@ class Frame:
         nbytes = lib.ges_workspace_bytes(P, width, height, pair_capacity)
         if nbytes == 0:
             raise L.GESError("invalid frame size")
-        self.ws = torch.empty(nbytes + 256, dtype=torch.uint8, device=device)
+        self.ws = torch.zeros(nbytes + 256, dtype=torch.uint8, device=device)  # zero once (ges.h)
         base = self.ws.data_ptr()
         self.offset = (-base) % 256
         self.c = L.ges_frame()

@@ -1,6 +1,7 @@
 // ges_api.cu -- the C ABI (include/ges.h): workspace layout, argument checks
 // and the launch sequence of each stage.  Host code only; every kernel lives
 // in preprocess.cu / sort.cu / render.cu / particle_bwd.cu.
+#include <algorithm>
 #include <cstring>
 
 #include "ges_internal.h"
@@ -24,19 +25,15 @@ namespace {
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
-// Lookback scratch: K1 (1 word / tile), 4 depth passes, duplication, 2 tile passes.
+// Look-back scratch of the item scan (the radix passes are chain-free).
 struct LookbackLayout {
-    size_t pre, depth[4], dup, tile[2], total;  // word offsets
+    size_t scan, total;  // word offsets
 };
 
-LookbackLayout lookback_layout(int64_t P, int64_t cap) {
+LookbackLayout lookback_layout(int64_t P, int64_t /*cap*/) {
     LookbackLayout L;
-    size_t o = 0;
-    L.pre = o; o += (size_t)preprocess_lookback_words(P);
-    for (int d = 0; d < 4; ++d) { L.depth[d] = o; o += (size_t)radix_tiles(P) * kRadixDigits; }
-    L.dup = o; o += (size_t)duplicate_tiles(P);
-    for (int d = 0; d < 2; ++d) { L.tile[d] = o; o += (size_t)radix_tiles(cap) * kRadixDigits; }
-    L.total = o;
+    L.scan = 0;
+    L.total = (size_t)item_scan_tiles(P);
     return L;
 }
 
@@ -69,7 +66,7 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     g.hist = (uint32_t*)take(sizeof(uint32_t) * 8 * 256);
     g.tile_diff = (int32_t*)take(sizeof(int32_t) * (size_t)(tx + 1) * (ty + 1));
     g.lookback = (uint32_t*)take(sizeof(uint32_t) * L.total);
-    g.lookback_bytes = off;  // bytes of the zero region from the workspace base
+    g.zero_bytes = off;  // bytes of the zero region from the workspace base
     // --- per particle ---
     g.depth = (float*)take(sizeof(float) * P);
     g.pay0 = (float*)take(16 * (size_t)P);
@@ -84,15 +81,17 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
         g.vis_val[k] = (uint32_t*)take(sizeof(uint32_t) * P);
     }
     g.sorted_vis = g.vis_val[0];
-    for (int k = 0; k < 2; ++k) {
-        g.pair_tile[k] = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
-        g.pair_val[k] = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
-    }
-    g.list = (g.tile_bits <= 8) ? g.pair_val[1] : g.pair_val[0];
+    g.radix_hist = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * (size_t)radix_tiles(std::max<int64_t>(P, cap)));
+    g.radix_total = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits);
+    g.item_offset = (uint32_t*)take(sizeof(uint32_t) * P);
+    g.tile_first = (uint32_t*)take(sizeof(uint32_t) * (size_t)slot_tiles(cap));
+    g.pair_tile = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
+    g.pair_val = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
+    g.list = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
     g.ranges = (uint32_t*)take(sizeof(uint32_t) * (size_t)(T + 1));
     g.final_T = (float*)take(sizeof(float) * HW);
     g.n_contrib = (uint32_t*)take(sizeof(uint32_t) * HW);
-    g.grad2d = (float*)take(sizeof(float) * 9 * (size_t)P);
+    g.grad2d = (float*)take(sizeof(float) * kGrad2dStride * (size_t)P);
     g.workspace_bytes = off;
     if (f) *f = g;
     return off;
@@ -150,7 +149,7 @@ ges_status ges_preprocess(const ges_particles* particles, const ges_camera* came
         !(settings->rho >= 0.0f) || (settings->phi_mode != GES_PHI_SCALE && settings->phi_mode != GES_PHI_VARIANCE))
         return GES_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
-    cudaError_t e = cudaMemsetAsync(frame->counters, 0, frame->lookback_bytes, s);
+    cudaError_t e = cudaMemsetAsync(frame->counters, 0, frame->zero_bytes, s);
     if (e != cudaSuccess) return GES_ERR_CUDA;
     PreprocessArgs a;
     a.mean = particles->mean; a.log_scale = particles->log_scale; a.quat = particles->quat;
@@ -160,10 +159,8 @@ ges_status ges_preprocess(const ges_particles* particles, const ges_camera* came
     a.cam = cam_params(camera);
     a.depth = frame->depth; a.pay0 = (float4*)frame->pay0; a.pay1 = (float4*)frame->pay1; a.pay2 = frame->pay2;
     a.radius = frame->radius; a.rect = (ushort4*)frame->rect; a.status = frame->status; a.flags = frame->flags;
-    a.vis_key = frame->vis_key[0]; a.vis_val = frame->vis_val[0];
+    a.vis_key = frame->vis_key[0];
     a.tile_diff = frame->tile_diff; a.hist = frame->hist;
-    const LookbackLayout L = lookback_layout(frame->P, frame->pair_capacity);
-    a.lookback = frame->lookback + L.pre;
     a.counters = (unsigned long long*)frame->counters;
     return cuda_status(launch_preprocess(a, s));
 }
@@ -179,42 +176,58 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     r.capacity = frame->pair_capacity;
     cudaError_t e = launch_ranges(r, s);
     if (e != cudaSuccess) return GES_ERR_CUDA;
-    // depth sort of the visible particles: 4 x 8-bit passes, ping-pong 0 -> 1 -> 0 -> 1 -> 0
+    // depth sort: pass 0 reads all P keys and drops the non-visible ones (compaction);
+    // ping-pong (vis_key[0]) -> 1 -> 0 -> 1 -> (vis_val[0])
     for (int d = 0; d < 4; ++d) {
         RadixPassArgs p;
-        p.keys_in = frame->vis_key[d & 1]; p.vals_in = frame->vis_val[d & 1];
-        p.keys_out = (d < 3) ? frame->vis_key[(d + 1) & 1] : nullptr;
-        p.vals_out = frame->vis_val[(d + 1) & 1];
-        p.count = ctr + GES_CTR_VISIBLE; p.max_items = frame->P;
-        p.digit_offset = frame->hist + d * 256;
-        p.lookback = frame->lookback + L.depth[d];
-        p.tile_counter = ctr + GES_CTR_TILE0 + 1 + d;
+        std::memset(&p, 0, sizeof(p));
+        const int in = (d == 0) ? 0 : ((d & 1) ? 1 : 0);
+        const int out = in ^ 1;
+        p.keys_in = frame->vis_key[in];
+        p.vals_in = (d == 0) ? nullptr : frame->vis_val[in];
+        p.keys_out = (d < 3) ? frame->vis_key[out] : nullptr;
+        p.vals_out = frame->vis_val[out];
+        p.count = (d == 0) ? nullptr : ctr + GES_CTR_VISIBLE;
+        p.max_items = frame->P;
+        p.tile_hist = frame->radix_hist;
+        p.hist_stride = radix_tiles(std::max<int64_t>(frame->P, frame->pair_capacity));
+        p.digit_total = frame->radix_total;
         p.shift = 8 * d;
-        p.overflow = nullptr;
+        p.drop_invalid = (d == 0) ? 1 : 0;
         if ((e = launch_radix_pass(p, s)) != cudaSuccess) return GES_ERR_CUDA;
     }
     frame->sorted_vis = frame->vis_val[0];
-    DuplicateArgs dp;
-    dp.sorted_vis = frame->sorted_vis; dp.rect = (const ushort4*)frame->rect; dp.counters = ctr;
-    dp.tiles_x = frame->tiles_x; dp.pair_tile = frame->pair_tile[0]; dp.pair_val = frame->pair_val[0];
-    dp.lookback = frame->lookback + L.dup; dp.tile_counter = ctr + GES_CTR_TILE0 + 5; dp.max_items = frame->P;
-    if ((e = launch_duplicate(dp, s)) != cudaSuccess) return GES_ERR_CUDA;
-    // stable sort of the pairs by tile id: 1 or 2 passes
+    // first pair slot of every sorted particle
+    ItemScanArgs is;
+    is.sorted_vis = frame->sorted_vis; is.rect = (const ushort4*)frame->rect; is.counters = ctr;
+    is.E = frame->item_offset; is.tile_first = frame->tile_first; is.lookback = frame->lookback + L.scan;
+    is.tile_counter = ctr + GES_CTR_TILE0;
+    if ((e = launch_item_scan(is, frame->P, s)) != cudaSuccess) return GES_ERR_CUDA;
+    // stable sort of the pairs by tile id; the first pass generates the pairs
     const int passes = frame->tile_bits <= 8 ? 1 : 2;
     for (int d = 0; d < passes; ++d) {
         RadixPassArgs p;
-        p.keys_in = frame->pair_tile[d]; p.vals_in = frame->pair_val[d];
-        p.keys_out = (d + 1 < passes) ? frame->pair_tile[d + 1] : nullptr;
-        p.vals_out = frame->pair_val[(d + 1) & 1];
-        p.count = ctr + GES_CTR_PAIRS; p.max_items = frame->pair_capacity;
-        p.digit_offset = frame->hist + (4 + d) * 256;
-        p.lookback = frame->lookback + L.tile[d];
-        p.tile_counter = ctr + GES_CTR_TILE0 + 6 + d;
+        std::memset(&p, 0, sizeof(p));
+        p.gen = (d == 0) ? 1 : 0;
+        p.keys_in = (d == 0) ? nullptr : frame->pair_tile;
+        p.vals_in = (d == 0) ? nullptr : frame->pair_val;
+        p.keys_out = (d + 1 < passes) ? frame->pair_tile : nullptr;
+        p.vals_out = (d + 1 < passes) ? frame->pair_val : frame->list;
+        p.count = ctr + GES_CTR_PAIRS;
+        p.max_items = frame->pair_capacity;
+        p.tile_hist = frame->radix_hist;
+        p.hist_stride = radix_tiles(std::max<int64_t>(frame->P, frame->pair_capacity));
+        p.digit_total = frame->radix_total;
         p.shift = 8 * d;
         p.overflow = ctr + GES_CTR_OVERFLOW;
+        p.tiles_x = frame->tiles_x;
+        p.sorted_vis = frame->sorted_vis;
+        p.rect = (const ushort4*)frame->rect;
+        p.E = frame->item_offset;
+        p.tile_first = frame->tile_first;
+        p.counters = ctr;
         if ((e = launch_radix_pass(p, s)) != cudaSuccess) return GES_ERR_CUDA;
     }
-    frame->list = frame->pair_val[passes & 1];
     return GES_OK;
 }
 
@@ -237,7 +250,6 @@ ges_status ges_render_bwd(const ges_particles* particles, const ges_camera* came
         !grads->sh || !grads->beta)
         return GES_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
-    if (cudaMemsetAsync(frame->grad2d, 0, sizeof(float) * 9 * (size_t)frame->P, s) != cudaSuccess) return GES_ERR_CUDA;
     RenderBwdArgs b;
     b.pay0 = (const float4*)frame->pay0; b.pay1 = (const float4*)frame->pay1; b.pay2 = frame->pay2;
     b.list = frame->list; b.ranges = frame->ranges; b.counters = (const unsigned long long*)frame->counters;

@@ -23,16 +23,13 @@ struct PreprocessArgs {
     ushort4* rect;
     uint8_t* status;
     uint8_t* flags;
-    uint32_t* vis_key;
-    uint32_t* vis_val;
+    uint32_t* vis_key;    // [P] depth bits, 0xffffffff if not visible
     int32_t* tile_diff;
     uint32_t* hist;       // [4][256] depth digits
-    uint32_t* lookback;   // [tiles]
     unsigned long long* counters;
 };
 
 cudaError_t launch_preprocess(const PreprocessArgs& a, cudaStream_t stream);
-int64_t preprocess_lookback_words(int64_t P);
 
 // --- sort / ranges ---------------------------------------------------------
 struct RangesArgs {
@@ -49,36 +46,45 @@ int num_sms();
 
 struct RadixPassArgs {
     const uint32_t* keys_in;
-    const uint32_t* vals_in;
+    const uint32_t* vals_in;          // null: the value is the input index
     uint32_t* keys_out;               // may be null (last pass)
     uint32_t* vals_out;
-    const unsigned long long* count;  // device item count
+    const unsigned long long* count;  // device item count (null: max_items)
     int64_t max_items;                // upper bound (grid sizing); items beyond are ignored
-    const uint32_t* digit_offset;     // [256] exclusive offsets of this pass's digits
-    uint32_t* lookback;               // [tiles][256], zeroed
-    unsigned long long* tile_counter; // zeroed
+    uint32_t* tile_hist;              // [256][hist_stride] per-tile digit counts -> offsets (digit-major)
+    int64_t hist_stride;              // >= number of tiles
+    uint32_t* digit_total;            // [256] column totals
     int shift;
-    const unsigned long long* overflow;  // if non-null and *overflow != 0: do nothing
+    int drop_invalid;                 // 1: keys == 0xffffffff are dropped (compaction)
+    const unsigned long long* overflow;  // non-null and set: do nothing
+    // gen = 1: keys/values generated from the sorted particles (pair expansion)
+    int gen;
+    int tiles_x;
+    const uint32_t* sorted_vis;
+    const ushort4* rect;
+    const uint32_t* E;
+    const uint32_t* tile_first;
+    const unsigned long long* counters;
 };
 cudaError_t launch_radix_pass(const RadixPassArgs& a, cudaStream_t stream);
 int64_t radix_tiles(int64_t n);
 constexpr int kRadixDigits = 256;
 
-struct DuplicateArgs {
-    const uint32_t* sorted_vis;       // [V] particle ids in depth order
+struct ItemScanArgs {
+    const uint32_t* sorted_vis;
     const ushort4* rect;
-    const unsigned long long* counters;  // visible count, overflow flag
-    int tiles_x;
-    uint32_t* pair_tile;
-    uint32_t* pair_val;
+    const unsigned long long* counters;
+    uint32_t* E;                      // [P]
+    uint32_t* tile_first;             // [cap/4096 + 2]
     uint32_t* lookback;               // [tiles]
     unsigned long long* tile_counter;
-    int64_t max_items;
 };
-cudaError_t launch_duplicate(const DuplicateArgs& a, cudaStream_t stream);
-int64_t duplicate_tiles(int64_t P);
+cudaError_t launch_item_scan(const ItemScanArgs& a, int64_t max_items, cudaStream_t stream);
+int64_t item_scan_tiles(int64_t n);
+int64_t slot_tiles(int64_t cap);
 
 // --- render ----------------------------------------------------------------
+constexpr int kGrad2dStride = 12;  // floats per particle in grad2d (3 x float4)
 struct RenderFwdArgs {
     const float4* pay0;
     const float4* pay1;
@@ -107,7 +113,7 @@ struct RenderBwdArgs {
     const float* final_T;
     const uint32_t* n_contrib;
     const float* dL_dimage;
-    float* grad2d;  // [9][P]: du, dv, dA, dB, dC (pre-scaled conic), dkappa, dr, dg, db
+    float* grad2d;  // [P][12]: du, dv, dA, dB | dC (pre-scaled conic), dkappa, dr, dg | db, 0, 0, 0
     int P;
 };
 cudaError_t launch_render_bwd(const RenderBwdArgs& a, cudaStream_t stream);
@@ -120,7 +126,7 @@ struct ParticleBwdArgs {
     CamParams cam;
     const uint8_t* status;
     const uint8_t* flags;
-    const float* grad2d;
+    float* grad2d;
     float *g_mean, *g_log_scale, *g_quat, *g_opacity_logit, *g_sh, *g_beta;
     int accumulate;
 };

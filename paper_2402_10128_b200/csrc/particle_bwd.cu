@@ -43,11 +43,12 @@ __global__ void __launch_bounds__(256) particle_bwd_kernel(ParticleBwdArgs a) {
     const float W[9] = {cam.R[0], cam.R[1], cam.R[2], cam.R[3], cam.R[4], cam.R[5], cam.R[6], cam.R[7], cam.R[8]};
     const int fl = a.flags[i];
     // ---- forward recompute ----
-    const float m0 = a.mean[i], m1 = a.mean[P + i], m2 = a.mean[2 * P + i];
+    const float m0 = __ldg(a.mean + i), m1 = __ldg(a.mean + P + i), m2 = __ldg(a.mean + 2 * P + i);
     const float tx = W[0] * m0 + W[1] * m1 + W[2] * m2 + cam.t[0];
     const float ty = W[3] * m0 + W[4] * m1 + W[5] * m2 + cam.t[1];
     const float tz = W[6] * m0 + W[7] * m1 + W[8] * m2 + cam.t[2];
-    const float q0 = a.quat[i], q1 = a.quat[P + i], q2 = a.quat[2 * P + i], q3 = a.quat[3 * P + i];
+    const float q0 = __ldg(a.quat + i), q1 = __ldg(a.quat + P + i), q2 = __ldg(a.quat + 2 * P + i),
+                q3 = __ldg(a.quat + 3 * P + i);
     const float nq = sqrtf(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
     const float inq = 1.0f / nq;
     const float w = q0 * inq, x = q1 * inq, y = q2 * inq, z = q3 * inq;
@@ -56,14 +57,14 @@ __global__ void __launch_bounds__(256) particle_bwd_kernel(ParticleBwdArgs a) {
                         2.f * (x * z - w * y), 2.f * (y * z + w * x), 1.f - 2.f * (x * x + y * y)};
     float phi = 1.f, mfac = 1.f, dm_dbeta = 0.f;
     if (!a.gaussian_only) {
-        phi = 2.f / (1.f + expf(-(a.rho * (a.beta[i] - 2.f))));
+        phi = 2.f / (1.f + expf(-(a.rho * (__ldg(a.beta + i) - 2.f))));
         const float dphi = a.rho * phi * (1.f - 0.5f * phi);
         if (a.phi_mode == GES_PHI_VARIANCE) { mfac = sqrtf(phi); dm_dbeta = 0.5f * dphi / mfac; }
         else { mfac = phi; dm_dbeta = dphi; }
     }
     float s[3], se[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) { s[k] = expf(a.log_scale[(size_t)k * P + i]); se[k] = s[k] * mfac; }
+    for (int k = 0; k < 3; ++k) { s[k] = expf(__ldg(a.log_scale + (size_t)k * P + i)); se[k] = s[k] * mfac; }
     float M[9];
 #pragma unroll
     for (int j = 0; j < 3; ++j)
@@ -98,12 +99,16 @@ __global__ void __launch_bounds__(256) particle_bwd_kernel(ParticleBwdArgs a) {
     const float idet = 1.f / det, idet2 = idet * idet;
 
     // ---- incoming 2-D gradients (pre-scaled conic -> a, b, c) ----
-    const float du = a.grad2d[i], dv = a.grad2d[(size_t)P + i];
-    const float da = a.grad2d[(size_t)2 * P + i] * (-0.5f * kLog2e);
-    const float db = a.grad2d[(size_t)3 * P + i] * (-kLog2e);
-    const float dc = a.grad2d[(size_t)4 * P + i] * (-0.5f * kLog2e);
-    const float dk = a.grad2d[(size_t)5 * P + i];
-    float drgb[3] = {a.grad2d[(size_t)6 * P + i], a.grad2d[(size_t)7 * P + i], a.grad2d[(size_t)8 * P + i]};
+    // 12-float record (du, dv, dA, dB | dC, dkappa, dr, dg | db, -, -, -), zeroed
+    // after reading so the buffer is clean for the next frame's backward
+    float4* rec = reinterpret_cast<float4*>(a.grad2d) + (size_t)i * (kGrad2dStride / 4);
+    const float4 r0 = rec[0], r1 = rec[1], r2 = rec[2];
+    const float du = r0.x, dv = r0.y;
+    const float da = r0.z * (-0.5f * kLog2e);
+    const float db = r0.w * (-kLog2e);
+    const float dc = r1.x * (-0.5f * kLog2e);
+    const float dk = r1.y;
+    float drgb[3] = {r1.z, r1.w, r2.x};
 
     // conic -> (A, B, C)
     const float gA = da * (-C * C * idet2) + db * (B * C * idet2) + dc * (idet - A * C * idet2);
@@ -188,12 +193,13 @@ __global__ void __launch_bounds__(256) particle_bwd_kernel(ParticleBwdArgs a) {
     for (int k = 0; k < K; ++k) {
         float acc3 = 0.f;
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) {
-            put(a.g_sh, 3 * k + ch, Y[k] * drgb[ch]);
-            acc3 += drgb[ch] * a.sh[(size_t)(3 * k + ch) * P + i];
-        }
+        for (int ch = 0; ch < 3; ++ch) acc3 += drgb[ch] * __ldg(a.sh + (size_t)(3 * k + ch) * P + i);
         wsh[k] = acc3;
     }
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) put(a.g_sh, 3 * k + ch, Y[k] * drgb[ch]);
 #pragma unroll
     for (int k = K; k < 16; ++k) wsh[k] = 0.f;
     float gx, gy, gz;
@@ -204,8 +210,11 @@ __global__ void __launch_bounds__(256) particle_bwd_kernel(ParticleBwdArgs a) {
     dmean[2] += (gz - uz * dotd) * idn;
 #pragma unroll
     for (int k = 0; k < 3; ++k) put(a.g_mean, k, dmean[k]);
-    const float kap = 1.f / (1.f + expf(-a.opacity_logit[i]));
+    const float kap = 1.f / (1.f + expf(-__ldg(a.opacity_logit + i)));
     put(a.g_opacity_logit, 0, dk * kap * (1.f - kap));
+    // leave the 2-D record zeroed for the next backward (ges.h)
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    rec[0] = z4; rec[1] = z4; rec[2] = z4;
 }
 
 cudaError_t launch_particle_bwd(const ParticleBwdArgs& a, cudaStream_t stream) {

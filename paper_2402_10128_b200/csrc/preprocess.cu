@@ -1,7 +1,7 @@
 // preprocess.cu -- S1: per-particle projection of GES
-// particles, fused with visible-list compaction (decoupled look-back), the
-// depth-key digit histograms of the following radix sort and the 2-D
-// difference grid of the particles' tile rects (-> per-tile pair counts).
+// particles, fused with the depth keys and digit histograms of the following
+// radix sort and the 2-D difference grid of the particles' tile rects
+// (-> per-tile pair counts).
 //
 // Paper: Eq. 2 kernel and Sigma; PAPER.md:249-254 EWA
 // Sigma' = J W Sigma W^T J^T with Sigma = R S S^T R^T and S "modified by"
@@ -13,9 +13,10 @@
 // HBM-bound: reads 48 B/particle (mean, log-scale, quat, logit, beta) plus 12K
 // bytes of SH for visible particles only; coalesced planar loads (lane i of a
 // warp reads element i of each plane).
+#include <algorithm>
+
 #include "ges_device.cuh"
 #include "ges_internal.h"
-#include "ges_scan.cuh"
 
 namespace ges {
 
@@ -168,31 +169,21 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
 }
 
 constexpr int kPreThreads = 256;
-constexpr int kPreItems = 4;
-constexpr int kPreTile = kPreThreads * kPreItems;
 
+// Grid-stride over particles: no cross-CTA dependency.  Every particle writes
+// its sort key (fp32 depth bits, or 0xffffffff when not visible -- dropped by
+// depth pass 0, which thereby compacts the visible set), its S1 state, and,
+// if visible, +/-1 into the 2-D difference grid of tile rects (-> per-tile
+// pair counts) and the four depth-digit histograms (block-aggregated).
 template <int K>
-__global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs a) {
+__global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(PreprocessArgs a) {
     __shared__ uint32_t s_hist[4][256];
-    __shared__ uint32_t s_warp[kPreItems][kPreThreads / 32];
-    __shared__ uint32_t s_tile, s_base;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     for (int k = tid; k < 4 * 256; k += kPreThreads) (&s_hist[0][0])[k] = 0;
-    if (tid == 0) s_tile = (uint32_t)atomicAdd(&a.counters[GES_CTR_TILE0], 1ull);
     __syncthreads();
-    const uint32_t tile = s_tile;
     const CamDerived cd = derive_camera(a.cam);
     const int stride_diff = a.cam.tiles_x + 1;
-
-    bool vis[kPreItems];
-    uint32_t key[kPreItems];
-#pragma unroll
-    for (int j = 0; j < kPreItems; ++j) {
-        const int64_t i64 = (int64_t)tile * kPreTile + j * kPreThreads + tid;
-        vis[j] = false;
-        key[j] = 0;
-        if (i64 >= a.P) continue;
-        const int i = (int)i64;
+    for (int i = blockIdx.x * kPreThreads + tid; i < a.P; i += gridDim.x * kPreThreads) {
         const PreOut o = preprocess_one<K>(a, cd, i);
         a.depth[i] = o.depth;
         a.pay0[i] = make_float4(o.u, o.v, o.ca, o.cb);
@@ -202,69 +193,42 @@ __global__ void __launch_bounds__(kPreThreads) preprocess_kernel(PreprocessArgs 
         a.rect[i] = make_ushort4((uint16_t)o.x0, (uint16_t)o.y0, (uint16_t)o.x1, (uint16_t)o.y1);
         a.status[i] = o.status;
         a.flags[i] = o.flags;
+        uint32_t key = 0xffffffffu;
         if (o.status == GES_VISIBLE) {
-            vis[j] = true;
-            key[j] = __float_as_uint(o.depth);
+            key = __float_as_uint(o.depth);
 #pragma unroll
-            for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(key[j] >> (8 * d)) & 255u], 1u);
+            for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(key >> (8 * d)) & 255u], 1u);
             atomicAdd(&a.tile_diff[o.y0 * stride_diff + o.x0], 1);
             atomicAdd(&a.tile_diff[o.y0 * stride_diff + o.x1], -1);
             atomicAdd(&a.tile_diff[o.y1 * stride_diff + o.x0], -1);
             atomicAdd(&a.tile_diff[o.y1 * stride_diff + o.x1], 1);
         }
-    }
-    // compaction in index order: item (j, warp, lane)
-    uint32_t ball[kPreItems];
-#pragma unroll
-    for (int j = 0; j < kPreItems; ++j) {
-        ball[j] = __ballot_sync(0xffffffffu, vis[j]);
-        if (lane == 0) s_warp[j][warp] = __popc(ball[j]);
+        a.vis_key[i] = key;
     }
     __syncthreads();
-    if (warp == 0) {
-        // exclusive scan of the kPreItems * 8 warp counts (j-major) in one warp
-        uint32_t v = (lane < kPreItems * 8) ? (&s_warp[0][0])[lane] : 0u;
-        uint32_t incl = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += n;
-        }
-        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-        if (lane < kPreItems * 8) (&s_warp[0][0])[lane] = incl - v;
-        const uint32_t prefix = lookback_warp(a.lookback, tile, total);
-        if (lane == 0) {
-            s_base = prefix;
-            if (total) atomicAdd(&a.counters[GES_CTR_VISIBLE], (unsigned long long)total);
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kPreItems; ++j) {
-        if (!vis[j]) continue;
-        const uint32_t pos = s_base + s_warp[j][warp] + __popc(ball[j] & ((1u << lane) - 1u));
-        a.vis_key[pos] = key[j];
-        a.vis_val[pos] = (uint32_t)((int64_t)tile * kPreTile + j * kPreThreads + tid);
-    }
+    uint32_t nvis = 0;
     for (int k = tid; k < 4 * 256; k += kPreThreads) {
         const uint32_t h = (&s_hist[0][0])[k];
+        if (k < 256) nvis += h;
         if (h) atomicAdd(&a.hist[k], h);
     }
+    // visible count = sum of the digit-0 histogram
+    for (int o = 16; o > 0; o >>= 1) nvis += __shfl_xor_sync(0xffffffffu, nvis, o);
+    if ((tid & 31) == 0 && nvis) atomicAdd(&a.counters[GES_CTR_VISIBLE], (unsigned long long)nvis);
 }
 
 cudaError_t launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {
-    const int64_t tiles = (a.P + kPreTile - 1) / kPreTile;
-    dim3 grid((unsigned)tiles), block(kPreThreads);
+    const int64_t need = (a.P + kPreThreads - 1) / kPreThreads;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)num_sms() * 6));
+    dim3 g((unsigned)grid), block(kPreThreads);
     switch (a.sh_degree) {
-        case 0: preprocess_kernel<1><<<grid, block, 0, stream>>>(a); break;
-        case 1: preprocess_kernel<4><<<grid, block, 0, stream>>>(a); break;
-        case 2: preprocess_kernel<9><<<grid, block, 0, stream>>>(a); break;
-        case 3: preprocess_kernel<16><<<grid, block, 0, stream>>>(a); break;
+        case 0: preprocess_kernel<1><<<g, block, 0, stream>>>(a); break;
+        case 1: preprocess_kernel<4><<<g, block, 0, stream>>>(a); break;
+        case 2: preprocess_kernel<9><<<g, block, 0, stream>>>(a); break;
+        case 3: preprocess_kernel<16><<<g, block, 0, stream>>>(a); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
-
-int64_t preprocess_lookback_words(int64_t P) { return (P + kPreTile - 1) / kPreTile; }
 
 }  // namespace ges

@@ -7,22 +7,37 @@
 // the Gaussian of the phi-bar-scaled covariance (the paper's approximate
 // rasterization "without taking the beta exponent"; R6).
 //
-// One CTA per tile, one thread per pixel.  Each batch of 256 list entries is
-// gathered once into shared memory (payload of the particle: 36 B) and then
-// evaluated by all 256 pixels; __syncthreads_count retires a tile as soon as
-// every pixel has terminated.  The backward walks the same lists back to
+// One CTA per tile, PPT (= 2) pixels per thread; warp w owns the
+// 8 x (4 PPT)-pixel region (x0 = 8 (w & 1), y0 = 4 PPT (w >> 1)) of the tile.
+// Each batch of 512 list
+// entries is gathered once into shared memory; while gathering, each thread
+// tests its entry against the 8 warp regions with an exact lower bound of the
+// Mahalanobis form over the region (the minimum of a positive-definite
+// quadratic over a box) and marks the regions where alpha >= 1/255 is
+// possible.  Each warp then walks only its own compacted entry list.  The
+// test is conservative (a margin of 0.01 in log2 units), so culled entries are
+// exactly the ones every pixel of the region would skip: results are
+// identical to the unculled loop.  __syncthreads_count retires the tile once
+// all pixels have terminated.  The backward walks the same lists back to
 // front from the last composited entry and reduces the nine per-pair
-// gradients across each warp with a recursive-halving shuffle (16 SHFL per
-// warp and entry instead of 45) into shared accumulators that are flushed
-// with one global atomic per (particle, tile, component).
+// gradients across each warp with a recursive-halving shuffle (24 SHFL per
+// warp and entry) and adds them with three vector reductions
+// (red.global.add.v4.f32) into the particle's 12-float gradient record.
 #include "ges_internal.h"
 
 namespace ges {
 
-__device__ __forceinline__ Splat2D load_splat(const float4* pay0, const float4* pay1, const float* pay2, uint32_t p) {
+constexpr int kBatch = 512;               // list entries staged per barrier
+constexpr float kCullMargin = 0.01f;      // log2 units (0.7% in alpha)
+
+struct Splat {
+    float u, v, A, B, C, kappa, r, g, b;
+};
+
+__device__ __forceinline__ Splat load_splat(const float4* pay0, const float4* pay1, const float* pay2, uint32_t p) {
     const float4 a = __ldg(pay0 + p);
     const float4 b = __ldg(pay1 + p);
-    Splat2D s;
+    Splat s;
     s.u = a.x; s.v = a.y;
     s.A = __fmul_rn(__fmul_rn(-0.5f, a.z), kLog2e);
     s.B = __fmul_rn(-a.w, kLog2e);
@@ -32,92 +47,212 @@ __device__ __forceinline__ Splat2D load_splat(const float4* pay0, const float4* 
     return s;
 }
 
-// exact same instruction sequence in forward and backward
-__device__ __forceinline__ float raw_exponent(const Splat2D& s, float dx, float dy) {
-    const float t1 = __fmaf_rn(s.A, dx, __fmul_rn(s.B, dy));
-    const float t2 = __fmul_rn(__fmul_rn(s.C, dy), dy);
+// p2 = A dx^2 + B dx dy + C dy^2 (log2 units), fixed op order: the forward and
+// the backward evaluate exactly this sequence, so their decisions agree.
+__device__ __forceinline__ float raw_exponent(float A, float B, float C, float dx, float dy) {
+    const float t1 = __fmaf_rn(A, dx, __fmul_rn(B, dy));
+    const float t2 = __fmul_rn(__fmul_rn(C, dy), dy);
     return __fmaf_rn(dx, t1, t2);
 }
 
-__global__ void __launch_bounds__(kBlock) render_fwd_kernel(RenderFwdArgs a) {
-    __shared__ float4 s_g0[kBlock];
-    __shared__ float4 s_g1[kBlock];
-    __shared__ float s_b[kBlock];
-    const int tile = blockIdx.x;
-    const int tid = threadIdx.x;
-    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int px = tx * kTile + (tid & (kTile - 1)), py = ty * kTile + (tid >> 4);
-    const bool inside = px < a.W && py < a.H;
-    const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;
-    uint32_t start = a.ranges[tile], end = a.ranges[tile + 1];
-    if (a.counters[GES_CTR_OVERFLOW]) start = end = 0;
-    float T = 1.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
-    bool done = !inside;
-    uint32_t last = 0, n_eval = end - start;
-    for (uint32_t b0 = start; b0 < end; b0 += kBlock) {
-        if (__syncthreads_count(done) == kBlock) break;
-        const uint32_t k = b0 + tid;
-        if (k < end) {
-            const Splat2D s = load_splat(a.pay0, a.pay1, a.pay2, __ldg(a.list + k));
-            s_g0[tid] = make_float4(s.u, s.v, s.A, s.B);
-            s_g1[tid] = make_float4(s.C, s.kappa, s.r, s.g);
-            s_b[tid] = s.b;
-        }
-        __syncthreads();
-        if (!done) {
-            const int n = (int)min((uint32_t)kBlock, end - b0);
-            for (int j = 0; j < n; ++j) {
-                const float4 g0 = s_g0[j];
-                const float4 g1 = s_g1[j];
-                Splat2D s;
-                s.u = g0.x; s.v = g0.y; s.A = g0.z; s.B = g0.w; s.C = g1.x;
-                const float dx = __fsub_rn(s.u, fpx), dy = __fsub_rn(s.v, fpy);
-                const float p2 = fminf(raw_exponent(s, dx, dy), 0.0f);
-                const float alpha = fminf(kAlphaMax, __fmul_rn(g1.y, fast_exp2(p2)));
-                if (alpha < kAlphaMin) continue;
-                const float Tn = __fmul_rn(T, __fsub_rn(1.0f, alpha));
-                if (Tn < kTMin) {
-                    done = true;
-                    n_eval = b0 - start + j + 1;
-                    break;
-                }
-                const float w = __fmul_rn(alpha, T);
-                cr = __fmaf_rn(g1.z, w, cr);
-                cg = __fmaf_rn(g1.w, w, cg);
-                cb = __fmaf_rn(s_b[j], w, cb);
-                T = Tn;
-                last = b0 - start + j + 1;
-            }
-        }
+// Minimum of Q = a x^2 + b x y + c y^2 (a, c > 0, 4ac > b^2) over the box
+// [x0, x1] x [y0, y1]: 0 if the box holds the origin, else on an edge.
+__device__ __forceinline__ float box_min_quadratic(float a, float b, float c, float ia2, float ic2, float x0, float x1,
+                                                   float y0, float y1) {
+    if (x0 <= 0.0f && x1 >= 0.0f && y0 <= 0.0f && y1 >= 0.0f) return 0.0f;
+    float m = 3.0e38f;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const float X = e ? x1 : x0;
+        const float y = fminf(fmaxf(-b * X * ic2, y0), y1);
+        m = fminf(m, (a * X + b * y) * X + c * y * y);
+        const float Y = e ? y1 : y0;
+        const float x = fminf(fmaxf(-b * Y * ia2, x0), x1);
+        m = fminf(m, (a * x + b * Y) * x + c * Y * Y);
     }
-    if (inside) {
-        const int pix = py * a.W + px;
-        const int plane = a.W * a.H;
-        a.image[pix] = __fmaf_rn(T, a.bg[0], cr);
-        a.image[plane + pix] = __fmaf_rn(T, a.bg[1], cg);
-        a.image[2 * plane + pix] = __fmaf_rn(T, a.bg[2], cb);
-        a.final_T[pix] = T;
-        a.n_contrib[pix] = last;
-        if (a.n_eval) a.n_eval[pix] = n_eval;
+    return m;
+}
+
+// Thread/pixel layout: PPT pixels per thread; warp w owns the 8 x (4 PPT)
+// region (x0 = 8 (w & 1), y0 = 4 PPT (w >> 1)) of the 16x16 tile; lane l
+// holds pixels (x0 + (l & 7), y0 + (l >> 3) + 4k), k < PPT.
+template <int PPT>
+struct Layout {
+    static constexpr int kThreads = kBlock / PPT;
+    static constexpr int kWarps = kThreads / 32;
+    static constexpr int kRegionH = 4 * PPT;
+    static constexpr int kLoads = kBatch / kThreads;  // entries staged per thread
+};
+
+// Bit w set if some pixel of warp region w may get alpha >= 1/255 from s.
+template <int PPT>
+__device__ __forceinline__ uint32_t region_mask(const Splat& s, int tile_x0, int tile_y0) {
+    using Lt = Layout<PPT>;
+    const float k255 = s.kappa * 255.0f;
+    if (!(k255 > 1.0f)) return 0u;
+    const float thr = __log2f(k255) + kCullMargin;  // cull if min(-p2) > thr
+    const float a = -s.A, b = -s.B, c = -s.C;
+    const float ia2 = 0.5f / a, ic2 = 0.5f / c;
+    uint32_t mask = 0;
+#pragma unroll
+    for (int w = 0; w < Lt::kWarps; ++w) {
+        const float rx = (float)(tile_x0 + 8 * (w & 1)), ry = (float)(tile_y0 + Lt::kRegionH * (w >> 1));
+        const float x0 = s.u - (rx + 7.5f), x1 = s.u - (rx + 0.5f);
+        const float y0 = s.v - (ry + (float)Lt::kRegionH - 0.5f), y1 = s.v - (ry + 0.5f);
+        if (box_min_quadratic(a, b, c, ia2, ic2, x0, x1, y0, y1) <= thr) mask |= 1u << w;
+    }
+    return mask;
+}
+
+// Per-warp compaction of the batch entries whose mask has this warp's bit.
+__device__ __forceinline__ int compact_warp_list(const uint8_t* s_mask, int n, int warp, uint16_t* out) {
+    const int lane = threadIdx.x & 31;
+    int cnt = 0;
+#pragma unroll
+    for (int c = 0; c < kBatch / 32; ++c) {
+        const int j = c * 32 + lane;
+        const bool bit = j < n && ((s_mask[j] >> warp) & 1u);
+        const uint32_t ball = __ballot_sync(0xffffffffu, bit);
+        if (bit) out[cnt + __popc(ball & ((1u << lane) - 1u))] = (uint16_t)j;
+        cnt += __popc(ball);
+    }
+    __syncwarp();
+    return cnt;
+}
+
+template <int PPT>
+__device__ __forceinline__ void pixel_base(int tile, int tiles_x, int tid, int& px, int& py0) {
+    const int warp = tid >> 5, lane = tid & 31;
+    px = (tile % tiles_x) * kTile + 8 * (warp & 1) + (lane & 7);
+    py0 = (tile / tiles_x) * kTile + Layout<PPT>::kRegionH * (warp >> 1) + (lane >> 3);
+}
+
+struct StagedBatch {
+    float4* g0;  // u, v, A, B
+    float4* g1;  // C, kappa, r, g
+    float* b;
+    uint32_t* pid;
+    uint8_t* mask;
+};
+
+template <int PPT>
+__device__ __forceinline__ void stage_batch(const float4* pay0, const float4* pay1, const float* pay2,
+                                            const uint32_t* list, uint32_t first, int n, int tile_x0, int tile_y0,
+                                            StagedBatch sb) {
+    using Lt = Layout<PPT>;
+#pragma unroll
+    for (int h = 0; h < Lt::kLoads; ++h) {
+        const int q = threadIdx.x + h * Lt::kThreads;
+        if (q < n) {
+            const uint32_t p = __ldg(list + first + q);
+            const Splat s = load_splat(pay0, pay1, pay2, p);
+            sb.g0[q] = make_float4(s.u, s.v, s.A, s.B);
+            sb.g1[q] = make_float4(s.C, s.kappa, s.r, s.g);
+            sb.b[q] = s.b;
+            if (sb.pid) sb.pid[q] = p;
+            sb.mask[q] = (uint8_t)region_mask<PPT>(s, tile_x0, tile_y0);
+        }
     }
 }
 
+template <int PPT>
+__global__ void __launch_bounds__(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdArgs a) {
+    using Lt = Layout<PPT>;
+    __shared__ float4 s_g0[kBatch];
+    __shared__ float4 s_g1[kBatch];
+    __shared__ float s_b[kBatch];
+    __shared__ uint8_t s_mask[kBatch];
+    __shared__ uint16_t s_list[Lt::kWarps][kBatch];
+    const int tile = blockIdx.x;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    int px, py0;
+    pixel_base<PPT>(tile, a.tiles_x, tid, px, py0);
+    const int tile_x0 = (tile % a.tiles_x) * kTile, tile_y0 = (tile / a.tiles_x) * kTile;
+    const float fpx = (float)px + 0.5f;
+    uint32_t start = a.ranges[tile], end = a.ranges[tile + 1];
+    if (a.counters[GES_CTR_OVERFLOW]) start = end = 0;
+    float T[PPT], cr[PPT], cg[PPT], cb[PPT];
+    uint32_t last[PPT], n_eval[PPT];
+    uint32_t done = 0;  // bit k: pixel k finished (or outside the image)
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        T[k] = 1.0f; cr[k] = cg[k] = cb[k] = 0.0f; last[k] = 0; n_eval[k] = end - start;
+        if (!(px < a.W && py0 + 4 * k < a.H)) done |= 1u << k;
+    }
+    constexpr uint32_t kAll = (1u << PPT) - 1u;
+    StagedBatch sb{s_g0, s_g1, s_b, nullptr, s_mask};
+    for (uint32_t b0 = start; b0 < end; b0 += kBatch) {
+        if (__syncthreads_count(done == kAll) == Lt::kThreads) break;
+        const int n = (int)min((uint32_t)kBatch, end - b0);
+        stage_batch<PPT>(a.pay0, a.pay1, a.pay2, a.list, b0, n, tile_x0, tile_y0, sb);
+        __syncthreads();
+        const int nw = compact_warp_list(s_mask, n, warp, s_list[warp]);
+        for (int i = 0; i < nw; ++i) {
+            if (__all_sync(0xffffffffu, done == kAll)) break;
+            const int j = s_list[warp][i];
+            if (done == kAll) continue;
+            const float4 g0 = s_g0[j];
+            const float4 g1 = s_g1[j];
+            const float dx = __fsub_rn(g0.x, fpx);
+            const uint32_t pos = b0 - start + j;
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                if (done & (1u << k)) continue;
+                const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
+                const float p2 = fminf(raw_exponent(g0.z, g0.w, g1.x, dx, dy), 0.0f);
+                const float alpha = fminf(kAlphaMax, __fmul_rn(g1.y, fast_exp2(p2)));
+                if (alpha < kAlphaMin) continue;
+                const float Tn = __fmul_rn(T[k], __fsub_rn(1.0f, alpha));
+                if (Tn < kTMin) {
+                    done |= 1u << k;
+                    n_eval[k] = pos + 1;
+                    continue;
+                }
+                const float w = __fmul_rn(alpha, T[k]);
+                cr[k] = __fmaf_rn(g1.z, w, cr[k]);
+                cg[k] = __fmaf_rn(g1.w, w, cg[k]);
+                cb[k] = __fmaf_rn(s_b[j], w, cb[k]);
+                T[k] = Tn;
+                last[k] = pos + 1;
+            }
+        }
+    }
+    const int plane = a.W * a.H;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        const int py = py0 + 4 * k;
+        if (px < a.W && py < a.H) {
+            const int pix = py * a.W + px;
+            a.image[pix] = __fmaf_rn(T[k], a.bg[0], cr[k]);
+            a.image[plane + pix] = __fmaf_rn(T[k], a.bg[1], cg[k]);
+            a.image[2 * plane + pix] = __fmaf_rn(T[k], a.bg[2], cb[k]);
+            a.final_T[pix] = T[k];
+            a.n_contrib[pix] = last[k];
+            if (a.n_eval) a.n_eval[pix] = n_eval[k];
+        }
+    }
+}
+
+constexpr int kPPT = 2;
+
 cudaError_t launch_render_fwd(const RenderFwdArgs& a, cudaStream_t stream) {
-    render_fwd_kernel<<<a.tiles_x * a.tiles_y, kBlock, 0, stream>>>(a);
+    render_fwd_kernel<kPPT><<<a.tiles_x * a.tiles_y, Layout<kPPT>::kThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
 // S5a backward
 // ---------------------------------------------------------------------------
-// Recursive-halving warp reduction of 9 (padded to 16) values.  On return
-// lane L holds the warp sum of component (L >> 1) (valid for L>>1 < 9, even L).
-__device__ __forceinline__ float warp_reduce9(float v[16]) {
+// Warp reduction of 9 (padded to 16) values by recursive halving: two
+// halving steps leave 4 components per lane (partially summed), three xor
+// steps finish them.  Lanes 0, 8 and 16 then hold components 0-3, 4-7 and
+// 8-11 (24 shuffles instead of 45 for nine full butterflies).
+__device__ __forceinline__ float4 warp_reduce_to_v4(float v[16]) {
     const int lane = threadIdx.x & 31;
 #pragma unroll
-    for (int step = 0; step < 4; ++step) {
-        const int o = 16 >> step;      // 16, 8, 4, 2
-        const int half = 8 >> step;    // 8, 4, 2, 1
+    for (int step = 0; step < 2; ++step) {
+        const int o = 16 >> step;      // 16, 8
+        const int half = 8 >> step;    // 8, 4
         const bool upper = (lane & o) != 0;
 #pragma unroll
         for (int i = 0; i < half; ++i) {
@@ -126,122 +261,124 @@ __device__ __forceinline__ float warp_reduce9(float v[16]) {
             v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
         }
     }
-    return v[0] + __shfl_xor_sync(0xffffffffu, v[0], 1);
+#pragma unroll
+    for (int o = 4; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
+    return make_float4(v[0], v[1], v[2], v[3]);
 }
 
-__global__ void __launch_bounds__(kBlock) render_bwd_kernel(RenderBwdArgs a) {
-    __shared__ float4 s_g0[kBlock];
-    __shared__ float4 s_g1[kBlock];
-    __shared__ float s_b[kBlock];
-    __shared__ uint32_t s_pid[kBlock];
-    __shared__ float s_acc[9][kBlock];
+__device__ __forceinline__ void red_add_v4(float* addr, float4 x) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(x.x), "f"(x.y), "f"(x.z),
+                 "f"(x.w)
+                 : "memory");
+}
+
+template <int PPT>
+__global__ void __launch_bounds__(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdArgs a) {
+    using Lt = Layout<PPT>;
+    __shared__ float4 s_g0[kBatch];
+    __shared__ float4 s_g1[kBatch];
+    __shared__ float s_b[kBatch];
+    __shared__ uint32_t s_pid[kBatch];
+    __shared__ uint8_t s_mask[kBatch];
+    __shared__ uint16_t s_list[Lt::kWarps][kBatch];
     __shared__ uint32_t s_max;
     const int tile = blockIdx.x;
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
-    const int px = tx * kTile + (tid & (kTile - 1)), py = ty * kTile + (tid >> 4);
-    const bool inside = px < a.W && py < a.H;
-    const float fpx = (float)px + 0.5f, fpy = (float)py + 0.5f;
-    uint32_t start = a.ranges[tile], end = a.ranges[tile + 1];
-    if (a.counters[GES_CTR_OVERFLOW]) start = end = 0;
-    const int pix = py * a.W + px;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    int px, py0;
+    pixel_base<PPT>(tile, a.tiles_x, tid, px, py0);
+    const int tile_x0 = (tile % a.tiles_x) * kTile, tile_y0 = (tile / a.tiles_x) * kTile;
+    const float fpx = (float)px + 0.5f;
+    const bool ovf = a.counters[GES_CTR_OVERFLOW] != 0;
+    const uint32_t start = ovf ? 0u : a.ranges[tile];
     const int plane = a.W * a.H;
-    float T = 1.0f, gr = 0.0f, gg = 0.0f, gb = 0.0f, Tfin = 1.0f;
-    uint32_t last = 0;
-    if (inside) {
-        Tfin = a.final_T[pix];
-        T = Tfin;
-        last = a.n_contrib[pix];
-        gr = a.dL_dimage[pix];
-        gg = a.dL_dimage[plane + pix];
-        gb = a.dL_dimage[2 * plane + pix];
+    float T[PPT], gr[PPT], gg[PPT], gb[PPT], bg_term[PPT], suffix[PPT];
+    uint32_t last[PPT];
+    uint32_t my_max = 0;
+#pragma unroll
+    for (int k = 0; k < PPT; ++k) {
+        const int py = py0 + 4 * k;
+        T[k] = 1.0f; gr[k] = gg[k] = gb[k] = 0.0f; last[k] = 0; suffix[k] = 0.0f;
+        float Tfin = 1.0f;
+        if (px < a.W && py < a.H && !ovf) {
+            const int pix = py * a.W + px;
+            Tfin = a.final_T[pix];
+            last[k] = a.n_contrib[pix];
+            gr[k] = a.dL_dimage[pix];
+            gg[k] = a.dL_dimage[plane + pix];
+            gb[k] = a.dL_dimage[2 * plane + pix];
+        }
+        T[k] = Tfin;
+        bg_term[k] = Tfin * (gr[k] * a.bg[0] + gg[k] * a.bg[1] + gb[k] * a.bg[2]);
+        my_max = max(my_max, last[k]);
     }
     if (tid == 0) s_max = 0;
-    for (int c = 0; c < 9; ++c) s_acc[c][tid] = 0.0f;
     __syncthreads();
-    if (last) atomicMax(&s_max, last);
+    if (my_max) atomicMax(&s_max, my_max);
     __syncthreads();
     const uint32_t max_last = s_max;
-    const float gbg = gr * a.bg[0] + gg * a.bg[1] + gb * a.bg[2];
-    const float bg_term = Tfin * gbg;
-    float suffix = 0.0f;  // sum_{j > k} (rgb_j . g) alpha_j T_j
-    for (int32_t b_end = (int32_t)max_last; b_end > 0; b_end -= kBlock) {
-        const int32_t b_begin = max(0, b_end - kBlock);
+    StagedBatch sb{s_g0, s_g1, s_b, s_pid, s_mask};
+    for (int32_t b_end = (int32_t)max_last; b_end > 0; b_end -= kBatch) {
+        const int32_t b_begin = max(0, b_end - kBatch);
         const int n = b_end - b_begin;
-        if (tid < n) {
-            const uint32_t p = __ldg(a.list + start + b_begin + tid);
-            const Splat2D s = load_splat(a.pay0, a.pay1, a.pay2, p);
-            s_g0[tid] = make_float4(s.u, s.v, s.A, s.B);
-            s_g1[tid] = make_float4(s.C, s.kappa, s.r, s.g);
-            s_b[tid] = s.b;
-            s_pid[tid] = p;
-        }
+        __syncthreads();  // previous batch fully consumed
+        stage_batch<PPT>(a.pay0, a.pay1, a.pay2, a.list, start + b_begin, n, tile_x0, tile_y0, sb);
         __syncthreads();
-        for (int j = n - 1; j >= 0; --j) {
+        const int nw = compact_warp_list(s_mask, n, warp, s_list[warp]);
+        for (int i = nw - 1; i >= 0; --i) {
+            const int j = s_list[warp][i];
             const uint32_t pos = (uint32_t)(b_begin + j);
             float v[16];
 #pragma unroll
             for (int c = 0; c < 16; ++c) v[c] = 0.0f;
             bool contrib = false;
-            if (pos < last) {
-                const float4 g0 = s_g0[j];
-                const float4 g1 = s_g1[j];
-                Splat2D s;
-                s.u = g0.x; s.v = g0.y; s.A = g0.z; s.B = g0.w; s.C = g1.x;
-                const float dx = __fsub_rn(s.u, fpx), dy = __fsub_rn(s.v, fpy);
-                const float p2raw = raw_exponent(s, dx, dy);
-                const float p2 = fminf(p2raw, 0.0f);
-                const float G = fast_exp2(p2);
+            const float4 g0 = s_g0[j];
+            const float4 g1 = s_g1[j];
+            const float rb = s_b[j];
+            const float dx = __fsub_rn(g0.x, fpx);
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                if (pos >= last[k]) continue;
+                const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
+                const float p2raw = raw_exponent(g0.z, g0.w, g1.x, dx, dy);
+                const float G = fast_exp2(fminf(p2raw, 0.0f));
                 const float araw = __fmul_rn(g1.y, G);
                 const float alpha = fminf(kAlphaMax, araw);
-                if (alpha >= kAlphaMin) {
-                    contrib = true;
-                    const float om = __fsub_rn(1.0f, alpha);
-                    const float inv_om = 1.0f / om;
-                    const float Tk = T * inv_om;  // transmittance before entry k
-                    const float rb = s_b[j];
-                    const float cgk = g1.z * gr + g1.w * gg + rb * gb;
-                    const float dalpha = Tk * cgk - (suffix + bg_term) * inv_om;
-                    suffix += cgk * alpha * Tk;
-                    const float w = alpha * Tk;
-                    v[6] = w * gr;
-                    v[7] = w * gg;
-                    v[8] = w * gb;
-                    if (araw < kAlphaMax) {
-                        v[5] = G * dalpha;
-                        // dL/dp2 with G = 2^p2: alpha = kappa 2^p2 -> d alpha / d p2 = alpha ln 2
-                        const float dp2 = (p2raw <= 0.0f) ? araw * dalpha * 0.69314718055994531f : 0.0f;
-                        v[0] = dp2 * (2.0f * s.A * dx + s.B * dy);   // d p2 / d u
-                        v[1] = dp2 * (s.B * dx + 2.0f * s.C * dy);   // d p2 / d v
-                        v[2] = dp2 * dx * dx;                        // d p2 / d A
-                        v[3] = dp2 * dx * dy;                        // d p2 / d B
-                        v[4] = dp2 * dy * dy;                        // d p2 / d C
-                    }
-                    T = Tk;
+                if (alpha < kAlphaMin) continue;
+                contrib = true;
+                const float inv_om = __fdividef(1.0f, __fsub_rn(1.0f, alpha));
+                const float Tk = T[k] * inv_om;  // transmittance before entry k
+                const float cgk = g1.z * gr[k] + g1.w * gg[k] + rb * gb[k];
+                const float dalpha = Tk * cgk - (suffix[k] + bg_term[k]) * inv_om;
+                const float w = alpha * Tk;
+                suffix[k] += cgk * w;
+                v[6] += w * gr[k];
+                v[7] += w * gg[k];
+                v[8] += w * gb[k];
+                if (araw < kAlphaMax) {
+                    v[5] += G * dalpha;
+                    // alpha = kappa 2^p2  ->  d alpha / d p2 = alpha ln 2
+                    const float dp2 = (p2raw <= 0.0f) ? araw * dalpha * 0.69314718055994531f : 0.0f;
+                    const float e = dp2 * dx, f = dp2 * dy;
+                    v[0] += 2.0f * g0.z * e + g0.w * f;   // d p2 / d u
+                    v[1] += g0.w * e + 2.0f * g1.x * f;   // d p2 / d v
+                    v[2] += e * dx;                       // d p2 / d A
+                    v[3] += e * dy;                       // d p2 / d B
+                    v[4] += f * dy;                       // d p2 / d C
                 }
+                T[k] = Tk;
             }
             if (__any_sync(0xffffffffu, contrib)) {
-                const float r = warp_reduce9(v);
-                const int c = lane >> 1;
-                if (!(lane & 1) && c < 9) atomicAdd(&s_acc[c][j], r);
+                const float4 r = warp_reduce_to_v4(v);
+                if ((lane & 7) == 0 && lane < 24) red_add_v4(a.grad2d + (size_t)s_pid[j] * kGrad2dStride + lane / 2, r);
             }
         }
-        __syncthreads();
-        if (tid < n) {
-            const uint32_t p = s_pid[tid];
-#pragma unroll
-            for (int c = 0; c < 9; ++c) {
-                const float x = s_acc[c][tid];
-                if (x != 0.0f) atomicAdd(a.grad2d + (size_t)c * a.P + p, x);
-                s_acc[c][tid] = 0.0f;
-            }
-        }
-        __syncthreads();
     }
 }
 
 cudaError_t launch_render_bwd(const RenderBwdArgs& a, cudaStream_t stream) {
-    render_bwd_kernel<<<a.tiles_x * a.tiles_y, kBlock, 0, stream>>>(a);
+    render_bwd_kernel<kPPT><<<a.tiles_x * a.tiles_y, Layout<kPPT>::kThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

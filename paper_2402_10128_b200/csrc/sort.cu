@@ -1,20 +1,28 @@
 // sort.cu -- S2/S3: per-tile ranges, depth radix sort of
-// the visible particles, (tile, particle) duplication in depth order, and the
-// stable radix sort of the pairs by tile id.
+// the visible particles, and the stable radix sort of the (tile, particle)
+// pairs by tile id, with the pair duplication fused into the first pass.
 //
 // Design: instead of a 64-bit LSD sort of
-// (tile_id << 32 | depth) keys (6 x 8-bit passes over M pairs), the depth order
-// is established once on the V visible particles (4 passes over V << M), the
-// pairs are emitted in that order, and a STABLE sort on the tile id alone (2
-// passes over M for <= 65536 tiles) yields exactly the (tile, depth, index)
-// order of the 64-bit keys.  The per-tile pair counts -- hence the ranges and
-// the tile-digit histograms -- come from a 2-D difference grid of the rects
-// built in S1, so no pass over the pairs is spent on counting.
-//
-// Every pass is a single-pass "onesweep" LSD step: 4096 keys per CTA,
-// warp-level multisplit ranking with __match_any_sync, decoupled look-back
-// across CTAs per digit, reordering through shared memory for coalesced
-// scatter.  Hand-written; no CUB.
+// (tile_id << 32 | depth) keys (6 x 8-bit passes over the M pairs), the depth
+// order is established once on the V visible particles (4 onesweep passes
+// over V << M; pass 0 also compacts the visible set), then the pairs are
+// generated in that order and sorted STABLY by tile id alone (2 passes for
+// <= 65536 tiles): every tile's list comes out in (depth bits, particle index)
+// order -- exactly the order of the 64-bit keys.
+//   item scan    exclusive prefix E[s] of the pair counts of the sorted
+//                particles (decoupled look-back) and, per 4096-slot tile, the
+//                particle holding its first slot;
+//   pass 1       each CTA owns 4096 consecutive pair SLOTS (balanced however
+//                unequal the particles' footprints are), stages the particles
+//                covering them in shared memory, expands its slots by a
+//                load-balanced search, and ranks/scatters them by the low tile
+//                digit -- the unsorted pair array is never written;
+//   pass 2       the high tile digit, writing only the particle ids = lists.
+// The per-tile counts (ranges, digit histograms) come from the 2-D difference
+// grid of S1, so no pass over the pairs is spent on counting.
+// Every pass: 4096 keys per CTA, warp multisplit ranking (__match_any_sync),
+// per-digit decoupled look-back with 4 predecessors in flight, shared-memory
+// reorder for coalesced scatter.  Hand-written; no CUB.
 #include <algorithm>
 
 #include "ges_internal.h"
@@ -153,227 +161,370 @@ cudaError_t launch_ranges(const RangesArgs& a, cudaStream_t stream) {
 }
 
 // ---------------------------------------------------------------------------
-// One onesweep LSD pass: 8-bit digit at `shift`, 256 threads x 16 keys.
+// Item scan: E[s] = sum_{s' < s} tiles(sorted_vis[s']), tile_first[j] = item
+// holding pair slot j * 4096.
+// ---------------------------------------------------------------------------
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+constexpr int kSlotTile = 4096;  // == radix tile
+
+int64_t item_scan_tiles(int64_t n) { return (n + kScanTile - 1) / kScanTile; }
+int64_t slot_tiles(int64_t cap) { return (cap + kSlotTile - 1) / kSlotTile + 2; }
+
+__device__ __forceinline__ uint32_t rect_count(ushort4 r) { return (uint32_t)(r.z - r.x) * (uint32_t)(r.w - r.y); }
+
+__global__ void __launch_bounds__(kScanThreads) item_scan_kernel(ItemScanArgs a) {
+    __shared__ uint32_t s_warp[kScanThreads / 32 + 1];
+    __shared__ uint32_t s_tile, s_prefix;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t V = (int64_t)a.counters[GES_CTR_VISIBLE];
+    if (tid == 0) s_tile = (uint32_t)atomicAdd(a.tile_counter, 1ull);
+    __syncthreads();
+    const int64_t tile = s_tile;
+    if (tile * kScanTile >= V) return;  // tickets are ordered: nobody waits on this one
+    const int64_t first = tile * kScanTile + (int64_t)tid * kScanItems;
+    uint32_t c[kScanItems], ids[kScanItems];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) ids[j] = (first + j < V) ? __ldg(a.sorted_vis + first + j) : 0u;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) c[j] = (first + j < V) ? rect_count(__ldg(a.rect + ids[j])) : 0u;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) sum += c[j];
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += nn;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t wv = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
+        uint32_t wi = wv;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t nn = __shfl_up_sync(0xffffffffu, wi, o);
+            if (lane >= o) wi += nn;
+        }
+        if (lane < kScanThreads / 32) s_warp[lane] = wi - wv;
+        const uint32_t total = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
+        const uint32_t prefix = lookback_warp(a.lookback, (uint32_t)tile, total);
+        if (lane == 0) s_prefix = prefix;
+    }
+    __syncthreads();
+    uint32_t e = s_prefix + s_warp[warp] + incl - sum;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        if (first + j < V) {
+            a.E[first + j] = e;
+            // slot tiles whose first slot lies in [e, e + c)
+            for (uint32_t st = (e + kSlotTile - 1) / kSlotTile; st * (uint64_t)kSlotTile < (uint64_t)e + c[j]; ++st)
+                a.tile_first[st] = (uint32_t)(first + j);
+        }
+        e += c[j];
+    }
+}
+
+cudaError_t launch_item_scan(const ItemScanArgs& a, int64_t max_items, cudaStream_t stream) {
+    const int64_t grid = std::max<int64_t>(1, item_scan_tiles(max_items));
+    item_scan_kernel<<<(unsigned)grid, kScanThreads, 0, stream>>>(a);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// LSD radix passes, reduce-then-scan (no inter-CTA waiting):
+//   radix_hist_kernel     per 4096-key tile: 8-bit digit histogram -> H[tile][256]
+//   radix_scan_kernel     per digit: exclusive scan of H[.][d] over the tiles,
+//                         column total -> T[d]
+//   radix_scatter_kernel  per tile: stable warp-multisplit ranking, shared-memory
+//                         reorder, scatter to off(d) + H[tile][d] + local rank
+// GEN = true: a tile's keys (tile ids) and values (particle ids) are generated
+// from the depth-sorted particles (load-balanced search over pair slots).
 // ---------------------------------------------------------------------------
 constexpr int kRadixThreads = 256;
 constexpr int kRadixItems = 16;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096
 constexpr int kRadixWarps = kRadixThreads / 32;
+constexpr uint32_t kInvalidKey = 0xffffffffu;
+static_assert(kRadixTile == kSlotTile, "slot tiles are radix tiles");
 
 int64_t radix_tiles(int64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
 
-__global__ void __launch_bounds__(kRadixThreads) radix_pass_kernel(RadixPassArgs a) {
+struct GenSmem {
+    uint32_t E[kRadixTile + 1];
+    uint32_t pid[kRadixTile + 1];
+    ushort4 rect[kRadixTile + 1];
+};
+
+__device__ __forceinline__ int64_t pass_count(const RadixPassArgs& a) {
+    return a.count ? min((int64_t)*a.count, a.max_items) : a.max_items;
+}
+
+// Loads (or generates) the tile's keys/values in warp-striped order: item j of
+// lane l of warp w is element w*512 + j*32 + l of the tile.  valid[j] marks
+// items that take part (inside n and, when dropping, not the invalid marker).
+template <bool GEN>
+__device__ __forceinline__ void load_tile(const RadixPassArgs& a, int64_t tile, int64_t n, uint32_t (&k)[kRadixItems],
+                                          uint32_t (&v)[kRadixItems], uint32_t& valid, uint32_t* s_keys,
+                                          uint32_t* s_vals, unsigned char* s_dyn, bool need_vals) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t base = tile * kRadixTile + warp * (kRadixItems * 32);
+    valid = 0;
+    if constexpr (GEN) {
+        GenSmem& g = *reinterpret_cast<GenSmem*>(s_dyn);
+        const int64_t slot0 = tile * kRadixTile;
+        const int nslots = (int)min((int64_t)kRadixTile, n - slot0);
+        const int64_t V = (int64_t)a.counters[GES_CTR_VISIBLE];
+        const int64_t f = a.tile_first[tile];
+        const int64_t last_item = (slot0 + kRadixTile < n) ? (int64_t)a.tile_first[tile + 1] : V - 1;
+        const int nit = (int)(last_item - f + 1);
+        for (int q = tid; q < nit; q += kRadixThreads) {
+            const uint32_t p = a.sorted_vis[f + q];
+            g.E[q] = a.E[f + q];
+            g.pid[q] = p;
+            g.rect[q] = a.rect[p];
+        }
+        __syncthreads();
+        // thread-contiguous slots, then an exchange to the warp-striped order
+        const int ls0 = tid * kRadixItems;
+        int it = 0;
+        if (ls0 < nslots) {
+            const uint32_t s0 = (uint32_t)(slot0 + ls0);
+            int lo = 0, hi = nit - 1;  // last item with E <= s0
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (g.E[mid] <= s0) lo = mid; else hi = mid - 1;
+            }
+            it = lo;
+        }
+        ushort4 r = g.rect[it];
+        uint32_t E0 = g.E[it], pid = g.pid[it], E1 = (it + 1 < nit) ? g.E[it + 1] : 0xffffffffu;
+        uint32_t w = r.z - r.x;
+        float inv_w = __frcp_rn((float)w);
+#pragma unroll
+        for (int j = 0; j < kRadixItems; ++j) {
+            const int ls = ls0 + j;
+            const uint32_t s = (uint32_t)(slot0 + ls);
+            if (ls < nslots) {
+                while (s >= E1) {
+                    ++it;
+                    r = g.rect[it];
+                    E0 = E1;
+                    pid = g.pid[it];
+                    E1 = (it + 1 < nit) ? g.E[it + 1] : 0xffffffffu;
+                    w = r.z - r.x;
+                    inv_w = __frcp_rn((float)w);
+                }
+                const uint32_t li = s - E0;
+                const uint32_t yy = __float2uint_rz(((float)li + 0.5f) * inv_w);
+                s_keys[ls] = (r.y + yy) * (uint32_t)a.tiles_x + r.x + (li - yy * w);
+                s_vals[ls] = pid;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kRadixItems; ++j) {
+            const int ls = warp * (kRadixItems * 32) + j * 32 + lane;
+            if (ls < nslots) {
+                k[j] = s_keys[ls];
+                v[j] = s_vals[ls];
+                valid |= 1u << j;
+            }
+        }
+        __syncthreads();
+    } else {
+#pragma unroll
+        for (int j = 0; j < kRadixItems; ++j) {
+            const int64_t idx = base + j * 32 + lane;
+            k[j] = kInvalidKey;
+            if (idx < n) {
+                k[j] = a.keys_in[idx];
+                if (need_vals) v[j] = a.vals_in ? a.vals_in[idx] : (uint32_t)idx;
+                if (!(a.drop_invalid && k[j] == kInvalidKey)) valid |= 1u << j;
+            }
+        }
+    }
+}
+
+template <bool GEN>
+__global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(RadixPassArgs a) {
+    __shared__ uint32_t s_keys[GEN ? kRadixTile : 1];
+    __shared__ uint32_t s_vals[GEN ? kRadixTile : 1];
+    __shared__ uint32_t s_hist[kRadixDigits];
+    extern __shared__ __align__(16) unsigned char s_dyn[];
+    if (a.overflow && *a.overflow) return;
+    const int64_t n = pass_count(a);
+    const int64_t tile = blockIdx.x;
+    if (tile * kRadixTile >= n) return;
+    s_hist[threadIdx.x] = 0;
+    uint32_t k[kRadixItems], v[kRadixItems], valid;
+    load_tile<GEN>(a, tile, n, k, v, valid, s_keys, s_vals, s_dyn, false);
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kRadixItems; ++j)
+        if (valid & (1u << j)) atomicAdd(&s_hist[(k[j] >> a.shift) & 255u], 1u);
+    __syncthreads();
+    a.tile_hist[(int64_t)threadIdx.x * a.hist_stride + tile] = s_hist[threadIdx.x];
+}
+
+// One CTA per digit: exclusive scan of H[.][d] over the tiles (in place).
+__global__ void __launch_bounds__(256) radix_scan_kernel(RadixPassArgs a) {
+    __shared__ uint32_t s_warp[9];
+    const int d = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (a.overflow && *a.overflow) return;
+    const int64_t n = pass_count(a);
+    const int nt = (int)((n + kRadixTile - 1) / kRadixTile);
+    const int per = (nt + 255) / 256;
+    const int t0 = min(nt, tid * per), t1 = min(nt, t0 + per);
+    uint32_t* col = a.tile_hist + (int64_t)d * a.hist_stride;  // digit-major: contiguous over tiles
+    uint32_t sum = 0;
+    for (int t = t0; t < t1; ++t) sum += col[t];
+    uint32_t incl = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += nn;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    if (tid == 0) {
+        uint32_t r = 0;
+        for (int w = 0; w < 8; ++w) { const uint32_t c = s_warp[w]; s_warp[w] = r; r += c; }
+        s_warp[8] = r;
+    }
+    __syncthreads();
+    uint32_t run = s_warp[warp] + incl - sum;
+    for (int t = t0; t < t1; ++t) {
+        const uint32_t c = col[t];
+        col[t] = run;
+        run += c;
+    }
+    if (tid == 0) a.digit_total[d] = s_warp[8];
+}
+
+template <bool GEN>
+__global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(RadixPassArgs a) {
     __shared__ uint32_t s_keys[kRadixTile];
     __shared__ uint32_t s_vals[kRadixTile];
     __shared__ uint32_t s_whist[kRadixWarps][kRadixDigits];
     __shared__ uint32_t s_local[kRadixDigits];
     __shared__ uint32_t s_global[kRadixDigits];
     __shared__ uint32_t s_warp[kRadixWarps + 1];
-    __shared__ uint32_t s_tile;
+    extern __shared__ __align__(16) unsigned char s_dyn[];
     if (a.overflow && *a.overflow) return;
-    const int64_t n = min((int64_t)*a.count, a.max_items);
-    const int64_t num_tiles = (n + kRadixTile - 1) / kRadixTile;
+    const int64_t n = pass_count(a);
+    const int64_t tile = blockIdx.x;
+    if (tile * kRadixTile >= n) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
-    while (true) {
-        if (tid == 0) s_tile = (uint32_t)atomicAdd(a.tile_counter, 1ull);
-        for (int d = tid; d < kRadixWarps * kRadixDigits; d += kRadixThreads) (&s_whist[0][0])[d] = 0;
-        __syncthreads();
-        const int64_t tile = s_tile;
-        if (tile >= num_tiles) break;
-        const int64_t base = tile * kRadixTile + warp * (kRadixItems * 32);
-        uint32_t k[kRadixItems], v[kRadixItems], rank[kRadixItems];
+    for (int d = tid; d < kRadixWarps * kRadixDigits; d += kRadixThreads) (&s_whist[0][0])[d] = 0;
+    // global digit offsets: exclusive scan of the column totals + this tile's prefix
+    {
+        const uint32_t tot = a.digit_total[tid];
+        uint32_t incl = tot;
 #pragma unroll
-        for (int j = 0; j < kRadixItems; ++j) {
-            const int64_t idx = base + j * 32 + lane;
-            if (idx < n) { k[j] = a.keys_in[idx]; v[j] = a.vals_in[idx]; }
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += nn;
         }
-        // warp multisplit ranking, items in (j, lane) = index order
-#pragma unroll
-        for (int j = 0; j < kRadixItems; ++j) {
-            const int64_t idx = base + j * 32 + lane;
-            const bool valid = idx < n;
-            const uint32_t d = valid ? ((k[j] >> a.shift) & 255u) : 256u;
-            const uint32_t peers = __match_any_sync(0xffffffffu, d);
-            uint32_t cnt = 0;
-            if (valid) cnt = s_whist[warp][d];
-            __syncwarp();
-            rank[j] = cnt + __popc(peers & lt_mask);
-            if (valid && lane == __ffs(peers) - 1) s_whist[warp][d] = cnt + __popc(peers);
-            __syncwarp();
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t r = 0;
+            for (int w = 0; w < kRadixWarps; ++w) { const uint32_t c = s_warp[w]; s_warp[w] = r; r += c; }
         }
         __syncthreads();
-        // per digit (thread = digit): exclusive over warps, block total
-        uint32_t tot = 0;
-        {
-            const int d = tid;
+        s_global[tid] = s_warp[warp] + incl - tot + a.tile_hist[(int64_t)tid * a.hist_stride + tile];
+        __syncthreads();
+    }
+    uint32_t k[kRadixItems], v[kRadixItems], rank[kRadixItems], valid;
+    load_tile<GEN>(a, tile, n, k, v, valid, s_keys, s_vals, s_dyn, true);
+    // warp multisplit ranking, items in (j, lane) = index order
 #pragma unroll
-            for (int w = 0; w < kRadixWarps; ++w) {
-                const uint32_t c = s_whist[w][d];
-                s_whist[w][d] = tot;
-                tot += c;
-            }
-            // publish + look back (serial per digit)
-            uint32_t* st = a.lookback + tile * kRadixDigits;
-            uint32_t excl = 0;
-            if (tile == 0) {
-                st_volatile(&st[d], kFlagPrefix | tot);
-            } else {
-                st_volatile(&st[d], kFlagAgg | tot);
-                int64_t p = tile - 1;
-                while (true) {
-                    const uint32_t w = ld_volatile(a.lookback + p * kRadixDigits + d);
-                    if (w == 0) continue;
-                    excl += w & kValueMask;
-                    if (w & kFlagPrefix) break;
-                    --p;
-                }
-                st_volatile(&st[d], kFlagPrefix | (excl + tot));
-            }
-            s_global[d] = a.digit_offset[d] + excl;
+    for (int j = 0; j < kRadixItems; ++j) {
+        const bool ok = (valid >> j) & 1u;
+        const uint32_t d = ok ? ((k[j] >> a.shift) & 255u) : 256u;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        uint32_t cnt = 0;
+        if (ok) cnt = s_whist[warp][d];
+        __syncwarp();
+        rank[j] = cnt + __popc(peers & lt_mask);
+        if (ok && lane == 31 - __clz(peers)) s_whist[warp][d] = cnt + __popc(peers);
+        __syncwarp();
+    }
+    __syncthreads();
+    // per digit: exclusive over warps, block total; block-local exclusive scan
+    uint32_t tot = 0;
+#pragma unroll
+    for (int w = 0; w < kRadixWarps; ++w) {
+        const uint32_t c = s_whist[w][tid];
+        s_whist[w][tid] = tot;
+        tot += c;
+    }
+    {
+        uint32_t incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += nn;
         }
-        // block-local exclusive scan of the digit totals (for the smem reorder)
-        {
-            uint32_t incl = tot;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += nn;
-            }
-            if (lane == 31) s_warp[warp] = incl;
-            __syncthreads();
-            if (tid == 0) {
-                uint32_t r = 0;
-                for (int w = 0; w < kRadixWarps; ++w) { const uint32_t c = s_warp[w]; s_warp[w] = r; r += c; }
-            }
-            __syncthreads();
-            s_local[tid] = s_warp[warp] + incl - tot;
+        if (lane == 31) s_warp[warp] = incl;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t r = 0;
+            for (int w = 0; w < kRadixWarps; ++w) { const uint32_t c = s_warp[w]; s_warp[w] = r; r += c; }
+            s_warp[kRadixWarps] = r;
         }
         __syncthreads();
+        s_local[tid] = s_warp[warp] + incl - tot;
+    }
+    __syncthreads();
 #pragma unroll
-        for (int j = 0; j < kRadixItems; ++j) {
-            const int64_t idx = base + j * 32 + lane;
-            if (idx < n) {
-                const uint32_t d = (k[j] >> a.shift) & 255u;
-                const uint32_t pos = s_local[d] + s_whist[warp][d] + rank[j];
-                s_keys[pos] = k[j];
-                s_vals[pos] = v[j];
-            }
+    for (int j = 0; j < kRadixItems; ++j) {
+        if ((valid >> j) & 1u) {
+            const uint32_t dd = (k[j] >> a.shift) & 255u;
+            const uint32_t pos = s_local[dd] + s_whist[warp][dd] + rank[j];
+            s_keys[pos] = k[j];
+            s_vals[pos] = v[j];
         }
-        __syncthreads();
-        const int nvalid = (int)min((int64_t)kRadixTile, n - tile * kRadixTile);
-        for (int s = tid; s < nvalid; s += kRadixThreads) {
-            const uint32_t key = s_keys[s];
-            const uint32_t d = (key >> a.shift) & 255u;
-            const uint32_t out = s_global[d] + (uint32_t)s - s_local[d];
-            if (a.keys_out) a.keys_out[out] = key;
-            a.vals_out[out] = s_vals[s];
-        }
-        __syncthreads();
+    }
+    __syncthreads();
+    const int nvalid = (int)s_warp[kRadixWarps];
+    for (int s = tid; s < nvalid; s += kRadixThreads) {
+        const uint32_t key = s_keys[s];
+        const uint32_t dd = (key >> a.shift) & 255u;
+        const uint32_t out = s_global[dd] + (uint32_t)s - s_local[dd];
+        if (a.keys_out) a.keys_out[out] = key;
+        a.vals_out[out] = s_vals[s];
     }
 }
 
 cudaError_t launch_radix_pass(const RadixPassArgs& a, cudaStream_t stream) {
-    const int sms = num_sms();
-    const int64_t tiles = radix_tiles(a.max_items);
-    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sms * 4));
-    radix_pass_kernel<<<(unsigned)grid, kRadixThreads, 0, stream>>>(a);
-    return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// S2 duplication: visible particles in depth order -> (tile, particle) pairs
-// ---------------------------------------------------------------------------
-constexpr int kDupThreads = 256;
-constexpr int kDupItems = 4;
-constexpr int kDupTile = kDupThreads * kDupItems;
-
-int64_t duplicate_tiles(int64_t P) { return (P + kDupTile - 1) / kDupTile; }
-
-__global__ void __launch_bounds__(kDupThreads) duplicate_kernel(DuplicateArgs a) {
-    __shared__ uint32_t s_start[kDupTile + 1];  // inclusive-prefix form: item q covers [s_start[q], s_start[q+1])
-    __shared__ uint32_t s_pid[kDupTile];
-    __shared__ ushort4 s_rect[kDupTile];
-    __shared__ uint32_t s_warp[kDupItems][kDupThreads / 32];
-    __shared__ uint32_t s_tile, s_base, s_total;
-    if (a.counters[GES_CTR_OVERFLOW]) return;
-    const int64_t V = (int64_t)a.counters[GES_CTR_VISIBLE];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = (uint32_t)atomicAdd(a.tile_counter, 1ull);
-    __syncthreads();
-    const int64_t tile = s_tile;
-    if (tile * kDupTile >= V) return;  // tiles are claimed in order: nobody waits on this one
-    // items in order q = j * 256 + tid (coalesced loads, index order j-major)
-    uint32_t cnt[kDupItems];
-#pragma unroll
-    for (int j = 0; j < kDupItems; ++j) {
-        const int q = j * kDupThreads + tid;
-        const int64_t s = tile * kDupTile + q;
-        cnt[j] = 0;
-        if (s < V) {
-            const uint32_t p = a.sorted_vis[s];
-            const ushort4 r = a.rect[p];
-            s_pid[q] = p;
-            s_rect[q] = r;
-            cnt[j] = (uint32_t)(r.z - r.x) * (uint32_t)(r.w - r.y);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, radix_tiles(a.max_items));
+    cudaError_t e;
+    if (a.gen) {
+        static bool configured = false;
+        if (!configured) {
+            cudaFuncSetAttribute(radix_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(GenSmem));
+            cudaFuncSetAttribute(radix_scatter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(GenSmem));
+            configured = true;
         }
+        radix_hist_kernel<true><<<grid, kRadixThreads, sizeof(GenSmem), stream>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        radix_scan_kernel<<<kRadixDigits, 256, 0, stream>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        radix_scatter_kernel<true><<<grid, kRadixThreads, sizeof(GenSmem), stream>>>(a);
+    } else {
+        radix_hist_kernel<false><<<grid, kRadixThreads, 0, stream>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        radix_scan_kernel<<<kRadixDigits, 256, 0, stream>>>(a);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        radix_scatter_kernel<false><<<grid, kRadixThreads, 0, stream>>>(a);
     }
-    // block exclusive scan over q
-    uint32_t incl[kDupItems];
-#pragma unroll
-    for (int j = 0; j < kDupItems; ++j) {
-        uint32_t x = cnt[j];
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t nn = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += nn;
-        }
-        incl[j] = x;
-        if (lane == 31) s_warp[j][warp] = x;
-    }
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t v = (&s_warp[0][0])[lane];
-        uint32_t x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t nn = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += nn;
-        }
-        (&s_warp[0][0])[lane] = x - v;
-        const uint32_t total = __shfl_sync(0xffffffffu, x, 31);
-        const uint32_t prefix = lookback_warp(a.lookback, (uint32_t)tile, total);
-        if (lane == 0) { s_base = prefix; s_total = total; }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < kDupItems; ++j) {
-        const int q = j * kDupThreads + tid;
-        s_start[q] = s_warp[j][warp] + incl[j] - cnt[j];
-    }
-    if (tid == 0) s_start[kDupTile] = s_total;
-    __syncthreads();
-    // load-balanced emission: one pair slot per thread per round
-    const uint32_t total = s_total, gbase = s_base;
-    for (uint32_t s = tid; s < total; s += kDupThreads) {
-        // largest q with s_start[q] <= s (items with zero pairs are skipped naturally)
-        int lo = 0, hi = kDupTile - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (s_start[mid] <= s) lo = mid; else hi = mid - 1;
-        }
-        const ushort4 r = s_rect[lo];
-        const uint32_t li = s - s_start[lo];
-        const uint32_t w = (uint32_t)(r.z - r.x);
-        const uint32_t ty = r.y + li / w, tx = r.x + li % w;
-        a.pair_tile[gbase + s] = ty * (uint32_t)a.tiles_x + tx;
-        a.pair_val[gbase + s] = s_pid[lo];
-    }
-}
-
-cudaError_t launch_duplicate(const DuplicateArgs& a, cudaStream_t stream) {
-    const int64_t tiles = duplicate_tiles(a.max_items);
-    duplicate_kernel<<<(unsigned)std::max<int64_t>(1, tiles), kDupThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
 
