@@ -219,7 +219,8 @@ def run_ours(args) -> None:
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
     ev = lambda: torch.cuda.Event(enable_timing=True)
-    stage_names = ("preprocess", "sort", "render_fwd", "render_bwd", "allreduce")
+    stage_names = ("preprocess", "sort", "render_fwd", "render_bwd_tiles", "backward_particles", "allreduce")
+    NS = len(stage_names)
 
     def step(timers=None):
         def mark(i):
@@ -232,11 +233,13 @@ def run_ours(args) -> None:
         mark(2)
         G.ges_render_fwd(frame, st, image, None, stream)
         mark(3)
-        G.ges_render_bwd(params, cam, st, frame, dL, grads, False, stream)
+        G.ges_render_bwd_tiles(st, frame, dL, stream)        # S5a } == ges_render_bwd,
         mark(4)
+        G.ges_backward_particles(params, cam, st, frame, grads, False, stream)  # S5b } timed apart
+        mark(5)
         if world > 1:
             dist.all_reduce(grads.flat)
-        mark(5)
+        mark(6)
 
     for _ in range(args.warmup):
         step()
@@ -253,11 +256,11 @@ def run_ours(args) -> None:
     with ClockSampler(dev.index) as clk:
         for _ in range(args.steps):
             flush.fill_(1)
-            timers = [ev() for _ in range(6)]
+            timers = [ev() for _ in range(NS + 1)]
             step(timers)
             timers[-1].synchronize()
-            step_ms.append(timers[0].elapsed_time(timers[5]))
-            for i in range(5):
+            step_ms.append(timers[0].elapsed_time(timers[NS]))
+            for i in range(NS):
                 stage_ms[i] += timers[i].elapsed_time(timers[i + 1])
         torch.cuda.synchronize()
     if world > 1:
@@ -279,26 +282,30 @@ def run_ours(args) -> None:
                         args.steps)
 
     # ---- algorithmic work for the roofline ----
+    n_comp = torch.zeros(W * H, dtype=torch.int32, device=dev)
     G.ges_preprocess(params, cam, st, frame, stream)
     G.ges_sort(frame, stream)
-    G.ges_render_fwd(frame, st, image, n_eval, stream)
+    G.ges_render_fwd(frame, st, image, n_eval, stream, n_comp=n_comp)
     torch.cuda.synchronize()
     e_fwd = int(n_eval.to(torch.int64).sum().item())
-    e_bwd = int(frame.view("n_contrib", torch.int32, W * H).to(torch.int64).sum().item())
+    e_comp = int(n_comp.to(torch.int64).sum().item())
     peaks, peak_src = measured_peaks()
     clocks = clk.summary()
     sm_mhz = clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    alu_peak = sms * 128 * sm_mhz * 1e6 / 1e12  # T thread-instr/s
+    alu_peak = sms * 128 * sm_mhz * 1e6 / 1e12  # T FP32 thread-instr/s
+    K = scene.particles.K
     rows = {
-        "render_bwd": ("alu", e_bwd * BWD_OPS / (stage_ms[3] / 1e3) / 1e12, alu_peak, "Tinstr/s"),
-        "render_fwd": ("alu", e_fwd * FWD_OPS / (stage_ms[2] / 1e3) / 1e12, alu_peak, "Tinstr/s"),
+        "render_bwd_tiles": ("alu", e_comp * BWD_OPS / (stage_ms[3] / 1e3) / 1e12, alu_peak, "Tinstr/s"),
+        "render_fwd": ("alu", e_comp * FWD_OPS / (stage_ms[2] / 1e3) / 1e12, alu_peak, "Tinstr/s"),
+        "preprocess": ("hbm", preprocess_bytes(P, int(cnt.visible), scene.particles.sh_degree)
+                       / (stage_ms[0] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"),
+        "sort": ("hbm", sort_algorithmic_bytes(P, int(cnt.visible), int(cnt.pairs), frame.c.tile_bits)
+                 / (stage_ms[1] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"),
+        "backward_particles": ("hbm", particle_bwd_bytes(P, int(cnt.visible), K) / (stage_ms[4] / 1e3) / 1e9,
+                               peaks["hbm_gbs"], "GB/s"),
     }
-    pre_bytes = preprocess_bytes(P, int(cnt.visible), scene.particles.sh_degree)
-    rows["preprocess"] = ("hbm", pre_bytes / (stage_ms[0] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s")
-    sort_bytes = sort_algorithmic_bytes(P, int(cnt.visible), int(cnt.pairs), frame.c.tile_bits)
-    rows["sort"] = ("hbm", sort_bytes / (stage_ms[1] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s")
-    dom = max(range(4), key=lambda i: stage_ms[i])
+    dom = max(range(5), key=lambda i: stage_ms[i])
     dname = stage_names[dom]
     bound, achieved, peak, unit = rows[dname]
 
@@ -318,7 +325,8 @@ def run_ours(args) -> None:
             "vs_gaussian_equivalent": {"ges_fwd_ms": fwd_ms, "gaussian_fwd_ms": g_ms, "ratio": g_ms / fwd_ms,
                                        "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
             "stages_ms": {n: float(stage_ms[i]) for i, n in enumerate(stage_names)},
-            "counts": {"visible": int(cnt.visible), "pairs": int(cnt.pairs), "evals_fwd": e_fwd, "evals_bwd": e_bwd},
+            "counts": {"visible": int(cnt.visible), "pairs": int(cnt.pairs), "evals_fwd": e_fwd,
+                       "composited": e_comp},
             "roofline": {"kernel": dname, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                          "frac": achieved / peak, "traffic": None,
                          "peak_source": peak_src if bound == "hbm" else
@@ -334,10 +342,11 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-# algorithmic FP32-pipe thread-instructions per pixel-entry evaluation
-FWD_OPS = 19
-BWD_OPS = 45
-LAUNCHES_PER_STEP = 12  # K1, ranges, 4 depth passes, duplicate, 2 tile passes, K6, K7, K8
+# algorithmic FP32 thread-instructions per composited (pixel, entry)
+FWD_OPS = 20
+BWD_OPS = 38
+# preprocess, ranges, 4 depth passes x (hist, scan, scatter), item scan, 2 tile passes x 3, fwd, bwd tiles, particles
+LAUNCHES_PER_STEP = 1 + 1 + 12 + 1 + 6 + 1 + 1 + 1
 
 
 def preprocess_bytes(P, V, deg):
@@ -348,11 +357,18 @@ def preprocess_bytes(P, V, deg):
 
 
 def sort_algorithmic_bytes(P, V, M, tile_bits):
-    depth = 4 * V * 16                      # 4 LSD passes, key+value read+write
-    dup = V * (4 + 8) + M * 8               # read ids + rects, write (tile, id)
-    tile_passes = 1 if tile_bits <= 8 else 2
-    tiles = (tile_passes - 1) * M * 16 + M * 12   # last pass writes values only
-    return depth + dup + tiles
+    depth = P * 4 + V * 8 + 3 * V * 16      # pass 0 reads P keys, writes V (key, id); passes 1-3 move V
+    scan = V * (4 + 8 + 4 + 16)             # item scan: ids, rects; offsets + item records out
+    # tile passes: the first reads the item records and writes (tile, id) pairs (or ids only when it is
+    # the last pass); the second reads 8 B/pair and writes the 4-B lists
+    tiles = V * 16 + (M * 8 + M * 12 if tile_bits > 8 else M * 4)
+    return depth + scan + tiles
+
+
+def particle_bwd_bytes(P, V, K):
+    # reads: status/flags 2 B for all, params 14 floats + SH 3K floats + 48 B 2-D record for visible;
+    # writes: (14 + 3K) gradient floats for all (overwrite) + 48 B record reset for visible
+    return P * 2 + V * (4 * (14 + 3 * K) + 48 + 48) + P * 4 * (11 + 3 * K)
 
 
 def time_forward(G, params, cam, st, frame, image, flush, stream, steps):

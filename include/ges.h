@@ -142,6 +142,7 @@ typedef struct {
     uint32_t *radix_total; /* [256] digit totals of the current pass               */
     /* ---- S2 pairs and S3 ranges ---- */
     uint32_t *item_offset; /* [P] first pair slot of each depth-sorted visible particle */
+    uint32_t *item_rec;    /* [P][4] packed (slot, particle, x0|y0<<16, x1|y1<<16)     */
     uint32_t *tile_first;  /* [cap/4096+2] sorted particle holding slot 4096*j        */
     uint32_t *pair_tile;   /* [cap] tile ids after the first tile-digit pass          */
     uint32_t *pair_val;    /* [cap] particle ids after the first tile-digit pass      */
@@ -181,15 +182,30 @@ ges_status ges_preprocess(const ges_particles *particles, const ges_camera *came
 ges_status ges_sort(ges_frame *frame, void *stream);
 
 /* S4.  image: [3][H][W] fp32 (device).  Also writes frame.final_T and
- * frame.n_contrib.  n_eval (optional, [H*W] u32, may be NULL) receives the
- * number of list entries each pixel evaluated (diagnostics / roofline). */
+ * frame.n_contrib.  Optional diagnostics ([H*W] u32 each, may be NULL):
+ * n_eval = list entries each pixel evaluated (up to and including the one that
+ * stopped it), n_comp = entries it composited (alpha >= 1/255, before the stop)
+ * -- the algorithmic work of S4 and S5. */
 ges_status ges_render_fwd(ges_frame *frame, const ges_settings *settings, float *image, uint32_t *n_eval,
-                          void *stream);
+                          uint32_t *n_comp, void *stream);
 
-/* S5.  dL_dimage: [3][H][W] fp32 (device).  Writes frame.grad2d, then the
- * parameter gradients into `grads`. */
+/* S5 = S5a then S5b.  dL_dimage: [3][H][W] fp32 (device); gradients of
+ * L = <dL_dimage, image> w.r.t. every particle parameter go to `grads`.
+ * Needs the frame's S1-S4 state (same particles, camera, settings). */
 ges_status ges_render_bwd(const ges_particles *particles, const ges_camera *camera, const ges_settings *settings,
                           ges_frame *frame, const float *dL_dimage, const ges_grads *grads, void *stream);
+
+/* S5a alone: the per-tile adjoint of S4 (Eq. 3); adds the 2-D gradients
+ * into frame.grad2d. */
+ges_status ges_render_bwd_tiles(const ges_settings *settings, ges_frame *frame, const float *dL_dimage,
+                                void *stream);
+
+/* S5b alone: chain frame.grad2d to the parameters (mean, log-scale,
+ * quaternion, opacity logit, SH, beta through phi-bar, Eq. 6) and reset
+ * frame.grad2d to zero. */
+ges_status ges_backward_particles(const ges_particles *particles, const ges_camera *camera,
+                                  const ges_settings *settings, ges_frame *frame, const ges_grads *grads,
+                                  void *stream);
 
 /* Copies the frame's counts to host memory.  Synchronises `stream`. */
 ges_status ges_counts_get(const ges_frame *frame, ges_counts *host_out, void *stream);

@@ -318,7 +318,7 @@ static int composite_pixel(const OrSplat2D *s, const int32_t *lst, int64_t n, do
 
 int or_render_fwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets, const int32_t *list,
                   const uint8_t *tile_mask, double *image, double *final_T, int32_t *n_contrib, int32_t *n_eval,
-                  uint8_t *amb) {
+                  int32_t *n_comp, uint8_t *amb) {
     const int W = sc->width, H = sc->height;
     const int64_t T = (int64_t)sc->tiles_x * sc->tiles_y;
 #pragma omp parallel for schedule(dynamic, 2)
@@ -333,7 +333,8 @@ int or_render_fwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
                 if (px >= W || py >= H) continue;
                 const int64_t pix = (int64_t)py * W + px;
                 double C[3], Tf;
-                composite_pixel(s, lst, n, px + 0.5, py + 0.5, C, &Tf, &n_contrib[pix], &n_eval[pix], &amb[pix], NULL);
+                n_comp[pix] = composite_pixel(s, lst, n, px + 0.5, py + 0.5, C, &Tf, &n_contrib[pix], &n_eval[pix],
+                                              &amb[pix], NULL);
                 for (int ch = 0; ch < 3; ++ch) image[(int64_t)ch * W * H + pix] = C[ch] + Tf * sc->bg[ch];
                 final_T[pix] = Tf;
             }

@@ -281,6 +281,7 @@ def render_fwd(pre, cam, st: Settings, offsets, lst, tile_mask=None) -> dict:
     fT = np.zeros((H, W), np.float64)
     nc = np.zeros((H, W), np.int32)
     ne = np.zeros((H, W), np.int32)
+    ncomp = np.zeros((H, W), np.int32)
     amb = np.zeros((H, W), np.uint8)
     mp = None
     if tile_mask is not None:
@@ -289,8 +290,8 @@ def render_fwd(pre, cam, st: Settings, offsets, lst, tile_mask=None) -> dict:
     lst = keep(np.ascontiguousarray(lst if lst.size else np.zeros(1, np.int32), dtype=np.int32))
     lib().or_render_fwd(C.byref(_screen(cam, st)), C.byref(sp), _ptr(offsets, C.c_int64), _ptr(lst, C.c_int32), mp,
                         _ptr(img, C.c_double), _ptr(fT, C.c_double), _ptr(nc, C.c_int32), _ptr(ne, C.c_int32),
-                        _ptr(amb, C.c_uint8))
-    return {"image": img, "final_T": fT, "n_contrib": nc, "n_eval": ne, "amb": amb}
+                        _ptr(ncomp, C.c_int32), _ptr(amb, C.c_uint8))
+    return {"image": img, "final_T": fT, "n_contrib": nc, "n_eval": ne, "n_comp": ncomp, "amb": amb}
 
 
 def render_bwd(pre, cam, st: Settings, offsets, lst, dL_dimg, tile_mask=None) -> np.ndarray:

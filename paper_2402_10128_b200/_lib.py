@@ -57,7 +57,7 @@ class ges_frame(C.Structure):
         ("depth", C.c_void_p), ("pay0", C.c_void_p), ("pay1", C.c_void_p), ("pay2", C.c_void_p),
         ("radius", C.c_void_p), ("rect", C.c_void_p), ("status", C.c_void_p), ("flags", C.c_void_p),
         ("vis_key", C.c_void_p * 2), ("vis_val", C.c_void_p * 2), ("sorted_vis", C.c_void_p),
-        ("radix_hist", C.c_void_p), ("radix_total", C.c_void_p), ("item_offset", C.c_void_p), ("tile_first", C.c_void_p), ("pair_tile", C.c_void_p),
+        ("radix_hist", C.c_void_p), ("radix_total", C.c_void_p), ("item_offset", C.c_void_p), ("item_rec", C.c_void_p), ("tile_first", C.c_void_p), ("pair_tile", C.c_void_p),
         ("pair_val", C.c_void_p), ("list", C.c_void_p),
         ("ranges", C.c_void_p), ("tile_diff", C.c_void_p), ("hist", C.c_void_p), ("lookback", C.c_void_p),
         ("counters", C.c_void_p), ("zero_bytes", C.c_size_t),
@@ -67,7 +67,8 @@ class ges_frame(C.Structure):
 
 
 EXPORTS = ["ges_workspace_bytes", "ges_frame_init", "ges_preprocess", "ges_sort", "ges_render_fwd",
-           "ges_render_bwd", "ges_counts_get", "ges_status_string", "ges_version"]
+           "ges_render_bwd", "ges_render_bwd_tiles", "ges_backward_particles", "ges_counts_get",
+           "ges_status_string", "ges_version"]
 
 _lib = None
 
@@ -97,10 +98,15 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         L.ges_sort.argtypes = [C.POINTER(ges_frame), C.c_void_p]
         L.ges_render_fwd.restype = C.c_int
         L.ges_render_fwd.argtypes = [C.POINTER(ges_frame), C.POINTER(ges_settings), C.c_void_p, C.c_void_p,
-                                     C.c_void_p]
+                                     C.c_void_p, C.c_void_p]
         L.ges_render_bwd.restype = C.c_int
         L.ges_render_bwd.argtypes = [C.POINTER(ges_particles), C.POINTER(ges_camera), C.POINTER(ges_settings),
                                      C.POINTER(ges_frame), C.c_void_p, C.POINTER(ges_grads), C.c_void_p]
+        L.ges_render_bwd_tiles.restype = C.c_int
+        L.ges_render_bwd_tiles.argtypes = [C.POINTER(ges_settings), C.POINTER(ges_frame), C.c_void_p, C.c_void_p]
+        L.ges_backward_particles.restype = C.c_int
+        L.ges_backward_particles.argtypes = [C.POINTER(ges_particles), C.POINTER(ges_camera), C.POINTER(ges_settings),
+                                             C.POINTER(ges_frame), C.POINTER(ges_grads), C.c_void_p]
         L.ges_counts_get.restype = C.c_int
         L.ges_counts_get.argtypes = [C.POINTER(ges_frame), C.POINTER(ges_counts), C.c_void_p]
         L.ges_status_string.restype = C.c_char_p

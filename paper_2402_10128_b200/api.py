@@ -162,11 +162,12 @@ def ges_sort(frame: Frame, stream=None) -> None:
 
 
 def ges_render_fwd(frame: Frame, settings: Settings, image: torch.Tensor, n_eval: Optional[torch.Tensor] = None,
-                   stream=None) -> None:
+                   stream=None, n_comp: Optional[torch.Tensor] = None) -> None:
     assert image.dtype == torch.float32 and image.is_contiguous() and image.numel() == 3 * frame.width * frame.height
     s = settings.c()
     ne = C.c_void_p(n_eval.data_ptr()) if n_eval is not None else None
-    L.check(L.load().ges_render_fwd(C.byref(frame.c), C.byref(s), C.c_void_p(image.data_ptr()), ne,
+    nc = C.c_void_p(n_comp.data_ptr()) if n_comp is not None else None
+    L.check(L.load().ges_render_fwd(C.byref(frame.c), C.byref(s), C.c_void_p(image.data_ptr()), ne, nc,
                                     C.c_void_p(_stream(stream))), "ges_render_fwd")
 
 
@@ -177,6 +178,20 @@ def ges_render_bwd(particles: PlanarParams, camera, settings: Settings, frame: F
     L.check(L.load().ges_render_bwd(C.byref(p), C.byref(c), C.byref(s), C.byref(frame.c),
                                     C.c_void_p(dL_dimage.data_ptr()), C.byref(g), C.c_void_p(_stream(stream))),
             "ges_render_bwd")
+
+
+def ges_render_bwd_tiles(settings: Settings, frame: Frame, dL_dimage: torch.Tensor, stream=None) -> None:
+    assert dL_dimage.dtype == torch.float32 and dL_dimage.is_contiguous()
+    s = settings.c()
+    L.check(L.load().ges_render_bwd_tiles(C.byref(s), C.byref(frame.c), C.c_void_p(dL_dimage.data_ptr()),
+                                          C.c_void_p(_stream(stream))), "ges_render_bwd_tiles")
+
+
+def ges_backward_particles(particles: PlanarParams, camera, settings: Settings, frame: Frame, grads: PlanarParams,
+                           accumulate: bool = False, stream=None) -> None:
+    p, c, s, g = particles.c_particles(), c_camera(camera), settings.c(), grads.c_grads(accumulate)
+    L.check(L.load().ges_backward_particles(C.byref(p), C.byref(c), C.byref(s), C.byref(frame.c), C.byref(g),
+                                            C.c_void_p(_stream(stream))), "ges_backward_particles")
 
 
 class Renderer:
@@ -193,13 +208,13 @@ class Renderer:
         self.frame = Frame(self.P, self.width, self.height, cap, self.device)
 
     def forward(self, particles: PlanarParams, camera, settings: Settings, image: Optional[torch.Tensor] = None,
-                n_eval=None, stream=None, check_overflow: bool = True) -> torch.Tensor:
+                n_eval=None, stream=None, check_overflow: bool = True, n_comp=None) -> torch.Tensor:
         if image is None:
             image = torch.empty((3, self.height, self.width), dtype=torch.float32, device=self.device)
         for _ in range(3):
             ges_preprocess(particles, camera, settings, self.frame, stream)
             ges_sort(self.frame, stream)
-            ges_render_fwd(self.frame, settings, image, n_eval, stream)
+            ges_render_fwd(self.frame, settings, image, n_eval, stream, n_comp)
             if not check_overflow:
                 break
             cnt = self.frame.counts(stream)

@@ -84,6 +84,7 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     g.radix_hist = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * (size_t)radix_tiles(std::max<int64_t>(P, cap)));
     g.radix_total = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits);
     g.item_offset = (uint32_t*)take(sizeof(uint32_t) * P);
+    g.item_rec = (uint32_t*)take(16 * (size_t)P);
     g.tile_first = (uint32_t*)take(sizeof(uint32_t) * (size_t)slot_tiles(cap));
     g.pair_tile = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
     g.pair_val = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
@@ -193,6 +194,7 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
         p.hist_stride = radix_tiles(std::max<int64_t>(frame->P, frame->pair_capacity));
         p.digit_total = frame->radix_total;
         p.shift = 8 * d;
+        p.digit_bits = 8;
         p.drop_invalid = (d == 0) ? 1 : 0;
         if ((e = launch_radix_pass(p, s)) != cudaSuccess) return GES_ERR_CUDA;
     }
@@ -200,7 +202,7 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     // first pair slot of every sorted particle
     ItemScanArgs is;
     is.sorted_vis = frame->sorted_vis; is.rect = (const ushort4*)frame->rect; is.counters = ctr;
-    is.E = frame->item_offset; is.tile_first = frame->tile_first; is.lookback = frame->lookback + L.scan;
+    is.E = frame->item_offset; is.items = (uint4*)frame->item_rec; is.tile_first = frame->tile_first; is.lookback = frame->lookback + L.scan;
     is.tile_counter = ctr + GES_CTR_TILE0;
     if ((e = launch_item_scan(is, frame->P, s)) != cudaSuccess) return GES_ERR_CUDA;
     // stable sort of the pairs by tile id; the first pass generates the pairs
@@ -219,11 +221,13 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
         p.hist_stride = radix_tiles(std::max<int64_t>(frame->P, frame->pair_capacity));
         p.digit_total = frame->radix_total;
         p.shift = 8 * d;
+        p.digit_bits = std::max(1, std::min(8, frame->tile_bits - 8 * d));
         p.overflow = ctr + GES_CTR_OVERFLOW;
         p.tiles_x = frame->tiles_x;
         p.sorted_vis = frame->sorted_vis;
         p.rect = (const ushort4*)frame->rect;
         p.E = frame->item_offset;
+        p.items = (const uint4*)frame->item_rec;
         p.tile_first = frame->tile_first;
         p.counters = ctr;
         if ((e = launch_radix_pass(p, s)) != cudaSuccess) return GES_ERR_CUDA;
@@ -232,7 +236,7 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
 }
 
 ges_status ges_render_fwd(ges_frame* frame, const ges_settings* settings, float* image, uint32_t* n_eval,
-                          void* stream) {
+                          uint32_t* n_comp, void* stream) {
     if (!frame || !settings || !image) return GES_ERR_INVALID_ARG;
     RenderFwdArgs a;
     a.pay0 = (const float4*)frame->pay0; a.pay1 = (const float4*)frame->pay1; a.pay2 = frame->pay2;
@@ -240,16 +244,13 @@ ges_status ges_render_fwd(ges_frame* frame, const ges_settings* settings, float*
     a.W = frame->width; a.H = frame->height; a.tiles_x = frame->tiles_x; a.tiles_y = frame->tiles_y;
     for (int k = 0; k < 3; ++k) a.bg[k] = settings->background[k];
     a.image = image; a.final_T = frame->final_T; a.n_contrib = frame->n_contrib; a.n_eval = n_eval;
+    a.n_comp = n_comp;
     return cuda_status(launch_render_fwd(a, (cudaStream_t)stream));
 }
 
-ges_status ges_render_bwd(const ges_particles* particles, const ges_camera* camera, const ges_settings* settings,
-                          ges_frame* frame, const float* dL_dimage, const ges_grads* grads, void* stream) {
-    if (!frame || !settings || !dL_dimage || !grads || !particles_ok(particles) || !camera_ok(camera, frame) ||
-        particles->P != frame->P || !grads->mean || !grads->log_scale || !grads->quat || !grads->opacity_logit ||
-        !grads->sh || !grads->beta)
-        return GES_ERR_INVALID_ARG;
-    cudaStream_t s = (cudaStream_t)stream;
+ges_status ges_render_bwd_tiles(const ges_settings* settings, ges_frame* frame, const float* dL_dimage,
+                                void* stream) {
+    if (!frame || !settings || !dL_dimage) return GES_ERR_INVALID_ARG;
     RenderBwdArgs b;
     b.pay0 = (const float4*)frame->pay0; b.pay1 = (const float4*)frame->pay1; b.pay2 = frame->pay2;
     b.list = frame->list; b.ranges = frame->ranges; b.counters = (const unsigned long long*)frame->counters;
@@ -257,8 +258,16 @@ ges_status ges_render_bwd(const ges_particles* particles, const ges_camera* came
     for (int k = 0; k < 3; ++k) b.bg[k] = settings->background[k];
     b.final_T = frame->final_T; b.n_contrib = frame->n_contrib; b.dL_dimage = dL_dimage; b.grad2d = frame->grad2d;
     b.P = (int)frame->P;
-    cudaError_t e = launch_render_bwd(b, s);
-    if (e != cudaSuccess) return GES_ERR_CUDA;
+    return cuda_status(launch_render_bwd(b, (cudaStream_t)stream));
+}
+
+ges_status ges_backward_particles(const ges_particles* particles, const ges_camera* camera,
+                                  const ges_settings* settings, ges_frame* frame, const ges_grads* grads,
+                                  void* stream) {
+    if (!frame || !settings || !grads || !particles_ok(particles) || !camera_ok(camera, frame) ||
+        particles->P != frame->P || !grads->mean || !grads->log_scale || !grads->quat || !grads->opacity_logit ||
+        !grads->sh || !grads->beta)
+        return GES_ERR_INVALID_ARG;
     ParticleBwdArgs q;
     q.mean = particles->mean; q.log_scale = particles->log_scale; q.quat = particles->quat;
     q.opacity_logit = particles->opacity_logit; q.sh = particles->sh; q.beta = particles->beta;
@@ -269,7 +278,18 @@ ges_status ges_render_bwd(const ges_particles* particles, const ges_camera* came
     q.g_mean = grads->mean; q.g_log_scale = grads->log_scale; q.g_quat = grads->quat;
     q.g_opacity_logit = grads->opacity_logit; q.g_sh = grads->sh; q.g_beta = grads->beta;
     q.accumulate = grads->accumulate;
-    return cuda_status(launch_particle_bwd(q, s));
+    return cuda_status(launch_particle_bwd(q, (cudaStream_t)stream));
+}
+
+ges_status ges_render_bwd(const ges_particles* particles, const ges_camera* camera, const ges_settings* settings,
+                          ges_frame* frame, const float* dL_dimage, const ges_grads* grads, void* stream) {
+    if (!frame || !settings || !dL_dimage || !grads || !particles_ok(particles) || !camera_ok(camera, frame) ||
+        particles->P != frame->P || !grads->mean || !grads->log_scale || !grads->quat || !grads->opacity_logit ||
+        !grads->sh || !grads->beta)
+        return GES_ERR_INVALID_ARG;
+    const ges_status st = ges_render_bwd_tiles(settings, frame, dL_dimage, stream);
+    if (st != GES_OK) return st;
+    return ges_backward_particles(particles, camera, settings, frame, grads, stream);
 }
 
 ges_status ges_counts_get(const ges_frame* frame, ges_counts* host_out, void* stream) {

@@ -55,6 +55,7 @@ struct RadixPassArgs {
     int64_t hist_stride;              // >= number of tiles
     uint32_t* digit_total;            // [256] column totals
     int shift;
+    int digit_bits;                   // bits of the digit that can be non-zero (1..8)
     int drop_invalid;                 // 1: keys == 0xffffffff are dropped (compaction)
     const unsigned long long* overflow;  // non-null and set: do nothing
     // gen = 1: keys/values generated from the sorted particles (pair expansion)
@@ -63,6 +64,7 @@ struct RadixPassArgs {
     const uint32_t* sorted_vis;
     const ushort4* rect;
     const uint32_t* E;
+    const uint4* items;
     const uint32_t* tile_first;
     const unsigned long long* counters;
 };
@@ -75,6 +77,7 @@ struct ItemScanArgs {
     const ushort4* rect;
     const unsigned long long* counters;
     uint32_t* E;                      // [P]
+    uint4* items;                     // [P] packed (E, particle, rect x0|y0<<16, x1|y1<<16)
     uint32_t* tile_first;             // [cap/4096 + 2]
     uint32_t* lookback;               // [tiles]
     unsigned long long* tile_counter;
@@ -98,6 +101,7 @@ struct RenderFwdArgs {
     float* final_T;
     uint32_t* n_contrib;
     uint32_t* n_eval;
+    uint32_t* n_comp;
 };
 cudaError_t launch_render_fwd(const RenderFwdArgs& a, cudaStream_t stream);
 

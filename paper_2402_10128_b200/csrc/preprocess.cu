@@ -26,15 +26,33 @@ struct PreOut {
     uint8_t status, flags;
 };
 
+// The 12 per-particle scalars every particle needs (one memory round trip).
+struct ParamIn {
+    float mx, my, mz, qw, qx, qy, qz, ls0, ls1, ls2, beta, logit;
+};
+
+__device__ __forceinline__ ParamIn load_params(const PreprocessArgs& a, int i) {
+    const int P = a.P;
+    ParamIn p;
+    p.mx = __ldg(a.mean + i); p.my = __ldg(a.mean + P + i); p.mz = __ldg(a.mean + 2 * P + i);
+    p.qw = __ldg(a.quat + i); p.qx = __ldg(a.quat + P + i); p.qy = __ldg(a.quat + 2 * P + i);
+    p.qz = __ldg(a.quat + 3 * P + i);
+    p.ls0 = __ldg(a.log_scale + i); p.ls1 = __ldg(a.log_scale + P + i); p.ls2 = __ldg(a.log_scale + 2 * P + i);
+    p.beta = __ldg(a.beta + i);
+    p.logit = __ldg(a.opacity_logit + i);
+    return p;
+}
+
 template <int K>
-__device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const CamDerived& cd, int i) {
+__device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const CamDerived& cd, int i,
+                                                 const ParamIn& in) {
     const int P = a.P;
     const CamParams& c = a.cam;
     PreOut o;
     o.u = o.v = o.ca = o.cb = o.cc = o.kappa = o.r = o.g = o.b = 0.0f;
     o.radius = o.x0 = o.y0 = o.x1 = o.y1 = 0;
     o.flags = 0;
-    const float mx = __ldg(a.mean + i), my = __ldg(a.mean + P + i), mz = __ldg(a.mean + 2 * P + i);
+    const float mx = in.mx, my = in.my, mz = in.mz;
     // camera space t = W mu + t
     float tx = fmul(c.R[0], mx); tx = ffma(c.R[1], my, tx); tx = ffma(c.R[2], mz, tx); tx = fadd(tx, c.t[0]);
     float ty = fmul(c.R[3], mx); ty = ffma(c.R[4], my, ty); ty = ffma(c.R[5], mz, ty); ty = fadd(ty, c.t[1]);
@@ -43,8 +61,7 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
     if (!(tz > c.near_z)) { o.status = GES_CULL_NEAR; return o; }
 
     // normalised quaternion -> rotation
-    float qw = __ldg(a.quat + i), qx = __ldg(a.quat + P + i), qy = __ldg(a.quat + 2 * P + i),
-          qz = __ldg(a.quat + 3 * P + i);
+    float qw = in.qw, qx = in.qx, qy = in.qy, qz = in.qz;
     float n2 = fmul(qw, qw); n2 = ffma(qx, qx, n2); n2 = ffma(qy, qy, n2); n2 = ffma(qz, qz, n2);
     if (!(n2 > 0.0f) || !isfinite(n2)) { o.status = GES_DEGENERATE; return o; }
     const float nq = fsqrt(n2);
@@ -66,7 +83,7 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
     // phi-bar (Eq. 6) -> effective scale (R1)
     float mfac = 1.0f;
     if (!a.gaussian_only) {
-        const float d = fsub(__ldg(a.beta + i), 2.0f);
+        const float d = fsub(in.beta, 2.0f);
         const float ar = fmul(a.rho, d);
         const float e = exp_spec(-ar);
         const float phi = fdiv(2.0f, fadd(1.0f, e));
@@ -74,7 +91,7 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
     }
     float se[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) se[k] = fmul(exp_spec(__ldg(a.log_scale + k * P + i)), mfac);
+    for (int k = 0; k < 3; ++k) se[k] = fmul(exp_spec(k == 0 ? in.ls0 : (k == 1 ? in.ls1 : in.ls2)), mfac);
 
     // Sigma = M M^T, M = R diag(se)
     float M[3][3];
@@ -162,7 +179,7 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
         rgb[ch] = acc;
     }
     o.r = rgb[0]; o.g = rgb[1]; o.b = rgb[2];
-    o.kappa = fdiv(1.0f, fadd(1.0f, exp_spec(-__ldg(a.opacity_logit + i))));
+    o.kappa = fdiv(1.0f, fadd(1.0f, exp_spec(-in.logit)));
     o.flags = fl;
     o.status = GES_VISIBLE;
     return o;
@@ -184,7 +201,8 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(PreprocessAr
     const CamDerived cd = derive_camera(a.cam);
     const int stride_diff = a.cam.tiles_x + 1;
     for (int i = blockIdx.x * kPreThreads + tid; i < a.P; i += gridDim.x * kPreThreads) {
-        const PreOut o = preprocess_one<K>(a, cd, i);
+        const ParamIn in = load_params(a, i);
+        const PreOut o = preprocess_one<K>(a, cd, i, in);
         a.depth[i] = o.depth;
         a.pay0[i] = make_float4(o.u, o.v, o.ca, o.cb);
         a.pay1[i] = make_float4(o.cc, o.kappa, o.r, o.g);

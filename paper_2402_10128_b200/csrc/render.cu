@@ -23,6 +23,8 @@
 // gradients across each warp with a recursive-halving shuffle (24 SHFL per
 // warp and entry) and adds them with three vector reductions
 // (red.global.add.v4.f32) into the particle's 12-float gradient record.
+#include <cstdlib>
+
 #include "ges_internal.h"
 
 namespace ges {
@@ -172,11 +174,11 @@ __global__ void __launch_bounds__(Layout<PPT>::kThreads) render_fwd_kernel(Rende
     uint32_t start = a.ranges[tile], end = a.ranges[tile + 1];
     if (a.counters[GES_CTR_OVERFLOW]) start = end = 0;
     float T[PPT], cr[PPT], cg[PPT], cb[PPT];
-    uint32_t last[PPT], n_eval[PPT];
+    uint32_t last[PPT], n_eval[PPT], n_comp[PPT];
     uint32_t done = 0;  // bit k: pixel k finished (or outside the image)
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
-        T[k] = 1.0f; cr[k] = cg[k] = cb[k] = 0.0f; last[k] = 0; n_eval[k] = end - start;
+        T[k] = 1.0f; cr[k] = cg[k] = cb[k] = 0.0f; last[k] = 0; n_eval[k] = end - start; n_comp[k] = 0;
         if (!(px < a.W && py0 + 4 * k < a.H)) done |= 1u << k;
     }
     constexpr uint32_t kAll = (1u << PPT) - 1u;
@@ -190,30 +192,30 @@ __global__ void __launch_bounds__(Layout<PPT>::kThreads) render_fwd_kernel(Rende
         for (int i = 0; i < nw; ++i) {
             if (__all_sync(0xffffffffu, done == kAll)) break;
             const int j = s_list[warp][i];
-            if (done == kAll) continue;
             const float4 g0 = s_g0[j];
             const float4 g1 = s_g1[j];
+            const float gbl = s_b[j];
             const float dx = __fsub_rn(g0.x, fpx);
-            const uint32_t pos = b0 - start + j;
+            const uint32_t pos1 = b0 - start + j + 1;
+            // branch-free per pixel: the decisions become predicates
 #pragma unroll
             for (int k = 0; k < PPT; ++k) {
-                if (done & (1u << k)) continue;
                 const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
                 const float p2 = fminf(raw_exponent(g0.z, g0.w, g1.x, dx, dy), 0.0f);
                 const float alpha = fminf(kAlphaMax, __fmul_rn(g1.y, fast_exp2(p2)));
-                if (alpha < kAlphaMin) continue;
+                const bool live = !((done >> k) & 1u) && alpha >= kAlphaMin;
                 const float Tn = __fmul_rn(T[k], __fsub_rn(1.0f, alpha));
-                if (Tn < kTMin) {
-                    done |= 1u << k;
-                    n_eval[k] = pos + 1;
-                    continue;
-                }
-                const float w = __fmul_rn(alpha, T[k]);
+                const bool stop = live && Tn < kTMin;
+                const bool comp = live && !stop;
+                done |= (stop ? 1u : 0u) << k;
+                n_eval[k] = stop ? pos1 : n_eval[k];
+                const float w = comp ? __fmul_rn(alpha, T[k]) : 0.0f;
                 cr[k] = __fmaf_rn(g1.z, w, cr[k]);
                 cg[k] = __fmaf_rn(g1.w, w, cg[k]);
-                cb[k] = __fmaf_rn(s_b[j], w, cb[k]);
-                T[k] = Tn;
-                last[k] = pos + 1;
+                cb[k] = __fmaf_rn(gbl, w, cb[k]);
+                T[k] = comp ? Tn : T[k];
+                last[k] = comp ? pos1 : last[k];
+                n_comp[k] += comp ? 1u : 0u;
             }
         }
     }
@@ -229,14 +231,24 @@ __global__ void __launch_bounds__(Layout<PPT>::kThreads) render_fwd_kernel(Rende
             a.final_T[pix] = T[k];
             a.n_contrib[pix] = last[k];
             if (a.n_eval) a.n_eval[pix] = n_eval[k];
+            if (a.n_comp) a.n_comp[pix] = n_comp[k];
         }
     }
 }
 
-constexpr int kPPT = 2;
+// Pixels per thread (tuning knob; GES_PPT_FWD / GES_PPT_BWD override for experiments).
+static int ppt_from_env(const char* name, int dflt) {
+    const char* e = getenv(name);
+    const int v = e ? atoi(e) : dflt;
+    return (v == 1 || v == 2 || v == 4) ? v : dflt;
+}
 
 cudaError_t launch_render_fwd(const RenderFwdArgs& a, cudaStream_t stream) {
-    render_fwd_kernel<kPPT><<<a.tiles_x * a.tiles_y, Layout<kPPT>::kThreads, 0, stream>>>(a);
+    static const int ppt = ppt_from_env("GES_PPT_FWD", 2);
+    const int grid = a.tiles_x * a.tiles_y;
+    if (ppt == 1) render_fwd_kernel<1><<<grid, Layout<1>::kThreads, 0, stream>>>(a);
+    else if (ppt == 4) render_fwd_kernel<4><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
+    else render_fwd_kernel<2><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
 
@@ -378,7 +390,11 @@ __global__ void __launch_bounds__(Layout<PPT>::kThreads) render_bwd_kernel(Rende
 }
 
 cudaError_t launch_render_bwd(const RenderBwdArgs& a, cudaStream_t stream) {
-    render_bwd_kernel<kPPT><<<a.tiles_x * a.tiles_y, Layout<kPPT>::kThreads, 0, stream>>>(a);
+    static const int ppt = ppt_from_env("GES_PPT_BWD", 4);
+    const int grid = a.tiles_x * a.tiles_y;
+    if (ppt == 1) render_bwd_kernel<1><<<grid, Layout<1>::kThreads, 0, stream>>>(a);
+    else if (ppt == 4) render_bwd_kernel<4><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
+    else render_bwd_kernel<2><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

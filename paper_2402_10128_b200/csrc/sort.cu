@@ -186,10 +186,13 @@ __global__ void __launch_bounds__(kScanThreads) item_scan_kernel(ItemScanArgs a)
     const int64_t first = tile * kScanTile + (int64_t)tid * kScanItems;
     uint32_t c[kScanItems], ids[kScanItems];
     uint32_t sum = 0;
+    ushort4 rc[kScanItems];
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) ids[j] = (first + j < V) ? __ldg(a.sorted_vis + first + j) : 0u;
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) c[j] = (first + j < V) ? rect_count(__ldg(a.rect + ids[j])) : 0u;
+    for (int j = 0; j < kScanItems; ++j) rc[j] = (first + j < V) ? __ldg(a.rect + ids[j]) : make_ushort4(0, 0, 0, 0);
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) c[j] = rect_count(rc[j]);
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) sum += c[j];
     uint32_t incl = sum;
@@ -219,6 +222,9 @@ __global__ void __launch_bounds__(kScanThreads) item_scan_kernel(ItemScanArgs a)
     for (int j = 0; j < kScanItems; ++j) {
         if (first + j < V) {
             a.E[first + j] = e;
+            // packed item record for the pair expansion: one coalesced 16-B load there
+            a.items[first + j] = make_uint4(e, ids[j], (uint32_t)rc[j].x | ((uint32_t)rc[j].y << 16),
+                                            (uint32_t)rc[j].z | ((uint32_t)rc[j].w << 16));
             // slot tiles whose first slot lies in [e, e + c)
             for (uint32_t st = (e + kSlotTile - 1) / kSlotTile; st * (uint64_t)kSlotTile < (uint64_t)e + c[j]; ++st)
                 a.tile_first[st] = (uint32_t)(first + j);
@@ -252,10 +258,14 @@ static_assert(kRadixTile == kSlotTile, "slot tiles are radix tiles");
 
 int64_t radix_tiles(int64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
 
+// Particles covering a tile's 4096 slots are staged in shared memory when
+// there are at most kStageMax of them (the common case: a particle touches
+// ~20 tiles); tiles of many tiny particles read them from L2 instead.
+constexpr int kStageMax = 2048;
 struct GenSmem {
-    uint32_t E[kRadixTile + 1];
-    uint32_t pid[kRadixTile + 1];
-    ushort4 rect[kRadixTile + 1];
+    uint32_t E[kStageMax];
+    uint32_t pid[kStageMax];
+    ushort4 rect[kStageMax];
 };
 
 __device__ __forceinline__ int64_t pass_count(const RadixPassArgs& a) {
@@ -280,13 +290,30 @@ __device__ __forceinline__ void load_tile(const RadixPassArgs& a, int64_t tile, 
         const int64_t f = a.tile_first[tile];
         const int64_t last_item = (slot0 + kRadixTile < n) ? (int64_t)a.tile_first[tile + 1] : V - 1;
         const int nit = (int)(last_item - f + 1);
-        for (int q = tid; q < nit; q += kRadixThreads) {
-            const uint32_t p = a.sorted_vis[f + q];
-            g.E[q] = a.E[f + q];
-            g.pid[q] = p;
-            g.rect[q] = a.rect[p];
+        const bool staged = nit <= kStageMax;
+        if (staged) {
+            constexpr int kU = kStageMax / kRadixThreads;
+            uint4 rec[kU];
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int q = tid + u * kRadixThreads;
+                if (q < nit) rec[u] = __ldg(a.items + f + q);
+            }
+#pragma unroll
+            for (int u = 0; u < kU; ++u) {
+                const int q = tid + u * kRadixThreads;
+                if (q < nit) {
+                    g.E[q] = rec[u].x;
+                    g.pid[q] = rec[u].y;
+                    g.rect[q] = make_ushort4((uint16_t)(rec[u].z & 0xffffu), (uint16_t)(rec[u].z >> 16),
+                                             (uint16_t)(rec[u].w & 0xffffu), (uint16_t)(rec[u].w >> 16));
+                }
+            }
         }
         __syncthreads();
+        auto itemE = [&](int q) -> uint32_t { return staged ? g.E[q] : __ldg(a.E + f + q); };
+        auto itemPid = [&](int q) -> uint32_t { return staged ? g.pid[q] : __ldg(a.sorted_vis + f + q); };
+        auto itemRect = [&](int q) -> ushort4 { return staged ? g.rect[q] : __ldg(a.rect + itemPid(q)); };
         // thread-contiguous slots, then an exchange to the warp-striped order
         const int ls0 = tid * kRadixItems;
         int it = 0;
@@ -295,32 +322,42 @@ __device__ __forceinline__ void load_tile(const RadixPassArgs& a, int64_t tile, 
             int lo = 0, hi = nit - 1;  // last item with E <= s0
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
-                if (g.E[mid] <= s0) lo = mid; else hi = mid - 1;
+                if (itemE(mid) <= s0) lo = mid; else hi = mid - 1;
             }
             it = lo;
         }
-        ushort4 r = g.rect[it];
-        uint32_t E0 = g.E[it], pid = g.pid[it], E1 = (it + 1 < nit) ? g.E[it + 1] : 0xffffffffu;
+        // walk the thread's 16 consecutive slots: one division per item start, then
+        // the tile advances along the rect's rows incrementally
+        ushort4 r = itemRect(it);
+        uint32_t pid = itemPid(it), E1 = (it + 1 < nit) ? itemE(it + 1) : 0xffffffffu;
         uint32_t w = r.z - r.x;
-        float inv_w = __frcp_rn((float)w);
+        uint32_t xx = 0, yy = 0;
+        if (ls0 < nslots) {
+            const uint32_t li = (uint32_t)(slot0 + ls0) - itemE(it);
+            // li / w exactly: the quotient is < 2^16, far from rounding trouble
+            yy = __float2uint_rz(((float)li + 0.5f) * __fdividef(1.0f, (float)w));
+            xx = li - yy * w;
+        }
 #pragma unroll
         for (int j = 0; j < kRadixItems; ++j) {
             const int ls = ls0 + j;
             const uint32_t s = (uint32_t)(slot0 + ls);
             if (ls < nslots) {
-                while (s >= E1) {
-                    ++it;
-                    r = g.rect[it];
-                    E0 = E1;
-                    pid = g.pid[it];
-                    E1 = (it + 1 < nit) ? g.E[it + 1] : 0xffffffffu;
+                if (s >= E1) {  // next item(s); items are never empty
+                    do {
+                        ++it;
+                        E1 = (it + 1 < nit) ? itemE(it + 1) : 0xffffffffu;
+                    } while (s >= E1);
+                    r = itemRect(it);
+                    pid = itemPid(it);
                     w = r.z - r.x;
-                    inv_w = __frcp_rn((float)w);
+                    xx = 0;
+                    yy = 0;
                 }
-                const uint32_t li = s - E0;
-                const uint32_t yy = __float2uint_rz(((float)li + 0.5f) * inv_w);
-                s_keys[ls] = (r.y + yy) * (uint32_t)a.tiles_x + r.x + (li - yy * w);
-                s_vals[ls] = pid;
+                const int pad = ls + (ls >> 5);  // +1 word per 32: conflict-free both ways
+                s_keys[pad] = (r.y + yy) * (uint32_t)a.tiles_x + r.x + xx;
+                s_vals[pad] = pid;
+                if (++xx == w) { xx = 0; ++yy; }
             }
         }
         __syncthreads();
@@ -328,30 +365,44 @@ __device__ __forceinline__ void load_tile(const RadixPassArgs& a, int64_t tile, 
         for (int j = 0; j < kRadixItems; ++j) {
             const int ls = warp * (kRadixItems * 32) + j * 32 + lane;
             if (ls < nslots) {
-                k[j] = s_keys[ls];
-                v[j] = s_vals[ls];
+                const int pad = ls + (ls >> 5);
+                k[j] = s_keys[pad];
+                v[j] = s_vals[pad];
                 valid |= 1u << j;
             }
         }
         __syncthreads();
     } else {
+        // issue every load before any use (all in flight together)
 #pragma unroll
         for (int j = 0; j < kRadixItems; ++j) {
             const int64_t idx = base + j * 32 + lane;
-            k[j] = kInvalidKey;
-            if (idx < n) {
-                k[j] = a.keys_in[idx];
-                if (need_vals) v[j] = a.vals_in ? a.vals_in[idx] : (uint32_t)idx;
-                if (!(a.drop_invalid && k[j] == kInvalidKey)) valid |= 1u << j;
+            k[j] = (idx < n) ? __ldg(a.keys_in + idx) : kInvalidKey;
+        }
+        if (need_vals) {
+            if (a.vals_in) {
+#pragma unroll
+                for (int j = 0; j < kRadixItems; ++j) {
+                    const int64_t idx = base + j * 32 + lane;
+                    v[j] = (idx < n) ? __ldg(a.vals_in + idx) : 0u;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < kRadixItems; ++j) v[j] = (uint32_t)(base + j * 32 + lane);
             }
+        }
+#pragma unroll
+        for (int j = 0; j < kRadixItems; ++j) {
+            const int64_t idx = base + j * 32 + lane;
+            if (idx < n && !(a.drop_invalid && k[j] == kInvalidKey)) valid |= 1u << j;
         }
     }
 }
 
 template <bool GEN>
 __global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(RadixPassArgs a) {
-    __shared__ uint32_t s_keys[GEN ? kRadixTile : 1];
-    __shared__ uint32_t s_vals[GEN ? kRadixTile : 1];
+    __shared__ uint32_t s_keys[GEN ? kRadixTile + kRadixTile / 32 : 1];
+    __shared__ uint32_t s_vals[GEN ? kRadixTile + kRadixTile / 32 : 1];
     __shared__ uint32_t s_hist[kRadixDigits];
     extern __shared__ __align__(16) unsigned char s_dyn[];
     if (a.overflow && *a.overflow) return;
@@ -406,8 +457,8 @@ __global__ void __launch_bounds__(256) radix_scan_kernel(RadixPassArgs a) {
 
 template <bool GEN>
 __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(RadixPassArgs a) {
-    __shared__ uint32_t s_keys[kRadixTile];
-    __shared__ uint32_t s_vals[kRadixTile];
+    __shared__ uint32_t s_keys[kRadixTile + kRadixTile / 32];
+    __shared__ uint32_t s_vals[kRadixTile + kRadixTile / 32];
     __shared__ uint32_t s_whist[kRadixWarps][kRadixDigits];
     __shared__ uint32_t s_local[kRadixDigits];
     __shared__ uint32_t s_global[kRadixDigits];
@@ -419,6 +470,9 @@ __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(RadixPassA
     if (tile * kRadixTile >= n) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    // keys first: their loads overlap the offset computation below
+    uint32_t k[kRadixItems], v[kRadixItems], rank[kRadixItems], valid;
+    load_tile<GEN>(a, tile, n, k, v, valid, s_keys, s_vals, s_dyn, true);
     for (int d = tid; d < kRadixWarps * kRadixDigits; d += kRadixThreads) (&s_whist[0][0])[d] = 0;
     // global digit offsets: exclusive scan of the column totals + this tile's prefix
     {
@@ -439,19 +493,25 @@ __global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(RadixPassA
         s_global[tid] = s_warp[warp] + incl - tot + a.tile_hist[(int64_t)tid * a.hist_stride + tile];
         __syncthreads();
     }
-    uint32_t k[kRadixItems], v[kRadixItems], rank[kRadixItems], valid;
-    load_tile<GEN>(a, tile, n, k, v, valid, s_keys, s_vals, s_dyn, true);
-    // warp multisplit ranking, items in (j, lane) = index order
+    // warp multisplit ranking, items in (j, lane) = index order.  The lanes
+    // holding the same digit are found with one ballot per digit bit (only the
+    // bits this pass can hold), which issues at full rate, unlike MATCH.
+    const int nbits = a.digit_bits;
 #pragma unroll
     for (int j = 0; j < kRadixItems; ++j) {
         const bool ok = (valid >> j) & 1u;
-        const uint32_t d = ok ? ((k[j] >> a.shift) & 255u) : 256u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t d = (k[j] >> a.shift) & 255u;
+        uint32_t peers = __ballot_sync(0xffffffffu, ok);
+        for (int b = 0; b < nbits; ++b) {
+            const uint32_t bit = (d >> b) & 1u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+            peers &= bit ? bal : ~bal;
+        }
         uint32_t cnt = 0;
         if (ok) cnt = s_whist[warp][d];
         __syncwarp();
         rank[j] = cnt + __popc(peers & lt_mask);
-        if (ok && lane == 31 - __clz(peers)) s_whist[warp][d] = cnt + __popc(peers);
+        if (ok && (peers >> lane) == 1u) s_whist[warp][d] = cnt + __popc(peers);
         __syncwarp();
     }
     __syncthreads();

@@ -17,7 +17,8 @@ def gpu_forward(parts, cam, gs, pair_capacity=None, n_eval=True):
     dev = G.PlanarParams.from_inputs(parts)
     r = G.Renderer(P, cam.width, cam.height, pair_capacity=pair_capacity)
     ne = torch.zeros(cam.width * cam.height, dtype=torch.int32, device="cuda") if n_eval else None
-    img = r.forward(dev, cam, gs, n_eval=ne)
+    ncp = torch.zeros(cam.width * cam.height, dtype=torch.int32, device="cuda") if n_eval else None
+    img = r.forward(dev, cam, gs, n_eval=ne, n_comp=ncp)
     torch.cuda.synchronize()
     f = r.frame
     cnt = f.counts()
@@ -39,6 +40,7 @@ def gpu_forward(parts, cam, gs, pair_capacity=None, n_eval=True):
     }
     if ne is not None:
         out["n_eval"] = ne.cpu().numpy().reshape(cam.height, cam.width)
+        out["n_comp"] = ncp.cpu().numpy().reshape(cam.height, cam.width)
     return out
 
 

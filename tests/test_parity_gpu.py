@@ -61,6 +61,7 @@ def compare_image(out, ref, tol=1e-4, max_amb_frac=2e-3):
     assert np.abs(out["final_T"][ok] - ref["final_T"][ok]).max() <= tol
     if "n_eval" in out:
         assert np.array_equal(out["n_eval"][ok], ref["n_eval"][ok])
+        assert np.array_equal(out["n_comp"][ok], ref["n_comp"][ok])
 
 
 def compare_grads(gg, ref, pre, amb, tiles_x, max_bad_frac=1e-3):

@@ -1,0 +1,63 @@
+"""Summaries of ncu outputs for profiles/ (markdown).
+
+    python tools/summarize_ncu.py launches <launches.csv>      # per-kernel device time
+    python tools/summarize_ncu.py full <report.ncu-rep>        # key metrics per captured kernel
+"""
+import collections
+import csv
+import io
+import subprocess
+import sys
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h, data = rows[hi], rows[hi + 1:]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    order, agg = [], collections.defaultdict(list)
+    for r in data:
+        k = r[ki].split("(")[0]
+        if k not in agg:
+            order.append(k)
+        agg[k].append(float(r[vi]) / 1000.0)
+    print("| kernel | launches | median us | min us | max us |")
+    print("|---|---|---|---|---|")
+    for k in order:
+        v = sorted(agg[k])
+        print(f"| `{k}` | {len(v)} | {v[len(v) // 2]:.1f} | {v[0]:.1f} | {v[-1]:.1f} |")
+
+
+WANT = ["Duration", "DRAM Throughput", "Memory Throughput", "Compute (SM) Throughput", "Issue Slots Busy",
+        "Executed Ipc Active", "Achieved Occupancy", "Registers Per Thread", "L2 Hit Rate"]
+RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "smsp__inst_executed.sum"]
+
+
+def full(path):
+    det = subprocess.run(["ncu", "-i", path, "--page", "details", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(det)))
+    h = rows[0]
+    ki, ii, mi, vi, ui = (h.index(x) for x in ("Kernel Name", "ID", "Metric Name", "Metric Value", "Metric Unit"))
+    per = collections.OrderedDict()
+    for r in rows[1:]:
+        key = (r[ii], r[ki].split("(")[0])
+        if r[mi] in WANT:
+            per.setdefault(key, {})[r[mi]] = f"{r[vi]} {r[ui]}".strip()
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    hr = rr[0]
+    units = rr[1]
+    rawv = {}
+    for row in rr[2:]:
+        key = (row[hr.index("ID")], row[hr.index("Kernel Name")].split("(")[0])
+        rawv[key] = {m: f"{row[hr.index(m)]} {units[hr.index(m)]}" for m in RAW if m in hr}
+    cols = WANT + RAW
+    print("| id | kernel | " + " | ".join(cols) + " |")
+    print("|---|---|" + "---|" * len(cols))
+    for key, d in per.items():
+        d.update(rawv.get(key, {}))
+        print(f"| {key[0]} | `{key[1]}` | " + " | ".join(d.get(c, "") for c in cols) + " |")
+
+
+if __name__ == "__main__":
+    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
