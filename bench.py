@@ -214,7 +214,7 @@ def run_ours(args) -> None:
     r = G.Renderer(P, W, H, device=dev)
     r.forward(params, cam, st, image)               # sizes the pair buffer (one sync)
     cnt = r.frame.counts()
-    r.grow(int(cnt.pairs))                          # capacity = 1.25 M, fixed from here on
+    r.grow(int(cnt.slots))                          # capacity = 1.25 x slots, fixed from here on
     frame = r.frame
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=dev)
 
@@ -325,7 +325,7 @@ def run_ours(args) -> None:
             "vs_gaussian_equivalent": {"ges_fwd_ms": fwd_ms, "gaussian_fwd_ms": g_ms, "ratio": g_ms / fwd_ms,
                                        "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
             "stages_ms": {n: float(stage_ms[i]) for i, n in enumerate(stage_names)},
-            "counts": {"visible": int(cnt.visible), "pairs": int(cnt.pairs), "evals_fwd": e_fwd,
+            "counts": {"visible": int(cnt.visible), "pairs": int(cnt.pairs), "slots": int(cnt.slots), "evals_fwd": e_fwd,
                        "composited": e_comp},
             "roofline": {"kernel": dname, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                          "frac": achieved / peak, "traffic": None,
@@ -359,9 +359,9 @@ def preprocess_bytes(P, V, deg):
 def sort_algorithmic_bytes(P, V, M, tile_bits):
     depth = P * 4 + V * 8 + 3 * V * 16      # pass 0 reads P keys, writes V (key, id); passes 1-3 move V
     scan = V * (4 + 8 + 4 + 16)             # item scan: ids, rects; offsets + item records out
-    # tile passes: the first reads the item records and writes (tile, id) pairs (or ids only when it is
-    # the last pass); the second reads 8 B/pair and writes the 4-B lists
-    tiles = V * 16 + (M * 8 + M * 12 if tile_bits > 8 else M * 4)
+    # tile passes: the first reads the item records (+ 32 B geometry) and writes the M member
+    # (tile, id) pairs; the second moves them (8 B in, 8 B out); ranges read the M sorted tile ids
+    tiles = V * 48 + M * 8 + (M * 16 if tile_bits > 8 else 0) + M * 4
     return depth + scan + tiles
 
 

@@ -44,10 +44,11 @@
  *     pixel (row i, col j) samples the point (j+0.5, i+0.5).
  *   - Images are planar fp32 [3][H][W], linear, unclamped.
  *   - Errors: argument errors return GES_ERR_INVALID_ARG before any launch;
- *     launch failures return GES_ERR_CUDA.  A frame whose pair count M
- *     exceeds its capacity sets counts.overflow; ges_sort then writes no
- *     pairs and the renders draw nothing: the caller regrows the workspace
- *     (ges_workspace_bytes with a larger capacity) and re-runs.
+ *     launch failures return GES_ERR_CUDA.  A frame whose pair-slot count
+ *     (sum of rect areas) exceeds its capacity sets counts.overflow;
+ *     ges_sort then writes no pairs and the renders draw nothing: the caller
+ *     regrows the workspace (ges_workspace_bytes with a larger capacity) and
+ *     re-runs.
  */
 #ifndef GES_H_
 #define GES_H_
@@ -107,15 +108,23 @@ typedef struct {
 } ges_grads;
 
 typedef struct {
-    int64_t visible;    /* particles with status GES_VISIBLE                     */
-    int64_t pairs;      /* M = sum over visible particles of tiles touched       */
-    int64_t capacity;   /* pair capacity of the frame                            */
-    int32_t overflow;   /* 1 if pairs > capacity: lists and images are invalid   */
+    int64_t visible;    /* particles with status GES_VISIBLE                        */
+    int64_t pairs;      /* M = (tile, particle) pairs in the per-tile lists          */
+    int64_t slots;      /* sum over visible particles of their rect areas (>= M)     */
+    int64_t capacity;   /* pair capacity of the frame                               */
+    int32_t overflow;   /* 1 if slots > capacity: lists and images are invalid       */
     int32_t _pad;
 } ges_counts;
 
 /* Counter slots inside frame.counters (uint64). */
-enum { GES_CTR_VISIBLE = 0, GES_CTR_PAIRS = 1, GES_CTR_OVERFLOW = 2, GES_CTR_TILE0 = 3, GES_CTR_N = 16 };
+enum {
+    GES_CTR_VISIBLE = 0,  /* V: visible particles                                 */
+    GES_CTR_PAIRS = 1,    /* M: (tile, particle) pairs in the lists (R8/R10)        */
+    GES_CTR_OVERFLOW = 2, /* 1 if SLOTS > pair capacity                             */
+    GES_CTR_SLOTS = 3,    /* rect pairs = sum of rect areas (pair-slot count)       */
+    GES_CTR_TICKET = 4,   /* scratch                                                */
+    GES_CTR_N = 16
+};
 
 /* A frame: every per-frame device array, carved by ges_frame_init out of ONE
  * caller-owned device workspace.  The struct lives in caller (host) memory;
@@ -139,18 +148,17 @@ typedef struct {
     uint32_t *sorted_vis;  /* [V] visible particles in (depth, index) order (alias) */
     /* ---- S2 radix scratch ---- */
     uint32_t *radix_hist;  /* [256][max(P,cap)/4096] per-tile digit counts -> offsets (digit-major) */
-    uint32_t *radix_total; /* [256] digit totals of the current pass               */
+    uint32_t *radix_total; /* [2][256] digit totals of the two tile passes (depth passes use [0]) */
     /* ---- S2 pairs and S3 ranges ---- */
     uint32_t *item_offset; /* [P] first pair slot of each depth-sorted visible particle */
     uint32_t *item_rec;    /* [P][4] packed (slot, particle, x0|y0<<16, x1|y1<<16)     */
     uint32_t *tile_first;  /* [cap/4096+2] sorted particle holding slot 4096*j        */
     uint32_t *pair_tile;   /* [cap] tile ids after the first tile-digit pass          */
     uint32_t *pair_val;    /* [cap] particle ids after the first tile-digit pass      */
+    uint32_t *list_tile;   /* [cap] tile id of every list entry (sorted)              */
     uint32_t *list;        /* [cap] per-tile lists: tile t = list[ranges[t] .. ranges[t+1]) */
     uint32_t *ranges;      /* [T+1]                                               */
-    int32_t *tile_diff;    /* [(tiles_y+1)*(tiles_x+1)] 2-D difference grid of rects */
-    uint32_t *hist;        /* [8][256] radix digit histograms -> exclusive offsets  */
-    uint32_t *lookback;    /* decoupled look-back scratch                         */
+    uint32_t *lookback;    /* decoupled look-back scratch (item scan)             */
     uint64_t *counters;    /* [GES_CTR_N]                                         */
     size_t zero_bytes;     /* bytes from `counters` zeroed at the start of a frame */
     /* ---- S4 / S5 ---- */

@@ -11,7 +11,8 @@
  *   S1  preprocess_f32 / preprocess_f64      (ges_geom.inc; KEYSPEC fp32 / fp64)
  *       exp_spec                              (KEYSPEC exp)
  *   S2  or_pairs_sorted: brute-force (tile, depth) keys + qsort
- *       or_tile_lists:   per-tile membership (tile in rect_i), sorted by
+ *       or_tile_lists:   per-tile membership (tile in rect_i and the tile
+ *                        reaches alpha >= 0.98/255, tile_member), sorted by
  *                        (depth bits, index)                          (R8, R11)
  *   S4  or_render_fwd:   per pixel, front-to-back alpha compositing of its
  *                        tile's list in fp64 (Eq. 3; R7, R12)
@@ -82,12 +83,33 @@ float or_exp_spec(float x) {
     return p * two_k;
 }
 
+/* KEYSPEC log for x > 1 (normal): x = m 2^e with m in [sqrt(1/2), sqrt(2));
+ * ln m = 2 atanh(s), s = (m-1)/(m+1), odd series to s^9; + e ln2. */
+float or_log_spec(float x) {
+    uint32_t bits;
+    memcpy(&bits, &x, 4);
+    int e = (int)(bits >> 23) - 127;
+    float m = f32_from_bits((bits & 0x7fffffu) | 0x3f800000u);
+    if (m > 1.41421354f) { m = m * 0.5f; e += 1; }
+    const float s = (m - 1.0f) / (m + 1.0f);
+    const float s2 = s * s;
+    float p = (float)(1.0 / 9.0);
+    p = fmaf(p, s2, (float)(1.0 / 7.0));
+    p = fmaf(p, s2, (float)(1.0 / 5.0));
+    p = fmaf(p, s2, (float)(1.0 / 3.0));
+    p = fmaf(p, s2, 1.0f);
+    float t = s * p;
+    t = t + t;
+    return fmaf((float)e, (float)0.69314718055994531, t);
+}
+
 /* ---------------- fp32 KEYSPEC instantiation ---------------- */
 #define REAL float
 #define PREAL float
 #define SFX(n) n##_f32
 #define FMA fmaf
 #define EXPF or_exp_spec
+#define LOGF or_log_spec
 #define SQRTF sqrtf
 #define FLOORF floorf
 #define CEILF ceilf
@@ -99,6 +121,7 @@ float or_exp_spec(float x) {
 #undef SFX
 #undef FMA
 #undef EXPF
+#undef LOGF
 #undef SQRTF
 #undef FLOORF
 #undef CEILF
@@ -111,6 +134,7 @@ float or_exp_spec(float x) {
 #define SFX(n) n##_f64
 #define FMA fma
 #define EXPF exp
+#define LOGF log
 #define SQRTF sqrt
 #define FLOORF floor
 #define CEILF ceil
@@ -122,6 +146,7 @@ float or_exp_spec(float x) {
 #undef SFX
 #undef FMA
 #undef EXPF
+#undef LOGF
 #undef SQRTF
 #undef FLOORF
 #undef CEILF
@@ -149,6 +174,29 @@ static int cmp_pair(const void *a, const void *b) {
     return (x->idx > y->idx) - (x->idx < y->idx);
 }
 
+/* Geometry for the tile-membership test (NULL: plain rect membership). */
+typedef struct {
+    int32_t precision;  /* 0: fp32 KEYSPEC arrays, 1: fp64 */
+    int32_t _pad;
+    int64_t P;
+    const void *uv, *conic, *kappa; /* [2][P], [3][P], [P] */
+} OrGeom;
+
+static int or_member(const OrGeom *g, int64_t i, int tx, int ty) {
+    if (!g) return 1;
+    const int64_t P = g->P;
+    if (g->precision == 0) {
+        const float *uv = (const float *)g->uv, *cn = (const float *)g->conic, *k = (const float *)g->kappa;
+        return tile_member_f32(uv[i], uv[P + i], cn[i], cn[P + i], cn[2 * P + i], k[i], tx, ty);
+    }
+    const double *uv = (const double *)g->uv, *cn = (const double *)g->conic, *k = (const double *)g->kappa;
+    return tile_member_f64(uv[i], uv[P + i], cn[i], cn[P + i], cn[2 * P + i], k[i], tx, ty);
+}
+
+int or_tile_member_f32(float u, float v, float a, float b, float c, float kappa, int tx, int ty) {
+    return tile_member_f32(u, v, a, b, c, kappa, tx, ty);
+}
+
 /* Number of (particle, tile) pairs. */
 int64_t or_count_pairs(int64_t P, const int32_t *status, const int32_t *tiles) {
     int64_t M = 0;
@@ -161,11 +209,13 @@ int64_t or_count_pairs(int64_t P, const int32_t *status, const int32_t *tiles) {
  * key = (tile_id << 32) | depth_bits, sort ascending by (key, particle index).
  * depth_bits[i] = the fp32 bit pattern of the depth (positive => monotone). */
 int64_t or_pairs_sorted(int64_t P, const int32_t *status, const int32_t *rect, const uint32_t *depth_bits,
-                        int32_t tiles_x, uint64_t *keys_out, int32_t *vals_out, int64_t cap) {
+                        const OrGeom *geom, int32_t tiles_x, uint64_t *keys_out, int32_t *vals_out, int64_t cap) {
     int64_t M = 0;
-    for (int64_t i = 0; i < P; ++i)
-        if (status[i] == OR_VISIBLE)
-            M += (int64_t)(rect[2 * P + i] - rect[i]) * (rect[3 * P + i] - rect[P + i]);
+    for (int64_t i = 0; i < P; ++i) {
+        if (status[i] != OR_VISIBLE) continue;
+        for (int ty = rect[P + i]; ty < rect[3 * P + i]; ++ty)
+            for (int tx = rect[i]; tx < rect[2 * P + i]; ++tx) M += or_member(geom, i, tx, ty);
+    }
     if (M > cap) return -M;
     OrPair *pr = (OrPair *)malloc(sizeof(OrPair) * (size_t)(M > 0 ? M : 1));
     int64_t m = 0;
@@ -173,6 +223,7 @@ int64_t or_pairs_sorted(int64_t P, const int32_t *status, const int32_t *rect, c
         if (status[i] != OR_VISIBLE) continue;
         for (int ty = rect[P + i]; ty < rect[3 * P + i]; ++ty)
             for (int tx = rect[i]; tx < rect[2 * P + i]; ++tx) {
+                if (!or_member(geom, i, tx, ty)) continue;
                 uint64_t tile = (uint64_t)ty * (uint64_t)tiles_x + (uint64_t)tx;
                 pr[m].key = (tile << 32) | (uint64_t)depth_bits[i];
                 pr[m].idx = (int32_t)i;
@@ -190,8 +241,8 @@ int64_t or_pairs_sorted(int64_t P, const int32_t *status, const int32_t *rect, c
  * offsets has T+1 entries.  If list == NULL only offsets are produced.
  * Returns the total list length. */
 int64_t or_tile_lists(int64_t P, const int32_t *status, const int32_t *rect, const uint64_t *order,
-                      int32_t tiles_x, int32_t tiles_y, const uint8_t *tile_mask, int64_t *offsets,
-                      int32_t *list, int64_t cap) {
+                      const OrGeom *geom, int32_t tiles_x, int32_t tiles_y, const uint8_t *tile_mask,
+                      int64_t *offsets, int32_t *list, int64_t cap) {
     const int64_t T = (int64_t)tiles_x * tiles_y;
     int64_t *cnt = (int64_t *)calloc((size_t)T + 1, sizeof(int64_t));
     for (int64_t i = 0; i < P; ++i) {
@@ -199,7 +250,7 @@ int64_t or_tile_lists(int64_t P, const int32_t *status, const int32_t *rect, con
         for (int ty = rect[P + i]; ty < rect[3 * P + i]; ++ty)
             for (int tx = rect[i]; tx < rect[2 * P + i]; ++tx) {
                 int64_t tile = (int64_t)ty * tiles_x + tx;
-                if (!tile_mask || tile_mask[tile]) cnt[tile]++;
+                if ((!tile_mask || tile_mask[tile]) && or_member(geom, i, tx, ty)) cnt[tile]++;
             }
     }
     offsets[0] = 0;
@@ -215,6 +266,7 @@ int64_t or_tile_lists(int64_t P, const int32_t *status, const int32_t *rect, con
             for (int tx = rect[i]; tx < rect[2 * P + i]; ++tx) {
                 int64_t tile = (int64_t)ty * tiles_x + tx;
                 if (tile_mask && !tile_mask[tile]) continue;
+                if (!or_member(geom, i, tx, ty)) continue;
                 pr[cnt[tile]].key = order[i];
                 pr[cnt[tile]].idx = (int32_t)i;
                 cnt[tile]++;
@@ -488,10 +540,11 @@ int or_backward_particles(const OrParticles_f64 *pp, const OrCamera *cam, const 
     if (!status_in || !flags_in) {
         OrPre_f64 pre;
         double *buf = (double *)calloc((size_t)P * 16, sizeof(double));
-        int32_t *ib = (int32_t *)calloc((size_t)P * 9, sizeof(int32_t));
+        int32_t *ib = (int32_t *)calloc((size_t)P * 13, sizeof(int32_t));
         pre.depth = buf; pre.uv = buf + P; pre.conic = buf + 3 * P; pre.cov2d = buf + 6 * P;
         pre.kappa = buf + 9 * P; pre.rgb = buf + 10 * P;
         pre.radius = ib; pre.rect = ib + P; pre.tiles = ib + 5 * P; pre.status = ib + 6 * P; pre.flags = ib + 7 * P;
+        pre.rect3 = ib + 8 * P;
         preprocess_f64(pp, cam, st, &pre);
         st64 = (int32_t *)malloc(sizeof(int32_t) * (size_t)P);
         fl64 = (int32_t *)malloc(sizeof(int32_t) * (size_t)P);
@@ -651,4 +704,8 @@ void or_set_num_threads(int n) {
 /* Vectorised helpers for the pins. */
 void or_exp_spec_array(const float *x, float *y, int64_t n) {
     for (int64_t i = 0; i < n; ++i) y[i] = or_exp_spec(x[i]);
+}
+
+void or_log_spec_array(const float *x, float *y, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) y[i] = or_log_spec(x[i]);
 }

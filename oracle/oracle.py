@@ -69,7 +69,7 @@ def _particles_struct(ctype):
 def _pre_struct(ctype):
     class _Pre(C.Structure):
         _fields_ = [(n, C.POINTER(ctype)) for n in ("depth", "uv", "conic", "cov2d", "kappa", "rgb")] + [
-            (n, C.POINTER(C.c_int32)) for n in ("radius", "rect", "tiles", "status", "flags")]
+            (n, C.POINTER(C.c_int32)) for n in ("radius", "rect", "rect3", "tiles", "status", "flags")]
     return _Pre
 
 
@@ -80,6 +80,11 @@ _PreF32, _PreF64 = _pre_struct(C.c_float), _pre_struct(C.c_double)
 class _Screen(C.Structure):
     _fields_ = [("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
                 ("bg", C.c_double * 3)]
+
+
+class _Geom(C.Structure):
+    _fields_ = [("precision", C.c_int32), ("_pad", C.c_int32), ("P", C.c_int64), ("uv", C.c_void_p),
+                ("conic", C.c_void_p), ("kappa", C.c_void_p)]
 
 
 class _Splat2D(C.Structure):
@@ -183,13 +188,13 @@ def preprocess(parts, cam, st: Settings, precision: str = "f32") -> dict:
     out = {
         "depth": np.zeros(P, dtype), "uv": np.zeros((2, P), dtype), "conic": np.zeros((3, P), dtype),
         "cov2d": np.zeros((3, P), dtype), "kappa": np.zeros(P, dtype), "rgb": np.zeros((3, P), dtype),
-        "radius": np.zeros(P, np.int32), "rect": np.zeros((4, P), np.int32), "tiles": np.zeros(P, np.int32),
-        "status": np.zeros(P, np.int32), "flags": np.zeros(P, np.int32),
+        "radius": np.zeros(P, np.int32), "rect": np.zeros((4, P), np.int32), "rect3": np.zeros((4, P), np.int32),
+        "tiles": np.zeros(P, np.int32), "status": np.zeros(P, np.int32), "flags": np.zeros(P, np.int32),
     }
     pre = (_PreF32 if precision == "f32" else _PreF64)()
     for n in ("depth", "uv", "conic", "cov2d", "kappa", "rgb"):
         setattr(pre, n, _ptr(out[n], ct))
-    for n in ("radius", "rect", "tiles", "status", "flags"):
+    for n in ("radius", "rect", "rect3", "tiles", "status", "flags"):
         setattr(pre, n, _ptr(out[n], C.c_int32))
     c, s = _cam(cam), _settings(st)
     fn = lib().or_preprocess_f32 if precision == "f32" else lib().or_preprocess_f64
@@ -217,22 +222,60 @@ def count_pairs(pre) -> int:
                                     _ptr(pre["tiles"], C.c_int32)))
 
 
-def pairs_sorted(pre):
+MEMBERSHIPS = ("rect", "exact", "all", "sigma3")
+
+
+def _membership(pre, membership):
+    """(status, rect, tile-test geometry or None) of a membership rule:
+    'rect'   = the R10 rect (the tight alpha >= 0.98/255 box; the kernel's rule),
+    'exact'  = R10 rect AND the tile itself reaches alpha >= 0.98/255 (R8 test),
+    'all'    = every particle that passed the geometric tests, in every tile
+               (the definitional sum of Eq. 3 with the alpha skip; brute force),
+    'sigma3' = the inherited 3-sigma rect (R7; a different, truncating rule).
+    'rect', 'exact' and 'all' give identical images and gradients (pinned in
+    test_oracle_pins)."""
+    assert membership in MEMBERSHIPS, membership
+    st = pre["status"]
+    if membership == "sigma3":
+        return st, np.ascontiguousarray(pre["rect3"]), None
+    if membership == "all":
+        st = np.where(st == OFFSCREEN, VISIBLE, st).astype(np.int32)
+        rect = np.zeros_like(pre["rect"])
+        rect[2], rect[3] = pre["tiles_x"], pre["tiles_y"]
+        return st, rect, None
+    if membership == "rect":
+        return st, pre["rect"], None
+    g = _Geom()
+    g.precision = 0 if pre["precision"] == "f32" else 1
+    g.P = pre["status"].size
+    g.uv, g.conic, g.kappa = pre["uv"].ctypes.data, pre["conic"].ctypes.data, pre["kappa"].ctypes.data
+    return st, pre["rect"], g
+
+
+def _rect_pairs(status, rect) -> int:
+    vis = status == VISIBLE
+    area = (rect[2] - rect[0]).astype(np.int64) * (rect[3] - rect[1]).astype(np.int64)
+    return int(area[vis].sum())
+
+
+def pairs_sorted(pre, membership="rect"):
     """All (key, particle) pairs sorted by (key, index); key = tile<<32 | depth bits."""
     assert pre["precision"] == "f32"
     P = pre["status"].size
-    M = count_pairs(pre)
+    st, rect, g = _membership(pre, membership)
+    M = _rect_pairs(st, rect)  # rect pairs: an upper bound
     keys = np.zeros(max(M, 1), np.uint64)
     vals = np.zeros(max(M, 1), np.int32)
     db = np.ascontiguousarray(pre["depth"].view(np.uint32))
-    got = lib().or_pairs_sorted(C.c_int64(P), _ptr(pre["status"], C.c_int32), _ptr(pre["rect"], C.c_int32),
-                                _ptr(db, C.c_uint32), C.c_int32(pre["tiles_x"]), _ptr(keys, C.c_uint64),
-                                _ptr(vals, C.c_int32), C.c_int64(keys.size))
-    assert got == M, (got, M)
-    return keys[:M], vals[:M]
+    got = lib().or_pairs_sorted(C.c_int64(P), _ptr(st, C.c_int32), _ptr(rect, C.c_int32),
+                                _ptr(db, C.c_uint32), C.byref(g) if g is not None else None,
+                                C.c_int32(pre["tiles_x"]), _ptr(keys, C.c_uint64), _ptr(vals, C.c_int32),
+                                C.c_int64(keys.size))
+    assert 0 <= got <= M, (got, M)
+    return keys[:got], vals[:got]
 
 
-def tile_lists(pre, tile_mask: Optional[np.ndarray] = None):
+def tile_lists(pre, tile_mask: Optional[np.ndarray] = None, membership="rect"):
     """Per-tile membership lists sorted by (depth key, index): (offsets[T+1], list)."""
     P = pre["status"].size
     T = pre["tiles_x"] * pre["tiles_y"]
@@ -242,8 +285,10 @@ def tile_lists(pre, tile_mask: Optional[np.ndarray] = None):
     if tile_mask is not None:
         tile_mask = np.ascontiguousarray(tile_mask, dtype=np.uint8)
         mask_p = _ptr(tile_mask, C.c_uint8)
-    args = (C.c_int64(P), _ptr(pre["status"], C.c_int32), _ptr(pre["rect"], C.c_int32), _ptr(order, C.c_uint64),
-            C.c_int32(pre["tiles_x"]), C.c_int32(pre["tiles_y"]), mask_p, _ptr(offsets, C.c_int64))
+    st, rect, g = _membership(pre, membership)
+    args = (C.c_int64(P), _ptr(st, C.c_int32), _ptr(rect, C.c_int32), _ptr(order, C.c_uint64),
+            C.byref(g) if g is not None else None, C.c_int32(pre["tiles_x"]), C.c_int32(pre["tiles_y"]), mask_p,
+            _ptr(offsets, C.c_int64))
     total = lib().or_tile_lists(*args, None, C.c_int64(0))
     lst = np.zeros(max(total, 1), np.int32)
     got = lib().or_tile_lists(*args, _ptr(lst, C.c_int32), C.c_int64(lst.size))
@@ -341,20 +386,21 @@ def split_planes(flat, K):
 # ---------------------------------------------------------------------------
 # whole pipeline
 # ---------------------------------------------------------------------------
-def render(parts, cam, st: Settings, precision: str = "f32", tile_mask=None) -> dict:
+def render(parts, cam, st: Settings, precision: str = "f32", tile_mask=None, membership="rect") -> dict:
     """Definitional forward: S1 in `precision`, membership + depth sort, fp64
     compositing.  Returns the preprocess dict merged with the image outputs."""
     pre = preprocess(parts, cam, st, precision)
-    offsets, lst = tile_lists(pre, tile_mask)
+    offsets, lst = tile_lists(pre, tile_mask, membership)
     out = render_fwd(pre, cam, st, offsets, lst, tile_mask)
     out.update(pre=pre, offsets=offsets, list=lst)
     return out
 
 
-def render_and_grad(parts, cam, st: Settings, dL_dimg, precision: str = "f32", tile_mask=None) -> dict:
+def render_and_grad(parts, cam, st: Settings, dL_dimg, precision: str = "f32", tile_mask=None,
+                    membership="rect") -> dict:
     """Forward + full backward.  Decisions (visibility, clamps, membership) are
     taken in `precision`; compositing and adjoints are fp64."""
-    out = render(parts, cam, st, precision, tile_mask)
+    out = render(parts, cam, st, precision, tile_mask, membership)
     pre = out["pre"]
     g2d = render_bwd(pre, cam, st, out["offsets"], out["list"], dL_dimg, tile_mask)
     grads = backward_particles(parts, cam, st, g2d, pre["status"], pre["flags"])
@@ -366,6 +412,14 @@ def loss_f64(parts, cam, st: Settings, dL_dimg) -> float:
     """L = <dL/dimage, image> of the all-fp64 pipeline (for finite differences)."""
     out = render(parts, cam, st, "f64")
     return float(np.sum(out["image"] * dL_dimg))
+
+
+def log_spec(x) -> np.ndarray:
+    """The KEYSPEC natural log (ges_oracle.c or_log_spec), elementwise, x > 1."""
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.zeros_like(x)
+    lib().or_log_spec_array(_ptr(x, C.c_float), _ptr(y, C.c_float), C.c_int64(x.size))
+    return y
 
 
 def exp_spec(x) -> np.ndarray:

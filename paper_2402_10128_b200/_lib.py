@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, "libges.so")
 GES_OK, GES_ERR_INVALID_ARG, GES_ERR_CAPACITY, GES_ERR_CUDA, GES_ERR_UNSUPPORTED = range(5)
 GES_PHI_SCALE, GES_PHI_VARIANCE = 0, 1
 GES_VISIBLE, GES_CULL_NEAR, GES_DEGENERATE, GES_OFFSCREEN = range(4)
-GES_CTR_VISIBLE, GES_CTR_PAIRS, GES_CTR_OVERFLOW, GES_CTR_TILE0, GES_CTR_N = 0, 1, 2, 3, 16
+GES_CTR_VISIBLE, GES_CTR_PAIRS, GES_CTR_OVERFLOW, GES_CTR_SLOTS, GES_CTR_TICKET, GES_CTR_N = 0, 1, 2, 3, 4, 16
 
 _fp = C.POINTER(C.c_float)
 _u32p = C.POINTER(C.c_uint32)
@@ -45,8 +45,8 @@ class ges_grads(C.Structure):
 
 
 class ges_counts(C.Structure):
-    _fields_ = [("visible", C.c_int64), ("pairs", C.c_int64), ("capacity", C.c_int64), ("overflow", C.c_int32),
-                ("_pad", C.c_int32)]
+    _fields_ = [("visible", C.c_int64), ("pairs", C.c_int64), ("slots", C.c_int64), ("capacity", C.c_int64),
+                ("overflow", C.c_int32), ("_pad", C.c_int32)]
 
 
 class ges_frame(C.Structure):
@@ -57,9 +57,9 @@ class ges_frame(C.Structure):
         ("depth", C.c_void_p), ("pay0", C.c_void_p), ("pay1", C.c_void_p), ("pay2", C.c_void_p),
         ("radius", C.c_void_p), ("rect", C.c_void_p), ("status", C.c_void_p), ("flags", C.c_void_p),
         ("vis_key", C.c_void_p * 2), ("vis_val", C.c_void_p * 2), ("sorted_vis", C.c_void_p),
-        ("radix_hist", C.c_void_p), ("radix_total", C.c_void_p), ("item_offset", C.c_void_p), ("item_rec", C.c_void_p), ("tile_first", C.c_void_p), ("pair_tile", C.c_void_p),
-        ("pair_val", C.c_void_p), ("list", C.c_void_p),
-        ("ranges", C.c_void_p), ("tile_diff", C.c_void_p), ("hist", C.c_void_p), ("lookback", C.c_void_p),
+        ("radix_hist", C.c_void_p), ("radix_total", C.c_void_p), ("item_offset", C.c_void_p), ("item_rec", C.c_void_p),
+        ("tile_first", C.c_void_p), ("pair_tile", C.c_void_p), ("pair_val", C.c_void_p),
+        ("list_tile", C.c_void_p), ("list", C.c_void_p), ("ranges", C.c_void_p), ("lookback", C.c_void_p),
         ("counters", C.c_void_p), ("zero_bytes", C.c_size_t),
         ("final_T", C.c_void_p), ("n_contrib", C.c_void_p), ("grad2d", C.c_void_p),
         ("workspace_bytes", C.c_size_t),

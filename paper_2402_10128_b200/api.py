@@ -220,7 +220,7 @@ class Renderer:
             cnt = self.frame.counts(stream)
             if not cnt.overflow:
                 break
-            self.grow(cnt.pairs)
+            self.grow(cnt.slots)
         return image
 
     def backward(self, particles: PlanarParams, camera, settings: Settings, dL_dimage: torch.Tensor,

@@ -60,11 +60,9 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     ges_frame g;
     std::memset(&g, 0, sizeof(g));
     g.P = P; g.pair_capacity = cap; g.width = W; g.height = H; g.tiles_x = tx; g.tiles_y = ty;
-    g.num_tiles = (int32_t)T; g.tile_bits = bits_for(T); g.sh_degree_max = 3;
+    g.num_tiles = (int32_t)T; g.tile_bits = std::max(1, bits_for(T)); g.sh_degree_max = 3;
     // --- zero-per-frame region (one memset in ges_preprocess) ---
     g.counters = (uint64_t*)take(sizeof(uint64_t) * GES_CTR_N);
-    g.hist = (uint32_t*)take(sizeof(uint32_t) * 8 * 256);
-    g.tile_diff = (int32_t*)take(sizeof(int32_t) * (size_t)(tx + 1) * (ty + 1));
     g.lookback = (uint32_t*)take(sizeof(uint32_t) * L.total);
     g.zero_bytes = off;  // bytes of the zero region from the workspace base
     // --- per particle ---
@@ -82,12 +80,13 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     }
     g.sorted_vis = g.vis_val[0];
     g.radix_hist = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * (size_t)radix_tiles(std::max<int64_t>(P, cap)));
-    g.radix_total = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits);
+    g.radix_total = (uint32_t*)take(sizeof(uint32_t) * 2 * kRadixDigits);
     g.item_offset = (uint32_t*)take(sizeof(uint32_t) * P);
     g.item_rec = (uint32_t*)take(16 * (size_t)P);
     g.tile_first = (uint32_t*)take(sizeof(uint32_t) * (size_t)slot_tiles(cap));
     g.pair_tile = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
     g.pair_val = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
+    g.list_tile = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
     g.list = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
     g.ranges = (uint32_t*)take(sizeof(uint32_t) * (size_t)(T + 1));
     g.final_T = (float*)take(sizeof(float) * HW);
@@ -138,7 +137,7 @@ ges_status ges_frame_init(void* workspace, size_t bytes, int64_t P, int32_t widt
         return GES_ERR_INVALID_ARG;
     if (((uintptr_t)workspace) % kAlign) return GES_ERR_INVALID_ARG;
     const int tx = tiles_of(width), ty = tiles_of(height);
-    if ((int64_t)tx * ty > 65536 || ranges_smem_bytes(tx, ty) > 200 * 1024) return GES_ERR_INVALID_ARG;
+    if ((int64_t)tx * ty > 65536) return GES_ERR_INVALID_ARG;
     if (bytes < layout(nullptr, P, width, height, pair_capacity, nullptr)) return GES_ERR_CAPACITY;
     layout((char*)workspace, P, width, height, pair_capacity, frame);
     return GES_OK;
@@ -161,7 +160,6 @@ ges_status ges_preprocess(const ges_particles* particles, const ges_camera* came
     a.depth = frame->depth; a.pay0 = (float4*)frame->pay0; a.pay1 = (float4*)frame->pay1; a.pay2 = frame->pay2;
     a.radius = frame->radius; a.rect = (ushort4*)frame->rect; a.status = frame->status; a.flags = frame->flags;
     a.vis_key = frame->vis_key[0];
-    a.tile_diff = frame->tile_diff; a.hist = frame->hist;
     a.counters = (unsigned long long*)frame->counters;
     return cuda_status(launch_preprocess(a, s));
 }
@@ -171,12 +169,8 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long* ctr = (unsigned long long*)frame->counters;
     const LookbackLayout L = lookback_layout(frame->P, frame->pair_capacity);
-    RangesArgs r;
-    r.tile_diff = frame->tile_diff; r.tiles_x = frame->tiles_x; r.tiles_y = frame->tiles_y;
-    r.tile_bits = frame->tile_bits; r.ranges = frame->ranges; r.hist = frame->hist; r.counters = ctr;
-    r.capacity = frame->pair_capacity;
-    cudaError_t e = launch_ranges(r, s);
-    if (e != cudaSuccess) return GES_ERR_CUDA;
+    const int64_t hist_stride = radix_tiles(std::max<int64_t>(frame->P, frame->pair_capacity));
+    cudaError_t e;
     // depth sort: pass 0 reads all P keys and drops the non-visible ones (compaction);
     // ping-pong (vis_key[0]) -> 1 -> 0 -> 1 -> (vis_val[0])
     for (int d = 0; d < 4; ++d) {
@@ -191,7 +185,7 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
         p.count = (d == 0) ? nullptr : ctr + GES_CTR_VISIBLE;
         p.max_items = frame->P;
         p.tile_hist = frame->radix_hist;
-        p.hist_stride = radix_tiles(std::max<int64_t>(frame->P, frame->pair_capacity));
+        p.hist_stride = hist_stride;
         p.digit_total = frame->radix_total;
         p.shift = 8 * d;
         p.digit_bits = 8;
@@ -199,27 +193,30 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
         if ((e = launch_radix_pass(p, s)) != cudaSuccess) return GES_ERR_CUDA;
     }
     frame->sorted_vis = frame->vis_val[0];
-    // first pair slot of every sorted particle
+    // pair slots of every sorted particle (rect areas), capacity check
     ItemScanArgs is;
     is.sorted_vis = frame->sorted_vis; is.rect = (const ushort4*)frame->rect; is.counters = ctr;
-    is.E = frame->item_offset; is.items = (uint4*)frame->item_rec; is.tile_first = frame->tile_first; is.lookback = frame->lookback + L.scan;
-    is.tile_counter = ctr + GES_CTR_TILE0;
+    is.capacity = frame->pair_capacity;
+    is.E = frame->item_offset; is.items = (uint4*)frame->item_rec; is.tile_first = frame->tile_first;
+    is.lookback = frame->lookback + L.scan; is.tile_counter = ctr + GES_CTR_TICKET;
     if ((e = launch_item_scan(is, frame->P, s)) != cudaSuccess) return GES_ERR_CUDA;
-    // stable sort of the pairs by tile id; the first pass generates the pairs
+    // stable sort of the pairs by tile id; the first pass generates them
     const int passes = frame->tile_bits <= 8 ? 1 : 2;
     for (int d = 0; d < passes; ++d) {
         RadixPassArgs p;
         std::memset(&p, 0, sizeof(p));
+        const bool last = d + 1 == passes;
         p.gen = (d == 0) ? 1 : 0;
         p.keys_in = (d == 0) ? nullptr : frame->pair_tile;
         p.vals_in = (d == 0) ? nullptr : frame->pair_val;
-        p.keys_out = (d + 1 < passes) ? frame->pair_tile : nullptr;
-        p.vals_out = (d + 1 < passes) ? frame->pair_val : frame->list;
-        p.count = ctr + GES_CTR_PAIRS;
+        p.keys_out = last ? frame->list_tile : frame->pair_tile;
+        p.vals_out = last ? frame->list : frame->pair_val;
+        p.count = (d == 0) ? ctr + GES_CTR_SLOTS : nullptr;
+        p.count_totals = (d == 0) ? nullptr : frame->radix_total;  // pairs of pass 1
         p.max_items = frame->pair_capacity;
         p.tile_hist = frame->radix_hist;
-        p.hist_stride = radix_tiles(std::max<int64_t>(frame->P, frame->pair_capacity));
-        p.digit_total = frame->radix_total;
+        p.hist_stride = hist_stride;
+        p.digit_total = frame->radix_total + (d & 1) * kRadixDigits;
         p.shift = 8 * d;
         p.digit_bits = std::max(1, std::min(8, frame->tile_bits - 8 * d));
         p.overflow = ctr + GES_CTR_OVERFLOW;
@@ -232,6 +229,12 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
         p.counters = ctr;
         if ((e = launch_radix_pass(p, s)) != cudaSuccess) return GES_ERR_CUDA;
     }
+    RangesArgs r;
+    r.keys = frame->list_tile;
+    r.count_totals = frame->radix_total;  // pass 1's totals = all pairs
+    r.tiles_x = frame->tiles_x; r.tiles_y = frame->tiles_y;
+    r.ranges = frame->ranges; r.counters = ctr; r.max_pairs = frame->pair_capacity;
+    if ((e = launch_ranges(r, s)) != cudaSuccess) return GES_ERR_CUDA;
     return GES_OK;
 }
 
@@ -300,6 +303,7 @@ ges_status ges_counts_get(const ges_frame* frame, ges_counts* host_out, void* st
     if (cudaStreamSynchronize(s) != cudaSuccess) return GES_ERR_CUDA;
     host_out->visible = (int64_t)c[GES_CTR_VISIBLE];
     host_out->pairs = (int64_t)c[GES_CTR_PAIRS];
+    host_out->slots = (int64_t)c[GES_CTR_SLOTS];
     host_out->capacity = frame->pair_capacity;
     host_out->overflow = (int32_t)c[GES_CTR_OVERFLOW];
     host_out->_pad = 0;

@@ -49,6 +49,25 @@ __device__ __forceinline__ float exp_spec(float x) {
     return fmul(p, __uint_as_float((uint32_t)(ki + 127) << 23));
 }
 
+// KEYSPEC log for normal x > 1: x = m 2^e, m folded into [sqrt(1/2), sqrt(2)];
+// ln m = 2 atanh(s), s = (m-1)/(m+1), odd Horner chain to s^9; + e ln2.
+__device__ __forceinline__ float log_spec(float x) {
+    const uint32_t bits = __float_as_uint(x);
+    int e = (int)(bits >> 23) - 127;
+    float m = __uint_as_float((bits & 0x7fffffu) | 0x3f800000u);
+    if (m > 1.41421354f) { m = fmul(m, 0.5f); e += 1; }
+    const float s = fdiv(fsub(m, 1.0f), fadd(m, 1.0f));
+    const float s2 = fmul(s, s);
+    float p = (float)(1.0 / 9.0);
+    p = ffma(p, s2, (float)(1.0 / 7.0));
+    p = ffma(p, s2, (float)(1.0 / 5.0));
+    p = ffma(p, s2, (float)(1.0 / 3.0));
+    p = ffma(p, s2, 1.0f);
+    float t = fmul(s, p);
+    t = fadd(t, t);
+    return ffma((float)e, (float)0.69314718055994531, t);
+}
+
 // Real spherical harmonics up to degree 3 (Condon-Shortley phase), index
 // k = l^2 + l + m, KEYSPEC op order.
 struct SHConst {

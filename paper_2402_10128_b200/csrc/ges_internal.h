@@ -24,36 +24,26 @@ struct PreprocessArgs {
     uint8_t* status;
     uint8_t* flags;
     uint32_t* vis_key;    // [P] depth bits, 0xffffffff if not visible
-    int32_t* tile_diff;
-    uint32_t* hist;       // [4][256] depth digits
     unsigned long long* counters;
 };
 
 cudaError_t launch_preprocess(const PreprocessArgs& a, cudaStream_t stream);
 
 // --- sort / ranges ---------------------------------------------------------
-struct RangesArgs {
-    const int32_t* tile_diff;
-    int tiles_x, tiles_y, tile_bits;
-    uint32_t* ranges;                 // [T+1]
-    uint32_t* hist;                   // [8][256]: 0-3 depth digits (in: counts, out: offsets), 4-5 tile digits
-    unsigned long long* counters;
-    int64_t capacity;
-};
-cudaError_t launch_ranges(const RangesArgs& a, cudaStream_t stream);
-int ranges_smem_bytes(int tiles_x, int tiles_y);  // must be <= 200 KB
 int num_sms();
+constexpr int kRadixDigits = 256;
 
 struct RadixPassArgs {
     const uint32_t* keys_in;
     const uint32_t* vals_in;          // null: the value is the input index
-    uint32_t* keys_out;               // may be null (last pass)
+    uint32_t* keys_out;               // may be null
     uint32_t* vals_out;
     const unsigned long long* count;  // device item count (null: max_items)
+    const uint32_t* count_totals;     // non-null: item count = sum of these 256 digit totals
     int64_t max_items;                // upper bound (grid sizing); items beyond are ignored
     uint32_t* tile_hist;              // [256][hist_stride] per-tile digit counts -> offsets (digit-major)
     int64_t hist_stride;              // >= number of tiles
-    uint32_t* digit_total;            // [256] column totals
+    uint32_t* digit_total;            // [256] column totals of this pass
     int shift;
     int digit_bits;                   // bits of the digit that can be non-zero (1..8)
     int drop_invalid;                 // 1: keys == 0xffffffff are dropped (compaction)
@@ -70,12 +60,12 @@ struct RadixPassArgs {
 };
 cudaError_t launch_radix_pass(const RadixPassArgs& a, cudaStream_t stream);
 int64_t radix_tiles(int64_t n);
-constexpr int kRadixDigits = 256;
 
 struct ItemScanArgs {
     const uint32_t* sorted_vis;
     const ushort4* rect;
-    const unsigned long long* counters;
+    unsigned long long* counters;     // reads VISIBLE; writes SLOTS, OVERFLOW
+    int64_t capacity;
     uint32_t* E;                      // [P]
     uint4* items;                     // [P] packed (E, particle, rect x0|y0<<16, x1|y1<<16)
     uint32_t* tile_first;             // [cap/4096 + 2]
@@ -85,6 +75,16 @@ struct ItemScanArgs {
 cudaError_t launch_item_scan(const ItemScanArgs& a, int64_t max_items, cudaStream_t stream);
 int64_t item_scan_tiles(int64_t n);
 int64_t slot_tiles(int64_t cap);
+
+struct RangesArgs {
+    const uint32_t* keys;             // [M] sorted tile ids
+    const uint32_t* count_totals;     // M = sum of these 256 digit totals
+    int tiles_x, tiles_y;
+    uint32_t* ranges;                 // [T+1]
+    unsigned long long* counters;     // writes PAIRS
+    int64_t max_pairs;
+};
+cudaError_t launch_ranges(const RangesArgs& a, cudaStream_t stream);
 
 // --- render ----------------------------------------------------------------
 constexpr int kGrad2dStride = 12;  // floats per particle in grad2d (3 x float4)

@@ -1,7 +1,5 @@
 // preprocess.cu -- S1: per-particle projection of GES
-// particles, fused with the depth keys and digit histograms of the following
-// radix sort and the 2-D difference grid of the particles' tile rects
-// (-> per-tile pair counts).
+// particles and the depth keys of the following radix sort.
 //
 // Paper: Eq. 2 kernel and Sigma; PAPER.md:249-254 EWA
 // Sigma' = J W Sigma W^T J^T with Sigma = R S S^T R^T and S "modified by"
@@ -149,16 +147,28 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
     const float rad = ceilf(fmul(3.0f, fsqrt(lam)));
     const float u = ffma(c.fx, xn, c.cx), v = ffma(c.fy, yn, c.cy);
     if (!isfinite(u) || !isfinite(v) || !isfinite(rad)) { o.status = GES_DEGENERATE; return o; }
-    const float fx0 = floorf(fmul(fsub(u, rad), 0.0625f));
-    const float fx1 = fadd(floorf(fmul(fadd(u, rad), 0.0625f)), 1.0f);
-    const float fy0 = floorf(fmul(fsub(v, rad), 0.0625f));
-    const float fy1 = fadd(floorf(fmul(fadd(v, rad), 0.0625f)), 1.0f);
+    // rect (R10): tiles whose pixel centres meet the bounding box of
+    // the ellipse kappa exp(-Q/2) >= 0.98/255: half-extents sqrt(Q_thr A),
+    // sqrt(Q_thr C) with Q_thr = 2 ln(255 kappa / 0.98).
+    const float kap = fdiv(1.0f, fadd(1.0f, exp_spec(-in.logit)));
+    const float kr = fdiv(fmul(kap, 255.0f), 0.98f);
+    float qthr = 0.0f;
+    if (kr > 1.0f) { qthr = log_spec(kr); qthr = fadd(qthr, qthr); }
+    const float ex = fsqrt(fmul(qthr, A)), ey = fsqrt(fmul(qthr, C));
+    const float fx0 = ceilf(fmul(fsub(fsub(u, ex), 15.5f), 0.0625f));
+    const float fx1 = fadd(floorf(fmul(fsub(fadd(u, ex), 0.5f), 0.0625f)), 1.0f);
+    const float fy0 = ceilf(fmul(fsub(fsub(v, ey), 15.5f), 0.0625f));
+    const float fy1 = fadd(floorf(fmul(fsub(fadd(v, ey), 0.5f), 0.0625f)), 1.0f);
     const float ftx = (float)c.tiles_x, fty = (float)c.tiles_y;
     o.x0 = (int)fminf(fmaxf(fx0, 0.0f), ftx);
     o.x1 = (int)fminf(fmaxf(fx1, 0.0f), ftx);
     o.y0 = (int)fminf(fmaxf(fy0, 0.0f), fty);
     o.y1 = (int)fminf(fmaxf(fy1, 0.0f), fty);
+    if (o.x1 < o.x0) o.x1 = o.x0;
+    if (o.y1 < o.y0) o.y1 = o.y0;
+    if (!(kr > 1.0f)) o.x1 = o.x0;
     o.u = u; o.v = v; o.ca = ca; o.cb = cb; o.cc = ccn;
+    o.kappa = kap;
     o.radius = (int)rad;
     if ((o.x1 - o.x0) * (o.y1 - o.y0) == 0) { o.status = GES_OFFSCREEN; return o; }
 
@@ -179,7 +189,6 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
         rgb[ch] = acc;
     }
     o.r = rgb[0]; o.g = rgb[1]; o.b = rgb[2];
-    o.kappa = fdiv(1.0f, fadd(1.0f, exp_spec(-in.logit)));
     o.flags = fl;
     o.status = GES_VISIBLE;
     return o;
@@ -188,51 +197,33 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
 constexpr int kPreThreads = 256;
 
 // Grid-stride over particles: no cross-CTA dependency.  Every particle writes
-// its sort key (fp32 depth bits, or 0xffffffff when not visible -- dropped by
-// depth pass 0, which thereby compacts the visible set), its S1 state, and,
-// if visible, +/-1 into the 2-D difference grid of tile rects (-> per-tile
-// pair counts) and the four depth-digit histograms (block-aggregated).
+// its S1 state and its sort key (fp32 depth bits, or 0xffffffff when not
+// visible -- dropped by depth pass 0, which thereby compacts the visible set).
 template <int K>
 __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(PreprocessArgs a) {
-    __shared__ uint32_t s_hist[4][256];
-    const int tid = threadIdx.x;
-    for (int k = tid; k < 4 * 256; k += kPreThreads) (&s_hist[0][0])[k] = 0;
-    __syncthreads();
+    const int tid = threadIdx.x, lane = tid & 31;
     const CamDerived cd = derive_camera(a.cam);
-    const int stride_diff = a.cam.tiles_x + 1;
-    for (int i = blockIdx.x * kPreThreads + tid; i < a.P; i += gridDim.x * kPreThreads) {
-        const ParamIn in = load_params(a, i);
-        const PreOut o = preprocess_one<K>(a, cd, i, in);
-        a.depth[i] = o.depth;
-        a.pay0[i] = make_float4(o.u, o.v, o.ca, o.cb);
-        a.pay1[i] = make_float4(o.cc, o.kappa, o.r, o.g);
-        a.pay2[i] = o.b;
-        a.radius[i] = o.radius;
-        a.rect[i] = make_ushort4((uint16_t)o.x0, (uint16_t)o.y0, (uint16_t)o.x1, (uint16_t)o.y1);
-        a.status[i] = o.status;
-        a.flags[i] = o.flags;
-        uint32_t key = 0xffffffffu;
-        if (o.status == GES_VISIBLE) {
-            key = __float_as_uint(o.depth);
-#pragma unroll
-            for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(key >> (8 * d)) & 255u], 1u);
-            atomicAdd(&a.tile_diff[o.y0 * stride_diff + o.x0], 1);
-            atomicAdd(&a.tile_diff[o.y0 * stride_diff + o.x1], -1);
-            atomicAdd(&a.tile_diff[o.y1 * stride_diff + o.x0], -1);
-            atomicAdd(&a.tile_diff[o.y1 * stride_diff + o.x1], 1);
-        }
-        a.vis_key[i] = key;
-    }
-    __syncthreads();
     uint32_t nvis = 0;
-    for (int k = tid; k < 4 * 256; k += kPreThreads) {
-        const uint32_t h = (&s_hist[0][0])[k];
-        if (k < 256) nvis += h;
-        if (h) atomicAdd(&a.hist[k], h);
+    for (int base = blockIdx.x * kPreThreads; base < a.P; base += gridDim.x * kPreThreads) {
+        const int i = base + tid;
+        bool vis = false;
+        if (i < a.P) {
+            const ParamIn in = load_params(a, i);
+            const PreOut o = preprocess_one<K>(a, cd, i, in);
+            a.depth[i] = o.depth;
+            a.pay0[i] = make_float4(o.u, o.v, o.ca, o.cb);
+            a.pay1[i] = make_float4(o.cc, o.kappa, o.r, o.g);
+            a.pay2[i] = o.b;
+            a.radius[i] = o.radius;
+            a.rect[i] = make_ushort4((uint16_t)o.x0, (uint16_t)o.y0, (uint16_t)o.x1, (uint16_t)o.y1);
+            a.status[i] = o.status;
+            a.flags[i] = o.flags;
+            vis = o.status == GES_VISIBLE;
+            a.vis_key[i] = vis ? __float_as_uint(o.depth) : 0xffffffffu;
+        }
+        nvis += __popc(__ballot_sync(0xffffffffu, vis));
     }
-    // visible count = sum of the digit-0 histogram
-    for (int o = 16; o > 0; o >>= 1) nvis += __shfl_xor_sync(0xffffffffu, nvis, o);
-    if ((tid & 31) == 0 && nvis) atomicAdd(&a.counters[GES_CTR_VISIBLE], (unsigned long long)nvis);
+    if (lane == 0 && nvis) atomicAdd(&a.counters[GES_CTR_VISIBLE], (unsigned long long)nvis);
 }
 
 cudaError_t launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {

@@ -157,7 +157,7 @@ __device__ __forceinline__ void stage_batch(const float4* pay0, const float4* pa
     }
 }
 
-template <int PPT>
+template <int PPT, bool DIAG>
 __global__ void __launch_bounds__(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdArgs a) {
     using Lt = Layout<PPT>;
     __shared__ float4 s_g0[kBatch];
@@ -208,14 +208,14 @@ __global__ void __launch_bounds__(Layout<PPT>::kThreads) render_fwd_kernel(Rende
                 const bool stop = live && Tn < kTMin;
                 const bool comp = live && !stop;
                 done |= (stop ? 1u : 0u) << k;
-                n_eval[k] = stop ? pos1 : n_eval[k];
+                if (DIAG) n_eval[k] = stop ? pos1 : n_eval[k];
                 const float w = comp ? __fmul_rn(alpha, T[k]) : 0.0f;
                 cr[k] = __fmaf_rn(g1.z, w, cr[k]);
                 cg[k] = __fmaf_rn(g1.w, w, cg[k]);
                 cb[k] = __fmaf_rn(gbl, w, cb[k]);
                 T[k] = comp ? Tn : T[k];
                 last[k] = comp ? pos1 : last[k];
-                n_comp[k] += comp ? 1u : 0u;
+                if (DIAG) n_comp[k] += comp ? 1u : 0u;
             }
         }
     }
@@ -230,8 +230,8 @@ __global__ void __launch_bounds__(Layout<PPT>::kThreads) render_fwd_kernel(Rende
             a.image[2 * plane + pix] = __fmaf_rn(T[k], a.bg[2], cb[k]);
             a.final_T[pix] = T[k];
             a.n_contrib[pix] = last[k];
-            if (a.n_eval) a.n_eval[pix] = n_eval[k];
-            if (a.n_comp) a.n_comp[pix] = n_comp[k];
+            if (DIAG && a.n_eval) a.n_eval[pix] = n_eval[k];
+            if (DIAG && a.n_comp) a.n_comp[pix] = n_comp[k];
         }
     }
 }
@@ -246,9 +246,17 @@ static int ppt_from_env(const char* name, int dflt) {
 cudaError_t launch_render_fwd(const RenderFwdArgs& a, cudaStream_t stream) {
     static const int ppt = ppt_from_env("GES_PPT_FWD", 2);
     const int grid = a.tiles_x * a.tiles_y;
-    if (ppt == 1) render_fwd_kernel<1><<<grid, Layout<1>::kThreads, 0, stream>>>(a);
-    else if (ppt == 4) render_fwd_kernel<4><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
-    else render_fwd_kernel<2><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
+    const bool diag = a.n_eval || a.n_comp;  // the counters cost issue slots: only when asked
+    if (ppt == 1) {
+        if (diag) render_fwd_kernel<1, true><<<grid, Layout<1>::kThreads, 0, stream>>>(a);
+        else render_fwd_kernel<1, false><<<grid, Layout<1>::kThreads, 0, stream>>>(a);
+    } else if (ppt == 4) {
+        if (diag) render_fwd_kernel<4, true><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
+        else render_fwd_kernel<4, false><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
+    } else {
+        if (diag) render_fwd_kernel<2, true><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
+        else render_fwd_kernel<2, false><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
+    }
     return cudaGetLastError();
 }
 

@@ -1,28 +1,27 @@
-// sort.cu -- S2/S3: per-tile ranges, depth radix sort of
-// the visible particles, and the stable radix sort of the (tile, particle)
-// pairs by tile id, with the pair duplication fused into the first pass.
+// sort.cu -- S2/S3: depth radix sort of the visible
+// particles, generation of the (tile, particle) pairs in depth order (every
+// tile of each particle's R10 rect), stable radix sort of the pairs by tile id,
+// per-tile ranges.
 //
 // Design: instead of a 64-bit LSD sort of
-// (tile_id << 32 | depth) keys (6 x 8-bit passes over the M pairs), the depth
-// order is established once on the V visible particles (4 onesweep passes
-// over V << M; pass 0 also compacts the visible set), then the pairs are
-// generated in that order and sorted STABLY by tile id alone (2 passes for
-// <= 65536 tiles): every tile's list comes out in (depth bits, particle index)
-// order -- exactly the order of the 64-bit keys.
-//   item scan    exclusive prefix E[s] of the pair counts of the sorted
-//                particles (decoupled look-back) and, per 4096-slot tile, the
-//                particle holding its first slot;
-//   pass 1       each CTA owns 4096 consecutive pair SLOTS (balanced however
-//                unequal the particles' footprints are), stages the particles
-//                covering them in shared memory, expands its slots by a
-//                load-balanced search, and ranks/scatters them by the low tile
-//                digit -- the unsorted pair array is never written;
-//   pass 2       the high tile digit, writing only the particle ids = lists.
-// The per-tile counts (ranges, digit histograms) come from the 2-D difference
-// grid of S1, so no pass over the pairs is spent on counting.
-// Every pass: 4096 keys per CTA, warp multisplit ranking (__match_any_sync),
-// per-digit decoupled look-back with 4 predecessors in flight, shared-memory
-// reorder for coalesced scatter.  Hand-written; no CUB.
+// (tile_id << 32 | depth) keys (6 x 8-bit passes over all pairs), the depth
+// order is established once on the V visible particles (4 passes over
+// V << M; pass 0 also compacts the visible set), then the pairs are generated
+// in that order and sorted STABLY by tile id alone (2 passes for <= 65536
+// tiles): every tile's list comes out in (depth bits, particle index) order --
+// exactly the order of the 64-bit keys.
+//   item scan   exclusive prefix E[s] of the rect areas of the sorted particles
+//               (decoupled look-back), packed item records, the particle that
+//               holds the first slot of each 4096-slot tile, the slot count;
+//   pass 1      each CTA owns 4096 consecutive pair SLOTS (balanced however
+//               unequal the footprints are), stages the particles covering
+//               them in shared memory, expands its slots by a load-balanced
+//               search, ranks and scatters them by the low tile digit -- no unsorted pair array is ever written;
+//   pass 2      the high tile digit;
+//   ranges      the boundaries of the sorted tile ids.
+// Each pass is reduce-then-scan (per-tile digit histograms, one column scan
+// per digit, scatter): no CTA ever waits for another.  Ranking is a warp
+// multisplit with one ballot per digit bit.  Hand-written; no CUB.
 #include <algorithm>
 
 #include "ges_internal.h"
@@ -30,144 +29,14 @@
 
 namespace ges {
 
-// ---------------------------------------------------------------------------
-// S3: ranges and digit offsets (one CTA)
-// ---------------------------------------------------------------------------
-constexpr int kRangesThreads = 1024;
-
-__device__ __forceinline__ uint32_t block_excl_scan_1024(uint32_t v, uint32_t* s_warp, uint32_t& total) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t incl = v;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += n;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t w = s_warp[lane];
-        uint32_t wi = w;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t n = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += n;
-        }
-        s_warp[lane] = wi - w;
-        if (lane == 31) s_warp[32] = wi;
-    }
-    __syncthreads();
-    const uint32_t res = s_warp[warp] + incl - v;
-    total = s_warp[32];
-    __syncthreads();
-    return res;
-}
-
-__global__ void __launch_bounds__(kRangesThreads) ranges_kernel(RangesArgs a) {
-    extern __shared__ int32_t s_grid[];  // (tiles_y + 1) x (tiles_x + 1)
-    __shared__ uint32_t s_warp[33];
-    __shared__ uint32_t s_th[2][256];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int tx = a.tiles_x, ty = a.tiles_y, sx = tx + 1;
-    const int G = sx * (ty + 1);
-    for (int k = tid; k < 512; k += kRangesThreads) (&s_th[0][0])[k] = 0;
-    for (int k = tid; k < G; k += kRangesThreads) s_grid[k] = a.tile_diff[k];
-    __syncthreads();
-    // 2-D prefix sum of the difference grid: rows (warp per row), then columns
-    for (int y = warp; y <= ty; y += kRangesThreads / 32) {
-        int32_t carry = 0;
-        for (int x0 = 0; x0 <= tx; x0 += 32) {
-            const int x = x0 + lane;
-            int32_t v = (x <= tx) ? s_grid[y * sx + x] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t nn = __shfl_up_sync(0xffffffffu, v, o);
-                if (lane >= o) v += nn;
-            }
-            if (x <= tx) s_grid[y * sx + x] = v + carry;
-            carry += __shfl_sync(0xffffffffu, v, 31);
-        }
-    }
-    __syncthreads();
-    for (int x = warp; x <= tx; x += kRangesThreads / 32) {
-        int32_t carry = 0;
-        for (int y0 = 0; y0 <= ty; y0 += 32) {
-            const int y = y0 + lane;
-            int32_t v = (y <= ty) ? s_grid[y * sx + x] : 0;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t nn = __shfl_up_sync(0xffffffffu, v, o);
-                if (lane >= o) v += nn;
-            }
-            if (y <= ty) s_grid[y * sx + x] = v + carry;
-            carry += __shfl_sync(0xffffffffu, v, 31);
-        }
-    }
-    __syncthreads();
-    // exclusive scan of the per-tile counts in tile order (t = y * tx + x)
-    const int T = tx * ty;
-    const int per = (T + kRangesThreads - 1) / kRangesThreads;
-    const int t0 = min(T, tid * per), t1 = min(T, t0 + per);
-    uint32_t local = 0;
-    for (int t = t0; t < t1; ++t) {
-        const uint32_t c = (uint32_t)s_grid[(t / tx) * sx + (t % tx)];
-        local += c;
-        atomicAdd(&s_th[0][t & 255], c);
-        atomicAdd(&s_th[1][(t >> 8) & 255], c);
-    }
-    uint32_t total;
-    uint32_t run = block_excl_scan_1024(local, s_warp, total);
-    for (int t = t0; t < t1; ++t) {
-        a.ranges[t] = run;
-        run += (uint32_t)s_grid[(t / tx) * sx + (t % tx)];
-    }
-    if (tid == 0) {
-        a.ranges[T] = total;
-        a.counters[GES_CTR_PAIRS] = total;
-        a.counters[GES_CTR_OVERFLOW] = (int64_t)total > a.capacity ? 1ull : 0ull;
-    }
-    __syncthreads();
-    // exclusive digit offsets: 4 depth digit histograms (from S1) + 2 tile digits
-    if (tid < 6 * 32) {
-        const int h = tid >> 5;
-        uint32_t* src = (h < 4) ? (a.hist + h * 256) : s_th[h - 4];
-        uint32_t* dst = a.hist + h * 256;
-        uint32_t vals[8], s = 0;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) { vals[q] = src[lane * 8 + q]; s += vals[q]; }
-        uint32_t incl = s;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t n = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += n;
-        }
-        uint32_t run2 = incl - s;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) { dst[lane * 8 + q] = run2; run2 += vals[q]; }
-    }
-}
-
-int ranges_smem_bytes(int tiles_x, int tiles_y) { return (tiles_x + 1) * (tiles_y + 1) * 4; }
-
-cudaError_t launch_ranges(const RangesArgs& a, cudaStream_t stream) {
-    const int smem = ranges_smem_bytes(a.tiles_x, a.tiles_y);
-    static int configured = 0;
-    if (smem > 48 * 1024 && configured < smem) {
-        cudaFuncSetAttribute(ranges_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        configured = 200 * 1024;
-    }
-    ranges_kernel<<<1, kRangesThreads, smem, stream>>>(a);
-    return cudaGetLastError();
-}
+constexpr int kSlotTile = 4096;  // pair slots per CTA == radix tile
 
 // ---------------------------------------------------------------------------
-// Item scan: E[s] = sum_{s' < s} tiles(sorted_vis[s']), tile_first[j] = item
-// holding pair slot j * 4096.
+// Item scan
 // ---------------------------------------------------------------------------
 constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
-constexpr int kSlotTile = 4096;  // == radix tile
 
 int64_t item_scan_tiles(int64_t n) { return (n + kScanTile - 1) / kScanTile; }
 int64_t slot_tiles(int64_t cap) { return (cap + kSlotTile - 1) / kSlotTile + 2; }
@@ -179,22 +48,24 @@ __global__ void __launch_bounds__(kScanThreads) item_scan_kernel(ItemScanArgs a)
     __shared__ uint32_t s_tile, s_prefix;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t V = (int64_t)a.counters[GES_CTR_VISIBLE];
+    if (V == 0) {
+        if (blockIdx.x == 0 && tid == 0) a.counters[GES_CTR_SLOTS] = 0;
+        return;
+    }
     if (tid == 0) s_tile = (uint32_t)atomicAdd(a.tile_counter, 1ull);
     __syncthreads();
     const int64_t tile = s_tile;
     if (tile * kScanTile >= V) return;  // tickets are ordered: nobody waits on this one
     const int64_t first = tile * kScanTile + (int64_t)tid * kScanItems;
     uint32_t c[kScanItems], ids[kScanItems];
-    uint32_t sum = 0;
     ushort4 rc[kScanItems];
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) ids[j] = (first + j < V) ? __ldg(a.sorted_vis + first + j) : 0u;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) rc[j] = (first + j < V) ? __ldg(a.rect + ids[j]) : make_ushort4(0, 0, 0, 0);
+    uint32_t sum = 0;
 #pragma unroll
-    for (int j = 0; j < kScanItems; ++j) c[j] = rect_count(rc[j]);
-#pragma unroll
-    for (int j = 0; j < kScanItems; ++j) sum += c[j];
+    for (int j = 0; j < kScanItems; ++j) { c[j] = rect_count(rc[j]); sum += c[j]; }
     uint32_t incl = sum;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -220,14 +91,20 @@ __global__ void __launch_bounds__(kScanThreads) item_scan_kernel(ItemScanArgs a)
     uint32_t e = s_prefix + s_warp[warp] + incl - sum;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        if (first + j < V) {
-            a.E[first + j] = e;
+        const int64_t s = first + j;
+        if (s < V) {
+            a.E[s] = e;
             // packed item record for the pair expansion: one coalesced 16-B load there
-            a.items[first + j] = make_uint4(e, ids[j], (uint32_t)rc[j].x | ((uint32_t)rc[j].y << 16),
-                                            (uint32_t)rc[j].z | ((uint32_t)rc[j].w << 16));
+            a.items[s] = make_uint4(e, ids[j], (uint32_t)rc[j].x | ((uint32_t)rc[j].y << 16),
+                                    (uint32_t)rc[j].z | ((uint32_t)rc[j].w << 16));
             // slot tiles whose first slot lies in [e, e + c)
             for (uint32_t st = (e + kSlotTile - 1) / kSlotTile; st * (uint64_t)kSlotTile < (uint64_t)e + c[j]; ++st)
-                a.tile_first[st] = (uint32_t)(first + j);
+                a.tile_first[st] = (uint32_t)s;
+            if (s == V - 1) {  // total pair slots, capacity check
+                const uint64_t slots = (uint64_t)e + c[j];
+                a.counters[GES_CTR_SLOTS] = slots;
+                a.counters[GES_CTR_OVERFLOW] = (int64_t)slots > a.capacity ? 1ull : 0ull;
+            }
         }
         e += c[j];
     }
@@ -241,11 +118,11 @@ cudaError_t launch_item_scan(const ItemScanArgs& a, int64_t max_items, cudaStrea
 
 // ---------------------------------------------------------------------------
 // LSD radix passes, reduce-then-scan (no inter-CTA waiting):
-//   radix_hist_kernel     per 4096-key tile: 8-bit digit histogram -> H[tile][256]
-//   radix_scan_kernel     per digit: exclusive scan of H[.][d] over the tiles,
+//   radix_hist_kernel     per 4096-key tile: digit histogram -> H[d][tile]
+//   radix_scan_kernel     per digit: exclusive scan of H[d][.] over the tiles,
 //                         column total -> T[d]
 //   radix_scatter_kernel  per tile: stable warp-multisplit ranking, shared-memory
-//                         reorder, scatter to off(d) + H[tile][d] + local rank
+//                         reorder, scatter to off(d) + H[d][tile] + local rank
 // GEN = true: a tile's keys (tile ids) and values (particle ids) are generated
 // from the depth-sorted particles (load-balanced search over pair slots).
 // ---------------------------------------------------------------------------
@@ -258,10 +135,10 @@ static_assert(kRadixTile == kSlotTile, "slot tiles are radix tiles");
 
 int64_t radix_tiles(int64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
 
-// Particles covering a tile's 4096 slots are staged in shared memory when
+// Particles covering a CTA's 4096 slots are staged in shared memory when
 // there are at most kStageMax of them (the common case: a particle touches
 // ~20 tiles); tiles of many tiny particles read them from L2 instead.
-constexpr int kStageMax = 2048;
+constexpr int kStageMax = 1024;
 struct GenSmem {
     uint32_t E[kStageMax];
     uint32_t pid[kStageMax];
@@ -269,16 +146,22 @@ struct GenSmem {
 };
 
 __device__ __forceinline__ int64_t pass_count(const RadixPassArgs& a) {
+    if (a.count_totals) {  // item count = sum of the previous pass's digit totals
+        uint32_t n = 0;
+        for (int d = 0; d < kRadixDigits; ++d) n += a.count_totals[d];
+        return min((int64_t)n, a.max_items);
+    }
     return a.count ? min((int64_t)*a.count, a.max_items) : a.max_items;
 }
 
 // Loads (or generates) the tile's keys/values in warp-striped order: item j of
-// lane l of warp w is element w*512 + j*32 + l of the tile.  valid[j] marks
-// items that take part (inside n and, when dropping, not the invalid marker).
+// lane l of warp w is element w*512 + j*32 + l of the tile.  valid bit j marks
+// items that take part.
 template <bool GEN>
-__device__ __forceinline__ void load_tile(const RadixPassArgs& a, int64_t tile, int64_t n, uint32_t (&k)[kRadixItems],
-                                          uint32_t (&v)[kRadixItems], uint32_t& valid, uint32_t* s_keys,
-                                          uint32_t* s_vals, unsigned char* s_dyn, bool need_vals) {
+__device__ __forceinline__ void load_tile(const RadixPassArgs& a, int64_t tile, int64_t n,
+                                          uint32_t (&k)[kRadixItems], uint32_t (&v)[kRadixItems], uint32_t& valid,
+                                          uint32_t* s_keys, uint32_t* s_vals, unsigned char* s_dyn,
+                                          bool need_vals) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = tile * kRadixTile + warp * (kRadixItems * 32);
     valid = 0;
@@ -354,8 +237,10 @@ __device__ __forceinline__ void load_tile(const RadixPassArgs& a, int64_t tile, 
                     xx = 0;
                     yy = 0;
                 }
+                const uint32_t tx = r.x + xx, ty = r.y + yy;
+                const uint32_t key = ty * (uint32_t)a.tiles_x + tx;
                 const int pad = ls + (ls >> 5);  // +1 word per 32: conflict-free both ways
-                s_keys[pad] = (r.y + yy) * (uint32_t)a.tiles_x + r.x + xx;
+                s_keys[pad] = key;
                 s_vals[pad] = pid;
                 if (++xx == w) { xx = 0; ++yy; }
             }
@@ -367,7 +252,7 @@ __device__ __forceinline__ void load_tile(const RadixPassArgs& a, int64_t tile, 
             if (ls < nslots) {
                 const int pad = ls + (ls >> 5);
                 k[j] = s_keys[pad];
-                v[j] = s_vals[pad];
+                if (need_vals) v[j] = s_vals[pad];
                 valid |= 1u << j;
             }
         }
@@ -420,7 +305,7 @@ __global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(RadixPassArgs
     a.tile_hist[(int64_t)threadIdx.x * a.hist_stride + tile] = s_hist[threadIdx.x];
 }
 
-// One CTA per digit: exclusive scan of H[.][d] over the tiles (in place).
+// One CTA per digit: exclusive scan of H[d][.] over the tiles (in place).
 __global__ void __launch_bounds__(256) radix_scan_kernel(RadixPassArgs a) {
     __shared__ uint32_t s_warp[9];
     const int d = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -585,6 +470,34 @@ cudaError_t launch_radix_pass(const RadixPassArgs& a, cudaStream_t stream) {
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         radix_scatter_kernel<false><<<grid, kRadixThreads, 0, stream>>>(a);
     }
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// S3: per-tile ranges from the sorted tile ids
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) ranges_kernel(RangesArgs a) {
+    const int T = a.tiles_x * a.tiles_y;
+    if (a.counters[GES_CTR_OVERFLOW]) {
+        for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= T; t += gridDim.x * blockDim.x) a.ranges[t] = 0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.counters[GES_CTR_PAIRS] = 0;
+        return;
+    }
+    uint32_t M = 0;
+    for (int d = 0; d < kRadixDigits; ++d) M += a.count_totals[d];
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.counters[GES_CTR_PAIRS] = M;
+    // entry m opens every tile in (key[m-1], key[m]]; the end closes (key[M-1], T]
+    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m <= (int64_t)M;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        const int prev = m > 0 ? (int)a.keys[m - 1] : -1;
+        const int cur = m < (int64_t)M ? (int)a.keys[m] : T;
+        for (int t = prev + 1; t <= cur; ++t) a.ranges[t] = (uint32_t)m;
+    }
+}
+
+cudaError_t launch_ranges(const RangesArgs& a, cudaStream_t stream) {
+    const int grid = std::max(1, std::min(num_sms() * 8, (int)((a.max_pairs + 255) / 256)));
+    ranges_kernel<<<grid, 256, 0, stream>>>(a);
     return cudaGetLastError();
 }
 

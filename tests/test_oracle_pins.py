@@ -4,6 +4,10 @@ oracle's own formulas).  Runs on CPU (`-m "not gpu"`).
 Each test names the passage it pins.  A plausible mistake anywhere in the
 oracle (a dropped term, a wrong sign, a transposed operand) fails one of them:
   * exp_spec                  vs libm exp in fp64 (<= 2 ulp), exp(0) = 1
+  * log_spec                  vs libm log in fp64 (<= 3 ulp), log(2^k) = k ln2
+  * tile rect (R10)           brute-force alpha over every pixel; the 'all'
+                              membership (every particle in every tile) gives
+                              the same image and gradients
   * phi-bar, Eq. 6            golden values from tests/golden/phi_bar.txt
   * Sigma, S*phi, EWA         vs scipy rotation + numerically differentiated
                               pinhole projection (independent Jacobian)
@@ -279,6 +283,85 @@ def test_permutation_invariance_and_convexity():
     assert a["image"].min() >= 0.0 and a["image"].max() <= 1.0
 
 
+def test_log_spec_accuracy_and_powers_of_two():
+    x = np.exp(np.linspace(1e-6, 12.0, 400001)).astype(np.float32)
+    x = x[x > 1]
+    y = O.log_spec(x).astype(np.float64)
+    ref = np.log(x.astype(np.float64))
+    ulp = np.spacing(ref.astype(np.float32)).astype(np.float64)
+    assert (np.abs(y - ref) / ulp).max() <= 3.0
+    k = np.arange(1, 20)
+    p2 = O.log_spec((2.0 ** k).astype(np.float32)).astype(np.float64)
+    assert np.allclose(p2, k * math.log(2.0), rtol=0, atol=1e-6)
+
+
+def _alpha_image(pre, i, W, H):
+    """kappa exp(-Q/2) of particle i at every pixel centre (x + 0.5, y + 0.5), fp64."""
+    px, py = np.meshgrid(np.arange(W) + 0.5, np.arange(H) + 0.5)
+    ca, cb, cc = pre["conic"][:, i].astype(np.float64)
+    dx, dy = float(pre["uv"][0, i]) - px, float(pre["uv"][1, i]) - py
+    q = ca * dx * dx + cc * dy * dy + 2.0 * cb * dx * dy
+    return float(pre["kappa"][i]) * np.exp(-0.5 * q)
+
+
+def test_rect_holds_every_pixel_that_reaches_the_alpha_threshold():
+    """R10: a pixel outside rect_i's tiles never sees alpha_i >= 1/255, and the
+    rect is no wider than the 0.98/255 box needs (brute force over all pixels)."""
+    sc = gi.random_small_scene(11, P=80, W=192, H=128, log_scale_mu=-1.7, kappa_max=0.99)
+    cam = sc.cameras[0]
+    pre = O.preprocess(sc.particles, cam, O.Settings(), "f32")
+    W, H = cam.width, cam.height
+    n_vis = n_tight = 0
+    for i in range(sc.particles.P):
+        if pre["status"][i] not in (O.VISIBLE, O.OFFSCREEN):
+            continue
+        a = _alpha_image(pre, i, W, H)
+        x0, y0, x1, y1 = pre["rect"][:, i]
+        inside = np.zeros((H, W), bool)
+        inside[16 * y0:16 * y1, 16 * x0:16 * x1] = True
+        assert a[~inside].max(initial=0.0) < 1.0 / 255, i
+        q = 2.0 * math.log(255.0 * float(pre["kappa"][i]) / 0.98) if pre["kappa"][i] > 0.98 / 255 else 0.0
+        ex, ey = math.sqrt(q * float(pre["cov2d"][0, i])), math.sqrt(q * float(pre["cov2d"][2, i]))
+        u, v = float(pre["uv"][0, i]), float(pre["uv"][1, i])
+        unclipped = u - ex > 0 and u + ex < W and v - ey > 0 and v + ey < H
+        if pre["status"][i] == O.VISIBLE:
+            n_vis += 1
+            if not unclipped:
+                continue
+            n_tight += 1
+            # tight: no rect edge tile column/row lies beyond the pixels that
+            # reach alpha >= 0.25/255 (the pixel grid is within half a pixel of
+            # the ellipse's extreme points; sigma >= sqrt(0.3) px after dilation)
+            ys, xs = np.nonzero(a >= 0.25 / 255)
+            assert ys.size > 0
+            assert x0 >= xs.min() // 16 and x1 - 1 <= xs.max() // 16, i
+            assert y0 >= ys.min() // 16 and y1 - 1 <= ys.max() // 16, i
+        else:
+            assert a.max() < 1.0 / 255
+    assert n_vis > 40 and n_tight > 20, (n_vis, n_tight)
+
+
+def test_rect_membership_equals_all_particles_in_all_tiles():
+    """Eq. 3 with the alpha skip sums over ALL particles; restricting each to its
+    rect tiles (R10) or to tiles that reach the threshold (R8 'exact') changes
+    nothing: bit-identical images, gradients equal to 1e-12."""
+    sc = gi.random_small_scene(12, P=120, W=96, H=64, log_scale_mu=-1.3, kappa_max=0.99)
+    cam = sc.cameras[0]
+    g = gi.upstream_grad(sc.seed, 0, cam.width, cam.height)
+    outs = {m: O.render_and_grad(sc.particles, cam, O.Settings(), g, membership=m)
+            for m in ("rect", "all", "exact")}
+    a = outs["rect"]
+    assert a["list"].size < outs["all"]["list"].size
+    for m in ("all", "exact"):
+        b = outs[m]
+        assert np.array_equal(a["image"], b["image"]), m
+        # n_contrib is a position in the tile's list, so only its zero set is shared
+        assert np.array_equal(a["n_contrib"] > 0, b["n_contrib"] > 0), m
+        assert np.array_equal(a["final_T"], b["final_T"]), m
+        for k in a["grads"]:
+            assert np.allclose(a["grads"][k], b["grads"][k], rtol=1e-12, atol=1e-12), (m, k)
+
+
 # --------------------------------------------------------------------------
 # Keys, sort, lists: numpy brute force on tiny inputs
 # --------------------------------------------------------------------------
@@ -286,7 +369,7 @@ def test_keys_and_lists_bruteforce():
     sc = gi.make_config(0, P=300)
     cam = sc.cameras[0]
     pre = O.preprocess(sc.particles, cam, O.Settings(), "f32")
-    keys, vals = O.pairs_sorted(pre)
+    keys, vals = O.pairs_sorted(pre, membership="rect")
     tx = pre["tiles_x"]
     db = pre["depth"].view(np.uint32)
     ek, ev = [], []
@@ -301,7 +384,7 @@ def test_keys_and_lists_bruteforce():
     ek, ev = np.array(ek, np.uint64), np.array(ev, np.int32)
     o = np.lexsort((ev, ek))
     assert np.array_equal(keys, ek[o]) and np.array_equal(vals, ev[o])
-    offsets, lst = O.tile_lists(pre)
+    offsets, lst = O.tile_lists(pre, membership="rect")
     tiles = (keys >> np.uint64(32)).astype(np.int64)
     for t in range(tx * pre["tiles_y"]):
         sel = vals[tiles == t]
@@ -424,3 +507,37 @@ def test_ambiguity_flags_are_rare_on_config0():
     sc = gi.make_config(0)
     out = O.render(sc.particles, sc.cameras[0], O.Settings(), "f32")
     assert (out["amb"] != 0).mean() < 1e-3
+
+
+def test_exact_membership_changes_nothing_but_the_lists():
+    """R8: dropping (tile, particle) pairs that cannot reach alpha >= 0.98/255
+    anywhere in the tile leaves images and gradients exactly unchanged, and
+    the kept pairs keep their (tile, depth, index) order."""
+    sc = gi.make_config(1, P=4000)
+    cam = sc.cameras[0]
+    g = gi.upstream_grad(sc.seed, 0, cam.width, cam.height)
+    a = O.render_and_grad(sc.particles, cam, O.Settings(), g, membership="rect")
+    b = O.render_and_grad(sc.particles, cam, O.Settings(), g, membership="exact")
+    assert np.array_equal(a["image"], b["image"])
+    assert np.array_equal(a["n_contrib"] > 0, b["n_contrib"] > 0)
+    for k in a["grads"]:
+        assert np.allclose(a["grads"][k], b["grads"][k], rtol=1e-12, atol=1e-12), k
+    kr, vr = O.pairs_sorted(a["pre"], membership="rect")
+    ke, ve = O.pairs_sorted(a["pre"], membership="exact")
+    assert 0 < ke.size < kr.size
+    pos = {(int(k), int(v)): n for n, (k, v) in enumerate(zip(kr, vr))}
+    idx = np.array([pos[(int(k), int(v))] for k, v in zip(ke, ve)])
+    assert np.all(np.diff(idx) > 0)   # a subsequence of the rect order
+    # membership really is the alpha test: every dropped pair's particle is at most
+    # 0.98/255 at the tile's nearest pixel centre (brute force over the tile's pixels)
+    pre = a["pre"]
+    dropped = set(zip(kr.tolist(), vr.tolist())) - set(zip(ke.tolist(), ve.tolist()))
+    tx_n = pre["tiles_x"]
+    for k, i in list(dropped)[:200]:
+        t = k >> 32
+        ty, tx = divmod(t, tx_n)
+        px, py = np.meshgrid(np.arange(16) + 16 * tx + 0.5, np.arange(16) + 16 * ty + 0.5)
+        ca, cb, cc = pre["conic"][:, i].astype(np.float64)
+        dx, dy = pre["uv"][0, i] - px, pre["uv"][1, i] - py
+        alpha = pre["kappa"][i] * np.exp(-0.5 * (ca * dx * dx + cc * dy * dy) - cb * dx * dy)
+        assert alpha.max() < 0.99 / 255

@@ -22,7 +22,7 @@ params = G.PlanarParams.from_inputs(sc.particles)
 st = G.Settings(rho=sc.rho)
 r = G.Renderer(params.P, cam.width, cam.height)
 img = r.forward(params, cam, st)
-r.grow(int(r.frame.counts().pairs))
+r.grow(int(r.frame.counts().slots))
 dL = torch.from_numpy(gi.upstream_grad(sc.seed, 0, cam.width, cam.height)).cuda()
 grads = G.PlanarParams.zeros(params.P, params.sh_degree)
 for _ in range(args.steps):
