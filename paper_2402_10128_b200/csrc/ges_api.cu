@@ -211,8 +211,7 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
         p.vals_in = (d == 0) ? nullptr : frame->pair_val;
         p.keys_out = last ? frame->list_tile : frame->pair_tile;
         p.vals_out = last ? frame->list : frame->pair_val;
-        p.count = (d == 0) ? ctr + GES_CTR_SLOTS : nullptr;
-        p.count_totals = (d == 0) ? nullptr : frame->radix_total;  // pairs of pass 1
+        p.count = ctr + GES_CTR_SLOTS;  // every slot is a pair (R10 rects)
         p.max_items = frame->pair_capacity;
         p.tile_hist = frame->radix_hist;
         p.hist_stride = hist_stride;
@@ -231,7 +230,6 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     }
     RangesArgs r;
     r.keys = frame->list_tile;
-    r.count_totals = frame->radix_total;  // pass 1's totals = all pairs
     r.tiles_x = frame->tiles_x; r.tiles_y = frame->tiles_y;
     r.ranges = frame->ranges; r.counters = ctr; r.max_pairs = frame->pair_capacity;
     if ((e = launch_ranges(r, s)) != cudaSuccess) return GES_ERR_CUDA;

@@ -39,7 +39,6 @@ struct RadixPassArgs {
     uint32_t* keys_out;               // may be null
     uint32_t* vals_out;
     const unsigned long long* count;  // device item count (null: max_items)
-    const uint32_t* count_totals;     // non-null: item count = sum of these 256 digit totals
     int64_t max_items;                // upper bound (grid sizing); items beyond are ignored
     uint32_t* tile_hist;              // [256][hist_stride] per-tile digit counts -> offsets (digit-major)
     int64_t hist_stride;              // >= number of tiles
@@ -78,7 +77,6 @@ int64_t slot_tiles(int64_t cap);
 
 struct RangesArgs {
     const uint32_t* keys;             // [M] sorted tile ids
-    const uint32_t* count_totals;     // M = sum of these 256 digit totals
     int tiles_x, tiles_y;
     uint32_t* ranges;                 // [T+1]
     unsigned long long* counters;     // writes PAIRS

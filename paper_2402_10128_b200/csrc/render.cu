@@ -19,10 +19,10 @@
 // exactly the ones every pixel of the region would skip: results are
 // identical to the unculled loop.  __syncthreads_count retires the tile once
 // all pixels have terminated.  The backward walks the same lists back to
-// front from the last composited entry and reduces the nine per-pair
-// gradients across each warp with a recursive-halving shuffle (24 SHFL per
-// warp and entry) and adds them with three vector reductions
-// (red.global.add.v4.f32) into the particle's 12-float gradient record.
+// front from the last composited entry of each warp and reduces the nine
+// per-pair gradients across the warp with an uneven recursive-halving shuffle
+// (12 SHFL per warp and entry), then nine lanes add them (red.global.add.f32)
+// into the particle's 12-float gradient record.
 #include <cstdlib>
 
 #include "ges_internal.h"
@@ -263,35 +263,49 @@ cudaError_t launch_render_fwd(const RenderFwdArgs& a, cudaStream_t stream) {
 // ---------------------------------------------------------------------------
 // S5a backward
 // ---------------------------------------------------------------------------
-// Warp reduction of 9 (padded to 16) values by recursive halving: two
-// halving steps leave 4 components per lane (partially summed), three xor
-// steps finish them.  Lanes 0, 8 and 16 then hold components 0-3, 4-7 and
-// 8-11 (24 shuffles instead of 45 for nine full butterflies).
-__device__ __forceinline__ float4 warp_reduce_to_v4(float v[16]) {
-    const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int step = 0; step < 2; ++step) {
-        const int o = 16 >> step;      // 16, 8
-        const int half = 8 >> step;    // 8, 4
-        const bool upper = (lane & o) != 0;
-#pragma unroll
-        for (int i = 0; i < half; ++i) {
-            const float send = upper ? v[i] : v[i + half];
-            const float keep = upper ? v[i + half] : v[i];
-            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-        }
-    }
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1)
-#pragma unroll
-        for (int i = 0; i < 4; ++i) v[i] += __shfl_xor_sync(0xffffffffu, v[i], o);
-    return make_float4(v[0], v[1], v[2], v[3]);
+// Warp sum of the nine per-pair gradient components by recursive halving over
+// uneven component sets: xor 16 splits {0-4 | 5-8} (5 SHFL), xor 8 splits the
+// remaining slots {0-2 | 3-4} (3), xor 4 {0-1 | 2} (2), xor 2 (1), xor 1 (1):
+// 12 shuffles.  Afterwards lanes l and l^1 hold the full sum of component
+// reduce9_component(l) (or -1: no component).
+__device__ __forceinline__ int reduce9_component(int lane) {
+    const int i2 = ((lane & 4) ? 2 : 0) + ((lane & 2) ? 1 : 0);
+    const int i1 = ((lane & 8) ? 3 : 0) + i2;
+    const bool hi = (lane & 16) != 0;
+    if (i2 > 2 || i1 > (hi ? 3 : 4)) return -1;
+    return (hi ? 5 : 0) + i1;
 }
 
-__device__ __forceinline__ void red_add_v4(float* addr, float4 x) {
-    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(x.x), "f"(x.y), "f"(x.z),
-                 "f"(x.w)
-                 : "memory");
+__device__ __forceinline__ float warp_reduce9(const float v[9]) {
+    const int lane = threadIdx.x & 31;
+    const bool u16 = (lane & 16) != 0, u8 = (lane & 8) != 0, u4 = (lane & 4) != 0, u2 = (lane & 2) != 0;
+    float w[6];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) {
+        const float lo = v[i], hi = (i < 4) ? v[5 + i] : 0.0f;
+        w[i] = (u16 ? hi : lo) + __shfl_xor_sync(0xffffffffu, u16 ? lo : hi, 16);
+    }
+    w[5] = 0.0f;
+    float x[4];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const float lo = w[i], hi = w[3 + i];
+        x[i] = (u8 ? hi : lo) + __shfl_xor_sync(0xffffffffu, u8 ? lo : hi, 8);
+    }
+    x[3] = 0.0f;
+    float y[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float lo = x[i], hi = x[2 + i];
+        y[i] = (u4 ? hi : lo) + __shfl_xor_sync(0xffffffffu, u4 ? lo : hi, 4);
+    }
+    float z = (u2 ? y[1] : y[0]) + __shfl_xor_sync(0xffffffffu, u2 ? y[0] : y[1], 2);
+    z += __shfl_xor_sync(0xffffffffu, z, 1);
+    return z;
+}
+
+__device__ __forceinline__ void red_add(float* addr, float x) {
+    asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(x) : "memory");
 }
 
 template <int PPT>
@@ -335,9 +349,11 @@ __global__ void __launch_bounds__(Layout<PPT>::kThreads) render_bwd_kernel(Rende
     }
     if (tid == 0) s_max = 0;
     __syncthreads();
-    if (my_max) atomicMax(&s_max, my_max);
+    const uint32_t warp_max = __reduce_max_sync(0xffffffffu, my_max);
+    if (lane == 0 && warp_max) atomicMax(&s_max, warp_max);
     __syncthreads();
     const uint32_t max_last = s_max;
+    const int red_comp = reduce9_component(lane);
     StagedBatch sb{s_g0, s_g1, s_b, s_pid, s_mask};
     for (int32_t b_end = (int32_t)max_last; b_end > 0; b_end -= kBatch) {
         const int32_t b_begin = max(0, b_end - kBatch);
@@ -345,53 +361,56 @@ __global__ void __launch_bounds__(Layout<PPT>::kThreads) render_bwd_kernel(Rende
         __syncthreads();  // previous batch fully consumed
         stage_batch<PPT>(a.pay0, a.pay1, a.pay2, a.list, start + b_begin, n, tile_x0, tile_y0, sb);
         __syncthreads();
-        const int nw = compact_warp_list(s_mask, n, warp, s_list[warp]);
+        // this warp's pixels composite nothing at or behind list position warp_max
+        const int nw_lim = (int)min((int64_t)n, max((int64_t)0, (int64_t)warp_max - b_begin));
+        const int nw = compact_warp_list(s_mask, nw_lim, warp, s_list[warp]);
         for (int i = nw - 1; i >= 0; --i) {
             const int j = s_list[warp][i];
             const uint32_t pos = (uint32_t)(b_begin + j);
-            float v[16];
+            float v[9];
 #pragma unroll
-            for (int c = 0; c < 16; ++c) v[c] = 0.0f;
+            for (int c = 0; c < 9; ++c) v[c] = 0.0f;
             bool contrib = false;
             const float4 g0 = s_g0[j];
             const float4 g1 = s_g1[j];
             const float rb = s_b[j];
             const float dx = __fsub_rn(g0.x, fpx);
+            const float twoA = g0.z + g0.z, twoC = g1.x + g1.x;
+            // branch-free per pixel: the forward's decisions become predicates
 #pragma unroll
             for (int k = 0; k < PPT; ++k) {
-                if (pos >= last[k]) continue;
                 const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
                 const float p2raw = raw_exponent(g0.z, g0.w, g1.x, dx, dy);
                 const float G = fast_exp2(fminf(p2raw, 0.0f));
                 const float araw = __fmul_rn(g1.y, G);
                 const float alpha = fminf(kAlphaMax, araw);
-                if (alpha < kAlphaMin) continue;
-                contrib = true;
+                const bool m = pos < last[k] && alpha >= kAlphaMin;
+                contrib |= m;
                 const float inv_om = __fdividef(1.0f, __fsub_rn(1.0f, alpha));
-                const float Tk = T[k] * inv_om;  // transmittance before entry k
+                const float Tk = m ? T[k] * inv_om : T[k];  // transmittance before this entry
                 const float cgk = g1.z * gr[k] + g1.w * gg[k] + rb * gb[k];
+                const float w = m ? alpha * Tk : 0.0f;
                 const float dalpha = Tk * cgk - (suffix[k] + bg_term[k]) * inv_om;
-                const float w = alpha * Tk;
+                const float dal = (m && araw < kAlphaMax) ? dalpha : 0.0f;
                 suffix[k] += cgk * w;
                 v[6] += w * gr[k];
                 v[7] += w * gg[k];
                 v[8] += w * gb[k];
-                if (araw < kAlphaMax) {
-                    v[5] += G * dalpha;
-                    // alpha = kappa 2^p2  ->  d alpha / d p2 = alpha ln 2
-                    const float dp2 = (p2raw <= 0.0f) ? araw * dalpha * 0.69314718055994531f : 0.0f;
-                    const float e = dp2 * dx, f = dp2 * dy;
-                    v[0] += 2.0f * g0.z * e + g0.w * f;   // d p2 / d u
-                    v[1] += g0.w * e + 2.0f * g1.x * f;   // d p2 / d v
-                    v[2] += e * dx;                       // d p2 / d A
-                    v[3] += e * dy;                       // d p2 / d B
-                    v[4] += f * dy;                       // d p2 / d C
-                }
+                v[5] += G * dal;
+                // alpha = kappa 2^p2  ->  d alpha / d p2 = alpha ln 2
+                const float dp2 = (p2raw <= 0.0f) ? araw * dal * 0.69314718055994531f : 0.0f;
+                const float e = dp2 * dx, f = dp2 * dy;
+                v[0] += twoA * e + g0.w * f;   // d p2 / d u
+                v[1] += g0.w * e + twoC * f;   // d p2 / d v
+                v[2] += e * dx;                // d p2 / d A
+                v[3] += e * dy;                // d p2 / d B
+                v[4] += f * dy;                // d p2 / d C
                 T[k] = Tk;
             }
             if (__any_sync(0xffffffffu, contrib)) {
-                const float4 r = warp_reduce_to_v4(v);
-                if ((lane & 7) == 0 && lane < 24) red_add_v4(a.grad2d + (size_t)s_pid[j] * kGrad2dStride + lane / 2, r);
+                const float r = warp_reduce9(v);
+                if (red_comp >= 0 && (lane & 1) == 0)
+                    red_add(a.grad2d + (size_t)s_pid[j] * kGrad2dStride + red_comp, r);
             }
         }
     }

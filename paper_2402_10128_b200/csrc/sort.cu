@@ -146,11 +146,6 @@ struct GenSmem {
 };
 
 __device__ __forceinline__ int64_t pass_count(const RadixPassArgs& a) {
-    if (a.count_totals) {  // item count = sum of the previous pass's digit totals
-        uint32_t n = 0;
-        for (int d = 0; d < kRadixDigits; ++d) n += a.count_totals[d];
-        return min((int64_t)n, a.max_items);
-    }
     return a.count ? min((int64_t)*a.count, a.max_items) : a.max_items;
 }
 
@@ -483,8 +478,7 @@ __global__ void __launch_bounds__(256) ranges_kernel(RangesArgs a) {
         if (blockIdx.x == 0 && threadIdx.x == 0) a.counters[GES_CTR_PAIRS] = 0;
         return;
     }
-    uint32_t M = 0;
-    for (int d = 0; d < kRadixDigits; ++d) M += a.count_totals[d];
+    const uint32_t M = (uint32_t)min((int64_t)a.counters[GES_CTR_SLOTS], a.max_pairs);
     if (blockIdx.x == 0 && threadIdx.x == 0) a.counters[GES_CTR_PAIRS] = M;
     // entry m opens every tile in (key[m-1], key[m]]; the end closes (key[M-1], T]
     for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m <= (int64_t)M;
