@@ -85,7 +85,7 @@ typedef struct {
 } ges_particles;
 
 typedef struct {
-    int32_t width, height;      /* pixels; 16x16 tiles: tiles_x * tiles_y <= 65536 */
+    int32_t width, height;      /* pixels, each <= 4096 (16x16 tiles, <= 256 per axis) */
     float fx, fy, cx, cy;       /* pinhole intrinsics (pixels)               */
     float near_z;               /* particles with camera z <= near_z culled  */
     float R[9];                 /* world -> camera rotation, row-major       */
@@ -155,7 +155,7 @@ typedef struct {
     uint32_t *tile_first;  /* [cap/4096+2] sorted particle holding slot 4096*j        */
     uint32_t *pair_tile;   /* [cap] tile ids after the first tile-digit pass          */
     uint32_t *pair_val;    /* [cap] particle ids after the first tile-digit pass      */
-    uint32_t *list_tile;   /* [cap] tile id of every list entry (sorted)              */
+    uint32_t *list_tile;   /* [cap] key (ty << 8 | tx) of every list entry (sorted)   */
     uint32_t *list;        /* [cap] per-tile lists: tile t = list[ranges[t] .. ranges[t+1]) */
     uint32_t *ranges;      /* [T+1]                                               */
     uint32_t *lookback;    /* decoupled look-back scratch (item scan)             */

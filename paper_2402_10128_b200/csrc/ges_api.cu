@@ -137,7 +137,7 @@ ges_status ges_frame_init(void* workspace, size_t bytes, int64_t P, int32_t widt
         return GES_ERR_INVALID_ARG;
     if (((uintptr_t)workspace) % kAlign) return GES_ERR_INVALID_ARG;
     const int tx = tiles_of(width), ty = tiles_of(height);
-    if ((int64_t)tx * ty > 65536) return GES_ERR_INVALID_ARG;
+    if (tx > 256 || ty > 256) return GES_ERR_INVALID_ARG;
     if (bytes < layout(nullptr, P, width, height, pair_capacity, nullptr)) return GES_ERR_CAPACITY;
     layout((char*)workspace, P, width, height, pair_capacity, frame);
     return GES_OK;
@@ -201,7 +201,8 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     is.lookback = frame->lookback + L.scan; is.tile_counter = ctr + GES_CTR_TICKET;
     if ((e = launch_item_scan(is, frame->P, s)) != cudaSuccess) return GES_ERR_CUDA;
     // stable sort of the pairs by tile id; the first pass generates them
-    const int passes = frame->tile_bits <= 8 ? 1 : 2;
+    // pair keys are (ty << 8 | tx): pass 0 sorts by the column, pass 1 by the row
+    const int passes = frame->tiles_y > 1 ? 2 : 1;
     for (int d = 0; d < passes; ++d) {
         RadixPassArgs p;
         std::memset(&p, 0, sizeof(p));
@@ -217,7 +218,7 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
         p.hist_stride = hist_stride;
         p.digit_total = frame->radix_total + (d & 1) * kRadixDigits;
         p.shift = 8 * d;
-        p.digit_bits = std::max(1, std::min(8, frame->tile_bits - 8 * d));
+        p.digit_bits = std::max(1, bits_for(d == 0 ? frame->tiles_x : frame->tiles_y));
         p.overflow = ctr + GES_CTR_OVERFLOW;
         p.tiles_x = frame->tiles_x;
         p.sorted_vis = frame->sorted_vis;

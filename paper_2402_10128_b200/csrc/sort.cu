@@ -123,8 +123,10 @@ cudaError_t launch_item_scan(const ItemScanArgs& a, int64_t max_items, cudaStrea
 //                         column total -> T[d]
 //   radix_scatter_kernel  per tile: stable warp-multisplit ranking, shared-memory
 //                         reorder, scatter to off(d) + H[d][tile] + local rank
-// GEN = true: a tile's keys (tile ids) and values (particle ids) are generated
-// from the depth-sorted particles (load-balanced search over pair slots).
+// GEN = true: a tile's keys (ty << 8 | tx) and values (particle ids) are
+// generated from the depth-sorted particles (load-balanced search over pair
+// slots); its digit is the tile column tx, whose histogram gen_hist_kernel
+// computes from the items alone.
 // ---------------------------------------------------------------------------
 constexpr int kRadixThreads = 256;
 constexpr int kRadixItems = 16;
@@ -233,7 +235,7 @@ __device__ __forceinline__ void load_tile(const RadixPassArgs& a, int64_t tile, 
                     yy = 0;
                 }
                 const uint32_t tx = r.x + xx, ty = r.y + yy;
-                const uint32_t key = ty * (uint32_t)a.tiles_x + tx;
+                const uint32_t key = (ty << 8) | tx;
                 const int pad = ls + (ls >> 5);  // +1 word per 32: conflict-free both ways
                 s_keys[pad] = key;
                 s_vals[pad] = pid;
@@ -298,6 +300,60 @@ __global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(RadixPassArgs
         if (valid & (1u << j)) atomicAdd(&s_hist[(k[j] >> a.shift) & 255u], 1u);
     __syncthreads();
     a.tile_hist[(int64_t)threadIdx.x * a.hist_stride + tile] = s_hist[threadIdx.x];
+}
+
+// GEN pass histogram without generating the pairs: the digit of a pair is
+// its tile column tx, so the slots an item holds inside this CTA's 4096-slot
+// window add +1 over column ranges -- at most three range updates per item
+// (partial first row, full rows, partial last row) in a 257-entry difference
+// array -- followed by a prefix sum over the 256 columns.
+__global__ void __launch_bounds__(kRadixThreads) gen_hist_kernel(RadixPassArgs a) {
+    __shared__ int s_diff[kRadixDigits + 1];
+    __shared__ int s_warp[kRadixWarps];
+    if (a.overflow && *a.overflow) return;
+    const int64_t n = pass_count(a);
+    const int64_t tile = blockIdx.x;
+    if (tile * kRadixTile >= n) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    s_diff[tid] = 0;
+    if (tid == 0) s_diff[kRadixDigits] = 0;
+    __syncthreads();
+    const int64_t slot0 = tile * kRadixTile, slot1 = min(slot0 + kRadixTile, n);
+    const int64_t V = (int64_t)a.counters[GES_CTR_VISIBLE];
+    const int64_t f = a.tile_first[tile];
+    const int64_t last_item = (slot1 < n) ? (int64_t)a.tile_first[tile + 1] : V - 1;
+    for (int64_t q = f + tid; q <= last_item; q += kRadixThreads) {
+        const uint4 rec = __ldg(a.items + q);
+        const int x0 = (int)(rec.z & 0xffffu), y0 = (int)(rec.z >> 16);
+        const int x1 = (int)(rec.w & 0xffffu), y1 = (int)(rec.w >> 16);
+        const int64_t e0 = rec.x;
+        const uint32_t w = (uint32_t)(x1 - x0), area = w * (uint32_t)(y1 - y0);
+        const int64_t lo = max(slot0, e0) - e0, hi = min(slot1, e0 + (int64_t)area) - e0;  // slots [lo, hi) of the item
+        if (lo >= hi) continue;
+        const uint32_t ra = (uint32_t)lo / w, ca = (uint32_t)lo - ra * w;
+        const uint32_t rb = (uint32_t)hi / w, cb = (uint32_t)hi - rb * w;
+        if (ra == rb) {
+            atomicAdd(&s_diff[x0 + ca], 1); atomicAdd(&s_diff[x0 + cb], -1);
+        } else {
+            atomicAdd(&s_diff[x0 + ca], 1); atomicAdd(&s_diff[x1], -1);          // row ra from column ca
+            if (rb > ra + 1) { atomicAdd(&s_diff[x0], (int)(rb - ra - 1)); atomicAdd(&s_diff[x1], -(int)(rb - ra - 1)); }
+            if (cb > 0) { atomicAdd(&s_diff[x0], 1); atomicAdd(&s_diff[x0 + cb], -1); }  // row rb up to cb
+        }
+    }
+    __syncthreads();
+    // inclusive prefix over the columns
+    const int d = s_diff[tid];
+    int incl = d;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int nn = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += nn;
+    }
+    if (lane == 31) s_warp[warp] = incl;
+    __syncthreads();
+    int base = 0;
+    for (int w2 = 0; w2 < warp; ++w2) base += s_warp[w2];
+    a.tile_hist[(int64_t)tid * a.hist_stride + tile] = (uint32_t)(base + incl);
 }
 
 // One CTA per digit: exclusive scan of H[d][.] over the tiles (in place).
@@ -447,13 +503,11 @@ cudaError_t launch_radix_pass(const RadixPassArgs& a, cudaStream_t stream) {
     if (a.gen) {
         static bool configured = false;
         if (!configured) {
-            cudaFuncSetAttribute(radix_hist_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(GenSmem));
             cudaFuncSetAttribute(radix_scatter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(GenSmem));
             configured = true;
         }
-        radix_hist_kernel<true><<<grid, kRadixThreads, sizeof(GenSmem), stream>>>(a);
+        gen_hist_kernel<<<grid, kRadixThreads, 0, stream>>>(a);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
         radix_scan_kernel<<<kRadixDigits, 256, 0, stream>>>(a);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -480,17 +534,35 @@ __global__ void __launch_bounds__(256) ranges_kernel(RangesArgs a) {
     }
     const uint32_t M = (uint32_t)min((int64_t)a.counters[GES_CTR_SLOTS], a.max_pairs);
     if (blockIdx.x == 0 && threadIdx.x == 0) a.counters[GES_CTR_PAIRS] = M;
-    // entry m opens every tile in (key[m-1], key[m]]; the end closes (key[M-1], T]
-    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m <= (int64_t)M;
-         m += (int64_t)gridDim.x * blockDim.x) {
-        const int prev = m > 0 ? (int)a.keys[m - 1] : -1;
-        const int cur = m < (int64_t)M ? (int)a.keys[m] : T;
-        for (int t = prev + 1; t <= cur; ++t) a.ranges[t] = (uint32_t)m;
+    // entry m opens every tile in (tile[m-1], tile[m]]; the end closes (tile[M-1], T];
+    // tile(key) = ty * tiles_x + tx for key = ty << 8 | tx (monotone in the key)
+    auto tile_of = [&](uint32_t k) { return (int)(k >> 8) * a.tiles_x + (int)(k & 255u); };
+    // four entries per thread (one 16-B load) plus the entry before them
+    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 4 * g <= (int64_t)M;
+         g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t m0 = 4 * g;
+        uint32_t k[4];
+        if (m0 + 4 <= (int64_t)M) {
+            const uint4 q = __ldg(reinterpret_cast<const uint4*>(a.keys + m0));
+            k[0] = q.x; k[1] = q.y; k[2] = q.z; k[3] = q.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) k[j] = (m0 + j < (int64_t)M) ? __ldg(a.keys + m0 + j) : 0u;
+        }
+        int prev = m0 > 0 ? tile_of(__ldg(a.keys + m0 - 1)) : -1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t m = m0 + j;
+            if (m > (int64_t)M) break;
+            const int cur = m < (int64_t)M ? tile_of(k[j]) : T;
+            for (int t = prev + 1; t <= cur; ++t) a.ranges[t] = (uint32_t)m;
+            prev = cur;
+        }
     }
 }
 
 cudaError_t launch_ranges(const RangesArgs& a, cudaStream_t stream) {
-    const int grid = std::max(1, std::min(num_sms() * 8, (int)((a.max_pairs + 255) / 256)));
+    const int grid = std::max(1, std::min(num_sms() * 8, (int)((a.max_pairs / 4 + 256) / 256)));
     ranges_kernel<<<grid, 256, 0, stream>>>(a);
     return cudaGetLastError();
 }

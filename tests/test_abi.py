@@ -74,6 +74,11 @@ def test_workspace_and_frame_carving_host_only():
     assert lib.ges_frame_init(C.c_void_p(base), nbytes - 1, P, W, H, cap, C.byref(f)) == L.GES_ERR_CAPACITY
     assert lib.ges_frame_init(C.c_void_p(base + 8), nbytes, P, W, H, cap, C.byref(f)) == L.GES_ERR_INVALID_ARG
     assert lib.ges_frame_init(None, nbytes, P, W, H, cap, C.byref(f)) == L.GES_ERR_INVALID_ARG
+    for (w2, h2) in ((4097, 16), (16, 4097)):  # > 256 tiles on an axis
+        big = lib.ges_workspace_bytes(P, w2, h2, cap)
+        assert lib.ges_frame_init(C.c_void_p(base), big, P, w2, h2, cap, C.byref(f)) == L.GES_ERR_INVALID_ARG
+    assert lib.ges_frame_init(C.c_void_p(base), lib.ges_workspace_bytes(P, 4096, 4096, cap), P, 4096, 4096, cap,
+                              C.byref(f)) == L.GES_OK
     assert lib.ges_sort(None, None) == L.GES_ERR_INVALID_ARG
     assert lib.ges_status_string(L.GES_ERR_CAPACITY).decode().startswith("workspace")
     assert b"sm_100a" in lib.ges_version()
