@@ -51,6 +51,24 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
+STAGE_KERNEL = {"preprocess": "preprocess_kernel", "render_fwd": "render_fwd_kernel",
+                "render_bwd_tiles": "render_bwd_kernel", "backward_particles": "particle_bwd_kernel"}
+
+
+def committed_traffic(stage):
+    """DRAM bytes per launch of the stage's kernel from the committed ncu --set full
+    capture (profiles/r1_traffic.json, written by tools/summarize_ncu.py traffic), or None."""
+    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    k = STAGE_KERNEL.get(stage)
+    if not k or not os.path.exists(p):
+        return None, None
+    with open(p) as f:
+        d = json.load(f).get(k)
+    if not d:
+        return None, None
+    return d["traffic_bytes"], f"ncu --set full, {d['report']} ({d['kernel']})"
+
+
 # ---------------------------------------------------------------------------
 # clocks sampled during the timed region
 # ---------------------------------------------------------------------------
@@ -300,7 +318,7 @@ def run_ours(args) -> None:
         "render_fwd": ("alu", e_comp * FWD_OPS / (stage_ms[2] / 1e3) / 1e12, alu_peak, "Tinstr/s"),
         "preprocess": ("hbm", preprocess_bytes(P, int(cnt.visible), scene.particles.sh_degree)
                        / (stage_ms[0] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"),
-        "sort": ("hbm", sort_algorithmic_bytes(P, int(cnt.visible), int(cnt.pairs), frame.c.tile_bits)
+        "sort": ("hbm", sort_algorithmic_bytes(P, int(cnt.visible), int(cnt.pairs), frame.c.tiles_y > 1)
                  / (stage_ms[1] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"),
         "backward_particles": ("hbm", particle_bwd_bytes(P, int(cnt.visible), K) / (stage_ms[4] / 1e3) / 1e9,
                                peaks["hbm_gbs"], "GB/s"),
@@ -308,6 +326,7 @@ def run_ours(args) -> None:
     dom = max(range(5), key=lambda i: stage_ms[i])
     dname = stage_names[dom]
     bound, achieved, peak, unit = rows[dname]
+    traffic, traffic_src = committed_traffic(dname)
 
     e2e = None
     if not args.no_e2e:
@@ -328,7 +347,7 @@ def run_ours(args) -> None:
             "counts": {"visible": int(cnt.visible), "pairs": int(cnt.pairs), "slots": int(cnt.slots), "evals_fwd": e_fwd,
                        "composited": e_comp},
             "roofline": {"kernel": dname, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": peak_src if bound == "hbm" else
                          f"derived: {sms} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (median SM clock under load)",
                          "all": {k: {"bound": v[0], "achieved": v[1], "peak": v[2], "unit": v[3],
@@ -356,12 +375,12 @@ def preprocess_bytes(P, V, deg):
     return P * (4 * 12 + 54) + V * (4 * 3 * K + 8)
 
 
-def sort_algorithmic_bytes(P, V, M, tile_bits):
+def sort_algorithmic_bytes(P, V, M, two_pass):
     depth = P * 4 + V * 8 + 3 * V * 16      # pass 0 reads P keys, writes V (key, id); passes 1-3 move V
     scan = V * (4 + 8 + 4 + 16)             # item scan: ids, rects; offsets + item records out
-    # tile passes: the first reads the item records (+ 32 B geometry) and writes the M member
-    # (tile, id) pairs; the second moves them (8 B in, 8 B out); ranges read the M sorted tile ids
-    tiles = V * 48 + M * 8 + (M * 16 if tile_bits > 8 else 0) + M * 4
+    # pair passes: the first reads the item records and writes the M (key, id) pairs; the second
+    # moves them (8 B in, 8 B out); ranges read the M sorted keys
+    tiles = V * 16 + M * 8 + (M * 16 if two_pass else 0) + M * 4
     return depth + scan + tiles
 
 

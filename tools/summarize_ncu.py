@@ -2,8 +2,12 @@
 
     python tools/summarize_ncu.py launches <launches.csv>      # per-kernel device time
     python tools/summarize_ncu.py full <report.ncu-rep>        # key metrics per captured kernel
+    python tools/summarize_ncu.py traffic <report.ncu-rep>...  # JSON: DRAM bytes per launch per kernel
 """
+import json
+import re
 import collections
+import os
 import csv
 import io
 import subprocess
@@ -59,5 +63,31 @@ def full(path):
         print(f"| {key[0]} | `{key[1]}` | " + " | ".join(d.get(c, "") for c in cols) + " |")
 
 
+def _bytes(v, unit):
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+    return float(v.replace(",", "")) * scale.get(unit.strip(), 1.0)
+
+
+def traffic(*paths):
+    """dram__bytes_read.sum + dram__bytes_write.sum per captured launch, keyed by the
+    kernel's base name (template arguments dropped): what bench.py reports as
+    roofline.traffic for its dominant kernel."""
+    out = {}
+    for path in paths:
+        raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rr = list(csv.reader(io.StringIO(raw)))
+        hr, units = rr[0], rr[1]
+        for row in rr[2:]:
+            name = row[hr.index("Kernel Name")].split("(")[0]
+            base = re.sub(r"<.*", "", name.replace("void ", "")).split("::")[-1]
+            rd = _bytes(row[hr.index("dram__bytes_read.sum")], units[hr.index("dram__bytes_read.sum")])
+            wr = _bytes(row[hr.index("dram__bytes_write.sum")], units[hr.index("dram__bytes_write.sum")])
+            dur = row[hr.index("gpu__time_duration.sum")] if "gpu__time_duration.sum" in hr else ""
+            out[base] = {"kernel": name, "dram_read_bytes": rd, "dram_write_bytes": wr, "traffic_bytes": rd + wr,
+                         "duration": f"{dur} {units[hr.index('gpu__time_duration.sum')]}" if dur else None,
+                         "report": os.path.basename(path)}
+    print(json.dumps(out, indent=1, sort_keys=True))
+
+
 if __name__ == "__main__":
-    {"launches": launches, "full": full}[sys.argv[1]](sys.argv[2])
+    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
