@@ -28,191 +28,201 @@ __global__ void __launch_bounds__(256) particle_bwd_kernel(ParticleBwdArgs a) {
         float* p = base + (size_t)plane * P + i;
         *p = acc ? (*p + val) : val;
     };
-    if (a.status[i] != GES_VISIBLE) {
-        if (!acc) {
-            for (int c = 0; c < 3; ++c) { a.g_mean[(size_t)c * P + i] = 0.f; a.g_log_scale[(size_t)c * P + i] = 0.f; }
-            for (int c = 0; c < 4; ++c) a.g_quat[(size_t)c * P + i] = 0.f;
-            a.g_opacity_logit[i] = 0.f;
-            for (int c = 0; c < 3 * K; ++c) a.g_sh[(size_t)c * P + i] = 0.f;
-            a.g_beta[i] = 0.f;
+    // Every thread of a warp stores every plane in the same instruction (zeros
+    // for particles that are not visible): full 32-B sectors, no partial-sector
+    // read-modify-write in DRAM.
+    const bool vis = a.status[i] == GES_VISIBLE;
+    float o_mean[3] = {0.f, 0.f, 0.f}, o_ls[3] = {0.f, 0.f, 0.f}, o_q[4] = {0.f, 0.f, 0.f, 0.f};
+    float o_op = 0.f, o_beta = 0.f;
+    float Y[16], drgb[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Y[k] = 0.f;
+    if (vis) {
+        const CamParams& cam = a.cam;
+        const CamDerived cd = derive_camera(cam);
+        const float W[9] = {cam.R[0], cam.R[1], cam.R[2], cam.R[3], cam.R[4], cam.R[5], cam.R[6], cam.R[7], cam.R[8]};
+        const int fl = a.flags[i];
+        // ---- forward recompute ----
+        const float m0 = __ldg(a.mean + i), m1 = __ldg(a.mean + P + i), m2 = __ldg(a.mean + 2 * P + i);
+        const float tx = W[0] * m0 + W[1] * m1 + W[2] * m2 + cam.t[0];
+        const float ty = W[3] * m0 + W[4] * m1 + W[5] * m2 + cam.t[1];
+        const float tz = W[6] * m0 + W[7] * m1 + W[8] * m2 + cam.t[2];
+        const float q0 = __ldg(a.quat + i), q1 = __ldg(a.quat + P + i), q2 = __ldg(a.quat + 2 * P + i),
+                    q3 = __ldg(a.quat + 3 * P + i);
+        const float nq = sqrtf(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
+        const float inq = 1.0f / nq;
+        const float w = q0 * inq, x = q1 * inq, y = q2 * inq, z = q3 * inq;
+        const float R[9] = {1.f - 2.f * (y * y + z * z), 2.f * (x * y - w * z), 2.f * (x * z + w * y),
+                            2.f * (x * y + w * z), 1.f - 2.f * (x * x + z * z), 2.f * (y * z - w * x),
+                            2.f * (x * z - w * y), 2.f * (y * z + w * x), 1.f - 2.f * (x * x + y * y)};
+        float phi = 1.f, mfac = 1.f, dm_dbeta = 0.f;
+        if (!a.gaussian_only) {
+            phi = 2.f / (1.f + expf(-(a.rho * (__ldg(a.beta + i) - 2.f))));
+            const float dphi = a.rho * phi * (1.f - 0.5f * phi);
+            if (a.phi_mode == GES_PHI_VARIANCE) { mfac = sqrtf(phi); dm_dbeta = 0.5f * dphi / mfac; }
+            else { mfac = phi; dm_dbeta = dphi; }
         }
-        return;
-    }
-    const CamParams& cam = a.cam;
-    const CamDerived cd = derive_camera(cam);
-    const float W[9] = {cam.R[0], cam.R[1], cam.R[2], cam.R[3], cam.R[4], cam.R[5], cam.R[6], cam.R[7], cam.R[8]};
-    const int fl = a.flags[i];
-    // ---- forward recompute ----
-    const float m0 = __ldg(a.mean + i), m1 = __ldg(a.mean + P + i), m2 = __ldg(a.mean + 2 * P + i);
-    const float tx = W[0] * m0 + W[1] * m1 + W[2] * m2 + cam.t[0];
-    const float ty = W[3] * m0 + W[4] * m1 + W[5] * m2 + cam.t[1];
-    const float tz = W[6] * m0 + W[7] * m1 + W[8] * m2 + cam.t[2];
-    const float q0 = __ldg(a.quat + i), q1 = __ldg(a.quat + P + i), q2 = __ldg(a.quat + 2 * P + i),
-                q3 = __ldg(a.quat + 3 * P + i);
-    const float nq = sqrtf(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
-    const float inq = 1.0f / nq;
-    const float w = q0 * inq, x = q1 * inq, y = q2 * inq, z = q3 * inq;
-    const float R[9] = {1.f - 2.f * (y * y + z * z), 2.f * (x * y - w * z), 2.f * (x * z + w * y),
-                        2.f * (x * y + w * z), 1.f - 2.f * (x * x + z * z), 2.f * (y * z - w * x),
-                        2.f * (x * z - w * y), 2.f * (y * z + w * x), 1.f - 2.f * (x * x + y * y)};
-    float phi = 1.f, mfac = 1.f, dm_dbeta = 0.f;
-    if (!a.gaussian_only) {
-        phi = 2.f / (1.f + expf(-(a.rho * (__ldg(a.beta + i) - 2.f))));
-        const float dphi = a.rho * phi * (1.f - 0.5f * phi);
-        if (a.phi_mode == GES_PHI_VARIANCE) { mfac = sqrtf(phi); dm_dbeta = 0.5f * dphi / mfac; }
-        else { mfac = phi; dm_dbeta = dphi; }
-    }
-    float s[3], se[3];
+        float s[3], se[3];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) { s[k] = expf(__ldg(a.log_scale + (size_t)k * P + i)); se[k] = s[k] * mfac; }
-    float M[9];
+        for (int k = 0; k < 3; ++k) { s[k] = expf(__ldg(a.log_scale + (size_t)k * P + i)); se[k] = s[k] * mfac; }
+        float M[9];
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
+        for (int j = 0; j < 3; ++j)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) M[j * 3 + k] = R[j * 3 + k] * se[k];
-    float Sig[9];
+            for (int k = 0; k < 3; ++k) M[j * 3 + k] = R[j * 3 + k] * se[k];
+        float Sig[9];
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
+        for (int j = 0; j < 3; ++j)
 #pragma unroll
-        for (int l = 0; l < 3; ++l) Sig[j * 3 + l] = M[j * 3] * M[l * 3] + M[j * 3 + 1] * M[l * 3 + 1] + M[j * 3 + 2] * M[l * 3 + 2];
-    const bool clx = (fl >> 3) & 1, cly = (fl >> 4) & 1;
-    const float Lx = (tx / tz > 0.f) ? cd.limx : -cd.limx, Ly = (ty / tz > 0.f) ? cd.limy : -cd.limy;
-    const float txc = clx ? Lx * tz : tx, tyc = cly ? Ly * tz : ty;
-    const float itz = 1.f / tz, itz2 = itz * itz;
-    const float j00 = cam.fx * itz, j02 = -cam.fx * txc * itz2, j11 = cam.fy * itz, j12 = -cam.fy * tyc * itz2;
-    float Tm[6];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        Tm[k] = j00 * W[k] + j02 * W[6 + k];
-        Tm[3 + k] = j11 * W[3 + k] + j12 * W[6 + k];
-    }
-    float TS[6];
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
-#pragma unroll
-        for (int k = 0; k < 3; ++k)
-            TS[j * 3 + k] = Tm[j * 3] * Sig[k] + Tm[j * 3 + 1] * Sig[3 + k] + Tm[j * 3 + 2] * Sig[6 + k];
-    const float A = TS[0] * Tm[0] + TS[1] * Tm[1] + TS[2] * Tm[2] + kDilation;
-    const float B = TS[0] * Tm[3] + TS[1] * Tm[4] + TS[2] * Tm[5];
-    const float C = TS[3] * Tm[3] + TS[4] * Tm[4] + TS[5] * Tm[5] + kDilation;
-    const float det = A * C - B * B;
-    const float idet = 1.f / det, idet2 = idet * idet;
-
-    // ---- incoming 2-D gradients (pre-scaled conic -> a, b, c) ----
-    // 12-float record (du, dv, dA, dB | dC, dkappa, dr, dg | db, -, -, -), zeroed
-    // after reading so the buffer is clean for the next frame's backward
-    float4* rec = reinterpret_cast<float4*>(a.grad2d) + (size_t)i * (kGrad2dStride / 4);
-    const float4 r0 = rec[0], r1 = rec[1], r2 = rec[2];
-    const float du = r0.x, dv = r0.y;
-    const float da = r0.z * (-0.5f * kLog2e);
-    const float db = r0.w * (-kLog2e);
-    const float dc = r1.x * (-0.5f * kLog2e);
-    const float dk = r1.y;
-    float drgb[3] = {r1.z, r1.w, r2.x};
-
-    // conic -> (A, B, C)
-    const float gA = da * (-C * C * idet2) + db * (B * C * idet2) + dc * (idet - A * C * idet2);
-    const float gB = da * (2.f * B * C * idet2) + db * (-idet - 2.f * B * B * idet2) + dc * (2.f * A * B * idet2);
-    const float gC = da * (idet - A * C * idet2) + db * (A * B * idet2) + dc * (-A * A * idet2);
-    // dSig = T^T Gc T with Gc = [[gA, gB], [0, gC]]
-    float dSig[9];
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-#pragma unroll
-        for (int l = 0; l < 3; ++l)
-            dSig[k * 3 + l] = Tm[k] * (gA * Tm[l] + gB * Tm[3 + l]) + Tm[3 + k] * (gC * Tm[3 + l]);
-    // dT = (Gc + Gc^T) T Sig
-    float dT[6];
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        dT[k] = 2.f * gA * TS[k] + gB * TS[3 + k];
-        dT[3 + k] = gB * TS[k] + 2.f * gC * TS[3 + k];
-    }
-    // Sig = M M^T -> dM = (dSig + dSig^T) M
-    float dM[9];
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
+            for (int l = 0; l < 3; ++l) Sig[j * 3 + l] = M[j * 3] * M[l * 3] + M[j * 3 + 1] * M[l * 3 + 1] + M[j * 3 + 2] * M[l * 3 + 2];
+        const bool clx = (fl >> 3) & 1, cly = (fl >> 4) & 1;
+        const float Lx = (tx / tz > 0.f) ? cd.limx : -cd.limx, Ly = (ty / tz > 0.f) ? cd.limy : -cd.limy;
+        const float txc = clx ? Lx * tz : tx, tyc = cly ? Ly * tz : ty;
+        const float itz = 1.f / tz, itz2 = itz * itz;
+        const float j00 = cam.fx * itz, j02 = -cam.fx * txc * itz2, j11 = cam.fy * itz, j12 = -cam.fy * tyc * itz2;
+        float Tm[6];
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            float acc2 = 0.f;
-#pragma unroll
-            for (int l = 0; l < 3; ++l) acc2 += (dSig[j * 3 + l] + dSig[l * 3 + j]) * M[l * 3 + k];
-            dM[j * 3 + k] = acc2;
+            Tm[k] = j00 * W[k] + j02 * W[6 + k];
+            Tm[3 + k] = j11 * W[3 + k] + j12 * W[6 + k];
         }
-    float dR[9], dse[3] = {0.f, 0.f, 0.f};
+        float TS[6];
 #pragma unroll
-    for (int j = 0; j < 3; ++j)
+        for (int j = 0; j < 2; ++j)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) { dR[j * 3 + k] = dM[j * 3 + k] * se[k]; dse[k] += dM[j * 3 + k] * R[j * 3 + k]; }
-    float dbeta = 0.f;
+            for (int k = 0; k < 3; ++k)
+                TS[j * 3 + k] = Tm[j * 3] * Sig[k] + Tm[j * 3 + 1] * Sig[3 + k] + Tm[j * 3 + 2] * Sig[6 + k];
+        const float A = TS[0] * Tm[0] + TS[1] * Tm[1] + TS[2] * Tm[2] + kDilation;
+        const float B = TS[0] * Tm[3] + TS[1] * Tm[4] + TS[2] * Tm[5];
+        const float C = TS[3] * Tm[3] + TS[4] * Tm[4] + TS[5] * Tm[5] + kDilation;
+        const float det = A * C - B * B;
+        const float idet = 1.f / det, idet2 = idet * idet;
+
+        // ---- incoming 2-D gradients (pre-scaled conic -> a, b, c) ----
+        // 12-float record (du, dv, dA, dB | dC, dkappa, dr, dg | db, -, -, -), zeroed
+        // after reading so the buffer is clean for the next frame's backward
+        const float4* rrec = reinterpret_cast<const float4*>(a.grad2d) + (size_t)i * (kGrad2dStride / 4);
+        const float4 r0 = rrec[0], r1 = rrec[1], r2 = rrec[2];
+        const float du = r0.x, dv = r0.y;
+        const float da = r0.z * (-0.5f * kLog2e);
+        const float db = r0.w * (-kLog2e);
+        const float dc = r1.x * (-0.5f * kLog2e);
+        const float dk = r1.y;
+        drgb[0] = r1.z; drgb[1] = r1.w; drgb[2] = r2.x;
+
+        // conic -> (A, B, C)
+        const float gA = da * (-C * C * idet2) + db * (B * C * idet2) + dc * (idet - A * C * idet2);
+        const float gB = da * (2.f * B * C * idet2) + db * (-idet - 2.f * B * B * idet2) + dc * (2.f * A * B * idet2);
+        const float gC = da * (idet - A * C * idet2) + db * (A * B * idet2) + dc * (-A * A * idet2);
+        // dSig = T^T Gc T with Gc = [[gA, gB], [0, gC]]
+        float dSig[9];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
-        put(a.g_log_scale, k, dse[k] * se[k]);
-        dbeta += dse[k] * s[k] * dm_dbeta;
-    }
-    put(a.g_beta, 0, dbeta);
-    float dq[4];
-    dq[0] = dR[1] * (-2.f * z) + dR[2] * (2.f * y) + dR[3] * (2.f * z) + dR[5] * (-2.f * x) + dR[6] * (-2.f * y) + dR[7] * (2.f * x);
-    dq[1] = dR[1] * (2.f * y) + dR[2] * (2.f * z) + dR[3] * (2.f * y) + dR[4] * (-4.f * x) + dR[5] * (-2.f * w) +
-            dR[6] * (2.f * z) + dR[7] * (2.f * w) + dR[8] * (-4.f * x);
-    dq[2] = dR[0] * (-4.f * y) + dR[1] * (2.f * x) + dR[2] * (2.f * w) + dR[3] * (2.f * x) + dR[5] * (2.f * z) +
-            dR[6] * (-2.f * w) + dR[7] * (2.f * z) + dR[8] * (-4.f * y);
-    dq[3] = dR[0] * (-4.f * z) + dR[1] * (-2.f * w) + dR[2] * (2.f * x) + dR[3] * (2.f * w) + dR[4] * (-4.f * z) +
-            dR[5] * (2.f * y) + dR[6] * (2.f * x) + dR[7] * (2.f * y);
-    const float qh[4] = {w, x, y, z};
-    const float dotq = qh[0] * dq[0] + qh[1] * dq[1] + qh[2] * dq[2] + qh[3] * dq[3];
+        for (int k = 0; k < 3; ++k)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) put(a.g_quat, k, (dq[k] - qh[k] * dotq) * inq);
-    // T = J W -> dJ = dT W^T (entries 00, 02, 11, 12)
-    const float dj00 = dT[0] * W[0] + dT[1] * W[1] + dT[2] * W[2];
-    const float dj02 = dT[0] * W[6] + dT[1] * W[7] + dT[2] * W[8];
-    const float dj11 = dT[3] * W[3] + dT[4] * W[4] + dT[5] * W[5];
-    const float dj12 = dT[3] * W[6] + dT[4] * W[7] + dT[5] * W[8];
-    float dtx = 0.f, dty = 0.f, dtz = 0.f;
-    dtz += dj00 * (-cam.fx * itz2) + dj11 * (-cam.fy * itz2);
-    if (!clx) { dtx += dj02 * (-cam.fx * itz2); dtz += dj02 * (2.f * cam.fx * tx * itz2 * itz); }
-    else { dtz += dj02 * (cam.fx * Lx * itz2); }
-    if (!cly) { dty += dj12 * (-cam.fy * itz2); dtz += dj12 * (2.f * cam.fy * ty * itz2 * itz); }
-    else { dtz += dj12 * (cam.fy * Ly * itz2); }
-    dtx += du * cam.fx * itz; dtz += du * (-cam.fx * tx * itz2);
-    dty += dv * cam.fy * itz; dtz += dv * (-cam.fy * ty * itz2);
-    float dmean[3];
+            for (int l = 0; l < 3; ++l)
+                dSig[k * 3 + l] = Tm[k] * (gA * Tm[l] + gB * Tm[3 + l]) + Tm[3 + k] * (gC * Tm[3 + l]);
+        // dT = (Gc + Gc^T) T Sig
+        float dT[6];
 #pragma unroll
-    for (int k = 0; k < 3; ++k) dmean[k] = W[k] * dtx + W[3 + k] * dty + W[6 + k] * dtz;
-    // colour
-    const float d0 = m0 - cd.c0, d1 = m1 - cd.c1, d2 = m2 - cd.c2;
-    const float dn = sqrtf(d0 * d0 + d1 * d1 + d2 * d2), idn = 1.f / dn;
-    const float ux = d0 * idn, uy = d1 * idn, uz = d2 * idn;
-    float Y[16];
-    sh_basis<K>(ux, uy, uz, Y);
+        for (int k = 0; k < 3; ++k) {
+            dT[k] = 2.f * gA * TS[k] + gB * TS[3 + k];
+            dT[3 + k] = gB * TS[k] + 2.f * gC * TS[3 + k];
+        }
+        // Sig = M M^T -> dM = (dSig + dSig^T) M
+        float dM[9];
 #pragma unroll
-    for (int ch = 0; ch < 3; ++ch)
-        if ((fl >> ch) & 1) drgb[ch] = 0.f;
-    float wsh[16];
+        for (int j = 0; j < 3; ++j)
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-        float acc3 = 0.f;
+            for (int k = 0; k < 3; ++k) {
+                float acc2 = 0.f;
 #pragma unroll
-        for (int ch = 0; ch < 3; ++ch) acc3 += drgb[ch] * __ldg(a.sh + (size_t)(3 * k + ch) * P + i);
-        wsh[k] = acc3;
-    }
+                for (int l = 0; l < 3; ++l) acc2 += (dSig[j * 3 + l] + dSig[l * 3 + j]) * M[l * 3 + k];
+                dM[j * 3 + k] = acc2;
+            }
+        float dR[9], dse[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) { dR[j * 3 + k] = dM[j * 3 + k] * se[k]; dse[k] += dM[j * 3 + k] * R[j * 3 + k]; }
+        float dbeta = 0.f;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            o_ls[k] = dse[k] * se[k];
+            dbeta += dse[k] * s[k] * dm_dbeta;
+        }
+        o_beta = dbeta;
+        float dq[4];
+        dq[0] = dR[1] * (-2.f * z) + dR[2] * (2.f * y) + dR[3] * (2.f * z) + dR[5] * (-2.f * x) + dR[6] * (-2.f * y) + dR[7] * (2.f * x);
+        dq[1] = dR[1] * (2.f * y) + dR[2] * (2.f * z) + dR[3] * (2.f * y) + dR[4] * (-4.f * x) + dR[5] * (-2.f * w) +
+                dR[6] * (2.f * z) + dR[7] * (2.f * w) + dR[8] * (-4.f * x);
+        dq[2] = dR[0] * (-4.f * y) + dR[1] * (2.f * x) + dR[2] * (2.f * w) + dR[3] * (2.f * x) + dR[5] * (2.f * z) +
+                dR[6] * (-2.f * w) + dR[7] * (2.f * z) + dR[8] * (-4.f * y);
+        dq[3] = dR[0] * (-4.f * z) + dR[1] * (-2.f * w) + dR[2] * (2.f * x) + dR[3] * (2.f * w) + dR[4] * (-4.f * z) +
+                dR[5] * (2.f * y) + dR[6] * (2.f * x) + dR[7] * (2.f * y);
+        const float qh[4] = {w, x, y, z};
+        const float dotq = qh[0] * dq[0] + qh[1] * dq[1] + qh[2] * dq[2] + qh[3] * dq[3];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o_q[k] = (dq[k] - qh[k] * dotq) * inq;
+        // T = J W -> dJ = dT W^T (entries 00, 02, 11, 12)
+        const float dj00 = dT[0] * W[0] + dT[1] * W[1] + dT[2] * W[2];
+        const float dj02 = dT[0] * W[6] + dT[1] * W[7] + dT[2] * W[8];
+        const float dj11 = dT[3] * W[3] + dT[4] * W[4] + dT[5] * W[5];
+        const float dj12 = dT[3] * W[6] + dT[4] * W[7] + dT[5] * W[8];
+        float dtx = 0.f, dty = 0.f, dtz = 0.f;
+        dtz += dj00 * (-cam.fx * itz2) + dj11 * (-cam.fy * itz2);
+        if (!clx) { dtx += dj02 * (-cam.fx * itz2); dtz += dj02 * (2.f * cam.fx * tx * itz2 * itz); }
+        else { dtz += dj02 * (cam.fx * Lx * itz2); }
+        if (!cly) { dty += dj12 * (-cam.fy * itz2); dtz += dj12 * (2.f * cam.fy * ty * itz2 * itz); }
+        else { dtz += dj12 * (cam.fy * Ly * itz2); }
+        dtx += du * cam.fx * itz; dtz += du * (-cam.fx * tx * itz2);
+        dty += dv * cam.fy * itz; dtz += dv * (-cam.fy * ty * itz2);
+        float dmean[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) dmean[k] = W[k] * dtx + W[3 + k] * dty + W[6 + k] * dtz;
+        // colour
+        const float d0 = m0 - cd.c0, d1 = m1 - cd.c1, d2 = m2 - cd.c2;
+        const float dn = sqrtf(d0 * d0 + d1 * d1 + d2 * d2), idn = 1.f / dn;
+        const float ux = d0 * idn, uy = d1 * idn, uz = d2 * idn;
+        sh_basis<K>(ux, uy, uz, Y);
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch)
+            if ((fl >> ch) & 1) drgb[ch] = 0.f;
+        float wsh[16];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            float acc3 = 0.f;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) acc3 += drgb[ch] * __ldg(a.sh + (size_t)(3 * k + ch) * P + i);
+            wsh[k] = acc3;
+        }
+#pragma unroll
+        for (int k = K; k < 16; ++k) wsh[k] = 0.f;
+        float gx, gy, gz;
+        sh_basis_grad_dot<K>(ux, uy, uz, wsh, gx, gy, gz);
+        const float dotd = ux * gx + uy * gy + uz * gz;
+        dmean[0] += (gx - ux * dotd) * idn;
+        dmean[1] += (gy - uy * dotd) * idn;
+        dmean[2] += (gz - uz * dotd) * idn;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) o_mean[k] = dmean[k];
+        const float kap = 1.f / (1.f + expf(-__ldg(a.opacity_logit + i)));
+        o_op = dk * kap * (1.f - kap);
+    }  // vis
+#pragma unroll
+    for (int k = 0; k < 3; ++k) put(a.g_mean, k, o_mean[k]);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) put(a.g_log_scale, k, o_ls[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) put(a.g_quat, k, o_q[k]);
+    put(a.g_opacity_logit, 0, o_op);
 #pragma unroll
     for (int k = 0; k < K; ++k)
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) put(a.g_sh, 3 * k + ch, Y[k] * drgb[ch]);
-#pragma unroll
-    for (int k = K; k < 16; ++k) wsh[k] = 0.f;
-    float gx, gy, gz;
-    sh_basis_grad_dot<K>(ux, uy, uz, wsh, gx, gy, gz);
-    const float dotd = ux * gx + uy * gy + uz * gz;
-    dmean[0] += (gx - ux * dotd) * idn;
-    dmean[1] += (gy - uy * dotd) * idn;
-    dmean[2] += (gz - uz * dotd) * idn;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) put(a.g_mean, k, dmean[k]);
-    const float kap = 1.f / (1.f + expf(-__ldg(a.opacity_logit + i)));
-    put(a.g_opacity_logit, 0, dk * kap * (1.f - kap));
-    // leave the 2-D record zeroed for the next backward (ges.h)
+    put(a.g_beta, 0, o_beta);
+    // leave the 2-D record zeroed for the next backward (ges.h); every particle's
+    // record is written so the 48-B records cover whole sectors
+    float4* rec = reinterpret_cast<float4*>(a.grad2d) + (size_t)i * (kGrad2dStride / 4);
     const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
     rec[0] = z4; rec[1] = z4; rec[2] = z4;
 }
