@@ -142,6 +142,9 @@ typedef struct {
     uint16_t *rect;        /* [P][4] tile rect x0, y0, x1, y1 (exclusive ends)           */
     uint8_t *status;       /* [P] ges_particle_status                                   */
     uint8_t *flags;        /* [P] bit0-2 rgb clamped at 0, bit3/4 Jacobian x/y clamped   */
+    float *drgb_ddir;      /* [9][P] d rgb_c / d u_d (u: unit view direction, dY/du of the
+                              SH polynomials), plane 3c + d; 0 where rgb_c is clamped
+                              or the particle is not visible (read by S5b)            */
     /* ---- S2 depth sort of the visible particles ---- */
     uint32_t *vis_key[2];  /* [P] depth bits (0xffffffff = not visible), ping-pong */
     uint32_t *vis_val[2];  /* [P] particle index, ping-pong                      */

@@ -35,14 +35,18 @@ def is_stale() -> bool:
     return any(os.path.getmtime(d) > t for d in _deps())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not is_stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB) -> str:
+    """Compile and link.  `defines` (-DNAME=VALUE tuning knobs) and `out` are for
+    experiment variants (`python _build.py --variant NAME -DKNOB=V ...` writes
+    build/variants/NAME/libges.so; load it with GES_LIB=<path>)."""
+    if out == LIB and not defines and not force and not is_stale():
         return LIB
-    os.makedirs(BUILD_DIR, exist_ok=True)
+    bdir = BUILD_DIR if out == LIB else os.path.join(os.path.dirname(out), "obj")
+    os.makedirs(bdir, exist_ok=True)
 
     def compile_one(src):
-        obj = os.path.join(BUILD_DIR, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-Xptxas", "-v", "-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(bdir, src.replace(".cu", ".o"))
+        cmd = [NVCC, *FLAGS, *defines, "-Xptxas", "-v", "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
@@ -52,16 +56,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = out + f".tmp{os.getpid()}"
     cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs, "-cudart", "static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, out)
     if verbose:
-        print(f"built {LIB}", file=sys.stderr)
-    return LIB
+        print(f"built {out}", file=sys.stderr)
+    return out
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
+    args = sys.argv[1:]
+    defs = [a for a in args if a.startswith("-D")]
+    if "--variant" in args:
+        name = args[args.index("--variant") + 1]
+        build(verbose=True, defines=defs, out=os.path.join(BUILD_DIR, "variants", name, "libges.so"))
+    else:
+        build(force="--force" in args or bool(defs), verbose=True, defines=defs)

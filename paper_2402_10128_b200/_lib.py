@@ -12,7 +12,8 @@ import os
 from . import _build
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libges.so")
+# GES_LIB: load an experiment variant built by `_build.py --variant` instead
+LIB_PATH = os.environ.get("GES_LIB") or os.path.join(_HERE, "libges.so")
 
 GES_OK, GES_ERR_INVALID_ARG, GES_ERR_CAPACITY, GES_ERR_CUDA, GES_ERR_UNSUPPORTED = range(5)
 GES_PHI_SCALE, GES_PHI_VARIANCE = 0, 1
@@ -56,6 +57,7 @@ class ges_frame(C.Structure):
         ("num_tiles", C.c_int32), ("tile_bits", C.c_int32), ("sh_degree_max", C.c_int32), ("_pad", C.c_int32),
         ("depth", C.c_void_p), ("pay0", C.c_void_p), ("pay1", C.c_void_p), ("pay2", C.c_void_p),
         ("radius", C.c_void_p), ("rect", C.c_void_p), ("status", C.c_void_p), ("flags", C.c_void_p),
+        ("drgb_ddir", C.c_void_p),
         ("vis_key", C.c_void_p * 2), ("vis_val", C.c_void_p * 2), ("sorted_vis", C.c_void_p),
         ("radix_hist", C.c_void_p), ("radix_total", C.c_void_p), ("item_offset", C.c_void_p), ("item_rec", C.c_void_p),
         ("tile_first", C.c_void_p), ("pair_tile", C.c_void_p), ("pair_val", C.c_void_p),
@@ -81,7 +83,7 @@ def load(build_if_missing: bool = True) -> C.CDLL:
     """Loads libges.so (building it first if the sources are newer)."""
     global _lib
     if _lib is None:
-        if build_if_missing:
+        if build_if_missing and not os.environ.get("GES_LIB"):
             _build.build()
         if not os.path.exists(LIB_PATH):
             raise GESError(f"libges.so not built ({LIB_PATH}); run __graft_entry__.build()")

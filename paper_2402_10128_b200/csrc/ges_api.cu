@@ -74,6 +74,7 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     g.rect = (uint16_t*)take(8 * (size_t)P);
     g.status = (uint8_t*)take((size_t)P);
     g.flags = (uint8_t*)take((size_t)P);
+    g.drgb_ddir = (float*)take(sizeof(float) * 9 * (size_t)P);
     for (int k = 0; k < 2; ++k) {
         g.vis_key[k] = (uint32_t*)take(sizeof(uint32_t) * P);
         g.vis_val[k] = (uint32_t*)take(sizeof(uint32_t) * P);
@@ -159,6 +160,7 @@ ges_status ges_preprocess(const ges_particles* particles, const ges_camera* came
     a.cam = cam_params(camera);
     a.depth = frame->depth; a.pay0 = (float4*)frame->pay0; a.pay1 = (float4*)frame->pay1; a.pay2 = frame->pay2;
     a.radius = frame->radius; a.rect = (ushort4*)frame->rect; a.status = frame->status; a.flags = frame->flags;
+    a.drgb_ddir = frame->drgb_ddir;
     a.vis_key = frame->vis_key[0];
     a.counters = (unsigned long long*)frame->counters;
     return cuda_status(launch_preprocess(a, s));
@@ -276,7 +278,7 @@ ges_status ges_backward_particles(const ges_particles* particles, const ges_came
     q.P = (int)particles->P; q.sh_degree = particles->sh_degree;
     q.rho = settings->rho; q.phi_mode = settings->phi_mode; q.gaussian_only = settings->gaussian_only ? 1 : 0;
     q.cam = cam_params(camera);
-    q.status = frame->status; q.flags = frame->flags; q.grad2d = frame->grad2d;
+    q.status = frame->status; q.flags = frame->flags; q.grad2d = frame->grad2d; q.drgb_ddir = frame->drgb_ddir;
     q.g_mean = grads->mean; q.g_log_scale = grads->log_scale; q.g_quat = grads->quat;
     q.g_opacity_logit = grads->opacity_logit; q.g_sh = grads->sh; q.g_beta = grads->beta;
     q.accumulate = grads->accumulate;

@@ -23,6 +23,7 @@ struct PreprocessArgs {
     ushort4* rect;
     uint8_t* status;
     uint8_t* flags;
+    float* drgb_ddir;     // [9][P] d rgb / d unit direction (for S5b)
     uint32_t* vis_key;    // [P] depth bits, 0xffffffff if not visible
     unsigned long long* counters;
 };
@@ -128,6 +129,7 @@ struct ParticleBwdArgs {
     CamParams cam;
     const uint8_t* status;
     const uint8_t* flags;
+    const float* drgb_ddir;           // [9][P] from S1
     float* grad2d;
     float *g_mean, *g_log_scale, *g_quat, *g_opacity_logit, *g_sh, *g_beta;
     int accumulate;

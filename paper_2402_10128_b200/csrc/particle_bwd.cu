@@ -18,8 +18,12 @@
 
 namespace ges {
 
+#ifndef GES_PBWD_MINB  // tuning knob: min resident CTAs per SM (register cap)
+#define GES_PBWD_MINB 4
+#endif
+
 template <int K>
-__global__ void __launch_bounds__(256) particle_bwd_kernel(ParticleBwdArgs a) {
+__global__ void __launch_bounds__(256, GES_PBWD_MINB) particle_bwd_kernel(ParticleBwdArgs a) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.P) return;
     const int P = a.P;
@@ -187,18 +191,15 @@ __global__ void __launch_bounds__(256) particle_bwd_kernel(ParticleBwdArgs a) {
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch)
             if ((fl >> ch) & 1) drgb[ch] = 0.f;
-        float wsh[16];
+        // d L / d u = sum_ch dL/drgb_ch * d rgb_ch / d u (S1 stored the Jacobian, zero rows
+        // where the channel was clamped)
+        float gx = 0.f, gy = 0.f, gz = 0.f;
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            float acc3 = 0.f;
-#pragma unroll
-            for (int ch = 0; ch < 3; ++ch) acc3 += drgb[ch] * __ldg(a.sh + (size_t)(3 * k + ch) * P + i);
-            wsh[k] = acc3;
+        for (int ch = 0; ch < 3; ++ch) {
+            gx += drgb[ch] * __ldg(a.drgb_ddir + (size_t)(3 * ch) * P + i);
+            gy += drgb[ch] * __ldg(a.drgb_ddir + (size_t)(3 * ch + 1) * P + i);
+            gz += drgb[ch] * __ldg(a.drgb_ddir + (size_t)(3 * ch + 2) * P + i);
         }
-#pragma unroll
-        for (int k = K; k < 16; ++k) wsh[k] = 0.f;
-        float gx, gy, gz;
-        sh_basis_grad_dot<K>(ux, uy, uz, wsh, gx, gy, gz);
         const float dotd = ux * gx + uy * gy + uz * gz;
         dmean[0] += (gx - ux * dotd) * idn;
         dmean[1] += (gy - uy * dotd) * idn;

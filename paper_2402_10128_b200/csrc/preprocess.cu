@@ -20,6 +20,7 @@ namespace ges {
 
 struct PreOut {
     float depth, u, v, ca, cb, cc, kappa, r, g, b;
+    float J[9];  // d rgb / d unit direction, 0 unless visible and unclamped
     int radius, x0, y0, x1, y1;
     uint8_t status, flags;
 };
@@ -49,6 +50,8 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
     PreOut o;
     o.u = o.v = o.ca = o.cb = o.cc = o.kappa = o.r = o.g = o.b = 0.0f;
     o.radius = o.x0 = o.y0 = o.x1 = o.y1 = 0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) o.J[k] = 0.0f;
     o.flags = 0;
     const float mx = in.mx, my = in.my, mz = in.mz;
     // camera space t = W mu + t
@@ -176,17 +179,28 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
     const float dx = fsub(mx, cd.c0), dy = fsub(my, cd.c1), dz = fsub(mz, cd.c2);
     float dn2 = fmul(dx, dx); dn2 = ffma(dy, dy, dn2); dn2 = ffma(dz, dz, dn2);
     const float dn = fsqrt(dn2);
+    const float ux = fdiv(dx, dn), uy = fdiv(dy, dn), uz = fdiv(dz, dn);
     float Y[16];
-    sh_basis<K>(fdiv(dx, dn), fdiv(dy, dn), fdiv(dz, dn), Y);
+    sh_basis<K>(ux, uy, uz, Y);
     float rgb[3];
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-        float acc = fmul(Y[0], __ldg(a.sh + (size_t)ch * P + i));
+        float w[16];
 #pragma unroll
-        for (int k = 1; k < K; ++k) acc = ffma(Y[k], __ldg(a.sh + (size_t)(3 * k + ch) * P + i), acc);
+        for (int k = 0; k < 16; ++k) w[k] = (k < K) ? __ldg(a.sh + (size_t)(3 * k + ch) * P + i) : 0.0f;
+        float acc = fmul(Y[0], w[0]);
+#pragma unroll
+        for (int k = 1; k < K; ++k) acc = ffma(Y[k], w[k], acc);
         acc = fadd(acc, 0.5f);
-        if (acc < 0.0f) { acc = 0.0f; fl |= (uint8_t)(1u << ch); }
+        const bool clamped = acc < 0.0f;
+        if (clamped) { acc = 0.0f; fl |= (uint8_t)(1u << ch); }
         rgb[ch] = acc;
+        // d rgb_ch / d u for S5b (so the backward need not re-read the SH planes)
+        float gx, gy, gz;
+        sh_basis_grad_dot<K>(ux, uy, uz, w, gx, gy, gz);
+        o.J[3 * ch] = clamped ? 0.0f : gx;
+        o.J[3 * ch + 1] = clamped ? 0.0f : gy;
+        o.J[3 * ch + 2] = clamped ? 0.0f : gz;
     }
     o.r = rgb[0]; o.g = rgb[1]; o.b = rgb[2];
     o.flags = fl;
@@ -200,7 +214,10 @@ constexpr int kPreThreads = 256;
 // its S1 state and its sort key (fp32 depth bits, or 0xffffffff when not
 // visible -- dropped by depth pass 0, which thereby compacts the visible set).
 template <int K>
-__global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(PreprocessArgs a) {
+#ifndef GES_PRE_MINB  // tuning knob: min resident CTAs per SM (register cap)
+#define GES_PRE_MINB 3
+#endif
+__global__ void __launch_bounds__(kPreThreads, GES_PRE_MINB) preprocess_kernel(PreprocessArgs a) {
     const int tid = threadIdx.x, lane = tid & 31;
     const CamDerived cd = derive_camera(a.cam);
     uint32_t nvis = 0;
@@ -218,6 +235,8 @@ __global__ void __launch_bounds__(kPreThreads, 3) preprocess_kernel(PreprocessAr
             a.rect[i] = make_ushort4((uint16_t)o.x0, (uint16_t)o.y0, (uint16_t)o.x1, (uint16_t)o.y1);
             a.status[i] = o.status;
             a.flags[i] = o.flags;
+#pragma unroll
+            for (int k = 0; k < 9; ++k) a.drgb_ddir[(size_t)k * a.P + i] = o.J[k];
             vis = o.status == GES_VISIBLE;
             a.vis_key[i] = vis ? __float_as_uint(o.depth) : 0xffffffffu;
         }

@@ -29,7 +29,13 @@
 
 namespace ges {
 
-constexpr int kBatch = 512;               // list entries staged per barrier
+constexpr int kBatch = 512;
+#ifndef GES_RFWD_MINB  // tuning knobs: min resident CTAs per SM (register cap)
+#define GES_RFWD_MINB 1
+#endif
+#ifndef GES_RBWD_MINB
+#define GES_RBWD_MINB 1
+#endif               // list entries staged per barrier
 constexpr float kCullMargin = 0.01f;      // log2 units (0.7% in alpha)
 
 struct Splat {
@@ -158,7 +164,7 @@ __device__ __forceinline__ void stage_batch(const float4* pay0, const float4* pa
 }
 
 template <int PPT, bool DIAG>
-__global__ void __launch_bounds__(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdArgs a) {
+__global__ void __launch_bounds__(Layout<PPT>::kThreads, GES_RFWD_MINB) render_fwd_kernel(RenderFwdArgs a) {
     using Lt = Layout<PPT>;
     __shared__ float4 s_g0[kBatch];
     __shared__ float4 s_g1[kBatch];
@@ -309,7 +315,7 @@ __device__ __forceinline__ void red_add(float* addr, float x) {
 }
 
 template <int PPT>
-__global__ void __launch_bounds__(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdArgs a) {
+__global__ void __launch_bounds__(Layout<PPT>::kThreads, GES_RBWD_MINB) render_bwd_kernel(RenderBwdArgs a) {
     using Lt = Layout<PPT>;
     __shared__ float4 s_g0[kBatch];
     __shared__ float4 s_g1[kBatch];

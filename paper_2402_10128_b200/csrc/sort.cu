@@ -129,6 +129,9 @@ cudaError_t launch_item_scan(const ItemScanArgs& a, int64_t max_items, cudaStrea
 // computes from the items alone.
 // ---------------------------------------------------------------------------
 constexpr int kRadixThreads = 256;
+#ifndef GES_SCAT_MINB  // tuning knob: min resident CTAs per SM for the scatter kernels
+#define GES_SCAT_MINB 3
+#endif
 constexpr int kRadixItems = 16;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096
 constexpr int kRadixWarps = kRadixThreads / 32;
@@ -392,7 +395,7 @@ __global__ void __launch_bounds__(256) radix_scan_kernel(RadixPassArgs a) {
 }
 
 template <bool GEN>
-__global__ void __launch_bounds__(kRadixThreads) radix_scatter_kernel(RadixPassArgs a) {
+__global__ void __launch_bounds__(kRadixThreads, GES_SCAT_MINB) radix_scatter_kernel(RadixPassArgs a) {
     __shared__ uint32_t s_keys[kRadixTile + kRadixTile / 32];
     __shared__ uint32_t s_vals[kRadixTile + kRadixTile / 32];
     __shared__ uint32_t s_whist[kRadixWarps][kRadixDigits];

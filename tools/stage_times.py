@@ -27,12 +27,12 @@ img = r.forward(params, cam, st)
 r.grow(int(r.frame.counts().slots))
 dL = torch.from_numpy(gi.upstream_grad(sc.seed, 0, cam.width, cam.height)).cuda()
 grads = G.PlanarParams.zeros(params.P, params.sh_degree)
-names = ["preprocess", "sort", "render_fwd", "render_bwd"]
+names = ["preprocess", "sort", "render_fwd", "render_bwd_tiles", "backward_particles"]
 acc = {n: [] for n in names}
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for it in range(args.steps + 3):
     flush.fill_(1)
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
     ev[0].record()
     G.ges_preprocess(params, cam, st, r.frame)
     ev[1].record()
@@ -40,12 +40,14 @@ for it in range(args.steps + 3):
     ev[2].record()
     G.ges_render_fwd(r.frame, st, img)
     ev[3].record()
-    G.ges_render_bwd(params, cam, st, r.frame, dL, grads)
+    G.ges_render_bwd_tiles(st, r.frame, dL)
     ev[4].record()
-    ev[4].synchronize()
+    G.ges_backward_particles(params, cam, st, r.frame, grads)
+    ev[5].record()
+    ev[5].synchronize()
     if it >= 3:
         for i, n in enumerate(names):
             acc[n].append(ev[i].elapsed_time(ev[i + 1]))
-res = {n: statistics.median(v) for n, v in acc.items()}
-res["total"] = sum(res.values())
+res = {n: round(statistics.median(v), 4) for n, v in acc.items()}
+res["total"] = round(sum(res.values()), 4)
 print(json.dumps({"tag": args.tag, "env": {k: v for k, v in os.environ.items() if k.startswith("GES_")}, **res}))
