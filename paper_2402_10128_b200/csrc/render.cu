@@ -30,11 +30,16 @@
 namespace ges {
 
 constexpr int kBatch = 512;
-#ifndef GES_RFWD_MINB  // tuning knobs: min resident CTAs per SM (register cap)
-#define GES_RFWD_MINB 1
+// tuning knobs: min resident CTAs per SM (register cap); unset = ptxas's choice
+#ifdef GES_RFWD_MINB
+#define GES_RFWD_LB(t) __launch_bounds__(t, GES_RFWD_MINB)
+#else
+#define GES_RFWD_LB(t) __launch_bounds__(t)
 #endif
-#ifndef GES_RBWD_MINB
-#define GES_RBWD_MINB 1
+#ifdef GES_RBWD_MINB
+#define GES_RBWD_LB(t) __launch_bounds__(t, GES_RBWD_MINB)
+#else
+#define GES_RBWD_LB(t) __launch_bounds__(t)
 #endif               // list entries staged per barrier
 constexpr float kCullMargin = 0.01f;      // log2 units (0.7% in alpha)
 
@@ -164,7 +169,7 @@ __device__ __forceinline__ void stage_batch(const float4* pay0, const float4* pa
 }
 
 template <int PPT, bool DIAG>
-__global__ void __launch_bounds__(Layout<PPT>::kThreads, GES_RFWD_MINB) render_fwd_kernel(RenderFwdArgs a) {
+__global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdArgs a) {
     using Lt = Layout<PPT>;
     __shared__ float4 s_g0[kBatch];
     __shared__ float4 s_g1[kBatch];
@@ -315,7 +320,7 @@ __device__ __forceinline__ void red_add(float* addr, float x) {
 }
 
 template <int PPT>
-__global__ void __launch_bounds__(Layout<PPT>::kThreads, GES_RBWD_MINB) render_bwd_kernel(RenderBwdArgs a) {
+__global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdArgs a) {
     using Lt = Layout<PPT>;
     __shared__ float4 s_g0[kBatch];
     __shared__ float4 s_g1[kBatch];
@@ -373,16 +378,16 @@ __global__ void __launch_bounds__(Layout<PPT>::kThreads, GES_RBWD_MINB) render_b
         for (int i = nw - 1; i >= 0; --i) {
             const int j = s_list[warp][i];
             const uint32_t pos = (uint32_t)(b_begin + j);
-            float v[9];
-#pragma unroll
-            for (int c = 0; c < 9; ++c) v[c] = 0.0f;
             bool contrib = false;
             const float4 g0 = s_g0[j];
             const float4 g1 = s_g1[j];
             const float rb = s_b[j];
             const float dx = __fsub_rn(g0.x, fpx);
-            const float twoA = g0.z + g0.z, twoC = g1.x + g1.x;
-            // branch-free per pixel: the forward's decisions become predicates
+            // Per pixel only the sums the chain rule needs: with q = G dalpha (kappa
+            // factored out) and dp2 = kappa ln2 q, the conic/mean terms are
+            // sum dp2 (dx, dy) and sum dp2 (dx^2, dx dy, dy^2); dx is the thread's
+            // column, so S0 = sum q, S1 = sum q dy, S2 = sum q dy^2 suffice.
+            float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, dk = 0.0f, dr = 0.0f, dgc = 0.0f, dbc = 0.0f;
 #pragma unroll
             for (int k = 0; k < PPT; ++k) {
                 const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
@@ -399,20 +404,31 @@ __global__ void __launch_bounds__(Layout<PPT>::kThreads, GES_RBWD_MINB) render_b
                 const float dalpha = Tk * cgk - (suffix[k] + bg_term[k]) * inv_om;
                 const float dal = (m && araw < kAlphaMax) ? dalpha : 0.0f;
                 suffix[k] += cgk * w;
-                v[6] += w * gr[k];
-                v[7] += w * gg[k];
-                v[8] += w * gb[k];
-                v[5] += G * dal;
-                // alpha = kappa 2^p2  ->  d alpha / d p2 = alpha ln 2
-                const float dp2 = (p2raw <= 0.0f) ? araw * dal * 0.69314718055994531f : 0.0f;
-                const float e = dp2 * dx, f = dp2 * dy;
-                v[0] += twoA * e + g0.w * f;   // d p2 / d u
-                v[1] += g0.w * e + twoC * f;   // d p2 / d v
-                v[2] += e * dx;                // d p2 / d A
-                v[3] += e * dy;                // d p2 / d B
-                v[4] += f * dy;                // d p2 / d C
+                dr += w * gr[k];
+                dgc += w * gg[k];
+                dbc += w * gb[k];
+                const float q = G * dal;          // d L / d kappa contribution
+                dk += q;
+                const float qm = (p2raw <= 0.0f) ? q : 0.0f;  // exponent not clamped (R19)
+                S0 += qm;
+                const float t = qm * dy;
+                S1 += t;
+                S2 += t * dy;
                 T[k] = Tk;
             }
+            // alpha = kappa 2^p2: d alpha / d p2 = alpha ln 2, so dL/dp2 = kappa ln2 q
+            const float kl = g1.y * 0.69314718055994531f;
+            const float E = kl * dx * S0, F = kl * S1;  // sum dp2 dx, sum dp2 dy
+            float v[9];
+            v[0] = 2.0f * g0.z * E + g0.w * F;   // d p2 / d u
+            v[1] = g0.w * E + 2.0f * g1.x * F;   // d p2 / d v
+            v[2] = dx * E;                       // d p2 / d A
+            v[3] = dx * F;                       // d p2 / d B
+            v[4] = kl * S2;                      // d p2 / d C
+            v[5] = dk;
+            v[6] = dr;
+            v[7] = dgc;
+            v[8] = dbc;
             if (__any_sync(0xffffffffu, contrib)) {
                 const float r = warp_reduce9(v);
                 if (red_comp >= 0 && (lane & 1) == 0)
