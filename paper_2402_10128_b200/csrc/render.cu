@@ -60,12 +60,25 @@ __device__ __forceinline__ Splat load_splat(const float4* pay0, const float4* pa
     return s;
 }
 
-// p2 = A dx^2 + B dx dy + C dy^2 (log2 units), fixed op order: the forward and
+// p2 = A dx^2 + B dx dy + C dy^2 (log2 units) as c0 + dy (c1 + C dy) with the
+// per-(entry, thread) constants c0 = A dx^2, c1 = B dx (a thread's pixels share
+// their column, so dx): two FMAs per pixel.  Fixed op order: the forward and
 // the backward evaluate exactly this sequence, so their decisions agree.
-__device__ __forceinline__ float raw_exponent(float A, float B, float C, float dx, float dy) {
-    const float t1 = __fmaf_rn(A, dx, __fmul_rn(B, dy));
-    const float t2 = __fmul_rn(__fmul_rn(C, dy), dy);
-    return __fmaf_rn(dx, t1, t2);
+struct ExpCol {
+    float c0, c1;
+};
+__device__ __forceinline__ ExpCol exp_col(float A, float B, float dx) {
+    return ExpCol{__fmul_rn(__fmul_rn(A, dx), dx), __fmul_rn(B, dx)};
+}
+__device__ __forceinline__ float raw_exponent(ExpCol e, float C, float dy) {
+    return __fmaf_rn(dy, __fmaf_rn(C, dy, e.c1), e.c0);
+}
+
+// 1 / x for x in [0.01, 1] (x = 1 - alpha): one MUFU.RCP, no range fix-up.
+__device__ __forceinline__ float fast_rcp(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
 // Minimum of Q = a x^2 + b x y + c y^2 (a, c > 0, 4ac > b^2) over the box
@@ -207,12 +220,13 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
             const float4 g1 = s_g1[j];
             const float gbl = s_b[j];
             const float dx = __fsub_rn(g0.x, fpx);
+            const ExpCol ec = exp_col(g0.z, g0.w, dx);
             const uint32_t pos1 = b0 - start + j + 1;
             // branch-free per pixel: the decisions become predicates
 #pragma unroll
             for (int k = 0; k < PPT; ++k) {
                 const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
-                const float p2 = fminf(raw_exponent(g0.z, g0.w, g1.x, dx, dy), 0.0f);
+                const float p2 = fminf(raw_exponent(ec, g1.x, dy), 0.0f);
                 const float alpha = fminf(kAlphaMax, __fmul_rn(g1.y, fast_exp2(p2)));
                 const bool live = !((done >> k) & 1u) && alpha >= kAlphaMin;
                 const float Tn = __fmul_rn(T[k], __fsub_rn(1.0f, alpha));
@@ -338,13 +352,14 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
     const bool ovf = a.counters[GES_CTR_OVERFLOW] != 0;
     const uint32_t start = ovf ? 0u : a.ranges[tile];
     const int plane = a.W * a.H;
-    float T[PPT], gr[PPT], gg[PPT], gb[PPT], bg_term[PPT], suffix[PPT];
+    // U = T_final bg . g + sum over entries behind of c_j . g alpha_j T_j
+    float T[PPT], gr[PPT], gg[PPT], gb[PPT], U[PPT];
     uint32_t last[PPT];
     uint32_t my_max = 0;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
         const int py = py0 + 4 * k;
-        T[k] = 1.0f; gr[k] = gg[k] = gb[k] = 0.0f; last[k] = 0; suffix[k] = 0.0f;
+        T[k] = 1.0f; gr[k] = gg[k] = gb[k] = 0.0f; last[k] = 0;
         float Tfin = 1.0f;
         if (px < a.W && py < a.H && !ovf) {
             const int pix = py * a.W + px;
@@ -355,7 +370,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             gb[k] = a.dL_dimage[2 * plane + pix];
         }
         T[k] = Tfin;
-        bg_term[k] = Tfin * (gr[k] * a.bg[0] + gg[k] * a.bg[1] + gb[k] * a.bg[2]);
+        U[k] = Tfin * (gr[k] * a.bg[0] + gg[k] * a.bg[1] + gb[k] * a.bg[2]);
         my_max = max(my_max, last[k]);
     }
     if (tid == 0) s_max = 0;
@@ -383,6 +398,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             const float4 g1 = s_g1[j];
             const float rb = s_b[j];
             const float dx = __fsub_rn(g0.x, fpx);
+            const ExpCol ec = exp_col(g0.z, g0.w, dx);
             // Per pixel only the sums the chain rule needs: with q = G dalpha (kappa
             // factored out) and dp2 = kappa ln2 q, the conic/mean terms are
             // sum dp2 (dx, dy) and sum dp2 (dx^2, dx dy, dy^2); dx is the thread's
@@ -391,19 +407,19 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
 #pragma unroll
             for (int k = 0; k < PPT; ++k) {
                 const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
-                const float p2raw = raw_exponent(g0.z, g0.w, g1.x, dx, dy);
+                const float p2raw = raw_exponent(ec, g1.x, dy);
                 const float G = fast_exp2(fminf(p2raw, 0.0f));
                 const float araw = __fmul_rn(g1.y, G);
                 const float alpha = fminf(kAlphaMax, araw);
                 const bool m = pos < last[k] && alpha >= kAlphaMin;
                 contrib |= m;
-                const float inv_om = __fdividef(1.0f, __fsub_rn(1.0f, alpha));
+                const float inv_om = fast_rcp(__fsub_rn(1.0f, alpha));
                 const float Tk = m ? T[k] * inv_om : T[k];  // transmittance before this entry
                 const float cgk = g1.z * gr[k] + g1.w * gg[k] + rb * gb[k];
                 const float w = m ? alpha * Tk : 0.0f;
-                const float dalpha = Tk * cgk - (suffix[k] + bg_term[k]) * inv_om;
+                const float dalpha = Tk * cgk - U[k] * inv_om;
                 const float dal = (m && araw < kAlphaMax) ? dalpha : 0.0f;
-                suffix[k] += cgk * w;
+                U[k] += cgk * w;
                 dr += w * gr[k];
                 dgc += w * gg[k];
                 dbc += w * gb[k];
