@@ -14,6 +14,36 @@ import subprocess
 import sys
 
 
+# launches of each kernel in one bench step (config 3: 13 tile rows > 1 -> two pair passes)
+STEP = {"preprocess_kernel<16>": 1, "radix_hist_kernel<0>": 5, "radix_scan_kernel": 6, "radix_scatter_kernel<0>": 5,
+        "item_scan_kernel": 1, "gen_hist_kernel": 1, "radix_scatter_kernel<1>": 1, "ranges_kernel": 1,
+        "render_fwd_kernel<2, 0>": 1, "render_bwd_kernel<4>": 1, "particle_bwd_kernel<16>": 1}
+
+
+def share(path):
+    """Per-step share of each kernel from the launch list (median x launches per step)."""
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
+    h, data = rows[hi], rows[hi + 1:]
+    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+    agg = collections.defaultdict(list)
+    for r in data:
+        k = r[ki].split("(")[0].replace("void ", "").replace("ges::", "")
+        agg[k].append(float(r[vi]) / 1000.0)
+    tot = 0.0
+    out = []
+    for k, n in STEP.items():
+        v = sorted(agg.get(k, [0.0]))
+        t = v[len(v) // 2] * n
+        out.append((k, n, t))
+        tot += t
+    print("| kernel | per step | us per step (median x n) | share |")
+    print("|---|---|---|---|")
+    for k, n, t in out:
+        print(f"| `{k}` | {n} | {t:.1f} | {100 * t / tot:.1f}% |")
+    print(f"| total | | {tot:.1f} | |")
+
+
 def launches(path):
     rows = list(csv.reader(open(path)))
     hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
@@ -90,4 +120,4 @@ def traffic(*paths):
 
 
 if __name__ == "__main__":
-    {"launches": launches, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
+    {"launches": launches, "share": share, "full": full, "traffic": traffic}[sys.argv[1]](*sys.argv[2:])
