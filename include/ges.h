@@ -97,6 +97,14 @@ typedef struct {
     int32_t phi_mode;           /* ges_phi_mode                                              */
     int32_t gaussian_only;      /* 1: beta ignored (phi = 1) -- the equivalent Gaussian rasterizer */
     float background[3];
+    /* Screen-tile band (BASELINE config 3 "the 8 GPUs splitting
+     * screen-tile bands of one frame"): render only the tile rows
+     * r = tile_row_begin + k * tile_row_step.  (0, 0) and (0, 1) = the full frame;
+     * otherwise 0 <= tile_row_begin < tile_row_step.  ges_preprocess records the band
+     * in the frame; ges_render_* require the same band.  Per-tile lists and pixels
+     * of a band are identical to the full frame's; pixels outside it are untouched;
+     * the S5 gradients of all bands sum to the full frame's. */
+    int32_t tile_row_begin, tile_row_step;
 } ges_settings;
 
 /* Gradients, planar [C][P] fp32 in the parameter layout.  accumulate = 1 adds
@@ -133,6 +141,9 @@ typedef struct {
     int64_t P, pair_capacity;
     int32_t width, height, tiles_x, tiles_y, num_tiles, tile_bits;
     int32_t sh_degree_max, _pad;
+    int32_t band_begin, band_step; /* tile rows of this frame: band_begin + k band_step (ges_settings) */
+    int32_t band_rows, _pad2;      /* k < band_rows; the lists and ranges index band tiles
+                                      t = k * tiles_x + tx, and rect rows are band rows k  */
     /* ---- S1 per-particle state ---- */
     float *depth;          /* [P] camera-space z                                       */
     float *pay0;           /* [P][4] (u, v, a, b): projected mean, conic a, b           */

@@ -37,7 +37,7 @@ class ges_camera(C.Structure):
 
 class ges_settings(C.Structure):
     _fields_ = [("rho", C.c_float), ("phi_mode", C.c_int32), ("gaussian_only", C.c_int32),
-                ("background", C.c_float * 3)]
+                ("background", C.c_float * 3), ("tile_row_begin", C.c_int32), ("tile_row_step", C.c_int32)]
 
 
 class ges_grads(C.Structure):
@@ -55,6 +55,7 @@ class ges_frame(C.Structure):
         ("P", C.c_int64), ("pair_capacity", C.c_int64),
         ("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
         ("num_tiles", C.c_int32), ("tile_bits", C.c_int32), ("sh_degree_max", C.c_int32), ("_pad", C.c_int32),
+        ("band_begin", C.c_int32), ("band_step", C.c_int32), ("band_rows", C.c_int32), ("_pad2", C.c_int32),
         ("depth", C.c_void_p), ("pay0", C.c_void_p), ("pay1", C.c_void_p), ("pay2", C.c_void_p),
         ("radius", C.c_void_p), ("rect", C.c_void_p), ("status", C.c_void_p), ("flags", C.c_void_p),
         ("drgb_ddir", C.c_void_p),

@@ -33,12 +33,15 @@ class Settings:
     phi_mode: int = L.GES_PHI_SCALE
     gaussian_only: int = 0
     background: Sequence[float] = (0.0, 0.0, 0.0)
+    tile_row_begin: int = 0          # screen-tile band: rows begin + k*step (ges.h)
+    tile_row_step: int = 1
 
     def c(self) -> L.ges_settings:
         s = L.ges_settings()
         s.rho, s.phi_mode, s.gaussian_only = float(self.rho), int(self.phi_mode), int(self.gaussian_only)
         for k in range(3):
             s.background[k] = float(self.background[k])
+        s.tile_row_begin, s.tile_row_step = int(self.tile_row_begin), int(self.tile_row_step)
         return s
 
 

@@ -61,6 +61,7 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     std::memset(&g, 0, sizeof(g));
     g.P = P; g.pair_capacity = cap; g.width = W; g.height = H; g.tiles_x = tx; g.tiles_y = ty;
     g.num_tiles = (int32_t)T; g.tile_bits = std::max(1, bits_for(T)); g.sh_degree_max = 3;
+    g.band_begin = 0; g.band_step = 1; g.band_rows = ty;
     // --- zero-per-frame region (one memset in ges_preprocess) ---
     g.counters = (uint64_t*)take(sizeof(uint64_t) * GES_CTR_N);
     g.lookback = (uint32_t*)take(sizeof(uint32_t) * L.total);
@@ -113,6 +114,20 @@ bool particles_ok(const ges_particles* p) {
            p->log_scale && p->quat && p->opacity_logit && p->sh && p->beta;
 }
 
+// Band of a settings struct: (begin, step), validated; rows = #{r < tiles_y : r = begin + k step}.
+bool band_of(const ges_settings* s, int tiles_y, int* begin, int* step, int* rows) {
+    int b = s->tile_row_begin, n = s->tile_row_step;
+    if (n == 0 && b == 0) n = 1;
+    if (n < 1 || b < 0 || b >= n) return false;
+    *begin = b; *step = n; *rows = b < tiles_y ? (tiles_y - b + n - 1) / n : 0;
+    return true;
+}
+
+bool band_matches(const ges_settings* s, const ges_frame* f) {
+    int b, n, r;
+    return band_of(s, f->tiles_y, &b, &n, &r) && b == f->band_begin && n == f->band_step;
+}
+
 bool camera_ok(const ges_camera* c, const ges_frame* f) {
     return c && c->width == f->width && c->height == f->height && c->near_z > 0.0f && c->fx > 0.0f && c->fy > 0.0f;
 }
@@ -149,6 +164,9 @@ ges_status ges_preprocess(const ges_particles* particles, const ges_camera* came
     if (!frame || !settings || !particles_ok(particles) || !camera_ok(camera, frame) || particles->P != frame->P ||
         !(settings->rho >= 0.0f) || (settings->phi_mode != GES_PHI_SCALE && settings->phi_mode != GES_PHI_VARIANCE))
         return GES_ERR_INVALID_ARG;
+    int band_begin, band_step, band_rows;
+    if (!band_of(settings, frame->tiles_y, &band_begin, &band_step, &band_rows)) return GES_ERR_INVALID_ARG;
+    frame->band_begin = band_begin; frame->band_step = band_step; frame->band_rows = band_rows;
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(frame->counters, 0, frame->zero_bytes, s);
     if (e != cudaSuccess) return GES_ERR_CUDA;
@@ -162,6 +180,7 @@ ges_status ges_preprocess(const ges_particles* particles, const ges_camera* came
     a.radius = frame->radius; a.rect = (ushort4*)frame->rect; a.status = frame->status; a.flags = frame->flags;
     a.drgb_ddir = frame->drgb_ddir;
     a.vis_key = frame->vis_key[0];
+    a.band_begin = band_begin; a.band_step = band_step;
     a.counters = (unsigned long long*)frame->counters;
     return cuda_status(launch_preprocess(a, s));
 }
@@ -204,7 +223,7 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     if ((e = launch_item_scan(is, frame->P, s)) != cudaSuccess) return GES_ERR_CUDA;
     // stable sort of the pairs by tile id; the first pass generates them
     // pair keys are (ty << 8 | tx): pass 0 sorts by the column, pass 1 by the row
-    const int passes = frame->tiles_y > 1 ? 2 : 1;
+    const int passes = frame->band_rows > 1 ? 2 : 1;
     for (int d = 0; d < passes; ++d) {
         RadixPassArgs p;
         std::memset(&p, 0, sizeof(p));
@@ -220,7 +239,7 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
         p.hist_stride = hist_stride;
         p.digit_total = frame->radix_total + (d & 1) * kRadixDigits;
         p.shift = 8 * d;
-        p.digit_bits = std::max(1, bits_for(d == 0 ? frame->tiles_x : frame->tiles_y));
+        p.digit_bits = std::max(1, bits_for(d == 0 ? frame->tiles_x : frame->band_rows));
         p.overflow = ctr + GES_CTR_OVERFLOW;
         p.tiles_x = frame->tiles_x;
         p.sorted_vis = frame->sorted_vis;
@@ -233,7 +252,7 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     }
     RangesArgs r;
     r.keys = frame->list_tile;
-    r.tiles_x = frame->tiles_x; r.tiles_y = frame->tiles_y;
+    r.tiles_x = frame->tiles_x; r.tiles_y = frame->band_rows;
     r.ranges = frame->ranges; r.counters = ctr; r.max_pairs = frame->pair_capacity;
     if ((e = launch_ranges(r, s)) != cudaSuccess) return GES_ERR_CUDA;
     return GES_OK;
@@ -241,11 +260,12 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
 
 ges_status ges_render_fwd(ges_frame* frame, const ges_settings* settings, float* image, uint32_t* n_eval,
                           uint32_t* n_comp, void* stream) {
-    if (!frame || !settings || !image) return GES_ERR_INVALID_ARG;
+    if (!frame || !settings || !image || !band_matches(settings, frame)) return GES_ERR_INVALID_ARG;
     RenderFwdArgs a;
     a.pay0 = (const float4*)frame->pay0; a.pay1 = (const float4*)frame->pay1; a.pay2 = frame->pay2;
     a.list = frame->list; a.ranges = frame->ranges; a.counters = (const unsigned long long*)frame->counters;
-    a.W = frame->width; a.H = frame->height; a.tiles_x = frame->tiles_x; a.tiles_y = frame->tiles_y;
+    a.W = frame->width; a.H = frame->height; a.tiles_x = frame->tiles_x; a.tiles_y = frame->band_rows;
+    a.band_begin = frame->band_begin; a.band_step = frame->band_step;
     for (int k = 0; k < 3; ++k) a.bg[k] = settings->background[k];
     a.image = image; a.final_T = frame->final_T; a.n_contrib = frame->n_contrib; a.n_eval = n_eval;
     a.n_comp = n_comp;
@@ -254,11 +274,12 @@ ges_status ges_render_fwd(ges_frame* frame, const ges_settings* settings, float*
 
 ges_status ges_render_bwd_tiles(const ges_settings* settings, ges_frame* frame, const float* dL_dimage,
                                 void* stream) {
-    if (!frame || !settings || !dL_dimage) return GES_ERR_INVALID_ARG;
+    if (!frame || !settings || !dL_dimage || !band_matches(settings, frame)) return GES_ERR_INVALID_ARG;
     RenderBwdArgs b;
     b.pay0 = (const float4*)frame->pay0; b.pay1 = (const float4*)frame->pay1; b.pay2 = frame->pay2;
     b.list = frame->list; b.ranges = frame->ranges; b.counters = (const unsigned long long*)frame->counters;
-    b.W = frame->width; b.H = frame->height; b.tiles_x = frame->tiles_x; b.tiles_y = frame->tiles_y;
+    b.W = frame->width; b.H = frame->height; b.tiles_x = frame->tiles_x; b.tiles_y = frame->band_rows;
+    b.band_begin = frame->band_begin; b.band_step = frame->band_step;
     for (int k = 0; k < 3; ++k) b.bg[k] = settings->background[k];
     b.final_T = frame->final_T; b.n_contrib = frame->n_contrib; b.dL_dimage = dL_dimage; b.grad2d = frame->grad2d;
     b.P = (int)frame->P;

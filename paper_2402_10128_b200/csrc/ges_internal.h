@@ -25,6 +25,7 @@ struct PreprocessArgs {
     uint8_t* flags;
     float* drgb_ddir;     // [9][P] d rgb / d unit direction (for S5b)
     uint32_t* vis_key;    // [P] depth bits, 0xffffffff if not visible
+    int band_begin, band_step;  // rect rows become band rows (ges_settings tile band)
     unsigned long long* counters;
 };
 
@@ -94,7 +95,8 @@ struct RenderFwdArgs {
     const uint32_t* list;
     const uint32_t* ranges;
     const unsigned long long* counters;
-    int W, H, tiles_x, tiles_y;
+    int W, H, tiles_x, tiles_y;       // tiles_y = the band's rows (ges_frame.band_rows)
+    int band_begin, band_step;        // band tile row k is image tile row band_begin + k band_step
     float bg[3];
     float* image;
     float* final_T;
@@ -111,7 +113,8 @@ struct RenderBwdArgs {
     const uint32_t* list;
     const uint32_t* ranges;
     const unsigned long long* counters;
-    int W, H, tiles_x, tiles_y;
+    int W, H, tiles_x, tiles_y;       // tiles_y = the band's rows (ges_frame.band_rows)
+    int band_begin, band_step;        // band tile row k is image tile row band_begin + k band_step
     float bg[3];
     const float* final_T;
     const uint32_t* n_contrib;

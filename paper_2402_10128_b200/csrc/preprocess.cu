@@ -170,6 +170,11 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
     if (o.x1 < o.x0) o.x1 = o.x0;
     if (o.y1 < o.y0) o.y1 = o.y0;
     if (!(kr > 1.0f)) o.x1 = o.x0;
+    if (a.band_step > 1) {  // image tile rows -> band rows: row r = begin + k step <-> k
+        const int b = a.band_begin, n = a.band_step;
+        o.y0 = o.y0 > b ? (o.y0 - b + n - 1) / n : 0;
+        o.y1 = o.y1 > b ? (o.y1 - b + n - 1) / n : 0;
+    }
     o.u = u; o.v = v; o.ca = ca; o.cb = cb; o.cc = ccn;
     o.kappa = kap;
     o.radius = (int)rad;

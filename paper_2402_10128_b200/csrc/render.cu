@@ -146,11 +146,17 @@ __device__ __forceinline__ int compact_warp_list(const uint8_t* s_mask, int n, i
     return cnt;
 }
 
+// Band tile t = k tiles_x + tx is image tile (tx, band_begin + k band_step).
+__device__ __forceinline__ void tile_origin(int tile, int tiles_x, int band_begin, int band_step, int& x0, int& y0) {
+    x0 = (tile % tiles_x) * kTile;
+    y0 = (band_begin + (tile / tiles_x) * band_step) * kTile;
+}
+
 template <int PPT>
-__device__ __forceinline__ void pixel_base(int tile, int tiles_x, int tid, int& px, int& py0) {
+__device__ __forceinline__ void pixel_base(int tile_x0, int tile_y0, int tid, int& px, int& py0) {
     const int warp = tid >> 5, lane = tid & 31;
-    px = (tile % tiles_x) * kTile + 8 * (warp & 1) + (lane & 7);
-    py0 = (tile / tiles_x) * kTile + Layout<PPT>::kRegionH * (warp >> 1) + (lane >> 3);
+    px = tile_x0 + 8 * (warp & 1) + (lane & 7);
+    py0 = tile_y0 + Layout<PPT>::kRegionH * (warp >> 1) + (lane >> 3);
 }
 
 struct StagedBatch {
@@ -192,8 +198,9 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
     const int tile = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5;
     int px, py0;
-    pixel_base<PPT>(tile, a.tiles_x, tid, px, py0);
-    const int tile_x0 = (tile % a.tiles_x) * kTile, tile_y0 = (tile / a.tiles_x) * kTile;
+    int tile_x0, tile_y0;
+    tile_origin(tile, a.tiles_x, a.band_begin, a.band_step, tile_x0, tile_y0);
+    pixel_base<PPT>(tile_x0, tile_y0, tid, px, py0);
     const float fpx = (float)px + 0.5f;
     uint32_t start = a.ranges[tile], end = a.ranges[tile + 1];
     if (a.counters[GES_CTR_OVERFLOW]) start = end = 0;
@@ -346,8 +353,9 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
     const int tile = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int px, py0;
-    pixel_base<PPT>(tile, a.tiles_x, tid, px, py0);
-    const int tile_x0 = (tile % a.tiles_x) * kTile, tile_y0 = (tile / a.tiles_x) * kTile;
+    int tile_x0, tile_y0;
+    tile_origin(tile, a.tiles_x, a.band_begin, a.band_step, tile_x0, tile_y0);
+    pixel_base<PPT>(tile_x0, tile_y0, tid, px, py0);
     const float fpx = (float)px + 0.5f;
     const bool ovf = a.counters[GES_CTR_OVERFLOW] != 0;
     const uint32_t start = ovf ? 0u : a.ranges[tile];

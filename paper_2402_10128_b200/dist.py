@@ -1,19 +1,30 @@
-"""Multi-GPU plumbing for view data parallelism.
+"""Multi-GPU plumbing.
 
-Particles are replicated on every rank; rank r renders the views assigned to
-it (fwd + bwd, gradients accumulated into one flat planar buffer with
-`accumulate=1`), then ONE allreduce (sum) over the process group -- NCCL over
-NVLink on the B200 box, gloo in the CPU tests.  The gradient of the summed
-loss over all views is then identical on every rank.
+View data parallelism: particles are replicated on every rank; rank r renders
+the views assigned to it (fwd + bwd, gradients accumulated into one flat planar
+buffer with `accumulate=1`), then ONE allreduce (sum) over the process group --
+NCCL over NVLink on the B200 box, gloo in the CPU tests.  The gradient of the
+summed loss over all views is then identical on every rank.
+
+Screen-tile bands (BASELINE config 3: "the 8 GPUs splitting screen-tile bands
+of one frame"): rank r renders the tile rows r, r + N, r + 2N, ... of the same
+frame (interleaved for load balance; ges_settings tile_row_begin/step), then
+the band pixels are all-gathered into the full image.  The per-tile lists and
+pixels of a band are the full frame's, so the gathered image is bit-identical
+to a one-GPU render; for fwd+bwd the per-band particle gradients are summed
+with the same allreduce.
 """
 from __future__ import annotations
 
+import dataclasses
 from typing import List, Sequence
 
 import torch
 import torch.distributed as dist
 
 from .api import PlanarParams, Renderer, Settings
+
+TILE = 16
 
 
 def views_for_rank(n_views: int, rank: int, world: int) -> List[int]:
@@ -61,5 +72,62 @@ class ViewDataParallel:
             first = False
         if first:  # no views on this rank: contribute zeros
             self.grads.flat.zero_()
+        allreduce_grads(self.grads.flat, self.group)
+        return self.grads
+
+
+# ---------------------------------------------------------------------------
+# screen-tile bands
+# ---------------------------------------------------------------------------
+def band_pixel_rows(height: int, rank: int, world: int) -> torch.Tensor:
+    """Image rows rendered by `rank`: the 16-row tile rows rank, rank + world, ..."""
+    if world < 1 or not (0 <= rank < world):
+        raise ValueError("bad rank/world")
+    tiles_y = (height + TILE - 1) // TILE
+    rows = [r * TILE + j for r in range(rank, tiles_y, world) for j in range(TILE) if r * TILE + j < height]
+    return torch.tensor(rows, dtype=torch.long)
+
+
+def band_settings(settings: Settings, rank: int, world: int) -> Settings:
+    b, n = (rank, world) if world > 1 else (0, 1)
+    return dataclasses.replace(settings, tile_row_begin=b, tile_row_step=n)
+
+
+def gather_bands(image: torch.Tensor, rank: int, world: int, group=None) -> torch.Tensor:
+    """All-gather the band rows of a [3][H][W] image (each rank wrote only its own
+    band) into the full image on every rank (one all_gather of equal-size,
+    padded band buffers; rows are then scattered back in place)."""
+    if world == 1:
+        return image
+    H = image.shape[1]
+    rows = [band_pixel_rows(H, r, world).to(image.device) for r in range(world)]
+    n_max = max(int(x.numel()) for x in rows)
+    mine = torch.zeros((3, n_max, image.shape[2]), dtype=image.dtype, device=image.device)
+    mine[:, :rows[rank].numel()] = image.index_select(1, rows[rank])
+    parts = [torch.empty_like(mine) for _ in range(world)]
+    dist.all_gather(parts, mine, group=group)
+    out = torch.empty_like(image)
+    for r in range(world):
+        out.index_copy_(1, rows[r], parts[r][:, :rows[r].numel()])
+    return out
+
+
+class BandParallelFrame:
+    """This rank's screen-tile band of one frame: forward (gathered image) and
+    backward (allreduced parameter gradients)."""
+
+    def __init__(self, params: PlanarParams, camera, settings: Settings, rank: int, world: int, device="cuda",
+                 group=None):
+        self.params, self.camera, self.rank, self.world, self.group = params, camera, rank, world, group
+        self.settings = band_settings(settings, rank, world)
+        self.renderer = Renderer(params.P, camera.width, camera.height, device=device)
+        self.grads = PlanarParams.zeros(params.P, params.sh_degree, device)
+
+    def forward(self, stream=None) -> torch.Tensor:
+        img = self.renderer.forward(self.params, self.camera, self.settings, stream=stream)
+        return gather_bands(img, self.rank, self.world, self.group)
+
+    def backward(self, dL_dimage: torch.Tensor, stream=None) -> PlanarParams:
+        self.renderer.backward(self.params, self.camera, self.settings, dL_dimage, grads=self.grads, stream=stream)
         allreduce_grads(self.grads.flat, self.group)
         return self.grads

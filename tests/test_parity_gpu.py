@@ -239,3 +239,52 @@ def test_full_size_config3_sampled():
     d = np.abs(out["image"][:, sel] - ref["image"][:, sel])
     assert d.max() <= 1e-4, d.max()
     assert np.array_equal(out["n_contrib"][sel], ref["n_contrib"][sel])
+
+
+@pytest.mark.parametrize("world", [3, 8])
+def test_screen_tile_bands_match_full_frame(world):
+    """SURVEY.md §8(e) screen-tile bands: band b renders tile rows b, b + N, ...
+    Its per-tile lists and its pixels are bit-identical to the full frame's,
+    pixels outside the band are untouched, and the S5 gradients of all bands
+    sum to the full frame's (atomics reorder the sums: 1e-4 relative)."""
+    sc = gi.make_config(2)
+    cam = sc.cameras[0]
+    gs = G.Settings(rho=sc.rho)
+    dL = gi.upstream_grad(sc.seed, 0, cam.width, cam.height)
+    out = gpu_forward(sc.particles, cam, gs)
+    g_full, _ = gpu_backward(out, cam, gs, dL)
+    params = out["params"]
+    tx = out["renderer"].frame.c.tiles_x
+    ty = out["renderer"].frame.c.tiles_y
+    dLt = torch.from_numpy(dL).cuda()
+    acc = G.PlanarParams.zeros(params.P, params.sh_degree)
+    for b in range(world):
+        gb = G.Settings(rho=sc.rho, tile_row_begin=b, tile_row_step=world)
+        r = G.Renderer(params.P, cam.width, cam.height)
+        img = torch.full((3, cam.height, cam.width), -7.0, device="cuda")
+        r.forward(params, cam, gb, image=img)
+        r.backward(params, cam, gb, dLt, grads=acc, accumulate=b > 0)
+        torch.cuda.synchronize()
+        f = r.frame
+        rows_t = list(range(b, ty, world))
+        assert (f.c.band_begin, f.c.band_step, f.c.band_rows) == (b, world, len(rows_t))
+        img = img.cpu().numpy()
+        pix = np.zeros(cam.height, bool)
+        for t in rows_t:
+            pix[16 * t:16 * t + 16] = True
+        assert np.array_equal(img[:, pix], out["image"][:, pix])
+        assert np.all(img[:, ~pix] == -7.0)
+        rng = f.ranges().cpu().numpy().view(np.uint32).astype(np.int64)
+        lst = f.list(int(f.counts().pairs)).cpu().numpy().view(np.uint32)
+        for k, t in enumerate(rows_t):
+            for x in range(tx):
+                full = out["list"][out["ranges"][t * tx + x]:out["ranges"][t * tx + x + 1]]
+                band = lst[rng[k * tx + x]:rng[k * tx + x + 1]]
+                assert np.array_equal(full, band), (b, t, x)
+    for n in G.PARAM_NAMES:
+        a = getattr(acc, n).cpu().numpy().astype(np.float64)
+        # float atomics sum in another order: 1e-4 relative, plus a floor of 1e-6 of the
+        # group's largest entry for sums that cancel
+        floor = 1e-6 + 1e-6 * np.abs(g_full[n]).max()
+        bad = np.abs(a - g_full[n]) > np.maximum(1e-4 * np.abs(g_full[n]), floor)
+        assert bad.sum() == 0, (n, int(bad.sum()))
