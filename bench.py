@@ -299,6 +299,10 @@ def run_ours(args) -> None:
     g_ms = time_forward(G, gauss, cam, G.Settings(rho=scene.rho, gaussian_only=1), g_frame, image, flush, stream,
                         args.steps)
 
+    # ---- one frame split into screen-tile bands over the ranks (forward, strong scaling) ----
+    cam0 = scene.cameras[0]
+    band_ms, band_pairs = time_band_forward(G, params, cam0, st, dev, flush, stream, args.steps, rank, world)
+
     # ---- algorithmic work for the roofline ----
     n_comp = torch.zeros(W * H, dtype=torch.int32, device=dev)
     G.ges_preprocess(params, cam, st, frame, stream)
@@ -341,6 +345,11 @@ def run_ours(args) -> None:
             "iters_per_s": 1e3 / ms_per_step,
             "fwd_only": {"value": W * H / (fwd_ms / 1e3) / 1e6 * world, "unit": "Mpixel-frames/s",
                          "ms": fwd_ms, "fps_per_gpu": 1e3 / fwd_ms},
+            "bands_fwd": {"value": cam0.width * cam0.height / (band_ms / 1e3) / 1e6, "unit": "Mpixel-frames/s",
+                          "ms": band_ms, "frames_per_s": 1e3 / band_ms, "scaling": "strong",
+                          "pairs_rank0": band_pairs,
+                          "note": f"one config-3 frame split into {world} interleaved tile-row bands, S1-S4 per "
+                                  f"rank + all_gather of the band pixels; device time, max over ranks"},
             "vs_gaussian_equivalent": {"ges_fwd_ms": fwd_ms, "gaussian_fwd_ms": g_ms, "ratio": g_ms / fwd_ms,
                                        "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
             "stages_ms": {n: float(stage_ms[i]) for i, n in enumerate(stage_names)},
@@ -408,6 +417,46 @@ def time_forward(G, params, cam, st, frame, image, flush, stream, steps):
         b.synchronize()
         ms.append(a.elapsed_time(b))
     return float(statistics.mean(ms))
+
+
+def time_band_forward(G, params, cam, st, dev, flush, stream, steps, rank, world):
+    """Forward of ONE frame split into `world` interleaved screen-tile bands
+    (BASELINE config 3): each rank runs S1-S4 on its band, then
+    the band pixels are all-gathered (NCCL) into the full image on every rank.
+    Device time (CUDA events), max over ranks.  Strong scaling."""
+    import torch
+    import torch.distributed as dist
+    from paper_2402_10128_b200 import dist as gdist
+    bst = gdist.band_settings(st, rank, world)
+    r = G.Renderer(params.P, cam.width, cam.height, device=dev)
+    img = torch.zeros((3, cam.height, cam.width), dtype=torch.float32, device=dev)
+    r.forward(params, cam, bst, img)
+    r.grow(int(r.frame.counts().slots))
+    frame = r.frame
+
+    def once():
+        G.ges_preprocess(params, cam, bst, frame, stream)
+        G.ges_sort(frame, stream)
+        G.ges_render_fwd(frame, bst, img, None, stream)
+        return gdist.gather_bands(img, rank, world)
+    for _ in range(2):
+        once()
+    ms = []
+    for _ in range(steps):
+        flush.fill_(1)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        once()
+        b.record(stream)
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    t = torch.tensor([float(statistics.mean(ms))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), int(frame.counts().pairs)
 
 
 def gaussian_equivalent(G, scene, cam, dev):
