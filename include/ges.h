@@ -131,6 +131,7 @@ enum {
     GES_CTR_OVERFLOW = 2, /* 1 if SLOTS > pair capacity                             */
     GES_CTR_SLOTS = 3,    /* rect pairs = sum of rect areas (pair-slot count)       */
     GES_CTR_TICKET = 4,   /* scratch                                                */
+    GES_CTR_CHUNKS = 5,   /* binning chunks of this frame (<= frame.bin_chunks)     */
     GES_CTR_N = 16
 };
 
@@ -160,16 +161,17 @@ typedef struct {
     uint32_t *vis_key[2];  /* [P] depth bits (0xffffffff = not visible), ping-pong */
     uint32_t *vis_val[2];  /* [P] particle index, ping-pong                      */
     uint32_t *sorted_vis;  /* [V] visible particles in (depth, index) order (alias) */
-    /* ---- S2 radix scratch ---- */
-    uint32_t *radix_hist;  /* [256][max(P,cap)/4096] per-tile digit counts -> offsets (digit-major) */
-    uint32_t *radix_total; /* [2][256] digit totals of the two tile passes (depth passes use [0]) */
-    /* ---- S2 pairs and S3 ranges ---- */
-    uint32_t *item_offset; /* [P] first pair slot of each depth-sorted visible particle */
-    uint32_t *item_rec;    /* [P][4] packed (slot, particle, x0|y0<<16, x1|y1<<16)     */
-    uint32_t *tile_first;  /* [cap/4096+2] sorted particle holding slot 4096*j        */
-    uint32_t *pair_tile;   /* [cap] tile ids after the first tile-digit pass          */
-    uint32_t *pair_val;    /* [cap] particle ids after the first tile-digit pass      */
-    uint32_t *list_tile;   /* [cap] key (ty << 8 | tx) of every list entry (sorted)   */
+    /* ---- S2 radix scratch (depth passes) ---- */
+    uint32_t *radix_hist;  /* [256][P/4096] per-tile digit counts -> offsets (digit-major) */
+    uint32_t *radix_total; /* [256] digit totals of the current depth pass                 */
+    /* ---- S2 pairs and S3 ranges: direct tile binning ---- */
+    uint32_t *item_offset; /* [P] first pair slot E of each depth-sorted visible particle  */
+    uint32_t *item_rec;    /* [P][4] packed (E, particle, x0|y0<<16, x1|y1<<16)           */
+    uint32_t *chunk_first; /* [bin_chunks+1] first item of each binning chunk: the items s
+                              whose cost E[s] + 4 s lies in [k S, (k+1) S), S = bin_chunk_slots */
+    uint32_t *bin_table;   /* [num_tiles][bin_chunks] per-(tile, chunk) pair counts, then
+                              the chunk's offset inside the tile's list                   */
+    int64_t bin_chunk_slots, bin_chunks; /* S, and the chunk capacity ceil((capacity + 4 P) / S) */
     uint32_t *list;        /* [cap] per-tile lists: tile t = list[ranges[t] .. ranges[t+1]) */
     uint32_t *ranges;      /* [T+1]                                               */
     uint32_t *lookback;    /* decoupled look-back scratch (item scan)             */

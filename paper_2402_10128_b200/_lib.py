@@ -18,7 +18,8 @@ LIB_PATH = os.environ.get("GES_LIB") or os.path.join(_HERE, "libges.so")
 GES_OK, GES_ERR_INVALID_ARG, GES_ERR_CAPACITY, GES_ERR_CUDA, GES_ERR_UNSUPPORTED = range(5)
 GES_PHI_SCALE, GES_PHI_VARIANCE = 0, 1
 GES_VISIBLE, GES_CULL_NEAR, GES_DEGENERATE, GES_OFFSCREEN = range(4)
-GES_CTR_VISIBLE, GES_CTR_PAIRS, GES_CTR_OVERFLOW, GES_CTR_SLOTS, GES_CTR_TICKET, GES_CTR_N = 0, 1, 2, 3, 4, 16
+GES_CTR_VISIBLE, GES_CTR_PAIRS, GES_CTR_OVERFLOW, GES_CTR_SLOTS, GES_CTR_TICKET, GES_CTR_CHUNKS, GES_CTR_N = \
+    0, 1, 2, 3, 4, 5, 16
 
 _fp = C.POINTER(C.c_float)
 _u32p = C.POINTER(C.c_uint32)
@@ -61,8 +62,8 @@ class ges_frame(C.Structure):
         ("drgb_ddir", C.c_void_p),
         ("vis_key", C.c_void_p * 2), ("vis_val", C.c_void_p * 2), ("sorted_vis", C.c_void_p),
         ("radix_hist", C.c_void_p), ("radix_total", C.c_void_p), ("item_offset", C.c_void_p), ("item_rec", C.c_void_p),
-        ("tile_first", C.c_void_p), ("pair_tile", C.c_void_p), ("pair_val", C.c_void_p),
-        ("list_tile", C.c_void_p), ("list", C.c_void_p), ("ranges", C.c_void_p), ("lookback", C.c_void_p),
+        ("chunk_first", C.c_void_p), ("bin_table", C.c_void_p), ("bin_chunk_slots", C.c_int64),
+        ("bin_chunks", C.c_int64), ("list", C.c_void_p), ("ranges", C.c_void_p), ("lookback", C.c_void_p),
         ("counters", C.c_void_p), ("zero_bytes", C.c_size_t),
         ("final_T", C.c_void_p), ("n_contrib", C.c_void_p), ("grad2d", C.c_void_p),
         ("workspace_bytes", C.c_size_t),

@@ -81,14 +81,20 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
         g.vis_val[k] = (uint32_t*)take(sizeof(uint32_t) * P);
     }
     g.sorted_vis = g.vis_val[0];
-    g.radix_hist = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * (size_t)radix_tiles(std::max<int64_t>(P, cap)));
-    g.radix_total = (uint32_t*)take(sizeof(uint32_t) * 2 * kRadixDigits);
+    g.radix_hist = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * (size_t)radix_tiles(P));
+    g.radix_total = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits);
     g.item_offset = (uint32_t*)take(sizeof(uint32_t) * P);
     g.item_rec = (uint32_t*)take(16 * (size_t)P);
-    g.tile_first = (uint32_t*)take(sizeof(uint32_t) * (size_t)slot_tiles(cap));
-    g.pair_tile = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
-    g.pair_val = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
-    g.list_tile = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
+    // binning chunks: S >= 16384 slots, and the [T][chunks] table bounded by 2^24 entries
+    {
+        const int64_t cost = cap + kBinItemCost * P;  // chunk cost bound: M + kBinItemCost V
+        int64_t S = std::max<int64_t>(16384, (cost * T + (1 << 24) - 1) >> 24);
+        S = (S + 1023) / 1024 * 1024;
+        g.bin_chunk_slots = S;
+        g.bin_chunks = std::max<int64_t>(1, (cost + S - 1) / S);
+    }
+    g.chunk_first = (uint32_t*)take(sizeof(uint32_t) * (size_t)(g.bin_chunks + 1));
+    g.bin_table = (uint32_t*)take(sizeof(uint32_t) * (size_t)T * (size_t)g.bin_chunks);
     g.list = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
     g.ranges = (uint32_t*)take(sizeof(uint32_t) * (size_t)(T + 1));
     g.final_T = (float*)take(sizeof(float) * HW);
@@ -190,7 +196,7 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long* ctr = (unsigned long long*)frame->counters;
     const LookbackLayout L = lookback_layout(frame->P, frame->pair_capacity);
-    const int64_t hist_stride = radix_tiles(std::max<int64_t>(frame->P, frame->pair_capacity));
+    const int64_t hist_stride = radix_tiles(frame->P);
     cudaError_t e;
     // depth sort: pass 0 reads all P keys and drops the non-visible ones (compaction);
     // ping-pong (vis_key[0]) -> 1 -> 0 -> 1 -> (vis_val[0])
@@ -214,47 +220,24 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
         if ((e = launch_radix_pass(p, s)) != cudaSuccess) return GES_ERR_CUDA;
     }
     frame->sorted_vis = frame->vis_val[0];
-    // pair slots of every sorted particle (rect areas), capacity check
+    // pair slots of every sorted particle (rect areas), binning chunks, capacity check
     ItemScanArgs is;
     is.sorted_vis = frame->sorted_vis; is.rect = (const ushort4*)frame->rect; is.counters = ctr;
     is.capacity = frame->pair_capacity;
-    is.E = frame->item_offset; is.items = (uint4*)frame->item_rec; is.tile_first = frame->tile_first;
+    is.E = frame->item_offset; is.items = (uint4*)frame->item_rec;
+    is.chunk_first = frame->chunk_first; is.chunk_slots = frame->bin_chunk_slots;
     is.lookback = frame->lookback + L.scan; is.tile_counter = ctr + GES_CTR_TICKET;
     if ((e = launch_item_scan(is, frame->P, s)) != cudaSuccess) return GES_ERR_CUDA;
-    // stable sort of the pairs by tile id; the first pass generates them
-    // pair keys are (ty << 8 | tx): pass 0 sorts by the column, pass 1 by the row
-    const int passes = frame->band_rows > 1 ? 2 : 1;
-    for (int d = 0; d < passes; ++d) {
-        RadixPassArgs p;
-        std::memset(&p, 0, sizeof(p));
-        const bool last = d + 1 == passes;
-        p.gen = (d == 0) ? 1 : 0;
-        p.keys_in = (d == 0) ? nullptr : frame->pair_tile;
-        p.vals_in = (d == 0) ? nullptr : frame->pair_val;
-        p.keys_out = last ? frame->list_tile : frame->pair_tile;
-        p.vals_out = last ? frame->list : frame->pair_val;
-        p.count = ctr + GES_CTR_SLOTS;  // every slot is a pair (R10 rects)
-        p.max_items = frame->pair_capacity;
-        p.tile_hist = frame->radix_hist;
-        p.hist_stride = hist_stride;
-        p.digit_total = frame->radix_total + (d & 1) * kRadixDigits;
-        p.shift = 8 * d;
-        p.digit_bits = std::max(1, bits_for(d == 0 ? frame->tiles_x : frame->band_rows));
-        p.overflow = ctr + GES_CTR_OVERFLOW;
-        p.tiles_x = frame->tiles_x;
-        p.sorted_vis = frame->sorted_vis;
-        p.rect = (const ushort4*)frame->rect;
-        p.E = frame->item_offset;
-        p.items = (const uint4*)frame->item_rec;
-        p.tile_first = frame->tile_first;
-        p.counters = ctr;
-        if ((e = launch_radix_pass(p, s)) != cudaSuccess) return GES_ERR_CUDA;
-    }
-    RangesArgs r;
-    r.keys = frame->list_tile;
-    r.tiles_x = frame->tiles_x; r.tiles_y = frame->band_rows;
-    r.ranges = frame->ranges; r.counters = ctr; r.max_pairs = frame->pair_capacity;
-    if ((e = launch_ranges(r, s)) != cudaSuccess) return GES_ERR_CUDA;
+    // every (tile, particle) pair written once, in depth order, into its tile's list
+    BinArgs b;
+    b.items = (const uint4*)frame->item_rec; b.chunk_first = frame->chunk_first;
+    b.counters = ctr; b.counters_w = ctr;
+    b.table = frame->bin_table; b.ranges = frame->ranges; b.list = frame->list;
+    b.tiles_x = frame->tiles_x; b.rows = frame->band_rows;
+    b.win_rows = std::max(1, std::min(frame->band_rows, kBinWinTiles / frame->tiles_x));
+    b.cmax = (int)frame->bin_chunks; b.chunk_slots = frame->bin_chunk_slots;
+    b.rank_bits = std::max(1, bits_for((int64_t)((b.win_rows + 7) / 8) * frame->tiles_x));
+    if ((e = launch_bin(b, s)) != cudaSuccess) return GES_ERR_CUDA;
     return GES_OK;
 }
 

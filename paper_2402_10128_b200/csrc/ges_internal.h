@@ -48,16 +48,6 @@ struct RadixPassArgs {
     int shift;
     int digit_bits;                   // bits of the digit that can be non-zero (1..8)
     int drop_invalid;                 // 1: keys == 0xffffffff are dropped (compaction)
-    const unsigned long long* overflow;  // non-null and set: do nothing
-    // gen = 1: keys/values generated from the sorted particles (pair expansion)
-    int gen;
-    int tiles_x;
-    const uint32_t* sorted_vis;
-    const ushort4* rect;
-    const uint32_t* E;
-    const uint4* items;
-    const uint32_t* tile_first;
-    const unsigned long long* counters;
 };
 cudaError_t launch_radix_pass(const RadixPassArgs& a, cudaStream_t stream);
 int64_t radix_tiles(int64_t n);
@@ -69,22 +59,32 @@ struct ItemScanArgs {
     int64_t capacity;
     uint32_t* E;                      // [P]
     uint4* items;                     // [P] packed (E, particle, rect x0|y0<<16, x1|y1<<16)
-    uint32_t* tile_first;             // [cap/4096 + 2]
+    uint32_t* chunk_first;            // [cap/chunk_slots + 1] first item of every binning chunk
+    int64_t chunk_slots;              // pair slots per binning chunk (bin.cu)
     uint32_t* lookback;               // [tiles]
     unsigned long long* tile_counter;
 };
 cudaError_t launch_item_scan(const ItemScanArgs& a, int64_t max_items, cudaStream_t stream);
 int64_t item_scan_tiles(int64_t n);
-int64_t slot_tiles(int64_t cap);
 
-struct RangesArgs {
-    const uint32_t* keys;             // [M] sorted tile ids
-    int tiles_x, tiles_y;
+// --- direct tile binning (bin.cu) -------------------------------------------
+constexpr int kBinWinTiles = 8192;    // tiles of one binning window (shared-memory cursors)
+constexpr int kBinItemCost = 4;       // chunk cost of an item, in pair slots
+struct BinArgs {
+    const uint4* items;               // [V] item records in depth order (item scan)
+    const uint32_t* chunk_first;      // [chunks + 1]
+    const unsigned long long* counters;  // reads CHUNKS, OVERFLOW
+    unsigned long long* counters_w;   // writes PAIRS
+    uint32_t* table;                  // [T][cmax] per-(tile, chunk) counts -> offsets
     uint32_t* ranges;                 // [T+1]
-    unsigned long long* counters;     // writes PAIRS
-    int64_t max_pairs;
+    uint32_t* list;                   // [cap]
+    int tiles_x, rows;                // band tiles: T = tiles_x * rows
+    int win_rows;                     // tile rows per window (win_rows * tiles_x <= kBinWinTiles)
+    int cmax;                         // chunk capacity (table row length, grid.x)
+    int64_t chunk_slots;
+    int rank_bits;                    // bits of a warp-local tile id (ballot ranking)
 };
-cudaError_t launch_ranges(const RangesArgs& a, cudaStream_t stream);
+cudaError_t launch_bin(const BinArgs& a, cudaStream_t stream);
 
 // --- render ----------------------------------------------------------------
 constexpr int kGrad2dStride = 12;  // floats per particle in grad2d (3 x float4)

@@ -1,35 +1,24 @@
-// sort.cu -- S2/S3: depth radix sort of the visible
-// particles, generation of the (tile, particle) pairs in depth order (every
-// tile of each particle's R10 rect), stable radix sort of the pairs by tile id,
-// per-tile ranges.
+// sort.cu -- S2: depth radix sort of the visible particles
+// and the item scan that turns the depth-sorted particles into pair slots.
 //
 // Design: instead of a 64-bit LSD sort of
-// (tile_id << 32 | depth) keys (6 x 8-bit passes over all pairs), the depth
-// order is established once on the V visible particles (4 passes over
-// V << M; pass 0 also compacts the visible set), then the pairs are generated
-// in that order and sorted STABLY by tile id alone (2 passes for <= 65536
-// tiles): every tile's list comes out in (depth bits, particle index) order --
-// exactly the order of the 64-bit keys.
-//   item scan   exclusive prefix E[s] of the rect areas of the sorted particles
-//               (decoupled look-back), packed item records, the particle that
-//               holds the first slot of each 4096-slot tile, the slot count;
-//   pass 1      each CTA owns 4096 consecutive pair SLOTS (balanced however
-//               unequal the footprints are), stages the particles covering
-//               them in shared memory, expands its slots by a load-balanced
-//               search, ranks and scatters them by the low tile digit -- no unsorted pair array is ever written;
-//   pass 2      the high tile digit;
-//   ranges      the boundaries of the sorted tile ids.
-// Each pass is reduce-then-scan (per-tile digit histograms, one column scan
-// per digit, scatter): no CTA ever waits for another.  Ranking is a warp
-// multisplit with one ballot per digit bit.  Hand-written; no CUB.
+// (tile_id << 32 | depth) keys over all pairs, the depth order is established
+// once on the V visible particles (4 LSD passes over V << M; pass 0 also
+// compacts the visible set), then bin.cu writes every tile's list directly in
+// that order -- exactly the order of the 64-bit keys.
+//   depth passes  reduce-then-scan (per-tile digit histograms, one column scan
+//                 per digit, scatter): no CTA ever waits for another; ranking
+//                 is a warp multisplit with one ballot per digit bit;
+//   item scan     exclusive prefix E[s] of the rect areas of the sorted
+//                 particles (decoupled look-back), packed item records, the
+//                 first item of every binning chunk, the slot count M.
+// Hand-written; no CUB.
 #include <algorithm>
 
 #include "ges_internal.h"
 #include "ges_scan.cuh"
 
 namespace ges {
-
-constexpr int kSlotTile = 4096;  // pair slots per CTA == radix tile
 
 // ---------------------------------------------------------------------------
 // Item scan
@@ -39,7 +28,7 @@ constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
 int64_t item_scan_tiles(int64_t n) { return (n + kScanTile - 1) / kScanTile; }
-int64_t slot_tiles(int64_t cap) { return (cap + kSlotTile - 1) / kSlotTile + 2; }
+constexpr uint64_t kItemCost = kBinItemCost;
 
 __device__ __forceinline__ uint32_t rect_count(ushort4 r) { return (uint32_t)(r.z - r.x) * (uint32_t)(r.w - r.y); }
 
@@ -49,7 +38,7 @@ __global__ void __launch_bounds__(kScanThreads) item_scan_kernel(ItemScanArgs a)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t V = (int64_t)a.counters[GES_CTR_VISIBLE];
     if (V == 0) {
-        if (blockIdx.x == 0 && tid == 0) a.counters[GES_CTR_SLOTS] = 0;
+        if (blockIdx.x == 0 && tid == 0) { a.counters[GES_CTR_SLOTS] = 0; a.counters[GES_CTR_CHUNKS] = 0; }
         return;
     }
     if (tid == 0) s_tile = (uint32_t)atomicAdd(a.tile_counter, 1ull);
@@ -97,13 +86,22 @@ __global__ void __launch_bounds__(kScanThreads) item_scan_kernel(ItemScanArgs a)
             // packed item record for the pair expansion: one coalesced 16-B load there
             a.items[s] = make_uint4(e, ids[j], (uint32_t)rc[j].x | ((uint32_t)rc[j].y << 16),
                                     (uint32_t)rc[j].z | ((uint32_t)rc[j].w << 16));
-            // slot tiles whose first slot lies in [e, e + c)
-            for (uint32_t st = (e + kSlotTile - 1) / kSlotTile; st * (uint64_t)kSlotTile < (uint64_t)e + c[j]; ++st)
-                a.tile_first[st] = (uint32_t)s;
-            if (s == V - 1) {  // total pair slots, capacity check
-                const uint64_t slots = (uint64_t)e + c[j];
-                a.counters[GES_CTR_SLOTS] = slots;
-                a.counters[GES_CTR_OVERFLOW] = (int64_t)slots > a.capacity ? 1ull : 0ull;
+            // binning chunk k = the items whose cost W[s] = E[s] + kItemCost s lies in
+            // [k S, (k+1) S) (a pair costs 1, an item kItemCost: bin.cu's work per
+            // item), i.e. chunk_first[k] = min{s : W[s] >= k S}; item s + 1 is that
+            // minimum for every k with k S in (W[s], W[s+1]].  Item 0 opens chunk 0.
+            const uint64_t S = (uint64_t)a.chunk_slots, e1 = (uint64_t)e + c[j];
+            const uint64_t w0 = (uint64_t)e + kItemCost * (uint64_t)s, w1 = e1 + kItemCost * (uint64_t)(s + 1);
+            const bool ovf = (int64_t)e1 > a.capacity;
+            if (s == 0) a.chunk_first[0] = 0;
+            if (!ovf)
+                for (uint64_t k = w0 / S + 1; k * S <= w1; ++k) a.chunk_first[k] = (uint32_t)(s + 1);
+            if (s == V - 1) {  // total pair slots, capacity check, chunk count and closing entry
+                a.counters[GES_CTR_SLOTS] = e1;
+                a.counters[GES_CTR_OVERFLOW] = ovf ? 1ull : 0ull;
+                const uint64_t C = (w1 + S - 1) / S;
+                a.counters[GES_CTR_CHUNKS] = ovf ? 0ull : C;
+                if (!ovf) a.chunk_first[C] = (uint32_t)V;
             }
         }
         e += c[j];
@@ -117,16 +115,12 @@ cudaError_t launch_item_scan(const ItemScanArgs& a, int64_t max_items, cudaStrea
 }
 
 // ---------------------------------------------------------------------------
-// LSD radix passes, reduce-then-scan (no inter-CTA waiting):
+// LSD radix passes of the depth sort, reduce-then-scan (no inter-CTA waiting):
 //   radix_hist_kernel     per 4096-key tile: digit histogram -> H[d][tile]
 //   radix_scan_kernel     per digit: exclusive scan of H[d][.] over the tiles,
 //                         column total -> T[d]
 //   radix_scatter_kernel  per tile: stable warp-multisplit ranking, shared-memory
 //                         reorder, scatter to off(d) + H[d][tile] + local rank
-// GEN = true: a tile's keys (ty << 8 | tx) and values (particle ids) are
-// generated from the depth-sorted particles (load-balanced search over pair
-// slots); its digit is the tile column tx, whose histogram gen_hist_kernel
-// computes from the items alone.
 // ---------------------------------------------------------------------------
 constexpr int kRadixThreads = 256;
 #ifndef GES_SCAT_MINB  // tuning knob: min resident CTAs per SM for the scatter kernels
@@ -136,167 +130,55 @@ constexpr int kRadixItems = 16;
 constexpr int kRadixTile = kRadixThreads * kRadixItems;  // 4096
 constexpr int kRadixWarps = kRadixThreads / 32;
 constexpr uint32_t kInvalidKey = 0xffffffffu;
-static_assert(kRadixTile == kSlotTile, "slot tiles are radix tiles");
 
 int64_t radix_tiles(int64_t n) { return (n + kRadixTile - 1) / kRadixTile; }
-
-// Particles covering a CTA's 4096 slots are staged in shared memory when
-// there are at most kStageMax of them (the common case: a particle touches
-// ~20 tiles); tiles of many tiny particles read them from L2 instead.
-constexpr int kStageMax = 1024;
-struct GenSmem {
-    uint32_t E[kStageMax];
-    uint32_t pid[kStageMax];
-    ushort4 rect[kStageMax];
-};
 
 __device__ __forceinline__ int64_t pass_count(const RadixPassArgs& a) {
     return a.count ? min((int64_t)*a.count, a.max_items) : a.max_items;
 }
 
-// Loads (or generates) the tile's keys/values in warp-striped order: item j of
-// lane l of warp w is element w*512 + j*32 + l of the tile.  valid bit j marks
-// items that take part.
-template <bool GEN>
+// Loads the tile's keys/values in warp-striped order: item j of lane l of
+// warp w is element w*512 + j*32 + l of the tile.  valid bit j marks items
+// that take part.
 __device__ __forceinline__ void load_tile(const RadixPassArgs& a, int64_t tile, int64_t n,
                                           uint32_t (&k)[kRadixItems], uint32_t (&v)[kRadixItems], uint32_t& valid,
-                                          uint32_t* s_keys, uint32_t* s_vals, unsigned char* s_dyn,
                                           bool need_vals) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t base = tile * kRadixTile + warp * (kRadixItems * 32);
     valid = 0;
-    if constexpr (GEN) {
-        GenSmem& g = *reinterpret_cast<GenSmem*>(s_dyn);
-        const int64_t slot0 = tile * kRadixTile;
-        const int nslots = (int)min((int64_t)kRadixTile, n - slot0);
-        const int64_t V = (int64_t)a.counters[GES_CTR_VISIBLE];
-        const int64_t f = a.tile_first[tile];
-        const int64_t last_item = (slot0 + kRadixTile < n) ? (int64_t)a.tile_first[tile + 1] : V - 1;
-        const int nit = (int)(last_item - f + 1);
-        const bool staged = nit <= kStageMax;
-        if (staged) {
-            constexpr int kU = kStageMax / kRadixThreads;
-            uint4 rec[kU];
+    // issue every load before any use (all in flight together)
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const int q = tid + u * kRadixThreads;
-                if (q < nit) rec[u] = __ldg(a.items + f + q);
+    for (int j = 0; j < kRadixItems; ++j) {
+        const int64_t idx = base + j * 32 + lane;
+        k[j] = (idx < n) ? __ldg(a.keys_in + idx) : kInvalidKey;
+    }
+    if (need_vals) {
+        if (a.vals_in) {
+#pragma unroll
+            for (int j = 0; j < kRadixItems; ++j) {
+                const int64_t idx = base + j * 32 + lane;
+                v[j] = (idx < n) ? __ldg(a.vals_in + idx) : 0u;
             }
+        } else {
 #pragma unroll
-            for (int u = 0; u < kU; ++u) {
-                const int q = tid + u * kRadixThreads;
-                if (q < nit) {
-                    g.E[q] = rec[u].x;
-                    g.pid[q] = rec[u].y;
-                    g.rect[q] = make_ushort4((uint16_t)(rec[u].z & 0xffffu), (uint16_t)(rec[u].z >> 16),
-                                             (uint16_t)(rec[u].w & 0xffffu), (uint16_t)(rec[u].w >> 16));
-                }
-            }
+            for (int j = 0; j < kRadixItems; ++j) v[j] = (uint32_t)(base + j * 32 + lane);
         }
-        __syncthreads();
-        auto itemE = [&](int q) -> uint32_t { return staged ? g.E[q] : __ldg(a.E + f + q); };
-        auto itemPid = [&](int q) -> uint32_t { return staged ? g.pid[q] : __ldg(a.sorted_vis + f + q); };
-        auto itemRect = [&](int q) -> ushort4 { return staged ? g.rect[q] : __ldg(a.rect + itemPid(q)); };
-        // thread-contiguous slots, then an exchange to the warp-striped order
-        const int ls0 = tid * kRadixItems;
-        int it = 0;
-        if (ls0 < nslots) {
-            const uint32_t s0 = (uint32_t)(slot0 + ls0);
-            int lo = 0, hi = nit - 1;  // last item with E <= s0
-            while (lo < hi) {
-                const int mid = (lo + hi + 1) >> 1;
-                if (itemE(mid) <= s0) lo = mid; else hi = mid - 1;
-            }
-            it = lo;
-        }
-        // walk the thread's 16 consecutive slots: one division per item start, then
-        // the tile advances along the rect's rows incrementally
-        ushort4 r = itemRect(it);
-        uint32_t pid = itemPid(it), E1 = (it + 1 < nit) ? itemE(it + 1) : 0xffffffffu;
-        uint32_t w = r.z - r.x;
-        uint32_t xx = 0, yy = 0;
-        if (ls0 < nslots) {
-            const uint32_t li = (uint32_t)(slot0 + ls0) - itemE(it);
-            // li / w exactly: the quotient is < 2^16, far from rounding trouble
-            yy = __float2uint_rz(((float)li + 0.5f) * __fdividef(1.0f, (float)w));
-            xx = li - yy * w;
-        }
+    }
 #pragma unroll
-        for (int j = 0; j < kRadixItems; ++j) {
-            const int ls = ls0 + j;
-            const uint32_t s = (uint32_t)(slot0 + ls);
-            if (ls < nslots) {
-                if (s >= E1) {  // next item(s); items are never empty
-                    do {
-                        ++it;
-                        E1 = (it + 1 < nit) ? itemE(it + 1) : 0xffffffffu;
-                    } while (s >= E1);
-                    r = itemRect(it);
-                    pid = itemPid(it);
-                    w = r.z - r.x;
-                    xx = 0;
-                    yy = 0;
-                }
-                const uint32_t tx = r.x + xx, ty = r.y + yy;
-                const uint32_t key = (ty << 8) | tx;
-                const int pad = ls + (ls >> 5);  // +1 word per 32: conflict-free both ways
-                s_keys[pad] = key;
-                s_vals[pad] = pid;
-                if (++xx == w) { xx = 0; ++yy; }
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < kRadixItems; ++j) {
-            const int ls = warp * (kRadixItems * 32) + j * 32 + lane;
-            if (ls < nslots) {
-                const int pad = ls + (ls >> 5);
-                k[j] = s_keys[pad];
-                if (need_vals) v[j] = s_vals[pad];
-                valid |= 1u << j;
-            }
-        }
-        __syncthreads();
-    } else {
-        // issue every load before any use (all in flight together)
-#pragma unroll
-        for (int j = 0; j < kRadixItems; ++j) {
-            const int64_t idx = base + j * 32 + lane;
-            k[j] = (idx < n) ? __ldg(a.keys_in + idx) : kInvalidKey;
-        }
-        if (need_vals) {
-            if (a.vals_in) {
-#pragma unroll
-                for (int j = 0; j < kRadixItems; ++j) {
-                    const int64_t idx = base + j * 32 + lane;
-                    v[j] = (idx < n) ? __ldg(a.vals_in + idx) : 0u;
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < kRadixItems; ++j) v[j] = (uint32_t)(base + j * 32 + lane);
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kRadixItems; ++j) {
-            const int64_t idx = base + j * 32 + lane;
-            if (idx < n && !(a.drop_invalid && k[j] == kInvalidKey)) valid |= 1u << j;
-        }
+    for (int j = 0; j < kRadixItems; ++j) {
+        const int64_t idx = base + j * 32 + lane;
+        if (idx < n && !(a.drop_invalid && k[j] == kInvalidKey)) valid |= 1u << j;
     }
 }
 
-template <bool GEN>
 __global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(RadixPassArgs a) {
-    __shared__ uint32_t s_keys[GEN ? kRadixTile + kRadixTile / 32 : 1];
-    __shared__ uint32_t s_vals[GEN ? kRadixTile + kRadixTile / 32 : 1];
     __shared__ uint32_t s_hist[kRadixDigits];
-    extern __shared__ __align__(16) unsigned char s_dyn[];
-    if (a.overflow && *a.overflow) return;
     const int64_t n = pass_count(a);
     const int64_t tile = blockIdx.x;
     if (tile * kRadixTile >= n) return;
     s_hist[threadIdx.x] = 0;
     uint32_t k[kRadixItems], v[kRadixItems], valid;
-    load_tile<GEN>(a, tile, n, k, v, valid, s_keys, s_vals, s_dyn, false);
+    load_tile(a, tile, n, k, v, valid, false);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kRadixItems; ++j)
@@ -305,65 +187,10 @@ __global__ void __launch_bounds__(kRadixThreads) radix_hist_kernel(RadixPassArgs
     a.tile_hist[(int64_t)threadIdx.x * a.hist_stride + tile] = s_hist[threadIdx.x];
 }
 
-// GEN pass histogram without generating the pairs: the digit of a pair is
-// its tile column tx, so the slots an item holds inside this CTA's 4096-slot
-// window add +1 over column ranges -- at most three range updates per item
-// (partial first row, full rows, partial last row) in a 257-entry difference
-// array -- followed by a prefix sum over the 256 columns.
-__global__ void __launch_bounds__(kRadixThreads) gen_hist_kernel(RadixPassArgs a) {
-    __shared__ int s_diff[kRadixDigits + 1];
-    __shared__ int s_warp[kRadixWarps];
-    if (a.overflow && *a.overflow) return;
-    const int64_t n = pass_count(a);
-    const int64_t tile = blockIdx.x;
-    if (tile * kRadixTile >= n) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    s_diff[tid] = 0;
-    if (tid == 0) s_diff[kRadixDigits] = 0;
-    __syncthreads();
-    const int64_t slot0 = tile * kRadixTile, slot1 = min(slot0 + kRadixTile, n);
-    const int64_t V = (int64_t)a.counters[GES_CTR_VISIBLE];
-    const int64_t f = a.tile_first[tile];
-    const int64_t last_item = (slot1 < n) ? (int64_t)a.tile_first[tile + 1] : V - 1;
-    for (int64_t q = f + tid; q <= last_item; q += kRadixThreads) {
-        const uint4 rec = __ldg(a.items + q);
-        const int x0 = (int)(rec.z & 0xffffu), y0 = (int)(rec.z >> 16);
-        const int x1 = (int)(rec.w & 0xffffu), y1 = (int)(rec.w >> 16);
-        const int64_t e0 = rec.x;
-        const uint32_t w = (uint32_t)(x1 - x0), area = w * (uint32_t)(y1 - y0);
-        const int64_t lo = max(slot0, e0) - e0, hi = min(slot1, e0 + (int64_t)area) - e0;  // slots [lo, hi) of the item
-        if (lo >= hi) continue;
-        const uint32_t ra = (uint32_t)lo / w, ca = (uint32_t)lo - ra * w;
-        const uint32_t rb = (uint32_t)hi / w, cb = (uint32_t)hi - rb * w;
-        if (ra == rb) {
-            atomicAdd(&s_diff[x0 + ca], 1); atomicAdd(&s_diff[x0 + cb], -1);
-        } else {
-            atomicAdd(&s_diff[x0 + ca], 1); atomicAdd(&s_diff[x1], -1);          // row ra from column ca
-            if (rb > ra + 1) { atomicAdd(&s_diff[x0], (int)(rb - ra - 1)); atomicAdd(&s_diff[x1], -(int)(rb - ra - 1)); }
-            if (cb > 0) { atomicAdd(&s_diff[x0], 1); atomicAdd(&s_diff[x0 + cb], -1); }  // row rb up to cb
-        }
-    }
-    __syncthreads();
-    // inclusive prefix over the columns
-    const int d = s_diff[tid];
-    int incl = d;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int nn = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += nn;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    int base = 0;
-    for (int w2 = 0; w2 < warp; ++w2) base += s_warp[w2];
-    a.tile_hist[(int64_t)tid * a.hist_stride + tile] = (uint32_t)(base + incl);
-}
-
 // One CTA per digit: exclusive scan of H[d][.] over the tiles (in place).
 __global__ void __launch_bounds__(256) radix_scan_kernel(RadixPassArgs a) {
     __shared__ uint32_t s_warp[9];
     const int d = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (a.overflow && *a.overflow) return;
     const int64_t n = pass_count(a);
     const int nt = (int)((n + kRadixTile - 1) / kRadixTile);
     const int per = (nt + 255) / 256;
@@ -394,16 +221,13 @@ __global__ void __launch_bounds__(256) radix_scan_kernel(RadixPassArgs a) {
     if (tid == 0) a.digit_total[d] = s_warp[8];
 }
 
-template <bool GEN>
 __global__ void __launch_bounds__(kRadixThreads, GES_SCAT_MINB) radix_scatter_kernel(RadixPassArgs a) {
-    __shared__ uint32_t s_keys[kRadixTile + kRadixTile / 32];
-    __shared__ uint32_t s_vals[kRadixTile + kRadixTile / 32];
+    __shared__ uint32_t s_keys[kRadixTile];
+    __shared__ uint32_t s_vals[kRadixTile];
     __shared__ uint32_t s_whist[kRadixWarps][kRadixDigits];
     __shared__ uint32_t s_local[kRadixDigits];
     __shared__ uint32_t s_global[kRadixDigits];
     __shared__ uint32_t s_warp[kRadixWarps + 1];
-    extern __shared__ __align__(16) unsigned char s_dyn[];
-    if (a.overflow && *a.overflow) return;
     const int64_t n = pass_count(a);
     const int64_t tile = blockIdx.x;
     if (tile * kRadixTile >= n) return;
@@ -411,7 +235,7 @@ __global__ void __launch_bounds__(kRadixThreads, GES_SCAT_MINB) radix_scatter_ke
     const uint32_t lt_mask = (1u << lane) - 1u;
     // keys first: their loads overlap the offset computation below
     uint32_t k[kRadixItems], v[kRadixItems], rank[kRadixItems], valid;
-    load_tile<GEN>(a, tile, n, k, v, valid, s_keys, s_vals, s_dyn, true);
+    load_tile(a, tile, n, k, v, valid, true);
     for (int d = tid; d < kRadixWarps * kRadixDigits; d += kRadixThreads) (&s_whist[0][0])[d] = 0;
     // global digit offsets: exclusive scan of the column totals + this tile's prefix
     {
@@ -503,70 +327,11 @@ __global__ void __launch_bounds__(kRadixThreads, GES_SCAT_MINB) radix_scatter_ke
 cudaError_t launch_radix_pass(const RadixPassArgs& a, cudaStream_t stream) {
     const unsigned grid = (unsigned)std::max<int64_t>(1, radix_tiles(a.max_items));
     cudaError_t e;
-    if (a.gen) {
-        static bool configured = false;
-        if (!configured) {
-            cudaFuncSetAttribute(radix_scatter_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(GenSmem));
-            configured = true;
-        }
-        gen_hist_kernel<<<grid, kRadixThreads, 0, stream>>>(a);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        radix_scan_kernel<<<kRadixDigits, 256, 0, stream>>>(a);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        radix_scatter_kernel<true><<<grid, kRadixThreads, sizeof(GenSmem), stream>>>(a);
-    } else {
-        radix_hist_kernel<false><<<grid, kRadixThreads, 0, stream>>>(a);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        radix_scan_kernel<<<kRadixDigits, 256, 0, stream>>>(a);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-        radix_scatter_kernel<false><<<grid, kRadixThreads, 0, stream>>>(a);
-    }
-    return cudaGetLastError();
-}
-
-// ---------------------------------------------------------------------------
-// S3: per-tile ranges from the sorted tile ids
-// ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) ranges_kernel(RangesArgs a) {
-    const int T = a.tiles_x * a.tiles_y;
-    if (a.counters[GES_CTR_OVERFLOW]) {
-        for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= T; t += gridDim.x * blockDim.x) a.ranges[t] = 0;
-        if (blockIdx.x == 0 && threadIdx.x == 0) a.counters[GES_CTR_PAIRS] = 0;
-        return;
-    }
-    const uint32_t M = (uint32_t)min((int64_t)a.counters[GES_CTR_SLOTS], a.max_pairs);
-    if (blockIdx.x == 0 && threadIdx.x == 0) a.counters[GES_CTR_PAIRS] = M;
-    // entry m opens every tile in (tile[m-1], tile[m]]; the end closes (tile[M-1], T];
-    // tile(key) = ty * tiles_x + tx for key = ty << 8 | tx (monotone in the key)
-    auto tile_of = [&](uint32_t k) { return (int)(k >> 8) * a.tiles_x + (int)(k & 255u); };
-    // four entries per thread (one 16-B load) plus the entry before them
-    for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 4 * g <= (int64_t)M;
-         g += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t m0 = 4 * g;
-        uint32_t k[4];
-        if (m0 + 4 <= (int64_t)M) {
-            const uint4 q = __ldg(reinterpret_cast<const uint4*>(a.keys + m0));
-            k[0] = q.x; k[1] = q.y; k[2] = q.z; k[3] = q.w;
-        } else {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) k[j] = (m0 + j < (int64_t)M) ? __ldg(a.keys + m0 + j) : 0u;
-        }
-        int prev = m0 > 0 ? tile_of(__ldg(a.keys + m0 - 1)) : -1;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const int64_t m = m0 + j;
-            if (m > (int64_t)M) break;
-            const int cur = m < (int64_t)M ? tile_of(k[j]) : T;
-            for (int t = prev + 1; t <= cur; ++t) a.ranges[t] = (uint32_t)m;
-            prev = cur;
-        }
-    }
-}
-
-cudaError_t launch_ranges(const RangesArgs& a, cudaStream_t stream) {
-    const int grid = std::max(1, std::min(num_sms() * 8, (int)((a.max_pairs / 4 + 256) / 256)));
-    ranges_kernel<<<grid, 256, 0, stream>>>(a);
+    radix_hist_kernel<<<grid, kRadixThreads, 0, stream>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    radix_scan_kernel<<<kRadixDigits, 256, 0, stream>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    radix_scatter_kernel<<<grid, kRadixThreads, 0, stream>>>(a);
     return cudaGetLastError();
 }
 
