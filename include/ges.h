@@ -169,7 +169,7 @@ typedef struct {
     uint32_t *item_rec;    /* [P][4] packed (E, particle, x0|y0<<16, x1|y1<<16)           */
     uint32_t *chunk_first; /* [bin_chunks+1] first item of each binning chunk: the items s
                               whose cost E[s] + 4 s lies in [k S, (k+1) S), S = bin_chunk_slots */
-    uint32_t *bin_table;   /* [num_tiles][bin_chunks] per-(tile, chunk) pair counts, then
+    uint32_t *bin_table;   /* [bin_chunks][num_tiles] per-(chunk, tile) pair counts, then
                               the chunk's offset inside the tile's list                   */
     int64_t bin_chunk_slots, bin_chunks; /* S, and the chunk capacity ceil((capacity + 4 P) / S) */
     uint32_t *list;        /* [cap] per-tile lists: tile t = list[ranges[t] .. ranges[t+1]) */

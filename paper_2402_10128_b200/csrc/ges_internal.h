@@ -75,10 +75,11 @@ struct BinArgs {
     const uint32_t* chunk_first;      // [chunks + 1]
     const unsigned long long* counters;  // reads CHUNKS, OVERFLOW
     unsigned long long* counters_w;   // writes PAIRS
-    uint32_t* table;                  // [T][cmax] per-(tile, chunk) counts -> offsets
+    uint32_t* table;                  // [cmax][T] per-(chunk, tile) counts -> offsets
     uint32_t* ranges;                 // [T+1]
     uint32_t* list;                   // [cap]
     int tiles_x, rows;                // band tiles: T = tiles_x * rows
+    int64_t T;
     int win_rows;                     // tile rows per window (win_rows * tiles_x <= kBinWinTiles)
     int cmax;                         // chunk capacity (table row length, grid.x)
     int64_t chunk_slots;
