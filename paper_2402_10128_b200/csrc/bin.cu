@@ -223,85 +223,6 @@ __device__ __forceinline__ uint32_t class_pairs(const uint4 r, int R0, int R1, i
 
 constexpr int kQueue = 64;  // per-warp FIFO of item records (power of 2, >= 63)
 
-// Expands the next `ng` queued items (FIFO head) into their pairs in the
-// warp's rows, in (item, row, column) order, 32 pairs per round: the source
-// item of each lane from the item starts marked in shared memory, the tile by
-// an exact float division, the stable rank among equal tiles of the round by
-// a conflict test (owner bytes) and MATCH only when needed.
-__device__ __forceinline__ void expand_group(const BinArgs& a, const uint4* q, uint8_t* mark, int& qhead, int& qn,
-                                             int ng, int R0, int R1, int warp, int lane, uint32_t lt_mask, int tx,
-                                             uint32_t* s_cur, uint8_t* s_own) {
-    uint32_t cnt = 0, geo = 0, pid = 0;
-    float rw = 0.0f;
-    if (lane < ng) {
-        const uint4 r = q[(qhead + lane) & (kQueue - 1)];
-        cnt = class_pairs(r, R0, R1, warp, geo);
-        pid = r.y;
-        rw = __frcp_rn((float)(((geo >> 8) & 255u) + 1u));
-    }
-    qhead = (qhead + ng) & (kQueue - 1);
-    qn -= ng;
-    uint32_t incl = cnt;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += nn;
-    }
-    const uint32_t excl = incl - cnt;
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    int carry = 0;  // source lane of the pair before this round
-    for (uint32_t base = 0; base < total; base += 32) {
-        // source lane of pair base + lane: the last item starting at or before it
-        if (cnt && excl >= base && excl < base + 32) mark[excl - base] = (uint8_t)(lane + 1);
-        __syncwarp();
-        const uint32_t m = mark[lane];
-        mark[lane] = 0;
-        const uint32_t starts = __ballot_sync(0xffffffffu, m != 0u) & (0xffffffffu >> (31 - lane));
-        const int sm = (int)__shfl_sync(0xffffffffu, m, starts ? 31 - __clz(starts) : 0) - 1;
-        const int src = starts ? sm : carry;  // no start at or before this lane: the carried item
-        const uint32_t gi = base + lane;
-        const bool valid = gi < total;
-        const uint32_t s_excl = __shfl_sync(0xffffffffu, excl, src);
-        const uint32_t s_geo = __shfl_sync(0xffffffffu, geo, src);
-        const uint32_t s_pid = __shfl_sync(0xffffffffu, pid, src);
-        const float s_rw = __shfl_sync(0xffffffffu, rw, src);
-        carry = __shfl_sync(0xffffffffu, src, 31);
-        const uint32_t k = gi - s_excl;
-        const uint32_t w = ((s_geo >> 8) & 255u) + 1u;
-        // k / w exactly: k < 32 w, w <= 256 (quotient <= 31, far from rounding trouble)
-        const uint32_t ri = __float2uint_rz(__fmaf_rn((float)k, s_rw, 0.5f * s_rw));
-        const uint32_t xx = k - ri * w;
-        const uint32_t ly = (s_geo >> 16) + 8u * ri;
-        const uint32_t lt = ly * (uint32_t)tx + (s_geo & 255u) + xx;
-        // lanes of this round that hit the same tile: ranked in lane order
-        if (valid) s_own[lt] = (uint8_t)lane;
-        __syncwarp();
-        const bool lost = valid && s_own[lt] != (uint8_t)lane;
-        uint32_t peers = 1u << lane;
-        if (__any_sync(0xffffffffu, lost)) {
-#ifndef GES_BIN_BALLOT
-            peers = __match_any_sync(0xffffffffu, valid ? lt : 0xffffffffu);
-#else
-            const uint32_t cid = (ly >> 3) * (uint32_t)tx + (s_geo & 255u) + xx;
-            peers = __ballot_sync(0xffffffffu, valid);
-            for (int b = 0; b < a.rank_bits; ++b) {
-                const uint32_t bit = (cid >> b) & 1u;
-                const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-                peers &= bit ? bal : ~bal;
-            }
-#endif
-        }
-        uint32_t cur = 0;
-        if (valid) cur = s_cur[lt];
-        __syncwarp();
-        if (valid) {
-            a.list[cur + __popc(peers & lt_mask)] = s_pid;
-            if ((peers >> lane) == 1u) s_cur[lt] = cur + __popc(peers);
-        }
-        __syncwarp();
-    }
-}
-
 // --- mbarrier / TMA bulk-copy helpers (PTX) ---------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -335,7 +256,9 @@ constexpr int kStageRec = 512;  // item records per stage (8 KB)
 constexpr int kStages = 4;
 constexpr int kScatThreads = kBinThreads + 32;
 __global__ void __launch_bounds__(kScatThreads) bin_scatter_kernel(BinArgs a) {
-    extern __shared__ __align__(128) uint4 s_ring[];  // [kStages][kStageRec], then cursors, then owner bytes
+    extern __shared__ __align__(128) uint4 s_ring[];  // [kStages][kStageRec]
+    __shared__ uint32_t s_cur[kBinWinTiles];
+    __shared__ uint8_t s_own[kBinWinTiles];
     __shared__ uint4 s_q[kBinWarps][kQueue];
     __shared__ uint8_t s_mark[kBinWarps][32];
     __shared__ __align__(8) uint64_t s_full[kStages], s_empty[kStages];
@@ -347,8 +270,6 @@ __global__ void __launch_bounds__(kScatThreads) bin_scatter_kernel(BinArgs a) {
     const int R0 = (int)blockIdx.y * a.win_rows, R1 = min(a.rows, R0 + a.win_rows);
     const int tx = a.tiles_x, wt = (R1 - R0) * tx;
     const int64_t tbase = (int64_t)R0 * tx;
-    uint32_t* s_cur = reinterpret_cast<uint32_t*>(s_ring + kStages * kStageRec);
-    uint8_t* s_own = reinterpret_cast<uint8_t*>(s_cur + a.win_rows * tx);
     const uint32_t f = a.chunk_first[c], e = a.chunk_first[c + 1];
     const uint32_t nb = (e - f + kStageRec - 1) / kStageRec;
     if (tid == 0) {
@@ -373,9 +294,84 @@ __global__ void __launch_bounds__(kScatThreads) bin_scatter_kernel(BinArgs a) {
         }
         return;
     }
-    uint4* q = s_q[warp];
-    uint8_t* mark = s_mark[warp];
     int qhead = 0, qn = 0;  // FIFO state (warp-uniform)
+    // Expands the next `ng` queued items (FIFO head) into their pairs in the
+    // warp's rows, in (item, row, column) order, 32 pairs per round: the source
+    // item of each lane from the item starts marked in shared memory, the tile by
+    // an exact float division, the stable rank among equal tiles of the round by
+    // a conflict test (owner bytes) and MATCH only when needed.
+    auto expand_group = [&](int ng) {
+    uint32_t cnt = 0, geo = 0, pid = 0;
+    float rw = 0.0f;
+    if (lane < ng) {
+        const uint4 r = s_q[warp][(qhead + lane) & (kQueue - 1)];
+        cnt = class_pairs(r, R0, R1, warp, geo);
+        pid = r.y;
+        rw = __fdividef(1.0f, (float)(((geo >> 8) & 255u) + 1u));
+    }
+    qhead = (qhead + ng) & (kQueue - 1);
+    qn -= ng;
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += nn;
+    }
+    const uint32_t excl = incl - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    int carry = 0;  // source lane of the pair before this round
+    for (uint32_t base = 0; base < total; base += 32) {
+        // source lane of pair base + lane: the last item starting at or before it
+        if (cnt && excl >= base && excl < base + 32) s_mark[warp][excl - base] = (uint8_t)(lane + 1);
+        __syncwarp();
+        const uint32_t m = s_mark[warp][lane];
+        s_mark[warp][lane] = 0;
+        const uint32_t starts = __ballot_sync(0xffffffffu, m != 0u) & (0xffffffffu >> (31 - lane));
+        const int sm = (int)__shfl_sync(0xffffffffu, m, starts ? 31 - __clz(starts) : 0) - 1;
+        const int src = starts ? sm : carry;  // no start at or before this lane: the carried item
+        const uint32_t gi = base + lane;
+        const bool valid = gi < total;
+        const uint32_t s_excl = __shfl_sync(0xffffffffu, excl, src);
+        const uint32_t s_geo = __shfl_sync(0xffffffffu, geo, src);
+        const uint32_t s_pid = __shfl_sync(0xffffffffu, pid, src);
+        const float s_rw = __shfl_sync(0xffffffffu, rw, src);
+        carry = __shfl_sync(0xffffffffu, src, 31);
+        const uint32_t k = gi - s_excl;
+        const uint32_t w = ((s_geo >> 8) & 255u) + 1u;
+        // k / w exactly: k < 32 w, w <= 256, so the quotient (<= 31) is >= 0.5 / w from an
+        // integer while a few-ulp reciprocal errs by < 1e-5
+        const uint32_t ri = __float2uint_rz(__fmaf_rn((float)k, s_rw, 0.5f * s_rw));
+        const uint32_t xx = k - ri * w;
+        const uint32_t ly = (s_geo >> 16) + 8u * ri;
+        const uint32_t lt = ly * (uint32_t)tx + (s_geo & 255u) + xx;
+        // lanes of this round that hit the same tile: ranked in lane order
+        if (valid) s_own[lt] = (uint8_t)lane;
+        __syncwarp();
+        const bool lost = valid && s_own[lt] != (uint8_t)lane;
+        uint32_t peers = 1u << lane;
+        if (__any_sync(0xffffffffu, lost)) {
+#ifndef GES_BIN_BALLOT
+            peers = __match_any_sync(0xffffffffu, valid ? lt : 0xffffffffu);
+#else
+            const uint32_t cid = (ly >> 3) * (uint32_t)tx + (s_geo & 255u) + xx;
+            peers = __ballot_sync(0xffffffffu, valid);
+            for (int b = 0; b < a.rank_bits; ++b) {
+                const uint32_t bit = (cid >> b) & 1u;
+                const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+                peers &= bit ? bal : ~bal;
+            }
+#endif
+        }
+        uint32_t cur = 0;
+        if (valid) cur = s_cur[lt];
+        __syncwarp();
+        if (valid) {
+            a.list[cur + __popc(peers & lt_mask)] = s_pid;
+            if ((peers >> lane) == 1u) s_cur[lt] = cur + __popc(peers);
+        }
+        __syncwarp();
+    }
+};
     for (uint32_t b = 0; b < nb || qn > 0;) {
         if (b < nb) {
             // enqueue this stage's records with pairs in the warp's rows
@@ -390,18 +386,18 @@ __global__ void __launch_bounds__(kScatThreads) bin_scatter_kernel(BinArgs a) {
                 uint32_t g;
                 const bool rel = qi < n && class_pairs(r, R0, R1, warp, g) != 0u;
                 const uint32_t bal = __ballot_sync(0xffffffffu, rel);
-                if (rel) q[(qhead + qn + __popc(bal & lt_mask)) & (kQueue - 1)] = r;
+                if (rel) s_q[warp][(qhead + qn + __popc(bal & lt_mask)) & (kQueue - 1)] = r;
                 qn += __popc(bal);
                 __syncwarp();
                 if (qn >= 32) {  // expand a full group
-                    expand_group(a, q, mark, qhead, qn, 32, R0, R1, warp, lane, lt_mask, tx, s_cur, s_own);
+                    expand_group(32);
                 }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&s_empty[st]);
             ++b;
         } else {
-            expand_group(a, q, mark, qhead, qn, min(qn, 32), R0, R1, warp, lane, lt_mask, tx, s_cur, s_own);
+            expand_group(min(qn, 32));
         }
     }
 }
@@ -417,7 +413,7 @@ cudaError_t launch_bin(const BinArgs& a, cudaStream_t stream) {
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     bin_tilescan_kernel<<<1, kTileScanThreads, 0, stream>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    const int smem = kStages * kStageRec * 16 + a.win_rows * a.tiles_x * 5;  // ring, cursors, owner bytes
+    const int smem = kStages * kStageRec * 16;  // the record ring
     static int configured = 0;
     if (smem > configured) {
         if ((e = cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=

@@ -68,7 +68,7 @@ cudaError_t launch_item_scan(const ItemScanArgs& a, int64_t max_items, cudaStrea
 int64_t item_scan_tiles(int64_t n);
 
 // --- direct tile binning (bin.cu) -------------------------------------------
-constexpr int kBinWinTiles = 8192;    // tiles of one binning window (shared-memory cursors)
+constexpr int kBinWinTiles = 6144;    // tiles of one binning window (shared-memory cursors)
 constexpr int kBinItemCost = 4;       // chunk cost of an item, in pair slots
 struct BinArgs {
     const uint4* items;               // [V] item records in depth order (item scan)
