@@ -132,6 +132,7 @@ enum {
     GES_CTR_SLOTS = 3,    /* rect pairs = sum of rect areas (pair-slot count)       */
     GES_CTR_TICKET = 4,   /* scratch                                                */
     GES_CTR_CHUNKS = 5,   /* binning chunks of this frame (<= frame.bin_chunks)     */
+    GES_CTR_KEYMAX = 7,   /* largest visible depth key (depth sort pass plan)       */
     GES_CTR_N = 16
 };
 
@@ -143,8 +144,10 @@ typedef struct {
     int32_t width, height, tiles_x, tiles_y, num_tiles, tile_bits;
     int32_t sh_degree_max, _pad;
     int32_t band_begin, band_step; /* tile rows of this frame: band_begin + k band_step (ges_settings) */
-    int32_t band_rows, _pad2;      /* k < band_rows; the lists and ranges index band tiles
+    int32_t band_rows;             /* k < band_rows; the lists and ranges index band tiles
                                       t = k * tiles_x + tx, and rect rows are band rows k  */
+    uint32_t depth_key_base;       /* fp32 bits of the last ges_preprocess camera's near_z: every
+                                      visible depth key is larger (depth sort digit base)  */
     /* ---- S1 per-particle state ---- */
     float *depth;          /* [P] camera-space z                                       */
     float *pay0;           /* [P][4] (u, v, a, b): projected mean, conic a, b           */
@@ -160,10 +163,10 @@ typedef struct {
     /* ---- S2 depth sort of the visible particles ---- */
     uint32_t *vis_key[2];  /* [P] depth bits (0xffffffff = not visible), ping-pong */
     uint32_t *vis_val[2];  /* [P] particle index, ping-pong                      */
-    uint32_t *sorted_vis;  /* [V] visible particles in (depth, index) order (alias) */
+    uint32_t *sorted_vis;  /* [V] visible particles in (depth, index) order             */
     /* ---- S2 radix scratch (depth passes) ---- */
-    uint32_t *radix_hist;  /* [256][P/4096] per-tile digit counts -> offsets (digit-major) */
-    uint32_t *radix_total; /* [256] digit totals of the current depth pass                 */
+    uint32_t *radix_hist;  /* [256][G] per-CTA digit counts -> offsets (digit-major), G <= 1024 */
+    uint32_t *radix_total; /* [256] digit totals of the current pass, then [G] u64 area sums    */
     /* ---- S2 pairs and S3 ranges: direct tile binning ---- */
     uint32_t *item_offset; /* [P] first pair slot E of each depth-sorted visible particle  */
     uint32_t *item_rec;    /* [P][4] packed (E, particle, x0|y0<<16, x1|y1<<16)           */
@@ -174,7 +177,7 @@ typedef struct {
     int64_t bin_chunk_slots, bin_chunks; /* S, and the chunk capacity ceil((capacity + 4 P) / S) */
     uint32_t *list;        /* [cap] per-tile lists: tile t = list[ranges[t] .. ranges[t+1]) */
     uint32_t *ranges;      /* [T+1]                                               */
-    uint32_t *lookback;    /* decoupled look-back scratch (item scan)             */
+    uint32_t *lookback;    /* scratch (64 words, zeroed per frame)                 */
     uint64_t *counters;    /* [GES_CTR_N]                                         */
     size_t zero_bytes;     /* bytes from `counters` zeroed at the start of a frame */
     /* ---- S4 / S5 ---- */

@@ -3,7 +3,7 @@
 //
 // Input: the visible particles in (depth bits, index) order as packed item
 // records (E = first pair slot, particle, x0|y0<<16, x1|y1<<16 of the R10
-// rect; written by item_scan_kernel in sort.cu).  Output: the per-tile lists
+// rect; written by the item scan in sort.cu).  Output: the per-tile lists
 // list[ranges[t] .. ranges[t+1]) in (depth bits, index) order -- exactly the
 // order of a stable sort of the (tile << 32 | depth) keys -- without sorting
 // any pair.

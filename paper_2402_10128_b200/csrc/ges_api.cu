@@ -25,17 +25,6 @@ namespace {
 constexpr size_t kAlign = 256;
 size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
-// Look-back scratch of the item scan (the radix passes are chain-free).
-struct LookbackLayout {
-    size_t scan, total;  // word offsets
-};
-
-LookbackLayout lookback_layout(int64_t P, int64_t /*cap*/) {
-    LookbackLayout L;
-    L.scan = 0;
-    L.total = (size_t)item_scan_tiles(P);
-    return L;
-}
 
 int tiles_of(int px) { return (px + kTile - 1) / kTile; }
 
@@ -50,7 +39,6 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     const int tx = tiles_of(W), ty = tiles_of(H);
     const int64_t T = (int64_t)tx * ty;
     const int64_t HW = (int64_t)W * H;
-    const LookbackLayout L = lookback_layout(P, cap);
     size_t off = 0;
     auto take = [&](size_t bytes) -> char* {
         char* p = base ? base + off : nullptr;
@@ -64,7 +52,7 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     g.band_begin = 0; g.band_step = 1; g.band_rows = ty;
     // --- zero-per-frame region (one memset in ges_preprocess) ---
     g.counters = (uint64_t*)take(sizeof(uint64_t) * GES_CTR_N);
-    g.lookback = (uint32_t*)take(sizeof(uint32_t) * L.total);
+    g.lookback = (uint32_t*)take(sizeof(uint32_t) * 64);
     g.zero_bytes = off;  // bytes of the zero region from the workspace base
     // --- per particle ---
     g.depth = (float*)take(sizeof(float) * P);
@@ -80,9 +68,9 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
         g.vis_key[k] = (uint32_t*)take(sizeof(uint32_t) * P);
         g.vis_val[k] = (uint32_t*)take(sizeof(uint32_t) * P);
     }
-    g.sorted_vis = g.vis_val[0];
-    g.radix_hist = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * (size_t)radix_tiles(P));
-    g.radix_total = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits);
+    g.sorted_vis = (uint32_t*)take(sizeof(uint32_t) * P);
+    g.radix_hist = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * (size_t)kDsMaxGrid);
+    g.radix_total = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits + sizeof(uint64_t) * kDsMaxGrid);
     g.item_offset = (uint32_t*)take(sizeof(uint32_t) * P);
     g.item_rec = (uint32_t*)take(16 * (size_t)P);
     // binning chunks: S >= 16384 slots, and the [T][chunks] table bounded by 2^24 entries
@@ -173,6 +161,7 @@ ges_status ges_preprocess(const ges_particles* particles, const ges_camera* came
     int band_begin, band_step, band_rows;
     if (!band_of(settings, frame->tiles_y, &band_begin, &band_step, &band_rows)) return GES_ERR_INVALID_ARG;
     frame->band_begin = band_begin; frame->band_step = band_step; frame->band_rows = band_rows;
+    std::memcpy(&frame->depth_key_base, &camera->near_z, sizeof(uint32_t));
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(frame->counters, 0, frame->zero_bytes, s);
     if (e != cudaSuccess) return GES_ERR_CUDA;
@@ -195,39 +184,23 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     if (!frame) return GES_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long* ctr = (unsigned long long*)frame->counters;
-    const LookbackLayout L = lookback_layout(frame->P, frame->pair_capacity);
-    const int64_t hist_stride = radix_tiles(frame->P);
     cudaError_t e;
-    // depth sort: pass 0 reads all P keys and drops the non-visible ones (compaction);
-    // ping-pong (vis_key[0]) -> 1 -> 0 -> 1 -> (vis_val[0])
-    for (int d = 0; d < 4; ++d) {
-        RadixPassArgs p;
-        std::memset(&p, 0, sizeof(p));
-        const int in = (d == 0) ? 0 : ((d & 1) ? 1 : 0);
-        const int out = in ^ 1;
-        p.keys_in = frame->vis_key[in];
-        p.vals_in = (d == 0) ? nullptr : frame->vis_val[in];
-        p.keys_out = (d < 3) ? frame->vis_key[out] : nullptr;
-        p.vals_out = frame->vis_val[out];
-        p.count = (d == 0) ? nullptr : ctr + GES_CTR_VISIBLE;
-        p.max_items = frame->P;
-        p.tile_hist = frame->radix_hist;
-        p.hist_stride = hist_stride;
-        p.digit_total = frame->radix_total;
-        p.shift = 8 * d;
-        p.digit_bits = 8;
-        p.drop_invalid = (d == 0) ? 1 : 0;
-        if ((e = launch_radix_pass(p, s)) != cudaSuccess) return GES_ERR_CUDA;
-    }
-    frame->sorted_vis = frame->vis_val[0];
-    // pair slots of every sorted particle (rect areas), binning chunks, capacity check
-    ItemScanArgs is;
-    is.sorted_vis = frame->sorted_vis; is.rect = (const ushort4*)frame->rect; is.counters = ctr;
-    is.capacity = frame->pair_capacity;
-    is.E = frame->item_offset; is.items = (uint4*)frame->item_rec;
-    is.chunk_first = frame->chunk_first; is.chunk_slots = frame->bin_chunk_slots;
-    is.lookback = frame->lookback + L.scan; is.tile_counter = ctr + GES_CTR_TICKET;
-    if ((e = launch_item_scan(is, frame->P, s)) != cudaSuccess) return GES_ERR_CUDA;
+    // depth sort (4 passes; pass 0 compacts the visible set) + item scan: one
+    // cooperative kernel.  Keys: vis_key[0] -> [1] -> [0] -> [1] -> (values only) sorted_vis
+    DepthSortArgs ds;
+    ds.key0 = frame->vis_key[0];
+    ds.keys[0] = frame->vis_key[1]; ds.keys[1] = frame->vis_key[0];
+    ds.vals[0] = frame->vis_val[1]; ds.vals[1] = frame->vis_val[0];
+    ds.sorted_vis = frame->sorted_vis;
+    ds.hist = frame->radix_hist; ds.tot = frame->radix_total;
+    ds.part = (unsigned long long*)(frame->radix_total + kRadixDigits);
+    ds.P = frame->P; ds.G = 0; ds.key_base = frame->depth_key_base;
+    ds.rect = (const ushort4*)frame->rect;
+    ds.E = frame->item_offset; ds.items = (uint4*)frame->item_rec;
+    ds.chunk_first = frame->chunk_first; ds.chunk_slots = frame->bin_chunk_slots;
+    ds.capacity = frame->pair_capacity;
+    ds.counters = ctr;
+    if ((e = launch_depth_sort(ds, s)) != cudaSuccess) return GES_ERR_CUDA;
     // every (tile, particle) pair written once, in depth order, into its tile's list
     BinArgs b;
     b.items = (const uint4*)frame->item_rec; b.chunk_first = frame->chunk_first;

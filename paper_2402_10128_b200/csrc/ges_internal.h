@@ -33,39 +33,30 @@ cudaError_t launch_preprocess(const PreprocessArgs& a, cudaStream_t stream);
 
 // --- sort / ranges ---------------------------------------------------------
 int num_sms();
-constexpr int kRadixDigits = 256;
+constexpr int kRadixDigits = 512;  // max digits of a depth-sort pass (9 bits)
 
-struct RadixPassArgs {
-    const uint32_t* keys_in;
-    const uint32_t* vals_in;          // null: the value is the input index
-    uint32_t* keys_out;               // may be null
-    uint32_t* vals_out;
-    const unsigned long long* count;  // device item count (null: max_items)
-    int64_t max_items;                // upper bound (grid sizing); items beyond are ignored
-    uint32_t* tile_hist;              // [256][hist_stride] per-tile digit counts -> offsets (digit-major)
-    int64_t hist_stride;              // >= number of tiles
-    uint32_t* digit_total;            // [256] column totals of this pass
-    int shift;
-    int digit_bits;                   // bits of the digit that can be non-zero (1..8)
-    int drop_invalid;                 // 1: keys == 0xffffffff are dropped (compaction)
-};
-cudaError_t launch_radix_pass(const RadixPassArgs& a, cudaStream_t stream);
-int64_t radix_tiles(int64_t n);
+constexpr int kDsMaxGrid = 1024;      // max CTAs of the cooperative depth sort
 
-struct ItemScanArgs {
-    const uint32_t* sorted_vis;
+struct DepthSortArgs {
+    const uint32_t* key0;             // [P] preprocess keys: depth bits, 0xffffffff = not visible
+    uint32_t* keys[2];                // [P] ping-pong (keys[0] may not alias key0; keys[1] may)
+    uint32_t* vals[2];                // [P] ping-pong
+    uint32_t* sorted_vis;             // [V] out: visible particles in (depth bits, index) order
+    uint32_t* hist;                   // [256][G] per-CTA digit counts -> offsets
+    uint32_t* tot;                    // [256] digit totals
+    unsigned long long* part;         // [G] per-CTA rect-area sums (item scan)
+    int64_t P;
+    int G;                            // grid (set by the launcher)
+    uint32_t key_base;                // fp32 bits of near_z: every visible key is larger
     const ushort4* rect;
-    unsigned long long* counters;     // reads VISIBLE; writes SLOTS, OVERFLOW
-    int64_t capacity;
-    uint32_t* E;                      // [P]
-    uint4* items;                     // [P] packed (E, particle, rect x0|y0<<16, x1|y1<<16)
-    uint32_t* chunk_first;            // [cap/chunk_slots + 1] first item of every binning chunk
-    int64_t chunk_slots;              // pair slots per binning chunk (bin.cu)
-    uint32_t* lookback;               // [tiles]
-    unsigned long long* tile_counter;
+    uint32_t* E;                      // [V] first pair slot of each sorted particle
+    uint4* items;                     // [V] packed (E, particle, x0|y0<<16, x1|y1<<16)
+    uint32_t* chunk_first;            // [chunks + 1] first item of every binning chunk
+    int64_t chunk_slots;              // binning chunk cost S (bin.cu)
+    int64_t capacity;                 // pair capacity
+    unsigned long long* counters;     // reads VISIBLE; writes SLOTS, OVERFLOW, CHUNKS
 };
-cudaError_t launch_item_scan(const ItemScanArgs& a, int64_t max_items, cudaStream_t stream);
-int64_t item_scan_tiles(int64_t n);
+cudaError_t launch_depth_sort(const DepthSortArgs& a, cudaStream_t stream);
 
 // --- direct tile binning (bin.cu) -------------------------------------------
 constexpr int kBinWinTiles = 6144;    // tiles of one binning window (shared-memory cursors)
