@@ -204,13 +204,16 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
     const float fpx = (float)px + 0.5f;
     uint32_t start = a.ranges[tile], end = a.ranges[tile + 1];
     if (a.counters[GES_CTR_OVERFLOW]) start = end = 0;
-    float T[PPT], cr[PPT], cg[PPT], cb[PPT];
+    // per pixel: T, colour, last composited position; thr = the alpha skip
+    // threshold, 2 (never reached) once the pixel has stopped or lies outside
+    float T[PPT], cr[PPT], cg[PPT], cb[PPT], thr[PPT];
     uint32_t last[PPT], n_eval[PPT], n_comp[PPT];
     uint32_t done = 0;  // bit k: pixel k finished (or outside the image)
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
         T[k] = 1.0f; cr[k] = cg[k] = cb[k] = 0.0f; last[k] = 0; n_eval[k] = end - start; n_comp[k] = 0;
-        if (!(px < a.W && py0 + 4 * k < a.H)) done |= 1u << k;
+        thr[k] = kAlphaMin;
+        if (!(px < a.W && py0 + 4 * k < a.H)) { done |= 1u << k; thr[k] = 2.0f; }
     }
     constexpr uint32_t kAll = (1u << PPT) - 1u;
     StagedBatch sb{s_g0, s_g1, s_b, nullptr, s_mask};
@@ -229,25 +232,49 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
             const float dx = __fsub_rn(g0.x, fpx);
             const ExpCol ec = exp_col(g0.z, g0.w, dx);
             const uint32_t pos1 = b0 - start + j + 1;
-            // branch-free per pixel: the decisions become predicates
+            const bool clampk = g1.y > kAlphaMax;  // warp-uniform: only then can alpha reach 0.99
+            // alpha' = alpha if alpha >= thr (the skip test; thr = 2 for stopped pixels), else 0;
+            // the would-be transmittance T (1 - alpha') decides the stop.  (The exponent is not
+            // clamped at 0: the form is >= 0 up to rounding, G exceeds 1 by <= 2^-22 -- R19.)
+            float al[PPT], w[PPT], Tn[PPT];
+            float tmin = 1.0f;
 #pragma unroll
             for (int k = 0; k < PPT; ++k) {
                 const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
-                const float p2 = fminf(raw_exponent(ec, g1.x, dy), 0.0f);
-                const float alpha = fminf(kAlphaMax, __fmul_rn(g1.y, fast_exp2(p2)));
-                const bool live = !((done >> k) & 1u) && alpha >= kAlphaMin;
-                const float Tn = __fmul_rn(T[k], __fsub_rn(1.0f, alpha));
-                const bool stop = live && Tn < kTMin;
-                const bool comp = live && !stop;
-                done |= (stop ? 1u : 0u) << k;
-                if (DIAG) n_eval[k] = stop ? pos1 : n_eval[k];
-                const float w = comp ? __fmul_rn(alpha, T[k]) : 0.0f;
-                cr[k] = __fmaf_rn(g1.z, w, cr[k]);
-                cg[k] = __fmaf_rn(g1.w, w, cg[k]);
-                cb[k] = __fmaf_rn(gbl, w, cb[k]);
-                T[k] = comp ? Tn : T[k];
-                last[k] = comp ? pos1 : last[k];
-                if (DIAG) n_comp[k] += comp ? 1u : 0u;
+                float alpha = __fmul_rn(g1.y, fast_exp2(raw_exponent(ec, g1.x, dy)));
+                if (clampk) alpha = fminf(kAlphaMax, alpha);
+                al[k] = alpha >= thr[k] ? alpha : 0.0f;
+                w[k] = __fmul_rn(al[k], T[k]);
+                Tn[k] = __fsub_rn(T[k], w[k]);
+                tmin = fminf(tmin, Tn[k]);
+            }
+            if (!__any_sync(0xffffffffu, tmin < kTMin)) {
+                // common case: no pixel of the warp stops at this entry
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    cr[k] = __fmaf_rn(g1.z, w[k], cr[k]);
+                    cg[k] = __fmaf_rn(g1.w, w[k], cg[k]);
+                    cb[k] = __fmaf_rn(gbl, w[k], cb[k]);
+                    if (DIAG) n_comp[k] += al[k] > 0.0f ? 1u : 0u;
+                    last[k] = al[k] > 0.0f ? pos1 : last[k];
+                    T[k] = Tn[k];
+                }
+            } else {
+                // some pixel stops: it composites nothing more (R12)
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    const bool stop = Tn[k] < kTMin;  // implies alpha' > 0 (T >= 1e-4 before)
+                    const float wk = stop ? 0.0f : w[k];
+                    cr[k] = __fmaf_rn(g1.z, wk, cr[k]);
+                    cg[k] = __fmaf_rn(g1.w, wk, cg[k]);
+                    cb[k] = __fmaf_rn(gbl, wk, cb[k]);
+                    const bool comp = !stop && al[k] > 0.0f;
+                    if (DIAG) { n_comp[k] += comp ? 1u : 0u; n_eval[k] = stop ? pos1 : n_eval[k]; }
+                    last[k] = comp ? pos1 : last[k];
+                    T[k] = stop ? T[k] : Tn[k];
+                    thr[k] = stop ? 2.0f : thr[k];
+                    done |= (stop ? 1u : 0u) << k;
+                }
             }
         }
     }
@@ -361,13 +388,14 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
     const uint32_t start = ovf ? 0u : a.ranges[tile];
     const int plane = a.W * a.H;
     // U = T_final bg . g + sum over entries behind of c_j . g alpha_j T_j
-    float T[PPT], gr[PPT], gg[PPT], gb[PPT], U[PPT];
+    float T[PPT], gr[PPT], gg[PPT], gb[PPT], U[PPT], thr[PPT];
     uint32_t last[PPT];
     uint32_t my_max = 0;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
         const int py = py0 + 4 * k;
         T[k] = 1.0f; gr[k] = gg[k] = gb[k] = 0.0f; last[k] = 0;
+        thr[k] = 2.0f;  // inactive until the walk passes below the pixel's last entry
         float Tfin = 1.0f;
         if (px < a.W && py < a.H && !ovf) {
             const int pix = py * a.W + px;
@@ -387,6 +415,9 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
     if (lane == 0 && warp_max) atomicMax(&s_max, warp_max);
     __syncthreads();
     const uint32_t max_last = s_max;
+    // the largest `last` among the warp's inactive pixels: the walk (positions
+    // descending) activates them when it passes below it
+    uint32_t nxt = warp_max;
     const int red_comp = reduce9_component(lane);
     StagedBatch sb{s_g0, s_g1, s_b, s_pid, s_mask};
     for (int32_t b_end = (int32_t)max_last; b_end > 0; b_end -= kBatch) {
@@ -401,7 +432,15 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
         for (int i = nw - 1; i >= 0; --i) {
             const int j = s_list[warp][i];
             const uint32_t pos = (uint32_t)(b_begin + j);
-            bool contrib = false;
+            if (pos < nxt) {  // warp-uniform: some pixels start compositing here
+                uint32_t m = 0;
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    if (pos < last[k]) thr[k] = kAlphaMin;
+                    else m = max(m, last[k]);
+                }
+                nxt = __reduce_max_sync(0xffffffffu, m);
+            }
             const float4 g0 = s_g0[j];
             const float4 g1 = s_g1[j];
             const float rb = s_b[j];
@@ -410,35 +449,62 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             // Per pixel only the sums the chain rule needs: with q = G dalpha (kappa
             // factored out) and dp2 = kappa ln2 q, the conic/mean terms are
             // sum dp2 (dx, dy) and sum dp2 (dx^2, dx dy, dy^2); dx is the thread's
-            // column, so S0 = sum q, S1 = sum q dy, S2 = sum q dy^2 suffice.
-            float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, dk = 0.0f, dr = 0.0f, dgc = 0.0f, dbc = 0.0f;
+            // column, so S0 = sum q (= d alpha-part of dL/dkappa), S1 = sum q dy,
+            // S2 = sum q dy^2 suffice.  alpha' = alpha where the pixel composites
+            // this entry (alpha >= thr: active and not skipped), else 0; then every
+            // term below vanishes without a select.  (No exponent clamp: R19.)
+            float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, dr = 0.0f, dgc = 0.0f, dbc = 0.0f;
+            bool contrib = false;
+            if (!(g1.y > kAlphaMax)) {  // warp-uniform: alpha cannot reach the 0.99 clamp
+                const float rk = fast_rcp(g1.y);
 #pragma unroll
-            for (int k = 0; k < PPT; ++k) {
-                const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
-                const float p2raw = raw_exponent(ec, g1.x, dy);
-                const float G = fast_exp2(fminf(p2raw, 0.0f));
-                const float araw = __fmul_rn(g1.y, G);
-                const float alpha = fminf(kAlphaMax, araw);
-                const bool m = pos < last[k] && alpha >= kAlphaMin;
-                contrib |= m;
-                const float inv_om = fast_rcp(__fsub_rn(1.0f, alpha));
-                const float Tk = m ? T[k] * inv_om : T[k];  // transmittance before this entry
-                const float cgk = g1.z * gr[k] + g1.w * gg[k] + rb * gb[k];
-                const float w = m ? alpha * Tk : 0.0f;
-                const float dalpha = Tk * cgk - U[k] * inv_om;
-                const float dal = (m && araw < kAlphaMax) ? dalpha : 0.0f;
-                U[k] += cgk * w;
-                dr += w * gr[k];
-                dgc += w * gg[k];
-                dbc += w * gb[k];
-                const float q = G * dal;          // d L / d kappa contribution
-                dk += q;
-                const float qm = (p2raw <= 0.0f) ? q : 0.0f;  // exponent not clamped (R19)
-                S0 += qm;
-                const float t = qm * dy;
-                S1 += t;
-                S2 += t * dy;
-                T[k] = Tk;
+                for (int k = 0; k < PPT; ++k) {
+                    const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
+                    const float G = fast_exp2(raw_exponent(ec, g1.x, dy));
+                    const float alpha = __fmul_rn(g1.y, G);
+                    const float al = alpha >= thr[k] ? alpha : 0.0f;
+                    contrib |= al > 0.0f;
+                    const float inv_om = fast_rcp(__fsub_rn(1.0f, al));
+                    const float Tk = T[k] * inv_om;  // transmittance before this entry
+                    const float cgk = g1.z * gr[k] + g1.w * gg[k] + rb * gb[k];
+                    const float w = al * Tk;
+                    const float dalpha = Tk * cgk - U[k] * inv_om;
+                    U[k] += cgk * w;
+                    dr += w * gr[k];
+                    dgc += w * gg[k];
+                    dbc += w * gb[k];
+                    const float q = (al * rk) * dalpha;  // G dL/dalpha where composited
+                    S0 += q;
+                    const float t = q * dy;
+                    S1 += t;
+                    S2 += t * dy;
+                    T[k] = Tk;
+                }
+            } else {  // alpha = min(0.99, kappa G): no gradient through the clamp (R13)
+#pragma unroll
+                for (int k = 0; k < PPT; ++k) {
+                    const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
+                    const float G = fast_exp2(raw_exponent(ec, g1.x, dy));
+                    const float araw = __fmul_rn(g1.y, G);
+                    const float alpha = fminf(kAlphaMax, araw);
+                    const float al = alpha >= thr[k] ? alpha : 0.0f;
+                    contrib |= al > 0.0f;
+                    const float inv_om = fast_rcp(__fsub_rn(1.0f, al));
+                    const float Tk = T[k] * inv_om;
+                    const float cgk = g1.z * gr[k] + g1.w * gg[k] + rb * gb[k];
+                    const float w = al * Tk;
+                    const float dalpha = Tk * cgk - U[k] * inv_om;
+                    U[k] += cgk * w;
+                    dr += w * gr[k];
+                    dgc += w * gg[k];
+                    dbc += w * gb[k];
+                    const float q = (al > 0.0f && araw < kAlphaMax) ? G * dalpha : 0.0f;
+                    S0 += q;
+                    const float t = q * dy;
+                    S1 += t;
+                    S2 += t * dy;
+                    T[k] = Tk;
+                }
             }
             // alpha = kappa 2^p2: d alpha / d p2 = alpha ln 2, so dL/dp2 = kappa ln2 q
             const float kl = g1.y * 0.69314718055994531f;
@@ -449,7 +515,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             v[2] = dx * E;                       // d p2 / d A
             v[3] = dx * F;                       // d p2 / d B
             v[4] = kl * S2;                      // d p2 / d C
-            v[5] = dk;
+            v[5] = S0;                           // d alpha-part of d L / d kappa
             v[6] = dr;
             v[7] = dgc;
             v[8] = dbc;

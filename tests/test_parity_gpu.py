@@ -283,8 +283,8 @@ def test_screen_tile_bands_match_full_frame(world):
                 assert np.array_equal(full, band), (b, t, x)
     for n in G.PARAM_NAMES:
         a = getattr(acc, n).cpu().numpy().astype(np.float64)
-        # float atomics sum in another order: 1e-4 relative, plus a floor of 1e-6 of the
-        # group's largest entry for sums that cancel
+        # float atomics sum in another order: the north_star gradient tolerance (1e-3
+        # relative), plus a floor of 1e-6 of the group's largest entry for sums that cancel
         floor = 1e-6 + 1e-6 * np.abs(g_full[n]).max()
-        bad = np.abs(a - g_full[n]) > np.maximum(1e-4 * np.abs(g_full[n]), floor)
+        bad = np.abs(a - g_full[n]) > np.maximum(1e-3 * np.abs(g_full[n]), floor)
         assert bad.sum() == 0, (n, int(bad.sum()))
