@@ -42,9 +42,11 @@ __device__ __forceinline__ ParamIn load_params(const PreprocessArgs& a, int i) {
     return p;
 }
 
+// SH coefficient (plane 3k + ch) of this particle: sh[(3k + ch) * stride]
+// (global planes: sh = a.sh + i, stride P; a staged tile: its smem column, stride 128).
 template <int K>
 __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const CamDerived& cd, int i,
-                                                 const ParamIn& in) {
+                                                 const ParamIn& in, const float* sh, int sh_stride) {
     const int P = a.P;
     const CamParams& c = a.cam;
     PreOut o;
@@ -192,7 +194,7 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
     for (int ch = 0; ch < 3; ++ch) {
         float w[16];
 #pragma unroll
-        for (int k = 0; k < 16; ++k) w[k] = (k < K) ? __ldg(a.sh + (size_t)(3 * k + ch) * P + i) : 0.0f;
+        for (int k = 0; k < 16; ++k) w[k] = (k < K) ? sh[(size_t)(3 * k + ch) * sh_stride] : 0.0f;
         float acc = fmul(Y[0], w[0]);
 #pragma unroll
         for (int k = 1; k < K; ++k) acc = ffma(Y[k], w[k], acc);
@@ -215,6 +217,25 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
 
 constexpr int kPreThreads = 256;
 
+// Writes particle i's S1 state and its sort key (fp32 depth bits, or 0xffffffff
+// when not visible -- dropped by depth pass 0, which thereby compacts the
+// visible set).  Returns visibility.
+__device__ __forceinline__ bool store_out(const PreprocessArgs& a, int i, const PreOut& o) {
+    a.depth[i] = o.depth;
+    a.pay0[i] = make_float4(o.u, o.v, o.ca, o.cb);
+    a.pay1[i] = make_float4(o.cc, o.kappa, o.r, o.g);
+    a.pay2[i] = o.b;
+    a.radius[i] = o.radius;
+    a.rect[i] = make_ushort4((uint16_t)o.x0, (uint16_t)o.y0, (uint16_t)o.x1, (uint16_t)o.y1);
+    a.status[i] = o.status;
+    a.flags[i] = o.flags;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) a.drgb_ddir[(size_t)k * a.P + i] = o.J[k];
+    const bool vis = o.status == GES_VISIBLE;
+    a.vis_key[i] = vis ? __float_as_uint(o.depth) : 0xffffffffu;
+    return vis;
+}
+
 // Grid-stride over particles: no cross-CTA dependency.  Every particle writes
 // its S1 state and its sort key (fp32 depth bits, or 0xffffffff when not
 // visible -- dropped by depth pass 0, which thereby compacts the visible set).
@@ -231,26 +252,163 @@ __global__ void __launch_bounds__(kPreThreads, GES_PRE_MINB) preprocess_kernel(P
         bool vis = false;
         if (i < a.P) {
             const ParamIn in = load_params(a, i);
-            const PreOut o = preprocess_one<K>(a, cd, i, in);
-            a.depth[i] = o.depth;
-            a.pay0[i] = make_float4(o.u, o.v, o.ca, o.cb);
-            a.pay1[i] = make_float4(o.cc, o.kappa, o.r, o.g);
-            a.pay2[i] = o.b;
-            a.radius[i] = o.radius;
-            a.rect[i] = make_ushort4((uint16_t)o.x0, (uint16_t)o.y0, (uint16_t)o.x1, (uint16_t)o.y1);
-            a.status[i] = o.status;
-            a.flags[i] = o.flags;
-#pragma unroll
-            for (int k = 0; k < 9; ++k) a.drgb_ddir[(size_t)k * a.P + i] = o.J[k];
-            vis = o.status == GES_VISIBLE;
-            a.vis_key[i] = vis ? __float_as_uint(o.depth) : 0xffffffffu;
+            const PreOut o = preprocess_one<K>(a, cd, i, in, a.sh + i, a.P);
+            vis = store_out(a, i, o);
         }
         nvis += __popc(__ballot_sync(0xffffffffu, vis));
     }
     if (lane == 0 && nvis) atomicAdd(&a.counters[GES_CTR_VISIBLE], (unsigned long long)nvis);
 }
 
+// --- TMA-staged variant -------------------------------------------------------
+// One producer warp streams every input plane of a 128-particle tile (12 + 3K
+// planes x 512 B) into a 2-stage shared-memory ring with cp.async.bulk
+// (mbarrier completion); four consumer warps run S1 on the staged tile, one
+// particle per thread, and write the outputs directly.  The HBM reads of the
+// next tile overlap this tile's arithmetic without any loads held in registers.
+// Needs 16-B aligned planes (P % 4 == 0 and aligned base pointers); the last
+// partial tile is processed from global memory.
+constexpr int kPreTile = 128;
+constexpr int kPreStages = 2;
+constexpr int kPreTmaThreads = kPreTile + 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int K>
+__device__ __forceinline__ const float* pre_plane(const PreprocessArgs& a, int p) {
+    if (p < 3) return a.mean + (size_t)p * a.P;
+    if (p < 6) return a.log_scale + (size_t)(p - 3) * a.P;
+    if (p < 10) return a.quat + (size_t)(p - 6) * a.P;
+    if (p == 10) return a.opacity_logit;
+    if (p == 11) return a.beta;
+    return a.sh + (size_t)(p - 12) * a.P;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kPreTmaThreads) preprocess_tma_kernel(PreprocessArgs a) {
+    constexpr int NPL = 12 + 3 * K;
+    extern __shared__ __align__(128) float s_st[];  // [kPreStages][NPL][kPreTile]
+    __shared__ __align__(8) uint64_t s_full[kPreStages], s_empty[kPreStages];
+    __shared__ uint32_t s_nvis;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ntiles = a.P / kPreTile;
+    if (tid == 0) {
+        for (int st = 0; st < kPreStages; ++st) {
+            mbar_init(&s_full[st], 1);
+            mbar_init(&s_empty[st], kPreTile / 32);
+        }
+        s_nvis = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kPreTile / 32) {  // producer
+        if (lane == 0) {
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const int st = it % kPreStages;
+                if (it >= kPreStages) mbar_wait(&s_empty[st], ((it / kPreStages) - 1) & 1);
+                mbar_expect_tx(&s_full[st], NPL * kPreTile * 4);
+                float* dst = s_st + (size_t)st * NPL * kPreTile;
+                for (int p = 0; p < NPL; ++p)
+                    bulk_g2s(dst + p * kPreTile, pre_plane<K>(a, p) + (size_t)t * kPreTile, kPreTile * 4, &s_full[st]);
+            }
+        }
+        return;
+    }
+    const CamDerived cd = derive_camera(a.cam);
+    uint32_t nvis = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int st = it % kPreStages;
+        mbar_wait(&s_full[st], (it / kPreStages) & 1);
+        const float* sp = s_st + (size_t)st * NPL * kPreTile + tid;
+        ParamIn in;
+        in.mx = sp[0 * kPreTile]; in.my = sp[1 * kPreTile]; in.mz = sp[2 * kPreTile];
+        in.ls0 = sp[3 * kPreTile]; in.ls1 = sp[4 * kPreTile]; in.ls2 = sp[5 * kPreTile];
+        in.qw = sp[6 * kPreTile]; in.qx = sp[7 * kPreTile]; in.qy = sp[8 * kPreTile]; in.qz = sp[9 * kPreTile];
+        in.logit = sp[10 * kPreTile];
+        in.beta = sp[11 * kPreTile];
+        const int i = t * kPreTile + tid;
+        const PreOut o = preprocess_one<K>(a, cd, i, in, sp + 12 * kPreTile, kPreTile);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&s_empty[st]);  // the warp is done reading the stage
+        const bool vis = store_out(a, i, o);
+        nvis += __popc(__ballot_sync(0xffffffffu, vis));
+    }
+    // the partial last tile, from global memory
+    if (blockIdx.x == 0) {
+        const int i = ntiles * kPreTile + tid;
+        bool vis = false;
+        if (i < a.P) {
+            const ParamIn in = load_params(a, i);
+            const PreOut o = preprocess_one<K>(a, cd, i, in, a.sh + i, a.P);
+            vis = store_out(a, i, o);
+        }
+        nvis += __popc(__ballot_sync(0xffffffffu, vis));
+    }
+    if (lane == 0 && nvis) atomicAdd(&s_nvis, nvis);
+    asm volatile("bar.sync 1, %0;" ::"r"(kPreTile) : "memory");  // consumer warps only
+    if (tid == 0 && s_nvis) atomicAdd(&a.counters[GES_CTR_VISIBLE], (unsigned long long)s_nvis);
+}
+
+template <int K>
+static cudaError_t launch_preprocess_tma(const PreprocessArgs& a, cudaStream_t stream) {
+    constexpr int NPL = 12 + 3 * K;
+    const int smem = kPreStages * NPL * kPreTile * 4;
+    static int grid = 0;
+    if (grid == 0) {
+        cudaFuncSetAttribute(preprocess_tma_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, preprocess_tma_kernel<K>, kPreTmaThreads, smem);
+        grid = std::max(1, per_sm) * num_sms();
+    }
+    const int ntiles = a.P / kPreTile;
+    const int g = std::max(1, std::min(grid, ntiles));
+    preprocess_tma_kernel<K><<<g, kPreTmaThreads, smem, stream>>>(a);
+    return cudaGetLastError();
+}
+
+static bool planes_aligned(const PreprocessArgs& a) {
+    auto al = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+    return (a.P % 4) == 0 && a.P >= kPreTile && al(a.mean) && al(a.log_scale) && al(a.quat) &&
+           al(a.opacity_logit) && al(a.beta) && al(a.sh);
+}
+
 cudaError_t launch_preprocess(const PreprocessArgs& a, cudaStream_t stream) {
+#ifndef GES_PRE_NO_TMA
+    if (planes_aligned(a)) {
+        switch (a.sh_degree) {
+            case 0: return launch_preprocess_tma<1>(a, stream);
+            case 1: return launch_preprocess_tma<4>(a, stream);
+            case 2: return launch_preprocess_tma<9>(a, stream);
+            case 3: return launch_preprocess_tma<16>(a, stream);
+            default: return cudaErrorInvalidValue;
+        }
+    }
+#endif
     const int64_t need = (a.P + kPreThreads - 1) / kPreThreads;
     const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)num_sms() * 6));
     dim3 g((unsigned)grid), block(kPreThreads);
