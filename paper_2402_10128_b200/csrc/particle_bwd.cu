@@ -14,6 +14,8 @@
 //   u = fx x/z + cx, v = fy y/z + cy;  rgb = sum_k Y_k(dir) sh_k + 0.5 (>= 0)
 // HBM-bound: reads the parameters and 36 B of 2-D gradients, writes
 // (14 + 3K) * 4 B per visible particle.
+#include <algorithm>
+
 #include "ges_internal.h"
 
 namespace ges {
@@ -22,10 +24,34 @@ namespace ges {
 #define GES_PBWD_MINB 4
 #endif
 
+// The inputs S5b reads for one particle (from global memory or a staged tile).
+struct PbIn {
+    float m0, m1, m2, q0, q1, q2, q3, ls0, ls1, ls2, beta, logit;
+    float4 r0, r1, r2;  // the 12-float 2-D gradient record
+    float J[9];         // d rgb / d unit direction (S1)
+    int status, flags;
+};
+
+__device__ __forceinline__ PbIn pb_load_global(const ParticleBwdArgs& a, int i) {
+    const int P = a.P;
+    PbIn in;
+    in.status = a.status[i];
+    in.flags = a.flags[i];
+    in.m0 = __ldg(a.mean + i); in.m1 = __ldg(a.mean + P + i); in.m2 = __ldg(a.mean + 2 * P + i);
+    in.q0 = __ldg(a.quat + i); in.q1 = __ldg(a.quat + P + i); in.q2 = __ldg(a.quat + 2 * P + i);
+    in.q3 = __ldg(a.quat + 3 * P + i);
+    in.ls0 = __ldg(a.log_scale + i); in.ls1 = __ldg(a.log_scale + P + i); in.ls2 = __ldg(a.log_scale + 2 * P + i);
+    in.beta = __ldg(a.beta + i);
+    in.logit = __ldg(a.opacity_logit + i);
+    const float4* rrec = reinterpret_cast<const float4*>(a.grad2d) + (size_t)i * (kGrad2dStride / 4);
+    in.r0 = rrec[0]; in.r1 = rrec[1]; in.r2 = rrec[2];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) in.J[k] = __ldg(a.drgb_ddir + (size_t)k * P + i);
+    return in;
+}
+
 template <int K>
-__global__ void __launch_bounds__(256, GES_PBWD_MINB) particle_bwd_kernel(ParticleBwdArgs a) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= a.P) return;
+__device__ __forceinline__ void particle_bwd_one(const ParticleBwdArgs& a, int i, const PbIn& in) {
     const int P = a.P;
     const bool acc = a.accumulate != 0;
     auto put = [&](float* base, int plane, float val) {
@@ -35,7 +61,7 @@ __global__ void __launch_bounds__(256, GES_PBWD_MINB) particle_bwd_kernel(Partic
     // Every thread of a warp stores every plane in the same instruction (zeros
     // for particles that are not visible): full 32-B sectors, no partial-sector
     // read-modify-write in DRAM.
-    const bool vis = a.status[i] == GES_VISIBLE;
+    const bool vis = in.status == GES_VISIBLE;
     float o_mean[3] = {0.f, 0.f, 0.f}, o_ls[3] = {0.f, 0.f, 0.f}, o_q[4] = {0.f, 0.f, 0.f, 0.f};
     float o_op = 0.f, o_beta = 0.f;
     float Y[16], drgb[3] = {0.f, 0.f, 0.f};
@@ -45,14 +71,13 @@ __global__ void __launch_bounds__(256, GES_PBWD_MINB) particle_bwd_kernel(Partic
         const CamParams& cam = a.cam;
         const CamDerived cd = derive_camera(cam);
         const float W[9] = {cam.R[0], cam.R[1], cam.R[2], cam.R[3], cam.R[4], cam.R[5], cam.R[6], cam.R[7], cam.R[8]};
-        const int fl = a.flags[i];
+        const int fl = in.flags;
         // ---- forward recompute ----
-        const float m0 = __ldg(a.mean + i), m1 = __ldg(a.mean + P + i), m2 = __ldg(a.mean + 2 * P + i);
+        const float m0 = in.m0, m1 = in.m1, m2 = in.m2;
         const float tx = W[0] * m0 + W[1] * m1 + W[2] * m2 + cam.t[0];
         const float ty = W[3] * m0 + W[4] * m1 + W[5] * m2 + cam.t[1];
         const float tz = W[6] * m0 + W[7] * m1 + W[8] * m2 + cam.t[2];
-        const float q0 = __ldg(a.quat + i), q1 = __ldg(a.quat + P + i), q2 = __ldg(a.quat + 2 * P + i),
-                    q3 = __ldg(a.quat + 3 * P + i);
+        const float q0 = in.q0, q1 = in.q1, q2 = in.q2, q3 = in.q3;
         const float nq = sqrtf(q0 * q0 + q1 * q1 + q2 * q2 + q3 * q3);
         const float inq = 1.0f / nq;
         const float w = q0 * inq, x = q1 * inq, y = q2 * inq, z = q3 * inq;
@@ -61,14 +86,14 @@ __global__ void __launch_bounds__(256, GES_PBWD_MINB) particle_bwd_kernel(Partic
                             2.f * (x * z - w * y), 2.f * (y * z + w * x), 1.f - 2.f * (x * x + y * y)};
         float phi = 1.f, mfac = 1.f, dm_dbeta = 0.f;
         if (!a.gaussian_only) {
-            phi = 2.f / (1.f + expf(-(a.rho * (__ldg(a.beta + i) - 2.f))));
+            phi = 2.f / (1.f + expf(-(a.rho * (in.beta - 2.f))));
             const float dphi = a.rho * phi * (1.f - 0.5f * phi);
             if (a.phi_mode == GES_PHI_VARIANCE) { mfac = sqrtf(phi); dm_dbeta = 0.5f * dphi / mfac; }
             else { mfac = phi; dm_dbeta = dphi; }
         }
         float s[3], se[3];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) { s[k] = expf(__ldg(a.log_scale + (size_t)k * P + i)); se[k] = s[k] * mfac; }
+        for (int k = 0; k < 3; ++k) { s[k] = expf(k == 0 ? in.ls0 : (k == 1 ? in.ls1 : in.ls2)); se[k] = s[k] * mfac; }
         float M[9];
 #pragma unroll
         for (int j = 0; j < 3; ++j)
@@ -105,8 +130,7 @@ __global__ void __launch_bounds__(256, GES_PBWD_MINB) particle_bwd_kernel(Partic
         // ---- incoming 2-D gradients (pre-scaled conic -> a, b, c) ----
         // 12-float record (du, dv, dA, dB | dC, dkappa, dr, dg | db, -, -, -), zeroed
         // after reading so the buffer is clean for the next frame's backward
-        const float4* rrec = reinterpret_cast<const float4*>(a.grad2d) + (size_t)i * (kGrad2dStride / 4);
-        const float4 r0 = rrec[0], r1 = rrec[1], r2 = rrec[2];
+        const float4 r0 = in.r0, r1 = in.r1, r2 = in.r2;
         const float du = r0.x, dv = r0.y;
         const float da = r0.z * (-0.5f * kLog2e);
         const float db = r0.w * (-kLog2e);
@@ -196,9 +220,9 @@ __global__ void __launch_bounds__(256, GES_PBWD_MINB) particle_bwd_kernel(Partic
         float gx = 0.f, gy = 0.f, gz = 0.f;
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
-            gx += drgb[ch] * __ldg(a.drgb_ddir + (size_t)(3 * ch) * P + i);
-            gy += drgb[ch] * __ldg(a.drgb_ddir + (size_t)(3 * ch + 1) * P + i);
-            gz += drgb[ch] * __ldg(a.drgb_ddir + (size_t)(3 * ch + 2) * P + i);
+            gx += drgb[ch] * in.J[3 * ch];
+            gy += drgb[ch] * in.J[3 * ch + 1];
+            gz += drgb[ch] * in.J[3 * ch + 2];
         }
         const float dotd = ux * gx + uy * gy + uz * gz;
         dmean[0] += (gx - ux * dotd) * idn;
@@ -206,7 +230,7 @@ __global__ void __launch_bounds__(256, GES_PBWD_MINB) particle_bwd_kernel(Partic
         dmean[2] += (gz - uz * dotd) * idn;
 #pragma unroll
         for (int k = 0; k < 3; ++k) o_mean[k] = dmean[k];
-        const float kap = 1.f / (1.f + expf(-__ldg(a.opacity_logit + i)));
+        const float kap = 1.f / (1.f + expf(-in.logit));
         o_op = dk * kap * (1.f - kap);
     }  // vis
 #pragma unroll
@@ -228,7 +252,153 @@ __global__ void __launch_bounds__(256, GES_PBWD_MINB) particle_bwd_kernel(Partic
     rec[0] = z4; rec[1] = z4; rec[2] = z4;
 }
 
+template <int K>
+__global__ void __launch_bounds__(256, GES_PBWD_MINB) particle_bwd_kernel(ParticleBwdArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.P) return;
+    particle_bwd_one<K>(a, i, pb_load_global(a, i));
+}
+
+// --- TMA-staged variant (as S1's): a producer warp streams each 128-particle
+// tile's inputs -- 12 parameter planes, the 48-B 2-D gradient records, the 9
+// d rgb / d dir planes, status and flags (~17 KB) -- into a 3-stage ring
+// (cp.async.bulk, mbarriers); four consumer warps run the chain rule and store
+// the gradients.  Needs P % 4 == 0 and 16-B aligned planes; the partial last
+// tile goes through global loads.
+constexpr int kPbTile = 128;
+constexpr int kPbStages = 3;
+constexpr int kPbThreads = kPbTile + 32;
+constexpr int kPbPlanes = 12 + 9;
+struct PbStage {
+    float plane[kPbPlanes][kPbTile];       // mean 0-2, quat 3-6, log-scale 7-9, beta 10, logit 11, J 12-20
+    float4 rec[kPbTile * 3];               // grad2d records
+    uint8_t status[kPbTile], flags[kPbTile];
+};
+
+__device__ __forceinline__ uint32_t pb_smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void pb_mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(pb_smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void pb_mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra WAIT_%=;\n}" ::"r"(pb_smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void pb_mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(pb_smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void pb_mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(pb_smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void pb_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            pb_smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(pb_smem_u32(bar))
+        : "memory");
+}
+
+template <int K>
+__global__ void __launch_bounds__(kPbThreads) particle_bwd_tma_kernel(ParticleBwdArgs a) {
+    extern __shared__ __align__(128) unsigned char s_raw[];
+    PbStage* stg = reinterpret_cast<PbStage*>(s_raw);
+    __shared__ __align__(8) uint64_t s_full[kPbStages], s_empty[kPbStages];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int P = a.P, ntiles = P / kPbTile;
+    if (tid == 0) {
+        for (int st = 0; st < kPbStages; ++st) {
+            pb_mbar_init(&s_full[st], 1);
+            pb_mbar_init(&s_empty[st], kPbTile / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kPbTile / 32) {  // producer
+        if (lane == 0) {
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+                const int st = it % kPbStages;
+                if (it >= kPbStages) pb_mbar_wait(&s_empty[st], ((it / kPbStages) - 1) & 1);
+                constexpr uint32_t kBytes = kPbPlanes * kPbTile * 4 + kPbTile * 48 + 2 * kPbTile;
+                pb_mbar_expect_tx(&s_full[st], kBytes);
+                PbStage& S = stg[st];
+                const size_t i0 = (size_t)t * kPbTile;
+                const float* src[12] = {a.mean, a.mean + P, a.mean + 2 * (size_t)P, a.quat, a.quat + P,
+                                        a.quat + 2 * (size_t)P, a.quat + 3 * (size_t)P, a.log_scale,
+                                        a.log_scale + P, a.log_scale + 2 * (size_t)P, a.beta, a.opacity_logit};
+#pragma unroll
+                for (int p = 0; p < 12; ++p) pb_bulk(S.plane[p], src[p] + i0, kPbTile * 4, &s_full[st]);
+#pragma unroll
+                for (int k = 0; k < 9; ++k)
+                    pb_bulk(S.plane[12 + k], a.drgb_ddir + (size_t)k * P + i0, kPbTile * 4, &s_full[st]);
+                pb_bulk(S.rec, a.grad2d + i0 * kGrad2dStride, kPbTile * 48, &s_full[st]);
+                pb_bulk(S.status, a.status + i0, kPbTile, &s_full[st]);
+                pb_bulk(S.flags, a.flags + i0, kPbTile, &s_full[st]);
+            }
+        }
+        return;
+    }
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
+        const int st = it % kPbStages;
+        pb_mbar_wait(&s_full[st], (it / kPbStages) & 1);
+        const PbStage& S = stg[st];
+        PbIn in;
+        in.m0 = S.plane[0][tid]; in.m1 = S.plane[1][tid]; in.m2 = S.plane[2][tid];
+        in.q0 = S.plane[3][tid]; in.q1 = S.plane[4][tid]; in.q2 = S.plane[5][tid]; in.q3 = S.plane[6][tid];
+        in.ls0 = S.plane[7][tid]; in.ls1 = S.plane[8][tid]; in.ls2 = S.plane[9][tid];
+        in.beta = S.plane[10][tid]; in.logit = S.plane[11][tid];
+#pragma unroll
+        for (int k = 0; k < 9; ++k) in.J[k] = S.plane[12 + k][tid];
+        in.r0 = S.rec[3 * tid]; in.r1 = S.rec[3 * tid + 1]; in.r2 = S.rec[3 * tid + 2];
+        in.status = S.status[tid]; in.flags = S.flags[tid];
+        __syncwarp();
+        if (lane == 0) pb_mbar_arrive(&s_empty[st]);  // the warp has its inputs in registers
+        particle_bwd_one<K>(a, t * kPbTile + tid, in);
+    }
+    if (blockIdx.x == 0) {  // the partial last tile
+        const int i = ntiles * kPbTile + tid;
+        if (i < P) particle_bwd_one<K>(a, i, pb_load_global(a, i));
+    }
+}
+
+template <int K>
+static cudaError_t launch_particle_bwd_tma(const ParticleBwdArgs& a, cudaStream_t stream) {
+    const int smem = kPbStages * (int)sizeof(PbStage);
+    static int grid = 0;
+    if (grid == 0) {
+        cudaFuncSetAttribute(particle_bwd_tma_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, particle_bwd_tma_kernel<K>, kPbThreads, smem);
+        grid = std::max(1, per_sm) * num_sms();
+    }
+    const int g = std::max(1, std::min(grid, a.P / kPbTile));
+    particle_bwd_tma_kernel<K><<<g, kPbThreads, smem, stream>>>(a);
+    return cudaGetLastError();
+}
+
+static bool pb_aligned(const ParticleBwdArgs& a) {
+    auto al = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+    return (a.P % 4) == 0 && a.P >= kPbTile && al(a.mean) && al(a.log_scale) && al(a.quat) &&
+           al(a.opacity_logit) && al(a.beta) && al(a.drgb_ddir) && al(a.grad2d) && al(a.status) && al(a.flags);
+}
+
 cudaError_t launch_particle_bwd(const ParticleBwdArgs& a, cudaStream_t stream) {
+#ifndef GES_PBWD_NO_TMA
+    if (pb_aligned(a)) {
+        switch (a.sh_degree) {
+            case 0: return launch_particle_bwd_tma<1>(a, stream);
+            case 1: return launch_particle_bwd_tma<4>(a, stream);
+            case 2: return launch_particle_bwd_tma<9>(a, stream);
+            case 3: return launch_particle_bwd_tma<16>(a, stream);
+            default: return cudaErrorInvalidValue;
+        }
+    }
+#endif
     const int grid = (a.P + 255) / 256;
     switch (a.sh_degree) {
         case 0: particle_bwd_kernel<1><<<grid, 256, 0, stream>>>(a); break;
