@@ -51,14 +51,14 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback (B200_PROFILING.md)"
 
 
-STAGE_KERNEL = {"preprocess": "preprocess_kernel", "render_fwd": "render_fwd_kernel",
-                "render_bwd_tiles": "render_bwd_kernel", "backward_particles": "particle_bwd_kernel"}
+STAGE_KERNEL = {"preprocess": "preprocess_tma_kernel", "render_fwd": "render_fwd_kernel", "sort": "depth_sort_kernel",
+                "render_bwd_tiles": "render_bwd_kernel", "backward_particles": "particle_bwd_tma_kernel"}
 
 
 def committed_traffic(stage):
     """DRAM bytes per launch of the stage's kernel from the committed ncu --set full
-    capture (profiles/r1_traffic.json, written by tools/summarize_ncu.py traffic), or None."""
-    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    capture (profiles/r1b_traffic.json, written by tools/summarize_ncu.py traffic), or None."""
+    p = os.path.join(ROOT, "profiles", "r1b_traffic.json")
     k = STAGE_KERNEL.get(stage)
     if not k or not os.path.exists(p):
         return None, None
@@ -329,7 +329,7 @@ def run_ours(args) -> None:
         "render_fwd": ("alu", e_comp * FWD_OPS / (stage_ms[2] / 1e3) / 1e12, alu_peak, "Tinstr/s"),
         "preprocess": ("hbm", preprocess_bytes(P, int(cnt.visible), scene.particles.sh_degree)
                        / (stage_ms[0] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"),
-        "sort": ("hbm", sort_algorithmic_bytes(P, int(cnt.visible), int(cnt.pairs), frame.c.tiles_y > 1)
+        "sort": ("hbm", sort_algorithmic_bytes(P, int(cnt.visible), int(cnt.pairs), depth_passes(frame))
                  / (stage_ms[1] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"),
         "backward_particles": ("hbm", particle_bwd_bytes(P, int(cnt.visible), K) / (stage_ms[4] / 1e3) / 1e9,
                                peaks["hbm_gbs"], "GB/s"),
@@ -381,29 +381,42 @@ def run_ours(args) -> None:
 FWD_OPS = 20
 BWD_OPS = 38
 # preprocess, ranges, 4 depth passes x (hist, scan, scatter), item scan, 2 tile passes x 3, fwd, bwd tiles, particles
-LAUNCHES_PER_STEP = 1 + 1 + 12 + 1 + 6 + 1 + 1 + 1
+# preprocess, depth sort + item scan (one cooperative kernel), binning (count, column scan,
+# tile scan, scatter), fwd, bwd tiles, particle bwd
+LAUNCHES_PER_STEP = 1 + 1 + 4 + 1 + 1 + 1
 
 
 def preprocess_bytes(P, V, deg):
     K = (deg + 1) ** 2
-    # reads: 14 floats/particle (mean, log-scale, quat, logit, beta) for all, SH 3K floats for visible;
-    # writes: depth 4 + payload 36 + radius 4 + rect 8 + status/flags 2 = 54 B/particle, visible list 8 B/visible
-    return P * (4 * 12 + 54) + V * (4 * 3 * K + 8)
+    # reads: 12 floats/particle (mean, log-scale, quat, logit, beta) for all, SH 3K floats for visible;
+    # writes: depth 4 + payload 36 + radius 4 + rect 8 + status/flags 2 + d rgb/d dir 36 + key 4 = 94 B/particle
+    return P * (4 * 12 + 94) + V * 4 * 3 * K
 
 
-def sort_algorithmic_bytes(P, V, M, two_pass):
-    depth = P * 4 + V * 8 + 3 * V * 16      # pass 0 reads P keys, writes V (key, id); passes 1-3 move V
-    scan = V * (4 + 8 + 4 + 16)             # item scan: ids, rects; offsets + item records out
-    # pair passes: the first reads the item records and writes the M (key, id) pairs; the second
-    # moves them (8 B in, 8 B out); ranges read the M sorted keys
-    tiles = V * 16 + M * 8 + (M * 16 if two_pass else 0) + M * 4
-    return depth + scan + tiles
+def depth_passes(frame):
+    """Passes the depth sort ran: 9-bit digits over bits(max visible key - bits(near_z))."""
+    import torch
+    kmax = int(frame.view("counters", torch.int64, 16)[7].item()) & 0xffffffff
+    span = max(0, kmax - int(frame.c.depth_key_base))
+    return max(1, -(-span.bit_length() // 9))
+
+
+def sort_algorithmic_bytes(P, V, M, passes):
+    # depth sort: pass 0 reads the P keys twice (histogram, scatter); every later pass reads V keys
+    # (histogram) and V (key, id) (scatter); all but the last write V (key, id), the last writes
+    # the V ids and 16-B item records (gathering the 8-B rects)
+    depth = P * 4 * 2 + (passes - 1) * V * (4 + 8) + (passes - 1) * V * 8 + V * (4 + 16 + 8)
+    items = V * 16 * 2 + V * 8                 # item scan: records read twice, E + slot field written
+    # binning: count and scatter read the item records; the scatter writes the M list entries;
+    # the per-(chunk, tile) table and the ranges are O(chunks x tiles), small
+    binning = V * 16 * 2 + M * 4
+    return depth + items + binning
 
 
 def particle_bwd_bytes(P, V, K):
-    # reads: status/flags 2 B for all, params 14 floats + SH 3K floats + 48 B 2-D record for visible;
-    # writes: (14 + 3K) gradient floats for all (overwrite) + 48 B record reset for visible
-    return P * 2 + V * (4 * (14 + 3 * K) + 48 + 48) + P * 4 * (11 + 3 * K)
+    # reads: status/flags 2 B for all; params 12 floats + d rgb/d dir 9 floats + 48-B 2-D record for
+    # visible; writes: (14 + 3K) gradient floats for all (overwrite) + 48-B record reset
+    return P * 2 + V * (4 * (12 + 9) + 48 + 48) + P * 4 * (11 + 3 * K)
 
 
 def time_forward(G, params, cam, st, frame, image, flush, stream, steps):

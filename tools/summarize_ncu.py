@@ -14,10 +14,10 @@ import subprocess
 import sys
 
 
-# launches of each kernel in one bench step (config 3: 13 tile rows > 1 -> two pair passes)
-STEP = {"preprocess_kernel<16>": 1, "radix_hist_kernel<0>": 5, "radix_scan_kernel": 6, "radix_scatter_kernel<0>": 5,
-        "item_scan_kernel": 1, "gen_hist_kernel": 1, "radix_scatter_kernel<1>": 1, "ranges_kernel": 1,
-        "render_fwd_kernel<2, 0>": 1, "render_bwd_kernel<4>": 1, "particle_bwd_kernel<16>": 1}
+# launches of each kernel in one bench step
+STEP = {"preprocess_tma_kernel<16>": 1, "depth_sort_kernel": 1, "bin_count_kernel": 1, "bin_colscan_kernel": 1,
+        "bin_tilescan_kernel": 1, "bin_scatter_kernel": 1, "render_fwd_kernel<2, 0>": 1, "render_bwd_kernel<4>": 1,
+        "particle_bwd_tma_kernel<16>": 1}
 
 
 def share(path):
