@@ -52,6 +52,7 @@ typedef struct {
     int32_t phi_mode;
     int32_t gaussian_only;
     float bg[3];
+    int32_t kernel; /* 0: phi-bar-scaled Gaussian (R6); 1: exact GEF of Eq. 2 (NEXT-3) */
 } OrSettings;
 
 /* ------------------------------------------------------------------ */
@@ -292,6 +293,7 @@ typedef struct {
 typedef struct {
     int64_t P;
     const double *uv, *conic, *kappa, *rgb; /* planar [2][P], [3][P], [P], [3][P] */
+    const double *hbeta;                    /* [P] beta / 2 of the exact GEF kernel, or NULL (Gaussian) */
 } OrSplat2D;
 
 /* Decision thresholds are the fp32 constants of R7 (what the kernel compares
@@ -309,13 +311,15 @@ typedef struct {
     int32_t k;      /* position in the tile list */
     int32_t idx;    /* particle */
     double alpha, T, G, araw, dx, dy;
+    double Q, Qb;   /* exact kernel: Mahalanobis^2 Q and Q^(beta/2) */
     int clamped;    /* araw >= 0.99 -> alpha = 0.99, no gradient to kappa/power */
     int pos_power;  /* raw power > 0 was clamped to 0 */
 } OrComp;
 
 /* Front-to-back compositing of one pixel (Eq. 3 discretised: C = sum c_i a_i T_i,
  * T_i = prod_{j<i} (1 - a_j)), with the inherited rules (R7, R12):
- *   power = -1/2 (a dx^2 + c dy^2) - b dx dy, clamped to <= 0;
+ *   power = -1/2 (a dx^2 + c dy^2) - b dx dy, clamped to <= 0
+ *   [exact GEF kernel (Eq. 2): Q = -2 power, power = -1/2 Q^(beta/2)];
  *   alpha = min(0.99, kappa exp(power)); skip if alpha < 1/255;
  *   if T (1 - alpha) < 1e-4 stop WITHOUT compositing this particle.
  * Returns the number of composited entries written to rec (if rec != NULL).
@@ -338,11 +342,24 @@ static int composite_pixel(const OrSplat2D *s, const int32_t *lst, int64_t n, do
         double power = -qa - qb;
         int pos = 0;
         if (power > 0.0) { power = 0.0; pos = 1; }
+        /* fp32 error bound of alpha relative to itself (DESIGN.md R18) */
+        double erel = 2e-6 + 6e-7 * (fabs(qa) + fabs(qb)) + g_amb_margin;
+        double Q = 0.0, Qb = 0.0;
+        if (s->hbeta) {
+            const double hb = s->hbeta[i];
+            Q = -2.0 * power;
+            Qb = Q > 0.0 ? pow(Q, hb) : 0.0;
+            power = -0.5 * Qb;
+            /* the kernel's Q^(beta/2) = 2^(hb (log2 q + c)) and exp through MUFU approximations:
+             * relative error of Qb ~ ln2 hb (2.4e-7 |log2 Q| + 1.5 dq) + 2.4e-7, of G ~ Qb/2 that */
+            const double dq = 6e-7 * (fabs(qa) + fabs(qb)) / (qa + qb > 1e-30 ? qa + qb : 1e-30);
+            const double l2 = Q > 0.0 ? fabs(log2(Q)) : 0.0;
+            const double eQb = 0.6931 * hb * (2.4e-7 * l2 + 1.5 * dq) + 2.4e-7;
+            erel = 4.0 * (0.5 * Qb * eQb + 2.4e-7) + 2e-6 + g_amb_margin;
+        }
         const double G = exp(power);
         const double araw = s->kappa[i] * G;
         const double alpha = araw < OR_ALPHA_MAX ? araw : OR_ALPHA_MAX;
-        /* fp32 error bound of alpha relative to itself (DESIGN.md R18) */
-        const double erel = 2e-6 + 6e-7 * (fabs(qa) + fabs(qb)) + g_amb_margin;
         if (fabs(araw - OR_ALPHA_MIN) <= erel * araw) a |= 1;
         if (fabs(araw - OR_ALPHA_MAX) <= erel * araw) a |= 2;
         if (alpha < OR_ALPHA_MIN) continue;
@@ -355,6 +372,7 @@ static int composite_pixel(const OrSplat2D *s, const int32_t *lst, int64_t n, do
             OrComp *r = &rec[nrec];
             r->k = (int32_t)k; r->idx = i; r->alpha = alpha; r->T = T; r->G = G; r->araw = araw;
             r->dx = dx; r->dy = dy; r->clamped = !(araw < OR_ALPHA_MAX); r->pos_power = pos;
+            r->Q = Q; r->Qb = Qb;
         }
         ++nrec;
         T = Tn;
@@ -400,7 +418,11 @@ int or_render_fwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
  *   unclamped:  dL/dkappa += G dL/dalpha ;  dL/dpower = kappa G dL/dalpha
  *   dL/d(a,b,c) += dL/dpower (-dx^2/2, -dx dy, -dy^2/2)
  *   dL/d(u,v)   += dL/dpower (-(a dx + b dy), -(b dx + c dy))
- * Output g2d planar [9][P]: du, dv, da, db, dc, dkappa, dr, dg, db.
+ * exact GEF kernel: power = -1/2 Q^h, h = beta/2, Q = -2 power_g (the Gaussian
+ * power above), so the conic/mean chain takes dL/dpower_g = dL/dpower h Q^(h-1)
+ * and dL/dbeta += dL/dpower (-1/4 Q^h ln Q) (0 at Q = 0).
+ * Output g2d planar [10][P]: du, dv, da, db, dc, dkappa, dr, dg, db, dbeta. */
+/* (Gaussian kernel: the dbeta plane is 0; beta enters through phi-bar in S5b.)
  * Accumulation order is fixed: tiles ascending, pixels row-major within the
  * tile, list order -- independent of the thread count. */
 int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets, const int32_t *list,
@@ -409,7 +431,7 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
     const int64_t P = s->P;
     const int64_t T = (int64_t)sc->tiles_x * sc->tiles_y;
     const int64_t total = offsets[T];
-    double *acc = (double *)calloc((size_t)(total > 0 ? total : 1) * 9, sizeof(double));
+    double *acc = (double *)calloc((size_t)(total > 0 ? total : 1) * 10, sizeof(double));
     if (!acc) return -1;
 #pragma omp parallel
     {
@@ -422,7 +444,7 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
             const int tx = (int)(t % sc->tiles_x), ty = (int)(t / sc->tiles_x);
             const int32_t *lst = list + offsets[t];
             const int64_t n = offsets[t + 1] - offsets[t];
-            double *a9 = acc + offsets[t] * 9;
+            double *a9 = acc + offsets[t] * 10;
             for (int yy = 0; yy < 16; ++yy)
                 for (int xx = 0; xx < 16; ++xx) {
                     const int px = tx * 16 + xx, py = ty * 16 + yy;
@@ -441,11 +463,17 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
                         const double cg = s->rgb[i] * g[0] + s->rgb[P + i] * g[1] + s->rgb[2 * P + i] * g[2];
                         const double dalpha = c->T * cg - (suffix + Tf * gbg) / (1.0 - c->alpha);
                         suffix += cg * c->alpha * c->T;
-                        double *o = a9 + (int64_t)c->k * 9;
+                        double *o = a9 + (int64_t)c->k * 10;
                         for (int ch = 0; ch < 3; ++ch) o[6 + ch] += c->alpha * c->T * g[ch];
                         if (c->clamped) continue;
                         o[5] += c->G * dalpha;
-                        const double dpow = c->pos_power ? 0.0 : c->araw * dalpha;
+                        double dpow = c->pos_power ? 0.0 : c->araw * dalpha;
+                        if (s->hbeta) {
+                            const double hb = s->hbeta[i];
+                            const double d_all = c->araw * dalpha;  /* dL/dpower of the GEF power */
+                            o[9] += c->Q > 0.0 ? d_all * (-0.25 * c->Qb * log(c->Q)) : 0.0;
+                            dpow = c->Q > 0.0 ? d_all * hb * pow(c->Q, hb - 1.0) : 0.0;
+                        }
                         const double ca = s->conic[i], cb = s->conic[P + i], cc = s->conic[2 * P + i];
                         const double dx = c->dx, dy = c->dy;
                         o[0] += dpow * (-(ca * dx + cb * dy));
@@ -458,12 +486,12 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
         }
         free(rec);
     }
-    memset(g2d, 0, sizeof(double) * 9 * (size_t)P);
+    memset(g2d, 0, sizeof(double) * 10 * (size_t)P);
     for (int64_t t = 0; t < T; ++t) {
         if (tile_mask && !tile_mask[t]) continue;
         for (int64_t k = offsets[t]; k < offsets[t + 1]; ++k) {
             const int32_t i = list[k];
-            for (int c = 0; c < 9; ++c) g2d[c * P + i] += acc[k * 9 + c];
+            for (int c = 0; c < 10; ++c) g2d[c * P + i] += acc[k * 10 + c];
         }
     }
     free(acc);
@@ -571,7 +599,7 @@ int or_backward_particles(const OrParticles_f64 *pp, const OrCamera *cam, const 
                              2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)};
         double s[3], se[3];
         double phi = 1.0, mfac = 1.0, dm_dbeta = 0.0;
-        if (!st->gaussian_only) {
+        if (!st->gaussian_only && st->kernel == 0) {
             phi = 2.0 / (1.0 + exp(-(rho * (pp->beta[i] - 2.0))));
             const double dphi = rho * phi * (1.0 - 0.5 * phi); /* d phi-bar / d beta */
             if (st->phi_mode == OR_PHI_VARIANCE) { mfac = sqrt(phi); dm_dbeta = 0.5 * dphi / mfac; }
@@ -629,7 +657,7 @@ int or_backward_particles(const OrParticles_f64 *pp, const OrCamera *cam, const 
             gls[k * P + i] = dse[k] * se[k];
             dbeta += dse[k] * s[k] * dm_dbeta;
         }
-        gbeta[i] = dbeta;
+        gbeta[i] = dbeta + (st->kernel == 1 ? g2d[9 * P + i] : 0.0);  /* exact GEF: the direct term */
         /* R(q-hat) partials */
         double dqh[4];
         dqh[0] = dR[1] * (-2 * z) + dR[2] * (2 * y) + dR[3] * (2 * z) + dR[5] * (-2 * x) + dR[6] * (-2 * y) + dR[7] * (2 * x);

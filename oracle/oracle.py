@@ -56,7 +56,7 @@ class _Camera(C.Structure):
 
 class _Settings(C.Structure):
     _fields_ = [("rho", C.c_float), ("phi_mode", C.c_int32), ("gaussian_only", C.c_int32),
-                ("bg", C.c_float * 3)]
+                ("bg", C.c_float * 3), ("kernel", C.c_int32)]
 
 
 def _particles_struct(ctype):
@@ -88,7 +88,7 @@ class _Geom(C.Structure):
 
 
 class _Splat2D(C.Structure):
-    _fields_ = [("P", C.c_int64)] + [(n, C.POINTER(C.c_double)) for n in ("uv", "conic", "kappa", "rgb")]
+    _fields_ = [("P", C.c_int64)] + [(n, C.POINTER(C.c_double)) for n in ("uv", "conic", "kappa", "rgb", "hbeta")]
 
 
 def lib():
@@ -122,12 +122,16 @@ def set_num_threads(n: int) -> None:
 # ---------------------------------------------------------------------------
 # inputs
 # ---------------------------------------------------------------------------
+KERNEL_PHI_GAUSS, KERNEL_EXACT_BETA = 0, 1
+
+
 @dataclass
 class Settings:
     rho: float = 0.1
     phi_mode: int = PHI_SCALE
     gaussian_only: int = 0
     background: tuple = (0.0, 0.0, 0.0)
+    kernel: int = KERNEL_PHI_GAUSS  # 1: the exact GEF kernel of Eq. 2
 
 
 def _cam(cam) -> _Camera:
@@ -146,6 +150,7 @@ def _cam(cam) -> _Camera:
 def _settings(st: Settings) -> _Settings:
     s = _Settings()
     s.rho, s.phi_mode, s.gaussian_only = st.rho, int(st.phi_mode), int(st.gaussian_only)
+    s.kernel = int(st.kernel)
     for k in range(3):
         s.bg[k] = float(st.background[k])
     return s
@@ -200,6 +205,8 @@ def preprocess(parts, cam, st: Settings, precision: str = "f32") -> dict:
     fn = lib().or_preprocess_f32 if precision == "f32" else lib().or_preprocess_f64
     fn(C.byref(ps), C.byref(c), C.byref(s), C.byref(pre))
     out["precision"] = precision
+    # exact GEF kernel: beta / 2 per particle for the compositing (exact halving of the stored beta)
+    out["hbeta"] = 0.5 * np.asarray(parts.beta, dtype).astype(np.float64) if int(st.kernel) == 1 else None
     out["tiles_x"] = (cam.width + 15) // 16
     out["tiles_y"] = (cam.height + 15) // 16
     return out
@@ -314,6 +321,8 @@ def _splat(pre, keep):
     for n in ("uv", "conic", "kappa", "rgb"):
         a = keep(np.ascontiguousarray(pre[n], dtype=np.float64))
         setattr(s, n, _ptr(a, C.c_double))
+    if pre.get("hbeta") is not None:
+        s.hbeta = _ptr(keep(np.ascontiguousarray(pre["hbeta"], dtype=np.float64)), C.c_double)
     return s
 
 
@@ -340,11 +349,12 @@ def render_fwd(pre, cam, st: Settings, offsets, lst, tile_mask=None) -> dict:
 
 
 def render_bwd(pre, cam, st: Settings, offsets, lst, dL_dimg, tile_mask=None) -> np.ndarray:
-    """S5a: per-particle 2D gradients g2d [9][P] = (du, dv, da, db, dc, dkappa, dr, dg, db)."""
+    """S5a: per-particle 2D gradients g2d [10][P] = (du, dv, da, db, dc, dkappa, dr, dg, db, dbeta);
+    dbeta (the exact GEF kernel's direct shape term) is 0 for the phi-bar Gaussian kernel."""
     keep = _Keep()
     sp = _splat(pre, keep)
     P = pre["status"].size
-    g2d = np.zeros((9, P), np.float64)
+    g2d = np.zeros((10, P), np.float64)
     g = keep(np.ascontiguousarray(dL_dimg, dtype=np.float64))
     mp = None
     if tile_mask is not None:
