@@ -105,7 +105,18 @@ typedef struct {
      * of a band are identical to the full frame's; pixels outside it are untouched;
      * the S5 gradients of all bands sum to the full frame's. */
     int32_t tile_row_begin, tile_row_step;
+    /* Per-pixel kernel (ges_kernel).  GES_KERNEL_PHI_GAUSS (0): the paper's
+     * rasterization -- a Gaussian of the phi-bar-scaled covariance
+     * (R6).  GES_KERNEL_EXACT_BETA (1): Eq. 2 itself
+     * (SURVEY.md §8(f) NEXT-3): no phi-bar, per pixel
+     * alpha = min(0.99, kappa exp(-1/2 Q^(beta/2))), Q the Mahalanobis form of the
+     * dilated Sigma2D; rects bound Q <= (2 ln(255 kappa / 0.98))^(2/beta); the
+     * backward adds Eq. 2's direct dL/dbeta.  beta must be > 0 (else the particle
+     * is GES_DEGENERATE).  gaussian_only is ignored in this mode. */
+    int32_t kernel;
 } ges_settings;
+
+typedef enum { GES_KERNEL_PHI_GAUSS = 0, GES_KERNEL_EXACT_BETA = 1 } ges_kernel;
 
 /* Gradients, planar [C][P] fp32 in the parameter layout.  accumulate = 1 adds
  * into the buffers (several views before one allreduce), 0 overwrites. */
@@ -142,7 +153,8 @@ enum {
 typedef struct {
     int64_t P, pair_capacity;
     int32_t width, height, tiles_x, tiles_y, num_tiles, tile_bits;
-    int32_t sh_degree_max, _pad;
+    int32_t sh_degree_max;
+    int32_t kernel;                /* ges_kernel of the last ges_preprocess (renders must match) */
     int32_t band_begin, band_step; /* tile rows of this frame: band_begin + k band_step (ges_settings) */
     int32_t band_rows;             /* k < band_rows; the lists and ranges index band tiles
                                       t = k * tiles_x + tx, and rect rows are band rows k  */
@@ -153,6 +165,7 @@ typedef struct {
     float *pay0;           /* [P][4] (u, v, a, b): projected mean, conic a, b           */
     float *pay1;           /* [P][4] (c, kappa, r, g): conic c, opacity, colour r, g    */
     float *pay2;           /* [P]    colour b                                           */
+    float *pay3;           /* [P]    beta / 2 (exact GEF kernel only)                    */
     int32_t *radius;       /* [P] screen radius (pixels)                                */
     uint16_t *rect;        /* [P][4] tile rect x0, y0, x1, y1 (exclusive ends)           */
     uint8_t *status;       /* [P] ges_particle_status                                   */

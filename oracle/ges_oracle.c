@@ -350,12 +350,15 @@ static int composite_pixel(const OrSplat2D *s, const int32_t *lst, int64_t n, do
             Q = -2.0 * power;
             Qb = Q > 0.0 ? pow(Q, hb) : 0.0;
             power = -0.5 * Qb;
-            /* the kernel's Q^(beta/2) = 2^(hb (log2 q + c)) and exp through MUFU approximations:
-             * relative error of Qb ~ ln2 hb (2.4e-7 |log2 Q| + 1.5 dq) + 2.4e-7, of G ~ Qb/2 that */
+            /* R18 for the kernel's fp32 path Q^(beta/2) = 2^(hb (log2 q + c)), G = 2^(c' Q^hb):
+             * q carries the quadratic form's relative error dq (the Gaussian bound's 6e-7),
+             * lg2.approx adds <= 2.4e-7 absolute, hb (log2 Q) one rounding, ex2.approx <= 2.4e-7
+             * relative; G's relative error is Q^hb / 2 times Qb's.  Safety factor 2. */
             const double dq = 6e-7 * (fabs(qa) + fabs(qb)) / (qa + qb > 1e-30 ? qa + qb : 1e-30);
             const double l2 = Q > 0.0 ? fabs(log2(Q)) : 0.0;
-            const double eQb = 0.6931 * hb * (2.4e-7 * l2 + 1.5 * dq) + 2.4e-7;
-            erel = 4.0 * (0.5 * Qb * eQb + 2.4e-7) + 2e-6 + g_amb_margin;
+            const double eL = 2.4e-7 + dq / 0.6931;
+            const double eQb = 0.6931 * (hb * eL + 6e-8 * hb * l2) + 2.4e-7;
+            erel = 2.0 * (0.5 * Qb * eQb + 2.4e-7) + 2e-6 + g_amb_margin;
         }
         const double G = exp(power);
         const double araw = s->kappa[i] * G;

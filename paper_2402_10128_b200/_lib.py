@@ -17,6 +17,7 @@ LIB_PATH = os.environ.get("GES_LIB") or os.path.join(_HERE, "libges.so")
 
 GES_OK, GES_ERR_INVALID_ARG, GES_ERR_CAPACITY, GES_ERR_CUDA, GES_ERR_UNSUPPORTED = range(5)
 GES_PHI_SCALE, GES_PHI_VARIANCE = 0, 1
+GES_KERNEL_PHI_GAUSS, GES_KERNEL_EXACT_BETA = 0, 1
 GES_VISIBLE, GES_CULL_NEAR, GES_DEGENERATE, GES_OFFSCREEN = range(4)
 GES_CTR_VISIBLE, GES_CTR_PAIRS, GES_CTR_OVERFLOW, GES_CTR_SLOTS, GES_CTR_TICKET, GES_CTR_CHUNKS = 0, 1, 2, 3, 4, 5
 GES_CTR_KEYMAX, GES_CTR_N = 7, 16
@@ -38,7 +39,8 @@ class ges_camera(C.Structure):
 
 class ges_settings(C.Structure):
     _fields_ = [("rho", C.c_float), ("phi_mode", C.c_int32), ("gaussian_only", C.c_int32),
-                ("background", C.c_float * 3), ("tile_row_begin", C.c_int32), ("tile_row_step", C.c_int32)]
+                ("background", C.c_float * 3), ("tile_row_begin", C.c_int32), ("tile_row_step", C.c_int32),
+                ("kernel", C.c_int32)]
 
 
 class ges_grads(C.Structure):
@@ -55,9 +57,9 @@ class ges_frame(C.Structure):
     _fields_ = [
         ("P", C.c_int64), ("pair_capacity", C.c_int64),
         ("width", C.c_int32), ("height", C.c_int32), ("tiles_x", C.c_int32), ("tiles_y", C.c_int32),
-        ("num_tiles", C.c_int32), ("tile_bits", C.c_int32), ("sh_degree_max", C.c_int32), ("_pad", C.c_int32),
+        ("num_tiles", C.c_int32), ("tile_bits", C.c_int32), ("sh_degree_max", C.c_int32), ("kernel", C.c_int32),
         ("band_begin", C.c_int32), ("band_step", C.c_int32), ("band_rows", C.c_int32), ("depth_key_base", C.c_uint32),
-        ("depth", C.c_void_p), ("pay0", C.c_void_p), ("pay1", C.c_void_p), ("pay2", C.c_void_p),
+        ("depth", C.c_void_p), ("pay0", C.c_void_p), ("pay1", C.c_void_p), ("pay2", C.c_void_p), ("pay3", C.c_void_p),
         ("radius", C.c_void_p), ("rect", C.c_void_p), ("status", C.c_void_p), ("flags", C.c_void_p),
         ("drgb_ddir", C.c_void_p),
         ("vis_key", C.c_void_p * 2), ("vis_val", C.c_void_p * 2), ("sorted_vis", C.c_void_p),

@@ -35,6 +35,7 @@ class Settings:
     background: Sequence[float] = (0.0, 0.0, 0.0)
     tile_row_begin: int = 0          # screen-tile band: rows begin + k*step (ges.h)
     tile_row_step: int = 1
+    kernel: int = L.GES_KERNEL_PHI_GAUSS  # GES_KERNEL_EXACT_BETA: Eq. 2 per pixel (NEXT-3)
 
     def c(self) -> L.ges_settings:
         s = L.ges_settings()
@@ -42,6 +43,7 @@ class Settings:
         for k in range(3):
             s.background[k] = float(self.background[k])
         s.tile_row_begin, s.tile_row_step = int(self.tile_row_begin), int(self.tile_row_step)
+        s.kernel = int(self.kernel)
         return s
 
 

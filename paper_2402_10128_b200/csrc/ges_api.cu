@@ -59,6 +59,7 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     g.pay0 = (float*)take(16 * (size_t)P);
     g.pay1 = (float*)take(16 * (size_t)P);
     g.pay2 = (float*)take(sizeof(float) * P);
+    g.pay3 = (float*)take(sizeof(float) * P);
     g.radius = (int32_t*)take(sizeof(int32_t) * P);
     g.rect = (uint16_t*)take(8 * (size_t)P);
     g.status = (uint8_t*)take((size_t)P);
@@ -119,7 +120,7 @@ bool band_of(const ges_settings* s, int tiles_y, int* begin, int* step, int* row
 
 bool band_matches(const ges_settings* s, const ges_frame* f) {
     int b, n, r;
-    return band_of(s, f->tiles_y, &b, &n, &r) && b == f->band_begin && n == f->band_step;
+    return band_of(s, f->tiles_y, &b, &n, &r) && b == f->band_begin && n == f->band_step && s->kernel == f->kernel;
 }
 
 bool camera_ok(const ges_camera* c, const ges_frame* f) {
@@ -156,11 +157,13 @@ ges_status ges_frame_init(void* workspace, size_t bytes, int64_t P, int32_t widt
 ges_status ges_preprocess(const ges_particles* particles, const ges_camera* camera, const ges_settings* settings,
                           ges_frame* frame, void* stream) {
     if (!frame || !settings || !particles_ok(particles) || !camera_ok(camera, frame) || particles->P != frame->P ||
-        !(settings->rho >= 0.0f) || (settings->phi_mode != GES_PHI_SCALE && settings->phi_mode != GES_PHI_VARIANCE))
+        !(settings->rho >= 0.0f) || (settings->phi_mode != GES_PHI_SCALE && settings->phi_mode != GES_PHI_VARIANCE) ||
+        (settings->kernel != GES_KERNEL_PHI_GAUSS && settings->kernel != GES_KERNEL_EXACT_BETA))
         return GES_ERR_INVALID_ARG;
     int band_begin, band_step, band_rows;
     if (!band_of(settings, frame->tiles_y, &band_begin, &band_step, &band_rows)) return GES_ERR_INVALID_ARG;
     frame->band_begin = band_begin; frame->band_step = band_step; frame->band_rows = band_rows;
+    frame->kernel = settings->kernel;
     std::memcpy(&frame->depth_key_base, &camera->near_z, sizeof(uint32_t));
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaMemsetAsync(frame->counters, 0, frame->zero_bytes, s);
@@ -170,8 +173,10 @@ ges_status ges_preprocess(const ges_particles* particles, const ges_camera* came
     a.opacity_logit = particles->opacity_logit; a.sh = particles->sh; a.beta = particles->beta;
     a.P = (int)particles->P; a.sh_degree = particles->sh_degree;
     a.rho = settings->rho; a.phi_mode = settings->phi_mode; a.gaussian_only = settings->gaussian_only ? 1 : 0;
+    a.kernel = settings->kernel;
     a.cam = cam_params(camera);
     a.depth = frame->depth; a.pay0 = (float4*)frame->pay0; a.pay1 = (float4*)frame->pay1; a.pay2 = frame->pay2;
+    a.pay3 = frame->pay3;
     a.radius = frame->radius; a.rect = (ushort4*)frame->rect; a.status = frame->status; a.flags = frame->flags;
     a.drgb_ddir = frame->drgb_ddir;
     a.vis_key = frame->vis_key[0];
@@ -219,6 +224,7 @@ ges_status ges_render_fwd(ges_frame* frame, const ges_settings* settings, float*
     if (!frame || !settings || !image || !band_matches(settings, frame)) return GES_ERR_INVALID_ARG;
     RenderFwdArgs a;
     a.pay0 = (const float4*)frame->pay0; a.pay1 = (const float4*)frame->pay1; a.pay2 = frame->pay2;
+    a.pay3 = frame->pay3; a.exact = frame->kernel == GES_KERNEL_EXACT_BETA;
     a.list = frame->list; a.ranges = frame->ranges; a.counters = (const unsigned long long*)frame->counters;
     a.W = frame->width; a.H = frame->height; a.tiles_x = frame->tiles_x; a.tiles_y = frame->band_rows;
     a.band_begin = frame->band_begin; a.band_step = frame->band_step;
@@ -233,6 +239,7 @@ ges_status ges_render_bwd_tiles(const ges_settings* settings, ges_frame* frame, 
     if (!frame || !settings || !dL_dimage || !band_matches(settings, frame)) return GES_ERR_INVALID_ARG;
     RenderBwdArgs b;
     b.pay0 = (const float4*)frame->pay0; b.pay1 = (const float4*)frame->pay1; b.pay2 = frame->pay2;
+    b.pay3 = frame->pay3; b.exact = frame->kernel == GES_KERNEL_EXACT_BETA;
     b.list = frame->list; b.ranges = frame->ranges; b.counters = (const unsigned long long*)frame->counters;
     b.W = frame->width; b.H = frame->height; b.tiles_x = frame->tiles_x; b.tiles_y = frame->band_rows;
     b.band_begin = frame->band_begin; b.band_step = frame->band_step;
@@ -254,6 +261,7 @@ ges_status ges_backward_particles(const ges_particles* particles, const ges_came
     q.opacity_logit = particles->opacity_logit; q.sh = particles->sh; q.beta = particles->beta;
     q.P = (int)particles->P; q.sh_degree = particles->sh_degree;
     q.rho = settings->rho; q.phi_mode = settings->phi_mode; q.gaussian_only = settings->gaussian_only ? 1 : 0;
+    q.kernel = frame->kernel;
     q.cam = cam_params(camera);
     q.status = frame->status; q.flags = frame->flags; q.grad2d = frame->grad2d; q.drgb_ddir = frame->drgb_ddir;
     q.g_mean = grads->mean; q.g_log_scale = grads->log_scale; q.g_quat = grads->quat;

@@ -14,11 +14,13 @@ struct PreprocessArgs {
     int P, sh_degree;
     float rho;
     int phi_mode, gaussian_only;
+    int kernel;                       // ges_kernel: 1 = exact GEF of Eq. 2 (no phi-bar, exact rect)
     CamParams cam;
     float* depth;
     float4* pay0;
     float4* pay1;
     float* pay2;
+    float* pay3;                      // [P] beta / 2 (exact kernel)
     int32_t* radius;
     ushort4* rect;
     uint8_t* status;
@@ -84,6 +86,8 @@ struct RenderFwdArgs {
     const float4* pay0;
     const float4* pay1;
     const float* pay2;
+    const float* pay3;                // beta / 2 (exact kernel)
+    int exact;                        // 1: exact GEF kernel of Eq. 2
     const uint32_t* list;
     const uint32_t* ranges;
     const unsigned long long* counters;
@@ -102,6 +106,8 @@ struct RenderBwdArgs {
     const float4* pay0;
     const float4* pay1;
     const float* pay2;
+    const float* pay3;                // beta / 2 (exact kernel)
+    int exact;                        // 1: exact GEF kernel of Eq. 2
     const uint32_t* list;
     const uint32_t* ranges;
     const unsigned long long* counters;
@@ -111,7 +117,8 @@ struct RenderBwdArgs {
     const float* final_T;
     const uint32_t* n_contrib;
     const float* dL_dimage;
-    float* grad2d;  // [P][12]: du, dv, dA, dB | dC (pre-scaled conic), dkappa, dr, dg | db, 0, 0, 0
+    float* grad2d;  // [P][12]: du, dv, dA, dB | dC (pre-scaled conic), dkappa, dr, dg | db, dbeta*, 0, 0
+                    // (* exact kernel: Eq. 2's direct dL/dbeta)
     int P;
 };
 cudaError_t launch_render_bwd(const RenderBwdArgs& a, cudaStream_t stream);
@@ -121,6 +128,7 @@ struct ParticleBwdArgs {
     int P, sh_degree;
     float rho;
     int phi_mode, gaussian_only;
+    int kernel;                       // 1: exact GEF (no phi-bar; record[9] = direct dL/dbeta)
     CamParams cam;
     const uint8_t* status;
     const uint8_t* flags;

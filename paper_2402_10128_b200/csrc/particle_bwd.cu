@@ -85,7 +85,7 @@ __device__ __forceinline__ void particle_bwd_one(const ParticleBwdArgs& a, int i
                             2.f * (x * y + w * z), 1.f - 2.f * (x * x + z * z), 2.f * (y * z - w * x),
                             2.f * (x * z - w * y), 2.f * (y * z + w * x), 1.f - 2.f * (x * x + y * y)};
         float phi = 1.f, mfac = 1.f, dm_dbeta = 0.f;
-        if (!a.gaussian_only) {
+        if (!a.gaussian_only && a.kernel == GES_KERNEL_PHI_GAUSS) {
             phi = 2.f / (1.f + expf(-(a.rho * (in.beta - 2.f))));
             const float dphi = a.rho * phi * (1.f - 0.5f * phi);
             if (a.phi_mode == GES_PHI_VARIANCE) { mfac = sqrtf(phi); dm_dbeta = 0.5f * dphi / mfac; }
@@ -178,7 +178,8 @@ __device__ __forceinline__ void particle_bwd_one(const ParticleBwdArgs& a, int i
             o_ls[k] = dse[k] * se[k];
             dbeta += dse[k] * s[k] * dm_dbeta;
         }
-        o_beta = dbeta;
+        // exact GEF kernel: beta enters through Eq. 2's exponent only (record[9])
+        o_beta = a.kernel == GES_KERNEL_EXACT_BETA ? r2.y : dbeta;
         float dq[4];
         dq[0] = dR[1] * (-2.f * z) + dR[2] * (2.f * y) + dR[3] * (2.f * z) + dR[5] * (-2.f * x) + dR[6] * (-2.f * y) + dR[7] * (2.f * x);
         dq[1] = dR[1] * (2.f * y) + dR[2] * (2.f * z) + dR[3] * (2.f * y) + dR[4] * (-4.f * x) + dR[5] * (-2.f * w) +

@@ -20,6 +20,7 @@ namespace ges {
 
 struct PreOut {
     float depth, u, v, ca, cb, cc, kappa, r, g, b;
+    float hb;    // beta / 2 (exact kernel payload)
     float J[9];  // d rgb / d unit direction, 0 unless visible and unclamped
     int radius, x0, y0, x1, y1;
     uint8_t status, flags;
@@ -50,7 +51,7 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
     const int P = a.P;
     const CamParams& c = a.cam;
     PreOut o;
-    o.u = o.v = o.ca = o.cb = o.cc = o.kappa = o.r = o.g = o.b = 0.0f;
+    o.u = o.v = o.ca = o.cb = o.cc = o.kappa = o.r = o.g = o.b = o.hb = 0.0f;
     o.radius = o.x0 = o.y0 = o.x1 = o.y1 = 0;
 #pragma unroll
     for (int k = 0; k < 9; ++k) o.J[k] = 0.0f;
@@ -83,9 +84,12 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
     r[2][1] = fmul(2.0f, fadd(yz, wx));
     r[2][2] = fsub(1.0f, fmul(2.0f, fadd(xx, yy)));
 
-    // phi-bar (Eq. 6) -> effective scale (R1)
+    // exact GEF kernel (Eq. 2) needs beta > 0
+    if (a.kernel == GES_KERNEL_EXACT_BETA && !(in.beta > 0.0f)) { o.status = GES_DEGENERATE; return o; }
+    o.hb = fmul(0.5f, in.beta);
+    // phi-bar (Eq. 6) -> effective scale (R1); none in the exact kernel
     float mfac = 1.0f;
-    if (!a.gaussian_only) {
+    if (!a.gaussian_only && a.kernel == GES_KERNEL_PHI_GAUSS) {
         const float d = fsub(in.beta, 2.0f);
         const float ar = fmul(a.rho, d);
         const float e = exp_spec(-ar);
@@ -159,6 +163,11 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
     const float kr = fdiv(fmul(kap, 255.0f), 0.98f);
     float qthr = 0.0f;
     if (kr > 1.0f) { qthr = log_spec(kr); qthr = fadd(qthr, qthr); }
+    if (a.kernel == GES_KERNEL_EXACT_BETA && kr > 1.0f) {
+        // exact GEF: kappa exp(-1/2 Q^(beta/2)) >= 0.98/255 <=> Q <= exp((2/beta) ln(2 ln(255 kappa/0.98)))
+        const float hbi = fdiv(2.0f, in.beta);
+        qthr = exp_spec(fmul(hbi, log_spec(qthr)));
+    }
     const float ex = fsqrt(fmul(qthr, A)), ey = fsqrt(fmul(qthr, C));
     const float fx0 = ceilf(fmul(fsub(fsub(u, ex), 15.5f), 0.0625f));
     const float fx1 = fadd(floorf(fmul(fsub(fadd(u, ex), 0.5f), 0.0625f)), 1.0f);
@@ -225,6 +234,7 @@ __device__ __forceinline__ bool store_out(const PreprocessArgs& a, int i, const 
     a.pay0[i] = make_float4(o.u, o.v, o.ca, o.cb);
     a.pay1[i] = make_float4(o.cc, o.kappa, o.r, o.g);
     a.pay2[i] = o.b;
+    if (a.kernel == GES_KERNEL_EXACT_BETA) a.pay3[i] = o.hb;
     a.radius[i] = o.radius;
     a.rect[i] = make_ushort4((uint16_t)o.x0, (uint16_t)o.y0, (uint16_t)o.x1, (uint16_t)o.y1);
     a.status[i] = o.status;

@@ -111,12 +111,19 @@ struct Layout {
 };
 
 // Bit w set if some pixel of warp region w may get alpha >= 1/255 from s.
-template <int PPT>
-__device__ __forceinline__ uint32_t region_mask(const Splat& s, int tile_x0, int tile_y0) {
+// The bound on -p2 (log2 units): Gaussian kernel log2(255 kappa); exact GEF
+// kernel (hb = beta/2) 1/2 log2e Qc with Qc = (2 ln(255 kappa))^(1/hb), here
+// from fast intrinsics with a 2 % relative margin on top of the additive one.
+template <int PPT, bool EXACT>
+__device__ __forceinline__ uint32_t region_mask(const Splat& s, float hb, int tile_x0, int tile_y0) {
     using Lt = Layout<PPT>;
     const float k255 = s.kappa * 255.0f;
     if (!(k255 > 1.0f)) return 0u;
-    const float thr = __log2f(k255) + kCullMargin;  // cull if min(-p2) > thr
+    float thr = __log2f(k255) + kCullMargin;  // cull if min(-p2) > thr
+    if (EXACT) {
+        const float lq = __log2f(2.0f * __logf(k255)) * __fdividef(1.0f, hb);  // log2 Qc
+        thr = 0.5f * kLog2e * exp2f(lq) * 1.02f + kCullMargin;
+    }
     const float a = -s.A, b = -s.B, c = -s.C;
     const float ia2 = 0.5f / a, ic2 = 0.5f / c;
     uint32_t mask = 0;
@@ -128,6 +135,29 @@ __device__ __forceinline__ uint32_t region_mask(const Splat& s, int tile_x0, int
         if (box_min_quadratic(a, b, c, ia2, ic2, x0, x1, y0, y1) <= thr) mask |= 1u << w;
     }
     return mask;
+}
+
+// The exact GEF kernel (Eq. 2) from the log2-scaled Gaussian exponent p2 =
+// -1/2 log2e Q:  Q = 2 ln2 qp (qp = -p2), log2 Q = log2 qp + kC0,
+// Q^hb = 2^(hb log2 Q), G = exp(-1/2 Q^hb) = 2^(kC1 Q^hb).  qp is floored at
+// 1e-30 so that log2 and Q^(hb-1) stay finite at a pixel on the mean.
+constexpr float kGefC0 = 0.47123362f;    // log2(2 ln 2)
+constexpr float kGefC1 = -0.72134752f;   // -1/2 log2 e
+__device__ __forceinline__ float fast_log2(float x) {
+    float y;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+struct Gef {
+    float G, Qb, L, qp;  // G, Q^hb, log2 Q, -p2
+};
+__device__ __forceinline__ Gef gef_eval(float p2, float hb) {
+    Gef r;
+    r.qp = fmaxf(-p2, 1e-30f);
+    r.L = fast_log2(r.qp) + kGefC0;
+    r.Qb = fast_exp2(hb * r.L);
+    r.G = fast_exp2(kGefC1 * r.Qb);
+    return r;
 }
 
 // Per-warp compaction of the batch entries whose mask has this warp's bit.
@@ -165,12 +195,13 @@ struct StagedBatch {
     float* b;
     uint32_t* pid;
     uint8_t* mask;
+    float* hb;   // beta / 2 (exact kernel)
 };
 
-template <int PPT>
+template <int PPT, bool EXACT>
 __device__ __forceinline__ void stage_batch(const float4* pay0, const float4* pay1, const float* pay2,
-                                            const uint32_t* list, uint32_t first, int n, int tile_x0, int tile_y0,
-                                            StagedBatch sb) {
+                                            const float* pay3, const uint32_t* list, uint32_t first, int n,
+                                            int tile_x0, int tile_y0, StagedBatch sb) {
     using Lt = Layout<PPT>;
 #pragma unroll
     for (int h = 0; h < Lt::kLoads; ++h) {
@@ -182,17 +213,20 @@ __device__ __forceinline__ void stage_batch(const float4* pay0, const float4* pa
             sb.g1[q] = make_float4(s.C, s.kappa, s.r, s.g);
             sb.b[q] = s.b;
             if (sb.pid) sb.pid[q] = p;
-            sb.mask[q] = (uint8_t)region_mask<PPT>(s, tile_x0, tile_y0);
+            const float hb = EXACT ? __ldg(pay3 + p) : 1.0f;
+            if (EXACT) sb.hb[q] = hb;
+            sb.mask[q] = (uint8_t)region_mask<PPT, EXACT>(s, hb, tile_x0, tile_y0);
         }
     }
 }
 
-template <int PPT, bool DIAG>
+template <int PPT, bool DIAG, bool EXACT>
 __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdArgs a) {
     using Lt = Layout<PPT>;
     __shared__ float4 s_g0[kBatch];
     __shared__ float4 s_g1[kBatch];
     __shared__ float s_b[kBatch];
+    __shared__ float s_hb[EXACT ? kBatch : 1];
     __shared__ uint8_t s_mask[kBatch];
     __shared__ uint16_t s_list[Lt::kWarps][kBatch];
     const int tile = blockIdx.x;
@@ -216,11 +250,11 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
         if (!(px < a.W && py0 + 4 * k < a.H)) { done |= 1u << k; thr[k] = 2.0f; }
     }
     constexpr uint32_t kAll = (1u << PPT) - 1u;
-    StagedBatch sb{s_g0, s_g1, s_b, nullptr, s_mask};
+    StagedBatch sb{s_g0, s_g1, s_b, nullptr, s_mask, s_hb};
     for (uint32_t b0 = start; b0 < end; b0 += kBatch) {
         if (__syncthreads_count(done == kAll) == Lt::kThreads) break;
         const int n = (int)min((uint32_t)kBatch, end - b0);
-        stage_batch<PPT>(a.pay0, a.pay1, a.pay2, a.list, b0, n, tile_x0, tile_y0, sb);
+        stage_batch<PPT, EXACT>(a.pay0, a.pay1, a.pay2, a.pay3, a.list, b0, n, tile_x0, tile_y0, sb);
         __syncthreads();
         const int nw = compact_warp_list(s_mask, n, warp, s_list[warp]);
         for (int i = 0; i < nw; ++i) {
@@ -229,9 +263,16 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
             const float4 g0 = s_g0[j];
             const float4 g1 = s_g1[j];
             const float gbl = s_b[j];
+            const float hb = EXACT ? s_hb[j] : 1.0f;
             const float dx = __fsub_rn(g0.x, fpx);
             const ExpCol ec = exp_col(g0.z, g0.w, dx);
             const uint32_t pos1 = b0 - start + j + 1;
+            // per-pixel kernel value: Gaussian 2^p2, or Eq. 2's exp(-1/2 Q^(beta/2))
+            auto kern = [&](float dy) {
+                const float p2 = raw_exponent(ec, g1.x, dy);
+                if constexpr (EXACT) return gef_eval(p2, hb).G;
+                else return fast_exp2(p2);
+            };
             const bool clampk = g1.y > kAlphaMax;  // warp-uniform: only then can alpha reach 0.99
             // alpha' = alpha if alpha >= thr (the skip test; thr = 2 for stopped pixels), else 0;
             // the would-be transmittance T (1 - alpha') decides the stop.  (The exponent is not
@@ -241,7 +282,7 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
 #pragma unroll
             for (int k = 0; k < PPT; ++k) {
                 const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
-                float alpha = __fmul_rn(g1.y, fast_exp2(raw_exponent(ec, g1.x, dy)));
+                float alpha = __fmul_rn(g1.y, kern(dy));
                 if (clampk) alpha = fminf(kAlphaMax, alpha);
                 al[k] = alpha >= thr[k] ? alpha : 0.0f;
                 w[k] = __fmul_rn(al[k], T[k]);
@@ -295,26 +336,29 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
     }
 }
 
-// Pixels per thread (tuning knob; GES_PPT_FWD / GES_PPT_BWD override for experiments).
+// Pixels per thread (tuning knob; GES_PPT_FWD / GES_PPT_BWD = 2 or 4 override for experiments).
 static int ppt_from_env(const char* name, int dflt) {
     const char* e = getenv(name);
     const int v = e ? atoi(e) : dflt;
-    return (v == 1 || v == 2 || v == 4) ? v : dflt;
+    return (v == 2 || v == 4) ? v : dflt;
+}
+
+template <int PPT, bool EXACT>
+static void launch_fwd_ppt(const RenderFwdArgs& a, int grid, bool diag, cudaStream_t stream) {
+    if (diag) render_fwd_kernel<PPT, true, EXACT><<<grid, Layout<PPT>::kThreads, 0, stream>>>(a);
+    else render_fwd_kernel<PPT, false, EXACT><<<grid, Layout<PPT>::kThreads, 0, stream>>>(a);
 }
 
 cudaError_t launch_render_fwd(const RenderFwdArgs& a, cudaStream_t stream) {
     static const int ppt = ppt_from_env("GES_PPT_FWD", 2);
     const int grid = a.tiles_x * a.tiles_y;
     const bool diag = a.n_eval || a.n_comp;  // the counters cost issue slots: only when asked
-    if (ppt == 1) {
-        if (diag) render_fwd_kernel<1, true><<<grid, Layout<1>::kThreads, 0, stream>>>(a);
-        else render_fwd_kernel<1, false><<<grid, Layout<1>::kThreads, 0, stream>>>(a);
-    } else if (ppt == 4) {
-        if (diag) render_fwd_kernel<4, true><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
-        else render_fwd_kernel<4, false><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
+    if (a.exact) {
+        if (ppt == 4) launch_fwd_ppt<4, true>(a, grid, diag, stream);
+        else launch_fwd_ppt<2, true>(a, grid, diag, stream);
     } else {
-        if (diag) render_fwd_kernel<2, true><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
-        else render_fwd_kernel<2, false><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
+        if (ppt == 4) launch_fwd_ppt<4, false>(a, grid, diag, stream);
+        else launch_fwd_ppt<2, false>(a, grid, diag, stream);
     }
     return cudaGetLastError();
 }
@@ -322,26 +366,30 @@ cudaError_t launch_render_fwd(const RenderFwdArgs& a, cudaStream_t stream) {
 // ---------------------------------------------------------------------------
 // S5a backward
 // ---------------------------------------------------------------------------
-// Warp sum of the nine per-pair gradient components by recursive halving over
-// uneven component sets: xor 16 splits {0-4 | 5-8} (5 SHFL), xor 8 splits the
-// remaining slots {0-2 | 3-4} (3), xor 4 {0-1 | 2} (2), xor 2 (1), xor 1 (1):
-// 12 shuffles.  Afterwards lanes l and l^1 hold the full sum of component
-// reduce9_component(l) (or -1: no component).
-__device__ __forceinline__ int reduce9_component(int lane) {
+// Warp sum of the NV (9, or 10 with the exact kernel's dbeta) per-pair
+// gradient components by recursive halving over uneven component sets: xor 16
+// splits {0-4 | 5-(NV-1)} (5 SHFL), xor 8 splits the remaining slots {0-2 |
+// 3-4} (3), xor 4 {0-1 | 2} (2), xor 2 (1), xor 1 (1): 12 shuffles.
+// Afterwards lanes l and l^1 hold the full sum of component
+// reduce_component<NV>(l) (or -1: no component).
+template <int NV>
+__device__ __forceinline__ int reduce_component(int lane) {
     const int i2 = ((lane & 4) ? 2 : 0) + ((lane & 2) ? 1 : 0);
     const int i1 = ((lane & 8) ? 3 : 0) + i2;
     const bool hi = (lane & 16) != 0;
-    if (i2 > 2 || i1 > (hi ? 3 : 4)) return -1;
+    if (i2 > 2 || i1 > (hi ? NV - 6 : 4)) return -1;
     return (hi ? 5 : 0) + i1;
 }
 
-__device__ __forceinline__ float warp_reduce9(const float v[9]) {
+template <int NV>
+__device__ __forceinline__ float warp_reduce(const float (&v)[NV]) {
+    static_assert(NV == 9 || NV == 10, "9 or 10 components");
     const int lane = threadIdx.x & 31;
     const bool u16 = (lane & 16) != 0, u8 = (lane & 8) != 0, u4 = (lane & 4) != 0, u2 = (lane & 2) != 0;
     float w[6];
 #pragma unroll
     for (int i = 0; i < 5; ++i) {
-        const float lo = v[i], hi = (i < 4) ? v[5 + i] : 0.0f;
+        const float lo = v[i], hi = (5 + i < NV) ? v[5 + i] : 0.0f;
         w[i] = (u16 ? hi : lo) + __shfl_xor_sync(0xffffffffu, u16 ? lo : hi, 16);
     }
     w[5] = 0.0f;
@@ -367,12 +415,14 @@ __device__ __forceinline__ void red_add(float* addr, float x) {
     asm volatile("red.global.add.f32 [%0], %1;" ::"l"(addr), "f"(x) : "memory");
 }
 
-template <int PPT>
+template <int PPT, bool EXACT>
 __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdArgs a) {
     using Lt = Layout<PPT>;
+    constexpr int NV = EXACT ? 10 : 9;  // + Eq. 2's direct dL/dbeta
     __shared__ float4 s_g0[kBatch];
     __shared__ float4 s_g1[kBatch];
     __shared__ float s_b[kBatch];
+    __shared__ float s_hb[EXACT ? kBatch : 1];
     __shared__ uint32_t s_pid[kBatch];
     __shared__ uint8_t s_mask[kBatch];
     __shared__ uint16_t s_list[Lt::kWarps][kBatch];
@@ -418,13 +468,13 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
     // the largest `last` among the warp's inactive pixels: the walk (positions
     // descending) activates them when it passes below it
     uint32_t nxt = warp_max;
-    const int red_comp = reduce9_component(lane);
-    StagedBatch sb{s_g0, s_g1, s_b, s_pid, s_mask};
+    const int red_comp = reduce_component<NV>(lane);
+    StagedBatch sb{s_g0, s_g1, s_b, s_pid, s_mask, s_hb};
     for (int32_t b_end = (int32_t)max_last; b_end > 0; b_end -= kBatch) {
         const int32_t b_begin = max(0, b_end - kBatch);
         const int n = b_end - b_begin;
         __syncthreads();  // previous batch fully consumed
-        stage_batch<PPT>(a.pay0, a.pay1, a.pay2, a.list, start + b_begin, n, tile_x0, tile_y0, sb);
+        stage_batch<PPT, EXACT>(a.pay0, a.pay1, a.pay2, a.pay3, a.list, start + b_begin, n, tile_x0, tile_y0, sb);
         __syncthreads();
         // this warp's pixels composite nothing at or behind list position warp_max
         const int nw_lim = (int)min((int64_t)n, max((int64_t)0, (int64_t)warp_max - b_begin));
@@ -453,8 +503,60 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             // S2 = sum q dy^2 suffice.  alpha' = alpha where the pixel composites
             // this entry (alpha >= thr: active and not skipped), else 0; then every
             // term below vanishes without a select.  (No exponent clamp: R19.)
-            float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, dr = 0.0f, dgc = 0.0f, dbc = 0.0f;
+            float v[NV];
             bool contrib = false;
+            if constexpr (EXACT) {
+            float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, dk = 0.0f, Sb = 0.0f, dr = 0.0f, dgc = 0.0f, dbc = 0.0f;
+            const float hb = s_hb[j];
+            const bool clampk = g1.y > kAlphaMax;  // warp-uniform
+            const float rk = fast_rcp(g1.y);
+            // Eq. 2: G = exp(-1/2 Q^hb).  dG/dp2 = G hb Q^hb / (2 qp) (Q = 2 ln2 qp),
+            // dG/dbeta = -1/4 G Q^hb ln Q; with Gd = G dL/dalpha where composited:
+            // dL/dkappa += Gd, the moments take wm = Gd Q^hb / qp (factor kappa hb / 2),
+            // Sb = sum Gd Q^hb log2 Q (factor -1/4 kappa ln2).
+#pragma unroll
+            for (int k = 0; k < PPT; ++k) {
+                const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
+                const Gef ge = gef_eval(raw_exponent(ec, g1.x, dy), hb);
+                const float araw = __fmul_rn(g1.y, ge.G);
+                const float alpha = clampk ? fminf(kAlphaMax, araw) : araw;
+                const float al = alpha >= thr[k] ? alpha : 0.0f;
+                contrib |= al > 0.0f;
+                const float inv_om = fast_rcp(__fsub_rn(1.0f, al));
+                const float Tk = T[k] * inv_om;
+                const float cgk = g1.z * gr[k] + g1.w * gg[k] + rb * gb[k];
+                const float w = al * Tk;
+                const float dalpha = Tk * cgk - U[k] * inv_om;
+                U[k] += cgk * w;
+                dr += w * gr[k];
+                dgc += w * gg[k];
+                dbc += w * gb[k];
+                float Gd = (al * rk) * dalpha;  // G dL/dalpha where composited
+                if (clampk) Gd = (al > 0.0f && araw < kAlphaMax) ? ge.G * dalpha : 0.0f;
+                dk += Gd;
+                const float GQ = Gd * ge.Qb;
+                const float wm = GQ * fast_rcp(ge.qp);
+                S0 += wm;
+                const float t = wm * dy;
+                S1 += t;
+                S2 += t * dy;
+                Sb += GQ * ge.L;
+                T[k] = Tk;
+            }
+            const float kl = g1.y * 0.5f * hb;  // dL/dp2 = kl wm
+            const float E = kl * dx * S0, F = kl * S1;
+            v[0] = 2.0f * g0.z * E + g0.w * F;
+            v[1] = g0.w * E + 2.0f * g1.x * F;
+            v[2] = dx * E;
+            v[3] = dx * F;
+            v[4] = kl * S2;
+            v[5] = dk;
+            v[6] = dr;
+            v[7] = dgc;
+            v[8] = dbc;
+            v[NV - 1] = -0.25f * 0.69314718055994531f * g1.y * Sb;  // (NV = 10) d L / d beta
+            } else {
+            float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, dr = 0.0f, dgc = 0.0f, dbc = 0.0f;
             if (!(g1.y > kAlphaMax)) {  // warp-uniform: alpha cannot reach the 0.99 clamp
                 const float rk = fast_rcp(g1.y);
 #pragma unroll
@@ -509,7 +611,6 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             // alpha = kappa 2^p2: d alpha / d p2 = alpha ln 2, so dL/dp2 = kappa ln2 q
             const float kl = g1.y * 0.69314718055994531f;
             const float E = kl * dx * S0, F = kl * S1;  // sum dp2 dx, sum dp2 dy
-            float v[9];
             v[0] = 2.0f * g0.z * E + g0.w * F;   // d p2 / d u
             v[1] = g0.w * E + 2.0f * g1.x * F;   // d p2 / d v
             v[2] = dx * E;                       // d p2 / d A
@@ -519,8 +620,9 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             v[6] = dr;
             v[7] = dgc;
             v[8] = dbc;
+            }
             if (__any_sync(0xffffffffu, contrib)) {
-                const float r = warp_reduce9(v);
+                const float r = warp_reduce<NV>(v);
                 if (red_comp >= 0 && (lane & 1) == 0)
                     red_add(a.grad2d + (size_t)s_pid[j] * kGrad2dStride + red_comp, r);
             }
@@ -531,9 +633,13 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
 cudaError_t launch_render_bwd(const RenderBwdArgs& a, cudaStream_t stream) {
     static const int ppt = ppt_from_env("GES_PPT_BWD", 4);
     const int grid = a.tiles_x * a.tiles_y;
-    if (ppt == 1) render_bwd_kernel<1><<<grid, Layout<1>::kThreads, 0, stream>>>(a);
-    else if (ppt == 4) render_bwd_kernel<4><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
-    else render_bwd_kernel<2><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
+    if (a.exact) {
+        if (ppt == 4) render_bwd_kernel<4, true><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
+        else render_bwd_kernel<2, true><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
+    } else {
+        if (ppt == 4) render_bwd_kernel<4, false><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
+        else render_bwd_kernel<2, false><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
+    }
     return cudaGetLastError();
 }
 

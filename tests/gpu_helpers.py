@@ -7,9 +7,10 @@ import paper_2402_10128_b200 as G
 from oracle import oracle as O
 
 
-def settings_pair(rho=0.1, phi_mode=0, gaussian_only=0, background=(0.0, 0.0, 0.0)):
-    return (G.Settings(rho=rho, phi_mode=phi_mode, gaussian_only=gaussian_only, background=background),
-            O.Settings(rho=rho, phi_mode=phi_mode, gaussian_only=gaussian_only, background=background))
+def settings_pair(rho=0.1, phi_mode=0, gaussian_only=0, background=(0.0, 0.0, 0.0), kernel=0):
+    return (G.Settings(rho=rho, phi_mode=phi_mode, gaussian_only=gaussian_only, background=background, kernel=kernel),
+            O.Settings(rho=rho, phi_mode=phi_mode, gaussian_only=gaussian_only, background=background,
+                       kernel=kernel))
 
 
 def gpu_forward(parts, cam, gs, pair_capacity=None, n_eval=True):

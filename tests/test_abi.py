@@ -64,7 +64,7 @@ def test_workspace_and_frame_carving_host_only():
     assert (f.tiles_x, f.tiles_y, f.num_tiles) == (7, 5, 35)
     assert f.tile_bits == 6
     assert f.workspace_bytes == nbytes
-    ptrs = [f.depth, f.pay0, f.pay1, f.pay2, f.radius, f.rect, f.status, f.flags, f.drgb_ddir, f.vis_key[0], f.vis_key[1],
+    ptrs = [f.depth, f.pay0, f.pay1, f.pay2, f.pay3, f.radius, f.rect, f.status, f.flags, f.drgb_ddir, f.vis_key[0], f.vis_key[1],
             f.vis_val[0], f.vis_val[1], f.radix_hist, f.radix_total, f.item_offset, f.item_rec, f.chunk_first,
             f.bin_table, f.list, f.ranges, f.lookback, f.counters,
             f.final_T, f.n_contrib, f.grad2d]
