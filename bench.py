@@ -310,6 +310,12 @@ def run_ours(args) -> None:
     cam0 = scene.cameras[0]
     band_ms, band_pairs = time_band_forward(G, params, cam0, st, dev, flush, stream, args.steps, rank, world)
 
+    # ---- the exact GEF kernel of Eq. 2 on the same workload ----
+    G.ges_preprocess(params, cam, st, frame, stream)
+    G.ges_sort(frame, stream)
+    G.ges_render_fwd(frame, st, image, None, stream)   # the phi-bar Gaussian image, for comparison
+    exact = time_exact_kernel(G, params, cam, scene, dL, image, flush, stream, args.steps, dev)
+
     # ---- algorithmic work for the roofline ----
     n_comp = torch.zeros(W * H, dtype=torch.int32, device=dev)
     G.ges_preprocess(params, cam, st, frame, stream)
@@ -357,6 +363,7 @@ def run_ours(args) -> None:
                           "pairs_rank0": band_pairs,
                           "note": f"one config-3 frame split into {world} interleaved tile-row bands, S1-S4 per "
                                   f"rank + all_gather of the band pixels; device time, max over ranks"},
+            "exact_beta_kernel": exact,
             "vs_gaussian_equivalent": {"ges_fwd_ms": fwd_ms, "gaussian_fwd_ms": g_ms, "ratio": g_ms / fwd_ms,
                                        "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
             "stages_ms": {n: float(stage_ms[i]) for i, n in enumerate(stage_names)},
@@ -477,6 +484,56 @@ def time_band_forward(G, params, cam, st, dev, flush, stream, steps, rank, world
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item()), int(frame.counts().pairs)
+
+
+def time_exact_kernel(G, params, cam, scene, dL, image_phi, flush, stream, steps, dev):
+    """Forward and fwd+bwd step with the exact GEF kernel (ges_settings.kernel = 1) on the
+    bench workload, timed like the main step; plus how far its image lies from the
+    phi-bar Gaussian rasterization's (the approximation the paper makes)."""
+    import torch
+    W, H, P = cam.width, cam.height, params.P
+    st = G.Settings(rho=scene.rho, kernel=1)
+    r = G.Renderer(P, W, H, device=dev)
+    img = torch.empty((3, H, W), dtype=torch.float32, device=dev)
+    r.forward(params, cam, st, img)
+    r.grow(int(r.frame.counts().slots))
+    frame = r.frame
+    grads = G.PlanarParams.zeros(P, params.sh_degree, dev)
+
+    def fwd():
+        G.ges_preprocess(params, cam, st, frame, stream)
+        G.ges_sort(frame, stream)
+        G.ges_render_fwd(frame, st, img, None, stream)
+
+    def step():
+        fwd()
+        G.ges_render_bwd(params, cam, st, frame, dL, grads, False, stream)
+
+    out = {}
+    for name, fn in (("fwd", fwd), ("fwd_bwd", step)):
+        for _ in range(3):
+            fn()
+        ms = []
+        for _ in range(steps):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+        out[name + "_ms"] = float(statistics.mean(ms))
+    fwd()
+    torch.cuda.synchronize()
+    cnt = frame.counts()
+    d = (img - image_phi).abs()
+    return {"fwd": {"value": W * H / (out["fwd_ms"] / 1e3) / 1e6, "unit": "Mpixel-frames/s", "ms": out["fwd_ms"]},
+            "fwd_bwd": {"value": W * H / (out["fwd_bwd_ms"] / 1e3) / 1e6, "unit": "Mpixel-frames/s (fwd+bwd)",
+                        "ms": out["fwd_bwd_ms"]},
+            "pairs": int(cnt.pairs), "visible": int(cnt.visible),
+            "image_vs_phi_bar_gaussian": {"max_abs": float(d.max().item()), "mean_abs": float(d.mean().item())},
+            "note": "Eq. 2 per pixel (no phi-bar); footprints follow Q <= (2 ln(255 kappa))^(2/beta), "
+                    "so beta < 2 particles cover far more tiles"}
 
 
 def gaussian_equivalent(G, scene, cam, dev):
