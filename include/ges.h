@@ -255,6 +255,48 @@ const char *ges_status_string(ges_status s);
 /* Library version / build id (static string). */
 const char *ges_version(void);
 
+/* ------------------------------------------------------------------------
+ * Image-loss front end: Eq. 9
+ *   L = l_L1 L1 + l_ssim (1 - SSIM) + l_w L_omega,  l_L1 = 1 - l_ssim - l_w,
+ * with L_omega = ||(I - I_gt) . M_omega||_1 (Eq. 8) and the
+ * frequency mask M_omega of Eq. 7 (complement for omega <= 0.5
+ * :327, computed on a downsampled ground truth :1226).  Readings (DESIGN.md
+ * R22-R28): every term a mean over pixels and channels; SSIM with an 11 x 11
+ * Gaussian window (sigma 1.5), C1 = 0.01^2, C2 = 0.03^2, zero padding; the mask
+ * from the luminance 0.299 R + 0.587 G + 0.114 B, bilinear downsample to
+ * max(1, floor(n s + 1/2)) per axis, DoG = G(., 0.2 + 20 w) - G(., 0.1 + 10 w)
+ * (separable, radius ceil(3 sigma), reflect padding), |DoG| min-max normalised
+ * (a constant response gives 0), > eps_omega; nearest upsample (full-res pixel
+ * (i, j) reads mask_lo[floor(i Hd / H), floor(j Wd / W)]).
+ * Images are [3][H][W] fp32 device arrays; the caller owns every buffer and a
+ * device workspace of ges_loss_workspace_bytes(); stream-ordered, no sync.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+    float lambda_ssim;   /* 0.2 */
+    float lambda_omega;  /* 0.5        */
+    float eps_omega;     /* 0.5         */
+    float downsample;    /* 0.2        */
+} ges_loss_settings;
+
+/* Downsampled mask grid of a W x H image: Wd = max(1, floor(W s + 1/2)), same for H. */
+ges_status ges_loss_mask_dims(int32_t width, int32_t height, float downsample, int32_t *Wd, int32_t *Hd);
+
+/* Device workspace bytes for ges_loss_mask and ges_loss on a W x H image. */
+size_t ges_loss_workspace_bytes(int32_t width, int32_t height, float downsample);
+
+/* M_omega of `gt` for normalised frequency omega in [0, 1] (the schedule
+ * omega = iteration / iterations) into mask_lo [Hd][Wd] (u8 0/1).
+ * Errors: null pointers, W/H < 1, omega outside [0, 1], workspace too small. */
+ges_status ges_loss_mask(const float *gt, int32_t width, int32_t height, float omega, const ges_loss_settings *settings,
+                         void *workspace, size_t workspace_bytes, uint8_t *mask_lo, void *stream);
+
+/* Eq. 9 on (image, gt): dL_dimage [3][H][W] (overwritten) and loss_out[4] =
+ * (L, L1, SSIM, L_omega) on the device.  mask_lo = NULL drops the L_omega
+ * term (its weight still enters l_L1).  Errors as ges_loss_mask. */
+ges_status ges_loss(const float *image, const float *gt, const uint8_t *mask_lo, int32_t width, int32_t height,
+                    const ges_loss_settings *settings, void *workspace, size_t workspace_bytes, float *dL_dimage,
+                    float *loss_out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

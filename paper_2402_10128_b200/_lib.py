@@ -72,9 +72,15 @@ class ges_frame(C.Structure):
     ]
 
 
+class ges_loss_settings(C.Structure):
+    _fields_ = [("lambda_ssim", C.c_float), ("lambda_omega", C.c_float), ("eps_omega", C.c_float),
+                ("downsample", C.c_float)]
+
+
 EXPORTS = ["ges_workspace_bytes", "ges_frame_init", "ges_preprocess", "ges_sort", "ges_render_fwd",
            "ges_render_bwd", "ges_render_bwd_tiles", "ges_backward_particles", "ges_counts_get",
-           "ges_status_string", "ges_version"]
+           "ges_status_string", "ges_version", "ges_loss_mask_dims", "ges_loss_workspace_bytes", "ges_loss_mask",
+           "ges_loss"]
 
 _lib = None
 
@@ -118,6 +124,18 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         L.ges_status_string.restype = C.c_char_p
         L.ges_status_string.argtypes = [C.c_int]
         L.ges_version.restype = C.c_char_p
+        L.ges_loss_mask_dims.restype = C.c_int
+        L.ges_loss_mask_dims.argtypes = [C.c_int32, C.c_int32, C.c_float, C.POINTER(C.c_int32),
+                                         C.POINTER(C.c_int32)]
+        L.ges_loss_workspace_bytes.restype = C.c_size_t
+        L.ges_loss_workspace_bytes.argtypes = [C.c_int32, C.c_int32, C.c_float]
+        L.ges_loss_mask.restype = C.c_int
+        L.ges_loss_mask.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_float, C.POINTER(ges_loss_settings),
+                                    C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
+        L.ges_loss.restype = C.c_int
+        L.ges_loss.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                               C.POINTER(ges_loss_settings), C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
+                               C.c_void_p]
         _lib = L
     return _lib
 

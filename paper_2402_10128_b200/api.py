@@ -234,3 +234,63 @@ class Renderer:
             grads = PlanarParams.zeros(particles.P, particles.sh_degree, self.device)
         ges_render_bwd(particles, camera, settings, self.frame, dL_dimage, grads, accumulate, stream)
         return grads
+
+
+# --- loss front end (ges.h ges_loss*) -------------------
+@dataclasses.dataclass
+class LossSettings:
+    lambda_ssim: float = 0.2
+    lambda_omega: float = 0.5
+    eps_omega: float = 0.5
+    downsample: float = 0.2
+
+    def c(self) -> L.ges_loss_settings:
+        s = L.ges_loss_settings()
+        s.lambda_ssim, s.lambda_omega = float(self.lambda_ssim), float(self.lambda_omega)
+        s.eps_omega, s.downsample = float(self.eps_omega), float(self.downsample)
+        return s
+
+
+def ges_loss_mask_dims(width: int, height: int, downsample: float = 0.2):
+    wd, hd = C.c_int32(), C.c_int32()
+    L.check(L.load().ges_loss_mask_dims(width, height, downsample, C.byref(wd), C.byref(hd)), "ges_loss_mask_dims")
+    return int(wd.value), int(hd.value)
+
+
+class Loss:
+    """Owns the loss workspace for one image size (marshalling only: every step
+    runs in libges.so's loss kernels)."""
+
+    def __init__(self, width: int, height: int, settings: Optional[LossSettings] = None, device="cuda"):
+        self.W, self.H, self.settings = width, height, settings or LossSettings()
+        nbytes = L.load().ges_loss_workspace_bytes(width, height, self.settings.downsample)
+        if nbytes == 0:
+            raise L.GESError("ges_loss_workspace_bytes: invalid size")
+        self.ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        self.Wd, self.Hd = ges_loss_mask_dims(width, height, self.settings.downsample)
+        self.out = torch.zeros(4, dtype=torch.float32, device=device)
+
+    def mask(self, gt: torch.Tensor, omega: float, mask_lo: Optional[torch.Tensor] = None, stream=None):
+        assert gt.dtype == torch.float32 and gt.is_contiguous() and gt.numel() == 3 * self.W * self.H
+        if mask_lo is None:
+            mask_lo = torch.empty((self.Hd, self.Wd), dtype=torch.uint8, device=self.ws.device)
+        s = self.settings.c()
+        L.check(L.load().ges_loss_mask(C.c_void_p(gt.data_ptr()), self.W, self.H, float(omega), C.byref(s),
+                                       C.c_void_p(self.ws.data_ptr()), self.ws.numel(),
+                                       C.c_void_p(mask_lo.data_ptr()), C.c_void_p(_stream(stream))), "ges_loss_mask")
+        return mask_lo
+
+    def __call__(self, image: torch.Tensor, gt: torch.Tensor, mask_lo: Optional[torch.Tensor],
+                 dL_dimage: Optional[torch.Tensor] = None, stream=None):
+        """Returns (loss_out[4] = (L, L1, SSIM, L_omega) on the device, dL/dimage)."""
+        for t in (image, gt):
+            assert t.dtype == torch.float32 and t.is_contiguous() and t.numel() == 3 * self.W * self.H
+        if dL_dimage is None:
+            dL_dimage = torch.empty_like(image)
+        s = self.settings.c()
+        mp = C.c_void_p(mask_lo.data_ptr()) if mask_lo is not None else None
+        L.check(L.load().ges_loss(C.c_void_p(image.data_ptr()), C.c_void_p(gt.data_ptr()), mp, self.W, self.H,
+                                  C.byref(s), C.c_void_p(self.ws.data_ptr()), self.ws.numel(),
+                                  C.c_void_p(dL_dimage.data_ptr()), C.c_void_p(self.out.data_ptr()),
+                                  C.c_void_p(_stream(stream))), "ges_loss")
+        return self.out, dL_dimage

@@ -2,6 +2,7 @@
 // and the launch sequence of each stage.  Host code only; every kernel lives
 // in preprocess.cu / sort.cu / render.cu / particle_bwd.cu.
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "ges_internal.h"
@@ -308,5 +309,89 @@ const char* ges_status_string(ges_status st) {
 }
 
 const char* ges_version(void) { return "ges-b200 0.1 (sm_100a)"; }
+
+// ---------------------------------------------------------------------------
+// loss front end
+// ---------------------------------------------------------------------------
+namespace {
+int down_dim(int n, float s) { return std::max(1, (int)std::floor((double)n * (double)s + 0.5)); }
+
+struct LossLayout {
+    size_t d_mu, d_e2, d_exy, partial, lo, h1, h2, dog, minmax, total;
+};
+LossLayout loss_layout(int W, int H, float s) {
+    LossLayout L;
+    size_t off = 0;
+    auto take = [&](size_t bytes) { const size_t o = off; off = align_up(off + bytes); return o; };
+    const size_t n3 = (size_t)3 * W * H, nd = (size_t)down_dim(W, s) * down_dim(H, s);
+    L.d_mu = take(4 * n3); L.d_e2 = take(4 * n3); L.d_exy = take(4 * n3);
+    L.partial = take(4 * 3 * (size_t)loss_partials(W, H));
+    L.lo = take(4 * nd); L.h1 = take(4 * nd); L.h2 = take(4 * nd); L.dog = take(4 * nd);
+    L.minmax = take(8);
+    L.total = off;
+    return L;
+}
+bool loss_settings_ok(const ges_loss_settings* s) {
+    return s && s->lambda_ssim >= 0.0f && s->lambda_omega >= 0.0f && s->lambda_ssim + s->lambda_omega <= 1.0f &&
+           s->eps_omega >= 0.0f && s->eps_omega <= 1.0f && s->downsample > 0.0f && s->downsample <= 1.0f;
+}
+}  // namespace
+
+ges_status ges_loss_mask_dims(int32_t width, int32_t height, float downsample, int32_t* Wd, int32_t* Hd) {
+    if (width < 1 || height < 1 || !(downsample > 0.0f && downsample <= 1.0f) || !Wd || !Hd)
+        return GES_ERR_INVALID_ARG;
+    *Wd = down_dim(width, downsample);
+    *Hd = down_dim(height, downsample);
+    return GES_OK;
+}
+
+size_t ges_loss_workspace_bytes(int32_t width, int32_t height, float downsample) {
+    if (width < 1 || height < 1 || !(downsample > 0.0f && downsample <= 1.0f)) return 0;
+    return loss_layout(width, height, downsample).total;
+}
+
+ges_status ges_loss_mask(const float* gt, int32_t width, int32_t height, float omega, const ges_loss_settings* settings,
+                         void* workspace, size_t workspace_bytes, uint8_t* mask_lo, void* stream) {
+    if (!gt || !mask_lo || !workspace || width < 1 || height < 1 || !loss_settings_ok(settings) ||
+        !(omega >= 0.0f && omega <= 1.0f))
+        return GES_ERR_INVALID_ARG;
+    const LossLayout L = loss_layout(width, height, settings->downsample);
+    if (workspace_bytes < L.total) return GES_ERR_CAPACITY;
+    char* ws = (char*)workspace;
+    MaskArgs m;
+    m.gt = gt; m.W = width; m.H = height;
+    m.Wd = down_dim(width, settings->downsample); m.Hd = down_dim(height, settings->downsample);
+    const double w = (double)omega, s1 = 0.2 + 20.0 * w, s2 = 0.1 + 10.0 * w;  // Eq. 7 sigmas
+    m.r1 = (int)std::ceil(3.0 * s1); m.r2 = (int)std::ceil(3.0 * s2);
+    m.ih1 = (float)(1.0 / (2.0 * s1 * s1)); m.ih2 = (float)(1.0 / (2.0 * s2 * s2));
+    m.eps = settings->eps_omega;
+    m.complement = omega <= 0.5f;
+    m.lo = (float*)(ws + L.lo); m.h1 = (float*)(ws + L.h1); m.h2 = (float*)(ws + L.h2); m.dog = (float*)(ws + L.dog);
+    m.minmax = (unsigned*)(ws + L.minmax);
+    m.mask_lo = mask_lo;
+    return cuda_status(launch_mask(m, (cudaStream_t)stream));
+}
+
+ges_status ges_loss(const float* image, const float* gt, const uint8_t* mask_lo, int32_t width, int32_t height,
+                    const ges_loss_settings* settings, void* workspace, size_t workspace_bytes, float* dL_dimage,
+                    float* loss_out, void* stream) {
+    if (!image || !gt || !workspace || !dL_dimage || !loss_out || width < 1 || height < 1 ||
+        !loss_settings_ok(settings))
+        return GES_ERR_INVALID_ARG;
+    const LossLayout L = loss_layout(width, height, settings->downsample);
+    if (workspace_bytes < L.total) return GES_ERR_CAPACITY;
+    char* ws = (char*)workspace;
+    LossArgs a;
+    a.image = image; a.gt = gt; a.mask_lo = mask_lo;
+    a.W = width; a.H = height;
+    a.Wd = down_dim(width, settings->downsample); a.Hd = down_dim(height, settings->downsample);
+    a.lambda_ssim = settings->lambda_ssim; a.lambda_omega = settings->lambda_omega;
+    a.inv_n = (float)(1.0 / (3.0 * width * (double)height));
+    a.d_mu = (float*)(ws + L.d_mu); a.d_e2 = (float*)(ws + L.d_e2); a.d_exy = (float*)(ws + L.d_exy);
+    a.partial = (float*)(ws + L.partial);
+    a.nblocks = 0;
+    a.dL_dimage = dL_dimage; a.loss_out = loss_out;
+    return cuda_status(launch_loss(a, (cudaStream_t)stream));
+}
 
 }  // extern "C"

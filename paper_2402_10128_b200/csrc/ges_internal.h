@@ -139,4 +139,34 @@ struct ParticleBwdArgs {
 };
 cudaError_t launch_particle_bwd(const ParticleBwdArgs& a, cudaStream_t stream);
 
+// --- loss front end (loss.cu) ------------------------
+struct LossArgs {
+    const float* image;               // [3][H][W]
+    const float* gt;                  // [3][H][W]
+    const uint8_t* mask_lo;           // [Hd][Wd] M_omega on the downsampled grid (null: no L_omega term)
+    int W, H, Hd, Wd;
+    float lambda_ssim, lambda_omega;
+    float inv_n;                      // 1 / (3 H W)
+    float *d_mu, *d_e2, *d_exy;       // [3][H][W] SSIM partials (workspace)
+    float* partial;                   // [blocks][3] block sums (workspace)
+    int nblocks;
+    float* dL_dimage;                 // [3][H][W] out
+    float* loss_out;                  // [4] out: total, L1, SSIM, L_omega
+};
+cudaError_t launch_loss(const LossArgs& a, cudaStream_t stream);
+int64_t loss_partials(int W, int H);
+
+struct MaskArgs {
+    const float* gt;                  // [3][H][W]
+    int W, H, Hd, Wd;
+    int r1, r2;                       // blur radii ceil(3 sigma) of sigma1 = 0.2 + 20 w, sigma2 = 0.1 + 10 w
+    float ih1, ih2;                   // 1 / (2 sigma^2)
+    float eps;
+    int complement;                   // omega <= 0.5
+    float *lo, *h1, *h2, *dog;        // [Hd][Wd] workspace
+    unsigned* minmax;                 // [2] workspace
+    uint8_t* mask_lo;                 // [Hd][Wd] out
+};
+cudaError_t launch_mask(const MaskArgs& a, cudaStream_t stream);
+
 }  // namespace ges
