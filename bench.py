@@ -310,6 +310,9 @@ def run_ours(args) -> None:
     cam0 = scene.cameras[0]
     band_ms, band_pairs = time_band_forward(G, params, cam0, st, dev, flush, stream, args.steps, rank, world)
 
+    # ---- the loss front end and a full training step with it ----
+    loss_line = time_loss_front_end(G, params, cam, st, frame, grads, image, flush, stream, args.steps, dev)
+
     # ---- the exact GEF kernel of Eq. 2 on the same workload ----
     G.ges_preprocess(params, cam, st, frame, stream)
     G.ges_sort(frame, stream)
@@ -364,6 +367,7 @@ def run_ours(args) -> None:
                           "note": f"one config-3 frame split into {world} interleaved tile-row bands, S1-S4 per "
                                   f"rank + all_gather of the band pixels; device time, max over ranks"},
             "exact_beta_kernel": exact,
+            "loss_front_end": loss_line,
             "vs_gaussian_equivalent": {"ges_fwd_ms": fwd_ms, "gaussian_fwd_ms": g_ms, "ratio": g_ms / fwd_ms,
                                        "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
             "stages_ms": {n: float(stage_ms[i]) for i, n in enumerate(stage_names)},
@@ -484,6 +488,55 @@ def time_band_forward(G, params, cam, st, dev, flush, stream, steps, rank, world
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item()), int(frame.counts().pairs)
+
+
+def time_loss_front_end(G, params, cam, st, frame, grads, image, flush, stream, steps, dev):
+    """Eq. 9's loss on the bench frame (mask M_omega at omega = 0.75, L1 + SSIM + L_omega and
+    dL/dimage) alone, and one training step that uses it: S1-S4, the loss, S5.  The target
+    image is a synthetic smooth field (no dataset)."""
+    import torch
+    W, H = cam.width, cam.height
+    yy = torch.linspace(0, 1, H, device=dev)[:, None]
+    xx = torch.linspace(0, 1, W, device=dev)[None, :]
+    gt = torch.stack([0.5 + 0.3 * torch.sin(9 * xx + 4 * yy), 0.5 + 0.3 * torch.cos(7 * yy - 3 * xx),
+                      0.4 + 0.2 * torch.sin(13 * xx * yy)]).contiguous()
+    loss = G.Loss(W, H, device=dev)
+    mask = loss.mask(gt, 0.75, stream=stream)
+    dL = torch.empty_like(image)
+
+    def only_loss():
+        loss.mask(gt, 0.75, mask, stream=stream)
+        loss(image, gt, mask, dL, stream=stream)
+
+    def train_step():
+        G.ges_preprocess(params, cam, st, frame, stream)
+        G.ges_sort(frame, stream)
+        G.ges_render_fwd(frame, st, image, None, stream)
+        loss.mask(gt, 0.75, mask, stream=stream)
+        loss(image, gt, mask, dL, stream=stream)
+        G.ges_render_bwd(params, cam, st, frame, dL, grads, False, stream)
+
+    out = {}
+    for name, fn in (("loss", only_loss), ("train_step", train_step)):
+        for _ in range(3):
+            fn()
+        ms = []
+        for _ in range(steps):
+            flush.fill_(1)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+        out[name] = float(statistics.mean(ms))
+    n = 3 * W * H
+    moved = 4 * (2 * n + 3 * n + 3 * n + 2 * n + n)   # fwd reads I, I_gt, writes 3 SSIM partials; bwd reads them, I, I_gt, writes dL/dI
+    return {"loss_ms": out["loss"], "loss_GBps_moved": moved / (out["loss"] / 1e3) / 1e9,
+            "train_step_ms": out["train_step"],
+            "train_step": {"value": W * H / (out["train_step"] / 1e3) / 1e6, "unit": "Mpixel-frames/s (fwd+loss+bwd)"},
+            "note": "Eq. 9 (L1 + SSIM + L_omega at omega = 0.75) on the bench frame; train_step = S1-S4 + mask + "
+                    "loss + S5 with the loss's dL/dimage"}
 
 
 def time_exact_kernel(G, params, cam, scene, dL, image_phi, flush, stream, steps, dev):

@@ -10,8 +10,9 @@
 // HBM/stencil-bound; no tensor cores.  Per call:
 //   mask:  lum_down -> blur_h (both sigmas) -> blur_v + |DoG| + min/max ->
 //          threshold (all on the ~HW/25 downsampled grid)
-//   loss:  ssim_fwd (per 32 x 16 tile and channel: x, y with a 5-px halo in
-//          shared memory, separable 11-tap blurs of x, y, x^2, y^2, xy, the
+//   loss:  ssim_fwd (per 32 x 32 tile and channel: x, y with a 5-px halo in
+//          shared memory, separable 11-tap blurs of x, y, x^2, y^2, xy -- each
+//          thread two vertically adjacent pixels sharing 10 window rows --, the
 //          SSIM map and its three partials d_mu, d_E2, d_Exy, block sums of
 //          SSIM, |I - I_gt| and |I - I_gt| M) -> ssim_bwd (the partials'
 //          blurs = the window's adjoint, combined with the L1 and L_omega
@@ -23,158 +24,193 @@
 
 namespace ges {
 
-constexpr int kLTX = 32, kLTY = 16;             // loss tile
+constexpr int kLTX = 32, kLTY = 32;             // loss tile
 constexpr int kWin = 11, kWr = kWin / 2;        // SSIM window
-constexpr int kLThreads = kLTX * kLTY;          // one pixel per thread
+constexpr int kLThreads = 512;                  // 2 pixels per thread
+constexpr int kHX = kLTX + 2 * kWr, kHY = kLTY + 2 * kWr;
 constexpr float kC1 = 0.0001f, kC2 = 0.0009f;   // (0.01)^2, (0.03)^2
+// exp(-(k - 5)^2 / (2 1.5^2)) / sum, k = 0..10 (the SSIM window of R27), fp32
+__constant__ float kSsimW[kWin] = {0.00102838008f, 0.00759875814f, 0.0360007721f, 0.10936069f, 0.213005538f,
+                                   0.266011725f,   0.213005538f,   0.10936069f,   0.0360007721f, 0.00759875814f,
+                                   0.00102838008f};
 
-__device__ __forceinline__ void ssim_taps(float* w) {
-    if (threadIdx.x < kWin) {
-        float s = 0.0f;
-        for (int i = 0; i < kWin; ++i) {
-            const float d = (float)(i - kWr);
-            s += expf(-d * d / (2.0f * 1.5f * 1.5f));
-        }
-        const float d = (float)((int)threadIdx.x - kWr);  // signed: threadIdx.x is unsigned
-        w[threadIdx.x] = expf(-d * d / (2.0f * 1.5f * 1.5f)) / s;
+// Thread 0 gets the block sums of three values.
+__device__ __forceinline__ void block_sum3(float& a0, float& a1, float& a2, float (*s_red)[kLThreads / 32]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+        a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+        a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    if (lane == 0) { s_red[0][warp] = a0; s_red[1][warp] = a1; s_red[2][warp] = a2; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        a0 = a1 = a2 = 0.0f;
+        for (int w = 0; w < kLThreads / 32; ++w) { a0 += s_red[0][w]; a1 += s_red[1][w]; a2 += s_red[2][w]; }
     }
 }
 
-__device__ __forceinline__ float block_sum(float v, float* s_red) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    __syncthreads();
-    if (lane == 0) s_red[warp] = v;
-    __syncthreads();
-    float t = 0.0f;
-    if (threadIdx.x == 0)
-        for (int w = 0; w < kLThreads / 32; ++w) t += s_red[w];
-    return t;  // valid in thread 0
-}
-
+// full-resolution pixel (y, x) reads mask_lo[floor(y Hd / H), floor(x Wd / W)] (32-bit: sizes <= 4096)
 __device__ __forceinline__ uint8_t mask_at(const uint8_t* mask_lo, int Hd, int Wd, int H, int W, int y, int x) {
-    const int iy = min((int)(((int64_t)y * Hd) / H), Hd - 1), ix = min((int)(((int64_t)x * Wd) / W), Wd - 1);
+    const int iy = min((int)((unsigned)(y * Hd) / (unsigned)H), Hd - 1);
+    const int ix = min((int)((unsigned)(x * Wd) / (unsigned)W), Wd - 1);
     return mask_lo[iy * Wd + ix];
 }
 
 // ---- SSIM forward: 5 blurred moments, the map and its partials ------------
+// Per 32 x 32 tile and channel: x, y with a 5-px halo in shared memory (zero
+// outside the image), the horizontal 11-tap pass of x, y, x^2, y^2, xy for the
+// 42 rows, then the vertical pass for two pixels per thread.
 __global__ void __launch_bounds__(kLThreads) ssim_fwd_kernel(LossArgs a) {
-    __shared__ float s_w[kWin];
-    __shared__ float s_x[kLTY + 2 * kWr][kLTX + 2 * kWr];
-    __shared__ float s_y[kLTY + 2 * kWr][kLTX + 2 * kWr];
-    __shared__ float s_h[5][kLTY + 2 * kWr][kLTX];
-    __shared__ float s_red[kLThreads / 32];
+    __shared__ float s_in[2][kHY][kHX];   // x, y
+    __shared__ float s_h[5][kHY][kLTX];
+    __shared__ float s_red[3][kLThreads / 32];
     const int c = blockIdx.z, W = a.W, H = a.H;
     const int x0 = blockIdx.x * kLTX, y0 = blockIdx.y * kLTY;
     const float* X = a.image + (size_t)c * W * H;
     const float* Y = a.gt + (size_t)c * W * H;
-    ssim_taps(s_w);
-    for (int i = threadIdx.x; i < (kLTY + 2 * kWr) * (kLTX + 2 * kWr); i += kLThreads) {
-        const int r = i / (kLTX + 2 * kWr), q = i - r * (kLTX + 2 * kWr);
+    constexpr int kLoadIt = (kHY * kHX + kLThreads - 1) / kLThreads;
+    float lx[kLoadIt], ly[kLoadIt];
+#pragma unroll
+    for (int u = 0; u < kLoadIt; ++u) {  // every load in flight before any store
+        const int i = threadIdx.x + u * kLThreads;
+        const int r = i / kHX, q = i - r * kHX;
         const int gy = y0 + r - kWr, gx = x0 + q - kWr;
-        const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;  // zero padding
-        s_x[r][q] = in ? __ldg(X + (size_t)gy * W + gx) : 0.0f;
-        s_y[r][q] = in ? __ldg(Y + (size_t)gy * W + gx) : 0.0f;
+        const bool in = i < kHY * kHX && gx >= 0 && gx < W && gy >= 0 && gy < H;  // zero padding
+        lx[u] = in ? __ldg(X + (size_t)gy * W + gx) : 0.0f;
+        ly[u] = in ? __ldg(Y + (size_t)gy * W + gx) : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < kLoadIt; ++u) {
+        const int i = threadIdx.x + u * kLThreads;
+        if (i < kHY * kHX) {
+            const int r = i / kHX, q = i - r * kHX;
+            s_in[0][r][q] = lx[u]; s_in[1][r][q] = ly[u];
+        }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < (kLTY + 2 * kWr) * kLTX; i += kLThreads) {
+    for (int i = threadIdx.x; i < kHY * kLTX; i += kLThreads) {
         const int r = i / kLTX, q = i - r * kLTX;
-        float m1 = 0.f, m2 = 0.f, e11 = 0.f, e22 = 0.f, e12 = 0.f;
+        float m[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int k = 0; k < kWin; ++k) {
-            const float w = s_w[k], xv = s_x[r][q + k], yv = s_y[r][q + k];
-            m1 += w * xv; m2 += w * yv; e11 += w * xv * xv; e22 += w * yv * yv; e12 += w * xv * yv;
+            const float xv = s_in[0][r][q + k], yv = s_in[1][r][q + k];
+            const float wx = kSsimW[k] * xv, wy = kSsimW[k] * yv;
+            m[0] += wx; m[1] += wy;
+            m[2] = fmaf(wx, xv, m[2]); m[3] = fmaf(wy, yv, m[3]); m[4] = fmaf(wx, yv, m[4]);
         }
-        s_h[0][r][q] = m1; s_h[1][r][q] = m2; s_h[2][r][q] = e11; s_h[3][r][q] = e22; s_h[4][r][q] = e12;
+#pragma unroll
+        for (int j = 0; j < 5; ++j) s_h[j][r][q] = m[j];
     }
     __syncthreads();
-    const int ty = threadIdx.x / kLTX, tx = threadIdx.x - ty * kLTX;
-    const int gx = x0 + tx, gy = y0 + ty;
-    float S = 0.0f, ad = 0.0f, adm = 0.0f;
-    if (gx < W && gy < H) {
-        float mx = 0.f, my = 0.f, exx = 0.f, eyy = 0.f, exy = 0.f;
+    float sS = 0.0f, sA = 0.0f, sM = 0.0f;
+    // two vertically adjacent pixels per thread: their windows share 10 of 12 rows
+    const int tx = threadIdx.x & (kLTX - 1), ty0 = 2 * (threadIdx.x / kLTX);
+    float m[2][5] = {{0.f, 0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-        for (int k = 0; k < kWin; ++k) {
-            const float w = s_w[k];
-            mx += w * s_h[0][ty + k][tx]; my += w * s_h[1][ty + k][tx];
-            exx += w * s_h[2][ty + k][tx]; eyy += w * s_h[3][ty + k][tx]; exy += w * s_h[4][ty + k][tx];
+    for (int k = 0; k <= kWin; ++k) {
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            const float v = s_h[j][ty0 + k][tx];
+            if (k < kWin) m[0][j] = fmaf(kSsimW[k], v, m[0][j]);
+            if (k > 0) m[1][j] = fmaf(kSsimW[k - 1], v, m[1][j]);
         }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int ty = ty0 + h;
+        const int gx = x0 + tx, gy = y0 + ty;
+        if (gx >= W || gy >= H) continue;
+        const float mx = m[h][0], my = m[h][1], exx = m[h][2], eyy = m[h][3], exy = m[h][4];
         const float A1 = 2.f * mx * my + kC1, A2 = 2.f * (exy - mx * my) + kC2;
         const float B1 = mx * mx + my * my + kC1, B2 = (exx - mx * mx) + (eyy - my * my) + kC2;
-        const float iB = 1.0f / (B1 * B2);
-        S = A1 * A2 * iB;
+        const float iB1 = __frcp_rn(B1), iB2 = __frcp_rn(B2);
+        const float S = A1 * A2 * iB1 * iB2;
         const size_t pix = (size_t)c * W * H + (size_t)gy * W + gx;
-        a.d_mu[pix] = (2.f * my * A2 - 2.f * my * A1) * iB - S * (2.f * mx / B1 - 2.f * mx / B2);
-        a.d_e2[pix] = -S / B2;
-        a.d_exy[pix] = 2.f * A1 * iB;
-#ifdef GES_LOSS_DEBUG
-        if (c == 0) {
-            const size_t q = (size_t)gy * W + gx, n = (size_t)W * H;
-            a.d_mu[q] = mx; a.d_mu[n + q] = my; a.d_mu[2 * n + q] = exx; a.d_e2[q] = eyy; a.d_e2[n + q] = exy;
-            a.d_e2[2 * n + q] = s_w[threadIdx.x % kWin];
-        }
-#endif
-        const float d = s_x[ty + kWr][tx + kWr] - s_y[ty + kWr][tx + kWr];
-        ad = fabsf(d);
-        adm = a.mask_lo && mask_at(a.mask_lo, a.Hd, a.Wd, H, W, gy, gx) ? ad : 0.0f;
+        a.d_mu[pix] = 2.f * my * (A2 - A1) * iB1 * iB2 - S * 2.f * mx * (iB1 - iB2);
+        a.d_e2[pix] = -S * iB2;
+        a.d_exy[pix] = 2.f * A1 * iB1 * iB2;
+        const float d = fabsf(s_in[0][ty + kWr][tx + kWr] - s_in[1][ty + kWr][tx + kWr]);
+        sS += S;
+        sA += d;
+        if (a.mask_lo && mask_at(a.mask_lo, a.Hd, a.Wd, H, W, gy, gx)) sM += d;
     }
-    const int blk = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    const float sS = block_sum(S, s_red);
-    if (threadIdx.x == 0) a.partial[3 * blk] = sS;
-    const float sA = block_sum(ad, s_red);
-    if (threadIdx.x == 0) a.partial[3 * blk + 1] = sA;
-    const float sM = block_sum(adm, s_red);
-    if (threadIdx.x == 0) a.partial[3 * blk + 2] = sM;
+    block_sum3(sS, sA, sM, s_red);
+    if (threadIdx.x == 0) {
+        const int blk = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+        a.partial[3 * blk] = sS;
+        a.partial[3 * blk + 1] = sA;
+        a.partial[3 * blk + 2] = sM;
+    }
 }
 
 // ---- backward: the window's adjoint on the partials + L1 / L_omega ---------
 __global__ void __launch_bounds__(kLThreads) ssim_bwd_kernel(LossArgs a) {
-    __shared__ float s_w[kWin];
-    __shared__ float s_p[3][kLTY + 2 * kWr][kLTX + 2 * kWr];
-    __shared__ float s_h[3][kLTY + 2 * kWr][kLTX];
+    __shared__ float s_p[3][kHY][kHX];
+    __shared__ float s_h[3][kHY][kLTX];
     const int c = blockIdx.z, W = a.W, H = a.H;
     const int x0 = blockIdx.x * kLTX, y0 = blockIdx.y * kLTY;
     const size_t base = (size_t)c * W * H;
-    ssim_taps(s_w);
-    for (int i = threadIdx.x; i < (kLTY + 2 * kWr) * (kLTX + 2 * kWr); i += kLThreads) {
-        const int r = i / (kLTX + 2 * kWr), q = i - r * (kLTX + 2 * kWr);
+    constexpr int kLoadIt = (kHY * kHX + kLThreads - 1) / kLThreads;
+    float l0[kLoadIt], l1[kLoadIt], l2[kLoadIt];
+#pragma unroll
+    for (int u = 0; u < kLoadIt; ++u) {  // every load in flight before any store
+        const int i = threadIdx.x + u * kLThreads;
+        const int r = i / kHX, q = i - r * kHX;
         const int gy = y0 + r - kWr, gx = x0 + q - kWr;
-        const bool in = gx >= 0 && gx < W && gy >= 0 && gy < H;  // no window centred off the image
+        const bool in = i < kHY * kHX && gx >= 0 && gx < W && gy >= 0 && gy < H;  // no window off the image
         const size_t p = base + (size_t)gy * W + gx;
-        s_p[0][r][q] = in ? a.d_mu[p] : 0.0f;
-        s_p[1][r][q] = in ? a.d_e2[p] : 0.0f;
-        s_p[2][r][q] = in ? a.d_exy[p] : 0.0f;
+        l0[u] = in ? a.d_mu[p] : 0.0f;
+        l1[u] = in ? a.d_e2[p] : 0.0f;
+        l2[u] = in ? a.d_exy[p] : 0.0f;
+    }
+#pragma unroll
+    for (int u = 0; u < kLoadIt; ++u) {
+        const int i = threadIdx.x + u * kLThreads;
+        if (i < kHY * kHX) {
+            const int r = i / kHX, q = i - r * kHX;
+            s_p[0][r][q] = l0[u]; s_p[1][r][q] = l1[u]; s_p[2][r][q] = l2[u];
+        }
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < (kLTY + 2 * kWr) * kLTX; i += kLThreads) {
+    for (int i = threadIdx.x; i < kHY * kLTX; i += kLThreads) {
         const int r = i / kLTX, q = i - r * kLTX;
-        float b0 = 0.f, b1 = 0.f, b2 = 0.f;
+        float b[3] = {0.f, 0.f, 0.f};
 #pragma unroll
         for (int k = 0; k < kWin; ++k) {
-            const float w = s_w[k];
-            b0 += w * s_p[0][r][q + k]; b1 += w * s_p[1][r][q + k]; b2 += w * s_p[2][r][q + k];
+            const float w = kSsimW[k];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) b[j] = fmaf(w, s_p[j][r][q + k], b[j]);
         }
-        s_h[0][r][q] = b0; s_h[1][r][q] = b1; s_h[2][r][q] = b2;
+#pragma unroll
+        for (int j = 0; j < 3; ++j) s_h[j][r][q] = b[j];
     }
     __syncthreads();
-    const int ty = threadIdx.x / kLTX, tx = threadIdx.x - ty * kLTX;
-    const int gx = x0 + tx, gy = y0 + ty;
-    if (gx >= W || gy >= H) return;
-    float g0 = 0.f, g1 = 0.f, g2 = 0.f;
-#pragma unroll
-    for (int k = 0; k < kWin; ++k) {
-        const float w = s_w[k];
-        g0 += w * s_h[0][ty + k][tx]; g1 += w * s_h[1][ty + k][tx]; g2 += w * s_h[2][ty + k][tx];
-    }
-    const size_t p = base + (size_t)gy * W + gx;
-    const float xv = __ldg(a.image + p), yv = __ldg(a.gt + p);
-    const float dS = g0 + 2.f * xv * g1 + yv * g2;          // N d mean SSIM / dx
-    const float d = xv - yv;
-    const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
-    const float m = a.mask_lo && mask_at(a.mask_lo, a.Hd, a.Wd, H, W, gy, gx) ? 1.f : 0.f;
     const float lam_l1 = 1.0f - a.lambda_ssim - a.lambda_omega;
-    a.dL_dimage[p] = (lam_l1 * sg - a.lambda_ssim * dS + a.lambda_omega * sg * m) * a.inv_n;
+    const int tx = threadIdx.x & (kLTX - 1), ty0 = 2 * (threadIdx.x / kLTX);
+    float g[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+#pragma unroll
+    for (int k = 0; k <= kWin; ++k) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const float v = s_h[j][ty0 + k][tx];
+            if (k < kWin) g[0][j] = fmaf(kSsimW[k], v, g[0][j]);
+            if (k > 0) g[1][j] = fmaf(kSsimW[k - 1], v, g[1][j]);
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int gx = x0 + tx, gy = y0 + ty0 + h;
+        if (gx >= W || gy >= H) continue;
+        const size_t p = base + (size_t)gy * W + gx;
+        const float xv = __ldg(a.image + p), yv = __ldg(a.gt + p);
+        const float dS = g[h][0] + 2.f * xv * g[h][1] + yv * g[h][2];   // N d mean SSIM / dx
+        const float d = xv - yv;
+        const float sg = d > 0.f ? 1.f : (d < 0.f ? -1.f : 0.f);
+        const float m = a.mask_lo && mask_at(a.mask_lo, a.Hd, a.Wd, H, W, gy, gx) ? 1.f : 0.f;
+        a.dL_dimage[p] = (lam_l1 * sg - a.lambda_ssim * dS + a.lambda_omega * sg * m) * a.inv_n;
+    }
 }
 
 // one CTA: fixed-order fp64 sums of the block partials -> total, L1, SSIM, L_omega
