@@ -290,6 +290,63 @@ size_t ges_loss_workspace_bytes(int32_t width, int32_t height, float downsample)
 ges_status ges_loss_mask(const float *gt, int32_t width, int32_t height, float omega, const ges_loss_settings *settings,
                          void *workspace, size_t workspace_bytes, uint8_t *mask_lo, void *stream);
 
+/* ------------------------------------------------------------------------
+ * Optimizer and shape-aware density control (
+ * PAPER.md §4.4 :348-358, Appendix :1227-1271; readings DESIGN.md R29-R33).
+ * Parameter, gradient and Adam-moment buffers are planar fp32 [C][P] in the
+ * ges_particles order (mean 3, log_scale 3, quat 4, opacity_logit 1, sh 3K,
+ * beta 1; C = 12 + 3K), device, caller-owned; stream-ordered.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+    int32_t step;                 /* 1-based Adam step (bias correction)                          */
+    float lr_position;            /* ges_lr_position(step, ...) (:1232-1236)                      */
+    float lr_scaling, lr_rotation, lr_opacity; /* 0.005, 0.001, 0.05 (:1238-1242)                */
+    float lr_feature_dc, lr_feature_rest;      /* 0.0025 and 0.0025 / 20 (SH DC / higher bands)  */
+    float lr_shape;               /* 0.001 (:1242; :397 says 0.0015, R20)                          */
+    float beta1, beta2, eps;      /* 0.9, 0.999, 1e-15                                             */
+} ges_adam_settings;
+
+/* Log-linear position learning rate init -> final over max_steps (delay multiplier
+ * ramp over delay_steps; none for 0), the schedule of PAPER.md:1232-1236.  Host. */
+double ges_lr_position(int64_t step, double init, double final_, double delay_mult, int64_t max_steps,
+                       int64_t delay_steps);
+
+/* One bias-corrected Adam step of every plane (params, m, v updated in place). */
+ges_status ges_adam_step(float *params, const float *grads, float *m, float *v, int64_t P, int32_t sh_degree,
+                         const ges_adam_settings *settings, void *stream);
+
+/* Opacity reset (what = 0): logit <- min(logit, logit(0.01)); shape reset (what = 1):
+ * beta <- 2 (PAPER.md:1253 intervals; targets R30). */
+ges_status ges_reset(float *params, int64_t P, int32_t sh_degree, int32_t what, void *stream);
+
+/* Densification statistic of one view, between ges_render_bwd_tiles (S5a) and
+ * ges_backward_particles (S5b): for every visible particle accum += |(du W/2,
+ * dv H/2)| (the view-space gradient in NDC units) and count += 1 (R32). */
+ges_status ges_densify_stats(const ges_frame *frame, float *accum, float *count, void *stream);
+
+typedef struct {
+    float grad_threshold;   /* 3e-4 (:1250)                                */
+    float percent_dense;    /* 0.01 (:1246)                                */
+    float scene_extent;     /* clone if max exp(log s) <= percent_dense x this */
+    float opacity_prune;    /* 0.005 (:1248)                               */
+    float shape_prune;      /* prune if phi-bar_rho(beta) < this: 0.5 (:397; :1248 says 0.005, R20/R31) */
+    float rho;              /* of phi-bar (Eq. 6)                          */
+    uint64_t seed;          /* split positions: splitmix64 + Box-Muller on (seed, particle, child) */
+} ges_density_settings;
+
+/* Bytes of device workspace for ges_densify_prune on P particles. */
+size_t ges_densify_workspace_bytes(int64_t P);
+
+/* Prune / clone / split (R31-R33) into *_out planar [C][capacity_out] buffers,
+ * capacity_out >= 2 P (the largest possible set); the new count goes to the
+ * device int64 *P_out.  New order: kept particles in index order (a split parent
+ * replaced by its first child), then clones, then second split children; kept
+ * particles keep their Adam moments, new ones start at zero. */
+ges_status ges_densify_prune(const float *params, const float *m, const float *v, const float *accum,
+                             const float *count, int64_t P, int32_t sh_degree, const ges_density_settings *settings,
+                             float *params_out, float *m_out, float *v_out, int64_t capacity_out, void *workspace,
+                             size_t workspace_bytes, int64_t *P_out, void *stream);
+
 /* Eq. 9 on (image, gt): dL_dimage [3][H][W] (overwritten) and loss_out[4] =
  * (L, L1, SSIM, L_omega) on the device.  mask_lo = NULL drops the L_omega
  * term (its weight still enters l_L1).  Errors as ges_loss_mask. */

@@ -5,10 +5,12 @@ There is no CPU fallback: without a built libges.so (and a CUDA device) the
 entry points raise.
 """
 from ._lib import GESError, load  # noqa: F401
-from .api import (PARAM_NAMES, Frame, Loss, LossSettings, PlanarParams, Renderer, Settings,  # noqa: F401
-                  c_camera, ges_backward_particles, ges_loss_mask_dims, ges_preprocess, ges_render_bwd,
-                  ges_render_bwd_tiles, ges_render_fwd, ges_sort, n_planes, plane_counts)
+from .api import (PARAM_NAMES, Adam, AdamSettings, DensityControl, DensitySettings, Frame, Loss,  # noqa: F401
+                  LossSettings, PlanarParams, Renderer, Settings, c_camera, ges_backward_particles,
+                  ges_loss_mask_dims, ges_preprocess, ges_render_bwd, ges_render_bwd_tiles, ges_render_fwd,
+                  ges_reset, ges_sort, n_planes, plane_counts)
 
 __all__ = ["GESError", "load", "Frame", "PlanarParams", "Renderer", "Settings", "ges_preprocess", "ges_sort",
            "ges_render_fwd", "ges_render_bwd", "ges_render_bwd_tiles", "ges_backward_particles", "n_planes",
-           "plane_counts", "PARAM_NAMES", "c_camera", "Loss", "LossSettings", "ges_loss_mask_dims"]
+           "plane_counts", "PARAM_NAMES", "c_camera", "Loss", "LossSettings", "ges_loss_mask_dims",
+           "Adam", "AdamSettings", "DensityControl", "DensitySettings", "ges_reset"]

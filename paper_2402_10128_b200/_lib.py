@@ -77,10 +77,22 @@ class ges_loss_settings(C.Structure):
                 ("downsample", C.c_float)]
 
 
+class ges_adam_settings(C.Structure):
+    _fields_ = [("step", C.c_int32)] + [(n, C.c_float) for n in (
+        "lr_position", "lr_scaling", "lr_rotation", "lr_opacity", "lr_feature_dc", "lr_feature_rest", "lr_shape",
+        "beta1", "beta2", "eps")]
+
+
+class ges_density_settings(C.Structure):
+    _fields_ = [(n, C.c_float) for n in ("grad_threshold", "percent_dense", "scene_extent", "opacity_prune",
+                                         "shape_prune", "rho")] + [("seed", C.c_uint64)]
+
+
 EXPORTS = ["ges_workspace_bytes", "ges_frame_init", "ges_preprocess", "ges_sort", "ges_render_fwd",
            "ges_render_bwd", "ges_render_bwd_tiles", "ges_backward_particles", "ges_counts_get",
            "ges_status_string", "ges_version", "ges_loss_mask_dims", "ges_loss_workspace_bytes", "ges_loss_mask",
-           "ges_loss"]
+           "ges_loss", "ges_lr_position", "ges_adam_step", "ges_reset", "ges_densify_stats",
+           "ges_densify_workspace_bytes", "ges_densify_prune"]
 
 _lib = None
 
@@ -124,6 +136,20 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         L.ges_status_string.restype = C.c_char_p
         L.ges_status_string.argtypes = [C.c_int]
         L.ges_version.restype = C.c_char_p
+        L.ges_lr_position.restype = C.c_double
+        L.ges_lr_position.argtypes = [C.c_int64, C.c_double, C.c_double, C.c_double, C.c_int64, C.c_int64]
+        L.ges_adam_step.restype = C.c_int
+        L.ges_adam_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                                    C.POINTER(ges_adam_settings), C.c_void_p]
+        L.ges_reset.restype = C.c_int
+        L.ges_reset.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p]
+        L.ges_densify_stats.restype = C.c_int
+        L.ges_densify_stats.argtypes = [C.POINTER(ges_frame), C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ges_densify_workspace_bytes.restype = C.c_size_t
+        L.ges_densify_workspace_bytes.argtypes = [C.c_int64]
+        L.ges_densify_prune.restype = C.c_int
+        L.ges_densify_prune.argtypes = [C.c_void_p] * 5 + [C.c_int64, C.c_int32, C.POINTER(ges_density_settings)] + [
+            C.c_void_p] * 3 + [C.c_int64, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
         L.ges_loss_mask_dims.restype = C.c_int
         L.ges_loss_mask_dims.argtypes = [C.c_int32, C.c_int32, C.c_float, C.POINTER(C.c_int32),
                                          C.POINTER(C.c_int32)]

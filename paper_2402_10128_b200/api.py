@@ -294,3 +294,110 @@ class Loss:
                                   C.c_void_p(dL_dimage.data_ptr()), C.c_void_p(self.out.data_ptr()),
                                   C.c_void_p(_stream(stream))), "ges_loss")
         return self.out, dL_dimage
+
+
+# --- optimizer and density control (ges.h ges_adam_step ...) ---
+@dataclasses.dataclass
+class AdamSettings:
+    """Per-group learning rates of PAPER.md:1231-1244 (readings DESIGN.md R29)."""
+    lr_pos_init: float = 1.6e-4
+    lr_pos_final: float = 1.6e-6
+    lr_pos_delay_mult: float = 0.01
+    lr_pos_max_steps: int = 30000
+    lr_feature: float = 2.5e-3
+    lr_opacity: float = 0.05
+    lr_scaling: float = 5e-3
+    lr_rotation: float = 1e-3
+    lr_shape: float = 1e-3
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-15
+
+    def lr_position(self, step: int) -> float:
+        return L.load().ges_lr_position(step, self.lr_pos_init, self.lr_pos_final, self.lr_pos_delay_mult,
+                                        self.lr_pos_max_steps, 0)
+
+    def c(self, step: int) -> L.ges_adam_settings:
+        s = L.ges_adam_settings()
+        s.step = int(step)
+        s.lr_position = self.lr_position(step)
+        s.lr_scaling, s.lr_rotation, s.lr_opacity = self.lr_scaling, self.lr_rotation, self.lr_opacity
+        s.lr_feature_dc, s.lr_feature_rest, s.lr_shape = self.lr_feature, self.lr_feature / 20.0, self.lr_shape
+        s.beta1, s.beta2, s.eps = self.beta1, self.beta2, self.eps
+        return s
+
+
+class Adam:
+    """Fused Adam over a PlanarParams buffer (moments owned here)."""
+
+    def __init__(self, params: PlanarParams, settings: Optional[AdamSettings] = None):
+        self.settings = settings or AdamSettings()
+        self.m = PlanarParams.zeros(params.P, params.sh_degree, params.flat.device)
+        self.v = PlanarParams.zeros(params.P, params.sh_degree, params.flat.device)
+        self.t = 0
+
+    def step(self, params: PlanarParams, grads: PlanarParams, stream=None) -> None:
+        self.t += 1
+        s = self.settings.c(self.t)
+        L.check(L.load().ges_adam_step(C.c_void_p(params.flat.data_ptr()), C.c_void_p(grads.flat.data_ptr()),
+                                       C.c_void_p(self.m.flat.data_ptr()), C.c_void_p(self.v.flat.data_ptr()),
+                                       params.P, params.sh_degree, C.byref(s), C.c_void_p(_stream(stream))),
+                "ges_adam_step")
+
+
+def ges_reset(params: PlanarParams, what: int, stream=None) -> None:
+    """what = 0: opacity reset (kappa <= 0.01); 1: shape reset (beta = 2)."""
+    L.check(L.load().ges_reset(C.c_void_p(params.flat.data_ptr()), params.P, params.sh_degree, int(what),
+                               C.c_void_p(_stream(stream))), "ges_reset")
+
+
+@dataclasses.dataclass
+class DensitySettings:
+    grad_threshold: float = 3e-4
+    percent_dense: float = 0.01
+    scene_extent: float = 1.0
+    opacity_prune: float = 0.005
+    shape_prune: float = 0.5
+    rho: float = 0.1
+    seed: int = 0
+
+    def c(self) -> L.ges_density_settings:
+        s = L.ges_density_settings()
+        s.grad_threshold, s.percent_dense, s.scene_extent = self.grad_threshold, self.percent_dense, self.scene_extent
+        s.opacity_prune, s.shape_prune, s.rho, s.seed = self.opacity_prune, self.shape_prune, self.rho, int(self.seed)
+        return s
+
+
+class DensityControl:
+    """View-space gradient statistics and the densify/prune pass."""
+
+    def __init__(self, P: int, device="cuda"):
+        self.accum = torch.zeros(P, dtype=torch.float32, device=device)
+        self.count = torch.zeros(P, dtype=torch.float32, device=device)
+
+    def accumulate(self, frame: Frame, stream=None) -> None:
+        """Call between ges_render_bwd_tiles and ges_backward_particles."""
+        L.check(L.load().ges_densify_stats(C.byref(frame.c), C.c_void_p(self.accum.data_ptr()),
+                                           C.c_void_p(self.count.data_ptr()), C.c_void_p(_stream(stream))),
+                "ges_densify_stats")
+
+    def densify_prune(self, params: PlanarParams, opt: Adam, settings: DensitySettings, stream=None):
+        """Returns the new PlanarParams; opt's moments are replaced; the statistics reset (one sync)."""
+        P, deg, dev = params.P, params.sh_degree, params.flat.device
+        cap = 2 * P
+        outs = [torch.empty((n_planes(deg), cap), dtype=torch.float32, device=dev) for _ in range(3)]
+        ws = torch.empty(L.load().ges_densify_workspace_bytes(P), dtype=torch.uint8, device=dev)
+        p_out = torch.zeros(1, dtype=torch.int64, device=dev)
+        s = settings.c()
+        L.check(L.load().ges_densify_prune(
+            C.c_void_p(params.flat.data_ptr()), C.c_void_p(opt.m.flat.data_ptr()), C.c_void_p(opt.v.flat.data_ptr()),
+            C.c_void_p(self.accum.data_ptr()), C.c_void_p(self.count.data_ptr()), P, deg, C.byref(s),
+            C.c_void_p(outs[0].data_ptr()), C.c_void_p(outs[1].data_ptr()), C.c_void_p(outs[2].data_ptr()), cap,
+            C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(p_out.data_ptr()), C.c_void_p(_stream(stream))),
+            "ges_densify_prune")
+        n = int(p_out.item())
+        new = [PlanarParams(o[:, :n].contiguous(), n, deg) for o in outs]
+        opt.m, opt.v = new[1], new[2]
+        self.accum = torch.zeros(n, dtype=torch.float32, device=dev)
+        self.count = torch.zeros(n, dtype=torch.float32, device=dev)
+        return new[0]

@@ -394,4 +394,80 @@ ges_status ges_loss(const float* image, const float* gt, const uint8_t* mask_lo,
     return cuda_status(launch_loss(a, (cudaStream_t)stream));
 }
 
+
+// ---------------------------------------------------------------------------
+// optimizer and density control
+// ---------------------------------------------------------------------------
+double ges_lr_position(int64_t step, double init, double final_, double delay_mult, int64_t max_steps,
+                       int64_t delay_steps) {
+    if (step < 0 || (init == 0.0 && final_ == 0.0) || max_steps <= 0) return 0.0;
+    double delay = 1.0;
+    if (delay_steps > 0) {
+        const double t = std::min(std::max((double)step / (double)delay_steps, 0.0), 1.0);
+        delay = delay_mult + (1.0 - delay_mult) * std::sin(0.5 * 3.14159265358979323846 * t);
+    }
+    const double t = std::min(std::max((double)step / (double)max_steps, 0.0), 1.0);
+    return delay * std::exp(std::log(init) * (1.0 - t) + std::log(final_) * t);
+}
+
+ges_status ges_adam_step(float* params, const float* grads, float* m, float* v, int64_t P, int32_t sh_degree,
+                         const ges_adam_settings* s, void* stream) {
+    if (!params || !grads || !m || !v || !s || P < 1 || sh_degree < 0 || sh_degree > 3 || s->step < 1)
+        return GES_ERR_INVALID_ARG;
+    const int K = (sh_degree + 1) * (sh_degree + 1);
+    AdamArgs a;
+    a.params = params; a.grads = grads; a.m = m; a.v = v; a.P = P; a.n_planes = 12 + 3 * K;
+    a.lr_position = s->lr_position; a.lr_scaling = s->lr_scaling; a.lr_rotation = s->lr_rotation;
+    a.lr_opacity = s->lr_opacity; a.lr_feature_dc = s->lr_feature_dc; a.lr_feature_rest = s->lr_feature_rest;
+    a.lr_shape = s->lr_shape; a.beta1 = s->beta1; a.beta2 = s->beta2; a.eps = s->eps;
+    a.inv_bc1 = (float)(1.0 / (1.0 - std::pow((double)s->beta1, (double)s->step)));
+    a.inv_bc2 = (float)(1.0 / (1.0 - std::pow((double)s->beta2, (double)s->step)));
+    return cuda_status(launch_adam(a, (cudaStream_t)stream));
+}
+
+ges_status ges_reset(float* params, int64_t P, int32_t sh_degree, int32_t what, void* stream) {
+    if (!params || P < 1 || sh_degree < 0 || sh_degree > 3 || (what != 0 && what != 1)) return GES_ERR_INVALID_ARG;
+    const int K = (sh_degree + 1) * (sh_degree + 1);
+    if (what == 0)
+        return cuda_status(launch_reset(params, P, 10, (float)std::log(0.01 / 0.99), 0, (cudaStream_t)stream));
+    return cuda_status(launch_reset(params, P, 11 + 3 * K, 2.0f, 1, (cudaStream_t)stream));
+}
+
+ges_status ges_densify_stats(const ges_frame* frame, float* accum, float* count, void* stream) {
+    if (!frame || !accum || !count) return GES_ERR_INVALID_ARG;
+    DensifyStatsArgs a;
+    a.status = frame->status; a.grad2d = frame->grad2d; a.accum = accum; a.count = count;
+    a.P = frame->P; a.W = frame->width; a.H = frame->height;
+    return cuda_status(launch_densify_stats(a, (cudaStream_t)stream));
+}
+
+size_t ges_densify_workspace_bytes(int64_t P) {
+    if (P < 1) return 0;
+    return align_up((size_t)P) + align_up(sizeof(int) * 3 * (size_t)densify_blocks(P)) + align_up(3 * sizeof(long long));
+}
+
+ges_status ges_densify_prune(const float* params, const float* m, const float* v, const float* accum,
+                             const float* count, int64_t P, int32_t sh_degree, const ges_density_settings* s,
+                             float* params_out, float* m_out, float* v_out, int64_t capacity_out, void* workspace,
+                             size_t workspace_bytes, int64_t* P_out, void* stream) {
+    if (!params || !m || !v || !accum || !count || !s || !params_out || !m_out || !v_out || !workspace || !P_out ||
+        P < 1 || sh_degree < 0 || sh_degree > 3 || capacity_out < 2 * P)
+        return GES_ERR_INVALID_ARG;
+    if (workspace_bytes < ges_densify_workspace_bytes(P)) return GES_ERR_CAPACITY;
+    const int K = (sh_degree + 1) * (sh_degree + 1);
+    char* ws = (char*)workspace;
+    DensifyArgs a;
+    a.params = params; a.m = m; a.v = v; a.accum = accum; a.count = count;
+    a.P = P; a.cap_out = capacity_out; a.n_planes = 12 + 3 * K;
+    a.grad_threshold = s->grad_threshold; a.percent_dense = s->percent_dense; a.extent = s->scene_extent;
+    a.opacity_prune = s->opacity_prune; a.shape_prune = s->shape_prune; a.rho = s->rho; a.seed = s->seed;
+    a.params_out = params_out; a.m_out = m_out; a.v_out = v_out;
+    a.action = (uint8_t*)ws;
+    a.block_cnt = (int*)(ws + align_up((size_t)P));
+    a.totals = (long long*)(ws + align_up((size_t)P) + align_up(sizeof(int) * 3 * (size_t)densify_blocks(P)));
+    a.P_out = (long long*)P_out;
+    a.nblocks = 0;
+    return cuda_status(launch_densify_prune(a, (cudaStream_t)stream));
+}
+
 }  // extern "C"

@@ -169,4 +169,43 @@ struct MaskArgs {
 };
 cudaError_t launch_mask(const MaskArgs& a, cudaStream_t stream);
 
+// --- optimizer and density control (train.cu) ----------
+struct AdamArgs {
+    float* params;                    // [n_planes][P]
+    const float* grads;
+    float *m, *v;
+    int64_t P;
+    int n_planes;
+    float lr_position, lr_scaling, lr_rotation, lr_opacity, lr_feature_dc, lr_feature_rest, lr_shape;
+    float beta1, beta2, eps, inv_bc1, inv_bc2;
+};
+cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream);
+cudaError_t launch_reset(float* params, int64_t P, int plane, float cap, int mode, cudaStream_t stream);
+
+struct DensifyStatsArgs {
+    const uint8_t* status;
+    const float* grad2d;              // the frame's [P][12] records after S5a (du, dv at 0, 1)
+    float *accum, *count;             // [P]
+    int64_t P;
+    int W, H;
+};
+cudaError_t launch_densify_stats(const DensifyStatsArgs& a, cudaStream_t stream);
+
+struct DensifyArgs {
+    const float *params, *m, *v;      // [n_planes][P]
+    const float *accum, *count;       // [P]
+    int64_t P, cap_out;
+    int n_planes;
+    float grad_threshold, percent_dense, extent, opacity_prune, shape_prune, rho;
+    unsigned long long seed;
+    float *params_out, *m_out, *v_out;  // [n_planes][cap_out]
+    uint8_t* action;                  // [P] workspace
+    int* block_cnt;                   // [3 blocks] workspace
+    long long* totals;                // [3] workspace
+    long long* P_out;                 // device: the new particle count
+    int nblocks;
+};
+cudaError_t launch_densify_prune(const DensifyArgs& a, cudaStream_t stream);
+int64_t densify_blocks(int64_t P);
+
 }  // namespace ges
