@@ -516,8 +516,15 @@ def time_loss_front_end(G, params, cam, st, frame, grads, image, flush, stream, 
         loss(image, gt, mask, dL, stream=stream)
         G.ges_render_bwd(params, cam, st, frame, dL, grads, False, stream)
 
+    # the optimizer on a copy of the parameters (the timed steps must not drift the bench scene)
+    pcopy = G.PlanarParams(params.flat.clone(), params.P, params.sh_degree)
+    opt = G.Adam(pcopy)
+
+    def adam():
+        opt.step(pcopy, grads, stream=stream)
+
     out = {}
-    for name, fn in (("loss", only_loss), ("train_step", train_step)):
+    for name, fn in (("loss", only_loss), ("train_step", train_step), ("adam", adam)):
         for _ in range(3):
             fn()
         ms = []
@@ -532,7 +539,14 @@ def time_loss_front_end(G, params, cam, st, frame, grads, image, flush, stream, 
         out[name] = float(statistics.mean(ms))
     n = 3 * W * H
     moved = 4 * (2 * n + 3 * n + 3 * n + 2 * n + n)   # fwd reads I, I_gt, writes 3 SSIM partials; bwd reads them, I, I_gt, writes dL/dI
+    n_el = params.flat.numel()
+    adam_bytes = 28 * n_el   # reads p, g, m, v; writes p, m, v (fp32)
+    peaks, _ = measured_peaks()
     return {"loss_ms": out["loss"], "loss_GBps_moved": moved / (out["loss"] / 1e3) / 1e9,
+            "adam": {"ms": out["adam"], "GBps": adam_bytes / (out["adam"] / 1e3) / 1e9,
+                     "frac_hbm": adam_bytes / (out["adam"] / 1e3) / 1e9 / peaks["hbm_gbs"],
+                     "bytes": adam_bytes, "note": "fused Adam over all 60 x P planar parameters (NEXT-2)"},
+            "train_iteration_ms": out["train_step"] + out["adam"],
             "train_step_ms": out["train_step"],
             "train_step": {"value": W * H / (out["train_step"] / 1e3) / 1e6, "unit": "Mpixel-frames/s (fwd+loss+bwd)"},
             "note": "Eq. 9 (L1 + SSIM + L_omega at omega = 0.75) on the bench frame; train_step = S1-S4 + mask + "
