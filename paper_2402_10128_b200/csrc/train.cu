@@ -18,31 +18,63 @@
 namespace ges {
 
 // ---- Adam -------------------------------------------------------------------
+__device__ __forceinline__ float plane_lr(const AdamArgs& a, int plane) {
+    const int K3 = a.n_planes - 12;  // 3K SH planes
+    if (plane < 3) return a.lr_position;
+    if (plane < 6) return a.lr_scaling;
+    if (plane < 10) return a.lr_rotation;
+    if (plane == 10) return a.lr_opacity;
+    if (plane < 14) return a.lr_feature_dc;
+    if (plane < 11 + K3) return a.lr_feature_rest;
+    return a.lr_shape;
+}
+
+__device__ __forceinline__ void adam1(const AdamArgs& a, float lr, float g, float& p, float& m, float& v) {
+    m = a.beta1 * m + (1.0f - a.beta1) * g;
+    v = a.beta2 * v + (1.0f - a.beta2) * g * g;
+    p -= lr * (m * a.inv_bc1) / (sqrtf(v * a.inv_bc2) + a.eps);
+}
+
 __global__ void adam_kernel(AdamArgs a) {
     const int plane = blockIdx.y;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.P) return;
-    const int K3 = a.n_planes - 12;  // 3K SH planes
-    float lr;
-    if (plane < 3) lr = a.lr_position;
-    else if (plane < 6) lr = a.lr_scaling;
-    else if (plane < 10) lr = a.lr_rotation;
-    else if (plane == 10) lr = a.lr_opacity;
-    else if (plane < 14) lr = a.lr_feature_dc;
-    else if (plane < 11 + K3) lr = a.lr_feature_rest;
-    else lr = a.lr_shape;
+    const float lr = plane_lr(a, plane);
     const size_t q = (size_t)plane * a.P + i;
-    const float g = a.grads[q];
-    const float m = a.beta1 * a.m[q] + (1.0f - a.beta1) * g;
-    const float v = a.beta2 * a.v[q] + (1.0f - a.beta2) * g * g;
-    a.m[q] = m;
-    a.v[q] = v;
-    a.params[q] -= lr * (m * a.inv_bc1) / (sqrtf(v * a.inv_bc2) + a.eps);
+    float p = a.params[q], m = a.m[q], v = a.v[q];
+    adam1(a, lr, a.grads[q], p, m, v);
+    a.params[q] = p; a.m[q] = m; a.v[q] = v;
+}
+
+// P % 4 == 0 and 16-B aligned buffers: four elements per thread, float4 loads/stores
+__global__ void adam4_kernel(AdamArgs a) {
+    const int plane = blockIdx.y;
+    const int64_t i4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (4 * i4 >= a.P) return;
+    const float lr = plane_lr(a, plane);
+    const size_t q = ((size_t)plane * a.P) / 4 + i4;
+    float4 p = reinterpret_cast<float4*>(a.params)[q];
+    float4 m = reinterpret_cast<float4*>(a.m)[q];
+    float4 v = reinterpret_cast<float4*>(a.v)[q];
+    const float4 g = reinterpret_cast<const float4*>(a.grads)[q];
+    adam1(a, lr, g.x, p.x, m.x, v.x);
+    adam1(a, lr, g.y, p.y, m.y, v.y);
+    adam1(a, lr, g.z, p.z, m.z, v.z);
+    adam1(a, lr, g.w, p.w, m.w, v.w);
+    reinterpret_cast<float4*>(a.params)[q] = p;
+    reinterpret_cast<float4*>(a.m)[q] = m;
+    reinterpret_cast<float4*>(a.v)[q] = v;
 }
 
 cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream) {
-    const dim3 grid((unsigned)((a.P + 255) / 256), (unsigned)a.n_planes);
-    adam_kernel<<<grid, 256, 0, stream>>>(a);
+    auto al = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+    if (a.P % 4 == 0 && al(a.params) && al(a.grads) && al(a.m) && al(a.v)) {
+        const dim3 grid((unsigned)((a.P / 4 + 255) / 256), (unsigned)a.n_planes);
+        adam4_kernel<<<grid, 256, 0, stream>>>(a);
+    } else {
+        const dim3 grid((unsigned)((a.P + 255) / 256), (unsigned)a.n_planes);
+        adam_kernel<<<grid, 256, 0, stream>>>(a);
+    }
     return cudaGetLastError();
 }
 
