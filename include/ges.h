@@ -196,9 +196,14 @@ typedef struct {
     /* ---- S4 / S5 ---- */
     float *final_T;        /* [H*W] transmittance after the last composited particle   */
     uint32_t *n_contrib;   /* [H*W] list position of the last composited particle + 1  */
-    float *grad2d;         /* [P][12] per-particle 2-D gradient record (du, dv, dA, dB |
-                              dC, dkappa, dr, dg | db, 0, 0, 0), A..C = the log2-scaled
-                              conic; kept all-zero between backward passes            */
+    float *grad2d;         /* [P][12] per-particle S5a record: raw moments over the
+                              particle's composited pixels, q = G dL/dalpha:
+                              (sum q dx, sum q dy, sum q dx^2, sum q dx dy |
+                              sum q dy^2, dL/dkappa, dr, dg | db, Sb, 0, 0) with
+                              dx = u - px, dy = v - py, Sb = the exact kernel's
+                              sum G dL/dalpha Q^(beta/2) log2 Q; S5b turns them into
+                              dL/d(u, v, conic) with the per-particle factors
+                              (kappa, the conic).  Kept all-zero between backward passes */
     size_t workspace_bytes;
 } ges_frame;
 

@@ -437,7 +437,8 @@ ges_status ges_densify_stats(const ges_frame* frame, float* accum, float* count,
     if (!frame || !accum || !count) return GES_ERR_INVALID_ARG;
     DensifyStatsArgs a;
     a.status = frame->status; a.grad2d = frame->grad2d; a.accum = accum; a.count = count;
-    a.P = frame->P; a.W = frame->width; a.H = frame->height;
+    a.pay0 = (const float4*)frame->pay0; a.pay1 = (const float4*)frame->pay1; a.pay3 = frame->pay3;
+    a.P = frame->P; a.W = frame->width; a.H = frame->height; a.kernel = frame->kernel;
     return cuda_status(launch_densify_stats(a, (cudaStream_t)stream));
 }
 

@@ -184,10 +184,12 @@ cudaError_t launch_reset(float* params, int64_t P, int plane, float cap, int mod
 
 struct DensifyStatsArgs {
     const uint8_t* status;
-    const float* grad2d;              // the frame's [P][12] records after S5a (du, dv at 0, 1)
+    const float* grad2d;              // the frame's [P][12] raw-moment records after S5a
+    const float4 *pay0, *pay1;        // S1 payload: conic a, b (pay0.zw), c, kappa (pay1.xy)
+    const float* pay3;                // beta / 2 (exact kernel)
     float *accum, *count;             // [P]
     int64_t P;
-    int W, H;
+    int W, H, kernel;
 };
 cudaError_t launch_densify_stats(const DensifyStatsArgs& a, cudaStream_t stream);
 

@@ -127,14 +127,25 @@ __device__ __forceinline__ void particle_bwd_one(const ParticleBwdArgs& a, int i
         const float det = A * C - B * B;
         const float idet = 1.f / det, idet2 = idet * idet;
 
-        // ---- incoming 2-D gradients (pre-scaled conic -> a, b, c) ----
-        // 12-float record (du, dv, dA, dB | dC, dkappa, dr, dg | db, -, -, -), zeroed
-        // after reading so the buffer is clean for the next frame's backward
+        // ---- incoming 2-D gradients ----
+        // 12-float record of S5a's raw moments over the particle's composited pixels
+        // (q = G dL/dalpha): (sum q dx, sum q dy, sum q dx^2, sum q dx dy | sum q dy^2,
+        // dL/dkappa, dr, dg | db, Sb, -, -), zeroed after reading so the buffer is
+        // clean for the next frame's backward.  With p2 = A' dx^2 + B' dx dy + C' dy^2
+        // (the log2-scaled conic A' = -1/2 log2e a, B' = -log2e b, C' = -1/2 log2e c)
+        // and dL/dp2 = kl q (kl = kappa ln2; exact kernel kappa beta / 4):
+        // dL/du = kl (2 A' sum q dx + B' sum q dy), dL/dv = kl (B' sum q dx + 2 C' sum q dy),
+        // dL/dA' = kl sum q dx^2, dL/dB' = kl sum q dx dy, dL/dC' = kl sum q dy^2.
         const float4 r0 = in.r0, r1 = in.r1, r2 = in.r2;
-        const float du = r0.x, dv = r0.y;
-        const float da = r0.z * (-0.5f * kLog2e);
-        const float db = r0.w * (-kLog2e);
-        const float dc = r1.x * (-0.5f * kLog2e);
+        const float kap = 1.f / (1.f + expf(-in.logit));
+        const bool exact = a.kernel == GES_KERNEL_EXACT_BETA;
+        const float kl = exact ? kap * (0.25f * in.beta) : kap * 0.69314718055994531f;
+        const float cA = (C * idet) * (-0.5f * kLog2e), cB = (-B * idet) * (-kLog2e), cC = (A * idet) * (-0.5f * kLog2e);
+        const float E = kl * r0.x, F = kl * r0.y;
+        const float du = 2.f * cA * E + cB * F, dv = cB * E + 2.f * cC * F;
+        const float da = (kl * r0.z) * (-0.5f * kLog2e);
+        const float db = (kl * r0.w) * (-kLog2e);
+        const float dc = (kl * r1.x) * (-0.5f * kLog2e);
         const float dk = r1.y;
         drgb[0] = r1.z; drgb[1] = r1.w; drgb[2] = r2.x;
 
@@ -178,8 +189,9 @@ __device__ __forceinline__ void particle_bwd_one(const ParticleBwdArgs& a, int i
             o_ls[k] = dse[k] * se[k];
             dbeta += dse[k] * s[k] * dm_dbeta;
         }
-        // exact GEF kernel: beta enters through Eq. 2's exponent only (record[9])
-        o_beta = a.kernel == GES_KERNEL_EXACT_BETA ? r2.y : dbeta;
+        // exact GEF kernel: beta enters through Eq. 2's exponent only,
+        // dL/dbeta = -1/4 kappa ln2 Sb (record[9])
+        o_beta = exact ? (-0.25f * 0.69314718055994531f) * kap * r2.y : dbeta;
         float dq[4];
         dq[0] = dR[1] * (-2.f * z) + dR[2] * (2.f * y) + dR[3] * (2.f * z) + dR[5] * (-2.f * x) + dR[6] * (-2.f * y) + dR[7] * (2.f * x);
         dq[1] = dR[1] * (2.f * y) + dR[2] * (2.f * z) + dR[3] * (2.f * y) + dR[4] * (-4.f * x) + dR[5] * (-2.f * w) +
@@ -231,7 +243,6 @@ __device__ __forceinline__ void particle_bwd_one(const ParticleBwdArgs& a, int i
         dmean[2] += (gz - uz * dotd) * idn;
 #pragma unroll
         for (int k = 0; k < 3; ++k) o_mean[k] = dmean[k];
-        const float kap = 1.f / (1.f + expf(-in.logit));
         o_op = dk * kap * (1.f - kap);
     }  // vis
 #pragma unroll

@@ -543,18 +543,17 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
                 Sb += GQ * ge.L;
                 T[k] = Tk;
             }
-            const float kl = g1.y * 0.5f * hb;  // dL/dp2 = kl wm
-            const float E = kl * dx * S0, F = kl * S1;
-            v[0] = 2.0f * g0.z * E + g0.w * F;
-            v[1] = g0.w * E + 2.0f * g1.x * F;
-            v[2] = dx * E;
-            v[3] = dx * F;
-            v[4] = kl * S2;
+            // raw moments (dL/dp2 = kappa hb / 2 wm; S5b applies the per-particle factors)
+            v[0] = dx * S0;
+            v[1] = S1;
+            v[2] = dx * v[0];
+            v[3] = dx * S1;
+            v[4] = S2;
             v[5] = dk;
             v[6] = dr;
             v[7] = dgc;
             v[8] = dbc;
-            v[NV - 1] = -0.25f * 0.69314718055994531f * g1.y * Sb;  // (NV = 10) d L / d beta
+            v[NV - 1] = Sb;  // (NV = 10) d L / d beta = -1/4 kappa ln2 Sb
             } else {
             float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, dr = 0.0f, dgc = 0.0f, dbc = 0.0f;
             if (!(g1.y > kAlphaMax)) {  // warp-uniform: alpha cannot reach the 0.99 clamp
@@ -608,14 +607,15 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
                     T[k] = Tk;
                 }
             }
-            // alpha = kappa 2^p2: d alpha / d p2 = alpha ln 2, so dL/dp2 = kappa ln2 q
-            const float kl = g1.y * 0.69314718055994531f;
-            const float E = kl * dx * S0, F = kl * S1;  // sum dp2 dx, sum dp2 dy
-            v[0] = 2.0f * g0.z * E + g0.w * F;   // d p2 / d u
-            v[1] = g0.w * E + 2.0f * g1.x * F;   // d p2 / d v
-            v[2] = dx * E;                       // d p2 / d A
-            v[3] = dx * F;                       // d p2 / d B
-            v[4] = kl * S2;                      // d p2 / d C
+            // alpha = kappa 2^p2: d alpha / d p2 = alpha ln 2, so dL/dp2 = kappa ln2 q.
+            // The record takes the raw moments sum q (dx, dy, dx^2, dx dy, dy^2):
+            // every factor that turns them into dL/d(u, v, A, B, C) is constant per
+            // particle (kappa, the conic), so S5b applies it once after the sum.
+            v[0] = dx * S0;                      // sum q dx
+            v[1] = S1;                           // sum q dy
+            v[2] = dx * v[0];                    // sum q dx^2
+            v[3] = dx * S1;                      // sum q dx dy
+            v[4] = S2;                           // sum q dy^2
             v[5] = S0;                           // d alpha-part of d L / d kappa
             v[6] = dr;
             v[7] = dgc;

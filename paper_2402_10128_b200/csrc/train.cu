@@ -95,7 +95,13 @@ cudaError_t launch_reset(float* params, int64_t P, int plane, float cap, int mod
 __global__ void densify_stats_kernel(DensifyStatsArgs a) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= a.P || a.status[i] != GES_VISIBLE) return;
-    const float du = a.grad2d[(size_t)i * kGrad2dStride], dv = a.grad2d[(size_t)i * kGrad2dStride + 1];
+    // dL/du, dL/dv from S5a's raw moments (record layout: ges.h, particle_bwd.cu)
+    const float m1 = a.grad2d[(size_t)i * kGrad2dStride], s1 = a.grad2d[(size_t)i * kGrad2dStride + 1];
+    const float4 p0 = a.pay0[i], p1 = a.pay1[i];
+    const float kl = a.kernel == GES_KERNEL_EXACT_BETA ? p1.y * 0.5f * a.pay3[i] : p1.y * 0.69314718055994531f;
+    const float cA = p0.z * (-0.5f * kLog2e), cB = p0.w * (-kLog2e), cC = p1.x * (-0.5f * kLog2e);
+    const float E = kl * m1, F = kl * s1;
+    const float du = 2.f * cA * E + cB * F, dv = cB * E + 2.f * cC * F;
     const float gx = du * 0.5f * (float)a.W, gy = dv * 0.5f * (float)a.H;  // NDC units
     a.accum[i] += sqrtf(gx * gx + gy * gy);
     a.count[i] += 1.0f;

@@ -327,3 +327,22 @@ def test_screen_tile_bands_match_full_frame(world):
         floor = 1e-6 + 1e-6 * np.abs(g_full[n]).max()
         bad = np.abs(a - g_full[n]) > np.maximum(1e-3 * np.abs(g_full[n]), floor)
         assert bad.sum() == 0, (n, int(bad.sum()))
+
+
+@pytest.mark.parametrize("case", ["cfg4_camera", "wide_4096"])
+def test_binning_over_several_tile_windows(case):
+    """The binning kernels walk the tile grid in windows of <= 6144 tiles (one
+    shared-memory cursor table each).  Frames with more tiles than
+    one window -- config 4's 1600x1064 camera (2 windows) and a 4096-wide frame
+    (3 windows of 24 tile rows) -- must give the same bit-exact lists, ranges and
+    images as the oracle, including tiles on the window seams."""
+    if case == "cfg4_camera":
+        sc = gi.make_config(4, P=150000, n_views=1)
+        cam = sc.cameras[0]
+    else:
+        sc = gi.make_config(1, P=40000)
+        c0 = sc.cameras[0]
+        cam = gi.Camera(4096, 1024, 900.0, 900.0, 2048.0, 512.0, 0.2, c0.R, c0.t)
+    gs, osx = settings_pair(rho=sc.rho)
+    assert ((cam.width + 15) // 16) * ((cam.height + 15) // 16) > 6144
+    run_case(sc.particles, cam, gs, osx, gi.upstream_grad(sc.seed, 4, cam.width, cam.height))
