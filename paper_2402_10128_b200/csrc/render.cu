@@ -19,10 +19,10 @@
 // exactly the ones every pixel of the region would skip: results are
 // identical to the unculled loop.  __syncthreads_count retires the tile once
 // all pixels have terminated.  The backward walks the same lists back to
-// front from the last composited entry of each warp and reduces the nine
-// per-pair gradients across the warp with an uneven recursive-halving shuffle
-// (12 SHFL per warp and entry), then nine lanes add them (red.global.add.f32)
-// into the particle's 12-float gradient record.
+// front from the last composited entry of each warp and reduces the per-pair
+// gradient moments across the warp with a column-aware recursive-halving
+// shuffle (9 SHFL per warp and entry, grad_reduce), then nine lanes add them
+// (red.global.add.f32) into the particle's 12-float raw-moment record.
 #include <cstdlib>
 
 #include "ges_internal.h"
@@ -366,49 +366,53 @@ cudaError_t launch_render_fwd(const RenderFwdArgs& a, cudaStream_t stream) {
 // ---------------------------------------------------------------------------
 // S5a backward
 // ---------------------------------------------------------------------------
-// Warp sum of the NV (9, or 10 with the exact kernel's dbeta) per-pair
-// gradient components by recursive halving over uneven component sets: xor 16
-// splits {0-4 | 5-(NV-1)} (5 SHFL), xor 8 splits the remaining slots {0-2 |
-// 3-4} (3), xor 4 {0-1 | 2} (2), xor 2 (1), xor 1 (1): 12 shuffles.
-// Afterwards lanes l and l^1 hold the full sum of component
-// reduce_component<NV>(l) (or -1: no component).
-template <int NV>
-__device__ __forceinline__ int reduce_component(int lane) {
-    const int i2 = ((lane & 4) ? 2 : 0) + ((lane & 2) ? 1 : 0);
-    const int i1 = ((lane & 8) ? 3 : 0) + i2;
-    const bool hi = (lane & 16) != 0;
-    if (i2 > 2 || i1 > (hi ? NV - 6 : 4)) return -1;
-    return (hi ? 5 : 0) + i1;
+// Warp sum of the per-pair gradient terms.  Each lane holds its pixels' sums
+// S0 = sum q, S1 = sum q dy, S2 = sum q dy^2 and the colour terms (exact
+// kernel: + dk, Sb); the record wants sum q dx and sum q dx^2, sum q dx dy too.
+// Lanes l, l^8, l^16, l^24 share a pixel column (dx), so the first two
+// recursive-halving levels (xor 16, xor 8) sum the column's lanes, the column
+// moments are formed once per column (dx S0, dx^2 S0, dx S1), and the last three
+// levels (xor 4, 2, 1) sum the 8 columns:
+//   xor 16: lo {S0, S1, S2, dk} | hi {db, dr, dg, Sb}        4 SHFL (Gaussian 3)
+//   xor 8:  lo {., dk | db, Sb} | hi {S1, S2 | dr, dg}       2
+//   groups (bit 16, bit 8): 00 {dk, dx S0, dx^2 S0}, 01 {S1, S2, dx S1},
+//           10 {db, Sb}, 11 {dr, dg}   (Gaussian: dk = S0, no Sb)
+//   xor 4: {slot 0, 1 | slot 2} 2, xor 2: 1, xor 1: 1  -> 10 SHFL (Gaussian 9)
+// Afterwards lanes l and l^1 hold the full sum of record component
+// record_component<EXACT>(l) (or -1: none).
+template <bool EXACT>
+__device__ __forceinline__ int record_component(int lane) {
+    const int g = ((lane >> 3) & 3);           // bit 16 -> 2, bit 8 -> 1
+    const int slot = ((lane & 4) ? 2 : 0) + ((lane & 2) ? 1 : 0);
+    // record: 0 sum q dx, 1 sum q dy, 2 sum q dx^2, 3 sum q dx dy, 4 sum q dy^2,
+    //         5 dL/dkappa, 6 dr, 7 dg, 8 db, 9 Sb
+    constexpr int kMap[4][4] = {{5, 0, 2, -1}, {1, 4, 3, -1}, {8, EXACT ? 9 : -1, -1, -1}, {6, 7, -1, -1}};
+    return kMap[g][slot];
 }
 
-template <int NV>
-__device__ __forceinline__ float warp_reduce(const float (&v)[NV]) {
-    static_assert(NV == 9 || NV == 10, "9 or 10 components");
+template <bool EXACT>
+__device__ __forceinline__ float grad_reduce(float S0, float S1, float S2, float dk, float Sb, float dr, float dg,
+                                             float db, float dx) {
     const int lane = threadIdx.x & 31;
     const bool u16 = (lane & 16) != 0, u8 = (lane & 8) != 0, u4 = (lane & 4) != 0, u2 = (lane & 2) != 0;
-    float w[6];
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-        const float lo = v[i], hi = (5 + i < NV) ? v[5 + i] : 0.0f;
-        w[i] = (u16 ? hi : lo) + __shfl_xor_sync(0xffffffffu, u16 ? lo : hi, 16);
-    }
-    w[5] = 0.0f;
-    float x[4];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        const float lo = w[i], hi = w[3 + i];
-        x[i] = (u8 ? hi : lo) + __shfl_xor_sync(0xffffffffu, u8 ? lo : hi, 8);
-    }
-    x[3] = 0.0f;
-    float y[2];
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const float lo = x[i], hi = x[2 + i];
-        y[i] = (u4 ? hi : lo) + __shfl_xor_sync(0xffffffffu, u4 ? lo : hi, 4);
-    }
-    float z = (u2 ? y[1] : y[0]) + __shfl_xor_sync(0xffffffffu, u2 ? y[0] : y[1], 2);
-    z += __shfl_xor_sync(0xffffffffu, z, 1);
-    return z;
+    constexpr unsigned kAll = 0xffffffffu;
+    const float a0 = (u16 ? db : S0) + __shfl_xor_sync(kAll, u16 ? S0 : db, 16);
+    const float a1 = (u16 ? dr : S1) + __shfl_xor_sync(kAll, u16 ? S1 : dr, 16);
+    const float a2 = (u16 ? dg : S2) + __shfl_xor_sync(kAll, u16 ? S2 : dg, 16);
+    float a3 = 0.0f;
+    if (EXACT) a3 = (u16 ? Sb : dk) + __shfl_xor_sync(kAll, u16 ? dk : Sb, 16);
+    const float b0 = (u8 ? a1 : a0) + __shfl_xor_sync(kAll, u8 ? a0 : a1, 8);
+    const float b1 = (u8 ? a2 : a3) + __shfl_xor_sync(kAll, u8 ? a3 : a2, 8);
+    const bool g00 = !u16 && !u8, g01 = !u16 && u8;
+    const float t = dx * b0;  // column moment dx S (S0 in group 00, S1 in 01)
+    const float c0 = (EXACT && g00) ? b1 : b0;
+    const float c1 = g00 ? t : b1;
+    const float c2 = g00 ? dx * t : (g01 ? t : 0.0f);
+    const float d0 = (u4 ? c2 : c0) + __shfl_xor_sync(kAll, u4 ? c0 : c2, 4);
+    const float d1 = (u4 ? 0.0f : c1) + __shfl_xor_sync(kAll, u4 ? c1 : 0.0f, 4);
+    float e = (u2 ? d1 : d0) + __shfl_xor_sync(kAll, u2 ? d0 : d1, 2);
+    e += __shfl_xor_sync(kAll, e, 1);
+    return e;
 }
 
 __device__ __forceinline__ void red_add(float* addr, float x) {
@@ -418,7 +422,6 @@ __device__ __forceinline__ void red_add(float* addr, float x) {
 template <int PPT, bool EXACT>
 __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdArgs a) {
     using Lt = Layout<PPT>;
-    constexpr int NV = EXACT ? 10 : 9;  // + Eq. 2's direct dL/dbeta
     __shared__ float4 s_g0[kBatch];
     __shared__ float4 s_g1[kBatch];
     __shared__ float s_b[kBatch];
@@ -468,7 +471,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
     // the largest `last` among the warp's inactive pixels: the walk (positions
     // descending) activates them when it passes below it
     uint32_t nxt = warp_max;
-    const int red_comp = reduce_component<NV>(lane);
+    const int red_comp = record_component<EXACT>(lane);
     StagedBatch sb{s_g0, s_g1, s_b, s_pid, s_mask, s_hb};
     for (int32_t b_end = (int32_t)max_last; b_end > 0; b_end -= kBatch) {
         const int32_t b_begin = max(0, b_end - kBatch);
@@ -503,10 +506,9 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             // S2 = sum q dy^2 suffice.  alpha' = alpha where the pixel composites
             // this entry (alpha >= thr: active and not skipped), else 0; then every
             // term below vanishes without a select.  (No exponent clamp: R19.)
-            float v[NV];
             bool contrib = false;
-            if constexpr (EXACT) {
             float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, dk = 0.0f, Sb = 0.0f, dr = 0.0f, dgc = 0.0f, dbc = 0.0f;
+            if constexpr (EXACT) {
             const float hb = s_hb[j];
             const bool clampk = g1.y > kAlphaMax;  // warp-uniform
             const float rk = fast_rcp(g1.y);
@@ -543,19 +545,9 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
                 Sb += GQ * ge.L;
                 T[k] = Tk;
             }
-            // raw moments (dL/dp2 = kappa hb / 2 wm; S5b applies the per-particle factors)
-            v[0] = dx * S0;
-            v[1] = S1;
-            v[2] = dx * v[0];
-            v[3] = dx * S1;
-            v[4] = S2;
-            v[5] = dk;
-            v[6] = dr;
-            v[7] = dgc;
-            v[8] = dbc;
-            v[NV - 1] = Sb;  // (NV = 10) d L / d beta = -1/4 kappa ln2 Sb
+            // (dL/dp2 = kappa hb / 2 wm, dL/dbeta = -1/4 kappa ln2 Sb: S5b applies the
+            // per-particle factors)
             } else {
-            float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, dr = 0.0f, dgc = 0.0f, dbc = 0.0f;
             if (!(g1.y > kAlphaMax)) {  // warp-uniform: alpha cannot reach the 0.99 clamp
                 const float rk = fast_rcp(g1.y);
 #pragma unroll
@@ -611,18 +603,9 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             // The record takes the raw moments sum q (dx, dy, dx^2, dx dy, dy^2):
             // every factor that turns them into dL/d(u, v, A, B, C) is constant per
             // particle (kappa, the conic), so S5b applies it once after the sum.
-            v[0] = dx * S0;                      // sum q dx
-            v[1] = S1;                           // sum q dy
-            v[2] = dx * v[0];                    // sum q dx^2
-            v[3] = dx * S1;                      // sum q dx dy
-            v[4] = S2;                           // sum q dy^2
-            v[5] = S0;                           // d alpha-part of d L / d kappa
-            v[6] = dr;
-            v[7] = dgc;
-            v[8] = dbc;
             }
             if (__any_sync(0xffffffffu, contrib)) {
-                const float r = warp_reduce<NV>(v);
+                const float r = grad_reduce<EXACT>(S0, S1, S2, dk, Sb, dr, dgc, dbc, dx);
                 if (red_comp >= 0 && (lane & 1) == 0)
                     red_add(a.grad2d + (size_t)s_pid[j] * kGrad2dStride + red_comp, r);
             }
