@@ -160,6 +160,31 @@ __device__ __forceinline__ Gef gef_eval(float p2, float hb) {
     return r;
 }
 
+// Shared-memory loads from 32-bit shared-window addresses computed once per
+// CTA (the compiler otherwise rebuilds each array's address from the CTA id in
+// every iteration of the entry loops).
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ float lds_f(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+    return v;
+}
+
 // Per-warp compaction of the batch entries whose mask has this warp's bit.
 __device__ __forceinline__ int compact_warp_list(const uint8_t* s_mask, int n, int warp, uint16_t* out) {
     const int lane = threadIdx.x & 31;
@@ -251,19 +276,21 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
     }
     constexpr uint32_t kAll = (1u << PPT) - 1u;
     StagedBatch sb{s_g0, s_g1, s_b, nullptr, s_mask, s_hb};
+    const uint32_t a_g0 = smem_addr(s_g0), a_g1 = smem_addr(s_g1), a_b = smem_addr(s_b), a_hb = smem_addr(s_hb);
+    const uint32_t a_list = smem_addr(s_list[warp]);
     for (uint32_t b0 = start; b0 < end; b0 += kBatch) {
         if (__syncthreads_count(done == kAll) == Lt::kThreads) break;
         const int n = (int)min((uint32_t)kBatch, end - b0);
         stage_batch<PPT, EXACT>(a.pay0, a.pay1, a.pay2, a.pay3, a.list, b0, n, tile_x0, tile_y0, sb);
         __syncthreads();
+        if (__all_sync(0xffffffffu, done == kAll)) continue;  // the barrier above retires the tile
         const int nw = compact_warp_list(s_mask, n, warp, s_list[warp]);
         for (int i = 0; i < nw; ++i) {
-            if (__all_sync(0xffffffffu, done == kAll)) break;
-            const int j = s_list[warp][i];
-            const float4 g0 = s_g0[j];
-            const float4 g1 = s_g1[j];
-            const float gbl = s_b[j];
-            const float hb = EXACT ? s_hb[j] : 1.0f;
+            const int j = (int)lds_u16(a_list + 2u * (uint32_t)i);
+            const float4 g0 = lds_f4(a_g0 + 16u * (uint32_t)j);
+            const float4 g1 = lds_f4(a_g1 + 16u * (uint32_t)j);
+            const float gbl = lds_f(a_b + 4u * (uint32_t)j);
+            const float hb = EXACT ? lds_f(a_hb + 4u * (uint32_t)j) : 1.0f;
             const float dx = __fsub_rn(g0.x, fpx);
             const ExpCol ec = exp_col(g0.z, g0.w, dx);
             const uint32_t pos1 = b0 - start + j + 1;
@@ -316,6 +343,7 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
                     thr[k] = stop ? 2.0f : thr[k];
                     done |= (stop ? 1u : 0u) << k;
                 }
+                if (__all_sync(0xffffffffu, done == kAll)) break;  // done changes only here
             }
         }
     }
@@ -473,6 +501,8 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
     uint32_t nxt = warp_max;
     const int red_comp = record_component<EXACT>(lane);
     StagedBatch sb{s_g0, s_g1, s_b, s_pid, s_mask, s_hb};
+    const uint32_t a_g0 = smem_addr(s_g0), a_g1 = smem_addr(s_g1), a_b = smem_addr(s_b), a_hb = smem_addr(s_hb);
+    const uint32_t a_pid = smem_addr(s_pid), a_list = smem_addr(s_list[warp]);
     for (int32_t b_end = (int32_t)max_last; b_end > 0; b_end -= kBatch) {
         const int32_t b_begin = max(0, b_end - kBatch);
         const int n = b_end - b_begin;
@@ -483,7 +513,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
         const int nw_lim = (int)min((int64_t)n, max((int64_t)0, (int64_t)warp_max - b_begin));
         const int nw = compact_warp_list(s_mask, nw_lim, warp, s_list[warp]);
         for (int i = nw - 1; i >= 0; --i) {
-            const int j = s_list[warp][i];
+            const int j = (int)lds_u16(a_list + 2u * (uint32_t)i);
             const uint32_t pos = (uint32_t)(b_begin + j);
             if (pos < nxt) {  // warp-uniform: some pixels start compositing here
                 uint32_t m = 0;
@@ -494,9 +524,9 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
                 }
                 nxt = __reduce_max_sync(0xffffffffu, m);
             }
-            const float4 g0 = s_g0[j];
-            const float4 g1 = s_g1[j];
-            const float rb = s_b[j];
+            const float4 g0 = lds_f4(a_g0 + 16u * (uint32_t)j);
+            const float4 g1 = lds_f4(a_g1 + 16u * (uint32_t)j);
+            const float rb = lds_f(a_b + 4u * (uint32_t)j);
             const float dx = __fsub_rn(g0.x, fpx);
             const ExpCol ec = exp_col(g0.z, g0.w, dx);
             // Per pixel only the sums the chain rule needs: with q = G dalpha (kappa
@@ -509,7 +539,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             bool contrib = false;
             float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, dk = 0.0f, Sb = 0.0f, dr = 0.0f, dgc = 0.0f, dbc = 0.0f;
             if constexpr (EXACT) {
-            const float hb = s_hb[j];
+            const float hb = lds_f(a_hb + 4u * (uint32_t)j);
             const bool clampk = g1.y > kAlphaMax;  // warp-uniform
             const float rk = fast_rcp(g1.y);
             // Eq. 2: G = exp(-1/2 Q^hb).  dG/dp2 = G hb Q^hb / (2 qp) (Q = 2 ln2 qp),
@@ -607,7 +637,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             if (__any_sync(0xffffffffu, contrib)) {
                 const float r = grad_reduce<EXACT>(S0, S1, S2, dk, Sb, dr, dgc, dbc, dx);
                 if (red_comp >= 0 && (lane & 1) == 0)
-                    red_add(a.grad2d + (size_t)s_pid[j] * kGrad2dStride + red_comp, r);
+                    red_add(a.grad2d + (size_t)lds_u32(a_pid + 4u * (uint32_t)j) * kGrad2dStride + red_comp, r);
             }
         }
     }
