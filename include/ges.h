@@ -197,13 +197,15 @@ typedef struct {
     float *final_T;        /* [H*W] transmittance after the last composited particle   */
     uint32_t *n_contrib;   /* [H*W] list position of the last composited particle + 1  */
     float *grad2d;         /* [P][12] per-particle S5a record: raw moments over the
-                              particle's composited pixels, q = G dL/dalpha:
-                              (sum q dx, sum q dy, sum q dx^2, sum q dx dy |
-                              sum q dy^2, dL/dkappa, dr, dg | db, Sb, 0, 0) with
-                              dx = u - px, dy = v - py, Sb = the exact kernel's
-                              sum G dL/dalpha Q^(beta/2) log2 Q; S5b turns them into
-                              dL/d(u, v, conic) with the per-particle factors
-                              (kappa, the conic).  Kept all-zero between backward passes */
+                              particle's composited pixels (dx = u - px, dy = v - py),
+                              (sum m dx, sum m dy, sum m dx^2, sum m dx dy |
+                              sum m dy^2, K, dr, dg | db, Sb, 0, 0); Gaussian kernel
+                              m = kappa G dL/dalpha, K = kappa dL/dkappa; exact kernel
+                              m = G dL/dalpha Q^(beta/2) / qp, K = dL/dkappa, Sb =
+                              sum G dL/dalpha Q^(beta/2) log2 Q.  S5b turns them into
+                              dL/d(u, v, conic, kappa) with the per-particle factors
+                              (kappa, beta, the conic).  Kept all-zero between backward
+                              passes */
     size_t workspace_bytes;
 } ges_frame;
 

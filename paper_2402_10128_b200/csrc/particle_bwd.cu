@@ -128,25 +128,26 @@ __device__ __forceinline__ void particle_bwd_one(const ParticleBwdArgs& a, int i
         const float idet = 1.f / det, idet2 = idet * idet;
 
         // ---- incoming 2-D gradients ----
-        // 12-float record of S5a's raw moments over the particle's composited pixels
-        // (q = G dL/dalpha): (sum q dx, sum q dy, sum q dx^2, sum q dx dy | sum q dy^2,
-        // dL/dkappa, dr, dg | db, Sb, -, -), zeroed after reading so the buffer is
-        // clean for the next frame's backward.  With p2 = A' dx^2 + B' dx dy + C' dy^2
-        // (the log2-scaled conic A' = -1/2 log2e a, B' = -log2e b, C' = -1/2 log2e c)
-        // and dL/dp2 = kl q (kl = kappa ln2; exact kernel kappa beta / 4):
-        // dL/du = kl (2 A' sum q dx + B' sum q dy), dL/dv = kl (B' sum q dx + 2 C' sum q dy),
-        // dL/dA' = kl sum q dx^2, dL/dB' = kl sum q dx dy, dL/dC' = kl sum q dy^2.
+        // 12-float record of S5a's raw moments over the particle's composited pixels,
+        // (sum m dx, sum m dy, sum m dx^2, sum m dx dy | sum m dy^2, K, dr, dg | db, Sb, -, -),
+        // zeroed after reading so the buffer is clean for the next frame's backward.
+        // Gaussian kernel: m = kappa G dL/dalpha, dL/dp2 = ln2 m, K = kappa dL/dkappa;
+        // exact kernel: m = G dL/dalpha Q^hb / qp, dL/dp2 = kappa beta / 4 m, K = dL/dkappa.
+        // With p2 = A' dx^2 + B' dx dy + C' dy^2 (the log2-scaled conic A' = -1/2 log2e a,
+        // B' = -log2e b, C' = -1/2 log2e c) and dL/dp2 = kl m:
+        // dL/du = kl (2 A' sum m dx + B' sum m dy), dL/dv = kl (B' sum m dx + 2 C' sum m dy),
+        // dL/dA' = kl sum m dx^2, dL/dB' = kl sum m dx dy, dL/dC' = kl sum m dy^2.
         const float4 r0 = in.r0, r1 = in.r1, r2 = in.r2;
         const float kap = 1.f / (1.f + expf(-in.logit));
         const bool exact = a.kernel == GES_KERNEL_EXACT_BETA;
-        const float kl = exact ? kap * (0.25f * in.beta) : kap * 0.69314718055994531f;
+        const float kl = exact ? kap * (0.25f * in.beta) : 0.69314718055994531f;
         const float cA = (C * idet) * (-0.5f * kLog2e), cB = (-B * idet) * (-kLog2e), cC = (A * idet) * (-0.5f * kLog2e);
         const float E = kl * r0.x, F = kl * r0.y;
         const float du = 2.f * cA * E + cB * F, dv = cB * E + 2.f * cC * F;
         const float da = (kl * r0.z) * (-0.5f * kLog2e);
         const float db = (kl * r0.w) * (-kLog2e);
         const float dc = (kl * r1.x) * (-0.5f * kLog2e);
-        const float dk = r1.y;
+        const float dk = exact ? r1.y : r1.y / kap;
         drgb[0] = r1.z; drgb[1] = r1.w; drgb[2] = r2.x;
 
         // conic -> (A, B, C)

@@ -578,15 +578,17 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             // (dL/dp2 = kappa hb / 2 wm, dL/dbeta = -1/4 kappa ln2 Sb: S5b applies the
             // per-particle factors)
             } else {
+            // The Gaussian path accumulates kappa q = alpha' dL/dalpha (kappa, a
+            // per-particle constant, is divided out in S5b).
+            float amax = 0.0f;
             if (!(g1.y > kAlphaMax)) {  // warp-uniform: alpha cannot reach the 0.99 clamp
-                const float rk = fast_rcp(g1.y);
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) {
                     const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
                     const float G = fast_exp2(raw_exponent(ec, g1.x, dy));
                     const float alpha = __fmul_rn(g1.y, G);
                     const float al = alpha >= thr[k] ? alpha : 0.0f;
-                    contrib |= al > 0.0f;
+                    amax = fmaxf(amax, al);
                     const float inv_om = fast_rcp(__fsub_rn(1.0f, al));
                     const float Tk = T[k] * inv_om;  // transmittance before this entry
                     const float cgk = g1.z * gr[k] + g1.w * gg[k] + rb * gb[k];
@@ -596,7 +598,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
                     dr += w * gr[k];
                     dgc += w * gg[k];
                     dbc += w * gb[k];
-                    const float q = (al * rk) * dalpha;  // G dL/dalpha where composited
+                    const float q = al * dalpha;  // kappa G dL/dalpha where composited
                     S0 += q;
                     const float t = q * dy;
                     S1 += t;
@@ -611,7 +613,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
                     const float araw = __fmul_rn(g1.y, G);
                     const float alpha = fminf(kAlphaMax, araw);
                     const float al = alpha >= thr[k] ? alpha : 0.0f;
-                    contrib |= al > 0.0f;
+                    amax = fmaxf(amax, al);
                     const float inv_om = fast_rcp(__fsub_rn(1.0f, al));
                     const float Tk = T[k] * inv_om;
                     const float cgk = g1.z * gr[k] + g1.w * gg[k] + rb * gb[k];
@@ -621,7 +623,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
                     dr += w * gr[k];
                     dgc += w * gg[k];
                     dbc += w * gb[k];
-                    const float q = (al > 0.0f && araw < kAlphaMax) ? G * dalpha : 0.0f;
+                    const float q = (al > 0.0f && araw < kAlphaMax) ? araw * dalpha : 0.0f;
                     S0 += q;
                     const float t = q * dy;
                     S1 += t;
@@ -629,10 +631,11 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
                     T[k] = Tk;
                 }
             }
-            // alpha = kappa 2^p2: d alpha / d p2 = alpha ln 2, so dL/dp2 = kappa ln2 q.
-            // The record takes the raw moments sum q (dx, dy, dx^2, dx dy, dy^2):
-            // every factor that turns them into dL/d(u, v, A, B, C) is constant per
-            // particle (kappa, the conic), so S5b applies it once after the sum.
+            // alpha = kappa 2^p2: d alpha / d p2 = alpha ln 2, so dL/dp2 = ln2 (kappa q).
+            // The record takes the raw moments sum kappa q (dx, dy, dx^2, dx dy, dy^2):
+            // every factor that turns them into dL/d(u, v, A, B, C, kappa) is constant
+            // per particle (kappa, the conic), so S5b applies it once after the sum.
+            contrib = amax > 0.0f;
             }
             if (__any_sync(0xffffffffu, contrib)) {
                 const float r = grad_reduce<EXACT>(S0, S1, S2, dk, Sb, dr, dgc, dbc, dx);

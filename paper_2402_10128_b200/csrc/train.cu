@@ -98,7 +98,7 @@ __global__ void densify_stats_kernel(DensifyStatsArgs a) {
     // dL/du, dL/dv from S5a's raw moments (record layout: ges.h, particle_bwd.cu)
     const float m1 = a.grad2d[(size_t)i * kGrad2dStride], s1 = a.grad2d[(size_t)i * kGrad2dStride + 1];
     const float4 p0 = a.pay0[i], p1 = a.pay1[i];
-    const float kl = a.kernel == GES_KERNEL_EXACT_BETA ? p1.y * 0.5f * a.pay3[i] : p1.y * 0.69314718055994531f;
+    const float kl = a.kernel == GES_KERNEL_EXACT_BETA ? p1.y * 0.5f * a.pay3[i] : 0.69314718055994531f;
     const float cA = p0.z * (-0.5f * kLog2e), cB = p0.w * (-kLog2e), cC = p1.x * (-0.5f * kLog2e);
     const float E = kl * m1, F = kl * s1;
     const float du = 2.f * cA * E + cB * F, dv = cB * E + 2.f * cC * F;
