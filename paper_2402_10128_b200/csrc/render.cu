@@ -23,6 +23,7 @@
 // gradient moments across the warp with a column-aware recursive-halving
 // shuffle (9 SHFL per warp and entry, grad_reduce), then nine lanes add them
 // (red.global.add.f32) into the particle's 12-float raw-moment record.
+#include <cstddef>
 #include <cstdlib>
 
 #include "ges_internal.h"
@@ -164,6 +165,25 @@ __device__ __forceinline__ Gef gef_eval(float p2, float hb) {
 // CTA (the compiler otherwise rebuilds each array's address from the CTA id in
 // every iteration of the entry loops).
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+template <int OFF>
+__device__ __forceinline__ float4 lds_f4_at(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+%5];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a), "n"(OFF));
+    return v;
+}
+template <int OFF>
+__device__ __forceinline__ float lds_f_at(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF));
+    return v;
+}
+template <int OFF>
+__device__ __forceinline__ uint32_t lds_u32_at(uint32_t a) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(a), "n"(OFF));
+    return v;
+}
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {
     float4 v;
     asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -245,15 +265,28 @@ __device__ __forceinline__ void stage_batch(const float4* pay0, const float4* pa
     }
 }
 
+// One shared-memory block per CTA: the staged batch at compile-time offsets, so
+// an entry's fields are one base register + an immediate (ld.shared [r+imm]).
+template <int PPT, bool EXACT>
+struct RenderSmem {
+    float4 g0[kBatch];  // u, v, A, B
+    float4 g1[kBatch];  // C, kappa, r, g
+    float b[kBatch];
+    uint32_t pid[kBatch];
+    float hb[EXACT ? kBatch : 1];
+    uint16_t list[Layout<PPT>::kWarps][kBatch];
+    uint8_t mask[kBatch];
+    uint32_t max;
+    static constexpr int kG1 = kBatch * 16, kB = kBatch * 32, kPid = kBatch * 36, kHb = kBatch * 40;
+};
+
 template <int PPT, bool DIAG, bool EXACT>
 __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdArgs a) {
     using Lt = Layout<PPT>;
-    __shared__ float4 s_g0[kBatch];
-    __shared__ float4 s_g1[kBatch];
-    __shared__ float s_b[kBatch];
-    __shared__ float s_hb[EXACT ? kBatch : 1];
-    __shared__ uint8_t s_mask[kBatch];
-    __shared__ uint16_t s_list[Lt::kWarps][kBatch];
+    using Sm = RenderSmem<PPT, EXACT>;
+    __shared__ Sm S;
+    static_assert(offsetof(Sm, g1) == Sm::kG1 && offsetof(Sm, b) == Sm::kB && offsetof(Sm, pid) == Sm::kPid &&
+                  offsetof(Sm, hb) == Sm::kHb, "smem layout");
     const int tile = blockIdx.x;
     const int tid = threadIdx.x, warp = tid >> 5;
     int px, py0;
@@ -275,22 +308,23 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
         if (!(px < a.W && py0 + 4 * k < a.H)) { done |= 1u << k; thr[k] = 2.0f; }
     }
     constexpr uint32_t kAll = (1u << PPT) - 1u;
-    StagedBatch sb{s_g0, s_g1, s_b, nullptr, s_mask, s_hb};
-    const uint32_t a_g0 = smem_addr(s_g0), a_g1 = smem_addr(s_g1), a_b = smem_addr(s_b), a_hb = smem_addr(s_hb);
-    const uint32_t a_list = smem_addr(s_list[warp]);
+    StagedBatch sb{S.g0, S.g1, S.b, nullptr, S.mask, S.hb};
+    const uint32_t sbase = smem_addr(&S);
+    const uint32_t a_list = smem_addr(S.list[warp]);
     for (uint32_t b0 = start; b0 < end; b0 += kBatch) {
         if (__syncthreads_count(done == kAll) == Lt::kThreads) break;
         const int n = (int)min((uint32_t)kBatch, end - b0);
         stage_batch<PPT, EXACT>(a.pay0, a.pay1, a.pay2, a.pay3, a.list, b0, n, tile_x0, tile_y0, sb);
         __syncthreads();
         if (__all_sync(0xffffffffu, done == kAll)) continue;  // the barrier above retires the tile
-        const int nw = compact_warp_list(s_mask, n, warp, s_list[warp]);
+        const int nw = compact_warp_list(S.mask, n, warp, S.list[warp]);
         for (int i = 0; i < nw; ++i) {
             const int j = (int)lds_u16(a_list + 2u * (uint32_t)i);
-            const float4 g0 = lds_f4(a_g0 + 16u * (uint32_t)j);
-            const float4 g1 = lds_f4(a_g1 + 16u * (uint32_t)j);
-            const float gbl = lds_f(a_b + 4u * (uint32_t)j);
-            const float hb = EXACT ? lds_f(a_hb + 4u * (uint32_t)j) : 1.0f;
+            const uint32_t r16 = sbase + 16u * (uint32_t)j, r4 = sbase + 4u * (uint32_t)j;
+            const float4 g0 = lds_f4_at<0>(r16);
+            const float4 g1 = lds_f4_at<Sm::kG1>(r16);
+            const float gbl = lds_f_at<Sm::kB>(r4);
+            const float hb = EXACT ? lds_f_at<Sm::kHb>(r4) : 1.0f;
             const float dx = __fsub_rn(g0.x, fpx);
             const ExpCol ec = exp_col(g0.z, g0.w, dx);
             const uint32_t pos1 = b0 - start + j + 1;
@@ -450,14 +484,8 @@ __device__ __forceinline__ void red_add(float* addr, float x) {
 template <int PPT, bool EXACT>
 __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdArgs a) {
     using Lt = Layout<PPT>;
-    __shared__ float4 s_g0[kBatch];
-    __shared__ float4 s_g1[kBatch];
-    __shared__ float s_b[kBatch];
-    __shared__ float s_hb[EXACT ? kBatch : 1];
-    __shared__ uint32_t s_pid[kBatch];
-    __shared__ uint8_t s_mask[kBatch];
-    __shared__ uint16_t s_list[Lt::kWarps][kBatch];
-    __shared__ uint32_t s_max;
+    using Sm = RenderSmem<PPT, EXACT>;
+    __shared__ Sm S;
     const int tile = blockIdx.x;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int px, py0;
@@ -490,19 +518,19 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
         U[k] = Tfin * (gr[k] * a.bg[0] + gg[k] * a.bg[1] + gb[k] * a.bg[2]);
         my_max = max(my_max, last[k]);
     }
-    if (tid == 0) s_max = 0;
+    if (tid == 0) S.max = 0;
     __syncthreads();
     const uint32_t warp_max = __reduce_max_sync(0xffffffffu, my_max);
-    if (lane == 0 && warp_max) atomicMax(&s_max, warp_max);
+    if (lane == 0 && warp_max) atomicMax(&S.max, warp_max);
     __syncthreads();
-    const uint32_t max_last = s_max;
+    const uint32_t max_last = S.max;
     // the largest `last` among the warp's inactive pixels: the walk (positions
     // descending) activates them when it passes below it
     uint32_t nxt = warp_max;
     const int red_comp = record_component<EXACT>(lane);
-    StagedBatch sb{s_g0, s_g1, s_b, s_pid, s_mask, s_hb};
-    const uint32_t a_g0 = smem_addr(s_g0), a_g1 = smem_addr(s_g1), a_b = smem_addr(s_b), a_hb = smem_addr(s_hb);
-    const uint32_t a_pid = smem_addr(s_pid), a_list = smem_addr(s_list[warp]);
+    StagedBatch sb{S.g0, S.g1, S.b, S.pid, S.mask, S.hb};
+    const uint32_t sbase = smem_addr(&S);
+    const uint32_t a_list = smem_addr(S.list[warp]);
     for (int32_t b_end = (int32_t)max_last; b_end > 0; b_end -= kBatch) {
         const int32_t b_begin = max(0, b_end - kBatch);
         const int n = b_end - b_begin;
@@ -511,7 +539,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
         __syncthreads();
         // this warp's pixels composite nothing at or behind list position warp_max
         const int nw_lim = (int)min((int64_t)n, max((int64_t)0, (int64_t)warp_max - b_begin));
-        const int nw = compact_warp_list(s_mask, nw_lim, warp, s_list[warp]);
+        const int nw = compact_warp_list(S.mask, nw_lim, warp, S.list[warp]);
         for (int i = nw - 1; i >= 0; --i) {
             const int j = (int)lds_u16(a_list + 2u * (uint32_t)i);
             const uint32_t pos = (uint32_t)(b_begin + j);
@@ -524,9 +552,10 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
                 }
                 nxt = __reduce_max_sync(0xffffffffu, m);
             }
-            const float4 g0 = lds_f4(a_g0 + 16u * (uint32_t)j);
-            const float4 g1 = lds_f4(a_g1 + 16u * (uint32_t)j);
-            const float rb = lds_f(a_b + 4u * (uint32_t)j);
+            const uint32_t r16 = sbase + 16u * (uint32_t)j, r4 = sbase + 4u * (uint32_t)j;
+            const float4 g0 = lds_f4_at<0>(r16);
+            const float4 g1 = lds_f4_at<Sm::kG1>(r16);
+            const float rb = lds_f_at<Sm::kB>(r4);
             const float dx = __fsub_rn(g0.x, fpx);
             const ExpCol ec = exp_col(g0.z, g0.w, dx);
             // Per pixel only the sums the chain rule needs: with q = G dalpha (kappa
@@ -539,7 +568,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             bool contrib = false;
             float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, dk = 0.0f, Sb = 0.0f, dr = 0.0f, dgc = 0.0f, dbc = 0.0f;
             if constexpr (EXACT) {
-            const float hb = lds_f(a_hb + 4u * (uint32_t)j);
+            const float hb = lds_f_at<Sm::kHb>(r4);
             const bool clampk = g1.y > kAlphaMax;  // warp-uniform
             const float rk = fast_rcp(g1.y);
             // Eq. 2: G = exp(-1/2 Q^hb).  dG/dp2 = G hb Q^hb / (2 qp) (Q = 2 ln2 qp),
@@ -640,7 +669,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             if (__any_sync(0xffffffffu, contrib)) {
                 const float r = grad_reduce<EXACT>(S0, S1, S2, dk, Sb, dr, dgc, dbc, dx);
                 if (red_comp >= 0 && (lane & 1) == 0)
-                    red_add(a.grad2d + (size_t)lds_u32(a_pid + 4u * (uint32_t)j) * kGrad2dStride + red_comp, r);
+                    red_add(a.grad2d + (size_t)lds_u32_at<Sm::kPid>(r4) * kGrad2dStride + red_comp, r);
             }
         }
     }

@@ -241,8 +241,11 @@ def test_gradient_accumulate():
     g1, grads = gpu_backward(out, cam, gs, dL)
     g2, _ = gpu_backward(out, cam, gs, dL, accumulate=True, grads=grads)
     for n in G.PARAM_NAMES:
-        # float atomics reassociate between the two backward calls
-        assert np.allclose(g2[n], 2 * g1[n], rtol=1e-4, atol=1e-6)
+        # float atomics reassociate between the two backward calls: 1e-4 relative, plus
+        # a floor of 1e-6 of the group's largest entry for sums that cancel (as in the
+        # band test below; a rerun alone moves such entries by ~4e-7 of the maximum)
+        floor = 1e-6 + 1e-6 * np.abs(g1[n]).max()
+        assert np.all(np.abs(g2[n] - 2 * g1[n]) <= np.maximum(1e-4 * np.abs(g1[n]), floor)), n
 
 
 def test_full_size_config3_sampled():
