@@ -30,18 +30,20 @@
 
 namespace ges {
 
-constexpr int kBatch = 512;
+constexpr int kBatch = 512;  // list entries staged per barrier
 // tuning knobs: min resident CTAs per SM (register cap); unset = ptxas's choice
 #ifdef GES_RFWD_MINB
 #define GES_RFWD_LB(t) __launch_bounds__(t, GES_RFWD_MINB)
 #else
 #define GES_RFWD_LB(t) __launch_bounds__(t)
 #endif
+// backward: 9 resident 64-thread CTAs per SM (PPT 4; a 113-register cap, which
+// ptxas meets at 91 without spills) measured 2 % faster than ptxas's own 121
 #ifdef GES_RBWD_MINB
-#define GES_RBWD_LB(t) __launch_bounds__(t, GES_RBWD_MINB)
+#define GES_RBWD_LB(t, ppt) __launch_bounds__(t, GES_RBWD_MINB)
 #else
-#define GES_RBWD_LB(t) __launch_bounds__(t)
-#endif               // list entries staged per barrier
+#define GES_RBWD_LB(t, ppt) __launch_bounds__(t, (ppt) == 4 ? 9 : 1)
+#endif
 constexpr float kCullMargin = 0.01f;      // log2 units (0.7% in alpha)
 
 struct Splat {
@@ -482,7 +484,7 @@ __device__ __forceinline__ void red_add(float* addr, float x) {
 }
 
 template <int PPT, bool EXACT>
-__global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdArgs a) {
+__global__ void GES_RBWD_LB(Layout<PPT>::kThreads, PPT) render_bwd_kernel(RenderBwdArgs a) {
     using Lt = Layout<PPT>;
     using Sm = RenderSmem<PPT, EXACT>;
     __shared__ Sm S;
@@ -666,7 +668,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads) render_bwd_kernel(RenderBwdAr
             // per particle (kappa, the conic), so S5b applies it once after the sum.
             contrib = amax > 0.0f;
             }
-            if (__any_sync(0xffffffffu, contrib)) {
+            if (__any_sync(0xffffffffu, contrib)) {  // (measured: skipping beats always reducing)
                 const float r = grad_reduce<EXACT>(S0, S1, S2, dk, Sb, dr, dgc, dbc, dx);
                 if (red_comp >= 0 && (lane & 1) == 0)
                     red_add(a.grad2d + (size_t)lds_u32_at<Sm::kPid>(r4) * kGrad2dStride + red_comp, r);
