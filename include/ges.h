@@ -182,7 +182,9 @@ typedef struct {
     uint32_t *radix_total; /* [256] digit totals of the current pass, then [G] u64 area sums    */
     /* ---- S2 pairs and S3 ranges: direct tile binning ---- */
     uint32_t *item_offset; /* [P] first pair slot E of each depth-sorted visible particle  */
-    uint32_t *item_rec;    /* [P][4] packed (E, particle, x0|y0<<16, x1|y1<<16)           */
+    uint32_t *item_rec;    /* [P][4] packed (row classes, particle, x0|y0<<16, x1|y1<<16);
+                              row classes: bit r set if a tile row y of the rect has
+                              y = r (mod 8)                                            */
     uint32_t *chunk_first; /* [bin_chunks+1] first item of each binning chunk: the items s
                               whose cost E[s] + 4 s lies in [k S, (k+1) S), S = bin_chunk_slots */
     uint32_t *bin_table;   /* [bin_chunks][num_tiles] per-(chunk, tile) pair counts, then

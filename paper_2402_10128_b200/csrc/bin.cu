@@ -383,8 +383,10 @@ __global__ void __launch_bounds__(kScatThreads) bin_scatter_kernel(BinArgs a) {
                 const int qi = q0 + lane;
                 uint4 r = make_uint4(0, 0, 0, 0);
                 if (qi < n) r = rec[qi];
-                uint32_t g;
-                const bool rel = qi < n && class_pairs(r, R0, R1, warp, g) != 0u;
+                // the record's row-class mask (sort.cu); an item whose class rows all lie
+                // outside this window is dropped later (class_pairs = 0 in expand_group)
+                const int y0 = (int)(r.z >> 16), y1 = (int)(r.w >> 16);
+                const bool rel = qi < n && ((r.x >> warp) & 1u) && y1 > R0 && y0 < R1;
                 const uint32_t bal = __ballot_sync(0xffffffffu, rel);
                 if (rel) s_q[warp][(qhead + qn + __popc(bal & lt_mask)) & (kQueue - 1)] = r;
                 qn += __popc(bal);

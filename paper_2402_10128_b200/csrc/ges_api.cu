@@ -213,7 +213,9 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     b.counters = ctr; b.counters_w = ctr;
     b.table = frame->bin_table; b.ranges = frame->ranges; b.list = frame->list;
     b.tiles_x = frame->tiles_x; b.rows = frame->band_rows; b.T = (int64_t)frame->tiles_x * frame->band_rows;
+    // windows of whole 8-row groups (row class = row mod 8, precomputed per item)
     b.win_rows = std::max(1, std::min(frame->band_rows, kBinWinTiles / frame->tiles_x));
+    if (b.win_rows < frame->band_rows) b.win_rows &= ~7;
     b.cmax = (int)frame->bin_chunks; b.chunk_slots = frame->bin_chunk_slots;
     b.rank_bits = std::max(1, bits_for((int64_t)((b.win_rows + 7) / 8) * frame->tiles_x));
     if ((e = launch_bin(b, s)) != cudaSuccess) return GES_ERR_CUDA;

@@ -63,6 +63,15 @@ cudaError_t launch_depth_sort(const DepthSortArgs& a, cudaStream_t stream);
 // --- direct tile binning (bin.cu) -------------------------------------------
 constexpr int kBinWinTiles = 6144;    // tiles of one binning window (shared-memory cursors)
 constexpr int kBinItemCost = 4;       // chunk cost of an item, in pair slots
+// Bit r (r < 8) set if some tile row y in [y0, y1) has y = r (mod 8): the
+// binning scatter's warp r owns those rows (windows start at multiples of 8).
+__device__ __forceinline__ uint32_t row_class_mask(uint32_t y0, uint32_t y1) {
+    if (y1 <= y0) return 0u;
+    if (y1 - y0 >= 8u) return 0xffu;
+    const uint32_t m = ((1u << (y1 - y0)) - 1u) << (y0 & 7u);
+    return (m | (m >> 8)) & 0xffu;
+}
+
 struct BinArgs {
     const uint4* items;               // [V] item records in depth order (item scan)
     const uint32_t* chunk_first;      // [chunks + 1]

@@ -223,9 +223,9 @@ __device__ void ds_scatter(const DepthSortArgs& a, DsSmem& sm, const uint32_t* k
             vout[out] = pid;
             if (!last) {
                 kout[out] = key;
-            } else {  // item record (E filled in by the item scan)
+            } else {  // item record: row-class mask, particle, rect
                 const ushort4 rc = __ldg(a.rect + pid);
-                a.items[out] = make_uint4(0u, pid, (uint32_t)rc.x | ((uint32_t)rc.y << 16),
+                a.items[out] = make_uint4(row_class_mask(rc.y, rc.w), pid, (uint32_t)rc.x | ((uint32_t)rc.y << 16),
                                           (uint32_t)rc.z | ((uint32_t)rc.w << 16));
             }
         }
@@ -300,7 +300,6 @@ __device__ void ds_items(const DepthSortArgs& a, DsSmem& sm, int64_t V) {
                 if (s >= r1) break;
                 const uint64_t e1 = e + rec_count(rec[j]);
                 a.E[s] = (uint32_t)e;
-                a.items[s].x = (uint32_t)e;
                 // binning chunk k = the items whose cost W[s] = E[s] + kItemCost s lies in
                 // [k S, (k+1) S) (bin.cu): chunk_first[k] = min{s : W[s] >= k S}; item s + 1
                 // is that minimum for every k with k S in (W[s], W[s+1]].  Item 0 opens chunk 0.
