@@ -318,6 +318,7 @@ def run_ours(args) -> None:
     G.ges_sort(frame, stream)
     G.ges_render_fwd(frame, st, image, None, stream)   # the phi-bar Gaussian image, for comparison
     exact = time_exact_kernel(G, params, cam, scene, dL, image, flush, stream, args.steps, dev)
+    mix = time_mix1d(G, dev, stream, min(args.steps, 5))
 
     # ---- algorithmic work for the roofline ----
     n_comp = torch.zeros(W * H, dtype=torch.int32, device=dev)
@@ -367,6 +368,7 @@ def run_ours(args) -> None:
                           "note": f"one config-3 frame split into {world} interleaved tile-row bands, S1-S4 per "
                                   f"rank + all_gather of the band pixels; device time, max over ranks"},
             "exact_beta_kernel": exact,
+            "mix1d_sweep": mix,
             "loss_front_end": loss_line,
             "vs_gaussian_equivalent": {"ges_fwd_ms": fwd_ms, "gaussian_fwd_ms": g_ms, "ratio": g_ms / fwd_ms,
                                        "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
@@ -489,6 +491,81 @@ def time_band_forward(G, params, cam, st, dev, flush, stream, steps, rank, world
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item()), int(frame.counts().pairs)
 
+
+
+MIX_N = (2, 5, 8, 10, 15, 20, 50, 100)    # PAPER.md:628 component counts
+MIX_MUFU = {"gmm": (1, 1), "dog": (2, 2), "log": (1, 1), "gef": (3, 4)}   # ex2/lg2/rcp per (pass 1, pass 2) eval
+
+
+def time_mix1d(G, dev, stream, steps_timed, reps=20, n=512, fit_steps=100):
+    """NEXT-4: the paper's 1-D mixture sweep in one launch --
+    6 signals x N in {2, 5, 8, 10, 15, 20, 50, 100} x 4 models x {real, positive}
+    weights x `reps` seeded starts = 7680 independent Adam fits of `fit_steps` steps
+    on an n-sample grid over [-2, 2] (signal width 1), heavy runs first.  Roofline:
+    MUFU ex2/lg2/rcp results per (sample, component) evaluation against the rate a
+    probe kernel measures on this GPU."""
+    import numpy as np
+    import torch
+    kinds = ("square", "triangle", "parabolic", "half_sinusoid", "exponential", "gaussian")
+    targets = torch.stack([G.ges_mix_signal(k, 1.0, -2.0, 2.0, n) for k in kinds])
+    rng = np.random.default_rng(2402)
+    specs = []
+    for N in sorted(MIX_N, reverse=True):
+        for model in G.MIX_MODELS:
+            for pos in (True, False):
+                for t in range(len(kinds)):
+                    for _ in range(reps):
+                        specs.append((model, pos, N, t))
+    stride = 3 * max(MIX_N) + 1
+    th = np.zeros((len(specs), stride), np.float32)
+    for r, (model, pos, N, t) in enumerate(specs):
+        th[r, 0:N] = rng.uniform(-1.5, 1.5, N)
+        th[r, N:2 * N] = rng.uniform(0.1, 0.5, N)
+        th[r, 2 * N:3 * N] = rng.normal(-1.0, 0.3, N) if pos else rng.normal(0.3, 0.2, N)
+        th[r, 3 * N] = 2.0
+    th0 = torch.from_numpy(th).to(dev)
+    runs = G.mix_runs(specs)
+    sw = G.MixSweep(runs, th0.clone(), targets, -2.0, 2.0)
+    sw.fit(2, stream=stream)                       # warm-up
+    ms = []
+    for _ in range(max(1, steps_timed)):
+        sw.params.copy_(th0)
+        sw.m.zero_()
+        sw.v.zero_()
+        sw.t = 0
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        sw.fit(fit_steps, stream=stream)
+        b.record(stream)
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    t = float(statistics.median(ms))
+    loss = sw.loss.cpu().numpy()
+    evals = sum(N for (_, _, N, _) in specs) * n
+    mufu = sum(N * n * ((MIX_MUFU[m][0] + MIX_MUFU[m][1]) * fit_steps + MIX_MUFU[m][0]) for (m, _, N, _) in specs)
+    # the probe: 8 chains x iters ex2 per thread
+    out = torch.empty(148 * 8 * 256, dtype=torch.float32, device=dev)
+    lib = G.load()
+    import ctypes as C
+    iters, blocks = 4096, 148 * 8
+    for _ in range(2):
+        lib.ges_probe_mufu(C.c_void_p(out.data_ptr()), iters, blocks, C.c_void_p(stream.cuda_stream))
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    lib.ges_probe_mufu(C.c_void_p(out.data_ptr()), iters, blocks, C.c_void_p(stream.cuda_stream))
+    b.record(stream)
+    b.synchronize()
+    probe = 8.0 * iters * blocks * 256 / (a.elapsed_time(b) / 1e3) / 1e12
+    achieved = mufu / (t / 1e3) / 1e12
+    finite = np.isfinite(loss)
+    return {"runs": len(specs), "fit_steps": fit_steps, "samples": n, "ms": t,
+            "fits_per_s": len(specs) / (t / 1e3),
+            "component_sample_evals_per_s": evals * (2 * fit_steps + 1) / (t / 1e3),
+            "roofline": {"bound": "mufu", "achieved": achieved, "peak": probe, "unit": "T results/s",
+                         "frac": achieved / probe, "peak_source": "ges_probe_mufu (8 ex2 chains/thread) on this GPU"},
+            "finite_runs": int(finite.sum()), "median_final_loss": float(np.median(loss[finite])) if finite.any() else None,
+            "note": "NEXT-4 sweep: 7680 Adam fits (GMM/DoG/LoG/GEF, 6 signals, 8 N, real/positive weights, 20 "
+                    "seeds), one CTA per fit"}
 
 def time_loss_front_end(G, params, cam, st, frame, grads, image, flush, stream, steps, dev):
     """Eq. 9's loss on the bench frame (mask M_omega at omega = 0.75, L1 + SSIM + L_omega and

@@ -363,6 +363,66 @@ ges_status ges_loss(const float *image, const float *gt, const uint8_t *mask_lo,
                     const ges_loss_settings *settings, void *workspace, size_t workspace_bytes, float *dL_dimage,
                     float *loss_out, void *stream);
 
+
+/* ======================================================================
+ * NEXT-4: the 1-D mixture simulation of the Appendix
+ * (PAPER.md :606-745) and the Theorem-1 error integrals (:555-603).
+ * ====================================================================== */
+#define GES_MIX_MAX_N 128      /* components per run                       */
+#define GES_MIX_MAX_SAMPLES 49152 /* grid samples (residuals in shared memory) */
+typedef enum { GES_MIX_GMM = 0, GES_MIX_DOG = 1, GES_MIX_LOG = 2, GES_MIX_GEF = 3 } ges_mix_model;
+typedef enum {
+    GES_SIG_SQUARE = 0, GES_SIG_TRIANGLE = 1, GES_SIG_PARABOLIC = 2,
+    GES_SIG_HALF_SINUSOID = 3, GES_SIG_EXPONENTIAL = 4, GES_SIG_GAUSSIAN = 5
+} ges_signal;
+
+/* One independent fit (device array element, 16 bytes). */
+typedef struct {
+    int32_t model;      /* ges_mix_model                                              */
+    int32_t positive;   /* 1: w = exp(omega) (positive weights, R35); 0: w = omega    */
+    int32_t n_comp;     /* N in [1, GES_MIX_MAX_N]; params need stride >= 3 N + 1     */
+    int32_t target;     /* row of the target table                                   */
+} ges_mix_run;
+
+/* The sample grid x_j = x_lo + j (x_hi - x_lo) / (n - 1), 2 <= n <= GES_MIX_MAX_SAMPLES. */
+typedef struct { float x_lo, x_hi; int32_t n; } ges_mix_grid;
+
+typedef struct { float lr, beta1, beta2, eps; } ges_mix_adam;   /* torch.optim.Adam semantics */
+
+/* y[j] = signal(x_j) of width `width` (:662-745; zero outside (-width/2, width/2)
+ * except the Gaussian).  y: device [n]. */
+ges_status ges_mix_signal(int32_t kind, float width, const ges_mix_grid *grid, float *y, void *stream);
+
+/* Per run r: loss[r] = mean_j (h(x_j) - y_j)^2 of the mixture at params[r]
+ * (device [R][stride]: mu[N], s[N], omega[N], beta) against targets[run.target]
+ * (device [T][n]); grad (device [R][stride], may be NULL) = d loss / d params.
+ * A run with an invalid descriptor gets loss NaN. */
+ges_status ges_mix_eval(const ges_mix_run *runs, int32_t n_runs, const float *params, int32_t stride,
+                        const ges_mix_grid *grid, const float *targets, float *loss, float *grad, void *stream);
+
+/* `steps` Adam steps per run, in place on params and the moments m, v (device
+ * [R][stride], zero before a run's first step); step t uses bias corrections of
+ * t0 + 1 .. t0 + steps.  loss[r] = the MSE at the final parameters.  The beta
+ * slot changes only for GEF runs (its gradient is 0 otherwise).  One CTA per run:
+ * order heavy runs (large N) first. */
+ges_status ges_mix_fit(const ges_mix_run *runs, int32_t n_runs, float *params, float *m, float *v, int32_t stride,
+                       const ges_mix_grid *grid, const float *targets, const ges_mix_adam *adam, int32_t steps,
+                       int32_t t0, float *loss, void *stream);
+
+/* Theorem 1: E[a][b] = int |S(t) - A e^{-(|t|/alpha_a)^beta_b}| dt for the square
+ * wave S of amplitude A and width L, by composite Simpson with `intervals` (even,
+ * >= 2) panels on the substituted inner integral (see mix1d.cu); beta = 2 is the
+ * Gaussian's E_G.  alpha [na], beta [nb], E [na][nb]: device.  Non-positive
+ * alpha or beta give NaN. */
+ges_status ges_theorem1_errors(const float *alpha, int32_t na, const float *beta, int32_t nb, float A, float L,
+                               int32_t intervals, float *E, void *stream);
+
+/* Diagnostic: `blocks` x 256 threads each run 8 independent chains of `iters`
+ * MUFU ex2 (8 iters blocks 256 results in total); out: device [blocks * 256].
+ * The caller times it: the measured special-function rate is the roofline
+ * denominator of the ex2-bound kernels (mix1d). */
+ges_status ges_probe_mufu(float *out, int32_t iters, int32_t blocks, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

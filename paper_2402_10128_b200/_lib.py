@@ -83,6 +83,23 @@ class ges_adam_settings(C.Structure):
         "beta1", "beta2", "eps")]
 
 
+class ges_mix_run(C.Structure):
+    _fields_ = [("model", C.c_int32), ("positive", C.c_int32), ("n_comp", C.c_int32), ("target", C.c_int32)]
+
+
+class ges_mix_grid(C.Structure):
+    _fields_ = [("x_lo", C.c_float), ("x_hi", C.c_float), ("n", C.c_int32)]
+
+
+class ges_mix_adam(C.Structure):
+    _fields_ = [("lr", C.c_float), ("beta1", C.c_float), ("beta2", C.c_float), ("eps", C.c_float)]
+
+
+GES_MIX_GMM, GES_MIX_DOG, GES_MIX_LOG, GES_MIX_GEF = range(4)
+GES_MIX_MAX_N, GES_MIX_MAX_SAMPLES = 128, 49152
+GES_SIGNALS = ("square", "triangle", "parabolic", "half_sinusoid", "exponential", "gaussian")
+
+
 class ges_density_settings(C.Structure):
     _fields_ = [(n, C.c_float) for n in ("grad_threshold", "percent_dense", "scene_extent", "opacity_prune",
                                          "shape_prune", "rho")] + [("seed", C.c_uint64)]
@@ -92,7 +109,8 @@ EXPORTS = ["ges_workspace_bytes", "ges_frame_init", "ges_preprocess", "ges_sort"
            "ges_render_bwd", "ges_render_bwd_tiles", "ges_backward_particles", "ges_counts_get",
            "ges_status_string", "ges_version", "ges_loss_mask_dims", "ges_loss_workspace_bytes", "ges_loss_mask",
            "ges_loss", "ges_lr_position", "ges_adam_step", "ges_reset", "ges_densify_stats",
-           "ges_densify_workspace_bytes", "ges_densify_prune"]
+           "ges_densify_workspace_bytes", "ges_densify_prune", "ges_mix_signal", "ges_mix_eval", "ges_mix_fit",
+           "ges_theorem1_errors", "ges_probe_mufu"]
 
 _lib = None
 
@@ -162,6 +180,20 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         L.ges_loss.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                C.POINTER(ges_loss_settings), C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
                                C.c_void_p]
+        L.ges_mix_signal.restype = C.c_int
+        L.ges_mix_signal.argtypes = [C.c_int32, C.c_float, C.POINTER(ges_mix_grid), C.c_void_p, C.c_void_p]
+        L.ges_mix_eval.restype = C.c_int
+        L.ges_mix_eval.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.POINTER(ges_mix_grid), C.c_void_p,
+                                   C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ges_mix_fit.restype = C.c_int
+        L.ges_mix_fit.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                  C.POINTER(ges_mix_grid), C.c_void_p, C.POINTER(ges_mix_adam), C.c_int32, C.c_int32,
+                                  C.c_void_p, C.c_void_p]
+        L.ges_theorem1_errors.restype = C.c_int
+        L.ges_theorem1_errors.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_float, C.c_float,
+                                          C.c_int32, C.c_void_p, C.c_void_p]
+        L.ges_probe_mufu.restype = C.c_int
+        L.ges_probe_mufu.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
         _lib = L
     return _lib
 

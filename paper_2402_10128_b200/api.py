@@ -401,3 +401,77 @@ class DensityControl:
         self.accum = torch.zeros(n, dtype=torch.float32, device=dev)
         self.count = torch.zeros(n, dtype=torch.float32, device=dev)
         return new[0]
+
+
+# ---- NEXT-4: the 1-D mixture simulation and Theorem 1 (include/ges.h) --------------
+MIX_MODELS = ("gmm", "dog", "log", "gef")
+
+
+def _grid(x_lo: float, x_hi: float, n: int) -> L.ges_mix_grid:
+    g = L.ges_mix_grid()
+    g.x_lo, g.x_hi, g.n = float(x_lo), float(x_hi), int(n)
+    return g
+
+
+def ges_mix_signal(kind: str, width: float, x_lo: float, x_hi: float, n: int, stream=None) -> torch.Tensor:
+    """The ground-truth signal `kind` (L.GES_SIGNALS) on the grid, a device [n] tensor."""
+    y = torch.empty(n, dtype=torch.float32, device="cuda")
+    g = _grid(x_lo, x_hi, n)
+    L.check(L.load().ges_mix_signal(L.GES_SIGNALS.index(kind), float(width), C.byref(g), C.c_void_p(y.data_ptr()),
+                                    C.c_void_p(_stream(stream))), "ges_mix_signal")
+    return y
+
+
+def mix_runs(specs: Sequence) -> torch.Tensor:
+    """Device run table from (model name, positive, n_comp, target row) tuples."""
+    rows = [(MIX_MODELS.index(m), int(bool(p)), int(n), int(t)) for (m, p, n, t) in specs]
+    return torch.tensor(rows, dtype=torch.int32, device="cuda").reshape(-1, 4)
+
+
+class MixSweep:
+    """A batch of independent 1-D mixture fits (one CTA each) sharing a grid and a
+    target table: params / m / v are device [R][stride] tensors."""
+
+    def __init__(self, runs: torch.Tensor, params: torch.Tensor, targets: torch.Tensor, x_lo: float, x_hi: float):
+        self.runs = runs.contiguous()
+        self.params = params.contiguous()
+        self.targets = targets.contiguous()
+        self.grid = _grid(x_lo, x_hi, targets.shape[-1])
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.loss = torch.empty(self.runs.shape[0], dtype=torch.float32, device=self.params.device)
+        self.t = 0
+
+    def eval(self, grad: bool = True, stream=None):
+        g = torch.empty_like(self.params) if grad else None
+        L.check(L.load().ges_mix_eval(
+            C.c_void_p(self.runs.data_ptr()), self.runs.shape[0], C.c_void_p(self.params.data_ptr()),
+            self.params.shape[1], C.byref(self.grid), C.c_void_p(self.targets.data_ptr()),
+            C.c_void_p(self.loss.data_ptr()), C.c_void_p(g.data_ptr() if g is not None else 0),
+            C.c_void_p(_stream(stream))), "ges_mix_eval")
+        return self.loss, g
+
+    def fit(self, steps: int, lr: float = 1e-2, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+            stream=None) -> torch.Tensor:
+        a = L.ges_mix_adam()
+        a.lr, a.beta1, a.beta2, a.eps = lr, beta1, beta2, eps
+        L.check(L.load().ges_mix_fit(
+            C.c_void_p(self.runs.data_ptr()), self.runs.shape[0], C.c_void_p(self.params.data_ptr()),
+            C.c_void_p(self.m.data_ptr()), C.c_void_p(self.v.data_ptr()), self.params.shape[1], C.byref(self.grid),
+            C.c_void_p(self.targets.data_ptr()), C.byref(a), int(steps), int(self.t),
+            C.c_void_p(self.loss.data_ptr()), C.c_void_p(_stream(stream))), "ges_mix_fit")
+        self.t += int(steps)
+        return self.loss
+
+
+def ges_theorem1_errors(alpha: torch.Tensor, beta: torch.Tensor, A: float = 1.0, L_width: float = 1.0,
+                        intervals: int = 4096, stream=None) -> torch.Tensor:
+    """E[a][b] of Theorem 1 (square wave, amplitude A, width L) by quadrature on the device."""
+    alpha = alpha.contiguous().float()
+    beta = beta.contiguous().float()
+    E = torch.empty((alpha.numel(), beta.numel()), dtype=torch.float32, device=alpha.device)
+    L.check(L.load().ges_theorem1_errors(C.c_void_p(alpha.data_ptr()), alpha.numel(), C.c_void_p(beta.data_ptr()),
+                                         beta.numel(), float(A), float(L_width), int(intervals),
+                                         C.c_void_p(E.data_ptr()), C.c_void_p(_stream(stream))),
+            "ges_theorem1_errors")
+    return E

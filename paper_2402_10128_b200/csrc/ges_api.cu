@@ -473,4 +473,62 @@ ges_status ges_densify_prune(const float* params, const float* m, const float* v
     return cuda_status(launch_densify_prune(a, (cudaStream_t)stream));
 }
 
+// ---- NEXT-4: 1-D mixtures and Theorem 1 --------------------------------------
+static bool grid_ok(const ges_mix_grid* g) {
+    return g && g->n >= 2 && g->n <= GES_MIX_MAX_SAMPLES && std::isfinite(g->x_lo) && std::isfinite(g->x_hi) &&
+           g->x_hi > g->x_lo;
+}
+
+ges_status ges_mix_signal(int32_t kind, float width, const ges_mix_grid* grid, float* y, void* stream) {
+    if (!grid_ok(grid) || !y || kind < 0 || kind > 5 || !(width > 0.0f)) return GES_ERR_INVALID_ARG;
+    const float h = (grid->x_hi - grid->x_lo) / (float)(grid->n - 1);
+    return cuda_status(launch_mix_signal(kind, width, grid->x_lo, h, grid->n, y, (cudaStream_t)stream));
+}
+
+static ges_status mix_common(const ges_mix_run* runs, int32_t n_runs, float* params, int32_t stride,
+                             const ges_mix_grid* grid, const float* targets, float* loss, MixArgs& a) {
+    if (!runs || n_runs < 1 || !params || stride < 4 || !grid_ok(grid) || !targets || !loss) return GES_ERR_INVALID_ARG;
+    a.runs = runs; a.n_runs = n_runs; a.stride = stride; a.params = params; a.m = a.v = nullptr; a.grad = nullptr;
+    a.loss = loss; a.targets = targets; a.x_lo = grid->x_lo; a.n = grid->n;
+    a.h = (grid->x_hi - grid->x_lo) / (float)(grid->n - 1);
+    a.steps = 0; a.t0 = 0; a.lr = 0.0f; a.b1 = 0.9f; a.b2 = 0.999f; a.eps = 1e-8f;
+    return GES_OK;
+}
+
+ges_status ges_mix_eval(const ges_mix_run* runs, int32_t n_runs, const float* params, int32_t stride,
+                        const ges_mix_grid* grid, const float* targets, float* loss, float* grad, void* stream) {
+    MixArgs a;
+    const ges_status st = mix_common(runs, n_runs, const_cast<float*>(params), stride, grid, targets, loss, a);
+    if (st != GES_OK) return st;
+    a.grad = grad;
+    return cuda_status(launch_mix(a, false, (cudaStream_t)stream));
+}
+
+ges_status ges_mix_fit(const ges_mix_run* runs, int32_t n_runs, float* params, float* m, float* v, int32_t stride,
+                       const ges_mix_grid* grid, const float* targets, const ges_mix_adam* adam, int32_t steps,
+                       int32_t t0, float* loss, void* stream) {
+    MixArgs a;
+    const ges_status st = mix_common(runs, n_runs, params, stride, grid, targets, loss, a);
+    if (st != GES_OK) return st;
+    if (!m || !v || !adam || steps < 0 || t0 < 0 || !(adam->lr >= 0.0f) || !(adam->beta1 >= 0.0f && adam->beta1 < 1.0f) ||
+        !(adam->beta2 >= 0.0f && adam->beta2 < 1.0f) || !(adam->eps >= 0.0f))
+        return GES_ERR_INVALID_ARG;
+    a.m = m; a.v = v; a.steps = steps; a.t0 = t0;
+    a.lr = adam->lr; a.b1 = adam->beta1; a.b2 = adam->beta2; a.eps = adam->eps;
+    return cuda_status(launch_mix(a, true, (cudaStream_t)stream));
+}
+
+ges_status ges_theorem1_errors(const float* alpha, int32_t na, const float* beta, int32_t nb, float A, float L,
+                               int32_t intervals, float* E, void* stream) {
+    if (!alpha || !beta || !E || na < 1 || nb < 1 || intervals < 2 || (intervals & 1) || !(L > 0.0f) ||
+        !std::isfinite(A) || (int64_t)na * nb > (int64_t)1 << 26)
+        return GES_ERR_INVALID_ARG;
+    return cuda_status(launch_theorem1(alpha, na, beta, nb, A, L, intervals, E, (cudaStream_t)stream));
+}
+
+ges_status ges_probe_mufu(float* out, int32_t iters, int32_t blocks, void* stream) {
+    if (!out || iters < 1 || blocks < 1) return GES_ERR_INVALID_ARG;
+    return cuda_status(launch_mufu_probe(out, iters, blocks, (cudaStream_t)stream));
+}
+
 }  // extern "C"

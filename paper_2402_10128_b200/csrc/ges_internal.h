@@ -219,4 +219,24 @@ struct DensifyArgs {
 cudaError_t launch_densify_prune(const DensifyArgs& a, cudaStream_t stream);
 int64_t densify_blocks(int64_t P);
 
+// --- NEXT-4: 1-D mixtures and Theorem 1 (mix1d.cu) ------------------------
+struct MixArgs {
+    const ges_mix_run* runs;
+    int n_runs, stride;
+    float* params;
+    float *m, *v;            // Adam moments (fit)
+    float* grad;             // eval: [R][stride] or null
+    float* loss;             // [R]
+    const float* targets;    // [T][n]
+    float x_lo, h;
+    int n;
+    int steps, t0;
+    float lr, b1, b2, eps;
+};
+cudaError_t launch_mix_signal(int kind, float width, float x_lo, float h, int n, float* y, cudaStream_t stream);
+cudaError_t launch_mix(const MixArgs& a, bool fit, cudaStream_t stream);
+cudaError_t launch_mufu_probe(float* out, int iters, int blocks, cudaStream_t stream);
+cudaError_t launch_theorem1(const float* alpha, int na, const float* beta, int nb, float A, float L, int n, float* E,
+                            cudaStream_t stream);
+
 }  // namespace ges

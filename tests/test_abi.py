@@ -17,7 +17,7 @@ HEADER = os.path.join(ROOT, "include", "ges.h")
 def declared_functions():
     src = open(HEADER).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(ges_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(ges_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
@@ -34,7 +34,10 @@ def test_library_exports_every_declared_symbol():
 def test_ctypes_layout_matches_header(tmp_path):
     prog = tmp_path / "layout.c"
     structs = {"ges_particles": L.ges_particles, "ges_camera": L.ges_camera, "ges_settings": L.ges_settings,
-               "ges_grads": L.ges_grads, "ges_counts": L.ges_counts, "ges_frame": L.ges_frame}
+               "ges_grads": L.ges_grads, "ges_counts": L.ges_counts, "ges_frame": L.ges_frame,
+               "ges_loss_settings": L.ges_loss_settings, "ges_adam_settings": L.ges_adam_settings,
+               "ges_density_settings": L.ges_density_settings, "ges_mix_run": L.ges_mix_run,
+               "ges_mix_grid": L.ges_mix_grid, "ges_mix_adam": L.ges_mix_adam}
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{HEADER}"', 'int main(void) {']
     for s, cls in structs.items():
         lines.append(f'printf("{s} %zu\\n", sizeof({s}));')
@@ -107,3 +110,27 @@ def test_product_package_does_not_import_oracle():
             if fn.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, fn)).read()
                 assert "oracle" not in re.sub(r"(#|//).*", "", txt).lower() or fn == "_build.py", fn
+
+
+def test_mix_and_theorem_argument_checks_host_only():
+    """NEXT-4 entry points reject bad arguments before any launch (no device needed)."""
+    lib = L.load()
+    g = L.ges_mix_grid()
+    g.x_lo, g.x_hi, g.n = -2.0, 2.0, 512
+    fake = C.c_void_p(0x100000)
+    bad = L.ges_mix_grid()
+    bad.x_lo, bad.x_hi, bad.n = 1.0, -1.0, 512
+    assert lib.ges_mix_signal(0, 1.0, C.byref(bad), fake, None) == L.GES_ERR_INVALID_ARG
+    assert lib.ges_mix_signal(6, 1.0, C.byref(g), fake, None) == L.GES_ERR_INVALID_ARG
+    assert lib.ges_mix_signal(0, 0.0, C.byref(g), fake, None) == L.GES_ERR_INVALID_ARG
+    big = L.ges_mix_grid()
+    big.x_lo, big.x_hi, big.n = -1.0, 1.0, L.GES_MIX_MAX_SAMPLES + 1
+    assert lib.ges_mix_eval(fake, 4, fake, 16, C.byref(big), fake, fake, None, None) == L.GES_ERR_INVALID_ARG
+    assert lib.ges_mix_eval(fake, 0, fake, 16, C.byref(g), fake, fake, None, None) == L.GES_ERR_INVALID_ARG
+    assert lib.ges_mix_eval(fake, 4, fake, 3, C.byref(g), fake, fake, None, None) == L.GES_ERR_INVALID_ARG
+    a = L.ges_mix_adam()
+    a.lr, a.beta1, a.beta2, a.eps = 0.01, 1.0, 0.999, 1e-8
+    assert lib.ges_mix_fit(fake, 4, fake, fake, fake, 16, C.byref(g), fake, C.byref(a), 10, 0, fake,
+                           None) == L.GES_ERR_INVALID_ARG
+    assert lib.ges_theorem1_errors(fake, 4, fake, 4, 1.0, 1.0, 101, fake, None) == L.GES_ERR_INVALID_ARG
+    assert lib.ges_theorem1_errors(fake, 4, fake, 4, 1.0, 0.0, 100, fake, None) == L.GES_ERR_INVALID_ARG
