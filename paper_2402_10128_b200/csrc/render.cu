@@ -30,7 +30,10 @@
 
 namespace ges {
 
-constexpr int kBatch = 512;  // list entries staged per barrier
+#ifndef GES_BATCH
+#define GES_BATCH 256
+#endif
+constexpr int kBatch = GES_BATCH;  // list entries staged per barrier
 // tuning knobs: min resident CTAs per SM (register cap); unset = ptxas's choice
 #ifdef GES_RFWD_MINB
 #define GES_RFWD_LB(t) __launch_bounds__(t, GES_RFWD_MINB)
@@ -211,8 +214,13 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
 __device__ __forceinline__ int compact_warp_list(const uint8_t* s_mask, int n, int warp, uint16_t* out) {
     const int lane = threadIdx.x & 31;
     int cnt = 0;
+#ifdef GES_COMPACT_BOUNDED
+#pragma unroll 4
+    for (int c = 0; c < (n + 31) / 32; ++c) {
+#else
 #pragma unroll
     for (int c = 0; c < kBatch / 32; ++c) {
+#endif
         const int j = c * 32 + lane;
         const bool bit = j < n && ((s_mask[j] >> warp) & 1u);
         const uint32_t ball = __ballot_sync(0xffffffffu, bit);
@@ -407,8 +415,20 @@ static int ppt_from_env(const char* name, int dflt) {
     return (v == 2 || v == 4) ? v : dflt;
 }
 
+// Experiment knob: GES_CARVEOUT = preferred shared-memory carveout (percent) of the
+// render kernels; unset = the driver's choice.
+template <typename K>
+static void apply_carveout(K kernel) {
+    static const int pct = [] {
+        const char* e = getenv("GES_CARVEOUT");
+        return e ? atoi(e) : -1;
+    }();
+    if (pct >= 0) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+}
+
 template <int PPT, bool EXACT>
 static void launch_fwd_ppt(const RenderFwdArgs& a, int grid, bool diag, cudaStream_t stream) {
+    apply_carveout(render_fwd_kernel<PPT, false, EXACT>);
     if (diag) render_fwd_kernel<PPT, true, EXACT><<<grid, Layout<PPT>::kThreads, 0, stream>>>(a);
     else render_fwd_kernel<PPT, false, EXACT><<<grid, Layout<PPT>::kThreads, 0, stream>>>(a);
 }
@@ -684,8 +704,12 @@ cudaError_t launch_render_bwd(const RenderBwdArgs& a, cudaStream_t stream) {
         if (ppt == 4) render_bwd_kernel<4, true><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
         else render_bwd_kernel<2, true><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
     } else {
-        if (ppt == 4) render_bwd_kernel<4, false><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
-        else render_bwd_kernel<2, false><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
+        if (ppt == 4) {
+            apply_carveout(render_bwd_kernel<4, false>);
+            render_bwd_kernel<4, false><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
+        } else {
+            render_bwd_kernel<2, false><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
+        }
     }
     return cudaGetLastError();
 }
