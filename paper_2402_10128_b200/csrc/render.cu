@@ -253,16 +253,27 @@ struct StagedBatch {
     float* hb;   // beta / 2 (exact kernel)
 };
 
+// The list ids of a batch arrive in shared memory ahead of time (cp.async, one
+// batch early): staging then waits for the payload gathers only, not for the
+// id load that addresses them.
+__device__ __forceinline__ void prefetch_ids(uint32_t* dst, const uint32_t* list, uint32_t first, int n) {
+    for (int q = threadIdx.x; q < n; q += blockDim.x)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr(dst + q)), "l"(list + first + q)
+                     : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void wait_ids() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 template <int PPT, bool EXACT>
 __device__ __forceinline__ void stage_batch(const float4* pay0, const float4* pay1, const float* pay2,
-                                            const float* pay3, const uint32_t* list, uint32_t first, int n,
+                                            const float* pay3, const uint32_t* ids, int n,
                                             int tile_x0, int tile_y0, StagedBatch sb) {
     using Lt = Layout<PPT>;
 #pragma unroll
     for (int h = 0; h < Lt::kLoads; ++h) {
         const int q = threadIdx.x + h * Lt::kThreads;
         if (q < n) {
-            const uint32_t p = __ldg(list + first + q);
+            const uint32_t p = ids[q];
             const Splat s = load_splat(pay0, pay1, pay2, p);
             sb.g0[q] = make_float4(s.u, s.v, s.A, s.B);
             sb.g1[q] = make_float4(s.C, s.kappa, s.r, s.g);
@@ -285,6 +296,7 @@ struct RenderSmem {
     uint32_t pid[kBatch];
     float hb[EXACT ? kBatch : 1];
     uint16_t list[Layout<PPT>::kWarps][kBatch];
+    uint32_t ids[2][kBatch];  // list ids of this and the next batch
     uint8_t mask[kBatch];
     uint32_t max;
     static constexpr int kG1 = kBatch * 16, kB = kBatch * 32, kPid = kBatch * 36, kHb = kBatch * 40;
@@ -321,10 +333,14 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
     StagedBatch sb{S.g0, S.g1, S.b, nullptr, S.mask, S.hb};
     const uint32_t sbase = smem_addr(&S);
     const uint32_t a_list = smem_addr(S.list[warp]);
-    for (uint32_t b0 = start; b0 < end; b0 += kBatch) {
+    if (start < end) prefetch_ids(S.ids[0], a.list, start, (int)min((uint32_t)kBatch, end - start));
+    int buf = 0;
+    for (uint32_t b0 = start; b0 < end; b0 += kBatch, buf ^= 1) {
+        wait_ids();
         if (__syncthreads_count(done == kAll) == Lt::kThreads) break;
         const int n = (int)min((uint32_t)kBatch, end - b0);
-        stage_batch<PPT, EXACT>(a.pay0, a.pay1, a.pay2, a.pay3, a.list, b0, n, tile_x0, tile_y0, sb);
+        if (b0 + kBatch < end) prefetch_ids(S.ids[buf ^ 1], a.list, b0 + kBatch, (int)min((uint32_t)kBatch, end - b0 - kBatch));
+        stage_batch<PPT, EXACT>(a.pay0, a.pay1, a.pay2, a.pay3, S.ids[buf], n, tile_x0, tile_y0, sb);
         __syncthreads();
         if (__all_sync(0xffffffffu, done == kAll)) continue;  // the barrier above retires the tile
         const int nw = compact_warp_list(S.mask, n, warp, S.list[warp]);
@@ -391,6 +407,7 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
             }
         }
     }
+    wait_ids();  // no copy into shared memory outlives the CTA
     const int plane = a.W * a.H;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
@@ -553,11 +570,21 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads, PPT) render_bwd_kernel(Render
     StagedBatch sb{S.g0, S.g1, S.b, S.pid, S.mask, S.hb};
     const uint32_t sbase = smem_addr(&S);
     const uint32_t a_list = smem_addr(S.list[warp]);
-    for (int32_t b_end = (int32_t)max_last; b_end > 0; b_end -= kBatch) {
+    if (max_last > 0) {
+        const int32_t b0 = max(0, (int32_t)max_last - kBatch);
+        prefetch_ids(S.ids[0], a.list, start + (uint32_t)b0, (int)max_last - b0);
+    }
+    int buf = 0;
+    for (int32_t b_end = (int32_t)max_last; b_end > 0; b_end -= kBatch, buf ^= 1) {
         const int32_t b_begin = max(0, b_end - kBatch);
         const int n = b_end - b_begin;
-        __syncthreads();  // previous batch fully consumed
-        stage_batch<PPT, EXACT>(a.pay0, a.pay1, a.pay2, a.pay3, a.list, start + b_begin, n, tile_x0, tile_y0, sb);
+        wait_ids();
+        __syncthreads();  // previous batch fully consumed; this batch's ids visible
+        if (b_begin > 0) {
+            const int32_t nb = max(0, b_begin - kBatch);
+            prefetch_ids(S.ids[buf ^ 1], a.list, start + (uint32_t)nb, b_begin - nb);
+        }
+        stage_batch<PPT, EXACT>(a.pay0, a.pay1, a.pay2, a.pay3, S.ids[buf], n, tile_x0, tile_y0, sb);
         __syncthreads();
         // this warp's pixels composite nothing at or behind list position warp_max
         const int nw_lim = (int)min((int64_t)n, max((int64_t)0, (int64_t)warp_max - b_begin));
