@@ -727,9 +727,61 @@ def run_e2e(G, scene, cam, st, frame, dL_dev, dev, stream, steps, world):
     ms = a.elapsed_time(b) / steps
     h2d = host_params.flat.numel() * 4 + host_dL.numel() * 4
     d2h = host_img.numel() * 4
-    return {"value": world * cam.width * cam.height / (ms / 1e3) / 1e6, "unit": "Mpixel-frames/s (fwd+bwd)",
-            "ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "path": "pinned host -> device copy, ges_preprocess/sort/render_fwd/render_bwd, image -> host"}
+    out = {"value": world * cam.width * cam.height / (ms / 1e3) / 1e6, "unit": "Mpixel-frames/s (fwd+bwd)",
+           "ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "path": "pinned host -> device copy, ges_preprocess/sort/render_fwd/render_bwd, image -> host"}
+    out["train_step"] = run_e2e_train(G, scene, cam, st, frame, dev, stream, steps, world)
+    return out
+
+
+def run_e2e_train(G, scene, cam, st, frame, dev, stream, steps, world):
+    """A training iteration as a user runs it: parameters and Adam state resident
+    on the device, the view's ground-truth image copied in from pinned host memory
+    every step, S1-S4 + the Eq. 9 loss (mask at omega = 0.75) + S5 + Adam, and the
+    loss read back to the host every step."""
+    import torch
+    P, deg = scene.particles.P, scene.particles.sh_degree
+    W, H = cam.width, cam.height
+    params = G.PlanarParams.from_inputs(scene.particles, device=dev)
+    yy = torch.linspace(0, 1, H)[:, None]
+    xx = torch.linspace(0, 1, W)[None, :]
+    host_gt = torch.stack([0.5 + 0.3 * torch.sin(9 * xx + 4 * yy), 0.5 + 0.3 * torch.cos(7 * yy - 3 * xx),
+                           0.4 + 0.2 * torch.sin(13 * xx * yy)]).contiguous().pin_memory()
+    gt = torch.empty((3, H, W), dtype=torch.float32, device=dev)
+    img = torch.empty((3, H, W), dtype=torch.float32, device=dev)
+    dL = torch.empty_like(img)
+    grads = G.PlanarParams.zeros(P, deg, dev)
+    loss = G.Loss(W, H, device=dev)
+    mask = loss.mask(host_gt.to(dev), 0.75, stream=stream)
+    opt = G.Adam(params)
+    host_loss = torch.empty(4, dtype=torch.float32).pin_memory()
+
+    def one():
+        gt.copy_(host_gt, non_blocking=True)
+        G.ges_preprocess(params, cam, st, frame, stream)
+        G.ges_sort(frame, stream)
+        G.ges_render_fwd(frame, st, img, None, stream)
+        loss.mask(gt, 0.75, mask, stream=stream)
+        out, _ = loss(img, gt, mask, dL, stream=stream)
+        G.ges_render_bwd(params, cam, st, frame, dL, grads, False, stream)
+        opt.step(params, grads, stream=stream)
+        host_loss.copy_(out, non_blocking=True)
+
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        one()
+    b.record(stream)
+    b.synchronize()
+    ms = a.elapsed_time(b) / steps
+    return {"value": world * W * H / (ms / 1e3) / 1e6, "unit": "Mpixel-frames/s (fwd+loss+bwd+Adam)",
+            "ms_per_step": ms, "h2d_bytes_per_step": host_gt.numel() * 4, "d2h_bytes_per_step": host_loss.numel() * 4,
+            "final_loss": float(host_loss[0]), "pair_overflow": bool(frame.counts().overflow),
+            "path": "parameters resident; ground truth pinned host -> device, S1-S4, ges_loss_mask + ges_loss, "
+                    "S5, ges_adam_step, loss -> host"}
 
 
 def cpu_baseline(scene):
