@@ -123,3 +123,22 @@ def test_theorem1_errors_against_closed_form():
     # the theorem on the device's numbers: some beta beats the Gaussian (beta = 2)
     k2 = list(betas).index(2.0)
     assert np.all(np.delete(E, k2, axis=1).min(axis=1) < E[:, k2])
+
+
+def test_largest_run_and_grid():
+    """GES_MIX_MAX_N components on GES_MIX_MAX_SAMPLES samples (the residuals fill
+    ~192 KB of shared memory): loss and gradient still match the oracle."""
+    from paper_2402_10128_b200 import _lib as L
+    N, n = L.GES_MIX_MAX_N, L.GES_MIX_MAX_SAMPLES
+    grid = (-2.0, 2.0, n)
+    rng = np.random.default_rng(41)
+    th = _params(rng, "gef", N, 3 * N + 1)
+    th[2 * N:3 * N] = rng.normal(-3.0, 0.3, N)
+    targets = torch.stack([G.ges_mix_signal("square", 1.0, *grid)])
+    sw = G.MixSweep(G.mix_runs([("gef", True, N, 0)]), torch.from_numpy(th[None]).cuda(), targets, grid[0], grid[1])
+    loss, grad = sw.eval()
+    x = _x32(*grid)
+    Lr, gr = M.loss_and_grad("gef", True, th.astype(np.float64), N, x, M.signal("square", x, 1.0))
+    assert abs(float(loss[0]) - Lr) <= 1e-4 * Lr
+    g = grad.cpu().numpy()[0]
+    assert np.all(np.abs(g - gr) <= 1e-3 * np.abs(gr) + 1e-5 * np.abs(gr).max() + 1e-9)

@@ -349,3 +349,37 @@ def test_binning_over_several_tile_windows(case):
     gs, osx = settings_pair(rho=sc.rho)
     assert ((cam.width + 15) // 16) * ((cam.height + 15) // 16) > 6144
     run_case(sc.particles, cam, gs, osx, gi.upstream_grad(sc.seed, 4, cam.width, cam.height))
+
+
+def test_exact_kernel_bands_match_full_frame():
+    """Screen-tile bands with the exact GEF kernel: every band's
+    pixels bit-identical to the full frame's, and the bands' S5 gradients sum to the
+    full frame's (float atomics reorder: the tolerance of the Gaussian band test)."""
+    sc = gi.make_config(1, P=20000)
+    cam = sc.cameras[0]
+    gs = G.Settings(rho=sc.rho, kernel=1)
+    dL = gi.upstream_grad(sc.seed, 0, cam.width, cam.height)
+    out = gpu_forward(sc.particles, cam, gs)
+    g_full, _ = gpu_backward(out, cam, gs, dL)
+    params = out["params"]
+    dLt = torch.from_numpy(dL).cuda()
+    acc = G.PlanarParams.zeros(params.P, params.sh_degree)
+    world = 3
+    for b in range(world):
+        gb = G.Settings(rho=sc.rho, kernel=1, tile_row_begin=b, tile_row_step=world)
+        r = G.Renderer(params.P, cam.width, cam.height)
+        img = torch.full((3, cam.height, cam.width), -7.0, device="cuda")
+        r.forward(params, cam, gb, image=img)
+        r.backward(params, cam, gb, dLt, grads=acc, accumulate=b > 0)
+        torch.cuda.synchronize()
+        img = img.cpu().numpy()
+        pix = np.zeros(cam.height, bool)
+        for t in range(b, r.frame.c.tiles_y, world):
+            pix[16 * t:16 * t + 16] = True
+        assert np.array_equal(img[:, pix], out["image"][:, pix])
+        assert np.all(img[:, ~pix] == -7.0)
+    for n in G.PARAM_NAMES:
+        a = getattr(acc, n).cpu().numpy().astype(np.float64)
+        floor = 1e-6 + 1e-6 * np.abs(g_full[n]).max()
+        bad = np.abs(a - g_full[n]) > np.maximum(1e-3 * np.abs(g_full[n]), floor)
+        assert bad.sum() == 0, (n, int(bad.sum()))

@@ -31,8 +31,9 @@ def to_params(arr, deg):
     return G.PlanarParams(t, arr.shape[1], deg)
 
 
-def test_adam_steps_and_schedule():
-    deg, P = 3, 10000
+@pytest.mark.parametrize("deg,P", [(3, 10000), (3, 9999), (0, 1), (1, 4097)])
+def test_adam_steps_and_schedule(deg, P):
+    """P % 4 == 0 takes the float4 kernel, any other P the scalar one."""
     K = (deg + 1) ** 2
     p = planar(P, deg, 1)
     params = to_params(p, deg)
