@@ -319,6 +319,9 @@ def run_ours(args) -> None:
     G.ges_render_fwd(frame, st, image, None, stream)   # the phi-bar Gaussian image, for comparison
     exact = time_exact_kernel(G, params, cam, scene, dL, image, flush, stream, args.steps, dev)
     mix = time_mix1d(G, dev, stream, min(args.steps, 5))
+    batches = {"cfg2": time_view_batch(G, 2, dev, stream, min(args.steps, 20), rank, world),
+               "cfg4": time_view_batch(G, 4, dev, stream, min(args.steps, 10), rank, world)}
+    small = time_small_configs(G, dev, stream, min(args.steps, 50)) if world == 1 else None
 
     # ---- algorithmic work for the roofline ----
     n_comp = torch.zeros(W * H, dtype=torch.int32, device=dev)
@@ -369,6 +372,8 @@ def run_ours(args) -> None:
                                   f"rank + all_gather of the band pixels; device time, max over ranks"},
             "exact_beta_kernel": exact,
             "mix1d_sweep": mix,
+            "view_batch_iters": batches,
+            "small_configs": small,
             "loss_front_end": loss_line,
             "vs_gaussian_equivalent": {"ges_fwd_ms": fwd_ms, "gaussian_fwd_ms": g_ms, "ratio": g_ms / fwd_ms,
                                        "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
@@ -566,6 +571,106 @@ def time_mix1d(G, dev, stream, steps_timed, reps=20, n=512, fit_steps=100):
             "finite_runs": int(finite.sum()), "median_final_loss": float(np.median(loss[finite])) if finite.any() else None,
             "note": "NEXT-4 sweep: 7680 Adam fits (GMM/DoG/LoG/GEF, 6 signals, 8 N, real/positive weights, 20 "
                     "seeds), one CTA per fit"}
+
+
+def time_view_batch(G, cfg, dev, stream, steps, rank, world):
+    """SURVEY.md §8(d) iters/s: a fixed global batch of 8 views split 8/N per rank --
+    fwd+bwd of each view with the gradients accumulated, the NCCL allreduce (N > 1),
+    then a dependent update through ges_adam_step with every LR 0 (parameters
+    unchanged).  Config 2: its 8 orbit views; config 4: 8 of its 64 views.  Device
+    time, max over ranks; strong scaling (the global batch is fixed)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import ges_inputs as gi
+    scene = gi.make_config(cfg)
+    cams = scene.cameras[:8] if cfg == 2 else [scene.cameras[k] for k in
+                                               np.random.default_rng(2402).choice(len(scene.cameras), 8, replace=False)]
+    mine = [c for k, c in enumerate(cams) if k % world == rank]
+    params = G.PlanarParams.from_inputs(scene.particles, device=dev)
+    P, deg = params.P, params.sh_degree
+    grads = G.PlanarParams.zeros(P, deg, dev)
+    st = G.Settings(rho=scene.rho)
+    W, H = cams[0].width, cams[0].height
+    r = G.Renderer(P, W, H, device=dev)
+    img = torch.empty((3, H, W), dtype=torch.float32, device=dev)
+    dLs = [torch.from_numpy(gi.upstream_grad(scene.seed, k, W, H)).to(dev) for k in range(len(mine))]
+    for c in mine:                                    # size the frame for the largest view
+        r.forward(params, c, st, img)
+        r.grow(int(r.frame.counts().slots))
+    zero = G.AdamSettings(lr_pos_init=0.0, lr_pos_final=0.0, lr_feature=0.0, lr_opacity=0.0, lr_scaling=0.0,
+                          lr_rotation=0.0, lr_shape=0.0)
+    opt = G.Adam(params, zero)
+    frame = r.frame
+
+    def step():
+        for k, c in enumerate(mine):
+            G.ges_preprocess(params, c, st, frame, stream)
+            G.ges_sort(frame, stream)
+            G.ges_render_fwd(frame, st, img, None, stream)
+            G.ges_render_bwd(params, c, st, frame, dLs[k], grads, k > 0, stream)
+        if world > 1:
+            dist.all_reduce(grads.flat)
+        opt.step(params, grads, stream=stream)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        step()
+    b.record(stream)
+    b.synchronize()
+    t = torch.tensor([a.elapsed_time(b) / steps], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    assert not frame.counts().overflow
+    return {"config": gi.CONFIG_NAMES[cfg], "views_per_iter": 8, "views_per_rank": len(mine), "ms_per_iter": ms,
+            "iters_per_s": 1e3 / ms, "value": 8 * W * H / (ms / 1e3) / 1e6, "unit": "Mpixel-frames/s (fwd+bwd)",
+            "scaling": "strong"}
+
+
+def time_small_configs(G, dev, stream, steps):
+    """Mpixel-frames/s of the fwd+bwd step on configs 0-2 ('configs 0-2 also
+    reported'); config 1 at beta = 2, config 2 on its first view."""
+    import torch
+    import ges_inputs as gi
+    out = {}
+    for cfg, kw in ((0, {}), (1, {"beta_value": 2.0}), (2, {})):
+        scene = gi.make_config(cfg, **kw)
+        cam = scene.cameras[0]
+        params = G.PlanarParams.from_inputs(scene.particles, device=dev)
+        grads = G.PlanarParams.zeros(params.P, params.sh_degree, dev)
+        st = G.Settings(rho=scene.rho)
+        r = G.Renderer(params.P, cam.width, cam.height, device=dev)
+        img = torch.empty((3, cam.height, cam.width), dtype=torch.float32, device=dev)
+        r.forward(params, cam, st, img)
+        r.grow(int(r.frame.counts().slots))
+        dL = torch.from_numpy(gi.upstream_grad(scene.seed, 0, cam.width, cam.height)).to(dev)
+        frame = r.frame
+
+        def step():
+            G.ges_preprocess(params, cam, st, frame, stream)
+            G.ges_sort(frame, stream)
+            G.ges_render_fwd(frame, st, img, None, stream)
+            G.ges_render_bwd(params, cam, st, frame, dL, grads, False, stream)
+
+        for _ in range(3):
+            step()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            step()
+        b.record(stream)
+        b.synchronize()
+        ms = a.elapsed_time(b) / steps
+        out[gi.CONFIG_NAMES[cfg]] = {"ms": ms, "value": cam.width * cam.height / (ms / 1e3) / 1e6,
+                                     "unit": "Mpixel-frames/s (fwd+bwd)"}
+    return out
 
 def time_loss_front_end(G, params, cam, st, frame, grads, image, flush, stream, steps, dev):
     """Eq. 9's loss on the bench frame (mask M_omega at omega = 0.75, L1 + SSIM + L_omega and
