@@ -272,8 +272,29 @@ def run_ours(args) -> None:
     cnt = frame.counts()
     assert not cnt.overflow
 
-    # ---- timed region ----
-    stage_ms = np.zeros(len(stage_names))
+    # S1-S5 of one step captured once as a CUDA graph (the API is stream-ordered and
+    # capture-safe); the timed loop replays it, the NCCL allreduce follows on the stream
+    graph, graph_note = None, "off (--no-graph)"
+    if not args.no_graph:
+        try:
+            graph = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream()
+            cap.wait_stream(stream)
+            with torch.cuda.graph(graph, stream=cap):
+                G.ges_preprocess(params, cam, st, frame, cap)
+                G.ges_sort(frame, cap)
+                G.ges_render_fwd(frame, st, image, None, cap)
+                G.ges_render_bwd_tiles(st, frame, dL, cap)
+                G.ges_backward_particles(params, cam, st, frame, grads, False, cap)
+            stream.wait_stream(cap)
+            for _ in range(args.warmup):
+                graph.replay()
+            torch.cuda.synchronize()
+            graph_note = "S1-S5 replayed as one CUDA graph per step"
+        except Exception as e:  # noqa: BLE001 -- fall back to direct launches, reported
+            graph, graph_note = None, f"capture failed ({e}); direct launches"
+
+    # ---- timed region: K steps ----
     step_ms = []
     if world > 1:
         dist.barrier()
@@ -281,13 +302,29 @@ def run_ours(args) -> None:
     with ClockSampler(dev.index) as clk:
         for _ in range(args.steps):
             flush.fill_(1)
-            timers = [ev() for _ in range(NS + 1)]
-            step(timers)
-            timers[-1].synchronize()
-            step_ms.append(timers[0].elapsed_time(timers[NS]))
-            for i in range(NS):
-                stage_ms[i] += timers[i].elapsed_time(timers[i + 1])
+            t0, t1 = ev(), ev()
+            t0.record(stream)
+            if graph is not None:
+                graph.replay()
+                if world > 1:
+                    dist.all_reduce(grads.flat)
+            else:
+                step()
+            t1.record(stream)
+            t1.synchronize()
+            step_ms.append(t0.elapsed_time(t1))
         torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    # ---- per-stage breakdown: the same steps launched directly with an event per stage ----
+    stage_ms = np.zeros(len(stage_names))
+    for _ in range(args.steps):
+        flush.fill_(1)
+        timers = [ev() for _ in range(NS + 1)]
+        step(timers)
+        timers[-1].synchronize()
+        for i in range(NS):
+            stage_ms[i] += timers[i].elapsed_time(timers[i + 1])
     if world > 1:
         dist.barrier()
     total_ms = float(sum(step_ms))
@@ -377,7 +414,9 @@ def run_ours(args) -> None:
             "loss_front_end": loss_line,
             "vs_gaussian_equivalent": {"ges_fwd_ms": fwd_ms, "gaussian_fwd_ms": g_ms, "ratio": g_ms / fwd_ms,
                                        "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
+            "launch": graph_note,
             "stages_ms": {n: float(stage_ms[i]) for i, n in enumerate(stage_names)},
+            "stages_note": "per-stage CUDA events around direct launches of the same step (not the graph replay)",
             "counts": {"visible": int(cnt.visible), "pairs": int(cnt.pairs), "slots": int(cnt.slots), "evals_fwd": e_fwd,
                        "composited": e_comp},
             "roofline": {"kernel": dname, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
@@ -668,8 +707,31 @@ def time_small_configs(G, dev, stream, steps):
         b.record(stream)
         b.synchronize()
         ms = a.elapsed_time(b) / steps
+        # the same step captured once as a CUDA graph and replayed (launch overhead gone)
+        ms_graph = None
+        try:
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream()
+            cap.wait_stream(stream)
+            with torch.cuda.graph(g, stream=cap):
+                G.ges_preprocess(params, cam, st, frame, cap)
+                G.ges_sort(frame, cap)
+                G.ges_render_fwd(frame, st, img, None, cap)
+                G.ges_render_bwd(params, cam, st, frame, dL, grads, False, cap)
+            stream.wait_stream(cap)
+            for _ in range(3):
+                g.replay()
+            torch.cuda.synchronize()
+            a.record(stream)
+            for _ in range(steps):
+                g.replay()
+            b.record(stream)
+            b.synchronize()
+            ms_graph = a.elapsed_time(b) / steps
+        except Exception as e:  # noqa: BLE001 -- reported, not fatal
+            ms_graph = f"capture failed: {e}"
         out[gi.CONFIG_NAMES[cfg]] = {"ms": ms, "value": cam.width * cam.height / (ms / 1e3) / 1e6,
-                                     "unit": "Mpixel-frames/s (fwd+bwd)"}
+                                     "unit": "Mpixel-frames/s (fwd+bwd)", "ms_cuda_graph": ms_graph}
     return out
 
 def time_loss_front_end(G, params, cam, st, frame, grads, image, flush, stream, steps, dev):
@@ -906,6 +968,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch every kernel directly in the timed loop")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--ref-tiles", type=int, default=16)
     args = ap.parse_args()
