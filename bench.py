@@ -862,41 +862,71 @@ def gaussian_equivalent(G, scene, cam, dev):
 
 def run_e2e(G, scene, cam, st, frame, dL_dev, dev, stream, steps, world):
     """Public-API step with HOST inputs: pinned particles + dL/dimage copied in,
-    image copied out, every step, inside the timed region."""
+    image copied out, every step, inside the timed region.  The copies run on a
+    second stream, double-buffered: step k+1's inputs upload while step k computes
+    (the region starts before step 0's upload and ends after the last image lands
+    on the host), so a step costs max(PCIe transfer, compute)."""
     import torch
     P, deg = scene.particles.P, scene.particles.sh_degree
     host_params = G.PlanarParams.from_inputs(scene.particles, device="cpu", pin_memory=True)
     host_dL = dL_dev.cpu().pin_memory()
-    host_img = torch.empty((3, cam.height, cam.width), dtype=torch.float32).pin_memory()
-    dparams = G.PlanarParams.empty(P, deg, dev)
-    ddL = torch.empty_like(dL_dev)
-    img = torch.empty((3, cam.height, cam.width), dtype=torch.float32, device=dev)
+    host_img = [torch.empty((3, cam.height, cam.width), dtype=torch.float32).pin_memory() for _ in range(2)]
+    dparams = [G.PlanarParams.empty(P, deg, dev) for _ in range(2)]
+    ddL = [torch.empty_like(dL_dev) for _ in range(2)]
+    img = [torch.empty((3, cam.height, cam.width), dtype=torch.float32, device=dev) for _ in range(2)]
     grads = G.PlanarParams.zeros(P, deg, dev)
+    copy = torch.cuda.Stream(device=dev)
+    ev = lambda: torch.cuda.Event()
+    uploaded = [ev(), ev()]   # inputs of buffer b are on the device
+    consumed = [ev(), ev()]   # step using buffer b finished (its inputs and image may be reused)
+    drained = [ev(), ev()]    # image of buffer b is on the host
 
-    def one():
-        dparams.flat.copy_(host_params.flat, non_blocking=True)
-        ddL.copy_(host_dL, non_blocking=True)
-        G.ges_preprocess(dparams, cam, st, frame, stream)
+    def upload(b):
+        with torch.cuda.stream(copy):
+            copy.wait_event(consumed[b])
+            dparams[b].flat.copy_(host_params.flat, non_blocking=True)
+            ddL[b].copy_(host_dL, non_blocking=True)
+            uploaded[b].record(copy)
+
+    def compute(b):
+        stream.wait_event(uploaded[b])
+        stream.wait_event(drained[b])
+        G.ges_preprocess(dparams[b], cam, st, frame, stream)
         G.ges_sort(frame, stream)
-        G.ges_render_fwd(frame, st, img, None, stream)
-        G.ges_render_bwd(dparams, cam, st, frame, ddL, grads, False, stream)
-        host_img.copy_(img, non_blocking=True)
+        G.ges_render_fwd(frame, st, img[b], None, stream)
+        G.ges_render_bwd(dparams[b], cam, st, frame, ddL[b], grads, False, stream)
+        consumed[b].record(stream)
+        with torch.cuda.stream(copy):
+            copy.wait_event(consumed[b])
+            host_img[b].copy_(img[b], non_blocking=True)
+            drained[b].record(copy)
 
-    for _ in range(2):
-        one()
+    def run(n):
+        upload(0)
+        for k in range(n):
+            if k + 1 < n:
+                upload((k + 1) & 1)
+            compute(k & 1)
+        stream.wait_stream(copy)
+
+    for e in consumed + drained:
+        e.record(stream)
+    run(2)
     torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
-    for _ in range(steps):
-        one()
+    copy.wait_stream(stream)
+    run(steps)
     b.record(stream)
     b.synchronize()
     ms = a.elapsed_time(b) / steps
     h2d = host_params.flat.numel() * 4 + host_dL.numel() * 4
-    d2h = host_img.numel() * 4
+    d2h = host_img[0].numel() * 4
     out = {"value": world * cam.width * cam.height / (ms / 1e3) / 1e6, "unit": "Mpixel-frames/s (fwd+bwd)",
            "ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-           "path": "pinned host -> device copy, ges_preprocess/sort/render_fwd/render_bwd, image -> host"}
+           "h2d_GBps": h2d / (ms / 1e3) / 1e9,
+           "path": "pinned host -> device copy (second stream, double-buffered against the previous step's "
+                   "compute), ges_preprocess/sort/render_fwd/render_bwd, image -> host"}
     out["train_step"] = run_e2e_train(G, scene, cam, st, frame, dev, stream, steps, world)
     return out
 
