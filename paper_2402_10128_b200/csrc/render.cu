@@ -7,11 +7,11 @@
 // the Gaussian of the phi-bar-scaled covariance (the paper's approximate
 // rasterization "without taking the beta exponent"; R6).
 //
-// One CTA per tile, PPT (= 2) pixels per thread; warp w owns the
-// 8 x (4 PPT)-pixel region (x0 = 8 (w & 1), y0 = 4 PPT (w >> 1)) of the tile.
-// Each batch of 512 list
-// entries is gathered once into shared memory; while gathering, each thread
-// tests its entry against the 8 warp regions with an exact lower bound of the
+// One CTA per tile, PPT pixels per thread (2 forward, 4 backward); warp w owns
+// the 8 x (4 PPT)-pixel region (x0 = 8 (w & 1), y0 = 4 PPT (w >> 1)) of the tile.
+// Each batch of kBatch (256) list entries is gathered once into shared memory
+// (its list ids prefetched one batch early by cp.async); while gathering, each
+// thread tests its entry against the warp regions with an exact lower bound of the
 // Mahalanobis form over the region (the minimum of a positive-definite
 // quadratic over a box) and marks the regions where alpha >= 1/255 is
 // possible.  Each warp then walks only its own compacted entry list.  The
