@@ -274,12 +274,18 @@ __global__ void __launch_bounds__(256, GES_PBWD_MINB) particle_bwd_kernel(Partic
 
 // --- TMA-staged variant (as S1's): a producer warp streams each 128-particle
 // tile's inputs -- 12 parameter planes, the 48-B 2-D gradient records, the 9
-// d rgb / d dir planes, status and flags (~17 KB) -- into a 3-stage ring
+// d rgb / d dir planes, status and flags (~17 KB) -- into a 2-stage ring
 // (cp.async.bulk, mbarriers); four consumer warps run the chain rule and store
 // the gradients.  Needs P % 4 == 0 and 16-B aligned planes; the partial last
 // tile goes through global loads.
-constexpr int kPbTile = 128;
-constexpr int kPbStages = 3;
+#ifndef GES_PB_TILE
+#define GES_PB_TILE 128
+#endif
+#ifndef GES_PB_STAGES
+#define GES_PB_STAGES 2
+#endif
+constexpr int kPbTile = GES_PB_TILE;
+constexpr int kPbStages = GES_PB_STAGES;
 constexpr int kPbThreads = kPbTile + 32;
 constexpr int kPbPlanes = 12 + 9;
 struct PbStage {

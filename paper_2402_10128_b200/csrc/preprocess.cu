@@ -278,8 +278,14 @@ __global__ void __launch_bounds__(kPreThreads, GES_PRE_MINB) preprocess_kernel(P
 // next tile overlap this tile's arithmetic without any loads held in registers.
 // Needs 16-B aligned planes (P % 4 == 0 and aligned base pointers); the last
 // partial tile is processed from global memory.
-constexpr int kPreTile = 128;
-constexpr int kPreStages = 2;
+#ifndef GES_PRE_TILE
+#define GES_PRE_TILE 128
+#endif
+#ifndef GES_PRE_STAGES
+#define GES_PRE_STAGES 2
+#endif
+constexpr int kPreTile = GES_PRE_TILE;
+constexpr int kPreStages = GES_PRE_STAGES;
 constexpr int kPreTmaThreads = kPreTile + 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
