@@ -359,6 +359,7 @@ def run_ours(args) -> None:
     batches = {"cfg2": time_view_batch(G, 2, dev, stream, min(args.steps, 20), rank, world),
                "cfg4": time_view_batch(G, 4, dev, stream, min(args.steps, 10), rank, world)}
     small = time_small_configs(G, dev, stream, min(args.steps, 50)) if world == 1 else None
+    union = time_union_compaction(G, scene, dev, stream, min(args.steps, 20)) if world == 1 else None
 
     # ---- algorithmic work for the roofline ----
     n_comp = torch.zeros(W * H, dtype=torch.int32, device=dev)
@@ -411,6 +412,7 @@ def run_ours(args) -> None:
             "mix1d_sweep": mix,
             "view_batch_iters": batches,
             "small_configs": small,
+            "allreduce_union_compaction": union,
             "loss_front_end": loss_line,
             "vs_gaussian_equivalent": {"ges_fwd_ms": fwd_ms, "gaussian_fwd_ms": g_ms, "ratio": g_ms / fwd_ms,
                                        "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
@@ -733,6 +735,39 @@ def time_small_configs(G, dev, stream, steps):
         out[gi.CONFIG_NAMES[cfg]] = {"ms": ms, "value": cam.width * cam.height / (ms / 1e3) / 1e6,
                                      "unit": "Mpixel-frames/s (fwd+bwd)", "ms_cuda_graph": ms_graph}
     return out
+
+
+def time_union_compaction(G, scene, dev, stream, steps):
+    """SURVEY.md §8(e) visible-union compaction, measured on one GPU: the union of the
+    visible sets of config 3's 8 bench views (what 8 ranks would OR together), and
+    the device time of ges_grad_pack + ges_grad_unpack on the 60 x P planar gradient
+    -- against the bytes the allreduce would no longer move."""
+    import torch
+    from paper_2402_10128_b200 import dist as gdist
+    params = G.PlanarParams.from_inputs(scene.particles, device=dev)
+    P, C = params.P, params.flat.shape[0]
+    red = gdist.VisibleUnionReducer(P, C, dev)
+    st = G.Settings(rho=scene.rho)
+    cams = scene.cameras[:8]
+    r = G.Renderer(P, cams[0].width, cams[0].height, device=dev)
+    for c in cams:
+        r.forward(params, c, st)
+        red.add_view(r.frame)
+    union = int(red.mask.sum().item())
+    flat = torch.randn((C, P), dtype=torch.float32, device=dev)
+    packed, u = red.pack(flat, red.mask, force=True)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        red.pack(flat, red.mask, stream, force=True)
+        red.unpack(packed, None, flat, stream)
+    b.record(stream)
+    b.synchronize()
+    return {"views": len(cams), "union_particles": union, "union_frac": union / P,
+            "allreduce_bytes_dense": 4 * C * P, "allreduce_bytes_compact": 4 * C * union,
+            "index_pack_unpack_ms": a.elapsed_time(b) / steps,
+            "used_when": "union <= 0.5 P (VisibleUnionReducer.max_union); above it the dense allreduce runs",
+            "note": "view-DP allreduce of only the union of the ranks' visible particles (one host read of U)"}
 
 def time_loss_front_end(G, params, cam, st, frame, grads, image, flush, stream, steps, dev):
     """Eq. 9's loss on the bench frame (mask M_omega at omega = 0.75, L1 + SSIM + L_omega and

@@ -417,6 +417,36 @@ ges_status ges_mix_fit(const ges_mix_run *runs, int32_t n_runs, float *params, f
 ges_status ges_theorem1_errors(const float *alpha, int32_t na, const float *beta, int32_t nb, float A, float L,
                                int32_t intervals, float *E, void *stream);
 
+/* ---- view data parallelism: visible-union compaction of the gradient allreduce
+ * (SURVEY.md §8(e)).  A particle no view of any rank saw has a zero gradient on
+ * every rank, so only the union of the ranks' visible sets is reduced:
+ *   ges_mask_visible per view (mask |= visible), a MAX allreduce of the P-byte
+ *   mask, ges_grad_index, then (when U is small enough) ges_grad_pack, an
+ *   allreduce of the C * U packed floats and ges_grad_unpack. */
+
+/* mask[i] = 1 for every particle the frame's last ges_preprocess marked visible
+ * (other entries untouched).  mask: device uint8 [P]. */
+ges_status ges_mask_visible(const ges_frame *frame, uint8_t *mask, void *stream);
+
+/* Bytes of device workspace for ges_grad_index on P particles. */
+size_t ges_grad_pack_workspace_bytes(int64_t P);
+
+/* idx (device int32 [P]) <- the i with mask[i] != 0 in ascending order, *U (device
+ * int64) <- their count.  No synchronisation; read *U on the host to decide and to
+ * size the allreduce (compaction pays when U is well below P). */
+ges_status ges_grad_index(int64_t P, const uint8_t *mask, void *workspace, size_t workspace_bytes, int32_t *idx,
+                          int64_t *U, void *stream);
+
+/* packed (device float, >= C U) <- planar [C][U], packed[c U + k] = grads[c P + idx[k]]
+ * for k < *U.  grads: the planar [C][P] buffer. */
+ges_status ges_grad_pack(const float *grads, int64_t P, int32_t C, const int32_t *idx, const int64_t *U,
+                         float *packed, void *stream);
+
+/* grads[c P + idx[k]] = packed[c U + k] for k < *U (the reduced rows back into
+ * the planar buffer; the other entries are left as they are -- zero). */
+ges_status ges_grad_unpack(const float *packed, int64_t P, int32_t C, const int32_t *idx, const int64_t *U,
+                           float *grads, void *stream);
+
 /* Diagnostic: `blocks` x 256 threads each run 8 independent chains of `iters`
  * MUFU ex2 (8 iters blocks 256 results in total); out: device [blocks * 256].
  * The caller times it: the measured special-function rate is the roofline

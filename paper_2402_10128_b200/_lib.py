@@ -110,7 +110,8 @@ EXPORTS = ["ges_workspace_bytes", "ges_frame_init", "ges_preprocess", "ges_sort"
            "ges_status_string", "ges_version", "ges_loss_mask_dims", "ges_loss_workspace_bytes", "ges_loss_mask",
            "ges_loss", "ges_lr_position", "ges_adam_step", "ges_reset", "ges_densify_stats",
            "ges_densify_workspace_bytes", "ges_densify_prune", "ges_mix_signal", "ges_mix_eval", "ges_mix_fit",
-           "ges_theorem1_errors", "ges_probe_mufu"]
+           "ges_theorem1_errors", "ges_probe_mufu", "ges_mask_visible", "ges_grad_pack_workspace_bytes",
+           "ges_grad_index", "ges_grad_pack", "ges_grad_unpack"]
 
 _lib = None
 
@@ -192,6 +193,18 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         L.ges_theorem1_errors.restype = C.c_int
         L.ges_theorem1_errors.argtypes = [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_float, C.c_float,
                                           C.c_int32, C.c_void_p, C.c_void_p]
+        L.ges_mask_visible.restype = C.c_int
+        L.ges_mask_visible.argtypes = [C.POINTER(ges_frame), C.c_void_p, C.c_void_p]
+        L.ges_grad_pack_workspace_bytes.restype = C.c_size_t
+        L.ges_grad_pack_workspace_bytes.argtypes = [C.c_int64]
+        L.ges_grad_index.restype = C.c_int
+        L.ges_grad_index.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p,
+                                     C.c_void_p]
+        L.ges_grad_pack.restype = C.c_int
+        L.ges_grad_pack.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        L.ges_grad_unpack.restype = C.c_int
+        L.ges_grad_unpack.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_void_p]
         L.ges_probe_mufu.restype = C.c_int
         L.ges_probe_mufu.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]
         _lib = L

@@ -531,4 +531,34 @@ ges_status ges_probe_mufu(float* out, int32_t iters, int32_t blocks, void* strea
     return cuda_status(launch_mufu_probe(out, iters, blocks, (cudaStream_t)stream));
 }
 
+// ---- view-DP gradient compaction -----------------------------
+ges_status ges_mask_visible(const ges_frame* frame, uint8_t* mask, void* stream) {
+    if (!frame || !mask) return GES_ERR_INVALID_ARG;
+    return cuda_status(launch_mask_visible(frame->status, frame->P, mask, (cudaStream_t)stream));
+}
+
+size_t ges_grad_pack_workspace_bytes(int64_t P) {
+    if (P < 1) return 0;
+    return align_up(sizeof(int) * (size_t)grad_pack_blocks(P));
+}
+
+ges_status ges_grad_index(int64_t P, const uint8_t* mask, void* workspace, size_t workspace_bytes, int32_t* idx,
+                          int64_t* U, void* stream) {
+    if (P < 1 || P > 0x7fffffff || !mask || !workspace || !idx || !U) return GES_ERR_INVALID_ARG;
+    if (workspace_bytes < ges_grad_pack_workspace_bytes(P)) return GES_ERR_CAPACITY;
+    return cuda_status(launch_grad_index(P, mask, (int*)workspace, idx, (long long*)U, (cudaStream_t)stream));
+}
+
+ges_status ges_grad_pack(const float* grads, int64_t P, int32_t C, const int32_t* idx, const int64_t* U,
+                         float* packed, void* stream) {
+    if (!grads || P < 1 || P > 0x7fffffff || C < 1 || !idx || !U || !packed) return GES_ERR_INVALID_ARG;
+    return cuda_status(launch_grad_pack(grads, P, C, idx, (const long long*)U, packed, (cudaStream_t)stream));
+}
+
+ges_status ges_grad_unpack(const float* packed, int64_t P, int32_t C, const int32_t* idx, const int64_t* U,
+                           float* grads, void* stream) {
+    if (!packed || P < 1 || P > 0x7fffffff || C < 1 || !idx || !U || !grads) return GES_ERR_INVALID_ARG;
+    return cuda_status(launch_grad_unpack(packed, P, C, idx, (const long long*)U, grads, (cudaStream_t)stream));
+}
+
 }  // extern "C"

@@ -239,4 +239,14 @@ cudaError_t launch_mufu_probe(float* out, int iters, int blocks, cudaStream_t st
 cudaError_t launch_theorem1(const float* alpha, int na, const float* beta, int nb, float A, float L, int n, float* E,
                             cudaStream_t stream);
 
+// --- view-DP gradient compaction (grad_pack.cu) -----------------------------
+int64_t grad_pack_blocks(int64_t P);
+cudaError_t launch_mask_visible(const uint8_t* status, int64_t P, uint8_t* mask, cudaStream_t stream);
+cudaError_t launch_grad_index(int64_t P, const uint8_t* mask, int* counts, int* idx, long long* U,
+                              cudaStream_t stream);
+cudaError_t launch_grad_pack(const float* grads, int64_t P, int C, const int* idx, const long long* U, float* packed,
+                             cudaStream_t stream);
+cudaError_t launch_grad_unpack(const float* packed, int64_t P, int C, const int* idx, const long long* U,
+                               float* grads, cudaStream_t stream);
+
 }  // namespace ges

@@ -16,13 +16,15 @@ with the same allreduce.
 """
 from __future__ import annotations
 
+import ctypes as C
 import dataclasses
 from typing import List, Sequence
 
 import torch
 import torch.distributed as dist
 
-from .api import PlanarParams, Renderer, Settings
+from . import _lib as L
+from .api import Frame, PlanarParams, Renderer, Settings, _stream
 
 TILE = 16
 
@@ -41,13 +43,80 @@ def allreduce_grads(flat: torch.Tensor, group=None) -> torch.Tensor:
     return flat
 
 
+def allreduce_visible_union(flat: torch.Tensor, mask: torch.Tensor, pack, unpack, group=None) -> torch.Tensor:
+    """Visible-union compaction of the view-DP allreduce: OR the
+    ranks' visibility masks (a MAX allreduce of P bytes), pack the gradient rows of
+    the union, allreduce only those C U floats, unpack.  Particles outside the union
+    have zero gradient on every rank, so the result equals the dense allreduce.
+    pack(flat, mask) -> (packed 1-D tensor of C U floats, or None when the union is
+    too large for compaction to pay -- then the dense buffer is reduced -- , state);
+    unpack(packed, state, flat) writes the reduced rows back."""
+    world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+    if world > 1:
+        dist.all_reduce(mask, op=dist.ReduceOp.MAX, group=group)
+    packed, state = pack(flat, mask)
+    if packed is None:
+        return allreduce_grads(flat, group)
+    if world > 1 and packed.numel():
+        dist.all_reduce(packed, op=dist.ReduceOp.SUM, group=group)
+    unpack(packed, state, flat)
+    return flat
+
+
+class VisibleUnionReducer:
+    """Device buffers and the CUDA pack / unpack (ges_mask_visible, ges_grad_pack,
+    ges_grad_unpack) for allreduce_visible_union over a planar [C][P] gradient."""
+
+    def __init__(self, P: int, n_planes: int, device="cuda", max_union: float = 0.5):
+        # compaction moves 4 C U bytes twice on each rank to save 4 C (P - U) on the wire:
+        # above max_union P the dense allreduce is used
+        self.P, self.C, self.max_union = P, n_planes, max_union
+        self.mask = torch.zeros(P, dtype=torch.uint8, device=device)
+        self.idx = torch.empty(P, dtype=torch.int32, device=device)
+        self.U = torch.zeros(1, dtype=torch.int64, device=device)
+        self.packed = torch.empty(n_planes * P, dtype=torch.float32, device=device)
+        self.ws = torch.empty(max(1, L.load().ges_grad_pack_workspace_bytes(P)), dtype=torch.uint8, device=device)
+
+    def reset(self) -> None:
+        self.mask.zero_()
+
+    def add_view(self, frame: Frame, stream=None) -> None:
+        """Marks the particles the frame's last ges_preprocess found visible."""
+        L.check(L.load().ges_mask_visible(C.byref(frame.c), C.c_void_p(self.mask.data_ptr()),
+                                          C.c_void_p(_stream(stream))), "ges_mask_visible")
+
+    def pack(self, flat: torch.Tensor, mask: torch.Tensor, stream=None, force: bool = False):
+        lib = L.load()
+        L.check(lib.ges_grad_index(self.P, C.c_void_p(mask.data_ptr()), C.c_void_p(self.ws.data_ptr()),
+                                   self.ws.numel(), C.c_void_p(self.idx.data_ptr()), C.c_void_p(self.U.data_ptr()),
+                                   C.c_void_p(_stream(stream))), "ges_grad_index")
+        u = int(self.U.item())  # the one host read: the decision and the allreduce's size
+        if not force and u > self.max_union * self.P:
+            return None, u
+        L.check(lib.ges_grad_pack(C.c_void_p(flat.data_ptr()), self.P, self.C, C.c_void_p(self.idx.data_ptr()),
+                                  C.c_void_p(self.U.data_ptr()), C.c_void_p(self.packed.data_ptr()),
+                                  C.c_void_p(_stream(stream))), "ges_grad_pack")
+        return self.packed[: self.C * u], u
+
+    def unpack(self, packed: torch.Tensor, state, flat: torch.Tensor, stream=None) -> None:
+        L.check(L.load().ges_grad_unpack(C.c_void_p(packed.data_ptr()), self.P, self.C,
+                                         C.c_void_p(self.idx.data_ptr()), C.c_void_p(self.U.data_ptr()),
+                                         C.c_void_p(flat.data_ptr()), C.c_void_p(_stream(stream))),
+                "ges_grad_unpack")
+
+    def allreduce(self, flat: torch.Tensor, group=None) -> torch.Tensor:
+        return allreduce_visible_union(flat, self.mask, self.pack, self.unpack, group)
+
+
 class ViewDataParallel:
     """Renders this rank's views of one particle set and returns the
     allreduced parameter gradients of sum_v <dL/dimage_v, image_v>."""
 
     def __init__(self, params: PlanarParams, cameras: Sequence, settings: Settings, rank: int, world: int,
-                 device="cuda", group=None):
+                 device="cuda", group=None, compact: bool = False):
         self.params, self.cameras, self.settings = params, list(cameras), settings
+        # compact: reduce only the union of the ranks' visible particles (VisibleUnionReducer)
+        self.reducer = VisibleUnionReducer(params.P, params.flat.shape[0], device) if compact else None
         self.views = views_for_rank(len(self.cameras), rank, world)
         self.group = group
         cam0 = self.cameras[0]
@@ -63,16 +132,23 @@ class ViewDataParallel:
     def step(self, dL_dimages: dict, stream=None) -> PlanarParams:
         """dL_dimages: view -> [3][H][W] device tensor, for this rank's views."""
         first = True
+        if self.reducer is not None:
+            self.reducer.reset()
         for v in self.views:
             cam = self.cameras[v]
             r = self.renderers[(cam.width, cam.height)]
             self.images[v] = r.forward(self.params, cam, self.settings, stream=stream)
+            if self.reducer is not None:
+                self.reducer.add_view(r.frame, stream)
             r.backward(self.params, cam, self.settings, dL_dimages[v], grads=self.grads,
                        accumulate=not first, stream=stream)
             first = False
         if first:  # no views on this rank: contribute zeros
             self.grads.flat.zero_()
-        allreduce_grads(self.grads.flat, self.group)
+        if self.reducer is not None:
+            self.reducer.allreduce(self.grads.flat, self.group)
+        else:
+            allreduce_grads(self.grads.flat, self.group)
         return self.grads
 
 

@@ -148,3 +148,68 @@ def test_band_gather_and_gradient_allreduce_world2():
         img, flat = out[r]
         assert np.array_equal(img, ref["image"])
         assert np.allclose(flat, ref_flat, rtol=1e-5, atol=1e-6)
+
+
+# --------------------------------------------------------------------------
+# visible-union compaction of the view-DP allreduce
+# --------------------------------------------------------------------------
+def _view_grads_and_mask(sc, v):
+    cam = sc.cameras[v]   # zoomed in 3x: each view sees part of the object
+    cam = gi.Camera(96, 96, 3 * cam.fx * 96 / 800, 3 * cam.fy * 96 / 800, 48.0, 48.0, cam.near, cam.R, cam.t)
+    g = gi.upstream_grad(sc.seed, v, 96, 96)
+    r = O.render_and_grad(sc.particles, cam, O.Settings(), g)
+    pre = O.preprocess(sc.particles, cam, O.Settings(), "f32")
+    return _flat(r["grads"], sc.particles.K), (pre["status"] == O.VISIBLE).astype(np.uint8)
+
+
+def _np_pack(flat, mask):
+    idx = np.nonzero(mask.numpy())[0]
+    return torch.from_numpy(np.ascontiguousarray(flat.numpy()[:, idx]).reshape(-1)), idx
+
+
+def _np_unpack(packed, idx, flat):
+    flat.numpy()[:, idx] = packed.numpy().reshape(flat.shape[0], idx.size)
+
+
+def _union_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sc = _scene()
+        flat = torch.zeros((sc.particles.n_planes(), sc.particles.P), dtype=torch.float32)
+        mask = torch.zeros(sc.particles.P, dtype=torch.uint8)
+        for v in gdist.views_for_rank(N_VIEWS, rank, world):
+            g, m = _view_grads_and_mask(sc, v)
+            flat += torch.from_numpy(g)
+            mask |= torch.from_numpy(m)
+        local_mask = mask.clone()
+        gdist.allreduce_visible_union(flat, mask, _np_pack, _np_unpack)
+        out[rank] = (flat.numpy().copy(), mask.numpy().copy(), local_mask.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_visible_union_allreduce_world2():
+    """The compacted allreduce equals the dense one: every rank ends with the sum over
+    all views, the union mask is the OR of the ranks' masks, and no gradient outside
+    the union is nonzero anywhere (what makes the compaction exact)."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    port = _free_port()
+    mp.spawn(_union_worker, args=(world, port, out), nprocs=world, join=True)
+    sc = _scene()
+    gs = [_view_grads_and_mask(sc, v) for v in range(N_VIEWS)]
+    ref = sum(g.astype(np.float64) for g, _ in gs)
+    union = np.zeros(sc.particles.P, np.uint8)
+    for _, m in gs:
+        union |= m
+    assert np.all(ref[:, union == 0] == 0.0)
+    assert 0 < union.sum() < sc.particles.P
+    for r in range(world):
+        flat, mask, local = out[r]
+        assert np.array_equal(mask, union)
+        assert np.allclose(flat, ref, rtol=1e-5, atol=1e-6)
+    assert np.array_equal(out[0][0], out[1][0])
+    assert not np.array_equal(out[0][2], out[1][2])   # the ranks saw different particles
