@@ -57,8 +57,8 @@ STAGE_KERNEL = {"preprocess": "preprocess_tma_kernel", "render_fwd": "render_fwd
 
 def committed_traffic(stage):
     """DRAM bytes per launch of the stage's kernel from the committed ncu --set full
-    capture (profiles/r1d_traffic.json, written by tools/summarize_ncu.py traffic), or None."""
-    p = os.path.join(ROOT, "profiles", "r1d_traffic.json")
+    capture (profiles/r1h_traffic.json, written by tools/summarize_ncu.py traffic), or None."""
+    p = os.path.join(ROOT, "profiles", "r1h_traffic.json")
     k = STAGE_KERNEL.get(stage)
     if not k or not os.path.exists(p):
         return None, None
