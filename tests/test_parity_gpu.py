@@ -383,3 +383,47 @@ def test_exact_kernel_bands_match_full_frame():
         floor = 1e-6 + 1e-6 * np.abs(g_full[n]).max()
         bad = np.abs(a - g_full[n]) > np.maximum(1e-3 * np.abs(g_full[n]), floor)
         assert bad.sum() == 0, (n, int(bad.sum()))
+
+
+def test_step_captured_as_cuda_graph_matches_direct_launches():
+    """The API is stream-ordered and capture-safe (bench.py replays S1-S5 as one CUDA
+    graph): a captured step reproduces the directly launched step's image and lists
+    bit for bit, and its gradients up to float-atomic reordering."""
+    sc = gi.make_config(1, P=20000)
+    cam = sc.cameras[0]
+    st = G.Settings(rho=sc.rho)
+    params = G.PlanarParams.from_inputs(sc.particles)
+    r = G.Renderer(params.P, cam.width, cam.height)
+    img0 = torch.empty((3, cam.height, cam.width), device="cuda")
+    r.forward(params, cam, st, image=img0)
+    r.grow(int(r.frame.counts().slots))
+    frame = r.frame
+    dL = torch.from_numpy(gi.upstream_grad(sc.seed, 0, cam.width, cam.height)).cuda()
+    s = torch.cuda.current_stream()
+    img_a = torch.empty_like(img0)
+    g_a = G.PlanarParams.zeros(params.P, params.sh_degree)
+    G.ges_preprocess(params, cam, st, frame, s)
+    G.ges_sort(frame, s)
+    G.ges_render_fwd(frame, st, img_a, None, s)
+    G.ges_render_bwd(params, cam, st, frame, dL, g_a, False, s)
+    torch.cuda.synchronize()
+    lst_a = frame.list(int(frame.counts().pairs)).clone()
+    img_b = torch.full_like(img0, -1.0)
+    g_b = G.PlanarParams.zeros(params.P, params.sh_degree)
+    graph = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    cap.wait_stream(s)
+    with torch.cuda.graph(graph, stream=cap):
+        G.ges_preprocess(params, cam, st, frame, cap)
+        G.ges_sort(frame, cap)
+        G.ges_render_fwd(frame, st, img_b, None, cap)
+        G.ges_render_bwd(params, cam, st, frame, dL, g_b, False, cap)
+    s.wait_stream(cap)
+    graph.replay()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(img_a, img_b)
+    assert torch.equal(lst_a, frame.list(int(frame.counts().pairs)))
+    a, b = g_a.flat.cpu().numpy(), g_b.flat.cpu().numpy()
+    floor = 1e-6 + 1e-6 * np.abs(a).max()
+    assert np.all(np.abs(a - b) <= np.maximum(1e-4 * np.abs(a), floor))
