@@ -429,13 +429,21 @@ int or_render_fwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
  * Accumulation order is fixed: tiles ascending, pixels row-major within the
  * tile, list order -- independent of the thread count. */
 int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets, const int32_t *list,
-                  const uint8_t *tile_mask, const double *dL_dimg, double *g2d) {
+                  const uint8_t *tile_mask, const double *dL_dimg, double *g2d, double *g2d_abs) {
     const int W = sc->width, H = sc->height;
     const int64_t P = s->P;
     const int64_t T = (int64_t)sc->tiles_x * sc->tiles_y;
     const int64_t total = offsets[T];
     double *acc = (double *)calloc((size_t)(total > 0 ? total : 1) * 10, sizeof(double));
     if (!acc) return -1;
+    /* R19: the same sums with every operand replaced by its magnitude and every
+     * difference by a sum (sum over terms of |term|), for the condition number
+     * sum|terms| / |sum| of each gradient entry. */
+    double *aab = NULL;
+    if (g2d_abs) {
+        aab = (double *)calloc((size_t)(total > 0 ? total : 1) * 10, sizeof(double));
+        if (!aab) { free(acc); return -1; }
+    }
 #pragma omp parallel
     {
         int64_t maxn = 0;
@@ -459,7 +467,8 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
                     const int nr = composite_pixel(s, lst, n, px + 0.5, py + 0.5, C, &Tf, &nc, &ne, &am, rec);
                     const double g[3] = {dL_dimg[pix], dL_dimg[(int64_t)W * H + pix], dL_dimg[2 * (int64_t)W * H + pix]};
                     const double gbg = g[0] * sc->bg[0] + g[1] * sc->bg[1] + g[2] * sc->bg[2];
-                    double suffix = 0.0;
+                    const double gbg_abs = fabs(g[0] * sc->bg[0]) + fabs(g[1] * sc->bg[1]) + fabs(g[2] * sc->bg[2]);
+                    double suffix = 0.0, suffix_abs = 0.0;
                     for (int r = nr - 1; r >= 0; --r) {
                         const OrComp *c = &rec[r];
                         const int32_t i = c->idx;
@@ -468,14 +477,31 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
                         suffix += cg * c->alpha * c->T;
                         double *o = a9 + (int64_t)c->k * 10;
                         for (int ch = 0; ch < 3; ++ch) o[6 + ch] += c->alpha * c->T * g[ch];
+                        /* R19 magnitudes: the same expressions over |operands| */
+                        double *ob = aab ? aab + (offsets[t] + c->k) * 10 : NULL;
+                        double dalpha_abs = 0.0;
+                        if (ob) {
+                            const double cg_abs = fabs(s->rgb[i] * g[0]) + fabs(s->rgb[P + i] * g[1]) +
+                                                  fabs(s->rgb[2 * P + i] * g[2]);
+                            dalpha_abs = c->T * cg_abs + (suffix_abs + Tf * gbg_abs) / (1.0 - c->alpha);
+                            suffix_abs += cg_abs * c->alpha * c->T;
+                            for (int ch = 0; ch < 3; ++ch) ob[6 + ch] += fabs(c->alpha * c->T * g[ch]);
+                        }
                         if (c->clamped) continue;
                         o[5] += c->G * dalpha;
                         double dpow = c->pos_power ? 0.0 : c->araw * dalpha;
+                        double dpow_abs = c->pos_power ? 0.0 : c->araw * dalpha_abs;
+                        if (ob) ob[5] += c->G * dalpha_abs;
                         if (s->hbeta) {
                             const double hb = s->hbeta[i];
                             const double d_all = c->araw * dalpha;  /* dL/dpower of the GEF power */
                             o[9] += c->Q > 0.0 ? d_all * (-0.25 * c->Qb * log(c->Q)) : 0.0;
                             dpow = c->Q > 0.0 ? d_all * hb * pow(c->Q, hb - 1.0) : 0.0;
+                            if (ob) {
+                                const double d_all_abs = c->araw * dalpha_abs;
+                                ob[9] += c->Q > 0.0 ? d_all_abs * fabs(0.25 * c->Qb * log(c->Q)) : 0.0;
+                                dpow_abs = c->Q > 0.0 ? d_all_abs * hb * pow(c->Q, hb - 1.0) : 0.0;
+                            }
                         }
                         const double ca = s->conic[i], cb = s->conic[P + i], cc = s->conic[2 * P + i];
                         const double dx = c->dx, dy = c->dy;
@@ -484,6 +510,13 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
                         o[2] += dpow * (-0.5 * dx * dx);
                         o[3] += dpow * (-dx * dy);
                         o[4] += dpow * (-0.5 * dy * dy);
+                        if (ob) {
+                            ob[0] += dpow_abs * (fabs(ca * dx) + fabs(cb * dy));
+                            ob[1] += dpow_abs * (fabs(cb * dx) + fabs(cc * dy));
+                            ob[2] += dpow_abs * (0.5 * dx * dx);
+                            ob[3] += dpow_abs * fabs(dx * dy);
+                            ob[4] += dpow_abs * (0.5 * dy * dy);
+                        }
                     }
                 }
         }
@@ -496,6 +529,17 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
             const int32_t i = list[k];
             for (int c = 0; c < 10; ++c) g2d[c * P + i] += acc[k * 10 + c];
         }
+    }
+    if (g2d_abs) {
+        memset(g2d_abs, 0, sizeof(double) * 10 * (size_t)P);
+        for (int64_t t = 0; t < T; ++t) {
+            if (tile_mask && !tile_mask[t]) continue;
+            for (int64_t k = offsets[t]; k < offsets[t + 1]; ++k) {
+                const int32_t i = list[k];
+                for (int c = 0; c < 10; ++c) g2d_abs[c * P + i] += aab[k * 10 + c];
+            }
+        }
+        free(aab);
     }
     free(acc);
     return 0;
@@ -549,8 +593,21 @@ static void sh_basis_grad(double x, double y, double z, int K, double dY[16][3])
  * opacity_logit 1, sh 3K, beta 1.  status/flags (may be NULL) take the
  * visibility and clamp decisions from the fp32 path (the kernel's precision);
  * otherwise they are recomputed in fp64. */
-int or_backward_particles(const OrParticles_f64 *pp, const OrCamera *cam, const OrSettings *st,
-                          const double *g2d, const int32_t *status_in, const int32_t *flags_in, double *grads) {
+static void mat_abs(int n, const double *A, double *out) {
+    for (int i = 0; i < n; ++i) out[i] = fabs(A[i]);
+}
+
+/* absmode = 0: the gradients.  absmode = 1 (R19): the same chain evaluated over
+ * magnitudes -- g2d holds the S5a sums of |terms|, every coefficient and matrix
+ * is replaced by its absolute value (AB), every difference of terms by their
+ * sum -- giving sum|terms| of each parameter gradient, the denominator of its
+ * condition number.  AB() is the identity when absmode = 0, and every wrapped
+ * expression is written so that its value there is bit-identical to the plain
+ * chain (a - b == a + (-b)). */
+static int backward_particles_impl(const OrParticles_f64 *pp, const OrCamera *cam, const OrSettings *st,
+                                   const double *g2d, const int32_t *status_in, const int32_t *flags_in,
+                                   double *grads, const int absmode) {
+#define AB(x) (absmode ? fabs(x) : (x))
     const int64_t P = pp->P;
     const int K = (pp->sh_degree + 1) * (pp->sh_degree + 1);
     const int n_planes = 3 + 3 + 4 + 1 + 3 * K + 1;
@@ -633,62 +690,81 @@ int or_backward_particles(const OrParticles_f64 *pp, const OrCamera *cam, const 
         double drgb[3] = {g2d[6 * P + i], g2d[7 * P + i], g2d[8 * P + i]};
 
         /* conic (a,b,c) = (C, -B, A) / det  ->  (A, B, C) */
-        const double gA = da * (-C * C / det2) + db * (B * C / det2) + dc * (1.0 / det - A * C / det2);
-        const double gB = da * (2.0 * B * C / det2) + db * (-1.0 / det - 2.0 * B * B / det2) + dc * (2.0 * A * B / det2);
-        const double gC = da * (1.0 / det - A * C / det2) + db * (A * B / det2) + dc * (-A * A / det2);
+        const double gA = da * AB(-C * C / det2) + db * AB(B * C / det2) + dc * (AB(1.0 / det) + AB(-A * C / det2));
+        const double gB = da * AB(2.0 * B * C / det2) + db * (AB(-1.0 / det) + AB(-2.0 * B * B / det2)) +
+                          dc * AB(2.0 * A * B / det2);
+        const double gC = da * (AB(1.0 / det) + AB(-A * C / det2)) + db * AB(A * B / det2) + dc * AB(-A * A / det2);
+        /* magnitudes of the forward matrices the adjoint multiplies by */
+        double aTm[6], aTmT[6], aSig[9], aM[9], aMT[9];
+        if (absmode) {
+            mat_abs(9, M, aM);
+            mat_T(3, 3, aM, aMT);
+            mat_mul(3, 3, 3, aM, aMT, aSig);
+            double aJ[6], aW[9];
+            mat_abs(6, J, aJ);
+            mat_abs(9, Wm, aW);
+            mat_mul(2, 3, 3, aJ, aW, aTm);
+            mat_T(2, 3, aTm, aTmT);
+        } else {
+            memcpy(aTm, Tm, sizeof aTm); memcpy(aTmT, TmT, sizeof aTmT);
+            memcpy(aSig, Sig, sizeof aSig); memcpy(aM, M, sizeof aM);
+        }
         /* cov = T Sig T^T, read entries (0,0), (0,1), (1,1) */
         const double Gc[4] = {gA, gB, 0.0, gC};
         double GcT[4], Gs[4];
         mat_T(2, 2, Gc, GcT);
         for (int k = 0; k < 4; ++k) Gs[k] = Gc[k] + GcT[k];
         double tmp6[6], dSig[9], dT[6];
-        mat_mul(2, 2, 3, Gc, Tm, tmp6);      /* Gc T      */
-        mat_mul(3, 2, 3, TmT, tmp6, dSig);   /* T^T Gc T  */
+        mat_mul(2, 2, 3, Gc, aTm, tmp6);     /* Gc T      */
+        mat_mul(3, 2, 3, aTmT, tmp6, dSig);  /* T^T Gc T  */
         double GsT[6];
-        mat_mul(2, 2, 3, Gs, Tm, GsT);       /* (Gc+Gc^T) T */
-        mat_mul(2, 3, 3, GsT, Sig, dT);      /* ... Sig     */
+        mat_mul(2, 2, 3, Gs, aTm, GsT);      /* (Gc+Gc^T) T */
+        mat_mul(2, 3, 3, GsT, aSig, dT);     /* ... Sig     */
         /* Sig = M M^T */
         double dSigS[9], dM[9];
         for (int j = 0; j < 3; ++j) for (int k = 0; k < 3; ++k) dSigS[j * 3 + k] = dSig[j * 3 + k] + dSig[k * 3 + j];
-        mat_mul(3, 3, 3, dSigS, M, dM);
+        mat_mul(3, 3, 3, dSigS, aM, dM);
         /* M = R diag(se) */
         double dR[9], dse[3] = {0, 0, 0};
         for (int j = 0; j < 3; ++j)
-            for (int k = 0; k < 3; ++k) { dR[j * 3 + k] = dM[j * 3 + k] * se[k]; dse[k] += dM[j * 3 + k] * R[j * 3 + k]; }
+            for (int k = 0; k < 3; ++k) { dR[j * 3 + k] = dM[j * 3 + k] * se[k]; dse[k] += dM[j * 3 + k] * AB(R[j * 3 + k]); }
         double dbeta = 0.0;
         for (int k = 0; k < 3; ++k) {
             gls[k * P + i] = dse[k] * se[k];
-            dbeta += dse[k] * s[k] * dm_dbeta;
+            dbeta += dse[k] * s[k] * AB(dm_dbeta);
         }
         gbeta[i] = dbeta + (st->kernel == 1 ? g2d[9 * P + i] : 0.0);  /* exact GEF: the direct term */
         /* R(q-hat) partials */
         double dqh[4];
-        dqh[0] = dR[1] * (-2 * z) + dR[2] * (2 * y) + dR[3] * (2 * z) + dR[5] * (-2 * x) + dR[6] * (-2 * y) + dR[7] * (2 * x);
-        dqh[1] = dR[1] * (2 * y) + dR[2] * (2 * z) + dR[3] * (2 * y) + dR[4] * (-4 * x) + dR[5] * (-2 * w) +
-                 dR[6] * (2 * z) + dR[7] * (2 * w) + dR[8] * (-4 * x);
-        dqh[2] = dR[0] * (-4 * y) + dR[1] * (2 * x) + dR[2] * (2 * w) + dR[3] * (2 * x) + dR[5] * (2 * z) +
-                 dR[6] * (-2 * w) + dR[7] * (2 * z) + dR[8] * (-4 * y);
-        dqh[3] = dR[0] * (-4 * z) + dR[1] * (-2 * w) + dR[2] * (2 * x) + dR[3] * (2 * w) + dR[4] * (-4 * z) +
-                 dR[5] * (2 * y) + dR[6] * (2 * x) + dR[7] * (2 * y);
+        dqh[0] = dR[1] * AB(-2 * z) + dR[2] * AB(2 * y) + dR[3] * AB(2 * z) + dR[5] * AB(-2 * x) +
+                 dR[6] * AB(-2 * y) + dR[7] * AB(2 * x);
+        dqh[1] = dR[1] * AB(2 * y) + dR[2] * AB(2 * z) + dR[3] * AB(2 * y) + dR[4] * AB(-4 * x) + dR[5] * AB(-2 * w) +
+                 dR[6] * AB(2 * z) + dR[7] * AB(2 * w) + dR[8] * AB(-4 * x);
+        dqh[2] = dR[0] * AB(-4 * y) + dR[1] * AB(2 * x) + dR[2] * AB(2 * w) + dR[3] * AB(2 * x) + dR[5] * AB(2 * z) +
+                 dR[6] * AB(-2 * w) + dR[7] * AB(2 * z) + dR[8] * AB(-4 * y);
+        dqh[3] = dR[0] * AB(-4 * z) + dR[1] * AB(-2 * w) + dR[2] * AB(2 * x) + dR[3] * AB(2 * w) + dR[4] * AB(-4 * z) +
+                 dR[5] * AB(2 * y) + dR[6] * AB(2 * x) + dR[7] * AB(2 * y);
         const double qh[4] = {w, x, y, z};
-        const double dotq = qh[0] * dqh[0] + qh[1] * dqh[1] + qh[2] * dqh[2] + qh[3] * dqh[3];
-        for (int k = 0; k < 4; ++k) gq[k * P + i] = (dqh[k] - qh[k] * dotq) / nq;
+        const double dotq = AB(qh[0]) * dqh[0] + AB(qh[1]) * dqh[1] + AB(qh[2]) * dqh[2] + AB(qh[3]) * dqh[3];
+        for (int k = 0; k < 4; ++k) gq[k * P + i] = (dqh[k] + AB(-qh[k]) * dotq) / nq;
         /* T = J W  ->  dJ = dT W^T */
         double WT[9], dJ[6];
         mat_T(3, 3, Wm, WT);
+        if (absmode) mat_abs(9, WT, WT);
         mat_mul(2, 3, 3, dT, WT, dJ);
         double dt[3] = {0, 0, 0};
         const double tz2 = tz * tz, tz3 = tz2 * tz;
-        dt[2] += dJ[0] * (-fx / tz2) + dJ[4] * (-fy / tz2);
-        if (!clx) { dt[0] += dJ[2] * (-fx / tz2); dt[2] += dJ[2] * (2.0 * fx * tx / tz3); }
-        else { dt[2] += dJ[2] * (fx * Lx / tz2); }
-        if (!cly) { dt[1] += dJ[5] * (-fy / tz2); dt[2] += dJ[5] * (2.0 * fy * ty / tz3); }
-        else { dt[2] += dJ[5] * (fy * Ly / tz2); }
+        dt[2] += dJ[0] * AB(-fx / tz2) + dJ[4] * AB(-fy / tz2);
+        if (!clx) { dt[0] += dJ[2] * AB(-fx / tz2); dt[2] += dJ[2] * AB(2.0 * fx * tx / tz3); }
+        else { dt[2] += dJ[2] * AB(fx * Lx / tz2); }
+        if (!cly) { dt[1] += dJ[5] * AB(-fy / tz2); dt[2] += dJ[5] * AB(2.0 * fy * ty / tz3); }
+        else { dt[2] += dJ[5] * AB(fy * Ly / tz2); }
         /* projection u = fx tx/tz + cx, v = fy ty/tz + cy */
-        dt[0] += du * fx / tz; dt[2] += du * (-fx * tx / tz2);
-        dt[1] += dv * fy / tz; dt[2] += dv * (-fy * ty / tz2);
+        dt[0] += AB(du * fx / tz); dt[2] += du * AB(-fx * tx / tz2);
+        dt[1] += AB(dv * fy / tz); dt[2] += dv * AB(-fy * ty / tz2);
         double dmean[3];
-        for (int k = 0; k < 3; ++k) dmean[k] = Wm[0 * 3 + k] * dt[0] + Wm[1 * 3 + k] * dt[1] + Wm[2 * 3 + k] * dt[2];
+        for (int k = 0; k < 3; ++k)
+            dmean[k] = AB(Wm[0 * 3 + k]) * dt[0] + AB(Wm[1 * 3 + k]) * dt[1] + AB(Wm[2 * 3 + k]) * dt[2];
         /* colour: rgb = sum_k Y_k(dir) sh_k + 0.5, clamped at 0 */
         const double d[3] = {m[0] - ccen[0], m[1] - ccen[1], m[2] - ccen[2]};
         const double dn = sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
@@ -700,12 +776,12 @@ int or_backward_particles(const OrParticles_f64 *pp, const OrCamera *cam, const 
         double ddir[3] = {0, 0, 0};
         for (int k = 0; k < K; ++k)
             for (int ch = 0; ch < 3; ++ch) {
-                gsh[(int64_t)(3 * k + ch) * P + i] = Y[k] * drgb[ch];
+                gsh[(int64_t)(3 * k + ch) * P + i] = AB(Y[k]) * drgb[ch];
                 const double shv = pp->sh[(int64_t)(3 * k + ch) * P + i];
-                for (int e = 0; e < 3; ++e) ddir[e] += drgb[ch] * shv * dY[k][e];
+                for (int e = 0; e < 3; ++e) ddir[e] += AB(drgb[ch] * shv * dY[k][e]);
             }
-        const double dotd = dir[0] * ddir[0] + dir[1] * ddir[1] + dir[2] * ddir[2];
-        for (int e = 0; e < 3; ++e) dmean[e] += (ddir[e] - dir[e] * dotd) / dn;
+        const double dotd = AB(dir[0]) * ddir[0] + AB(dir[1]) * ddir[1] + AB(dir[2]) * ddir[2];
+        for (int e = 0; e < 3; ++e) dmean[e] += (ddir[e] + AB(-dir[e]) * dotd) / dn;
         for (int e = 0; e < 3; ++e) gmean[e * P + i] = dmean[e];
         /* opacity */
         const double kap = 1.0 / (1.0 + exp(-pp->opacity_logit[i]));
@@ -714,6 +790,20 @@ int or_backward_particles(const OrParticles_f64 *pp, const OrCamera *cam, const 
     free(st64);
     free(fl64);
     return 0;
+#undef AB
+}
+
+int or_backward_particles(const OrParticles_f64 *pp, const OrCamera *cam, const OrSettings *st,
+                          const double *g2d, const int32_t *status_in, const int32_t *flags_in, double *grads) {
+    return backward_particles_impl(pp, cam, st, g2d, status_in, flags_in, grads, 0);
+}
+
+/* R19: sum|terms| of every parameter gradient entry, from the S5a magnitudes
+ * g2d_abs of or_render_bwd (same layout as g2d). */
+int or_backward_particles_abs(const OrParticles_f64 *pp, const OrCamera *cam, const OrSettings *st,
+                              const double *g2d_abs, const int32_t *status_in, const int32_t *flags_in,
+                              double *bound) {
+    return backward_particles_impl(pp, cam, st, g2d_abs, status_in, flags_in, bound, 1);
 }
 
 int or_num_threads(void) {

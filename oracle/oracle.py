@@ -348,13 +348,15 @@ def render_fwd(pre, cam, st: Settings, offsets, lst, tile_mask=None) -> dict:
     return {"image": img, "final_T": fT, "n_contrib": nc, "n_eval": ne, "n_comp": ncomp, "amb": amb}
 
 
-def render_bwd(pre, cam, st: Settings, offsets, lst, dL_dimg, tile_mask=None) -> np.ndarray:
+def render_bwd(pre, cam, st: Settings, offsets, lst, dL_dimg, tile_mask=None, with_abs: bool = False):
     """S5a: per-particle 2D gradients g2d [10][P] = (du, dv, da, db, dc, dkappa, dr, dg, db, dbeta);
-    dbeta (the exact GEF kernel's direct shape term) is 0 for the phi-bar Gaussian kernel."""
+    dbeta (the exact GEF kernel's direct shape term) is 0 for the phi-bar Gaussian kernel.
+    with_abs: also return g2d_abs [10][P], the same sums over |terms| (R19), as (g2d, g2d_abs)."""
     keep = _Keep()
     sp = _splat(pre, keep)
     P = pre["status"].size
     g2d = np.zeros((10, P), np.float64)
+    g2d_abs = np.zeros((10, P), np.float64) if with_abs else None
     g = keep(np.ascontiguousarray(dL_dimg, dtype=np.float64))
     mp = None
     if tile_mask is not None:
@@ -362,9 +364,10 @@ def render_bwd(pre, cam, st: Settings, offsets, lst, dL_dimg, tile_mask=None) ->
         mp = _ptr(tile_mask, C.c_uint8)
     lst = keep(np.ascontiguousarray(lst if lst.size else np.zeros(1, np.int32), dtype=np.int32))
     rc = lib().or_render_bwd(C.byref(_screen(cam, st)), C.byref(sp), _ptr(offsets, C.c_int64),
-                             _ptr(lst, C.c_int32), mp, _ptr(g, C.c_double), _ptr(g2d, C.c_double))
+                             _ptr(lst, C.c_int32), mp, _ptr(g, C.c_double), _ptr(g2d, C.c_double),
+                             _ptr(g2d_abs, C.c_double) if with_abs else None)
     assert rc == 0
-    return g2d
+    return (g2d, g2d_abs) if with_abs else g2d
 
 
 def backward_particles(parts, cam, st: Settings, g2d, status=None, flags=None) -> dict:
@@ -380,6 +383,57 @@ def backward_particles(parts, cam, st: Settings, g2d, status=None, flags=None) -
     lib().or_backward_particles(C.byref(ps), C.byref(_cam(cam)), C.byref(_settings(st)), _ptr(g, C.c_double),
                                 sp, fp, _ptr(out, C.c_double))
     return split_planes(out, K)
+
+
+def grad_magnitude(parts, cam, st: Settings, g2d_abs, status, flags) -> dict:
+    """R19: sum over terms of |term| for every parameter gradient entry -- the S5b
+    chain evaluated over magnitudes (ges_oracle.c backward_particles_impl,
+    absmode) from the S5a magnitudes g2d_abs.  |g| <= bound always; the entry's
+    condition number is bound / |g|."""
+    keep = _Keep()
+    ps = _part_struct(parts, np.float64, keep)
+    P, K = parts.P, parts.K
+    n_planes = 3 + 3 + 4 + 1 + 3 * K + 1
+    out = np.zeros((n_planes, P), np.float64)
+    g = keep(np.ascontiguousarray(g2d_abs, dtype=np.float64))
+    sp = _ptr(keep(np.ascontiguousarray(status, np.int32)), C.c_int32)
+    fp = _ptr(keep(np.ascontiguousarray(flags, np.int32)), C.c_int32)
+    lib().or_backward_particles_abs(C.byref(ps), C.byref(_cam(cam)), C.byref(_settings(st)), _ptr(g, C.c_double),
+                                    sp, fp, _ptr(out, C.c_double))
+    return split_planes(out, K)
+
+
+def grad_error_scale(parts, cam, st: Settings, g2d, g2d_abs, status, flags) -> dict:
+    """R19: the first-order magnitude against which an fp32 evaluation of the
+    gradient chain is accurate, per parameter gradient entry:
+        scale = sum_j |L_j| g2d_abs_j  +  S5b_abs(|g2d|)
+    L = the per-particle linear map S5b (g2d -> parameter gradients), g2d_abs
+    the S5a sums of |terms| over pixels.  The first term bounds |L dg2d| for
+    per-term perturbations of the pixel sums (|dg2d_j| <= eps g2d_abs_j), the
+    second |dL g2d| for perturbations of the chain's own products.  An entry
+    whose scale / |g| is large is ill-conditioned: fp32 arithmetic on either
+    side moves it by ~eps * scale, however it is ordered."""
+    keep = _Keep()
+    ps = _part_struct(parts, np.float64, keep)
+    P, K = parts.P, parts.K
+    n_planes = 3 + 3 + 4 + 1 + 3 * K + 1
+    sp = _ptr(keep(np.ascontiguousarray(status, np.int32)), C.c_int32)
+    fp = _ptr(keep(np.ascontiguousarray(flags, np.int32)), C.c_int32)
+    c, s = _cam(cam), _settings(st)
+    total = np.zeros((n_planes, P), np.float64)
+    out = np.zeros((n_planes, P), np.float64)
+    e = np.zeros((10, P), np.float64)
+    for j in range(10 if int(st.kernel) == 1 else 9):
+        e[:] = 0.0
+        e[j] = g2d_abs[j]
+        lib().or_backward_particles(C.byref(ps), C.byref(c), C.byref(s), _ptr(e, C.c_double), sp, fp,
+                                    _ptr(out, C.c_double))
+        total += np.abs(out)
+    e[:] = np.abs(g2d)
+    lib().or_backward_particles_abs(C.byref(ps), C.byref(c), C.byref(s), _ptr(e, C.c_double), sp, fp,
+                                    _ptr(out, C.c_double))
+    total += out
+    return split_planes(total, K)
 
 
 def split_planes(flat, K):

@@ -64,20 +64,70 @@ def gpu_keys(out):
     return (tiles << np.uint64(32)) | db[lst]
 
 
-def ambiguous_particles(pre, amb_pixels, tiles_x):
-    """Particles whose rect covers a tile that holds an ambiguous pixel."""
-    ys, xs = np.nonzero(amb_pixels)
-    bad = np.zeros(pre["status"].size, bool)
-    if ys.size == 0:
-        return bad
-    tset = set(zip((ys // 16).tolist(), (xs // 16).tolist()))
-    x0, y0, x1, y1 = pre["rect"]
-    vis = pre["status"] == 0
-    for (ty, tx) in tset:
-        bad |= vis & (x0 <= tx) & (tx < x1) & (y0 <= ty) & (ty < y1)
-    return bad
-
-
 def grad_mismatch(ga, gr, rel=1e-3, floor=1e-6):
     """north_star: |g_gpu - g_ref| <= max(rel |g_ref|, floor)."""
     return np.abs(ga - gr) > np.maximum(rel * np.abs(gr), floor)
+
+
+# R19 (DESIGN.md): an fp32 evaluation of a gradient entry is accurate to about
+# R19_C * 2^-24 * scale, scale = the oracle's first-order magnitude of the entry
+# (oracle.grad_error_scale).  R19_C = 8 (per-term error: ex2.approx 2 ulp,
+# rcp.approx 1 ulp, ~5 roundings) + 24 (reduction depth: 5 SHFL levels, <= 19
+# levels of atomics and partial sums).
+EPS32 = 2.0 ** -24
+R19_C = 32.0
+
+
+def masked_upstream(dL, amb):
+    """dL/dimage with the oracle-flagged threshold-ambiguous pixels (R18) zeroed.
+    Every S5a term is linear in its pixel's dL/dC (and dL/dC . bg), so those
+    pixels drop out of both sides exactly and every particle can be compared."""
+    d = np.array(dL, np.float32, copy=True)
+    d[:, amb != 0] = 0.0
+    return d
+
+
+def oracle_grads(parts, cam, osx, pre, dL, offsets=None, lst=None):
+    """The oracle's S5 gradients and the R19 error scale of every entry."""
+    if offsets is None:
+        offsets, lst = O.tile_lists(pre)
+    g2d, gabs = O.render_bwd(pre, cam, osx, offsets, lst, dL, with_abs=True)
+    grads = O.backward_particles(parts, cam, osx, g2d, pre["status"], pre["flags"])
+    scale = O.grad_error_scale(parts, cam, osx, g2d, gabs, pre["status"], pre["flags"])
+    return grads, scale
+
+
+def check_grads(gg, ref, scale, status, label=""):
+    """Every visible particle's gradient entries against the oracle:
+    |g_gpu - g_ref| <= max(1e-3 |g_ref|, 1e-6)  (north_star), or, for entries
+    the oracle shows ill-conditioned (R19), <= R19_C eps32 scale.  Zero failures;
+    non-visible particles must have exactly zero gradients.  Returns a summary."""
+    vis = status == 0
+    V = int(vis.sum())
+    n_ent = n_strict = n_ill = n_bad = 0
+    worst_cond = 0.0
+    fails = []
+    for n in G.PARAM_NAMES:
+        a, r, s = gg[n], ref[n], scale[n]
+        assert np.all(a[..., ~vis] == 0.0), (n, "nonzero gradient of a non-visible particle")
+        a, r, s = a[..., vis], r[..., vis], s[..., vis]
+        d = np.abs(a - r)
+        strict = d <= np.maximum(1e-3 * np.abs(r), 1e-6)
+        ok = strict | (d <= R19_C * EPS32 * s)
+        n_ent += d.size
+        n_strict += int(strict.sum())
+        ill = ok & ~strict
+        n_ill += int(ill.sum())
+        if ill.any():
+            worst_cond = max(worst_cond, float((s[ill] / np.maximum(np.abs(r[ill]), 1e-30)).max()))
+        bad = ~ok
+        n_bad += int(bad.sum())
+        for idx in np.argwhere(bad)[:3]:
+            i = tuple(idx)
+            fails.append((n, i, float(a[i]), float(r[i]), float(s[i])))
+    msg = (f"[grad parity {label}] compared {V} of {V} visible particles ({n_ent} entries): "
+           f"{n_strict} within max(1e-3|g|, 1e-6), {n_ill} ill-conditioned (R19, max cond {worst_cond:.3g}) "
+           f"within {R19_C:g} eps32 x scale, {n_bad} failures")
+    print(msg)
+    assert n_bad == 0, (msg, fails[:10])
+    return {"visible": V, "entries": n_ent, "strict": n_strict, "ill_conditioned": n_ill}

@@ -273,6 +273,38 @@ def test_empty_scene_and_single_splat_at_center():
     assert np.allclose(out["image"][:, 16, 16], kappa * rgb + (1 - kappa) * bgc, atol=1e-12)
 
 
+def test_two_overlapping_splats_front_to_back_closed_form():
+    """Eq. 3 composites front to back: C = sum_i c_i a_i T_i with
+    T_i = prod_{j<i} (1 - a_j), i in increasing depth.  Two splats centred on the
+    same pixel centre (d = 0, G = 1, alpha = kappa) at depths z1 < z2 give
+    C = k1 c1 + (1 - k1) k2 c2 + (1 - k1)(1 - k2) bg.  Walking the list back to
+    front (or ordering by decreasing depth) gives k2 c2 + (1 - k2) k1 c1 + ... and
+    fails; so does compositing in index order (the far splat has the lower index)."""
+    cam = cam_identity(W=32, H=32, f=30.0)
+    bg = (0.1, 0.2, 0.3)
+    bgc = np.array([np.float32(c) for c in bg], np.float64)
+    z1, z2 = 3.0, 5.0
+    x1, x2 = (16.5 - 16.0) * z1 / 30.0, (16.5 - 16.0) * z2 / 30.0
+    sh_far = np.array([[0.9], [-0.6], [0.1]])
+    sh_near = np.array([[-0.7], [0.8], [0.3]])
+    mean = np.array([[x2, x1], [x2, x1], [z2, z1]])      # index 0 = far, index 1 = near
+    f32 = lambda a: np.ascontiguousarray(np.asarray(a, np.float64), np.float32)
+    parts = gi.Particles(f32(mean), f32(np.full((3, 2), -2.5)), f32(np.tile([[1.0], [0], [0], [0]], (1, 2))),
+                         f32([-0.2, 0.4]), f32(np.hstack([sh_far, sh_near])), f32([2.0, 2.0]), 0)
+    out = O.render(parts, cam, O.Settings(background=bg), "f64")
+    r32 = lambda v: np.asarray(v, np.float32).astype(np.float64)
+    k_far, k_near = 1 / (1 + math.exp(-r32(-0.2))), 1 / (1 + math.exp(-r32(0.4)))
+    Y00 = 0.5 / math.sqrt(math.pi)
+    c_far, c_near = Y00 * r32(sh_far[:, 0]) + 0.5, Y00 * r32(sh_near[:, 0]) + 0.5
+    front_to_back = k_near * c_near + (1 - k_near) * k_far * c_far + (1 - k_near) * (1 - k_far) * bgc
+    back_to_front = k_far * c_far + (1 - k_far) * k_near * c_near + (1 - k_near) * (1 - k_far) * bgc
+    got = out["image"][:, 16, 16]
+    assert np.abs(front_to_back - back_to_front).min() > 1e-2   # the two orders are distinguishable
+    assert np.allclose(got, front_to_back, rtol=0, atol=1e-12), (got, front_to_back, back_to_front)
+    assert abs(out["final_T"][16, 16] - (1 - k_near) * (1 - k_far)) < 1e-12
+    assert out["n_contrib"][16, 16] == 2
+
+
 def test_permutation_invariance_and_convexity():
     sc = gi.make_config(0, P=400)
     cam = sc.cameras[0]
@@ -541,3 +573,54 @@ def test_exact_membership_changes_nothing_but_the_lists():
         dx, dy = pre["uv"][0, i] - px, pre["uv"][1, i] - py
         alpha = pre["kappa"][i] * np.exp(-0.5 * (ca * dx * dx + cc * dy * dy) - cb * dx * dy)
         assert alpha.max() < 0.99 / 255
+
+
+# --------------------------------------------------------------------------
+# R19 magnitudes: sum over terms of |term| (the condition-number denominators)
+# --------------------------------------------------------------------------
+def test_r19_magnitudes_bound_the_gradients():
+    """|sum| <= sum |terms| for every S5a plane and every parameter gradient entry
+    (triangle inequality); the magnitudes are homogeneous of degree 1 in dL/dimage
+    and depend only on |dL/dimage| per term; with dL/dimage >= 0 and a black
+    background the colour planes have no cancellation (each term alpha T g >= 0)
+    and equal their sums exactly."""
+    sc = gi.make_config(0, P=600)
+    cam = sc.cameras[0]
+    st = O.Settings()
+    g = gi.upstream_grad(sc.seed, 0, cam.width, cam.height).astype(np.float64)
+    base = O.render(sc.particles, cam, st, "f32")
+    pre = base["pre"]
+    g2d, gabs = O.render_bwd(pre, cam, st, base["offsets"], base["list"], g, with_abs=True)
+    assert np.array_equal(g2d, O.render_bwd(pre, cam, st, base["offsets"], base["list"], g))
+    assert np.all(np.abs(g2d) <= gabs * (1 + 1e-12) + 1e-300)
+    scale = O.grad_error_scale(sc.particles, cam, st, g2d, gabs, pre["status"], pre["flags"])
+    grads = O.backward_particles(sc.particles, cam, st, g2d, pre["status"], pre["flags"])
+    for n in grads:
+        assert np.all(np.abs(grads[n]) <= scale[n] * (1 + 1e-12) + 1e-300), n
+    g2d2, gabs2 = O.render_bwd(pre, cam, st, base["offsets"], base["list"], 2.0 * g, with_abs=True)
+    assert np.allclose(gabs2, 2.0 * gabs, rtol=1e-13, atol=0)
+    gp = np.abs(g)
+    g2dp, gabsp = O.render_bwd(pre, cam, st, base["offsets"], base["list"], gp, with_abs=True)
+    assert np.array_equal(g2dp[6:9], gabsp[6:9])
+    # S5b over magnitudes: one plane, one single-term chain (opacity: dk kappa (1 - kappa))
+    e = np.zeros_like(g2d)
+    e[5] = gabs[5]
+    m = O.grad_magnitude(sc.particles, cam, st, e, pre["status"], pre["flags"])
+    ref = O.backward_particles(sc.particles, cam, st, e, pre["status"], pre["flags"])
+    assert np.allclose(m["opacity_logit"], np.abs(ref["opacity_logit"]), rtol=1e-15, atol=0)
+    assert np.all(m["sh"] == 0) and np.all(m["mean"] == 0)
+
+
+def test_r19_single_isotropic_splat_has_no_cancellation():
+    """One isotropic splat (b = 0), one pixel with a nonnegative upstream gradient,
+    black background: every S5a plane is a single term, so sum|terms| = |sum|."""
+    cam = cam_identity(W=32, H=32, f=30.0)
+    z = 3.0
+    p = one_particle([0.0, 0.0, z], [-2.2] * 3, logit=0.3)   # on the axis: conic b = 0 exactly
+    st = O.Settings()
+    base = O.render(p, cam, st, "f32")
+    g = np.zeros((3, 32, 32))
+    g[:, 16, 15] = [0.4, 1.1, 0.7]
+    g2d, gabs = O.render_bwd(base["pre"], cam, st, base["offsets"], base["list"], g, with_abs=True)
+    assert np.abs(g2d[:9]).min() > 0
+    assert np.allclose(np.abs(g2d[:9]), gabs[:9], rtol=1e-14, atol=0)
