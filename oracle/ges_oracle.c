@@ -314,6 +314,7 @@ typedef struct {
     double Q, Qb;   /* exact kernel: Mahalanobis^2 Q and Q^(beta/2) */
     int clamped;    /* araw >= 0.99 -> alpha = 0.99, no gradient to kappa/power */
     int pos_power;  /* raw power > 0 was clamped to 0 */
+    double ea, eT;  /* fp32 error bounds (R18 model): alpha relative, T_k relative */
 } OrComp;
 
 /* Front-to-back compositing of one pixel (Eq. 3 discretised: C = sum c_i a_i T_i,
@@ -327,7 +328,7 @@ typedef struct {
  * image may legitimately differ), bit1 = a 0.99-clamp decision does. */
 static int composite_pixel(const OrSplat2D *s, const int32_t *lst, int64_t n, double px, double py,
                            double C[3], double *T_out, int32_t *n_contrib, int32_t *n_eval, uint8_t *amb,
-                           OrComp *rec) {
+                           OrComp *rec, double *errT_out) {
     const int64_t P = s->P;
     double T = 1.0, errT = 0.0;
     int nrec = 0;
@@ -376,6 +377,7 @@ static int composite_pixel(const OrSplat2D *s, const int32_t *lst, int64_t n, do
             r->k = (int32_t)k; r->idx = i; r->alpha = alpha; r->T = T; r->G = G; r->araw = araw;
             r->dx = dx; r->dy = dy; r->clamped = !(araw < OR_ALPHA_MAX); r->pos_power = pos;
             r->Q = Q; r->Qb = Qb;
+            r->ea = erel; r->eT = errT;
         }
         ++nrec;
         T = Tn;
@@ -383,6 +385,7 @@ static int composite_pixel(const OrSplat2D *s, const int32_t *lst, int64_t n, do
         last = (int32_t)(k + 1);
     }
     *T_out = T;
+    if (errT_out) *errT_out = errT;
     *n_contrib = last;
     *n_eval = ne;
     *amb = a;
@@ -407,7 +410,7 @@ int or_render_fwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
                 const int64_t pix = (int64_t)py * W + px;
                 double C[3], Tf;
                 n_comp[pix] = composite_pixel(s, lst, n, px + 0.5, py + 0.5, C, &Tf, &n_contrib[pix], &n_eval[pix],
-                                              &amb[pix], NULL);
+                                              &amb[pix], NULL, NULL);
                 for (int ch = 0; ch < 3; ++ch) image[(int64_t)ch * W * H + pix] = C[ch] + Tf * sc->bg[ch];
                 final_T[pix] = Tf;
             }
@@ -429,19 +432,25 @@ int or_render_fwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
  * Accumulation order is fixed: tiles ascending, pixels row-major within the
  * tile, list order -- independent of the thread count. */
 int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets, const int32_t *list,
-                  const uint8_t *tile_mask, const double *dL_dimg, double *g2d, double *g2d_abs) {
+                  const uint8_t *tile_mask, const double *dL_dimg, double *g2d, double *g2d_mag) {
     const int W = sc->width, H = sc->height;
     const int64_t P = s->P;
     const int64_t T = (int64_t)sc->tiles_x * sc->tiles_y;
     const int64_t total = offsets[T];
     double *acc = (double *)calloc((size_t)(total > 0 ? total : 1) * 10, sizeof(double));
     if (!acc) return -1;
-    /* R19: the same sums with every operand replaced by its magnitude and every
-     * difference by a sum (sum over terms of |term|), for the condition number
-     * sum|terms| / |sum| of each gradient entry. */
+    /* R19 (g2d_mag, [20][P], may be NULL):
+     *   planes 0-9:  the same sums with every operand replaced by its magnitude
+     *                and every difference by a sum -- sum over terms of |term|,
+     *                the scale of fp32 rounding in the sums;
+     *   planes 10-19: sum over terms of |term| x (its first-order relative
+     *                sensitivity to the fp32 error of the alphas it depends on:
+     *                eps_alpha of the pair and the accumulated eps_T of T_k, the
+     *                error model of R18) -- how far any fp32 evaluation of the
+     *                forward quantities moves the sum. */
     double *aab = NULL;
-    if (g2d_abs) {
-        aab = (double *)calloc((size_t)(total > 0 ? total : 1) * 10, sizeof(double));
+    if (g2d_mag) {
+        aab = (double *)calloc((size_t)(total > 0 ? total : 1) * 20, sizeof(double));
         if (!aab) { free(acc); return -1; }
     }
 #pragma omp parallel
@@ -461,14 +470,14 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
                     const int px = tx * 16 + xx, py = ty * 16 + yy;
                     if (px >= W || py >= H) continue;
                     const int64_t pix = (int64_t)py * W + px;
-                    double C[3], Tf;
+                    double C[3], Tf, eTf;
                     int32_t nc, ne;
                     uint8_t am;
-                    const int nr = composite_pixel(s, lst, n, px + 0.5, py + 0.5, C, &Tf, &nc, &ne, &am, rec);
+                    const int nr = composite_pixel(s, lst, n, px + 0.5, py + 0.5, C, &Tf, &nc, &ne, &am, rec, &eTf);
                     const double g[3] = {dL_dimg[pix], dL_dimg[(int64_t)W * H + pix], dL_dimg[2 * (int64_t)W * H + pix]};
                     const double gbg = g[0] * sc->bg[0] + g[1] * sc->bg[1] + g[2] * sc->bg[2];
                     const double gbg_abs = fabs(g[0] * sc->bg[0]) + fabs(g[1] * sc->bg[1]) + fabs(g[2] * sc->bg[2]);
-                    double suffix = 0.0, suffix_abs = 0.0;
+                    double suffix = 0.0, suffix_abs = 0.0, suffix_sens = 0.0;
                     for (int r = nr - 1; r >= 0; --r) {
                         const OrComp *c = &rec[r];
                         const int32_t i = c->idx;
@@ -477,21 +486,34 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
                         suffix += cg * c->alpha * c->T;
                         double *o = a9 + (int64_t)c->k * 10;
                         for (int ch = 0; ch < 3; ++ch) o[6 + ch] += c->alpha * c->T * g[ch];
-                        /* R19 magnitudes: the same expressions over |operands| */
-                        double *ob = aab ? aab + (offsets[t] + c->k) * 10 : NULL;
-                        double dalpha_abs = 0.0;
+                        /* R19 magnitudes: the same expressions over |operands| (ob[0..9]) and
+                         * their fp32 sensitivities (ob[10..19]) */
+                        double *ob = aab ? aab + (offsets[t] + c->k) * 20 : NULL;
+                        double dalpha_abs = 0.0, dalpha_sens = 0.0;
                         if (ob) {
                             const double cg_abs = fabs(s->rgb[i] * g[0]) + fabs(s->rgb[P + i] * g[1]) +
                                                   fabs(s->rgb[2 * P + i] * g[2]);
-                            dalpha_abs = c->T * cg_abs + (suffix_abs + Tf * gbg_abs) / (1.0 - c->alpha);
+                            const double amp = c->ea * c->alpha / (1.0 - c->alpha); /* rel. error of 1 - alpha */
+                            const double tail = (suffix_abs + Tf * gbg_abs) / (1.0 - c->alpha);
+                            dalpha_abs = c->T * cg_abs + tail;
+                            dalpha_sens = c->T * cg_abs * c->eT + (suffix_sens + Tf * gbg_abs * eTf) / (1.0 - c->alpha) +
+                                          tail * amp;
                             suffix_abs += cg_abs * c->alpha * c->T;
-                            for (int ch = 0; ch < 3; ++ch) ob[6 + ch] += fabs(c->alpha * c->T * g[ch]);
+                            suffix_sens += cg_abs * c->alpha * c->T * (c->ea + c->eT);
+                            for (int ch = 0; ch < 3; ++ch) {
+                                ob[6 + ch] += fabs(c->alpha * c->T * g[ch]);
+                                ob[16 + ch] += fabs(c->alpha * c->T * g[ch]) * (c->ea + c->eT);
+                            }
                         }
                         if (c->clamped) continue;
                         o[5] += c->G * dalpha;
                         double dpow = c->pos_power ? 0.0 : c->araw * dalpha;
                         double dpow_abs = c->pos_power ? 0.0 : c->araw * dalpha_abs;
-                        if (ob) ob[5] += c->G * dalpha_abs;
+                        double dpow_sens = c->pos_power ? 0.0 : c->araw * (dalpha_sens + dalpha_abs * c->ea);
+                        if (ob) {
+                            ob[5] += c->G * dalpha_abs;
+                            ob[15] += c->G * (dalpha_sens + dalpha_abs * c->ea);
+                        }
                         if (s->hbeta) {
                             const double hb = s->hbeta[i];
                             const double d_all = c->araw * dalpha;  /* dL/dpower of the GEF power */
@@ -499,8 +521,13 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
                             dpow = c->Q > 0.0 ? d_all * hb * pow(c->Q, hb - 1.0) : 0.0;
                             if (ob) {
                                 const double d_all_abs = c->araw * dalpha_abs;
-                                ob[9] += c->Q > 0.0 ? d_all_abs * fabs(0.25 * c->Qb * log(c->Q)) : 0.0;
-                                dpow_abs = c->Q > 0.0 ? d_all_abs * hb * pow(c->Q, hb - 1.0) : 0.0;
+                                const double d_all_sens = c->araw * (dalpha_sens + dalpha_abs * c->ea);
+                                const double f9 = c->Q > 0.0 ? fabs(0.25 * c->Qb * log(c->Q)) : 0.0;
+                                const double fp = c->Q > 0.0 ? hb * pow(c->Q, hb - 1.0) : 0.0;
+                                ob[9] += d_all_abs * f9;
+                                ob[19] += (d_all_sens + d_all_abs * c->ea) * f9;
+                                dpow_abs = d_all_abs * fp;
+                                dpow_sens = (d_all_sens + d_all_abs * c->ea) * fp;
                             }
                         }
                         const double ca = s->conic[i], cb = s->conic[P + i], cc = s->conic[2 * P + i];
@@ -511,11 +538,9 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
                         o[3] += dpow * (-dx * dy);
                         o[4] += dpow * (-0.5 * dy * dy);
                         if (ob) {
-                            ob[0] += dpow_abs * (fabs(ca * dx) + fabs(cb * dy));
-                            ob[1] += dpow_abs * (fabs(cb * dx) + fabs(cc * dy));
-                            ob[2] += dpow_abs * (0.5 * dx * dx);
-                            ob[3] += dpow_abs * fabs(dx * dy);
-                            ob[4] += dpow_abs * (0.5 * dy * dy);
+                            const double geo[5] = {fabs(ca * dx) + fabs(cb * dy), fabs(cb * dx) + fabs(cc * dy),
+                                                   0.5 * dx * dx, fabs(dx * dy), 0.5 * dy * dy};
+                            for (int q = 0; q < 5; ++q) { ob[q] += dpow_abs * geo[q]; ob[10 + q] += dpow_sens * geo[q]; }
                         }
                     }
                 }
@@ -530,13 +555,13 @@ int or_render_bwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets
             for (int c = 0; c < 10; ++c) g2d[c * P + i] += acc[k * 10 + c];
         }
     }
-    if (g2d_abs) {
-        memset(g2d_abs, 0, sizeof(double) * 10 * (size_t)P);
+    if (g2d_mag) {
+        memset(g2d_mag, 0, sizeof(double) * 20 * (size_t)P);
         for (int64_t t = 0; t < T; ++t) {
             if (tile_mask && !tile_mask[t]) continue;
             for (int64_t k = offsets[t]; k < offsets[t + 1]; ++k) {
                 const int32_t i = list[k];
-                for (int c = 0; c < 10; ++c) g2d_abs[c * P + i] += aab[k * 10 + c];
+                for (int c = 0; c < 20; ++c) g2d_mag[c * P + i] += aab[k * 20 + c];
             }
         }
         free(aab);

@@ -351,12 +351,13 @@ def render_fwd(pre, cam, st: Settings, offsets, lst, tile_mask=None) -> dict:
 def render_bwd(pre, cam, st: Settings, offsets, lst, dL_dimg, tile_mask=None, with_abs: bool = False):
     """S5a: per-particle 2D gradients g2d [10][P] = (du, dv, da, db, dc, dkappa, dr, dg, db, dbeta);
     dbeta (the exact GEF kernel's direct shape term) is 0 for the phi-bar Gaussian kernel.
-    with_abs: also return g2d_abs [10][P], the same sums over |terms| (R19), as (g2d, g2d_abs)."""
+    with_abs: also return the R19 magnitudes g2d_mag [20][P] as (g2d, g2d_mag): planes 0-9 the same
+    sums over |terms|, planes 10-19 sum |term| x its fp32 sensitivity (ges_oracle.c or_render_bwd)."""
     keep = _Keep()
     sp = _splat(pre, keep)
     P = pre["status"].size
     g2d = np.zeros((10, P), np.float64)
-    g2d_abs = np.zeros((10, P), np.float64) if with_abs else None
+    g2d_abs = np.zeros((20, P), np.float64) if with_abs else None
     g = keep(np.ascontiguousarray(dL_dimg, dtype=np.float64))
     mp = None
     if tile_mask is not None:
@@ -403,16 +404,17 @@ def grad_magnitude(parts, cam, st: Settings, g2d_abs, status, flags) -> dict:
     return split_planes(out, K)
 
 
-def grad_error_scale(parts, cam, st: Settings, g2d, g2d_abs, status, flags) -> dict:
-    """R19: the first-order magnitude against which an fp32 evaluation of the
-    gradient chain is accurate, per parameter gradient entry:
-        scale = sum_j |L_j| g2d_abs_j  +  S5b_abs(|g2d|)
-    L = the per-particle linear map S5b (g2d -> parameter gradients), g2d_abs
-    the S5a sums of |terms| over pixels.  The first term bounds |L dg2d| for
-    per-term perturbations of the pixel sums (|dg2d_j| <= eps g2d_abs_j), the
-    second |dL g2d| for perturbations of the chain's own products.  An entry
-    whose scale / |g| is large is ill-conditioned: fp32 arithmetic on either
-    side moves it by ~eps * scale, however it is ordered."""
+def grad_error_scale(parts, cam, st: Settings, g2d, g2d_mag, status, flags) -> dict:
+    """R19: first-order error scales of an fp32 evaluation of every parameter
+    gradient entry, {"round": ..., "sens": ...}:
+        round = sum_j |L_j| g2d_mag[j]  +  S5b_abs(|g2d|)
+        sens  = sum_j |L_j| g2d_mag[10 + j]
+    L = the per-particle linear map S5b (g2d -> parameter gradients).  round x eps
+    bounds the rounding of the pixel sums (|dg2d_j| <= eps sum|terms|) and of the
+    chain's own products; sens is how far the fp32 error of the forward alphas
+    (and so of every T_k, R18's model) moves the entry.  An entry whose scales are
+    large against |g| is ill-conditioned: fp32 arithmetic on either side moves it
+    by about eps round + sens, however it is ordered."""
     keep = _Keep()
     ps = _part_struct(parts, np.float64, keep)
     P, K = parts.P, parts.K
@@ -420,20 +422,22 @@ def grad_error_scale(parts, cam, st: Settings, g2d, g2d_abs, status, flags) -> d
     sp = _ptr(keep(np.ascontiguousarray(status, np.int32)), C.c_int32)
     fp = _ptr(keep(np.ascontiguousarray(flags, np.int32)), C.c_int32)
     c, s = _cam(cam), _settings(st)
-    total = np.zeros((n_planes, P), np.float64)
+    rnd = np.zeros((n_planes, P), np.float64)
+    sens = np.zeros((n_planes, P), np.float64)
     out = np.zeros((n_planes, P), np.float64)
     e = np.zeros((10, P), np.float64)
     for j in range(10 if int(st.kernel) == 1 else 9):
-        e[:] = 0.0
-        e[j] = g2d_abs[j]
-        lib().or_backward_particles(C.byref(ps), C.byref(c), C.byref(s), _ptr(e, C.c_double), sp, fp,
-                                    _ptr(out, C.c_double))
-        total += np.abs(out)
+        for dst, src_plane in ((rnd, j), (sens, 10 + j)):
+            e[:] = 0.0
+            e[j] = g2d_mag[src_plane]
+            lib().or_backward_particles(C.byref(ps), C.byref(c), C.byref(s), _ptr(e, C.c_double), sp, fp,
+                                        _ptr(out, C.c_double))
+            dst += np.abs(out)
     e[:] = np.abs(g2d)
     lib().or_backward_particles_abs(C.byref(ps), C.byref(c), C.byref(s), _ptr(e, C.c_double), sp, fp,
                                     _ptr(out, C.c_double))
-    total += out
-    return split_planes(total, K)
+    rnd += out
+    return {"round": split_planes(rnd, K), "sens": split_planes(sens, K)}
 
 
 def split_planes(flat, K):

@@ -592,16 +592,19 @@ def test_r19_magnitudes_bound_the_gradients():
     pre = base["pre"]
     g2d, gabs = O.render_bwd(pre, cam, st, base["offsets"], base["list"], g, with_abs=True)
     assert np.array_equal(g2d, O.render_bwd(pre, cam, st, base["offsets"], base["list"], g))
-    assert np.all(np.abs(g2d) <= gabs * (1 + 1e-12) + 1e-300)
+    assert np.all(np.abs(g2d) <= gabs[:10] * (1 + 1e-12) + 1e-300)
+    assert np.all(gabs[10:] >= 0) and np.all(gabs[10:] <= 1e-3 * gabs[:10] + 1e-300)
     scale = O.grad_error_scale(sc.particles, cam, st, g2d, gabs, pre["status"], pre["flags"])
     grads = O.backward_particles(sc.particles, cam, st, g2d, pre["status"], pre["flags"])
     for n in grads:
-        assert np.all(np.abs(grads[n]) <= scale[n] * (1 + 1e-12) + 1e-300), n
+        assert np.all(np.abs(grads[n]) <= scale["round"][n] * (1 + 1e-12) + 1e-300), n
     g2d2, gabs2 = O.render_bwd(pre, cam, st, base["offsets"], base["list"], 2.0 * g, with_abs=True)
     assert np.allclose(gabs2, 2.0 * gabs, rtol=1e-13, atol=0)
     gp = np.abs(g)
     g2dp, gabsp = O.render_bwd(pre, cam, st, base["offsets"], base["list"], gp, with_abs=True)
     assert np.array_equal(g2dp[6:9], gabsp[6:9])
+    # the colour planes' sensitivity is exact: each term alpha T g moves by (eps_alpha + eps_T)
+    assert np.all(gabsp[16:19] >= 2e-6 * gabsp[6:9])
     # S5b over magnitudes: one plane, one single-term chain (opacity: dk kappa (1 - kappa))
     e = np.zeros_like(g2d)
     e[5] = gabs[5]
@@ -624,3 +627,5 @@ def test_r19_single_isotropic_splat_has_no_cancellation():
     g2d, gabs = O.render_bwd(base["pre"], cam, st, base["offsets"], base["list"], g, with_abs=True)
     assert np.abs(g2d[:9]).min() > 0
     assert np.allclose(np.abs(g2d[:9]), gabs[:9], rtol=1e-14, atol=0)
+    # one splat, T = 1 exactly: the colour terms move only with alpha (eps_alpha = 2e-6 + 6e-7 |q|)
+    assert np.all(gabs[16:19] > 2e-6 * gabs[6:9]) and np.all(gabs[16:19] < 1e-4 * gabs[6:9])
