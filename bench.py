@@ -135,66 +135,109 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# oracle (cpu_baseline / reference arm): bounded sample of the same workload
+# oracle (cpu_baseline / reference arm): the oracle as it stands, on the host cores
 # ---------------------------------------------------------------------------
-def oracle_sample(scene, cam_index: int, n_tiles: int = 24, seed: int = 0) -> dict:
-    """S1 over all particles, S2/S3 membership lists (all pairs counted), S4+S5a
-    on n_tiles sampled tiles, S5b over all particles; per-frame time is
-    extrapolated to every tile."""
+def host_info() -> dict:
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    model = ln.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def oracle_frame(scene, cam_index: int = 0) -> dict:
+    """One full binned frame of the oracle, fwd + bwd, no extrapolation: S1 over all
+    particles, the per-tile membership lists of every tile (S2/S3), S4 on every pixel,
+    S5a on every pixel (it recomposites each pixel in fp64), S5b over all particles."""
     from oracle import oracle as O
     import ges_inputs as gi
     cam = scene.cameras[cam_index]
     st = O.Settings(rho=scene.rho)
-    t0 = time.perf_counter()
-    pre = O.preprocess(scene.particles, cam, st, "f32")
-    t1 = time.perf_counter()
-    T = pre["tiles_x"] * pre["tiles_y"]
-    rng = np.random.default_rng(seed)
-    mask = np.zeros(T, np.uint8)
-    mask[rng.choice(T, min(n_tiles, T), replace=False)] = 1
-    offsets, lst = O.tile_lists(pre, mask)
-    t2 = time.perf_counter()
     dL = gi.upstream_grad(scene.seed, cam_index, cam.width, cam.height)
-    O.render_fwd(pre, cam, st, offsets, lst, mask)
-    g2d = O.render_bwd(pre, cam, st, offsets, lst, dL, mask)
-    t3 = time.perf_counter()
+    t = [time.perf_counter()]
+    pre = O.preprocess(scene.particles, cam, st, "f32")
+    t.append(time.perf_counter())
+    offsets, lst = O.tile_lists(pre)
+    t.append(time.perf_counter())
+    O.render_fwd(pre, cam, st, offsets, lst)
+    t.append(time.perf_counter())
+    g2d = O.render_bwd(pre, cam, st, offsets, lst, dL)
+    t.append(time.perf_counter())
     O.backward_particles(scene.particles, cam, st, g2d, pre["status"], pre["flags"])
-    t4 = time.perf_counter()
-    per_tile = (t3 - t2) / max(1, int(mask.sum()))
-    frame_s = (t1 - t0) + (t2 - t1) + per_tile * T + (t4 - t3)
-    return {"frame_s": frame_s, "threads": O.num_threads(), "tiles": int(mask.sum()), "T": T,
-            "t_pre": t1 - t0, "t_lists": t2 - t1, "t_tiles": t3 - t2, "t_s5b": t4 - t3}
+    t.append(time.perf_counter())
+    names = ("S1", "S2_S3_lists", "S4", "S5a", "S5b")
+    return {"frame_s": t[-1] - t[0], "stages_s": {n: t[i + 1] - t[i] for i, n in enumerate(names)},
+            "threads": O.num_threads()}
+
+
+def oracle_definitional_sample(scene, cam_index: int = 0, n_tiles: int = 16, seed: int = 0) -> dict:
+    """the definitional mode (every particle in every pixel's list,
+    depth-sorted, composited brute force) on n_tiles x 256 sampled pixels, fwd + bwd;
+    the per-frame time is an EXTRAPOLATION (x tiles / n_tiles) and labelled so."""
+    from oracle import oracle as O
+    import ges_inputs as gi
+    cam = scene.cameras[cam_index]
+    st = O.Settings(rho=scene.rho)
+    pre = O.preprocess(scene.particles, cam, st, "f32")
+    T = pre["tiles_x"] * pre["tiles_y"]
+    mask = np.zeros(T, np.uint8)
+    mask[np.random.default_rng(seed).choice(T, n_tiles, replace=False)] = 1
+    dL = gi.upstream_grad(scene.seed, cam_index, cam.width, cam.height)
+    t0 = time.perf_counter()
+    offsets, lst = O.tile_lists(pre, mask, membership="all")
+    O.render_fwd(pre, cam, st, offsets, lst, mask)
+    O.render_bwd(pre, cam, st, offsets, lst, dL, mask)
+    s = time.perf_counter() - t0
+    return {"pixels": 256 * n_tiles, "tiles": n_tiles, "entries_per_pixel": int(lst.size // max(1, n_tiles)),
+            "s": s, "frame_s_extrapolated": s * T / n_tiles,
+            "label": f"EXTRAPOLATION: definitional fwd+bwd of {n_tiles} sampled tiles x {T}/{n_tiles}"}
 
 
 def run_reference(args) -> None:
+    """The reference arm: the oracle (the only other implementation of the method;
+    the paper ships no code) on full frames of the same workload, fwd + bwd, on this
+    host's cores.  One untimed warm-up frame (the oracle keeps no state between
+    calls beyond the loaded library and first-touched pages), then K timed frames."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import ges_inputs as gi
     scene = gi.make_config(WORKLOAD_CFG)
     cam = scene.cameras[0]
-    n_tiles = args.ref_tiles
-    for _ in range(args.warmup if args.warmup < 1 else 1):
-        pass
-    times = []
-    info = None
-    for k in range(args.steps):
-        info = oracle_sample(scene, 0, n_tiles=n_tiles, seed=k)
+    if args.warmup > 0:
+        oracle_frame(scene, 0)
+    times, info = [], None
+    for _ in range(args.steps):
+        info = oracle_frame(scene, 0)
         times.append(info["frame_s"])
-    ms = 1e3 * statistics.mean(times)
+    ms = 1e3 * sum(times) / len(times)
     value = cam.width * cam.height / (ms / 1e3) / 1e6
-    sample = (f"S1+S5b over all {scene.particles.P} particles, S4+S5a on {info['tiles']} of {info['T']} "
-              f"tiles per step, per-frame time extrapolated to all tiles")
+    host = host_info()
+    sample = (f"one full config-3 frame per step (all {scene.particles.P} particles, all "
+              f"{cam.width}x{cam.height} pixels), binned mode, S1-S5 fwd+bwd; no extrapolation")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "Mpixel-frames/s (fwd+bwd)",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (fp32 S1)",
         "data": "synthetic", "config": workload_config(scene, cam, args.gpus),
+        "step_ms_stats": step_stats([1e3 * x for x in times]),
         "cpu_baseline": {"kind": "oracle", "value": value, "unit": "Mpixel-frames/s (fwd+bwd)",
-                         "cores": info["threads"], "sample": sample},
+                         "cores": info["threads"], "nproc": host["nproc"], "cpu_model": host["cpu_model"],
+                         "sample": sample, "stages_s": info["stages_s"]},
         "e2e": {"value": value, "unit": "Mpixel-frames/s (fwd+bwd)", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def step_stats(ms_list) -> dict:
+    a = np.asarray(ms_list, np.float64)
+    return {"n": int(a.size), "median": float(np.median(a)), "p10": float(np.percentile(a, 10)),
+            "p90": float(np.percentile(a, 90)), "mean": float(a.mean())}
 
 
 def workload_config(scene, cam, n):
@@ -220,6 +263,9 @@ def run_ours(args) -> None:
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        # NCCL's INIT log (ranks, channels, NVLS) on stderr so the run shows which algorithm it chose
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
@@ -335,6 +381,7 @@ def run_ours(args) -> None:
     ms_per_step = total_ms / args.steps
     stage_ms /= args.steps
     value = world * W * H / (ms_per_step / 1e3) / 1e6
+    comm = measure_comm(G, graph, step, grads, flush, stream, args.steps, ms_per_step, world, dev) if world > 1 else None
 
     # ---- forward-only throughput and the equivalent-Gaussian comparator (untimed above) ----
     fwd_ms = time_forward(G, params, cam, st, frame, image, flush, stream, args.steps)
@@ -361,7 +408,7 @@ def run_ours(args) -> None:
     small = time_small_configs(G, dev, stream, min(args.steps, 50)) if world == 1 else None
     union = time_union_compaction(G, scene, dev, stream, min(args.steps, 20)) if world == 1 else None
 
-    # ---- algorithmic work for the roofline ----
+    # ---- algorithmic work for the roofline (SURVEY.md §8(d) units) ----
     n_comp = torch.zeros(W * H, dtype=torch.int32, device=dev)
     G.ges_preprocess(params, cam, st, frame, stream)
     G.ges_sort(frame, stream)
@@ -369,38 +416,50 @@ def run_ours(args) -> None:
     torch.cuda.synchronize()
     e_fwd = int(n_eval.to(torch.int64).sum().item())
     e_comp = int(n_comp.to(torch.int64).sum().item())
+    e_bwd = int(frame.view("n_contrib", torch.int32, W * H).to(torch.int64).sum().item())
     peaks, peak_src = measured_peaks()
     clocks = clk.summary()
     sm_mhz = clocks["sm_mhz"] or peaks.get("sm_max_mhz", 1965.0)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     alu_peak = sms * 128 * sm_mhz * 1e6 / 1e12  # T FP32 thread-instr/s
     K = scene.particles.K
+    V = int(cnt.visible)
+    s1_bytes = 48 * P + (12 * K + 56) * V + 4 * (P - V)
     rows = {
-        "render_bwd_tiles": ("alu", e_comp * BWD_OPS / (stage_ms[3] / 1e3) / 1e12, alu_peak, "Tinstr/s"),
-        "render_fwd": ("alu", e_comp * FWD_OPS / (stage_ms[2] / 1e3) / 1e12, alu_peak, "Tinstr/s"),
-        "preprocess": ("hbm", preprocess_bytes(P, int(cnt.visible), scene.particles.sh_degree)
-                       / (stage_ms[0] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"),
-        "sort": ("hbm", sort_algorithmic_bytes(P, int(cnt.visible), int(cnt.pairs), depth_passes(frame))
-                 / (stage_ms[1] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s"),
-        "backward_particles": ("hbm", particle_bwd_bytes(P, int(cnt.visible), K) / (stage_ms[4] / 1e3) / 1e9,
-                               peaks["hbm_gbs"], "GB/s"),
+        "render_bwd_tiles": ("alu", K7_OPS * e_bwd / (stage_ms[3] / 1e3) / 1e12, alu_peak, "Tinstr/s",
+                             f"K7: {K7_OPS} FP32 instr x sum n_contrib ({e_bwd})"),
+        "render_fwd": ("alu", K6_OPS * e_fwd / (stage_ms[2] / 1e3) / 1e12, alu_peak, "Tinstr/s",
+                       f"K6: {K6_OPS} FP32 instr x E_fwd = sum n_eval ({e_fwd})"),
+        "preprocess": ("hbm", s1_bytes / (stage_ms[0] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s",
+                       f"K1: 48 P + (12K + 56) V + 4 (P - V) = {s1_bytes} B"),
+        "sort": ("hbm", sort_algorithmic_bytes(P, V, int(cnt.pairs), depth_passes(frame))
+                 / (stage_ms[1] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s",
+                 "K2-K5, bucket variant counting its own passes (depth radix over V, item scan, one list write)"),
+        "backward_particles": ("hbm", particle_bwd_bytes(P, V, K) / (stage_ms[4] / 1e3) / 1e9,
+                               peaks["hbm_gbs"], "GB/s",
+                               "K8: parameters and 2-D record read for visible particles, every gradient written"),
+        "render_fwd_useful": ("alu", FWD_OPS * e_comp / (stage_ms[2] / 1e3) / 1e12, alu_peak, "Tinstr/s",
+                              f"useful work only: {FWD_OPS} instr x composited (pixel, entry) pairs ({e_comp})"),
+        "render_bwd_useful": ("alu", BWD_OPS * e_comp / (stage_ms[3] / 1e3) / 1e12, alu_peak, "Tinstr/s",
+                              f"useful work only: {BWD_OPS} instr x composited (pixel, entry) pairs ({e_comp})"),
     }
     dom = max(range(5), key=lambda i: stage_ms[i])
     dname = stage_names[dom]
-    bound, achieved, peak, unit = rows[dname]
+    bound, achieved, peak, unit, _ = rows[dname]
     traffic, traffic_src = committed_traffic(dname)
 
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(G, scene, cam, st, frame, dL, dev, stream, args.steps, world)
     if rank == 0:
-        cpu = None if args.no_cpu else cpu_baseline(scene)
+        cpu = None if args.no_cpu else cpu_baseline(scene, args.definitional_tiles)
         line = {
             "metric": METRIC, "value": value, "unit": "Mpixel-frames/s (fwd+bwd)", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded, DESIGN.md recipe)",
             "config": workload_config(scene, cam, world),
             "iters_per_s": 1e3 / ms_per_step,
+            "step_ms_stats": step_stats(step_ms),
             "fwd_only": {"value": W * H / (fwd_ms / 1e3) / 1e6 * world, "unit": "Mpixel-frames/s",
                          "ms": fwd_ms, "fps_per_gpu": 1e3 / fwd_ms},
             "bands_fwd": {"value": cam0.width * cam0.height / (band_ms / 1e3) / 1e6, "unit": "Mpixel-frames/s",
@@ -417,16 +476,18 @@ def run_ours(args) -> None:
             "vs_gaussian_equivalent": {"ges_fwd_ms": fwd_ms, "gaussian_fwd_ms": g_ms, "ratio": g_ms / fwd_ms,
                                        "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
             "launch": graph_note,
+            "comm": comm,
             "stages_ms": {n: float(stage_ms[i]) for i, n in enumerate(stage_names)},
             "stages_note": "per-stage CUDA events around direct launches of the same step (not the graph replay)",
-            "counts": {"visible": int(cnt.visible), "pairs": int(cnt.pairs), "slots": int(cnt.slots), "evals_fwd": e_fwd,
-                       "composited": e_comp},
+            "counts": {"particles": P, "visible": V, "pairs": int(cnt.pairs), "slots": int(cnt.slots),
+                       "tiles": frame.c.tiles_x * frame.c.tiles_y, "evals_fwd": e_fwd, "sum_n_contrib": e_bwd,
+                       "composited": e_comp, "depth_passes": depth_passes(frame)},
             "roofline": {"kernel": dname, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                          "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                          "peak_source": peak_src if bound == "hbm" else
                          f"derived: {sms} SMs x 128 FP32 lanes x {sm_mhz:.0f} MHz (median SM clock under load)",
                          "all": {k: {"bound": v[0], "achieved": v[1], "peak": v[2], "unit": v[3],
-                                     "frac": v[1] / v[2]} for k, v in rows.items()}},
+                                     "frac": v[1] / v[2], "work": v[4]} for k, v in rows.items()}},
             "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": LAUNCHES_PER_STEP * args.steps,
             "clocks": clocks,
@@ -436,13 +497,54 @@ def run_ours(args) -> None:
         dist.destroy_process_group()
 
 
-# algorithmic FP32 thread-instructions per composited (pixel, entry)
+# FP32-pipe instructions per forward evaluation (K6: E_fwd = sum over pixels of the
+# list entries evaluated before the pixel terminates) and per backward entry (K7: sum n_contrib)
+K6_OPS = 15
+K7_OPS = 45
+# useful work only: FP32 instructions the method needs per composited (pixel, entry)
 FWD_OPS = 20
 BWD_OPS = 38
 # preprocess, ranges, 4 depth passes x (hist, scan, scatter), item scan, 2 tile passes x 3, fwd, bwd tiles, particles
 # preprocess, depth sort + item scan (one cooperative kernel), binning (count, column scan,
 # tile scan, scatter), fwd, bwd tiles, particle bwd
 LAUNCHES_PER_STEP = 1 + 1 + 4 + 1 + 1 + 1
+
+
+def measure_comm(G, graph, step, grads, flush, stream, steps, ms_per_step, world, dev):
+    """N > 1: exposed communication = the step with its
+    allreduce minus the same step without it (device time, max over ranks), and the
+    NCCL allreduce of the gradient buffer alone: algorithm and bus bandwidth
+    (busBW = algBW x 2 (N - 1) / N)."""
+    import torch
+    import torch.distributed as dist
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def timed(fn):
+        ms = []
+        for _ in range(steps):
+            flush.fill_(1)
+            dist.barrier()
+            torch.cuda.synchronize()
+            a, b = ev(), ev()
+            a.record(stream)
+            fn()
+            b.record(stream)
+            b.synchronize()
+            ms.append(a.elapsed_time(b))
+        t = torch.tensor([sum(ms) / len(ms)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    no_comm = timed(graph.replay if graph is not None else (lambda: None))
+    ar = timed(lambda: dist.all_reduce(grads.flat))
+    nbytes = grads.flat.numel() * 4
+    alg = nbytes / (ar / 1e3) / 1e9
+    env = {k: os.environ.get(k) for k in ("NCCL_NVLS_ENABLE", "NCCL_ALGO", "NCCL_PROTO") if os.environ.get(k)}
+    return {"ms_step_with_allreduce": ms_per_step, "ms_step_without_collective": no_comm,
+            "exposed_comm_ms": ms_per_step - no_comm, "allreduce_ms": ar, "allreduce_bytes": nbytes,
+            "algbw_GBps": alg, "busbw_GBps": alg * 2 * (world - 1) / world,
+            "nccl_version": ".".join(map(str, torch.cuda.nccl.version())), "nccl_env": env,
+            "note": "NCCL_DEBUG=INFO / SUBSYS=INIT on stderr shows the channels and whether NVLS was chosen"}
 
 
 def preprocess_bytes(P, V, deg):
@@ -1016,14 +1118,22 @@ def run_e2e_train(G, scene, cam, st, frame, dev, stream, steps, world):
                     "S5, ges_adam_step, loss -> host"}
 
 
-def cpu_baseline(scene):
-    info = oracle_sample(scene, 0, n_tiles=24)
+def cpu_baseline(scene, definitional_tiles=16):
+    """The oracle as it stands on this host: one full binned config-3 frame (fwd+bwd,
+    no extrapolation), plus SURVEY.md §8(d)'s definitional-mode sample (labelled as an
+    extrapolation)."""
+    info = oracle_frame(scene, 0)
     cam = scene.cameras[0]
     value = cam.width * cam.height / info["frame_s"] / 1e6
-    return {"value": value, "unit": "Mpixel-frames/s (fwd+bwd)", "cores": info["threads"], "kind": "oracle",
-            "sample": (f"S1+S5b over all {scene.particles.P} particles, S4+S5a on {info['tiles']} of "
-                       f"{info['T']} tiles, per-frame time extrapolated"),
-            "frame_s": info["frame_s"]}
+    host = host_info()
+    out = {"value": value, "unit": "Mpixel-frames/s (fwd+bwd)", "cores": info["threads"], "nproc": host["nproc"],
+           "cpu_model": host["cpu_model"], "kind": "oracle",
+           "sample": (f"one full frame: all {scene.particles.P} particles, all {cam.width}x{cam.height} pixels, "
+                      f"binned mode (R10 rect lists), S1-S5 fwd+bwd; no extrapolation"),
+           "frame_s": info["frame_s"], "stages_s": info["stages_s"]}
+    if definitional_tiles:
+        out["definitional"] = oracle_definitional_sample(scene, 0, definitional_tiles)
+    return out
 
 
 def main():
@@ -1035,7 +1145,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel directly in the timed loop")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--ref-tiles", type=int, default=16)
+    ap.add_argument("--definitional-tiles", type=int, default=16,
+                    help="tiles of the oracle's definitional-mode sample in cpu_baseline (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -287,6 +287,15 @@ def tile_lists(pre, tile_mask: Optional[np.ndarray] = None, membership="rect"):
     P = pre["status"].size
     T = pre["tiles_x"] * pre["tiles_y"]
     order = np.ascontiguousarray(depth_order_key(pre))
+    if membership == "all" and tile_mask is not None:
+        # every geometrically valid particle in every selected tile: each selected tile's
+        # list is the same (depth key, index) order of all of them (the definitional sum)
+        st, _, _ = _membership(pre, membership)
+        ids = np.nonzero(st == VISIBLE)[0]
+        srt = ids[np.lexsort((ids, order[ids]))].astype(np.int32)
+        sel = np.ascontiguousarray(tile_mask, dtype=np.uint8) != 0
+        offsets = np.concatenate([[0], np.cumsum(sel.astype(np.int64) * srt.size)])
+        return offsets, np.tile(srt, int(sel.sum()))
     offsets = np.zeros(T + 1, np.int64)
     mask_p = None
     if tile_mask is not None:

@@ -629,3 +629,20 @@ def test_r19_single_isotropic_splat_has_no_cancellation():
     assert np.allclose(np.abs(g2d[:9]), gabs[:9], rtol=1e-14, atol=0)
     # one splat, T = 1 exactly: the colour terms move only with alpha (eps_alpha = 2e-6 + 6e-7 |q|)
     assert np.all(gabs[16:19] > 2e-6 * gabs[6:9]) and np.all(gabs[16:19] < 1e-4 * gabs[6:9])
+
+
+def test_definitional_lists_on_sampled_tiles_match_the_c_enumeration():
+    """bench.py's definitional sample builds the 'all' membership of a few tiles
+    directly (every particle, (depth, index) order); it equals the C brute force."""
+    sc = gi.make_config(0, P=300)
+    cam = sc.cameras[0]
+    pre = O.preprocess(sc.particles, cam, O.Settings(), "f32")
+    T = pre["tiles_x"] * pre["tiles_y"]
+    mask = np.zeros(T, np.uint8)
+    mask[[3, 50, 200]] = 1
+    off, lst = O.tile_lists(pre, mask, membership="all")
+    full_off, full_lst = O.tile_lists(pre, np.ones(T, np.uint8), membership="all")
+    for t in range(T):
+        got = lst[off[t]:off[t + 1]]
+        want = full_lst[full_off[t]:full_off[t + 1]] if mask[t] else full_lst[:0]
+        assert np.array_equal(got, want), t
