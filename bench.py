@@ -56,9 +56,13 @@ STAGE_KERNEL = {"preprocess": "preprocess_tma_kernel", "render_fwd": "render_fwd
 
 
 def committed_traffic(stage):
-    """DRAM bytes per launch of the stage's kernel from the committed ncu --set full
-    capture (profiles/r1h_traffic.json, written by tools/summarize_ncu.py traffic), or None."""
-    p = os.path.join(ROOT, "profiles", "r1h_traffic.json")
+    """DRAM bytes per launch of the stage's kernel from the newest committed ncu --set full
+    capture (profiles/<round>_traffic.json, written by tools/summarize_ncu.py traffic), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_traffic.json")))
+    if not files:
+        return None, None
+    p = files[-1]
     k = STAGE_KERNEL.get(stage)
     if not k or not os.path.exists(p):
         return None, None
