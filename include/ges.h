@@ -178,8 +178,10 @@ typedef struct {
     uint32_t *vis_val[2];  /* [P] particle index, ping-pong                      */
     uint32_t *sorted_vis;  /* [V] visible particles in (depth, index) order             */
     /* ---- S2 radix scratch (depth passes) ---- */
-    uint32_t *radix_hist;  /* [256][G] per-CTA digit counts -> offsets (digit-major), G <= 1024 */
-    uint32_t *radix_total; /* [256] digit totals of the current pass, then [G] u64 area sums    */
+    uint32_t *radix_hist;  /* [4][1024][512] u32 per-CTA digit counts of each pass, published
+                              with a flag bit; then [1024][512] u64 last-pass area sums       */
+    uint32_t *radix_total; /* [4][512] u32 digit totals of each pass, then [512] u64 last-pass
+                              digit area totals (in the zero-per-frame region)               */
     /* ---- S2 pairs and S3 ranges: direct tile binning ---- */
     uint32_t *item_offset; /* [P] first pair slot E of each depth-sorted visible particle  */
     uint32_t *item_rec;    /* [P][4] packed (row classes, particle, x0|y0<<16, x1|y1<<16);

@@ -54,6 +54,9 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     // --- zero-per-frame region (one memset in ges_preprocess) ---
     g.counters = (uint64_t*)take(sizeof(uint64_t) * GES_CTR_N);
     g.lookback = (uint32_t*)take(sizeof(uint32_t) * 64);
+    // depth-sort digit totals: [kDsMaxPasses][512] u32 counts, then [512] u64 last-pass areas
+    g.radix_total = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * kDsMaxPasses +
+                                    sizeof(uint64_t) * kRadixDigits);
     g.zero_bytes = off;  // bytes of the zero region from the workspace base
     // --- per particle ---
     g.depth = (float*)take(sizeof(float) * P);
@@ -71,8 +74,11 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
         g.vis_val[k] = (uint32_t*)take(sizeof(uint32_t) * P);
     }
     g.sorted_vis = (uint32_t*)take(sizeof(uint32_t) * P);
-    g.radix_hist = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * (size_t)kDsMaxGrid);
-    g.radix_total = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits + sizeof(uint64_t) * kDsMaxGrid);
+    // depth-sort published words: [kDsMaxPasses][kDsMaxGrid][512] u32, then [kDsMaxGrid][512] u64
+    g.radix_hist = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * (size_t)kDsMaxGrid * kDsMaxPasses +
+                                   sizeof(uint64_t) * kRadixDigits * (size_t)kDsMaxGrid +
+                                   sizeof(uint32_t) * kRadixDigits * (size_t)kDsMaxGroups * kDsMaxPasses +
+                                   sizeof(uint64_t) * kRadixDigits * (size_t)kDsMaxGroups);
     g.item_offset = (uint32_t*)take(sizeof(uint32_t) * P);
     g.item_rec = (uint32_t*)take(16 * (size_t)P);
     // binning chunks: S >= 16384 slots, and the [T][chunks] table bounded by 2^24 entries
@@ -198,8 +204,12 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     ds.keys[0] = frame->vis_key[1]; ds.keys[1] = frame->vis_key[0];
     ds.vals[0] = frame->vis_val[1]; ds.vals[1] = frame->vis_val[0];
     ds.sorted_vis = frame->sorted_vis;
-    ds.hist = frame->radix_hist; ds.tot = frame->radix_total;
-    ds.part = (unsigned long long*)(frame->radix_total + kRadixDigits);
+    ds.st_cnt = frame->radix_hist;
+    ds.st_area = (unsigned long long*)(frame->radix_hist + (size_t)kRadixDigits * kDsMaxGrid * kDsMaxPasses);
+    ds.gt_cnt = (uint32_t*)(ds.st_area + (size_t)kRadixDigits * kDsMaxGrid);
+    ds.gt_area = (unsigned long long*)(ds.gt_cnt + (size_t)kRadixDigits * kDsMaxGroups * kDsMaxPasses);
+    ds.tot = frame->radix_total;
+    ds.atot = (unsigned long long*)(frame->radix_total + kRadixDigits * kDsMaxPasses);
     ds.P = frame->P; ds.G = 0; ds.key_base = frame->depth_key_base;
     ds.rect = (const ushort4*)frame->rect;
     ds.E = frame->item_offset; ds.items = (uint4*)frame->item_rec;

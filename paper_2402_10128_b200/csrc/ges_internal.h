@@ -38,15 +38,20 @@ int num_sms();
 constexpr int kRadixDigits = 512;  // max digits of a depth-sort pass (9 bits)
 
 constexpr int kDsMaxGrid = 1024;      // max CTAs of the cooperative depth sort
+constexpr int kDsMaxPasses = 4;       // 9-bit digits of a 32-bit key
+constexpr int kDsMaxGroups = kDsMaxGrid / 16;  // CTA groups of the two-level pass prefix (sort.cu)
 
 struct DepthSortArgs {
     const uint32_t* key0;             // [P] preprocess keys: depth bits, 0xffffffff = not visible
     uint32_t* keys[2];                // [P] ping-pong (keys[0] may not alias key0; keys[1] may)
     uint32_t* vals[2];                // [P] ping-pong
     uint32_t* sorted_vis;             // [V] out: visible particles in (depth bits, index) order
-    uint32_t* hist;                   // [256][G] per-CTA digit counts -> offsets
-    uint32_t* tot;                    // [256] digit totals
-    unsigned long long* part;         // [G] per-CTA rect-area sums (item scan)
+    uint32_t* st_cnt;                 // [kDsMaxPasses][kDsMaxGrid][512] published per-CTA digit counts
+    unsigned long long* st_area;      // [kDsMaxGrid][512] published per-CTA digit area sums (last pass)
+    uint32_t* gt_cnt;                 // [kDsMaxPasses][kDsMaxGroups][512] published group totals
+    unsigned long long* gt_area;      // [kDsMaxGroups][512] published group area totals (last pass)
+    uint32_t* tot;                    // [kDsMaxPasses][512] digit totals (zeroed per frame)
+    unsigned long long* atot;         // [512] last-pass digit area totals (zeroed per frame)
     int64_t P;
     int G;                            // grid (set by the launcher)
     uint32_t key_base;                // fp32 bits of near_z: every visible key is larger

@@ -256,7 +256,7 @@ template <int K>
 __global__ void __launch_bounds__(kPreThreads, GES_PRE_MINB) preprocess_kernel(PreprocessArgs a) {
     const int tid = threadIdx.x, lane = tid & 31;
     const CamDerived cd = derive_camera(a.cam);
-    uint32_t nvis = 0;
+    uint32_t nvis = 0, kmax = 0;  // visible count, largest visible depth key (depth sort pass plan)
     for (int base = blockIdx.x * kPreThreads; base < a.P; base += gridDim.x * kPreThreads) {
         const int i = base + tid;
         bool vis = false;
@@ -266,8 +266,11 @@ __global__ void __launch_bounds__(kPreThreads, GES_PRE_MINB) preprocess_kernel(P
             vis = store_out(a, i, o);
         }
         nvis += __popc(__ballot_sync(0xffffffffu, vis));
+        if (vis) kmax = max(kmax, a.vis_key[i]);
     }
     if (lane == 0 && nvis) atomicAdd(&a.counters[GES_CTR_VISIBLE], (unsigned long long)nvis);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if (lane == 0 && kmax) atomicMax(&a.counters[GES_CTR_KEYMAX], (unsigned long long)kmax);
 }
 
 // --- TMA-staged variant -------------------------------------------------------
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(kPreTmaThreads) preprocess_tma_kernel(Preproce
     constexpr int NPL = 12 + 3 * K;
     extern __shared__ __align__(128) float s_st[];  // [kPreStages][NPL][kPreTile]
     __shared__ __align__(8) uint64_t s_full[kPreStages], s_empty[kPreStages];
-    __shared__ uint32_t s_nvis;
+    __shared__ uint32_t s_nvis, s_kmax;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ntiles = a.P / kPreTile;
     if (tid == 0) {
@@ -337,6 +340,7 @@ __global__ void __launch_bounds__(kPreTmaThreads) preprocess_tma_kernel(Preproce
             mbar_init(&s_empty[st], kPreTile / 32);
         }
         s_nvis = 0;
+        s_kmax = 0;
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(kPreTmaThreads) preprocess_tma_kernel(Preproce
         return;
     }
     const CamDerived cd = derive_camera(a.cam);
-    uint32_t nvis = 0;
+    uint32_t nvis = 0, kmax = 0;  // visible count, largest visible depth key (depth sort pass plan)
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int st = it % kPreStages;
@@ -373,6 +377,7 @@ __global__ void __launch_bounds__(kPreTmaThreads) preprocess_tma_kernel(Preproce
         if (lane == 0) mbar_arrive(&s_empty[st]);  // the warp is done reading the stage
         const bool vis = store_out(a, i, o);
         nvis += __popc(__ballot_sync(0xffffffffu, vis));
+        if (vis) kmax = max(kmax, __float_as_uint(o.depth));
     }
     // the partial last tile, from global memory
     if (blockIdx.x == 0) {
@@ -382,12 +387,16 @@ __global__ void __launch_bounds__(kPreTmaThreads) preprocess_tma_kernel(Preproce
             const ParamIn in = load_params(a, i);
             const PreOut o = preprocess_one<K>(a, cd, i, in, a.sh + i, a.P);
             vis = store_out(a, i, o);
+            if (vis) kmax = max(kmax, __float_as_uint(o.depth));
         }
         nvis += __popc(__ballot_sync(0xffffffffu, vis));
     }
     if (lane == 0 && nvis) atomicAdd(&s_nvis, nvis);
+    kmax = __reduce_max_sync(0xffffffffu, kmax);
+    if (lane == 0 && kmax) atomicMax(&s_kmax, kmax);
     asm volatile("bar.sync 1, %0;" ::"r"(kPreTile) : "memory");  // consumer warps only
     if (tid == 0 && s_nvis) atomicAdd(&a.counters[GES_CTR_VISIBLE], (unsigned long long)s_nvis);
+    if (tid == 0 && s_kmax) atomicMax(&a.counters[GES_CTR_KEYMAX], (unsigned long long)s_kmax);
 }
 
 template <int K>

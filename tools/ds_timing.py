@@ -22,8 +22,10 @@ for _ in range(5):
 torch.cuda.synchronize()
 ctr = r.frame.view("counters", torch.int64, 16).cpu().tolist()
 t = ctr[8:16]
-names = ["key range", "pass 0", "pass 1", "pass 2", "pass 3/none", "items sum", "items scan"]
-for i, n in enumerate(names):
-    if t[i + 1] >= t[i] > 0:
-        print(f"{n:12s} {(t[i + 1] - t[i]) / 1e3:8.2f} us")
-print(f"total        {(t[7] - t[0]) / 1e3:8.2f} us")
+# slots: 0 start, 1 after phase H, 2 / 3 after passes 0 / 1 (non-last), 4 last pass hist done,
+# 5 last pass prefix done, 6 end
+names = [("phase H", 0, 1), ("pass 0", 1, 2), ("pass 1", 2, 3), ("last hist", 3, 4), ("last prefix", 4, 5),
+         ("last scatter", 5, 6), ("total", 0, 6)]
+for n, i, j in names:
+    if t[j] >= t[i] > 0:
+        print(f"{n:12s} {(t[j] - t[i]) / 1e3:8.2f} us")
