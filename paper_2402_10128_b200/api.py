@@ -381,8 +381,19 @@ class DensityControl:
                                            C.c_void_p(self.count.data_ptr()), C.c_void_p(_stream(stream))),
                 "ges_densify_stats")
 
-    def densify_prune(self, params: PlanarParams, opt: Adam, settings: DensitySettings, stream=None):
-        """Returns the new PlanarParams; opt's moments are replaced; the statistics reset (one sync)."""
+    def densify_prune(self, params: PlanarParams, opt: Adam, settings: DensitySettings, stream=None,
+                      group=None):
+        """Returns the new PlanarParams; opt's moments are replaced; the statistics reset (one sync).
+        Under torch.distributed (world > 1) the statistics are first summed over `group`
+        (dist.allreduce_density_stats), so every data-parallel rank densifies identically."""
+        from .dist import allreduce_density_stats
+        if stream is not None:  # the collective runs on torch's current stream: order it after `stream`
+            cur = torch.cuda.current_stream()
+            cur.wait_stream(stream)
+            allreduce_density_stats(self.accum, self.count, group)
+            stream.wait_stream(cur)
+        else:
+            allreduce_density_stats(self.accum, self.count, group)
         P, deg, dev = params.P, params.sh_degree, params.flat.device
         cap = 2 * P
         outs = [torch.empty((n_planes(deg), cap), dtype=torch.float32, device=dev) for _ in range(3)]

@@ -29,6 +29,14 @@ from .api import Frame, PlanarParams, Renderer, Settings, _stream
 TILE = 16
 
 
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        return False
+
+
 def views_for_rank(n_views: int, rank: int, world: int) -> List[int]:
     """Round-robin view assignment: rank r gets views r, r + world, ..."""
     if world < 1 or not (0 <= rank < world):
@@ -41,6 +49,22 @@ def allreduce_grads(flat: torch.Tensor, group=None) -> torch.Tensor:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
     return flat
+
+
+def allreduce_density_stats(accum: torch.Tensor, count: torch.Tensor, group=None) -> None:
+    """Sum the densification statistics (DensityControl.accum / .count: the per-particle
+    view-space gradient norms and the number of views that saw each particle) over the
+    group in place, so that every data-parallel rank takes the same clone / split /
+    prune decisions.  The mean over the
+    views a particle was visible in, accum / count, is then the global one: with the
+    parameters and Adam moments already identical on every rank (the gradients are
+    allreduced) and the split draws counter-based (seeded, R32), the
+    densified sets are bit-identical."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        both = torch.stack([accum, count])
+        dist.all_reduce(both, op=dist.ReduceOp.SUM, group=group)
+        accum.copy_(both[0])
+        count.copy_(both[1])
 
 
 def allreduce_visible_union(flat: torch.Tensor, mask: torch.Tensor, pack, unpack, group=None) -> torch.Tensor:
@@ -130,10 +154,16 @@ class ViewDataParallel:
         self.images = {}
 
     def step(self, dL_dimages: dict, stream=None) -> PlanarParams:
-        """dL_dimages: view -> [3][H][W] device tensor, for this rank's views."""
+        """dL_dimages: view -> [3][H][W] device tensor, for this rank's views.  Everything
+        runs on `stream` (default: torch's current stream); the collectives are issued on
+        torch's current stream after it waits for `stream`, and `stream` waits for them."""
+        cur = torch.cuda.current_stream() if torch.cuda.is_available() else None
+        if stream is not None and cur is not None:
+            stream.wait_stream(cur)  # inputs produced on the current stream
         first = True
         if self.reducer is not None:
-            self.reducer.reset()
+            with torch.cuda.stream(stream) if stream is not None else _nullctx():
+                self.reducer.reset()
         for v in self.views:
             cam = self.cameras[v]
             r = self.renderers[(cam.width, cam.height)]
@@ -144,11 +174,16 @@ class ViewDataParallel:
                        accumulate=not first, stream=stream)
             first = False
         if first:  # no views on this rank: contribute zeros
-            self.grads.flat.zero_()
+            with torch.cuda.stream(stream) if stream is not None else _nullctx():
+                self.grads.flat.zero_()
+        if stream is not None and cur is not None:
+            cur.wait_stream(stream)  # the masks and gradients are complete before any collective
         if self.reducer is not None:
             self.reducer.allreduce(self.grads.flat, self.group)
         else:
             allreduce_grads(self.grads.flat, self.group)
+        if stream is not None and cur is not None:
+            stream.wait_stream(cur)
         return self.grads
 
 

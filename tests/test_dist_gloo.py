@@ -213,3 +213,82 @@ def test_visible_union_allreduce_world2():
         assert np.allclose(flat, ref, rtol=1e-5, atol=1e-6)
     assert np.array_equal(out[0][0], out[1][0])
     assert not np.array_equal(out[0][2], out[1][2])   # the ranks saw different particles
+
+
+# --------------------------------------------------------------------------
+# DP-consistent density control
+# --------------------------------------------------------------------------
+from oracle import train as TR  # noqa: E402
+
+DENS_VIEWS = 4
+
+
+def _density_scene():
+    sc = gi.make_config(2, P=600, n_views=DENS_VIEWS)
+    K = sc.particles.K
+    params = np.concatenate([sc.particles.mean, sc.particles.log_scale, sc.particles.quat,
+                             sc.particles.opacity_logit[None], sc.particles.sh, sc.particles.beta[None]],
+                            axis=0).astype(np.float64)
+    # a few particles large and dense enough to split, a few faint enough to prune
+    params[3:6, :40] += 3.0
+    params[10, 40:60] = -8.0
+    return sc, params, K
+
+
+def _view_stats(sc, v):
+    """One view's contribution to the densification statistic (R32): the view-space
+    gradient norm |(du W/2, dv H/2)| of every particle the view saw, and a count of 1."""
+    cam = sc.cameras[v]
+    cam = gi.Camera(96, 96, 2 * cam.fx * 96 / 800, 2 * cam.fy * 96 / 800, 48.0, 48.0, cam.near, cam.R, cam.t)
+    g = gi.upstream_grad(sc.seed, v, 96, 96)
+    r = O.render_and_grad(sc.particles, cam, O.Settings(), g)
+    vis = r["pre"]["status"] == O.VISIBLE
+    norm = TR.viewspace_grad_norm(r["g2d"][0], r["g2d"][1], 96, 96)
+    return np.where(vis, norm, 0.0).astype(np.float32), vis.astype(np.float32)
+
+
+def _density_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sc, params, K = _density_scene()
+        accum = torch.zeros(sc.particles.P, dtype=torch.float32)
+        count = torch.zeros(sc.particles.P, dtype=torch.float32)
+        for v in gdist.views_for_rank(DENS_VIEWS, rank, world):
+            a, c = _view_stats(sc, v)
+            accum += torch.from_numpy(a)
+            count += torch.from_numpy(c)
+        local = TR.densify_prune(params, np.zeros_like(params), np.zeros_like(params), accum.numpy().astype(np.float64),
+                                 count.numpy().astype(np.float64), K, 1.0, 0.1, 7)[0]
+        gdist.allreduce_density_stats(accum, count)
+        new = TR.densify_prune(params, np.zeros_like(params), np.zeros_like(params), accum.numpy().astype(np.float64),
+                               count.numpy().astype(np.float64), K, 1.0, 0.1, 7)
+        out[rank] = (new[0], new[3], local, accum.numpy().copy(), count.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_density_control_is_identical_on_every_rank_world2():
+    """Clone / split / prune decisions come from the view-space gradient statistics
+    summed over ALL ranks' views (dist.allreduce_density_stats): both ranks produce
+    bit-identical densified sets, equal to a single process that saw every view --
+    while densifying on the local statistics alone would make the ranks diverge."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_density_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    sc, params, K = _density_scene()
+    stats = [_view_stats(sc, v) for v in range(DENS_VIEWS)]
+    accum = sum(a.astype(np.float64) for a, _ in stats)
+    count = sum(c.astype(np.float64) for _, c in stats)
+    ref = TR.densify_prune(params, np.zeros_like(params), np.zeros_like(params), accum, count, K, 1.0, 0.1, 7)
+    acts = ref[3]
+    assert (acts == 0).any() and (acts == 3).any() and (acts == 1).any()   # prune, split, keep all occur
+    for r in range(world):
+        new, act, _, a, c = out[r]
+        assert np.allclose(a, accum, rtol=1e-6, atol=1e-9) and np.array_equal(c, count)
+        assert np.array_equal(act, acts)
+        assert np.array_equal(new, ref[0])
+    assert np.array_equal(out[0][0], out[1][0])
+    assert out[0][2].shape != out[1][2].shape or not np.array_equal(out[0][2], out[1][2])  # local stats diverge
