@@ -223,6 +223,19 @@ size_t ges_workspace_bytes(int64_t P, int32_t width, int32_t height, int64_t pai
 ges_status ges_frame_init(void *workspace, size_t bytes, int64_t P, int32_t width, int32_t height,
                           int64_t pair_capacity, ges_frame *frame);
 
+/* The frame's sub-arrays as (byte offset from the workspace base, bytes) pairs,
+ * extents[2 i], extents[2 i + 1], in carving order: counters, lookback,
+ * radix_total, depth, pay0, pay1, pay2, pay3, radius, rect, status, flags,
+ * drgb_ddir, vis_key[0], vis_val[0], vis_key[1], vis_val[1], sorted_vis,
+ * radix_hist, item_offset, item_rec, chunk_first, bin_table, list, ranges,
+ * final_T, n_contrib, grad2d.  Each array starts 256-byte aligned; the bytes
+ * between one array's end and the next one's start are padding that no
+ * kernel touches (tests poison them to detect out-of-bounds writes).  Host-only.
+ * *count = the number of arrays; GES_ERR_CAPACITY if it exceeds `capacity`
+ * (extents then holds the first `capacity`).  extents may be NULL when
+ * capacity is 0 (query the count). */
+ges_status ges_frame_layout(const ges_frame *frame, int64_t *extents, int32_t capacity, int32_t *count);
+
 /* S1.  Writes the per-particle state, the visible list and the tile
  * histogram of `frame`.  particles/camera/settings are host structs whose
  * array pointers are device pointers; camera must match the frame size. */

@@ -105,7 +105,7 @@ class ges_density_settings(C.Structure):
                                          "shape_prune", "rho")] + [("seed", C.c_uint64)]
 
 
-EXPORTS = ["ges_workspace_bytes", "ges_frame_init", "ges_preprocess", "ges_sort", "ges_render_fwd",
+EXPORTS = ["ges_workspace_bytes", "ges_frame_init", "ges_frame_layout", "ges_preprocess", "ges_sort", "ges_render_fwd",
            "ges_render_bwd", "ges_render_bwd_tiles", "ges_backward_particles", "ges_counts_get",
            "ges_status_string", "ges_version", "ges_loss_mask_dims", "ges_loss_workspace_bytes", "ges_loss_mask",
            "ges_loss", "ges_lr_position", "ges_adam_step", "ges_reset", "ges_densify_stats",
@@ -134,6 +134,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         L.ges_frame_init.restype = C.c_int
         L.ges_frame_init.argtypes = [C.c_void_p, C.c_size_t, C.c_int64, C.c_int32, C.c_int32, C.c_int64,
                                      C.POINTER(ges_frame)]
+        L.ges_frame_layout.restype = C.c_int
+        L.ges_frame_layout.argtypes = [C.POINTER(ges_frame), C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]
         L.ges_preprocess.restype = C.c_int
         L.ges_preprocess.argtypes = [C.POINTER(ges_particles), C.POINTER(ges_camera), C.POINTER(ges_settings),
                                      C.POINTER(ges_frame), C.c_void_p]

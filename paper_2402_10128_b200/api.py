@@ -116,18 +116,45 @@ def _stream(stream) -> int:
 class Frame:
     """One frame workspace (a single torch uint8 allocation) and its C struct."""
 
-    def __init__(self, P: int, width: int, height: int, pair_capacity: int, device="cuda"):
+    # the frame's sub-arrays in carving order (ges.h ges_frame_layout)
+    LAYOUT = ("counters", "lookback", "radix_total", "depth", "pay0", "pay1", "pay2", "pay3", "radius", "rect",
+              "status", "flags", "drgb_ddir", "vis_key0", "vis_val0", "vis_key1", "vis_val1", "sorted_vis",
+              "radix_hist", "item_offset", "item_rec", "chunk_first", "bin_table", "list", "ranges", "final_T",
+              "n_contrib", "grad2d")
+
+    def __init__(self, P: int, width: int, height: int, pair_capacity: int, device="cuda",
+                 poison: Optional[int] = None, guard: int = 0):
+        """poison (tests): fill the workspace with this byte instead of zeros (grad2d,
+        which ges.h requires zeroed, is still zeroed); guard: extra bytes after the
+        workspace, filled with the poison byte."""
         lib = L.load()
         nbytes = lib.ges_workspace_bytes(P, width, height, pair_capacity)
         if nbytes == 0:
             raise L.GESError("invalid frame size")
-        self.ws = torch.zeros(nbytes + 256, dtype=torch.uint8, device=device)  # zero once (ges.h)
+        if poison is None:
+            self.ws = torch.zeros(nbytes + 256 + guard, dtype=torch.uint8, device=device)  # zero once (ges.h)
+        else:
+            self.ws = torch.full((nbytes + 256 + guard,), int(poison), dtype=torch.uint8, device=device)
         base = self.ws.data_ptr()
         self.offset = (-base) % 256
+        self.nbytes = nbytes
         self.c = L.ges_frame()
         L.check(lib.ges_frame_init(C.c_void_p(base + self.offset), nbytes, P, width, height, pair_capacity,
                                    C.byref(self.c)), "ges_frame_init")
         self.P, self.width, self.height, self.pair_capacity = P, width, height, pair_capacity
+        if poison is not None:
+            off, size = self.layout()["grad2d"]
+            self.ws[self.offset + off:self.offset + off + size].zero_()
+
+    def layout(self) -> dict:
+        """name -> (byte offset from the aligned workspace base, bytes) of every sub-array."""
+        n = C.c_int32(0)
+        L.load().ges_frame_layout(C.byref(self.c), None, 0, C.byref(n))
+        ext = (C.c_int64 * (2 * n.value))()
+        L.check(L.load().ges_frame_layout(C.byref(self.c), C.cast(ext, C.c_void_p), n.value, C.byref(n)),
+                "ges_frame_layout")
+        assert n.value == len(self.LAYOUT), (n.value, len(self.LAYOUT))
+        return {k: (ext[2 * i], ext[2 * i + 1]) for i, k in enumerate(self.LAYOUT)}
 
     # --- typed views into the workspace (tests / diagnostics) ---
     def view(self, field: str, dtype: torch.dtype, count: int, index: Optional[int] = None) -> torch.Tensor:

@@ -36,13 +36,17 @@ int bits_for(int64_t n) {
 }
 
 // Carves the frame; returns the total size.  base == nullptr => size only.
-size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_frame* f) {
+size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_frame* f, int64_t* extents = nullptr,
+              int32_t max_extents = 0, int32_t* n_extents = nullptr) {
     const int tx = tiles_of(W), ty = tiles_of(H);
     const int64_t T = (int64_t)tx * ty;
     const int64_t HW = (int64_t)W * H;
     size_t off = 0;
+    int32_t ne = 0;
     auto take = [&](size_t bytes) -> char* {
         char* p = base ? base + off : nullptr;
+        if (extents && ne < max_extents) { extents[2 * ne] = (int64_t)off; extents[2 * ne + 1] = (int64_t)bytes; }
+        ++ne;
         off = align_up(off + bytes);
         return p;
     };
@@ -97,6 +101,7 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     g.n_contrib = (uint32_t*)take(sizeof(uint32_t) * HW);
     g.grad2d = (float*)take(sizeof(float) * kGrad2dStride * (size_t)P);
     g.workspace_bytes = off;
+    if (n_extents) *n_extents = ne;
     if (f) *f = g;
     return off;
 }
@@ -146,6 +151,12 @@ extern "C" {
 size_t ges_workspace_bytes(int64_t P, int32_t width, int32_t height, int64_t pair_capacity) {
     if (P < 1 || width < 1 || height < 1 || pair_capacity < 1) return 0;
     return layout(nullptr, P, width, height, pair_capacity, nullptr);
+}
+
+ges_status ges_frame_layout(const ges_frame* frame, int64_t* extents, int32_t capacity, int32_t* count) {
+    if (!frame || !count || (capacity > 0 && !extents) || capacity < 0) return GES_ERR_INVALID_ARG;
+    layout(nullptr, frame->P, frame->width, frame->height, frame->pair_capacity, nullptr, extents, capacity, count);
+    return *count > capacity ? GES_ERR_CAPACITY : GES_OK;
 }
 
 ges_status ges_frame_init(void* workspace, size_t bytes, int64_t P, int32_t width, int32_t height,

@@ -82,6 +82,28 @@ def test_workspace_and_frame_carving_host_only():
         assert lib.ges_frame_init(C.c_void_p(base), big, P, w2, h2, cap, C.byref(f)) == L.GES_ERR_INVALID_ARG
     assert lib.ges_frame_init(C.c_void_p(base), lib.ges_workspace_bytes(P, 4096, 4096, cap), P, 4096, 4096, cap,
                               C.byref(f)) == L.GES_OK
+    # ges_frame_layout: every array's (offset, bytes), in carving order, 256-B aligned, disjoint,
+    # inside the workspace, matching the struct's pointers
+    f2 = L.ges_frame()
+    assert lib.ges_frame_init(C.c_void_p(base), nbytes, P, W, H, cap, C.byref(f2)) == L.GES_OK
+    n = C.c_int32(0)
+    assert lib.ges_frame_layout(C.byref(f2), None, 0, C.byref(n)) == L.GES_ERR_CAPACITY
+    ext = (C.c_int64 * (2 * n.value))()
+    assert lib.ges_frame_layout(C.byref(f2), C.cast(ext, C.c_void_p), n.value, C.byref(n)) == L.GES_OK
+    pairs = [(ext[2 * i], ext[2 * i + 1]) for i in range(n.value)]
+    assert all(o % 256 == 0 for o, _ in pairs)
+    assert all(o1 + s1 <= o2 for (o1, s1), (o2, _) in zip(pairs, pairs[1:]))
+    assert pairs[-1][0] + pairs[-1][1] <= f2.workspace_bytes == nbytes
+    names = ("counters", "lookback", "radix_total", "depth", "pay0", "pay1", "pay2", "pay3", "radius", "rect",
+             "status", "flags", "drgb_ddir", None, None, None, None, "sorted_vis", "radix_hist", "item_offset",
+             "item_rec", "chunk_first", "bin_table", "list", "ranges", "final_T", "n_contrib", "grad2d")
+    assert len(names) == n.value
+    for (o, s), nm in zip(pairs, names):
+        if nm:
+            assert getattr(f2, nm) == base + o, nm
+    assert (f2.vis_key[0], f2.vis_val[0], f2.vis_key[1], f2.vis_val[1]) == tuple(base + pairs[k][0] for k in range(13, 17))
+    assert pairs[names.index("depth")][1] == 4 * P and pairs[names.index("grad2d")][1] == 48 * P
+    assert lib.ges_frame_layout(None, None, 0, C.byref(n)) == L.GES_ERR_INVALID_ARG
     assert lib.ges_sort(None, None) == L.GES_ERR_INVALID_ARG
     assert lib.ges_status_string(L.GES_ERR_CAPACITY).decode().startswith("workspace")
     assert b"sm_100a" in lib.ges_version()
