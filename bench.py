@@ -862,16 +862,20 @@ def time_union_compaction(G, scene, dev, stream, steps):
     union = int(red.mask.sum().item())
     flat = torch.randn((C, P), dtype=torch.float32, device=dev)
     packed, u = red.pack(flat, red.mask, force=True)
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    a, b, c = ev(), ev(), ev()
     a.record(stream)
-    for _ in range(steps):
-        red.pack(flat, red.mask, stream, force=True)
-        red.unpack(packed, None, flat, stream)
+    for _ in range(steps):                      # device time only: no host read of U inside
+        red.index(red.mask, stream)
     b.record(stream)
-    b.synchronize()
+    for _ in range(steps):
+        red.pack_indexed(flat, stream)
+        red.unpack(packed, None, flat, stream)
+    c.record(stream)
+    c.synchronize()
     return {"views": len(cams), "union_particles": union, "union_frac": union / P,
             "allreduce_bytes_dense": 4 * C * P, "allreduce_bytes_compact": 4 * C * union,
-            "index_pack_unpack_ms": a.elapsed_time(b) / steps,
+            "index_ms": a.elapsed_time(b) / steps, "pack_unpack_ms": b.elapsed_time(c) / steps,
             "used_when": "union <= 0.5 P (VisibleUnionReducer.max_union); above it the dense allreduce runs",
             "note": "view-DP allreduce of only the union of the ranks' visible particles (one host read of U)"}
 

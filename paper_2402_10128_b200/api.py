@@ -243,17 +243,17 @@ class Renderer:
                 n_eval=None, stream=None, check_overflow: bool = True, n_comp=None) -> torch.Tensor:
         if image is None:
             image = torch.empty((3, self.height, self.width), dtype=torch.float32, device=self.device)
-        for _ in range(3):
+        for attempt in range(3):
             ges_preprocess(particles, camera, settings, self.frame, stream)
             ges_sort(self.frame, stream)
             ges_render_fwd(self.frame, settings, image, n_eval, stream, n_comp)
             if not check_overflow:
-                break
+                return image
             cnt = self.frame.counts(stream)
             if not cnt.overflow:
-                break
-            self.grow(cnt.slots)
-        return image
+                return image
+            self.grow(cnt.slots)   # the exact slot count: the next attempt fits unless the scene changed
+        raise L.GESError("pair capacity still exceeded after regrowing the frame twice")
 
     def backward(self, particles: PlanarParams, camera, settings: Settings, dL_dimage: torch.Tensor,
                  grads: Optional[PlanarParams] = None, accumulate: bool = False, stream=None) -> PlanarParams:

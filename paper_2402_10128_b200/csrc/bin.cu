@@ -416,7 +416,8 @@ cudaError_t launch_bin(const BinArgs& a, cudaStream_t stream) {
     bin_tilescan_kernel<<<1, kTileScanThreads, 0, stream>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const int smem = kStages * kStageRec * 16;  // the record ring
-    static int configured = 0;
+    static int configured_dev[kMaxDevices] = {0};
+    int& configured = configured_dev[current_device()];
     if (smem > configured) {
         if ((e = cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
             cudaSuccess)

@@ -11,14 +11,15 @@
 namespace ges {
 
 int num_sms() {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
+    static int sms[kMaxDevices] = {0};
+    const int d = current_device();
+    if (sms[d] == 0) {
+        int dev = 0, n = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        sms[d] = n > 0 ? n : 148;
     }
-    return sms;
+    return sms[d];
 }
 
 namespace {

@@ -33,6 +33,15 @@ struct PreprocessArgs {
 
 cudaError_t launch_preprocess(const PreprocessArgs& a, cudaStream_t stream);
 
+// Launch setup (function attributes, occupancy-derived grids) is per device: the
+// memos below are indexed by the current device.
+constexpr int kMaxDevices = 64;
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & (kMaxDevices - 1);
+}
+
 // --- sort / ranges ---------------------------------------------------------
 int num_sms();
 constexpr int kRadixDigits = 512;  // max digits of a depth-sort pass (9 bits)

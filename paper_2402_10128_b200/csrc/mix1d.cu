@@ -335,7 +335,8 @@ cudaError_t launch_mix_signal(int kind, float width, float x_lo, float h, int n,
 
 cudaError_t launch_mix(const MixArgs& a, bool fit, cudaStream_t stream) {
     const size_t smem = sizeof(float) * (size_t)a.n;
-    static size_t configured = 0;
+    static size_t configured_dev[kMaxDevices] = {0};
+    size_t& configured = configured_dev[current_device()];
     if (smem > 48 * 1024 && smem > configured) {
         cudaError_t e = cudaFuncSetAttribute(mix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;

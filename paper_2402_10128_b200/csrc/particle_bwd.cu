@@ -388,7 +388,8 @@ __global__ void __launch_bounds__(kPbThreads) particle_bwd_tma_kernel(ParticleBw
 template <int K>
 static cudaError_t launch_particle_bwd_tma(const ParticleBwdArgs& a, cudaStream_t stream) {
     const int smem = kPbStages * (int)sizeof(PbStage);
-    static int grid = 0;
+    static int grids[kMaxDevices] = {0};
+    int& grid = grids[current_device()];
     if (grid == 0) {
         cudaFuncSetAttribute(particle_bwd_tma_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0;

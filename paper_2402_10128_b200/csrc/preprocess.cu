@@ -403,7 +403,8 @@ template <int K>
 static cudaError_t launch_preprocess_tma(const PreprocessArgs& a, cudaStream_t stream) {
     constexpr int NPL = 12 + 3 * K;
     const int smem = kPreStages * NPL * kPreTile * 4;
-    static int grid = 0;
+    static int grids[kMaxDevices] = {0};
+    int& grid = grids[current_device()];
     if (grid == 0) {
         cudaFuncSetAttribute(preprocess_tma_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         int per_sm = 0;

@@ -529,10 +529,8 @@ __global__ void __launch_bounds__(kDsThreads, 1) depth_sort_kernel(DepthSortArgs
 }
 
 int depth_sort_grid() {
-    static int grid[64] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    dev &= 63;
+    static int grid[kMaxDevices] = {0};
+    const int dev = current_device();
     if (grid[dev] == 0) {
         int per_sm = 0;
         cudaFuncSetAttribute(depth_sort_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(DsSmem));

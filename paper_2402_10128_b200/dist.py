@@ -109,17 +109,30 @@ class VisibleUnionReducer:
         L.check(L.load().ges_mask_visible(C.byref(frame.c), C.c_void_p(self.mask.data_ptr()),
                                           C.c_void_p(_stream(stream))), "ges_mask_visible")
 
+    def index(self, mask: torch.Tensor, stream=None) -> None:
+        """Device-only: idx = the union's particles in order, U = their count (no host read)."""
+        L.check(L.load().ges_grad_index(self.P, C.c_void_p(mask.data_ptr()), C.c_void_p(self.ws.data_ptr()),
+                                        self.ws.numel(), C.c_void_p(self.idx.data_ptr()),
+                                        C.c_void_p(self.U.data_ptr()), C.c_void_p(_stream(stream))),
+                "ges_grad_index")
+
+    def pack_indexed(self, flat: torch.Tensor, stream=None) -> torch.Tensor:
+        """Device-only: the C U gradient floats of the indexed union into self.packed."""
+        L.check(L.load().ges_grad_pack(C.c_void_p(flat.data_ptr()), self.P, self.C, C.c_void_p(self.idx.data_ptr()),
+                                       C.c_void_p(self.U.data_ptr()), C.c_void_p(self.packed.data_ptr()),
+                                       C.c_void_p(_stream(stream))), "ges_grad_pack")
+        return self.packed
+
     def pack(self, flat: torch.Tensor, mask: torch.Tensor, stream=None, force: bool = False):
-        lib = L.load()
-        L.check(lib.ges_grad_index(self.P, C.c_void_p(mask.data_ptr()), C.c_void_p(self.ws.data_ptr()),
-                                   self.ws.numel(), C.c_void_p(self.idx.data_ptr()), C.c_void_p(self.U.data_ptr()),
-                                   C.c_void_p(_stream(stream))), "ges_grad_index")
-        u = int(self.U.item())  # the one host read: the decision and the allreduce's size
+        """Index, then ONE host read of U (it decides dense vs compact and sizes the
+        collective -- so a compact step is not graph-capturable, and on view sets that
+        cover most particles, e.g. the 8 config-3 bench views at 79 %, the dense
+        allreduce is cheaper: compact=True pays off for sparse-coverage view sets)."""
+        self.index(mask, stream)
+        u = int(self.U.item())
         if not force and u > self.max_union * self.P:
             return None, u
-        L.check(lib.ges_grad_pack(C.c_void_p(flat.data_ptr()), self.P, self.C, C.c_void_p(self.idx.data_ptr()),
-                                  C.c_void_p(self.U.data_ptr()), C.c_void_p(self.packed.data_ptr()),
-                                  C.c_void_p(_stream(stream))), "ges_grad_pack")
+        self.pack_indexed(flat, stream)
         return self.packed[: self.C * u], u
 
     def unpack(self, packed: torch.Tensor, state, flat: torch.Tensor, stream=None) -> None:
