@@ -339,6 +339,16 @@ double ges_lr_position(int64_t step, double init, double final_, double delay_mu
 ges_status ges_adam_step(float *params, const float *grads, float *m, float *v, int64_t P, int32_t sh_degree,
                          const ges_adam_settings *settings, void *stream);
 
+/* The same step on the contiguous range [begin, begin + count) of the flattened
+ * [C][P] buffers only (a ZeRO-1 optimizer shard of data-parallel training, each
+ * rank updating 1/N of the parameters after a reduce-scatter of the gradients):
+ * params, m, v are the FULL buffers, grads_range holds the range's count gradient
+ * values (element i <-> flat index begin + i).  Elementwise identical to
+ * ges_adam_step on those entries.  begin + count must not exceed C P. */
+ges_status ges_adam_step_range(float *params, const float *grads_range, float *m, float *v, int64_t P,
+                               int32_t sh_degree, const ges_adam_settings *settings, int64_t begin, int64_t count,
+                               void *stream);
+
 /* Opacity reset (what = 0): logit <- min(logit, logit(0.01)); shape reset (what = 1):
  * beta <- 2 (PAPER.md:1253 intervals; targets R30). */
 ges_status ges_reset(float *params, int64_t P, int32_t sh_degree, int32_t what, void *stream);

@@ -108,7 +108,7 @@ class ges_density_settings(C.Structure):
 EXPORTS = ["ges_workspace_bytes", "ges_frame_init", "ges_frame_layout", "ges_preprocess", "ges_sort", "ges_render_fwd",
            "ges_render_bwd", "ges_render_bwd_tiles", "ges_backward_particles", "ges_counts_get",
            "ges_status_string", "ges_version", "ges_loss_mask_dims", "ges_loss_workspace_bytes", "ges_loss_mask",
-           "ges_loss", "ges_lr_position", "ges_adam_step", "ges_reset", "ges_densify_stats",
+           "ges_loss", "ges_lr_position", "ges_adam_step", "ges_adam_step_range", "ges_reset", "ges_densify_stats",
            "ges_densify_workspace_bytes", "ges_densify_prune", "ges_mix_signal", "ges_mix_eval", "ges_mix_fit",
            "ges_theorem1_errors", "ges_probe_mufu", "ges_mask_visible", "ges_grad_pack_workspace_bytes",
            "ges_grad_index", "ges_grad_pack", "ges_grad_unpack"]
@@ -162,6 +162,9 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         L.ges_adam_step.restype = C.c_int
         L.ges_adam_step.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                     C.POINTER(ges_adam_settings), C.c_void_p]
+        L.ges_adam_step_range.restype = C.c_int
+        L.ges_adam_step_range.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                                          C.POINTER(ges_adam_settings), C.c_int64, C.c_int64, C.c_void_p]
         L.ges_reset.restype = C.c_int
         L.ges_reset.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_void_p]
         L.ges_densify_stats.restype = C.c_int

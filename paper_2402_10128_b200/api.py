@@ -363,6 +363,18 @@ class Adam:
         self.v = PlanarParams.zeros(params.P, params.sh_degree, params.flat.device)
         self.t = 0
 
+    def step_range(self, params: PlanarParams, grads_range: torch.Tensor, begin: int, count: int,
+                   stream=None) -> None:
+        """One step of the flat entries [begin, begin + count) only (ges_adam_step_range: a
+        ZeRO-1 shard); grads_range holds their gradients.  Advances the step count."""
+        self.t += 1
+        s = self.settings.c(self.t)
+        assert grads_range.dtype == torch.float32 and grads_range.is_contiguous() and grads_range.numel() >= count
+        L.check(L.load().ges_adam_step_range(C.c_void_p(params.flat.data_ptr()), C.c_void_p(grads_range.data_ptr()),
+                                             C.c_void_p(self.m.flat.data_ptr()), C.c_void_p(self.v.flat.data_ptr()),
+                                             params.P, params.sh_degree, C.byref(s), int(begin), int(count),
+                                             C.c_void_p(_stream(stream))), "ges_adam_step_range")
+
     def step(self, params: PlanarParams, grads: PlanarParams, stream=None) -> None:
         self.t += 1
         s = self.settings.c(self.t)

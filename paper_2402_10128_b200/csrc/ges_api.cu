@@ -449,6 +449,23 @@ ges_status ges_adam_step(float* params, const float* grads, float* m, float* v, 
     return cuda_status(launch_adam(a, (cudaStream_t)stream));
 }
 
+ges_status ges_adam_step_range(float* params, const float* grads_range, float* m, float* v, int64_t P,
+                               int32_t sh_degree, const ges_adam_settings* s, int64_t begin, int64_t count,
+                               void* stream) {
+    const int K = (sh_degree + 1) * (sh_degree + 1);
+    if (!params || !grads_range || !m || !v || !s || P < 1 || sh_degree < 0 || sh_degree > 3 || s->step < 1 ||
+        begin < 0 || count < 0 || begin + count > (int64_t)(12 + 3 * K) * P)
+        return GES_ERR_INVALID_ARG;
+    AdamArgs a;
+    a.params = params; a.grads = grads_range; a.m = m; a.v = v; a.P = P; a.n_planes = 12 + 3 * K;
+    a.lr_position = s->lr_position; a.lr_scaling = s->lr_scaling; a.lr_rotation = s->lr_rotation;
+    a.lr_opacity = s->lr_opacity; a.lr_feature_dc = s->lr_feature_dc; a.lr_feature_rest = s->lr_feature_rest;
+    a.lr_shape = s->lr_shape; a.beta1 = s->beta1; a.beta2 = s->beta2; a.eps = s->eps;
+    a.inv_bc1 = (float)(1.0 / (1.0 - std::pow((double)s->beta1, (double)s->step)));
+    a.inv_bc2 = (float)(1.0 / (1.0 - std::pow((double)s->beta2, (double)s->step)));
+    return cuda_status(launch_adam_range(a, begin, count, (cudaStream_t)stream));
+}
+
 ges_status ges_reset(float* params, int64_t P, int32_t sh_degree, int32_t what, void* stream) {
     if (!params || P < 1 || sh_degree < 0 || sh_degree > 3 || (what != 0 && what != 1)) return GES_ERR_INVALID_ARG;
     const int K = (sh_degree + 1) * (sh_degree + 1);

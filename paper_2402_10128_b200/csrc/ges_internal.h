@@ -203,6 +203,7 @@ struct AdamArgs {
     float beta1, beta2, eps, inv_bc1, inv_bc2;
 };
 cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream);
+cudaError_t launch_adam_range(const AdamArgs& a, int64_t begin, int64_t count, cudaStream_t stream);
 cudaError_t launch_reset(float* params, int64_t P, int plane, float cap, int mode, cudaStream_t stream);
 
 struct DensifyStatsArgs {

@@ -66,6 +66,52 @@ __global__ void adam4_kernel(AdamArgs a) {
     reinterpret_cast<float4*>(a.v)[q] = v;
 }
 
+// A contiguous range [begin, begin + count) of the flattened [C][P] buffer (a
+// ZeRO-1 shard: dist.ShardedAdam); the gradient holds the range only.  Four
+// elements per thread when begin, P are multiples of 4 (a float4 never straddles
+// a plane), else one.
+template <bool VEC>
+__global__ void adam_range_kernel(AdamArgs a, int64_t begin, int64_t count) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    if (VEC) {
+        for (int64_t i4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; 4 * i4 < count; i4 += stride) {
+            const int64_t q = begin + 4 * i4;
+            const float lr = plane_lr(a, (int)(q / a.P));
+            float4 p = *reinterpret_cast<float4*>(a.params + q);
+            float4 m = *reinterpret_cast<float4*>(a.m + q);
+            float4 v = *reinterpret_cast<float4*>(a.v + q);
+            const float4 g = *reinterpret_cast<const float4*>(a.grads + 4 * i4);
+            adam1(a, lr, g.x, p.x, m.x, v.x);
+            adam1(a, lr, g.y, p.y, m.y, v.y);
+            adam1(a, lr, g.z, p.z, m.z, v.z);
+            adam1(a, lr, g.w, p.w, m.w, v.w);
+            *reinterpret_cast<float4*>(a.params + q) = p;
+            *reinterpret_cast<float4*>(a.m + q) = m;
+            *reinterpret_cast<float4*>(a.v + q) = v;
+        }
+    } else {
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) {
+            const int64_t q = begin + i;
+            const float lr = plane_lr(a, (int)(q / a.P));
+            float p = a.params[q], m = a.m[q], v = a.v[q];
+            adam1(a, lr, a.grads[i], p, m, v);
+            a.params[q] = p; a.m[q] = m; a.v[q] = v;
+        }
+    }
+}
+
+cudaError_t launch_adam_range(const AdamArgs& a, int64_t begin, int64_t count, cudaStream_t stream) {
+    if (count <= 0) return cudaSuccess;
+    auto al = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
+    const bool vec = begin % 4 == 0 && count % 4 == 0 && a.P % 4 == 0 && al(a.params) && al(a.grads) && al(a.m) &&
+                     al(a.v);
+    const int64_t work = vec ? count / 4 : count;
+    const int grid = (int)std::min<int64_t>((work + 255) / 256, (int64_t)num_sms() * 16);
+    if (vec) adam_range_kernel<true><<<grid, 256, 0, stream>>>(a, begin, count);
+    else adam_range_kernel<false><<<grid, 256, 0, stream>>>(a, begin, count);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_adam(const AdamArgs& a, cudaStream_t stream) {
     auto al = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
     if (a.P % 4 == 0 && al(a.params) && al(a.grads) && al(a.m) && al(a.v)) {

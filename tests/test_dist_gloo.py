@@ -292,3 +292,66 @@ def test_density_control_is_identical_on_every_rank_world2():
         assert np.array_equal(new, ref[0])
     assert np.array_equal(out[0][0], out[1][0])
     assert out[0][2].shape != out[1][2].shape or not np.array_equal(out[0][2], out[1][2])  # local stats diverge
+
+
+# --------------------------------------------------------------------------
+# ZeRO-1 sharded optimizer step of the view-DP training step (dist.sharded_update)
+# --------------------------------------------------------------------------
+def _zero1_problem(sh_degree, P):
+    K = (sh_degree + 1) ** 2
+    C = 12 + 3 * K
+    rng = np.random.default_rng(11)
+    params = rng.normal(0, 1, (C, P))
+    local = [rng.normal(0, 1, (C, P)) for _ in range(2)]   # each rank's accumulated view gradients
+    return K, C, params, local
+
+
+def _zero1_worker(rank, world, port, sh_degree, P, steps, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        K, C, params0, local = _zero1_problem(sh_degree, P)
+        params = torch.from_numpy(params0.copy())
+        state = {"m": np.zeros((C, P)), "v": np.zeros((C, P)), "t": 0}
+
+        def update(gshard, begin, count):
+            # the oracle Adam (elementwise) on the flat range only
+            state["t"] += 1
+            g = np.zeros(C * P)
+            g[begin:begin + count] = gshard.numpy()[:count]
+            p2, m2, v2 = TR.adam_step(params.numpy().reshape(C, P), g.reshape(C, P), state["m"], state["v"],
+                                      state["t"], K)
+            sl = slice(begin, begin + count)
+            params.view(-1)[sl] = torch.from_numpy(p2.reshape(-1)[sl])
+            state["m"].reshape(-1)[sl] = m2.reshape(-1)[sl]
+            state["v"].reshape(-1)[sl] = v2.reshape(-1)[sl]
+
+        scratch = {}
+        for s in range(steps):
+            grads = torch.from_numpy(local[rank] * (1.0 + 0.1 * s))
+            gdist.sharded_update(grads.reshape(-1), params.view(-1), update, rank, world, scratch=scratch)
+        out[rank] = params.numpy().copy()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("sh_degree,P", [(3, 40), (0, 37)])   # C P even / odd (padded collectives)
+def test_zero1_sharded_update_world2(sh_degree, P):
+    """Reduce-scatter + per-shard Adam + all-gather (ZeRO-1) gives every rank the
+    parameters of a single process running Adam on the summed gradients."""
+    world, steps = 2, 3
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_zero1_worker, args=(world, _free_port(), sh_degree, P, steps, out), nprocs=world, join=True)
+    K, C, params, local = _zero1_problem(sh_degree, P)
+    m, v = np.zeros((C, P)), np.zeros((C, P))
+    for s in range(steps):
+        g = (local[0] + local[1]) * (1.0 + 0.1 * s)
+        params, m, v = TR.adam_step(params, g, m, v, s + 1, K)
+    for r in range(world):
+        assert np.allclose(out[r], params, rtol=1e-12, atol=1e-12)
+    assert np.array_equal(out[0], out[1])
+    begin0, c0, shard = gdist.shard_range(C * P, 0, world)
+    begin1, c1, _ = gdist.shard_range(C * P, 1, world)
+    assert begin0 == 0 and begin1 == shard and c0 + c1 == C * P

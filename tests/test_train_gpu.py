@@ -136,3 +136,27 @@ def test_densify_prune_parity():
     assert np.array_equal(got[6:, cols], q[6:, cols].astype(np.float32))
     assert not gm[:, cols].any() and not gv[:, cols].any()
     assert nk + int((act == 2).sum()) + int((act == 3).sum()) == q.shape[1]
+
+
+@pytest.mark.parametrize("deg,P,world", [(3, 10000, 8), (3, 9999, 3), (1, 4097, 2)])
+def test_adam_step_range_equals_full_step(deg, P, world):
+    """ges_adam_step_range (the ZeRO-1 shard update of dist.ShardedAdam) on every rank's
+    range of the flat buffer reproduces ges_adam_step bit for bit, ranges straddling
+    plane boundaries included (float4 and scalar kernels)."""
+    from paper_2402_10128_b200 import dist as gdist
+    p = planar(P, deg, 3)
+    g = planar(P, deg, 4)
+    full, parts = to_params(p, deg), to_params(p, deg)
+    grads = to_params(g, deg)
+    opt_full, opt_parts = G.Adam(full), G.Adam(parts)
+    for step in range(3):
+        opt_full.step(full, grads)
+        n = parts.flat.numel()
+        for r in range(world):
+            b, c, _ = gdist.shard_range(n, r, world)
+            opt_parts.step_range(parts, grads.flat.view(-1)[b:b + c].contiguous(), b, c)
+            opt_parts.t -= 1
+        opt_parts.t += 1
+    torch.cuda.synchronize()
+    assert torch.equal(full.flat, parts.flat)
+    assert torch.equal(opt_full.m.flat, opt_parts.m.flat) and torch.equal(opt_full.v.flat, opt_parts.v.flat)
