@@ -194,7 +194,8 @@ typedef struct {
     int64_t bin_chunk_slots, bin_chunks; /* S, and the chunk capacity ceil((capacity + 4 P) / S) */
     uint32_t *list;        /* [cap] per-tile lists: tile t = list[ranges[t] .. ranges[t+1]) */
     uint32_t *ranges;      /* [T+1]                                               */
-    uint32_t *lookback;    /* scratch (64 words, zeroed per frame)                 */
+    uint32_t *lookback;    /* [T/32 + 1] u64 published block sums of the range scan
+                              (decoupled look-back; zeroed per frame)              */
     uint64_t *counters;    /* [GES_CTR_N]                                         */
     size_t zero_bytes;     /* bytes from `counters` zeroed at the start of a frame */
     /* ---- S4 / S5 ---- */

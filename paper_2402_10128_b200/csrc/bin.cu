@@ -114,15 +114,31 @@ __global__ void __launch_bounds__(kBinThreads) bin_count_kernel(BinArgs a) {
 
 // Per block of 32 tiles (lane = tile): 32 warps split the chunks into
 // contiguous ranges; pass 1 sums each range, the ranges are scanned in shared
-// memory, pass 2 rewrites each count as its exclusive prefix; the tile total
-// goes to ranges[t].
+// memory, pass 2 rewrites each count as its exclusive prefix.  The tile totals
+// become the ranges (S3) in the same kernel: warp 0 scans its block's 32 totals
+// and finds the pairs of all earlier blocks by a decoupled look-back over their
+// published (flagged) sums -- no separate scan launch over the tiles.
 constexpr int kColThreads = 1024;
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = (1ull << 62) - 1;
+__device__ __forceinline__ unsigned long long lb_load(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void lb_store(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __global__ void __launch_bounds__(kColThreads) bin_colscan_kernel(BinArgs a) {
     __shared__ uint32_t s_sum[32][33];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t t = (int64_t)blockIdx.x * 32 + lane;
+    const int blk = blockIdx.x, nblk = gridDim.x;
+    const int64_t t = (int64_t)blk * 32 + lane;
     const bool ok = t < a.T;
-    if (a.counters[GES_CTR_OVERFLOW]) return;
+    if (a.counters[GES_CTR_OVERFLOW]) {  // nothing was binned: empty ranges
+        if (warp == 0 && ok) a.ranges[t] = 0;
+        if (warp == 0 && blk == nblk - 1 && lane == 0) { a.ranges[a.T] = 0; a.counters_w[GES_CTR_PAIRS] = 0; }
+        return;
+    }
     const int C = (int)bin_chunks(a);
     const int per = (C + 31) / 32;
     const int c0 = min(C, warp * per), c1 = min(C, c0 + per);
@@ -138,13 +154,44 @@ __global__ void __launch_bounds__(kColThreads) bin_colscan_kernel(BinArgs a) {
     s_sum[warp][lane] = sum;
     __syncthreads();
     if (warp == 0) {
-        uint32_t run = 0;
+        uint32_t run = 0;  // this tile's total
         for (int w = 0; w < 32; ++w) {
             const uint32_t x = s_sum[w][lane];
             s_sum[w][lane] = run;
             run += x;
         }
-        if (ok) a.ranges[t] = run;
+        // the block's exclusive prefix over its 32 tiles, its aggregate
+        uint32_t incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += nn;
+        }
+        const unsigned long long agg = __shfl_sync(0xffffffffu, incl, 31);
+        unsigned long long* st = a.lookback;
+        if (lane == 0) lb_store(st + blk, (blk == 0 ? kLbInc : kLbAgg) | agg);
+        // decoupled look-back over the earlier blocks, 32 at a time
+        unsigned long long excl = 0;
+        for (int j = blk - 1; j >= 0; j -= 32) {
+            const int idx = j - lane;
+            unsigned long long s = idx >= 0 ? lb_load(st + idx) : kLbInc;
+            while (__any_sync(0xffffffffu, (s & ~kLbVal) == 0ull)) {
+                if ((s & ~kLbVal) == 0ull) s = lb_load(st + idx);
+            }
+            const uint32_t inc = __ballot_sync(0xffffffffu, (s & kLbInc) != 0ull);
+            const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive predecessor (or this window)
+            unsigned long long v = lane <= stop ? (s & kLbVal) : 0ull;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            excl += v;
+            if (inc) break;
+        }
+        if (lane == 0 && blk > 0) lb_store(st + blk, kLbInc | (excl + agg));
+        if (ok) a.ranges[t] = (uint32_t)(excl + incl - run);
+        if (blk == nblk - 1 && lane == 31) {
+            a.ranges[a.T] = (uint32_t)(excl + incl);
+            a.counters_w[GES_CTR_PAIRS] = excl + incl;
+        }
     }
     __syncthreads();
     uint32_t run = s_sum[warp][lane];
@@ -157,53 +204,6 @@ __global__ void __launch_bounds__(kColThreads) bin_colscan_kernel(BinArgs a) {
             if (ok && c + u < c1) a.table[(int64_t)(c + u) * a.T + t] = run;
             run += v[u];
         }
-    }
-}
-
-// One CTA: exclusive prefix of the tile totals -> ranges[0..T], M.
-constexpr int kTileScanThreads = 1024;
-__global__ void __launch_bounds__(kTileScanThreads) bin_tilescan_kernel(BinArgs a) {
-    __shared__ uint32_t s_warp[kTileScanThreads / 32 + 1];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int T = a.tiles_x * a.rows;
-    if (a.counters[GES_CTR_OVERFLOW]) {
-        for (int t = tid; t <= T; t += kTileScanThreads) a.ranges[t] = 0;
-        if (tid == 0) a.counters_w[GES_CTR_PAIRS] = 0;
-        return;
-    }
-    const int per = (T + kTileScanThreads - 1) / kTileScanThreads;
-    const int t0 = min(T, tid * per), t1 = min(T, t0 + per);
-    uint32_t sum = 0;
-    for (int t = t0; t < t1; ++t) sum += a.ranges[t];
-    uint32_t incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += nn;
-    }
-    if (lane == 31) s_warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t wv = s_warp[lane];
-        uint32_t wi = wv;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t nn = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += nn;
-        }
-        s_warp[lane] = wi - wv;
-        if (lane == 31) s_warp[32] = wi;
-    }
-    __syncthreads();
-    uint32_t run = s_warp[warp] + incl - sum;
-    for (int t = t0; t < t1; ++t) {
-        const uint32_t v = a.ranges[t];
-        a.ranges[t] = run;
-        run += v;
-    }
-    if (tid == 0) {
-        a.ranges[T] = s_warp[32];
-        a.counters_w[GES_CTR_PAIRS] = s_warp[32];
     }
 }
 
@@ -411,9 +411,7 @@ cudaError_t launch_bin(const BinArgs& a, cudaStream_t stream) {
     cudaError_t e;
     bin_count_kernel<<<grid, kBinThreads, 0, stream>>>(a);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    bin_colscan_kernel<<<(unsigned)((T + 31) / 32), kColThreads, 0, stream>>>(a);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    bin_tilescan_kernel<<<1, kTileScanThreads, 0, stream>>>(a);
+    bin_colscan_kernel<<<(unsigned)((T + 31) / 32), kColThreads, 0, stream>>>(a);  // + the ranges (S3)
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const int smem = kStages * kStageRec * 16;  // the record ring
     static int configured_dev[kMaxDevices] = {0};

@@ -58,7 +58,7 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     g.band_begin = 0; g.band_step = 1; g.band_rows = ty;
     // --- zero-per-frame region (one memset in ges_preprocess) ---
     g.counters = (uint64_t*)take(sizeof(uint64_t) * GES_CTR_N);
-    g.lookback = (uint32_t*)take(sizeof(uint32_t) * 64);
+    g.lookback = (uint32_t*)take(sizeof(uint64_t) * (size_t)(T / 32 + 1));  // range-scan look-back words
     // depth-sort digit totals: [kDsMaxPasses][512] u32 counts, then [512] u64 last-pass areas
     g.radix_total = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * kDsMaxPasses +
                                     sizeof(uint64_t) * kRadixDigits);
@@ -234,6 +234,7 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     b.items = (const uint4*)frame->item_rec; b.chunk_first = frame->chunk_first;
     b.counters = ctr; b.counters_w = ctr;
     b.table = frame->bin_table; b.ranges = frame->ranges; b.list = frame->list;
+    b.lookback = (unsigned long long*)frame->lookback;
     b.tiles_x = frame->tiles_x; b.rows = frame->band_rows; b.T = (int64_t)frame->tiles_x * frame->band_rows;
     // windows of whole 8-row groups (row class = row mod 8, precomputed per item)
     b.win_rows = std::max(1, std::min(frame->band_rows, kBinWinTiles / frame->tiles_x));

@@ -92,6 +92,7 @@ struct BinArgs {
     const unsigned long long* counters;  // reads CHUNKS, OVERFLOW
     unsigned long long* counters_w;   // writes PAIRS
     uint32_t* table;                  // [cmax][T] per-(chunk, tile) counts -> offsets
+    unsigned long long* lookback;     // [T / 32 + 1] published block sums of the range scan (zeroed per frame)
     uint32_t* ranges;                 // [T+1]
     uint32_t* list;                   // [cap]
     int tiles_x, rows;                // band tiles: T = tiles_x * rows
