@@ -350,6 +350,20 @@ ges_status ges_adam_step_range(float *params, const float *grads_range, float *m
                                int32_t sh_degree, const ges_adam_settings *settings, int64_t begin, int64_t count,
                                void *stream);
 
+/* Particle storage order (not a step of the hot path):
+ * permutes the planar [C][P] parameter buffer (and, if given, the Adam moments
+ * m, v) into the Morton order of the particle means -- each axis quantised to
+ * 1024 cells of the means' bounding box, bits interleaved, ties in index order
+ * (a stable sort: the permutation is deterministic).  Call after loading a
+ * scene and after every ges_densify_prune: culled particles then come in runs,
+ * which S1 and S5b skip a 128-particle tile at a time.  perm_out[j] = the old
+ * index of the particle now at j (device, [P]).  Out-of-place (in != out).
+ * workspace: device, >= ges_reorder_workspace_bytes(P), 256-B aligned. */
+size_t ges_reorder_workspace_bytes(int64_t P);
+ges_status ges_reorder(const float *params, float *params_out, const float *m, float *m_out, const float *v,
+                       float *v_out, int64_t P, int32_t sh_degree, uint32_t *perm_out, void *workspace, size_t bytes,
+                       void *stream);
+
 /* Opacity reset (what = 0): logit <- min(logit, logit(0.01)); shape reset (what = 1):
  * beta <- 2 (PAPER.md:1253 intervals; targets R30). */
 ges_status ges_reset(float *params, int64_t P, int32_t sh_degree, int32_t what, void *stream);

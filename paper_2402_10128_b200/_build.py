@@ -17,7 +17,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libges.so")
 BUILD_DIR = os.path.join(HERE, "build")
-SOURCES = ["preprocess.cu", "sort.cu", "bin.cu", "render.cu", "particle_bwd.cu", "loss.cu", "train.cu", "mix1d.cu", "grad_pack.cu", "ges_api.cu"]
+SOURCES = ["preprocess.cu", "sort.cu", "bin.cu", "render.cu", "particle_bwd.cu", "loss.cu", "train.cu", "mix1d.cu", "grad_pack.cu", "reorder.cu", "ges_api.cu"]
 HEADERS = ["ges_device.cuh", "ges_internal.h", "ges_scan.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -384,6 +384,32 @@ class Adam:
                 "ges_adam_step")
 
 
+def reorder(params: PlanarParams, opt: Optional["Adam"] = None, stream=None):
+    """Particle storage order (ges_reorder): a new PlanarParams in the Morton order of
+    the means, and perm (int32 [P], perm[j] = old index of new particle j).  With an
+    Adam `opt`, its moments are permuted alongside (replaced in place).  Call after
+    loading a scene and after densify/prune."""
+    P, deg, dev = params.P, params.sh_degree, params.flat.device
+    lib = L.load()
+    nb = lib.ges_reorder_workspace_bytes(P)
+    ws = torch.empty(nb + 256, dtype=torch.uint8, device=dev)
+    base = ws.data_ptr() + (-ws.data_ptr()) % 256
+    out = PlanarParams.empty(P, deg, dev)
+    perm = torch.empty(P, dtype=torch.int32, device=dev)
+    m_in = m_out = v_in = v_out = None
+    if opt is not None:
+        m_out, v_out = PlanarParams.empty(P, deg, dev), PlanarParams.empty(P, deg, dev)
+        m_in, v_in = C.c_void_p(opt.m.flat.data_ptr()), C.c_void_p(opt.v.flat.data_ptr())
+    L.check(lib.ges_reorder(C.c_void_p(params.flat.data_ptr()), C.c_void_p(out.flat.data_ptr()), m_in,
+                            C.c_void_p(m_out.flat.data_ptr()) if m_out is not None else None, v_in,
+                            C.c_void_p(v_out.flat.data_ptr()) if v_out is not None else None, P, deg,
+                            C.c_void_p(perm.data_ptr()), C.c_void_p(base), nb, C.c_void_p(_stream(stream))),
+            "ges_reorder")
+    if opt is not None:
+        opt.m, opt.v = m_out, v_out
+    return out, perm
+
+
 def ges_reset(params: PlanarParams, what: int, stream=None) -> None:
     """what = 0: opacity reset (kappa <= 0.01); 1: shape reset (beta = 2)."""
     L.check(L.load().ges_reset(C.c_void_p(params.flat.data_ptr()), params.P, params.sh_degree, int(what),

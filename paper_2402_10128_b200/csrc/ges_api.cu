@@ -467,6 +467,23 @@ ges_status ges_adam_step_range(float* params, const float* grads_range, float* m
     return cuda_status(launch_adam_range(a, begin, count, (cudaStream_t)stream));
 }
 
+size_t ges_reorder_workspace_bytes(int64_t P) { return P < 1 ? 0 : reorder_workspace_bytes(P); }
+
+ges_status ges_reorder(const float* params, float* params_out, const float* m, float* m_out, const float* v,
+                       float* v_out, int64_t P, int32_t sh_degree, uint32_t* perm_out, void* workspace, size_t bytes,
+                       void* stream) {
+    if (!params || !params_out || !perm_out || !workspace || P < 1 || P > 0x7fffffff || sh_degree < 0 ||
+        sh_degree > 3 || (!m != !m_out) || (!v != !v_out) || params == params_out || (m && m == m_out) ||
+        (v && v == v_out))
+        return GES_ERR_INVALID_ARG;
+    if (bytes < reorder_workspace_bytes(P)) return GES_ERR_CAPACITY;
+    if (((uintptr_t)workspace) % kAlign) return GES_ERR_INVALID_ARG;
+    const int K = (sh_degree + 1) * (sh_degree + 1);
+    const float* in[3] = {params, m, v};
+    float* out[3] = {params_out, m_out, v_out};
+    return cuda_status(launch_reorder(in, out, 3, P, 12 + 3 * K, perm_out, workspace, (cudaStream_t)stream));
+}
+
 ges_status ges_reset(float* params, int64_t P, int32_t sh_degree, int32_t what, void* stream) {
     if (!params || P < 1 || sh_degree < 0 || sh_degree > 3 || (what != 0 && what != 1)) return GES_ERR_INVALID_ARG;
     const int K = (sh_degree + 1) * (sh_degree + 1);

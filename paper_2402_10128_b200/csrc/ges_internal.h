@@ -74,6 +74,11 @@ struct DepthSortArgs {
 };
 cudaError_t launch_depth_sort(const DepthSortArgs& a, cudaStream_t stream);
 
+// --- particle storage order (reorder.cu) --------------------------------------
+size_t reorder_workspace_bytes(int64_t P);
+cudaError_t launch_reorder(const float* const* in, float* const* out, int n_buffers, int64_t P, int n_planes,
+                           uint32_t* perm, void* workspace, cudaStream_t stream);
+
 // --- direct tile binning (bin.cu) -------------------------------------------
 constexpr int kBinWinTiles = 6144;    // tiles of one binning window (shared-memory cursors)
 constexpr int kBinItemCost = 4;       // chunk cost of an item, in pair slots

@@ -374,7 +374,7 @@ __device__ void ds_tile_write(const DepthSortArgs& a, DsSmem& sm, uint32_t nvali
             const uint32_t d = ds_digit(key, kmin, shift);
             const uint32_t out = sm.base[d] + (uint32_t)s - sm.local[d];
             vout[out] = sm.vals[s];
-            kout[out] = key;
+            if (kout) kout[out] = key;
         }
     } else {
         const uint2* rs = reinterpret_cast<const uint2*>(&sm.whist[0][0]);
@@ -425,7 +425,10 @@ __device__ void ds_tile_write(const DepthSortArgs& a, DsSmem& sm, uint32_t nvali
 // tile (V <= G x 8192 after pass 0) is ranked first and its digit counts (and
 // area sums) taken from the ranking; otherwise a counting sweep precedes.
 __device__ void ds_pass(const DepthSortArgs& a, DsSmem& sm, const uint32_t* kin, const uint32_t* vin, uint32_t* kout,
-                        uint32_t* vout, int64_t r0, int64_t r1, int p, bool last, int64_t V) {
+                        uint32_t* vout, int64_t r0, int64_t r1, int p, bool last_pass, int64_t V) {
+    // the item scan rides on the last pass of a frame's sort (a plain sort -- items == null,
+    // ges_reorder -- writes the sorted ids only)
+    const bool last = last_pass && a.items != nullptr;
     const int shift = kDsBits * p;
     const bool drop = p == 0;  // pass 0 reads the S1 keys: drops the non-visible ones
     if (p > 0 && r1 - r0 <= kDsTile) {
@@ -480,7 +483,7 @@ __global__ void __launch_bounds__(kDsThreads, 1) depth_sort_kernel(DepthSortArgs
     __syncthreads();
     {
         const int64_t h0 = range_lo(P, c, G), h1 = range_lo(P, c + 1, G);
-        if (npass == 1) {   // pass 0 is the last: its area sums too
+        if (npass == 1 && a.items) {   // pass 0 is the last: its area sums too
             ds_range_hist(a, sm, a.key0, nullptr, h0, h1, 0, true, true);
         } else {
             for (int64_t t0 = h0; t0 < h1; t0 += kDsTile) {
@@ -498,7 +501,7 @@ __global__ void __launch_bounds__(kDsThreads, 1) depth_sort_kernel(DepthSortArgs
         }
     }
     if (tid < kDsDigits) {  // pass 0 of this CTA's range is counted: publish it
-        if (npass == 1) a.st_area[(size_t)c * kDsDigits + tid] = kAreaFlag | sm.acnt[tid];
+        if (npass == 1 && a.items) a.st_area[(size_t)c * kDsDigits + tid] = kAreaFlag | sm.acnt[tid];
         a.st_cnt[(size_t)c * kDsDigits + tid] = kCntFlag | sm.cnt[tid];
     }
     grid.sync();

@@ -1,0 +1,80 @@
+"""Particle storage order (ges_reorder): a stable sort by
+Morton code of the means.  Checks: perm is a permutation, the buffers are gathered
+exactly, the codes (recomputed in numpy with the same fp32 ops) are non-decreasing
+along perm with ties in index order, Adam moments follow, and rendering is invariant:
+the image of the reordered scene equals the original's and its gradients are the
+original's permuted (both against the oracle-checked path)."""
+import numpy as np
+import pytest
+import torch
+
+import ges_inputs as gi
+import paper_2402_10128_b200 as G
+
+pytestmark = pytest.mark.gpu
+
+
+def morton_np(mean):
+    m = np.asarray(mean, np.float32)
+    lo, hi = m.min(axis=1), m.max(axis=1)
+    ext = (hi - lo).astype(np.float32)
+    scale = np.where(ext > 0, np.float32(1024.0) / np.where(ext > 0, ext, np.float32(1)), np.float32(0)).astype(
+        np.float32)
+    f = ((m - lo[:, None]).astype(np.float32) * scale[:, None]).astype(np.float32)
+    q = np.clip(f, 0.0, 1023.0).astype(np.uint32)
+
+    def spread(x):
+        x = x.astype(np.uint64)
+        x = (x | (x << 16)) & 0x030000FF
+        x = (x | (x << 8)) & 0x0300F00F
+        x = (x | (x << 4)) & 0x030C30C3
+        x = (x | (x << 2)) & 0x09249249
+        return x
+    return spread(q[0]) | (spread(q[1]) << 1) | (spread(q[2]) << 2)
+
+
+@pytest.mark.parametrize("cfg", [0, 3])
+def test_reorder_is_a_stable_morton_sort(cfg):
+    sc = gi.make_config(cfg)
+    params = G.PlanarParams.from_inputs(sc.particles)
+    opt = G.Adam(params)
+    g = G.PlanarParams.from_inputs(sc.particles)
+    opt.step(params, g)                      # non-trivial moments
+    m0, v0 = opt.m.flat.clone(), opt.v.flat.clone()
+    out, perm = G.reorder(params, opt)
+    torch.cuda.synchronize()
+    p = perm.cpu().numpy().astype(np.int64)
+    P = params.P
+    assert np.array_equal(np.sort(p), np.arange(P))
+    idx = torch.from_numpy(p).cuda()
+    assert torch.equal(out.flat, params.flat[:, idx])
+    assert torch.equal(opt.m.flat, m0[:, idx]) and torch.equal(opt.v.flat, v0[:, idx])
+    codes = morton_np(params.mean.cpu().numpy())[p]
+    assert np.all(np.diff(codes.astype(np.int64)) >= 0)
+    ties = np.diff(codes.astype(np.int64)) == 0
+    assert np.all(np.diff(p)[ties] > 0)      # equal codes keep index order
+    # deterministic
+    out2, perm2 = G.reorder(params)
+    assert torch.equal(perm, perm2) and torch.equal(out.flat, out2.flat)
+
+
+def test_rendering_is_invariant_under_reorder():
+    sc = gi.make_config(1, beta_value=2.0, P=20000)
+    cam = sc.cameras[0]
+    st = G.Settings(rho=0.1)
+    params = G.PlanarParams.from_inputs(sc.particles)
+    new, perm = G.reorder(params)
+    dL = torch.from_numpy(gi.upstream_grad(sc.seed, 0, cam.width, cam.height)).cuda()
+    r0 = G.Renderer(params.P, cam.width, cam.height)
+    r1 = G.Renderer(params.P, cam.width, cam.height)
+    img0 = r0.forward(params, cam, st)
+    img1 = r1.forward(new, cam, st)
+    g0 = r0.backward(params, cam, st, dL)
+    g1 = r1.backward(new, cam, st, dL)
+    torch.cuda.synchronize()
+    # equal-depth ties break by index, which the reorder changes: allow fp32 reassociation only
+    assert torch.allclose(img0, img1, rtol=0, atol=1e-6)
+    a = g0.flat[:, perm.long()].cpu().numpy().astype(np.float64)
+    b = g1.flat.cpu().numpy().astype(np.float64)
+    floor = 1e-6 + 1e-6 * np.abs(a).max()
+    assert np.all(np.abs(a - b) <= np.maximum(1e-4 * np.abs(a), floor))
