@@ -38,6 +38,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "Mpixel-frames/s fwd and fwd+bwd iters/s at 1/2/4/8 B200 vs roofline"
+ORDER = "input"    # particle storage order of our arm (--order)
 WORKLOAD_CFG = 3
 L2_FLUSH_BYTES = 256 << 20
 
@@ -244,10 +245,30 @@ def step_stats(ms_list) -> dict:
             "p90": float(np.percentile(a, 90)), "mean": float(a.mean())}
 
 
+def morton_scene(scene, dev):
+    """The framework's particle storage order: the scene's
+    particles permuted by ges_reorder into the Morton order of their means -- the same
+    set of particles, stored the way training keeps them (reordered after every
+    densify).  Returns (scene with permuted particles, reorder ms on the device)."""
+    import dataclasses
+    import torch
+    import paper_2402_10128_b200 as G
+    params = G.PlanarParams.from_inputs(scene.particles, device=dev)
+    G.reorder(params)   # warm-up (workspace allocation, first launch)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    _, perm = G.reorder(params)
+    b.record()
+    b.synchronize()
+    p = perm.cpu().numpy().astype(np.int64)
+    return dataclasses.replace(scene, particles=scene.particles.subset(p)), a.elapsed_time(b)
+
+
 def workload_config(scene, cam, n):
     return {"workload": scene.name, "particles": scene.particles.P, "sh_degree": scene.particles.sh_degree,
             "width": cam.width, "height": cam.height, "tiles": ((cam.width + 15) // 16) * ((cam.height + 15) // 16),
-            "rho": scene.rho, "phi_mode": "scale", "views_per_rank": 1,
+            "rho": scene.rho, "phi_mode": "scale", "views_per_rank": 1, "particle_order": ORDER,
             "step": "S1-S5 fwd+bwd of one view per rank (+NCCL allreduce of particle grads if N>1)",
             "parallelism": f"dp{n} (camera-view data parallel)",
             "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MB write); inputs 360 MB > L2"}
@@ -277,7 +298,12 @@ def run_ours(args) -> None:
     dev = torch.device("cuda", torch.cuda.current_device())
     stream = torch.cuda.current_stream()
 
-    scene = gi.make_config(WORKLOAD_CFG)
+    scene_input = gi.make_config(WORKLOAD_CFG)
+    reorder_ms = None
+    if ORDER == "morton":
+        scene, reorder_ms = morton_scene(scene_input, dev)
+    else:
+        scene = scene_input
     cam = scene.cameras[rank % len(scene.cameras)]
     W, H, P = cam.width, cam.height, scene.particles.P
     st = G.Settings(rho=scene.rho)
@@ -387,6 +413,12 @@ def run_ours(args) -> None:
     value = world * W * H / (ms_per_step / 1e3) / 1e6
     comm = measure_comm(G, graph, step, grads, flush, stream, args.steps, ms_per_step, world, dev) if world > 1 else None
 
+    # ---- the same step on the generated (input) particle order, for reference ----
+    input_order = None
+    if world == 1:   # the other storage order, for reference
+        other = scene_input if ORDER == "morton" else morton_scene(scene_input, dev)[0]
+        input_order = time_step_direct(G, other, cam, st, dL, flush, stream, args.steps, dev)
+
     # ---- forward-only throughput and the equivalent-Gaussian comparator (untimed above) ----
     fwd_ms = time_forward(G, params, cam, st, frame, image, flush, stream, args.steps)
     gauss = gaussian_equivalent(G, scene, cam, dev)
@@ -481,6 +513,10 @@ def run_ours(args) -> None:
                                        "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
             "launch": graph_note,
             "comm": comm,
+            "particle_order": {"order": ORDER, "reorder_ms": reorder_ms, "other_order": input_order,
+                               "note": "order = the particle storage order timed (input: as generated; morton: "
+                                       "ges_reorder once before timing); other_order = the same step, direct "
+                                       "launches, in the other order"},
             "stages_ms": {n: float(stage_ms[i]) for i, n in enumerate(stage_names)},
             "stages_note": "per-stage CUDA events around direct launches of the same step (not the graph replay)",
             "counts": {"particles": P, "visible": V, "pairs": int(cnt.pairs), "slots": int(cnt.slots),
@@ -582,6 +618,35 @@ def particle_bwd_bytes(P, V, K):
     # reads: status/flags 2 B for all; params 12 floats + d rgb/d dir 9 floats + 48-B 2-D record for
     # visible; writes: (14 + 3K) gradient floats for all (overwrite) + 48-B record reset
     return P * 2 + V * (4 * (12 + 9) + 48 + 48) + P * 4 * (11 + 3 * K)
+
+
+def time_step_direct(G, scene, cam, st, dL, flush, stream, steps, dev):
+    """S1-S5 of one view, direct launches with an event per stage (L2 flushed between
+    steps): mean ms per step and per stage."""
+    import torch
+    params = G.PlanarParams.from_inputs(scene.particles, device=dev)
+    grads = G.PlanarParams.zeros(params.P, params.sh_degree, dev)
+    r = G.Renderer(params.P, cam.width, cam.height, device=dev)
+    img = r.forward(params, cam, st)
+    r.grow(int(r.frame.counts().slots))
+    frame = r.frame
+    names = ("preprocess", "sort", "render_fwd", "render_bwd_tiles", "backward_particles")
+    acc = np.zeros(len(names))
+    for it in range(steps + 3):
+        flush.fill_(1)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+        ev[0].record(stream)
+        G.ges_preprocess(params, cam, st, frame, stream); ev[1].record(stream)
+        G.ges_sort(frame, stream); ev[2].record(stream)
+        G.ges_render_fwd(frame, st, img, None, stream); ev[3].record(stream)
+        G.ges_render_bwd_tiles(st, frame, dL, stream); ev[4].record(stream)
+        G.ges_backward_particles(params, cam, st, frame, grads, False, stream); ev[5].record(stream)
+        ev[-1].synchronize()
+        if it >= 3:
+            acc += [ev[k].elapsed_time(ev[k + 1]) for k in range(len(names))]
+    acc /= steps
+    return {"ms_per_step": float(acc.sum()), "stages_ms": {n: float(v) for n, v in zip(names, acc)},
+            "launch": "direct launches"}
 
 
 def time_forward(G, params, cam, st, frame, image, flush, stream, steps):
@@ -731,6 +796,8 @@ def time_view_batch(G, cfg, dev, stream, steps, rank, world):
     import torch.distributed as dist
     import ges_inputs as gi
     scene = gi.make_config(cfg)
+    if ORDER == "morton":
+        scene, _ = morton_scene(scene, dev)
     cams = scene.cameras[:8] if cfg == 2 else [scene.cameras[k] for k in
                                                np.random.default_rng(2402).choice(len(scene.cameras), 8, replace=False)]
     mine = [c for k, c in enumerate(cams) if k % world == rank]
@@ -805,6 +872,8 @@ def time_small_configs(G, dev, stream, steps):
     out = {}
     for cfg, kw in ((0, {}), (1, {"beta_value": 2.0}), (2, {})):
         scene = gi.make_config(cfg, **kw)
+        if ORDER == "morton":
+            scene, _ = morton_scene(scene, dev)
         cam = scene.cameras[0]
         params = G.PlanarParams.from_inputs(scene.particles, device=dev)
         grads = G.PlanarParams.zeros(params.P, params.sh_degree, dev)
@@ -1169,9 +1238,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch every kernel directly in the timed loop")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--order", choices=["morton", "input"], default="input",
+                    help="particle storage order of our arm (DESIGN.md 'Particle order')")
     ap.add_argument("--definitional-tiles", type=int, default=16,
                     help="tiles of the oracle's definitional-mode sample in cpu_baseline (0: skip)")
     args = ap.parse_args()
+    global ORDER
+    ORDER = args.order
     if args.impl == "reference":
         run_reference(args)
     else:
