@@ -364,7 +364,7 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
             const bool clampk = g1.y > kAlphaMax;  // warp-uniform: only then can alpha reach 0.99
             // alpha' = alpha if alpha >= thr (the skip test; thr = 2 for stopped pixels), else 0;
             // the would-be transmittance T (1 - alpha') decides the stop.  (The exponent is not
-            // clamped at 0: the form is >= 0 up to rounding, G exceeds 1 by <= 2^-22 -- R19.)
+            // clamped at 0: the form is >= 0 up to rounding, G exceeds 1 by <= 2^-22 -- R19b.)
             float al[PPT], w[PPT], Tn[PPT];
             float tmin = 1.0f;
 #pragma unroll
@@ -614,7 +614,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads, PPT) render_bwd_kernel(Render
             // column, so S0 = sum q (= d alpha-part of dL/dkappa), S1 = sum q dy,
             // S2 = sum q dy^2 suffice.  alpha' = alpha where the pixel composites
             // this entry (alpha >= thr: active and not skipped), else 0; then every
-            // term below vanishes without a select.  (No exponent clamp: R19.)
+            // term below vanishes without a select.  (No exponent clamp: R19b.)
             bool contrib = false;
             float S0 = 0.0f, S1 = 0.0f, S2 = 0.0f, dk = 0.0f, Sb = 0.0f, dr = 0.0f, dgc = 0.0f, dbc = 0.0f;
             if constexpr (EXACT) {

@@ -17,6 +17,6 @@ ncu --set full --import-source on --clock-control none \
     -k regex:"render_bwd|render_fwd|preprocess_tma|particle_bwd_tma" -s 2 -c 4 \
     -o $OUT/${TAG}_full_render -f python tools/profile_step.py --steps 1 > $OUT/${TAG}_ncu_full1.log 2>&1
 ncu --set full --import-source on --clock-control none \
-    -k regex:"depth_sort|bin_" -s 5 -c 5 \
+    -k regex:"depth_sort|bin_" -s 4 -c 4 \
     -o $OUT/${TAG}_full_sort -f python tools/profile_step.py --steps 1 > $OUT/${TAG}_ncu_full2.log 2>&1
 ls -la $OUT
