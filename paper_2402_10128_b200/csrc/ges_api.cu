@@ -89,7 +89,10 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     // binning chunks: S >= 16384 slots, and the [T][chunks] table bounded by 2^24 entries
     {
         const int64_t cost = cap + kBinItemCost * P;  // chunk cost bound: M + kBinItemCost V
-        int64_t S = std::max<int64_t>(16384, (cost * T + (1 << 24) - 1) >> 24);
+#ifndef GES_BIN_CHUNK_MIN
+#define GES_BIN_CHUNK_MIN 16384
+#endif
+        int64_t S = std::max<int64_t>(GES_BIN_CHUNK_MIN, (cost * T + (1 << 24) - 1) >> 24);
         S = (S + 1023) / 1024 * 1024;
         g.bin_chunk_slots = S;
         g.bin_chunks = std::max<int64_t>(1, (cost + S - 1) / S);
