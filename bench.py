@@ -544,10 +544,9 @@ K7_OPS = 45
 # useful work only: FP32 instructions the method needs per composited (pixel, entry)
 FWD_OPS = 20
 BWD_OPS = 38
-# preprocess, ranges, 4 depth passes x (hist, scan, scatter), item scan, 2 tile passes x 3, fwd, bwd tiles, particles
-# preprocess, depth sort + item scan (one cooperative kernel), binning (count, column scan,
-# tile scan, scatter), fwd, bwd tiles, particle bwd
-LAUNCHES_PER_STEP = 1 + 1 + 4 + 1 + 1 + 1
+# kernels per step: preprocess, depth sort + item scan (one cooperative kernel), binning (count,
+# column scan + ranges, scatter), fwd, bwd tiles, particle bwd (+ the frame's zero-region memset)
+LAUNCHES_PER_STEP = 1 + 1 + 3 + 1 + 1 + 1
 
 
 def measure_comm(G, graph, step, grads, flush, stream, steps, ms_per_step, world, dev):
