@@ -399,3 +399,23 @@ def test_step_captured_as_cuda_graph_matches_direct_launches():
     a, b = g_a.flat.cpu().numpy(), g_b.flat.cpu().numpy()
     floor = 1e-6 + 1e-6 * np.abs(a).max()
     assert np.all(np.abs(a - b) <= np.maximum(1e-4 * np.abs(a), floor))
+
+
+@pytest.mark.parametrize("P", [2000, 60000])
+def test_equal_depth_ties_keep_index_order(P):
+    """R11: equal depth keys are ordered by particle index.  Every particle at the
+    same camera depth (z = 4 exactly) spread over the image: the single-sweep depth
+    sort must be stable across warps, tiles and CTAs (60 K particles: several CTAs),
+    so every tile's list is in index order; S1 state, lists, image and gradients
+    against the oracle."""
+    sc = gi.make_config(1, beta_value=2.0, P=P)
+    parts = sc.particles.subset(slice(None))
+    parts.mean[2] = 4.0
+    cam = sc.cameras[0]
+    gs, osx = settings_pair()
+    out, pre = run_case(parts, cam, gs, osx, gi.upstream_grad(sc.seed, 0, cam.width, cam.height),
+                        label=f"equal depths P={P}")
+    r = out["ranges"]
+    for t in range(r.size - 1):
+        seg = out["list"][r[t]:r[t + 1]]
+        assert np.all(np.diff(seg) > 0), t
