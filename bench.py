@@ -269,6 +269,9 @@ def workload_config(scene, cam, n):
     return {"workload": scene.name, "particles": scene.particles.P, "sh_degree": scene.particles.sh_degree,
             "width": cam.width, "height": cam.height, "tiles": ((cam.width + 15) // 16) * ((cam.height + 15) // 16),
             "rho": scene.rho, "phi_mode": "scale", "views_per_rank": 1, "particle_order": ORDER,
+            "constants": {"tile": 16, "alpha_min": "1/255", "alpha_max": 0.99, "t_min": 1e-4, "dilation": 0.3,
+                          "lambda_floor": 0.1, "jacobian_clamp": 1.3, "sh_offset": 0.5, "near": 0.2,
+                          "rect": "alpha >= 0.98/255 box (R10)"},
             "step": "S1-S5 fwd+bwd of one view per rank (+NCCL allreduce of particle grads if N>1)",
             "parallelism": f"dp{n} (camera-view data parallel)",
             "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MB write); inputs 360 MB > L2"}
@@ -291,6 +294,7 @@ def run_ours(args) -> None:
         # NCCL's INIT log (ranks, channels, NVLS) on stderr so the run shows which algorithm it chose
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")   # a hung peer aborts, not hangs
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     else:
