@@ -141,8 +141,9 @@ enum {
     GES_CTR_PAIRS = 1,    /* M: (tile, particle) pairs in the lists (R8/R10)        */
     GES_CTR_OVERFLOW = 2, /* 1 if SLOTS > pair capacity                             */
     GES_CTR_SLOTS = 3,    /* rect pairs = sum of rect areas (pair-slot count)       */
-    GES_CTR_TICKET = 4,   /* scratch                                                */
-    GES_CTR_CHUNKS = 5,   /* binning chunks of this frame (<= frame.bin_chunks)     */
+    GES_CTR_TICKET = 4,   /* scratch: chunk tickets of the row binning              */
+    GES_CTR_TICKET_COLS = 5, /* scratch: chunk tickets of the column counts         */
+    GES_CTR_TICKET_EMIT = 6, /* scratch: chunk tickets of the column binning        */
     GES_CTR_KEYMAX = 7,   /* largest visible depth key (depth sort pass plan)       */
     GES_CTR_N = 16
 };
@@ -178,24 +179,27 @@ typedef struct {
     uint32_t *vis_val[2];  /* [P] particle index, ping-pong                      */
     uint32_t *sorted_vis;  /* [V] visible particles in (depth, index) order             */
     /* ---- S2 radix scratch (depth passes) ---- */
-    uint32_t *radix_hist;  /* [4][1024][512] u32 per-CTA digit counts of each pass, published
-                              with a flag bit; then [1024][512] u64 last-pass area sums       */
-    uint32_t *radix_total; /* [4][512] u32 digit totals of each pass, then [512] u64 last-pass
-                              digit area totals (in the zero-per-frame region)               */
-    /* ---- S2 pairs and S3 ranges: direct tile binning ---- */
-    uint32_t *item_offset; /* [P] first pair slot E of each depth-sorted visible particle  */
-    uint32_t *item_rec;    /* [P][4] packed (row classes, particle, x0|y0<<16, x1|y1<<16);
-                              row classes: bit r set if a tile row y of the rect has
-                              y = r (mod 8)                                            */
-    uint32_t *chunk_first; /* [bin_chunks+1] first item of each binning chunk: the items s
-                              whose cost E[s] + 4 s lies in [k S, (k+1) S), S = bin_chunk_slots */
-    uint32_t *bin_table;   /* [bin_chunks][num_tiles] per-(chunk, tile) pair counts, then
-                              the chunk's offset inside the tile's list                   */
-    int64_t bin_chunk_slots, bin_chunks; /* S, and the chunk capacity ceil((capacity + 4 P) / S) */
+    uint32_t *radix_hist;  /* [4][1024][512] u32 per-CTA digit counts of each pass, then
+                              [4][64][512] group totals, published with a flag bit       */
+    /* ---- S2 pairs and S3 ranges: row-then-column binning ---- */
+    uint32_t *items;       /* [P][2] depth-ordered visible particles: (particle,
+                              x0 | (x1-1) << 8 | y0 << 16 | (y1-1) << 24) of the rect */
+    uint32_t *row_count;   /* [tiles_y] items covering each band row (zeroed per frame) */
+    uint32_t *rowlist;     /* [cap][2] row lists: row r = the items covering r in depth
+                              order, at the exclusive prefix of row_count; entries
+                              (particle, x0 | (x1-1) << 8)                            */
+    uint32_t *tile_count;  /* [T] pairs per tile (zeroed per frame)                   */
+    uint32_t *row_pairs;   /* [tiles_y] pairs per band row (zeroed per frame)         */
+    uint32_t *lb_rows;     /* [2][row_chunks][tiles_y] published chunk / group words of
+                              the row binning (zeroed per frame)                      */
+    uint32_t *lb_cols;     /* [2][col_chunks][tiles_x] published words of the column
+                              counts (zeroed per frame)                               */
+    uint32_t *col_excl;    /* [col_chunks][tiles_x] offset of each column chunk inside
+                              its tiles' lists                                        */
+    int64_t row_chunks;    /* ceil(P / 2048): item chunks of the row binning           */
+    int64_t col_chunks;    /* ceil(cap / 4096) + tiles_y: row-list chunks (bound)      */
     uint32_t *list;        /* [cap] per-tile lists: tile t = list[ranges[t] .. ranges[t+1]) */
     uint32_t *ranges;      /* [T+1]                                               */
-    uint32_t *lookback;    /* [T/32 + 1] u64 published block sums of the range scan
-                              (decoupled look-back; zeroed per frame)              */
     uint64_t *counters;    /* [GES_CTR_N]                                         */
     size_t zero_bytes;     /* bytes from `counters` zeroed at the start of a frame */
     /* ---- S4 / S5 ---- */
@@ -225,11 +229,11 @@ ges_status ges_frame_init(void *workspace, size_t bytes, int64_t P, int32_t widt
                           int64_t pair_capacity, ges_frame *frame);
 
 /* The frame's sub-arrays as (byte offset from the workspace base, bytes) pairs,
- * extents[2 i], extents[2 i + 1], in carving order: counters, lookback,
- * radix_total, depth, pay0, pay1, pay2, pay3, radius, rect, status, flags,
+ * extents[2 i], extents[2 i + 1], in carving order: counters, row_count,
+ * tile_count, row_pairs, lb_rows, lb_cols (the zero-per-frame region), depth, pay0, pay1, pay2, pay3, radius, rect, status, flags,
  * drgb_ddir, vis_key[0], vis_val[0], vis_key[1], vis_val[1], sorted_vis,
- * radix_hist, item_offset, item_rec, chunk_first, bin_table, list, ranges,
- * final_T, n_contrib, grad2d.  Each array starts 256-byte aligned; the bytes
+ * radix_hist, items, rowlist, col_excl, list, ranges, final_T, n_contrib,
+ * grad2d.  Each array starts 256-byte aligned; the bytes
  * between one array's end and the next one's start are padding that no
  * kernel touches (tests poison them to detect out-of-bounds writes).  Host-only.
  * *count = the number of arrays; GES_ERR_CAPACITY if it exceeds `capacity`

@@ -19,7 +19,8 @@ GES_OK, GES_ERR_INVALID_ARG, GES_ERR_CAPACITY, GES_ERR_CUDA, GES_ERR_UNSUPPORTED
 GES_PHI_SCALE, GES_PHI_VARIANCE = 0, 1
 GES_KERNEL_PHI_GAUSS, GES_KERNEL_EXACT_BETA = 0, 1
 GES_VISIBLE, GES_CULL_NEAR, GES_DEGENERATE, GES_OFFSCREEN = range(4)
-GES_CTR_VISIBLE, GES_CTR_PAIRS, GES_CTR_OVERFLOW, GES_CTR_SLOTS, GES_CTR_TICKET, GES_CTR_CHUNKS = 0, 1, 2, 3, 4, 5
+GES_CTR_VISIBLE, GES_CTR_PAIRS, GES_CTR_OVERFLOW, GES_CTR_SLOTS = 0, 1, 2, 3
+GES_CTR_TICKET, GES_CTR_TICKET_COLS, GES_CTR_TICKET_EMIT = 4, 5, 6
 GES_CTR_KEYMAX, GES_CTR_N = 7, 16
 
 _fp = C.POINTER(C.c_float)
@@ -63,9 +64,10 @@ class ges_frame(C.Structure):
         ("radius", C.c_void_p), ("rect", C.c_void_p), ("status", C.c_void_p), ("flags", C.c_void_p),
         ("drgb_ddir", C.c_void_p),
         ("vis_key", C.c_void_p * 2), ("vis_val", C.c_void_p * 2), ("sorted_vis", C.c_void_p),
-        ("radix_hist", C.c_void_p), ("radix_total", C.c_void_p), ("item_offset", C.c_void_p), ("item_rec", C.c_void_p),
-        ("chunk_first", C.c_void_p), ("bin_table", C.c_void_p), ("bin_chunk_slots", C.c_int64),
-        ("bin_chunks", C.c_int64), ("list", C.c_void_p), ("ranges", C.c_void_p), ("lookback", C.c_void_p),
+        ("radix_hist", C.c_void_p), ("items", C.c_void_p), ("row_count", C.c_void_p), ("rowlist", C.c_void_p),
+        ("tile_count", C.c_void_p), ("row_pairs", C.c_void_p), ("lb_rows", C.c_void_p), ("lb_cols", C.c_void_p),
+        ("col_excl", C.c_void_p), ("row_chunks", C.c_int64), ("col_chunks", C.c_int64),
+        ("list", C.c_void_p), ("ranges", C.c_void_p),
         ("counters", C.c_void_p), ("zero_bytes", C.c_size_t),
         ("final_T", C.c_void_p), ("n_contrib", C.c_void_p), ("grad2d", C.c_void_p),
         ("workspace_bytes", C.c_size_t),

@@ -1,429 +1,558 @@
-// bin.cu -- S2 pair generation and S3 ranges by direct tile binning
+// bin.cu -- S2 pair generation and S3 ranges by row-then-column binning
 // (DESIGN.md "Sort").
 //
-// Input: the visible particles in (depth bits, index) order as packed item
-// records (E = first pair slot, particle, x0|y0<<16, x1|y1<<16 of the R10
-// rect; written by the item scan in sort.cu).  Output: the per-tile lists
-// list[ranges[t] .. ranges[t+1]) in (depth bits, index) order -- exactly the
-// order of a stable sort of the (tile << 32 | depth) keys -- without sorting
-// any pair.
+// Input: the visible particles in (depth bits, index) order as item records
+// (particle, packed tile rect; sort.cu) and the number of items covering each
+// band tile row.  Output: the per-tile lists list[ranges[t] .. ranges[t+1]) in
+// (depth bits, index) order -- exactly the order of a stable sort of the
+// (tile << 32 | depth) keys -- without sorting any pair.
 //
-// The depth-ordered items are cut into chunks of equal cost, cost = pairs +
-// kBinItemCost x items (the item scan records the first item of every chunk).  A tile's list is then the concatenation, in
-// chunk order, of each chunk's items covering the tile, in item order:
-//   bin_count     per (chunk, window of tile rows): per-tile counts of the
-//                 chunk's items from a 2-D difference array of their rects in
-//                 shared memory (4 atomics per item) -> table[chunk][t];
-//   bin_colscan   per 32-tile column block: exclusive prefix of table[.][t]
-//                 over the chunks (32 warps split the chunks), tile total ->
-//                 ranges[t];
-//   bin_tilescan  exclusive prefix of the tile totals -> ranges, M;
-//   bin_scatter   per (chunk, window): cursors = ranges[t] + table[chunk][t]
-//                 in shared memory; the chunk's item records stream into a
-//                 4-stage shared-memory ring by TMA bulk copies (one producer
-//                 warp, mbarriers); consumer warp w owns the window's tile rows
-//                 ly = w (mod 8), so no two warps ever touch one cursor.  The
-//                 warp expands 32 items at a time into its pairs (a warp scan
-//                 of their pair counts, a 5-step shuffle search per pair) in
-//                 (item, row, column) order; pairs of one round that hit the
-//                 same tile are ranked in lane order (a conflict test in
-//                 shared memory, then a ballot multisplit only when needed),
-//                 so every tile receives its items in item order.
-// Work is O(V + M) with no pass over the pairs other than writing them once.
+// A tile's list is the subsequence of the depth-ordered items covering it.
+// Two 1-D binnings produce it:
+//   bin_rows       items -> per-row lists (row r: the items covering r, in
+//                  order; entries (particle, x0 | (x1 - 1) << 8));
+//   bin_cols_count per chunk of a row list: the column counts, their prefix
+//                  over the row's earlier chunks, and (last chunk) the tile
+//                  totals of the row;
+//   bin_cols       per chunk of a row list: entries -> the tiles' lists; the
+//                  ranges (S3) from the tile totals.
+// Both binnings work the same way on a chunk of records held by 16 warps: a
+// warp's per-bin counts from a difference array in shared memory (2 atomics
+// per record), exclusive over the warps, the chunk's offsets over the earlier
+// chunks (published vectors, two levels of 16-chunk groups, no grid barrier),
+// then per group of 32 records the LANE MASK of every bin (the records covering
+// it) from a XOR difference array -- a lane owning bin b writes the records of
+// mask(b) in lane order at its own cursor: no two lanes share a cursor and no
+// ranking is needed.  Each chunk's output is staged in shared memory and
+// copied out as one contiguous run per bin.  Work is O(V + rows V + M); the
+// pairs are written once, in coalesced runs.
 #include <algorithm>
 
 #include "ges_internal.h"
 
 namespace ges {
 
-constexpr int kBinThreads = 256;
-constexpr int kBinWarps = kBinThreads / 32;  // row classes of the scatter
-constexpr int kDiffMax = kBinWinTiles + 2 * 256 + 1;  // (rows + 1) x (tiles_x + 1)
-static_assert(kBinWarps == 8, "row classes are ly mod 8");
+constexpr int kBinThreads = 512;
+constexpr int kBinWarps = kBinThreads / 32;
+constexpr int kRowItems = kRowChunk / kBinThreads;  // items per lane (4)
+constexpr int kColItems = kColChunk / kBinThreads;  // entries per lane (8)
+constexpr int kRowStage = 8192;   // staged row-list entries (8 B) per chunk
+constexpr int kColStage = 16384;  // staged list entries (4 B) per chunk
+constexpr uint32_t kPub = 0x80000000u;  // published word flag (values < 2^31)
+constexpr int kGroup = 16;
+constexpr int kScanRows = kMaxBandRows / 32;  // rows per lane of a one-warp row scan
+static_assert(kRowItems * kBinThreads == kRowChunk && kColItems * kBinThreads == kColChunk, "chunk sizes");
 
-__device__ __forceinline__ int64_t bin_chunks(const BinArgs& a) { return (int64_t)a.counters[GES_CTR_CHUNKS]; }
-
-__device__ __forceinline__ void unpack_rect(const uint4 r, int& x0, int& y0, int& x1, int& y1) {
-    x0 = (int)(r.z & 0xffffu); y0 = (int)(r.z >> 16); x1 = (int)(r.w & 0xffffu); y1 = (int)(r.w >> 16);
-}
-
-__global__ void __launch_bounds__(kBinThreads) bin_count_kernel(BinArgs a) {
-    __shared__ int s_diff[kDiffMax];
-    if (a.counters[GES_CTR_OVERFLOW]) return;
-    const int64_t c = blockIdx.x;
-    if (c >= bin_chunks(a)) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int R0 = (int)blockIdx.y * a.win_rows, R1 = min(a.rows, R0 + a.win_rows);
-    const int nr = R1 - R0, tx = a.tiles_x, pitch = tx + 1;
-    for (int i = tid; i < (nr + 1) * pitch; i += kBinThreads) s_diff[i] = 0;
-    __syncthreads();
-    const uint32_t f = a.chunk_first[c], e = a.chunk_first[c + 1];
-    constexpr int kU = 8;  // record loads in flight per thread
-    for (uint32_t s0 = f; s0 < e; s0 += kU * kBinThreads) {
-        uint4 rec[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            const uint32_t s = s0 + u * kBinThreads + tid;
-            rec[u] = s < e ? __ldg(a.items + s) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            int x0, y0, x1, y1;
-            unpack_rect(rec[u], x0, y0, x1, y1);
-            const int ya = max(y0, R0) - R0, yb = min(y1, R1) - R0;
-            if (ya >= yb) continue;  // also the padding records (empty rects)
-            atomicAdd(&s_diff[ya * pitch + x0], 1);
-            atomicAdd(&s_diff[ya * pitch + x1], -1);
-            atomicAdd(&s_diff[yb * pitch + x0], -1);
-            atomicAdd(&s_diff[yb * pitch + x1], 1);
-        }
-    }
-    __syncthreads();
-    // prefix along x: one warp per row
-    for (int y = warp; y < nr; y += kBinWarps) {
-        int run = 0;
-        for (int x0 = 0; x0 < tx; x0 += 32) {
-            const int x = x0 + lane;
-            const int v = x < tx ? s_diff[y * pitch + x] : 0;
-            int incl = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int nn = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += nn;
-            }
-            if (x < tx) s_diff[y * pitch + x] = run + incl;
-            run += __shfl_sync(0xffffffffu, incl, 31);
-        }
-    }
-    __syncthreads();
-    // prefix along y, one thread per column (shared memory only) ...
-    for (int x = tid; x < tx; x += kBinThreads) {
-        int run = 0;
-        for (int y = 0; y < nr; ++y) {
-            run += s_diff[y * pitch + x];
-            s_diff[y * pitch + x] = run;
-        }
-    }
-    __syncthreads();
-    // ... then table[c][t] (one coalesced row per chunk)
-    for (int i = tid; i < nr * tx; i += kBinThreads) {
-        const int y = i / tx, x = i - y * tx;
-        a.table[c * a.T + R0 * tx + i] = (uint32_t)s_diff[y * pitch + x];
-    }
-}
-
-// Per block of 32 tiles (lane = tile): 32 warps split the chunks into
-// contiguous ranges; pass 1 sums each range, the ranges are scanned in shared
-// memory, pass 2 rewrites each count as its exclusive prefix.  The tile totals
-// become the ranges (S3) in the same kernel: warp 0 scans its block's 32 totals
-// and finds the pairs of all earlier blocks by a decoupled look-back over their
-// published (flagged) sums -- no separate scan launch over the tiles.
-constexpr int kColThreads = 1024;
-constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = (1ull << 62) - 1;
-__device__ __forceinline__ unsigned long long lb_load(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
+__device__ __forceinline__ uint32_t lb_load(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
-__device__ __forceinline__ void lb_store(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+__device__ __forceinline__ void lb_store(uint32_t* p, uint32_t v) {
+    asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
-__global__ void __launch_bounds__(kColThreads) bin_colscan_kernel(BinArgs a) {
-    __shared__ uint32_t s_sum[32][33];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int blk = blockIdx.x, nblk = gridDim.x;
-    const int64_t t = (int64_t)blk * 32 + lane;
-    const bool ok = t < a.T;
-    if (a.counters[GES_CTR_OVERFLOW]) {  // nothing was binned: empty ranges
-        if (warp == 0 && ok) a.ranges[t] = 0;
-        if (warp == 0 && blk == nblk - 1 && lane == 0) { a.ranges[a.T] = 0; a.counters_w[GES_CTR_PAIRS] = 0; }
-        return;
-    }
-    const int C = (int)bin_chunks(a);
-    const int per = (C + 31) / 32;
-    const int c0 = min(C, warp * per), c1 = min(C, c0 + per);
-    uint32_t sum = 0;
-    constexpr int kU = 8;
-    for (int c = c0; c < c1; c += kU) {
-        uint32_t v[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) v[u] = (ok && c + u < c1) ? a.table[(int64_t)(c + u) * a.T + t] : 0u;
-#pragma unroll
-        for (int u = 0; u < kU; ++u) sum += v[u];
-    }
-    s_sum[warp][lane] = sum;
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t run = 0;  // this tile's total
-        for (int w = 0; w < 32; ++w) {
-            const uint32_t x = s_sum[w][lane];
-            s_sum[w][lane] = run;
-            run += x;
-        }
-        // the block's exclusive prefix over its 32 tiles, its aggregate
-        uint32_t incl = run;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += nn;
-        }
-        const unsigned long long agg = __shfl_sync(0xffffffffu, incl, 31);
-        unsigned long long* st = a.lookback;
-        if (lane == 0) lb_store(st + blk, (blk == 0 ? kLbInc : kLbAgg) | agg);
-        // decoupled look-back over the earlier blocks, 32 at a time
-        unsigned long long excl = 0;
-        for (int j = blk - 1; j >= 0; j -= 32) {
-            const int idx = j - lane;
-            unsigned long long s = idx >= 0 ? lb_load(st + idx) : kLbInc;
-            while (__any_sync(0xffffffffu, (s & ~kLbVal) == 0ull)) {
-                if ((s & ~kLbVal) == 0ull) s = lb_load(st + idx);
-            }
-            const uint32_t inc = __ballot_sync(0xffffffffu, (s & kLbInc) != 0ull);
-            const int stop = inc ? __ffs(inc) - 1 : 31;  // nearest inclusive predecessor (or this window)
-            unsigned long long v = lane <= stop ? (s & kLbVal) : 0ull;
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            excl += v;
-            if (inc) break;
-        }
-        if (lane == 0 && blk > 0) lb_store(st + blk, kLbInc | (excl + agg));
-        if (ok) a.ranges[t] = (uint32_t)(excl + incl - run);
-        if (blk == nblk - 1 && lane == 31) {
-            a.ranges[a.T] = (uint32_t)(excl + incl);
-            a.counters_w[GES_CTR_PAIRS] = excl + incl;
-        }
-    }
-    __syncthreads();
-    uint32_t run = s_sum[warp][lane];
-    for (int c = c0; c < c1; c += kU) {
-        uint32_t v[kU];
-#pragma unroll
-        for (int u = 0; u < kU; ++u) v[u] = (ok && c + u < c1) ? a.table[(int64_t)(c + u) * a.T + t] : 0u;
-#pragma unroll
-        for (int u = 0; u < kU; ++u) {
-            if (ok && c + u < c1) a.table[(int64_t)(c + u) * a.T + t] = run;
-            run += v[u];
-        }
-    }
+__device__ __forceinline__ uint32_t lb_wait(const uint32_t* p) {
+    uint32_t v = lb_load(p);
+    while (!(v & kPub)) v = lb_load(p);
+    return v & ~kPub;
 }
 
-// An item's pairs in the rows ly = warp (mod 8) of the window: count, and the
-// packed geometry (x0, w - 1, first row of the class).
-__device__ __forceinline__ uint32_t class_pairs(const uint4 r, int R0, int R1, int warp, uint32_t& geo) {
-    int x0, y0, x1, y1;
-    unpack_rect(r, x0, y0, x1, y1);
-    const int ya = max(y0, R0) - R0, yb = min(y1, R1) - R0;
-    if (ya >= yb) return 0u;
-    const int nrows = ((yb + 7 - warp) >> 3) - ((ya + 7 - warp) >> 3);
-    const int w = x1 - x0;
-    const int afirst = ya + ((warp - ya) & 7);  // first row of the class
-    geo = (uint32_t)x0 | ((uint32_t)(w - 1) << 8) | ((uint32_t)afirst << 16);
-    return (uint32_t)(nrows * w);
-}
-
-constexpr int kQueue = 64;  // per-warp FIFO of item records (power of 2, >= 63)
-
-// --- mbarrier / TMA bulk-copy helpers (PTX) ---------------------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n .reg .pred p;\n"
-        "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        " @!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-// Warps 0-7 consume the chunk's item records from a 4-stage ring that warp 8
-// fills with TMA bulk copies; each consumer appends the records with pairs in
-// its rows to a private FIFO and expands every 32 queued items into pairs.
-constexpr int kStageRec = 512;  // item records per stage (8 KB)
-constexpr int kStages = 4;
-constexpr int kScatThreads = kBinThreads + 32;
-__global__ void __launch_bounds__(kScatThreads) bin_scatter_kernel(BinArgs a) {
-    extern __shared__ __align__(128) uint4 s_ring[];  // [kStages][kStageRec]
-    __shared__ uint32_t s_cur[kBinWinTiles];
-    __shared__ uint8_t s_own[kBinWinTiles];
-    __shared__ uint4 s_q[kBinWarps][kQueue];
-    __shared__ uint8_t s_mark[kBinWarps][32];
-    __shared__ __align__(8) uint64_t s_full[kStages], s_empty[kStages];
-    if (a.counters[GES_CTR_OVERFLOW]) return;
-    const int64_t c = blockIdx.x;
-    if (c >= bin_chunks(a)) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t lt_mask = (1u << lane) - 1u;
-    const int R0 = (int)blockIdx.y * a.win_rows, R1 = min(a.rows, R0 + a.win_rows);
-    const int tx = a.tiles_x, wt = (R1 - R0) * tx;
-    const int64_t tbase = (int64_t)R0 * tx;
-    const uint32_t f = a.chunk_first[c], e = a.chunk_first[c + 1];
-    const uint32_t nb = (e - f + kStageRec - 1) / kStageRec;
-    if (tid == 0) {
-        for (int i = 0; i < kStages; ++i) {
-            mbar_init(&s_full[i], 1);
-            mbar_init(&s_empty[i], kBinWarps);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+// One warp: out[i] = sum of get(j) for j < i (i < n), out[n] = the total.
+template <int BPL, class F>
+__device__ __forceinline__ void warp_excl(F get, uint32_t* out, int n) {
+    const int lane = threadIdx.x & 31;
+    uint32_t v[BPL], run = 0;
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) {
+        const int i = lane * BPL + j;
+        v[j] = i < n ? get(i) : 0u;
+        run += v[j];
     }
-    for (int i = tid; i < wt; i += kScatThreads) s_cur[i] = a.ranges[tbase + i] + a.table[c * a.T + tbase + i];
-    if (warp < kBinWarps) s_mark[warp][lane] = 0;
-    __syncthreads();
-    if (warp == kBinWarps) {  // producer
-        if (lane == 0) {
-            for (uint32_t b = 0; b < nb; ++b) {
-                const int st = (int)(b % kStages);
-                if (b >= kStages) mbar_wait(&s_empty[st], ((b / kStages) - 1) & 1);
-                const uint32_t n = min((uint32_t)kStageRec, e - f - b * kStageRec);
-                mbar_expect_tx(&s_full[st], n * 16u);
-                bulk_g2s(s_ring + st * kStageRec, a.items + f + b * kStageRec, n * 16u, &s_full[st]);
-            }
-        }
-        return;
-    }
-    int qhead = 0, qn = 0;  // FIFO state (warp-uniform)
-    // Expands the next `ng` queued items (FIFO head) into their pairs in the
-    // warp's rows, in (item, row, column) order, 32 pairs per round: the source
-    // item of each lane from the item starts marked in shared memory, the tile by
-    // an exact float division, the stable rank among equal tiles of the round by
-    // a conflict test (owner bytes) and MATCH only when needed.
-    auto expand_group = [&](int ng) {
-    uint32_t cnt = 0, geo = 0, pid = 0;
-    float rw = 0.0f;
-    if (lane < ng) {
-        const uint4 r = s_q[warp][(qhead + lane) & (kQueue - 1)];
-        cnt = class_pairs(r, R0, R1, warp, geo);
-        pid = r.y;
-        rw = __fdividef(1.0f, (float)(((geo >> 8) & 255u) + 1u));
-    }
-    qhead = (qhead + ng) & (kQueue - 1);
-    qn -= ng;
-    uint32_t incl = cnt;
+    uint32_t incl = run;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
         if (lane >= o) incl += nn;
     }
-    const uint32_t excl = incl - cnt;
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-    int carry = 0;  // source lane of the pair before this round
-    for (uint32_t base = 0; base < total; base += 32) {
-        // source lane of pair base + lane: the last item starting at or before it
-        if (cnt && excl >= base && excl < base + 32) s_mark[warp][excl - base] = (uint8_t)(lane + 1);
-        __syncwarp();
-        const uint32_t m = s_mark[warp][lane];
-        s_mark[warp][lane] = 0;
-        const uint32_t starts = __ballot_sync(0xffffffffu, m != 0u) & (0xffffffffu >> (31 - lane));
-        const int sm = (int)__shfl_sync(0xffffffffu, m, starts ? 31 - __clz(starts) : 0) - 1;
-        const int src = starts ? sm : carry;  // no start at or before this lane: the carried item
-        const uint32_t gi = base + lane;
-        const bool valid = gi < total;
-        const uint32_t s_excl = __shfl_sync(0xffffffffu, excl, src);
-        const uint32_t s_geo = __shfl_sync(0xffffffffu, geo, src);
-        const uint32_t s_pid = __shfl_sync(0xffffffffu, pid, src);
-        const float s_rw = __shfl_sync(0xffffffffu, rw, src);
-        carry = __shfl_sync(0xffffffffu, src, 31);
-        const uint32_t k = gi - s_excl;
-        const uint32_t w = ((s_geo >> 8) & 255u) + 1u;
-        // k / w exactly: k < 32 w, w <= 256, so the quotient (<= 31) is >= 0.5 / w from an
-        // integer while a few-ulp reciprocal errs by < 1e-5
-        const uint32_t ri = __float2uint_rz(__fmaf_rn((float)k, s_rw, 0.5f * s_rw));
-        const uint32_t xx = k - ri * w;
-        const uint32_t ly = (s_geo >> 16) + 8u * ri;
-        const uint32_t lt = ly * (uint32_t)tx + (s_geo & 255u) + xx;
-        // lanes of this round that hit the same tile: ranked in lane order
-        if (valid) s_own[lt] = (uint8_t)lane;
-        __syncwarp();
-        const bool lost = valid && s_own[lt] != (uint8_t)lane;
-        uint32_t peers = 1u << lane;
-        if (__any_sync(0xffffffffu, lost)) {
-#ifndef GES_BIN_BALLOT
-            peers = __match_any_sync(0xffffffffu, valid ? lt : 0xffffffffu);
-#else
-            const uint32_t cid = (ly >> 3) * (uint32_t)tx + (s_geo & 255u) + xx;
-            peers = __ballot_sync(0xffffffffu, valid);
-            for (int b = 0; b < a.rank_bits; ++b) {
-                const uint32_t bit = (cid >> b) & 1u;
-                const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-                peers &= bit ? bal : ~bal;
-            }
-#endif
-        }
-        uint32_t cur = 0;
-        if (valid) cur = s_cur[lt];
-        __syncwarp();
-        if (valid) {
-            a.list[cur + __popc(peers & lt_mask)] = s_pid;
-            if ((peers >> lane) == 1u) s_cur[lt] = cur + __popc(peers);
-        }
-        __syncwarp();
+    uint32_t ex = incl - run;
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) {
+        const int i = lane * BPL + j;
+        if (i < n) out[i] = ex;
+        ex += v[j];
     }
-};
-    for (uint32_t b = 0; b < nb || qn > 0;) {
-        if (b < nb) {
-            // enqueue this stage's records with pairs in the warp's rows
-            const int st = (int)(b % kStages);
-            mbar_wait(&s_full[st], (b / kStages) & 1);
-            const uint4* rec = s_ring + st * kStageRec;
-            const int n = (int)min((uint32_t)kStageRec, e - f - b * kStageRec);
-            for (int q0 = 0; q0 < n; q0 += 32) {
-                const int qi = q0 + lane;
-                uint4 r = make_uint4(0, 0, 0, 0);
-                if (qi < n) r = rec[qi];
-                // the record's row-class mask (sort.cu); an item whose class rows all lie
-                // outside this window is dropped later (class_pairs = 0 in expand_group)
-                const int y0 = (int)(r.z >> 16), y1 = (int)(r.w >> 16);
-                const bool rel = qi < n && ((r.x >> warp) & 1u) && y1 > R0 && y0 < R1;
-                const uint32_t bal = __ballot_sync(0xffffffffu, rel);
-                if (rel) s_q[warp][(qhead + qn + __popc(bal & lt_mask)) & (kQueue - 1)] = r;
-                qn += __popc(bal);
-                __syncwarp();
-                if (qn >= 32) {  // expand a full group
-                    expand_group(32);
-                }
+    if (lane == 31) out[n] = ex;
+}
+
+// Bin of staged slot / chunk g: the last r with first[r] <= g (bins without
+// entries share their first value with the next bin).
+__device__ __forceinline__ int row_of(const uint32_t* first, int rows, uint32_t g) {
+    int lo = 0, hi = rows - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (first[mid] <= g) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+// Exclusive prefix over the earlier chunks of a sequence of published n-vectors,
+// in two levels of kGroup chunks (as sort.cu's pass prefix): the words of the
+// earlier chunks of this chunk's group, plus the group totals of the earlier
+// groups, each published by its group's last chunk after its in-group sum.  st:
+// the sequence's chunk words [chunks][n]; gt: its group words (indexed by the
+// group's first chunk); k: this chunk, nk: the sequence's chunks; agg (shared):
+// this chunk's vector; out (shared) = the sum over chunks < k.  Chunks are
+// claimed in order (tickets), so every awaited word has a running or finished
+// writer.
+__device__ void chunk_prefix(uint32_t* st, uint32_t* gt, int64_t k, int64_t nk, int n, const uint32_t* agg,
+                             uint32_t* out) {
+    const int tid = threadIdx.x;
+    for (int i = tid; i < n; i += kBinThreads) {
+        lb_store(st + k * n + i, kPub | agg[i]);
+        out[i] = 0;
+    }
+    __syncthreads();
+    const int64_t first = k / kGroup * kGroup, glast = (first + kGroup < nk ? first + kGroup : nk) - 1;
+    const int m = (int)(k - first);
+    for (int t = tid; t < n * m; t += kBinThreads) {
+        const int i = t % n, j = t / n;
+        atomicAdd(&out[i], lb_wait(st + (first + j) * n + i));
+    }
+    __syncthreads();
+    if (k == glast)
+        for (int i = tid; i < n; i += kBinThreads) lb_store(gt + first * n + i, kPub | (out[i] + agg[i]));
+    const int ng = (int)(first / kGroup);
+    for (int t = tid; t < n * ng; t += kBinThreads) {
+        const int i = t % n, gg = t / n;
+        atomicAdd(&out[i], lb_wait(gt + (int64_t)gg * kGroup * n + i));
+    }
+    __syncthreads();
+}
+
+// Per-warp bin counts of this lane's records (difference array in shared memory,
+// then a prefix over the bins; lane owns bins [lane BPL, lane BPL + BPL)).
+template <int BPL, int N>
+__device__ __forceinline__ void warp_counts(uint32_t* sc, const int (&lo)[N], const int (&hi)[N], uint32_t valid) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int g = 0; g < N; ++g)
+        if ((valid >> g) & 1u) {
+            atomicAdd(&sc[lo[g]], 1u);
+            atomicSub(&sc[hi[g]], 1u);
+        }
+    __syncwarp();
+    uint32_t v[BPL], run = 0;
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) {
+        run += sc[lane * BPL + j];
+        v[j] = run;
+    }
+    uint32_t incl = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += nn;
+    }
+    const uint32_t ex = incl - run;
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) sc[lane * BPL + j] = v[j] + ex;
+    if (lane == 0) sc[32 * BPL] = 0;
+    __syncwarp();
+}
+
+// Lane masks of one group of 32 records: m[j] = the lanes whose record covers bin
+// lane + 32 j, from a XOR difference array (sx: the warp's [32 BPL + 1] words,
+// all zero on entry and on return).  The prefix runs over contiguous bins per
+// lane; the masks are handed out strided so that a lane's bins lie far apart
+// (the records of a group cluster in neighbouring bins: the emission loop runs
+// max over lanes of the records per bin, per j).
+template <int BPL>
+__device__ __forceinline__ void group_masks(uint32_t* sx, bool valid, int lo, int hi, uint32_t (&m)[BPL]) {
+    const int lane = threadIdx.x & 31;
+    if (valid) {
+        atomicXor(&sx[lo], 1u << lane);
+        atomicXor(&sx[hi], 1u << lane);
+    }
+    __syncwarp();
+    uint32_t c[BPL], run = 0;
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) {
+        run ^= sx[lane * BPL + j];
+        c[j] = run;
+    }
+    uint32_t x = run;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t nn = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x ^= nn;
+    }
+    const uint32_t ex = x ^ run;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) sx[lane * BPL + j] = c[j] ^ ex;
+    if (lane == 0) sx[32 * BPL] = 0u;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) {
+        m[j] = sx[lane + 32 * j];
+        sx[lane + 32 * j] = 0u;
+    }
+    __syncwarp();
+}
+
+// Emission of one group: the lane owning bin b = lane + 32 j writes the payloads
+// of the records in m[j] (lane order) at dst[cur[j]++].
+template <int BPL, class T, class Pay>
+__device__ __forceinline__ void emit_group(T* dst, const uint32_t (&m)[BPL], uint32_t (&cur)[BPL], Pay pay) {
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) {
+        uint32_t bits = m[j];
+        while (__any_sync(0xffffffffu, bits != 0u)) {
+            const int b = bits ? __ffs(bits) - 1 : 0;
+            const T v = pay(b);
+            if (bits) {
+                dst[cur[j]++] = v;
+                bits &= bits - 1u;
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&s_empty[st]);
-            ++b;
-        } else {
-            expand_group(min(qn, 32));
         }
     }
 }
 
-cudaError_t launch_bin(const BinArgs& a, cudaStream_t stream) {
-    const int T = a.tiles_x * a.rows;
-    const unsigned nwin = (unsigned)((a.rows + a.win_rows - 1) / a.win_rows);
-    const dim3 grid((unsigned)std::max(1, a.cmax), std::max(1u, nwin));
-    cudaError_t e;
-    bin_count_kernel<<<grid, kBinThreads, 0, stream>>>(a);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    bin_colscan_kernel<<<(unsigned)((T + 31) / 32), kColThreads, 0, stream>>>(a);  // + the ranges (S3)
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    const int smem = kStages * kStageRec * 16;  // the record ring
-    static int configured_dev[kMaxDevices] = {0};
-    int& configured = configured_dev[current_device()];
-    if (smem > configured) {
-        if ((e = cudaFuncSetAttribute(bin_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
-            cudaSuccess)
-            return e;
-        configured = smem;
+// Copy-out of a staged chunk: bin x's run stage[lbase[x], lbase[x+1]) goes to
+// out[gbase[x] ...) (one warp per bin, coalesced).
+template <class T>
+__device__ __forceinline__ void copy_runs(const T* stage, T* out, const uint32_t* lbase, const uint32_t* gbase, int n) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int x = warp; x < n; x += kBinWarps) {
+        const uint32_t l0 = lbase[x], len = lbase[x + 1] - l0, g0 = gbase[x];
+        for (uint32_t i = lane; i < len; i += 32) out[g0 + i] = stage[l0 + i];
     }
-    bin_scatter_kernel<<<grid, kScatThreads, smem, stream>>>(a);
+}
+
+// ---- rows: items -> per-row lists ------------------------------------------
+template <int BPL>
+__global__ void __launch_bounds__(kBinThreads) bin_rows_kernel(BinArgs a) {
+    constexpr int NB = 32 * BPL;
+    __shared__ uint32_t s_cnt[kBinWarps][NB + 1];
+    __shared__ uint32_t s_msk[kBinWarps][NB + 1];
+    __shared__ uint32_t s_agg[NB], s_excl[NB], s_lbase[NB + 1], s_gbase[kMaxBandRows + 1];
+    __shared__ unsigned long long s_k;
+    extern __shared__ __align__(16) uint2 s_rstage[];  // [kRowStage]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rows = a.rows;
+    if ((int64_t)a.counters[GES_CTR_SLOTS] > a.capacity) {  // the lists would not fit: nothing is binned
+        if (blockIdx.x == 0 && tid == 0) a.counters[GES_CTR_OVERFLOW] = 1ull;
+        return;
+    }
+    const int64_t V = (int64_t)a.counters[GES_CTR_VISIBLE];
+    if (tid == 0) s_k = atomicAdd(&a.counters[GES_CTR_TICKET], 1ull);
+    for (int i = tid; i < kBinWarps * (NB + 1); i += kBinThreads) {
+        (&s_cnt[0][0])[i] = 0u;
+        (&s_msk[0][0])[i] = 0u;
+    }
+    __syncthreads();
+    const int64_t k = (int64_t)s_k, s0 = k * kRowChunk;
+    if (s0 >= V) return;
+    const int64_t nk = (V + kRowChunk - 1) / kRowChunk;
+    // this warp's 32 x kRowItems items, groups of 32 in order
+    uint32_t pid[kRowItems], xp[kRowItems];
+    int y0[kRowItems], y1[kRowItems];
+    uint32_t valid = 0;
+    const int64_t wb = s0 + (int64_t)warp * 32 * kRowItems;
+#pragma unroll
+    for (int g = 0; g < kRowItems; ++g) {
+        const int64_t idx = wb + g * 32 + lane;
+        const uint2 it = idx < V ? a.items[idx] : make_uint2(0u, 0u);
+        if (idx < V) valid |= 1u << g;
+        pid[g] = it.x;
+        xp[g] = it.y & 0xffffu;
+        y0[g] = (int)((it.y >> 16) & 255u);
+        y1[g] = (int)(it.y >> 24) + 1;
+    }
+    warp_counts<BPL>(s_cnt[warp], y0, y1, valid);
+    __syncthreads();
+    if (tid < rows) {  // exclusive over the warps; the chunk's row counts
+        uint32_t run = 0;
+        for (int w = 0; w < kBinWarps; ++w) {
+            const uint32_t x = s_cnt[w][tid];
+            s_cnt[w][tid] = run;
+            run += x;
+        }
+        s_agg[tid] = run;
+    }
+    __syncthreads();
+    chunk_prefix(a.lb_rows, a.lb_rows + a.row_chunks * rows, k, nk, rows, s_agg, s_excl);
+    if (warp == 0) {  // global first slot of this chunk's entries in each row
+        warp_excl<kScanRows>([&](int i) { return a.row_count[i]; }, s_gbase, rows);
+        __syncwarp();
+        for (int i = lane; i < rows; i += 32) s_gbase[i] += s_excl[i];
+    } else if (warp == 1) {  // staging offsets
+        warp_excl<BPL>([&](int i) { return s_agg[i]; }, s_lbase, rows);
+    }
+    __syncthreads();
+    const uint32_t total = s_lbase[rows];
+    const bool staged = total <= (uint32_t)kRowStage;
+    uint32_t cur[BPL];
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) {
+        const int y = lane + 32 * j;
+        cur[j] = y < rows ? (staged ? s_lbase[y] : s_gbase[y]) + s_cnt[warp][y] : 0u;
+    }
+#pragma unroll
+    for (int g = 0; g < kRowItems; ++g) {
+        uint32_t m[BPL];
+        group_masks<BPL>(s_msk[warp], (valid >> g) & 1u, y0[g], y1[g], m);
+        auto pay = [&](int b) {
+            return make_uint2(__shfl_sync(0xffffffffu, pid[g], b), __shfl_sync(0xffffffffu, xp[g], b));
+        };
+        if (staged) emit_group<BPL>(s_rstage, m, cur, pay);
+        else emit_group<BPL>(a.rowlist, m, cur, pay);
+    }
+    __syncthreads();
+    if (staged) copy_runs(s_rstage, a.rowlist, s_lbase, s_gbase, rows);
+}
+
+// Row scans shared by the column kernels: s_rb = first row-list entry of each
+// row, s_cf = first column chunk of each row ([rows] = the totals).
+__device__ __forceinline__ void row_tables(const BinArgs& a, uint32_t* s_rb, uint32_t* s_cf) {
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) warp_excl<kScanRows>([&](int i) { return a.row_count[i]; }, s_rb, a.rows);
+    else if (warp == 1)
+        warp_excl<kScanRows>([&](int i) { return (a.row_count[i] + (uint32_t)kColChunk - 1u) / (uint32_t)kColChunk; },
+                             s_cf, a.rows);
+}
+
+// ---- columns, pass 1: per-chunk column counts and their prefix ---------------
+template <int BPL>
+__global__ void __launch_bounds__(kBinThreads) bin_cols_count_kernel(BinArgs a) {
+    constexpr int NB = 32 * BPL;
+    __shared__ uint32_t s_rb[kMaxBandRows + 1], s_cf[kMaxBandRows + 1];
+    __shared__ uint32_t s_d[NB + 1], s_excl[NB];
+    __shared__ uint32_t s_sum;
+    __shared__ unsigned long long s_g;
+    if (a.counters[GES_CTR_OVERFLOW]) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rows = a.rows, tx = a.tiles_x;
+    row_tables(a, s_rb, s_cf);
+    __syncthreads();
+    const uint32_t G2 = s_cf[rows];
+    for (;;) {
+        if (tid == 0) { s_g = atomicAdd(&a.counters[GES_CTR_TICKET_COLS], 1ull); s_sum = 0; }
+        for (int i = tid; i <= NB; i += kBinThreads) s_d[i] = 0u;
+        __syncthreads();
+        const uint64_t g = s_g;
+        if (g >= G2) break;
+        const int y = row_of(s_cf, rows, (uint32_t)g);
+        const int64_t k = (int64_t)g - s_cf[y], nk = (int64_t)s_cf[y + 1] - s_cf[y];
+        const uint32_t e0 = s_rb[y] + (uint32_t)k * kColChunk, e1 = min(e0 + (uint32_t)kColChunk, s_rb[y + 1]);
+        uint32_t r[kColItems];
+#pragma unroll
+        for (int u = 0; u < kColItems; ++u) {
+            const uint32_t e = e0 + u * kBinThreads + tid;
+            r[u] = e < e1 ? a.rowlist[e].y : 0xffffffffu;
+        }
+#pragma unroll
+        for (int u = 0; u < kColItems; ++u)
+            if (r[u] != 0xffffffffu) {
+                atomicAdd(&s_d[r[u] & 255u], 1u);
+                atomicSub(&s_d[((r[u] >> 8) & 255u) + 1u], 1u);
+            }
+        __syncthreads();
+        if (warp == 0) {  // column counts (inclusive prefix of the difference array)
+            uint32_t v[BPL], run = 0;
+#pragma unroll
+            for (int j = 0; j < BPL; ++j) { run += s_d[lane * BPL + j]; v[j] = run; }
+            uint32_t incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += nn;
+            }
+            const uint32_t ex = incl - run;
+#pragma unroll
+            for (int j = 0; j < BPL; ++j) s_d[lane * BPL + j] = v[j] + ex;
+        }
+        __syncthreads();
+        const int64_t g0 = (int64_t)g - k;  // the row's first chunk
+        chunk_prefix(a.lb_cols + g0 * tx, a.lb_cols + (a.col_chunks + g0) * tx, k, nk, tx, s_d, s_excl);
+        for (int x = tid; x < tx; x += kBinThreads) a.col_excl[g * tx + x] = s_excl[x];
+        if (k == nk - 1) {  // the row's tile totals
+            uint32_t part = 0;
+            for (int x = tid; x < tx; x += kBinThreads) {
+                const uint32_t t = s_excl[x] + s_d[x];
+                a.tile_count[(int64_t)y * tx + x] = t;
+                part += t;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            if (lane == 0 && part) atomicAdd(&s_sum, part);
+            __syncthreads();
+            if (tid == 0) a.row_pairs[y] = s_sum;
+        }
+        __syncthreads();
+    }
+}
+
+// ---- columns, pass 2: row-list entries -> tile lists; the ranges -------------
+template <int BPL>
+__global__ void __launch_bounds__(kBinThreads) bin_cols_kernel(BinArgs a) {
+    constexpr int NB = 32 * BPL;
+    __shared__ uint32_t s_cnt[kBinWarps][NB + 1];
+    __shared__ uint32_t s_msk[kBinWarps][NB + 1];
+    __shared__ uint32_t s_rb[kMaxBandRows + 1], s_cf[kMaxBandRows + 1], s_rp[kMaxBandRows + 1];
+    __shared__ uint32_t s_lbase[NB + 1], s_gbase[NB + 1];
+    __shared__ unsigned long long s_g;
+    extern __shared__ __align__(16) uint32_t s_cstage[];  // [kColStage]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rows = a.rows, tx = a.tiles_x;
+    const bool ovf = a.counters[GES_CTR_OVERFLOW] != 0;
+    row_tables(a, s_rb, s_cf);
+    if (warp == 2) warp_excl<kScanRows>([&](int i) { return a.row_pairs[i]; }, s_rp, rows);
+    for (int i = tid; i < kBinWarps * (NB + 1); i += kBinThreads) (&s_msk[0][0])[i] = 0u;
+    __syncthreads();
+    // S3: ranges of the rows y = blockIdx.x (mod gridDim.x); on overflow every count is 0
+    if (warp == 0) {
+        for (int y = blockIdx.x; y < rows; y += gridDim.x) {
+            warp_excl<BPL>([&](int i) { return a.tile_count[(int64_t)y * tx + i]; }, s_gbase, tx);
+            __syncwarp();
+            for (int x = lane; x < tx; x += 32) a.ranges[(int64_t)y * tx + x] = s_rp[y] + s_gbase[x];
+            __syncwarp();
+        }
+        if (blockIdx.x == 0 && lane == 0) {
+            a.ranges[(int64_t)rows * tx] = s_rp[rows];
+            a.counters[GES_CTR_PAIRS] = s_rp[rows];
+        }
+    }
+    if (ovf) return;
+    const uint32_t G2 = s_cf[rows];
+    for (;;) {
+        if (tid == 0) s_g = atomicAdd(&a.counters[GES_CTR_TICKET_EMIT], 1ull);
+        for (int i = tid; i < kBinWarps * (NB + 1); i += kBinThreads) (&s_cnt[0][0])[i] = 0u;
+        __syncthreads();
+        const uint64_t g = s_g;
+        if (g >= G2) break;
+        const int y = row_of(s_cf, rows, (uint32_t)g);
+        const uint32_t k = (uint32_t)g - s_cf[y];
+        const uint32_t e0 = s_rb[y] + k * kColChunk, e1 = min(e0 + (uint32_t)kColChunk, s_rb[y + 1]);
+        if (warp == 0) {  // first list slot of this chunk's entries in each tile of the row
+            warp_excl<BPL>([&](int i) { return a.tile_count[(int64_t)y * tx + i]; }, s_gbase, tx);
+            __syncwarp();
+            for (int x = lane; x < tx; x += 32) s_gbase[x] += s_rp[y] + a.col_excl[g * tx + x];
+        }
+        // this warp's entries [e0 + warp 32 kColItems, ...), groups of 32 in order
+        uint32_t pid[kColItems];
+        int x0[kColItems], x1[kColItems];
+        uint32_t valid = 0;
+        const uint32_t wb = e0 + (uint32_t)warp * 32 * kColItems;
+#pragma unroll
+        for (int g2 = 0; g2 < kColItems; ++g2) {
+            const uint32_t e = wb + g2 * 32 + lane;
+            const uint2 r = e < e1 ? a.rowlist[e] : make_uint2(0u, 0u);
+            if (e < e1) valid |= 1u << g2;
+            pid[g2] = r.x;
+            x0[g2] = (int)(r.y & 255u);
+            x1[g2] = (int)((r.y >> 8) & 255u) + 1;
+        }
+        warp_counts<BPL>(s_cnt[warp], x0, x1, valid);
+        __syncthreads();
+        if (tid < tx) {  // exclusive over the warps; the chunk's column counts
+            uint32_t run = 0;
+            for (int w = 0; w < kBinWarps; ++w) {
+                const uint32_t x = s_cnt[w][tid];
+                s_cnt[w][tid] = run;
+                run += x;
+            }
+            s_lbase[tid] = run;
+        }
+        __syncthreads();
+        if (warp == 0) {  // staging offsets
+            uint32_t v[BPL];
+#pragma unroll
+            for (int j = 0; j < BPL; ++j) v[j] = lane * BPL + j < tx ? s_lbase[lane * BPL + j] : 0u;
+            __syncwarp();
+            warp_excl<BPL>([&](int i) {
+                uint32_t r = 0;
+#pragma unroll
+                for (int j = 0; j < BPL; ++j) r = (i == lane * BPL + j) ? v[j] : r;
+                return r;
+            }, s_lbase, tx);
+        }
+        __syncthreads();
+        const uint32_t total = s_lbase[tx];
+        const bool staged = total <= (uint32_t)kColStage;
+        uint32_t cur[BPL];
+#pragma unroll
+        for (int j = 0; j < BPL; ++j) {
+            const int x = lane + 32 * j;
+            cur[j] = x < tx ? (staged ? s_lbase[x] : s_gbase[x]) + s_cnt[warp][x] : 0u;
+        }
+#pragma unroll
+        for (int g2 = 0; g2 < kColItems; ++g2) {
+            uint32_t m[BPL];
+            group_masks<BPL>(s_msk[warp], (valid >> g2) & 1u, x0[g2], x1[g2], m);
+            auto pay = [&](int b) { return __shfl_sync(0xffffffffu, pid[g2], b); };
+            if (staged) emit_group<BPL>(s_cstage, m, cur, pay);
+            else emit_group<BPL>(a.list, m, cur, pay);
+        }
+        __syncthreads();
+        if (staged) copy_runs(s_cstage, a.list, s_lbase, s_gbase, tx);
+        __syncthreads();
+    }
+}
+
+template <class K>
+static cudaError_t set_smem(K kernel, int bytes, int* done) {
+    int& d = done[current_device()];
+    if (d) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) d = 1;
+    return e;
+}
+
+template <int BR>
+static cudaError_t launch_rows(const BinArgs& a, cudaStream_t stream) {
+    static int done[kMaxDevices] = {0};
+    const int smem = kRowStage * (int)sizeof(uint2);
+    cudaError_t e = set_smem(bin_rows_kernel<BR>, smem, done);
+    if (e != cudaSuccess) return e;
+    bin_rows_kernel<BR><<<(unsigned)std::max<int64_t>(1, a.row_chunks), kBinThreads, smem, stream>>>(a);
     return cudaGetLastError();
+}
+
+template <int BC>
+static cudaError_t launch_cols(const BinArgs& a, cudaStream_t stream) {
+    static int done[kMaxDevices] = {0};
+    const int smem = kColStage * (int)sizeof(uint32_t);
+    cudaError_t e = set_smem(bin_cols_kernel<BC>, smem, done);
+    if (e != cudaSuccess) return e;
+    bin_cols_count_kernel<BC><<<num_sms() * 4, kBinThreads, 0, stream>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    bin_cols_kernel<BC><<<num_sms() * 2, kBinThreads, smem, stream>>>(a);
+    return cudaGetLastError();
+}
+
+static int bins_per_lane(int n) {
+    const int b = std::max(1, (n + 31) / 32);
+    return b <= 4 ? b : 8;
+}
+
+cudaError_t launch_bin(const BinArgs& a, cudaStream_t stream) {
+    cudaError_t e;
+    switch (bins_per_lane(a.rows)) {
+        case 1: e = launch_rows<1>(a, stream); break;
+        case 2: e = launch_rows<2>(a, stream); break;
+        case 3: e = launch_rows<3>(a, stream); break;
+        case 4: e = launch_rows<4>(a, stream); break;
+        default: e = launch_rows<8>(a, stream); break;
+    }
+    if (e != cudaSuccess) return e;
+    switch (bins_per_lane(a.tiles_x)) {
+        case 1: return launch_cols<1>(a, stream);
+        case 2: return launch_cols<2>(a, stream);
+        case 3: return launch_cols<3>(a, stream);
+        case 4: return launch_cols<4>(a, stream);
+        default: return launch_cols<8>(a, stream);
+    }
 }
 
 }  // namespace ges

@@ -57,11 +57,14 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     g.num_tiles = (int32_t)T; g.tile_bits = std::max(1, bits_for(T)); g.sh_degree_max = 3;
     g.band_begin = 0; g.band_step = 1; g.band_rows = ty;
     // --- zero-per-frame region (one memset in ges_preprocess) ---
+    g.row_chunks = (P + kRowChunk - 1) / kRowChunk;
+    g.col_chunks = (cap + kColChunk - 1) / kColChunk + ty;
     g.counters = (uint64_t*)take(sizeof(uint64_t) * GES_CTR_N);
-    g.lookback = (uint32_t*)take(sizeof(uint64_t) * (size_t)(T / 32 + 1));  // range-scan look-back words
-    // depth-sort digit totals: [kDsMaxPasses][512] u32 counts, then [512] u64 last-pass areas
-    g.radix_total = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * kDsMaxPasses +
-                                    sizeof(uint64_t) * kRadixDigits);
+    g.row_count = (uint32_t*)take(sizeof(uint32_t) * ty);
+    g.tile_count = (uint32_t*)take(sizeof(uint32_t) * (size_t)T);
+    g.row_pairs = (uint32_t*)take(sizeof(uint32_t) * ty);
+    g.lb_rows = (uint32_t*)take(sizeof(uint32_t) * 2 * (size_t)g.row_chunks * ty);
+    g.lb_cols = (uint32_t*)take(sizeof(uint32_t) * 2 * (size_t)g.col_chunks * tx);
     g.zero_bytes = off;  // bytes of the zero region from the workspace base
     // --- per particle ---
     g.depth = (float*)take(sizeof(float) * P);
@@ -79,26 +82,12 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
         g.vis_val[k] = (uint32_t*)take(sizeof(uint32_t) * P);
     }
     g.sorted_vis = (uint32_t*)take(sizeof(uint32_t) * P);
-    // depth-sort published words: [kDsMaxPasses][kDsMaxGrid][512] u32, then [kDsMaxGrid][512] u64
+    // depth-sort published words: [kDsMaxPasses][kDsMaxGrid][512] u32, then [kDsMaxPasses][kDsMaxGroups][512]
     g.radix_hist = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * (size_t)kDsMaxGrid * kDsMaxPasses +
-                                   sizeof(uint64_t) * kRadixDigits * (size_t)kDsMaxGrid +
-                                   sizeof(uint32_t) * kRadixDigits * (size_t)kDsMaxGroups * kDsMaxPasses +
-                                   sizeof(uint64_t) * kRadixDigits * (size_t)kDsMaxGroups);
-    g.item_offset = (uint32_t*)take(sizeof(uint32_t) * P);
-    g.item_rec = (uint32_t*)take(16 * (size_t)P);
-    // binning chunks: S >= 16384 slots, and the [T][chunks] table bounded by 2^24 entries
-    {
-        const int64_t cost = cap + kBinItemCost * P;  // chunk cost bound: M + kBinItemCost V
-#ifndef GES_BIN_CHUNK_MIN
-#define GES_BIN_CHUNK_MIN 16384
-#endif
-        int64_t S = std::max<int64_t>(GES_BIN_CHUNK_MIN, (cost * T + (1 << 24) - 1) >> 24);
-        S = (S + 1023) / 1024 * 1024;
-        g.bin_chunk_slots = S;
-        g.bin_chunks = std::max<int64_t>(1, (cost + S - 1) / S);
-    }
-    g.chunk_first = (uint32_t*)take(sizeof(uint32_t) * (size_t)(g.bin_chunks + 1));
-    g.bin_table = (uint32_t*)take(sizeof(uint32_t) * (size_t)T * (size_t)g.bin_chunks);
+                                   sizeof(uint32_t) * kRadixDigits * (size_t)kDsMaxGroups * kDsMaxPasses);
+    g.items = (uint32_t*)take(8 * (size_t)P);
+    g.rowlist = (uint32_t*)take(8 * (size_t)cap);
+    g.col_excl = (uint32_t*)take(sizeof(uint32_t) * (size_t)g.col_chunks * tx);
     g.list = (uint32_t*)take(sizeof(uint32_t) * (size_t)cap);
     g.ranges = (uint32_t*)take(sizeof(uint32_t) * (size_t)(T + 1));
     g.final_T = (float*)take(sizeof(float) * HW);
@@ -212,38 +201,34 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long* ctr = (unsigned long long*)frame->counters;
     cudaError_t e;
-    // depth sort (4 passes; pass 0 compacts the visible set) + item scan: one
-    // cooperative kernel.  Keys: vis_key[0] -> [1] -> [0] -> [1] -> (values only) sorted_vis
+    // depth sort (<= 4 passes; pass 0 compacts the visible set; the last one writes the
+    // item records): one cooperative kernel.  Keys: vis_key[0] -> [1] -> [0] -> [1] ->
+    // (values only) sorted_vis
     DepthSortArgs ds;
     ds.key0 = frame->vis_key[0];
     ds.keys[0] = frame->vis_key[1]; ds.keys[1] = frame->vis_key[0];
     ds.vals[0] = frame->vis_val[1]; ds.vals[1] = frame->vis_val[0];
     ds.sorted_vis = frame->sorted_vis;
     ds.st_cnt = frame->radix_hist;
-    ds.st_area = (unsigned long long*)(frame->radix_hist + (size_t)kRadixDigits * kDsMaxGrid * kDsMaxPasses);
-    ds.gt_cnt = (uint32_t*)(ds.st_area + (size_t)kRadixDigits * kDsMaxGrid);
-    ds.gt_area = (unsigned long long*)(ds.gt_cnt + (size_t)kRadixDigits * kDsMaxGroups * kDsMaxPasses);
-    ds.tot = frame->radix_total;
-    ds.atot = (unsigned long long*)(frame->radix_total + kRadixDigits * kDsMaxPasses);
+    ds.gt_cnt = frame->radix_hist + (size_t)kRadixDigits * kDsMaxGrid * kDsMaxPasses;
     ds.P = frame->P; ds.G = 0; ds.key_base = frame->depth_key_base;
     ds.rect = (const ushort4*)frame->rect;
-    ds.E = frame->item_offset; ds.items = (uint4*)frame->item_rec;
-    ds.chunk_first = frame->chunk_first; ds.chunk_slots = frame->bin_chunk_slots;
-    ds.capacity = frame->pair_capacity;
+    ds.items = (uint2*)frame->items;
+    ds.row_count = frame->row_count;
+    ds.rows = frame->band_rows;
     ds.counters = ctr;
     if ((e = launch_depth_sort(ds, s)) != cudaSuccess) return GES_ERR_CUDA;
-    // every (tile, particle) pair written once, in depth order, into its tile's list
+    // rows, then columns: every (tile, particle) pair written once, in depth order
     BinArgs b;
-    b.items = (const uint4*)frame->item_rec; b.chunk_first = frame->chunk_first;
-    b.counters = ctr; b.counters_w = ctr;
-    b.table = frame->bin_table; b.ranges = frame->ranges; b.list = frame->list;
-    b.lookback = (unsigned long long*)frame->lookback;
-    b.tiles_x = frame->tiles_x; b.rows = frame->band_rows; b.T = (int64_t)frame->tiles_x * frame->band_rows;
-    // windows of whole 8-row groups (row class = row mod 8, precomputed per item)
-    b.win_rows = std::max(1, std::min(frame->band_rows, kBinWinTiles / frame->tiles_x));
-    if (b.win_rows < frame->band_rows) b.win_rows &= ~7;
-    b.cmax = (int)frame->bin_chunks; b.chunk_slots = frame->bin_chunk_slots;
-    b.rank_bits = std::max(1, bits_for((int64_t)((b.win_rows + 7) / 8) * frame->tiles_x));
+    b.items = (const uint2*)frame->items; b.row_count = frame->row_count;
+    b.rowlist = (uint2*)frame->rowlist;
+    b.lb_rows = frame->lb_rows; b.lb_cols = frame->lb_cols; b.col_excl = frame->col_excl;
+    b.tile_count = frame->tile_count; b.row_pairs = frame->row_pairs;
+    b.ranges = frame->ranges; b.list = frame->list;
+    b.counters = ctr;
+    b.tiles_x = frame->tiles_x; b.rows = frame->band_rows;
+    b.capacity = frame->pair_capacity;
+    b.row_chunks = frame->row_chunks; b.col_chunks = frame->col_chunks;
     if ((e = launch_bin(b, s)) != cudaSuccess) return GES_ERR_CUDA;
     return GES_OK;
 }

@@ -50,27 +50,30 @@ constexpr int kDsMaxGrid = 1024;      // max CTAs of the cooperative depth sort
 constexpr int kDsMaxPasses = 4;       // 9-bit digits of a 32-bit key
 constexpr int kDsMaxGroups = kDsMaxGrid / 16;  // CTA groups of the two-level pass prefix (sort.cu)
 
+constexpr int kMaxBandRows = 256;     // tile rows of a frame (ges_frame_init: <= 256 per axis)
+
+// Item record of a depth-sorted visible particle (sort.cu -> bin.cu): particle
+// index, and its nonempty tile rect [x0, x1) x [y0, y1) packed as
+// x0 | (x1 - 1) << 8 | y0 << 16 | (y1 - 1) << 24 (tile coordinates < 256).
+__device__ __forceinline__ uint32_t pack_rect(uint32_t x0, uint32_t y0, uint32_t x1, uint32_t y1) {
+    return x0 | ((x1 - 1u) << 8) | (y0 << 16) | ((y1 - 1u) << 24);
+}
+
 struct DepthSortArgs {
     const uint32_t* key0;             // [P] preprocess keys: depth bits, 0xffffffff = not visible
     uint32_t* keys[2];                // [P] ping-pong (keys[0] may not alias key0; keys[1] may)
     uint32_t* vals[2];                // [P] ping-pong
     uint32_t* sorted_vis;             // [V] out: visible particles in (depth bits, index) order
     uint32_t* st_cnt;                 // [kDsMaxPasses][kDsMaxGrid][512] published per-CTA digit counts
-    unsigned long long* st_area;      // [kDsMaxGrid][512] published per-CTA digit area sums (last pass)
     uint32_t* gt_cnt;                 // [kDsMaxPasses][kDsMaxGroups][512] published group totals
-    unsigned long long* gt_area;      // [kDsMaxGroups][512] published group area totals (last pass)
-    uint32_t* tot;                    // [kDsMaxPasses][512] digit totals (zeroed per frame)
-    unsigned long long* atot;         // [512] last-pass digit area totals (zeroed per frame)
     int64_t P;
     int G;                            // grid (set by the launcher)
     uint32_t key_base;                // fp32 bits of near_z: every visible key is larger
     const ushort4* rect;
-    uint32_t* E;                      // [V] first pair slot of each sorted particle
-    uint4* items;                     // [V] packed (E, particle, x0|y0<<16, x1|y1<<16)
-    uint32_t* chunk_first;            // [chunks + 1] first item of every binning chunk
-    int64_t chunk_slots;              // binning chunk cost S (bin.cu)
-    int64_t capacity;                 // pair capacity
-    unsigned long long* counters;     // reads VISIBLE; writes SLOTS, OVERFLOW, CHUNKS
+    uint2* items;                     // [V] out: (particle, pack_rect) in depth order (null: plain sort)
+    uint32_t* row_count;              // [rows] out (+=): items covering each band row (zeroed per frame)
+    int rows;                         // band rows (<= kMaxBandRows)
+    unsigned long long* counters;     // reads VISIBLE, KEYMAX; adds SLOTS
 };
 cudaError_t launch_depth_sort(const DepthSortArgs& a, cudaStream_t stream);
 
@@ -79,33 +82,24 @@ size_t reorder_workspace_bytes(int64_t P);
 cudaError_t launch_reorder(const float* const* in, float* const* out, int n_buffers, int64_t P, int n_planes,
                            uint32_t* perm, void* workspace, cudaStream_t stream);
 
-// --- direct tile binning (bin.cu) -------------------------------------------
-constexpr int kBinWinTiles = 6144;    // tiles of one binning window (shared-memory cursors)
-constexpr int kBinItemCost = 4;       // chunk cost of an item, in pair slots
-// Bit r (r < 8) set if some tile row y in [y0, y1) has y = r (mod 8): the
-// binning scatter's warp r owns those rows (windows start at multiples of 8).
-__device__ __forceinline__ uint32_t row_class_mask(uint32_t y0, uint32_t y1) {
-    if (y1 <= y0) return 0u;
-    if (y1 - y0 >= 8u) return 0xffu;
-    const uint32_t m = ((1u << (y1 - y0)) - 1u) << (y0 & 7u);
-    return (m | (m >> 8)) & 0xffu;
-}
-
+// --- row-then-column binning (bin.cu) ----------------------------------------
+constexpr int kRowChunk = 2048;       // items per row-binning CTA
+constexpr int kColChunk = 4096;       // row-list entries per column-binning CTA
 struct BinArgs {
-    const uint4* items;               // [V] item records in depth order (item scan)
-    const uint32_t* chunk_first;      // [chunks + 1]
-    const unsigned long long* counters;  // reads CHUNKS, OVERFLOW
-    unsigned long long* counters_w;   // writes PAIRS
-    uint32_t* table;                  // [cmax][T] per-(chunk, tile) counts -> offsets
-    unsigned long long* lookback;     // [T / 32 + 1] published block sums of the range scan (zeroed per frame)
+    const uint2* items;               // [V] depth-ordered item records (sort.cu)
+    const uint32_t* row_count;        // [rows] items covering each row (sort.cu)
+    uint2* rowlist;                   // [cap] per-row lists of (particle, x0 | (x1 - 1) << 8)
+    uint32_t* lb_rows;                // [2][row_chunks][rows] published words (zeroed per frame)
+    uint32_t* lb_cols;                // [2][col_chunks][tiles_x] published words (zeroed per frame)
+    uint32_t* col_excl;               // [col_chunks][tiles_x] per-chunk exclusive column offsets
+    uint32_t* tile_count;             // [rows][tiles_x] pairs per tile (zeroed per frame)
+    uint32_t* row_pairs;              // [rows] pairs per row (zeroed per frame)
     uint32_t* ranges;                 // [T+1]
     uint32_t* list;                   // [cap]
+    unsigned long long* counters;     // reads VISIBLE, SLOTS; writes OVERFLOW, PAIRS; tickets
     int tiles_x, rows;                // band tiles: T = tiles_x * rows
-    int64_t T;
-    int win_rows;                     // tile rows per window (win_rows * tiles_x <= kBinWinTiles)
-    int cmax;                         // chunk capacity (table row length, grid.x)
-    int64_t chunk_slots;
-    int rank_bits;                    // bits of a warp-local tile id (ballot ranking)
+    int64_t capacity;                 // pair capacity
+    int64_t row_chunks, col_chunks;   // capacities of the look-back words
 };
 cudaError_t launch_bin(const BinArgs& a, cudaStream_t stream);
 

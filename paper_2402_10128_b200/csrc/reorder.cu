@@ -98,7 +98,7 @@ __global__ void reorder_gather_kernel(const float* in, float* out, int64_t P, in
 }
 
 // Workspace: box (8 ints) | counters | keys0 [P] | keys [2][P] | vals [2][P] | the
-// depth sort's published words and totals.
+// depth sort's published words.
 static size_t carve(char* base, int64_t P, DepthSortArgs* ds, int** box) {
     size_t off = 0;
     auto take = [&](size_t bytes) -> char* {
@@ -114,17 +114,13 @@ static size_t carve(char* base, int64_t P, DepthSortArgs* ds, int** box) {
     uint32_t* v1 = (uint32_t*)take(4 * (size_t)P);
     uint32_t* v2 = (uint32_t*)take(4 * (size_t)P);
     uint32_t* stc = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * (size_t)kDsMaxGrid * kDsMaxPasses);
-    unsigned long long* sta = (unsigned long long*)take(sizeof(uint64_t) * kRadixDigits * (size_t)kDsMaxGrid);
     uint32_t* gtc = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * (size_t)kDsMaxGroups * kDsMaxPasses);
-    unsigned long long* gta = (unsigned long long*)take(sizeof(uint64_t) * kRadixDigits * (size_t)kDsMaxGroups);
-    uint32_t* tot = (uint32_t*)take(sizeof(uint32_t) * kRadixDigits * kDsMaxPasses + sizeof(uint64_t) * kRadixDigits);
     if (ds) {
         *ds = DepthSortArgs{};
         ds->key0 = k0;
         ds->keys[0] = k1; ds->keys[1] = k2;
         ds->vals[0] = v1; ds->vals[1] = v2;
-        ds->st_cnt = stc; ds->st_area = sta; ds->gt_cnt = gtc; ds->gt_area = gta;
-        ds->tot = tot; ds->atot = (unsigned long long*)(tot + kRadixDigits * kDsMaxPasses);
+        ds->st_cnt = stc; ds->gt_cnt = gtc;
         ds->P = P; ds->key_base = 0u;
         ds->counters = ctr;
     }

@@ -25,12 +25,11 @@
 //            are the sums of all group totals), then writes the reordered
 //            keys in coalesced runs.  One grid barrier between passes.  (A
 //            range longer than one tile is counted by a separate sweep.)
-//   last     the same, plus the item scan fused in: the first pair slot of
-//            a particle, E = exclusive prefix of the rect areas in sorted
-//            order, is the digit's area base (the area totals of the smaller
-//            digits + the earlier CTAs' published area sums of this digit) +
-//            a segmented block scan of the reordered tile; the item records,
-//            the binning chunk starts and the slot count follow from E.
+//   last     the same, writing the item records (particle, packed rect) of
+//            the depth-ordered visible particles for the binning (bin.cu),
+//            and per CTA: the pair slots (sum of rect areas) and the items
+//            covering each band row (a row difference array in shared memory)
+//            are added to SLOTS and row_count.
 // 3 grid barriers for 3 passes (was 11).  Hand-written; no CUB.
 #include <cooperative_groups.h>
 
@@ -47,49 +46,33 @@ constexpr int kDsWarps = kDsThreads / 32;
 constexpr int kDsItems = 8;
 constexpr int kDsTile = kDsThreads * kDsItems;  // 8192 keys
 constexpr uint32_t kInvalidKey = 0xffffffffu;
-constexpr uint64_t kItemCost = kBinItemCost;
 constexpr int kDsDigits = kRadixDigits;  // 9-bit digits
 constexpr int kDsBits = 9;
 constexpr uint32_t kCntFlag = 0x80000000u;            // published count word
-constexpr unsigned long long kAreaFlag = 1ull << 63;  // published area word
 
 struct DsSmem {
     uint32_t whist[kDsWarps][kDsDigits];  // per-warp digit counts -> offsets; last pass: the tile's rects
     uint32_t keys[kDsTile];
     uint32_t vals[kDsTile];
-    uint32_t xs[kDsTile + 1];            // last pass: exclusive block scan of the tile's areas
     uint32_t base[kDsDigits];            // running global position of each digit
     uint32_t local[kDsDigits];           // tile-local exclusive digit offsets
     uint32_t cnt[kDsDigits];             // tile (or range) digit counts
-    unsigned long long abase[kDsDigits]; // last pass: running area base of each digit
-    unsigned long long acnt[kDsDigits];  // last pass: range area sums per digit
-    unsigned long long atot[kDsDigits];  // last pass: global area totals per digit
+    int rowd[kMaxBandRows + 1];          // last pass: row difference counts of the CTA's items
+    unsigned long long area;             // last pass: the CTA's pair slots
     uint32_t warp[kDsWarps + 1];
-    unsigned long long warp64[kDsWarps + 1];
 };
 
 __device__ __forceinline__ uint32_t ds_digit(uint32_t key, uint32_t kmin, int shift) {
     return ((key - kmin) >> shift) & (kDsDigits - 1);
 }
 __device__ __forceinline__ int64_t range_lo(int64_t n, int c, int G) { return n * c / G; }
-__device__ __forceinline__ uint32_t rect_area(ushort4 r) {
-    return (uint32_t)(r.z - r.x) * (uint32_t)(r.w - r.y);
-}
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
     uint32_t v;
     asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
-__device__ __forceinline__ unsigned long long ld_volatile(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.volatile.global.u64 %0, [%1];" : "=l"(v) : "l"(p));
-    return v;
-}
 __device__ __forceinline__ void st_volatile(uint32_t* p, uint32_t v) {
     asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_volatile(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.volatile.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
 // Exclusive scan of v over the first 512 threads (16 warps); returns the
@@ -123,114 +106,74 @@ __device__ __forceinline__ T scan512(T v, T* s_warp, T* total) {
     return ex;
 }
 
-// This CTA's digit counts (and, in the last pass, rect-area sums) of its range
-// of a pass input (pass >= 1: V visible keys with particle ids).
-__device__ void ds_range_hist(const DepthSortArgs& a, DsSmem& sm, const uint32_t* kin, const uint32_t* vin,
-                              int64_t r0, int64_t r1, int shift, bool last, bool drop = false) {
+// This CTA's digit counts of its range of a pass input.
+__device__ void ds_range_hist(const DepthSortArgs& a, DsSmem& sm, const uint32_t* kin, int64_t r0, int64_t r1,
+                              int shift, bool drop) {
     const int tid = threadIdx.x;
-    uint32_t* apart = sm.local;  // u32 area partials of one 8192-key tile (< 2^29: areas <= 2^16)
-    if (tid < kDsDigits) { sm.cnt[tid] = 0; sm.acnt[tid] = 0; apart[tid] = 0; }
+    if (tid < kDsDigits) sm.cnt[tid] = 0;
     __syncthreads();
     for (int64_t t0 = r0; t0 < r1; t0 += kDsTile) {
-        uint32_t k[kDsItems], v[kDsItems];
+        uint32_t k[kDsItems];
 #pragma unroll
         for (int j = 0; j < kDsItems; ++j) {
             const int64_t idx = t0 + j * kDsThreads + tid;
             k[j] = idx < r1 ? __ldcg(kin + idx) : kInvalidKey;
-            v[j] = (last && idx < r1) ? (vin ? __ldcg(vin + idx) : (uint32_t)idx) : 0u;
-        }
-        uint32_t ar[kDsItems];
-        if (last) {
-#pragma unroll
-            for (int j = 0; j < kDsItems; ++j)
-                ar[j] = t0 + j * kDsThreads + tid < r1 && !(drop && k[j] == kInvalidKey) ? rect_area(__ldg(a.rect + v[j])) : 0u;
         }
 #pragma unroll
-        for (int j = 0; j < kDsItems; ++j) {
-            if (t0 + j * kDsThreads + tid < r1 && !(drop && k[j] == kInvalidKey)) {
-                const uint32_t d = ds_digit(k[j], a.key_base, shift);
-                atomicAdd(&sm.cnt[d], 1u);
-                if (last) atomicAdd(&apart[d], ar[j]);
-            }
-        }
-        if (last) {
-            __syncthreads();
-            if (tid < kDsDigits) { sm.acnt[tid] += apart[tid]; apart[tid] = 0; }
-        }
+        for (int j = 0; j < kDsItems; ++j)
+            if (t0 + j * kDsThreads + tid < r1 && !(drop && k[j] == kInvalidKey))
+                atomicAdd(&sm.cnt[ds_digit(k[j], a.key_base, shift)], 1u);
     }
     __syncthreads();
 }
 
-// Publishes this CTA's counts (and area sums) of pass p, then finds the sums
-// over the CTAs before it without a grid barrier, in two levels of groups of
-// kDsGroup CTAs: the published words of the earlier CTAs of its group, plus the
+// Publishes this CTA's digit counts of pass p, then finds the sums over the
+// CTAs before it without a grid barrier, in two levels of groups of kDsGroup
+// CTAs: the published words of the earlier CTAs of its group, plus the
 // published totals of the earlier groups (each written by its group's last CTA
 // after its own in-group sum) -- three dependent rounds of loads whatever c is.
-// Leaves in sm.base / sm.abase the CTA's first position / area base per digit.
+// Leaves in sm.base the CTA's first position per digit.
 constexpr int kDsGroup = 16;
 // Sum of the n flagged words base[0], base[stride], ... (spinning until each is
 // published), U loads in flight.
-template <typename T, T FLAG, int U>
-__device__ __forceinline__ T ds_sum_published(const T* base, size_t stride, int n) {
-    T s = 0;
+template <int U>
+__device__ __forceinline__ uint32_t ds_sum_published(const uint32_t* base, size_t stride, int n) {
+    uint32_t s = 0;
     for (int j0 = 0; j0 < n; j0 += U) {
-        T v[U];
+        uint32_t v[U];
 #pragma unroll
-        for (int j = 0; j < U; ++j) v[j] = j0 + j < n ? ld_volatile(base + (j0 + j) * stride) : FLAG;
+        for (int j = 0; j < U; ++j) v[j] = j0 + j < n ? ld_volatile(base + (j0 + j) * stride) : kCntFlag;
 #pragma unroll
         for (int j = 0; j < U; ++j) {
-            while (!(v[j] & FLAG)) v[j] = ld_volatile(base + (j0 + j) * stride);
-            s += v[j] & ~FLAG;
+            while (!(v[j] & kCntFlag)) v[j] = ld_volatile(base + (j0 + j) * stride);
+            s += v[j] & ~kCntFlag;
         }
     }
     return s;
 }
 
-__device__ void ds_prefix(const DepthSortArgs& a, DsSmem& sm, int p, bool last, bool publish) {
+__device__ void ds_prefix(const DepthSortArgs& a, DsSmem& sm, int p, bool publish) {
     const int c = blockIdx.x, G = gridDim.x, tid = threadIdx.x;
     const int g = c / kDsGroup, first = g * kDsGroup, glast = min(first + kDsGroup, G) - 1;
     uint32_t* stc = a.st_cnt + ((size_t)p * kDsMaxGrid) * kDsDigits;
     uint32_t* gtc = a.gt_cnt + ((size_t)p * kDsMaxGroups) * kDsDigits;
-    if (publish && tid < kDsDigits) {
-        if (last) st_volatile(a.st_area + (size_t)c * kDsDigits + tid, kAreaFlag | sm.acnt[tid]);
-        st_volatile(stc + (size_t)c * kDsDigits + tid, kCntFlag | sm.cnt[tid]);
-    }
-    // threads 0..511: the counts of digit tid; threads 512..1023: the area sums (last
-    // pass).  The digit totals are the sums of ALL group totals (every CTA has then
-    // published: the pass's implicit barrier).
-    const int d = tid & (kDsDigits - 1);
+    if (publish && tid < kDsDigits) st_volatile(stc + (size_t)c * kDsDigits + tid, kCntFlag | sm.cnt[tid]);
+    // the digit totals are the sums of ALL group totals (every CTA has then published:
+    // the pass's implicit barrier)
     const int ng = (G + kDsGroup - 1) / kDsGroup;
     uint32_t tot = 0;
-    unsigned long long atot = 0;
     if (tid < kDsDigits) {
-        const uint32_t in = ds_sum_published<uint32_t, kCntFlag, kDsGroup - 1>(stc + (size_t)first * kDsDigits + d,
-                                                                               kDsDigits, c - first);
+        const int d = tid;
+        const uint32_t in = ds_sum_published<kDsGroup - 1>(stc + (size_t)first * kDsDigits + d, kDsDigits, c - first);
         if (c == glast) st_volatile(gtc + (size_t)g * kDsDigits + d, kCntFlag | (in + sm.cnt[d]));
-        const uint32_t out = ds_sum_published<uint32_t, kCntFlag, 16>(gtc + d, kDsDigits, g);
-        tot = out + ds_sum_published<uint32_t, kCntFlag, 16>(gtc + (size_t)g * kDsDigits + d, kDsDigits, ng - g);
+        const uint32_t out = ds_sum_published<16>(gtc + d, kDsDigits, g);
+        tot = out + ds_sum_published<16>(gtc + (size_t)g * kDsDigits + d, kDsDigits, ng - g);
         sm.base[d] = in + out;
-    } else if (last) {
-        const unsigned long long in = ds_sum_published<unsigned long long, kAreaFlag, 8>(
-            a.st_area + (size_t)first * kDsDigits + d, kDsDigits, c - first);
-        if (c == glast) st_volatile(a.gt_area + (size_t)g * kDsDigits + d, kAreaFlag | (in + sm.acnt[d]));
-        const unsigned long long out =
-            ds_sum_published<unsigned long long, kAreaFlag, 8>(a.gt_area + d, kDsDigits, g);
-        atot = out + ds_sum_published<unsigned long long, kAreaFlag, 8>(a.gt_area + (size_t)g * kDsDigits + d,
-                                                                         kDsDigits, ng - g);
-        sm.abase[d] = in + out;
     }
-    if (last && tid >= kDsDigits) sm.atot[d] = atot;
     __syncthreads();
     // + the totals of the smaller digits
-    {
-        const uint32_t ex = scan512<uint32_t>(tot, sm.warp, nullptr);
-        if (tid < kDsDigits) sm.base[tid] += ex;
-    }
-    if (last) {
-        const unsigned long long t = tid < kDsDigits ? sm.atot[tid] : 0ull;
-        const unsigned long long ex = scan512<unsigned long long>(t, sm.warp64, nullptr);
-        if (tid < kDsDigits) sm.abase[tid] += ex;
-    }
+    const uint32_t ex = scan512<uint32_t>(tot, sm.warp, nullptr);
+    if (tid < kDsDigits) sm.base[tid] += ex;
     __syncthreads();
 }
 
@@ -313,59 +256,38 @@ __device__ uint32_t ds_tile_rank(DsSmem& sm, const uint32_t* kin, const uint32_t
 }
 
 // Last pass: the rect of every reordered key staged in shared memory (over the
-// free rank histograms) and sm.xs = the exclusive scan of their areas over the
-// tile (xs[nvalid] = the total); sm.acnt (if tile_sums) = the digit area sums.
-__device__ void ds_tile_areas(const DepthSortArgs& a, DsSmem& sm, uint32_t nvalid, bool tile_sums) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// free rank histograms); the tile's rect areas and row coverage accumulate into
+// sm.area and sm.rowd.
+__device__ void ds_tile_rects(const DepthSortArgs& a, DsSmem& sm, uint32_t nvalid) {
+    const int tid = threadIdx.x;
     uint2* rs = reinterpret_cast<uint2*>(&sm.whist[0][0]);
-    // thread tid owns the positions [8 tid, 8 tid + 8)
-    const int s0 = tid * kDsItems;
-    uint32_t ar[kDsItems], sum = 0;
+    const int s0 = tid * kDsItems;  // thread tid owns the positions [8 tid, 8 tid + 8)
     uint2 rc[kDsItems];
 #pragma unroll
     for (int j = 0; j < kDsItems; ++j)
         rc[j] = s0 + j < (int)nvalid ? __ldg(reinterpret_cast<const uint2*>(a.rect) + sm.vals[s0 + j]) : make_uint2(0, 0);
+    unsigned long long ar = 0;
 #pragma unroll
     for (int j = 0; j < kDsItems; ++j) {
-        rs[s0 + j] = rc[j];
-        ar[j] = ((rc[j].y & 0xffffu) - (rc[j].x & 0xffffu)) * ((rc[j].y >> 16) - (rc[j].x >> 16));
-        sum += ar[j];
-    }
-    uint32_t incl = sum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += nn;
-    }
-    if (lane == 31) sm.warp[warp] = incl;
-    __syncthreads();
-    if (warp == 0) {
-        const uint32_t wv = sm.warp[lane];
-        uint32_t wi = wv;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t nn = __shfl_up_sync(0xffffffffu, wi, o);
-            if (lane >= o) wi += nn;
+        if (s0 + j < (int)nvalid) {
+            rs[s0 + j] = rc[j];
+            const uint32_t y0 = rc[j].x >> 16, y1 = rc[j].y >> 16;
+            ar += (unsigned long long)((rc[j].y & 0xffffu) - (rc[j].x & 0xffffu)) * (y1 - y0);
+            atomicAdd(&sm.rowd[y0], 1);
+            atomicSub(&sm.rowd[y1], 1);
         }
-        sm.warp[lane] = wi - wv;
     }
-    __syncthreads();
-    uint32_t x = sm.warp[warp] + incl - sum;
 #pragma unroll
-    for (int j = 0; j < kDsItems; ++j) {
-        if (s0 + j <= (int)nvalid) sm.xs[s0 + j] = x;
-        x += ar[j];
-    }
-    if (tid == kDsThreads - 1) sm.xs[kDsTile] = x;   // (a full tile: nvalid = kDsTile)
+    for (int o = 16; o > 0; o >>= 1) ar += __shfl_xor_sync(0xffffffffu, ar, o);
+    if ((tid & 31) == 0 && ar) atomicAdd(&sm.area, ar);
     __syncthreads();
-    if (tile_sums && tid < kDsDigits) sm.acnt[tid] = sm.xs[sm.local[tid] + sm.cnt[tid]] - sm.xs[sm.local[tid]];
 }
 
 // Writes the reordered tile at its sorted positions (sm.base): the next pass's
-// keys and ids, or (last pass) the sorted ids, E, the item records and the
-// binning chunk starts.  Then advances sm.base (and sm.abase) past the tile.
+// keys and ids, or (last pass) the sorted ids and the item records.  Then
+// advances sm.base past the tile.
 __device__ void ds_tile_write(const DepthSortArgs& a, DsSmem& sm, uint32_t nvalid, uint32_t* kout, uint32_t* vout,
-                              int shift, bool last, int64_t V) {
+                              int shift, bool last) {
     const int tid = threadIdx.x;
     const uint32_t kmin = a.key_base;
     if (!last) {
@@ -378,43 +300,14 @@ __device__ void ds_tile_write(const DepthSortArgs& a, DsSmem& sm, uint32_t nvali
         }
     } else {
         const uint2* rs = reinterpret_cast<const uint2*>(&sm.whist[0][0]);
-        const uint64_t S = (uint64_t)a.chunk_slots;
-        const double invS = 1.0 / (double)S;
         for (int s = tid; s < (int)nvalid; s += kDsThreads) {
             const uint32_t d = ds_digit(sm.keys[s], kmin, shift);
-            const uint32_t seg = sm.local[d];
-            const int64_t out = (int64_t)sm.base[d] + s - seg;
-            const uint64_t e = sm.abase[d] + (sm.xs[s] - sm.xs[seg]);
-            const uint64_t e1 = e + (sm.xs[s + 1] - sm.xs[s]);
+            const uint32_t out = sm.base[d] + (uint32_t)s - sm.local[d];
             const uint32_t pid = sm.vals[s];
             const uint2 rc = rs[s];
             vout[out] = pid;
-            a.E[out] = (uint32_t)e;
-            a.items[out] = make_uint4(row_class_mask(rc.x >> 16, rc.y >> 16), pid, rc.x, rc.y);
-            // binning chunk k = the items whose cost W[s] = E[s] + kItemCost s lies in
-            // [k S, (k+1) S) (bin.cu): chunk_first[k] = min{s : W[s] >= k S}; item s + 1
-            // is that minimum for every k with k S in (W[s], W[s+1]].  Item 0 opens chunk 0.
-            const uint64_t w0 = e + kItemCost * (uint64_t)out;
-            const uint64_t w1 = e1 + kItemCost * (uint64_t)(out + 1);
-            const bool ovf = (int64_t)e1 > a.capacity;
-            if (out == 0) a.chunk_first[0] = 0;
-            if (!ovf) {
-                // floor(w0 / S) + 1 from a double quotient (exact after the correction; w < 2^53)
-                uint64_t kn = (uint64_t)((double)w0 * invS);
-                if (kn * S > w0) --kn;
-                else if ((kn + 1) * S <= w0) ++kn;
-                for (++kn; kn * S <= w1; ++kn) a.chunk_first[kn] = (uint32_t)(out + 1);
-            }
-            if (out == V - 1) {  // total pair slots, capacity check, chunk count and closing entry
-                a.counters[GES_CTR_SLOTS] = e1;
-                a.counters[GES_CTR_OVERFLOW] = ovf ? 1ull : 0ull;
-                const uint64_t C = (w1 + S - 1) / S;
-                a.counters[GES_CTR_CHUNKS] = ovf ? 0ull : C;
-                if (!ovf) a.chunk_first[C] = (uint32_t)V;
-            }
+            a.items[out] = make_uint2(pid, pack_rect(rc.x & 0xffffu, rc.x >> 16, rc.y & 0xffffu, rc.y >> 16));
         }
-        __syncthreads();
-        if (tid < kDsDigits) sm.abase[tid] += sm.xs[sm.local[tid] + sm.cnt[tid]] - sm.xs[sm.local[tid]];
     }
     __syncthreads();
     if (tid < kDsDigits) sm.base[tid] += sm.cnt[tid];
@@ -422,28 +315,40 @@ __device__ void ds_tile_write(const DepthSortArgs& a, DsSmem& sm, uint32_t nvali
 }
 
 // One pass over the CTA's range [r0, r1) of the pass input.  A range of one
-// tile (V <= G x 8192 after pass 0) is ranked first and its digit counts (and
-// area sums) taken from the ranking; otherwise a counting sweep precedes.
+// tile (V <= G x 8192 after pass 0) is ranked first and its digit counts taken
+// from the ranking; otherwise a counting sweep precedes.
 __device__ void ds_pass(const DepthSortArgs& a, DsSmem& sm, const uint32_t* kin, const uint32_t* vin, uint32_t* kout,
-                        uint32_t* vout, int64_t r0, int64_t r1, int p, bool last_pass, int64_t V) {
-    // the item scan rides on the last pass of a frame's sort (a plain sort -- items == null,
-    // ges_reorder -- writes the sorted ids only)
+                        uint32_t* vout, int64_t r0, int64_t r1, int p, bool last_pass) {
+    // the item records ride on the last pass of a frame's sort (a plain sort -- items ==
+    // null, ges_reorder -- writes the sorted ids only)
     const bool last = last_pass && a.items != nullptr;
     const int shift = kDsBits * p;
     const bool drop = p == 0;  // pass 0 reads the S1 keys: drops the non-visible ones
+    const int tid = threadIdx.x;
+    if (last) {
+        for (int i = tid; i <= a.rows; i += kDsThreads) sm.rowd[i] = 0;
+        if (tid == 0) sm.area = 0;
+        __syncthreads();
+    }
     if (p > 0 && r1 - r0 <= kDsTile) {
         const uint32_t nvalid = ds_tile_rank(sm, kin, vin, r0, r1, shift, drop, a.key_base);
-        if (last) ds_tile_areas(a, sm, nvalid, true);
-        ds_prefix(a, sm, p, last, true);
-        ds_tile_write(a, sm, nvalid, kout, vout, shift, last, V);
-        return;
+        if (last) ds_tile_rects(a, sm, nvalid);
+        ds_prefix(a, sm, p, true);
+        ds_tile_write(a, sm, nvalid, kout, vout, shift, last);
+    } else {
+        if (p > 0) ds_range_hist(a, sm, kin, r0, r1, shift, false);
+        ds_prefix(a, sm, p, p > 0);   // pass 0: counted and published by phase H
+        for (int64_t t0 = r0; t0 < r1; t0 += kDsTile) {
+            const uint32_t nvalid = ds_tile_rank(sm, kin, vin, t0, r1, shift, drop, a.key_base);
+            if (last) ds_tile_rects(a, sm, nvalid);
+            ds_tile_write(a, sm, nvalid, kout, vout, shift, last);
+        }
     }
-    if (p > 0) ds_range_hist(a, sm, kin, vin, r0, r1, shift, last);
-    ds_prefix(a, sm, p, last, p > 0);   // pass 0: counted and published by phase H
-    for (int64_t t0 = r0; t0 < r1; t0 += kDsTile) {
-        const uint32_t nvalid = ds_tile_rank(sm, kin, vin, t0, r1, shift, drop, a.key_base);
-        if (last) ds_tile_areas(a, sm, nvalid, false);
-        ds_tile_write(a, sm, nvalid, kout, vout, shift, last, V);
+    if (last) {  // the CTA's pair slots and row coverage
+        uint32_t v = tid < a.rows ? (uint32_t)sm.rowd[tid] : 0u;
+        const uint32_t ex = scan512<uint32_t>(v, sm.warp, nullptr);  // (rows <= 256 < 512)
+        if (tid < a.rows && ex + v) atomicAdd(a.row_count + tid, ex + v);
+        if (tid == 0 && sm.area) atomicAdd(&a.counters[GES_CTR_SLOTS], sm.area);
     }
 }
 
@@ -473,46 +378,32 @@ __global__ void __launch_bounds__(kDsThreads, 1) depth_sort_kernel(DepthSortArgs
     // ---- phase H: zero this CTA's published words, count pass 0 of its range ----
     for (int i = tid; i < kDsMaxPasses * kDsDigits; i += kDsThreads)
         a.st_cnt[((size_t)(i / kDsDigits) * kDsMaxGrid + c) * kDsDigits + (i % kDsDigits)] = 0u;
-    if (tid < kDsDigits) { a.st_area[(size_t)c * kDsDigits + tid] = 0ull; sm.cnt[tid] = 0; sm.acnt[tid] = 0; }
+    if (tid < kDsDigits) sm.cnt[tid] = 0;
     if (c == min((c / kDsGroup + 1) * kDsGroup, G) - 1) {  // the group's last CTA: its group totals
         const int g = c / kDsGroup;
         for (int i = tid; i < kDsMaxPasses * kDsDigits; i += kDsThreads)
             a.gt_cnt[((size_t)(i / kDsDigits) * kDsMaxGroups + g) * kDsDigits + (i % kDsDigits)] = 0u;
-        if (tid < kDsDigits) a.gt_area[(size_t)g * kDsDigits + tid] = 0ull;
     }
     __syncthreads();
     {
         const int64_t h0 = range_lo(P, c, G), h1 = range_lo(P, c + 1, G);
-        if (npass == 1 && a.items) {   // pass 0 is the last: its area sums too
-            ds_range_hist(a, sm, a.key0, nullptr, h0, h1, 0, true, true);
-        } else {
-            for (int64_t t0 = h0; t0 < h1; t0 += kDsTile) {
-                uint32_t k[kDsItems];
+        for (int64_t t0 = h0; t0 < h1; t0 += kDsTile) {
+            uint32_t k[kDsItems];
 #pragma unroll
-                for (int j = 0; j < kDsItems; ++j) {
-                    const int64_t idx = t0 + j * kDsThreads + tid;
-                    k[j] = idx < h1 ? __ldcg(a.key0 + idx) : kInvalidKey;
-                }
-#pragma unroll
-                for (int j = 0; j < kDsItems; ++j)
-                    if (k[j] != kInvalidKey) atomicAdd(&sm.cnt[ds_digit(k[j], kmin, 0)], 1u);
+            for (int j = 0; j < kDsItems; ++j) {
+                const int64_t idx = t0 + j * kDsThreads + tid;
+                k[j] = idx < h1 ? __ldcg(a.key0 + idx) : kInvalidKey;
             }
-            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < kDsItems; ++j)
+                if (k[j] != kInvalidKey) atomicAdd(&sm.cnt[ds_digit(k[j], kmin, 0)], 1u);
         }
+        __syncthreads();
     }
-    if (tid < kDsDigits) {  // pass 0 of this CTA's range is counted: publish it
-        if (npass == 1 && a.items) a.st_area[(size_t)c * kDsDigits + tid] = kAreaFlag | sm.acnt[tid];
-        a.st_cnt[(size_t)c * kDsDigits + tid] = kCntFlag | sm.cnt[tid];
-    }
+    if (tid < kDsDigits) a.st_cnt[(size_t)c * kDsDigits + tid] = kCntFlag | sm.cnt[tid];  // pass 0 counted
     grid.sync();
     ds_mark(a, 1);
-    if (V == 0) {
-        if (c == 0 && tid == 0) {
-            a.counters[GES_CTR_SLOTS] = 0;
-            a.counters[GES_CTR_CHUNKS] = 0;
-        }
-        return;
-    }
+    if (V == 0) return;
     // ---- the passes ----
     const uint32_t* kin = a.key0;
     const uint32_t* vin = nullptr;
@@ -522,7 +413,7 @@ __global__ void __launch_bounds__(kDsThreads, 1) depth_sort_kernel(DepthSortArgs
         const int64_t r0 = range_lo(n, c, G), r1 = range_lo(n, c + 1, G);
         uint32_t* kout = last ? nullptr : a.keys[p & 1];
         uint32_t* vout = last ? a.sorted_vis : a.vals[p & 1];
-        ds_pass(a, sm, kin, vin, kout, vout, r0, r1, p, last, V);
+        ds_pass(a, sm, kin, vin, kout, vout, r0, r1, p, last);
         if (!last) grid.sync();
         ds_mark(a, last ? 6 : 2 + p);
         kin = kout;
