@@ -201,20 +201,49 @@ __device__ __forceinline__ void group_masks(uint32_t* sx, bool valid, int lo, in
 }
 
 // Emission of one group: the lane owning bin b = lane + 32 j writes the payloads
-// of the records in m[j] (lane order) at dst[cur[j]++].
-template <int BPL, class T, class Pay>
-__device__ __forceinline__ void emit_group(T* dst, const uint32_t (&m)[BPL], uint32_t (&cur)[BPL], Pay pay) {
+// of the records in m[j] (lane order) at dst[cur[j]++].  No warp collective per
+// trip (VOTE and SHFL issue at a fraction of the ALU rate): the trip count is the
+// warp's largest popcount (one REDUX per j), the payloads come from shared memory.
+#ifdef GES_BIN_STATS
+__device__ unsigned long long g_bin_trips[2];  // emission loop trips: [0] rows, [1] columns
+#endif
+template <int BPL, class T>
+__device__ __forceinline__ void emit_group(T* dst, const uint32_t (&m)[BPL], uint32_t (&cur)[BPL], const T* pay) {
 #pragma unroll
     for (int j = 0; j < BPL; ++j) {
         uint32_t bits = m[j];
-        while (__any_sync(0xffffffffu, bits != 0u)) {
-            const int b = bits ? __ffs(bits) - 1 : 0;
-            const T v = pay(b);
+        const int n = (int)__reduce_max_sync(0xffffffffu, (unsigned)__popc(bits));
+#ifdef GES_BIN_STATS
+        if ((threadIdx.x & 31) == 0) atomicAdd(&g_bin_trips[sizeof(T) == 4], (unsigned long long)n);
+#endif
+        for (int t = 0; t < n; ++t) {
             if (bits) {
-                dst[cur[j]++] = v;
+                dst[cur[j]++] = pay[__ffs(bits) - 1];
                 bits &= bits - 1u;
             }
         }
+    }
+}
+
+// The same into a shared-memory stage, branch-free: a lane with no record left
+// in this bin writes to the stage's spare slot stage[spare].
+template <int BPL, class T>
+__device__ __forceinline__ void emit_group_staged(T* stage, uint32_t spare, const uint32_t (&m)[BPL],
+                                                  uint32_t (&cur)[BPL], const T* pay) {
+#pragma unroll
+    for (int j = 0; j < BPL; ++j) {
+        uint32_t bits = m[j];
+        const int n = (int)__reduce_max_sync(0xffffffffu, (unsigned)__popc(bits));
+        uint32_t c = cur[j];
+#pragma unroll 2
+        for (int t = 0; t < n; ++t) {
+            const uint32_t act = bits != 0u;
+            const T v = pay[(__ffs(bits) - 1) & 31];
+            stage[act ? c : spare] = v;
+            c += act;
+            bits &= bits - 1u;
+        }
+        cur[j] = c;
     }
 }
 
@@ -236,8 +265,9 @@ __global__ void __launch_bounds__(kBinThreads) bin_rows_kernel(BinArgs a) {
     __shared__ uint32_t s_cnt[kBinWarps][NB + 1];
     __shared__ uint32_t s_msk[kBinWarps][NB + 1];
     __shared__ uint32_t s_agg[NB], s_excl[NB], s_lbase[NB + 1], s_gbase[kMaxBandRows + 1];
+    __shared__ uint2 s_pay[kBinWarps][32];
     __shared__ unsigned long long s_k;
-    extern __shared__ __align__(16) uint2 s_rstage[];  // [kRowStage]
+    extern __shared__ __align__(16) uint2 s_rstage[];  // [kRowStage + 1] (+ the spare slot)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rows = a.rows;
     if ((int64_t)a.counters[GES_CTR_SLOTS] > a.capacity) {  // the lists would not fit: nothing is binned
@@ -301,12 +331,11 @@ __global__ void __launch_bounds__(kBinThreads) bin_rows_kernel(BinArgs a) {
 #pragma unroll
     for (int g = 0; g < kRowItems; ++g) {
         uint32_t m[BPL];
-        group_masks<BPL>(s_msk[warp], (valid >> g) & 1u, y0[g], y1[g], m);
-        auto pay = [&](int b) {
-            return make_uint2(__shfl_sync(0xffffffffu, pid[g], b), __shfl_sync(0xffffffffu, xp[g], b));
-        };
-        if (staged) emit_group<BPL>(s_rstage, m, cur, pay);
-        else emit_group<BPL>(a.rowlist, m, cur, pay);
+        s_pay[warp][lane] = make_uint2(pid[g], xp[g]);
+        group_masks<BPL>(s_msk[warp], (valid >> g) & 1u, y0[g], y1[g], m);  // (syncs the warp)
+        if (staged) emit_group_staged<BPL>(s_rstage, kRowStage, m, cur, s_pay[warp]);
+        else emit_group<BPL>(a.rowlist, m, cur, s_pay[warp]);
+        __syncwarp();
     }
     __syncthreads();
     if (staged) copy_runs(s_rstage, a.rowlist, s_lbase, s_gbase, rows);
@@ -401,8 +430,9 @@ __global__ void __launch_bounds__(kBinThreads) bin_cols_kernel(BinArgs a) {
     __shared__ uint32_t s_msk[kBinWarps][NB + 1];
     __shared__ uint32_t s_rb[kMaxBandRows + 1], s_cf[kMaxBandRows + 1], s_rp[kMaxBandRows + 1];
     __shared__ uint32_t s_lbase[NB + 1], s_gbase[NB + 1];
+    __shared__ uint32_t s_pay[kBinWarps][32];
     __shared__ unsigned long long s_g;
-    extern __shared__ __align__(16) uint32_t s_cstage[];  // [kColStage]
+    extern __shared__ __align__(16) uint32_t s_cstage[];  // [kColStage + 1] (+ the spare slot)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rows = a.rows, tx = a.tiles_x;
     const bool ovf = a.counters[GES_CTR_OVERFLOW] != 0;
@@ -489,10 +519,11 @@ __global__ void __launch_bounds__(kBinThreads) bin_cols_kernel(BinArgs a) {
 #pragma unroll
         for (int g2 = 0; g2 < kColItems; ++g2) {
             uint32_t m[BPL];
-            group_masks<BPL>(s_msk[warp], (valid >> g2) & 1u, x0[g2], x1[g2], m);
-            auto pay = [&](int b) { return __shfl_sync(0xffffffffu, pid[g2], b); };
-            if (staged) emit_group<BPL>(s_cstage, m, cur, pay);
-            else emit_group<BPL>(a.list, m, cur, pay);
+            s_pay[warp][lane] = pid[g2];
+            group_masks<BPL>(s_msk[warp], (valid >> g2) & 1u, x0[g2], x1[g2], m);  // (syncs the warp)
+            if (staged) emit_group_staged<BPL>(s_cstage, kColStage, m, cur, s_pay[warp]);
+            else emit_group<BPL>(a.list, m, cur, s_pay[warp]);
+            __syncwarp();
         }
         __syncthreads();
         if (staged) copy_runs(s_cstage, a.list, s_lbase, s_gbase, tx);
@@ -512,7 +543,7 @@ static cudaError_t set_smem(K kernel, int bytes, int* done) {
 template <int BR>
 static cudaError_t launch_rows(const BinArgs& a, cudaStream_t stream) {
     static int done[kMaxDevices] = {0};
-    const int smem = kRowStage * (int)sizeof(uint2);
+    const int smem = (kRowStage + 1) * (int)sizeof(uint2);
     cudaError_t e = set_smem(bin_rows_kernel<BR>, smem, done);
     if (e != cudaSuccess) return e;
     bin_rows_kernel<BR><<<(unsigned)std::max<int64_t>(1, a.row_chunks), kBinThreads, smem, stream>>>(a);
@@ -522,7 +553,7 @@ static cudaError_t launch_rows(const BinArgs& a, cudaStream_t stream) {
 template <int BC>
 static cudaError_t launch_cols(const BinArgs& a, cudaStream_t stream) {
     static int done[kMaxDevices] = {0};
-    const int smem = kColStage * (int)sizeof(uint32_t);
+    const int smem = (kColStage + 1) * (int)sizeof(uint32_t);
     cudaError_t e = set_smem(bin_cols_kernel<BC>, smem, done);
     if (e != cudaSuccess) return e;
     bin_cols_count_kernel<BC><<<num_sms() * 4, kBinThreads, 0, stream>>>(a);
@@ -556,3 +587,9 @@ cudaError_t launch_bin(const BinArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace ges
+
+#ifdef GES_BIN_STATS
+extern "C" void ges_debug_bin_trips(unsigned long long* out) {
+    cudaMemcpyFromSymbol(out, ges::g_bin_trips, sizeof(unsigned long long) * 2);
+}
+#endif

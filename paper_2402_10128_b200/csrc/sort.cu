@@ -182,9 +182,17 @@ __device__ void ds_prefix(const DepthSortArgs& a, DsSmem& sm, int p, bool publis
 // digit (warp multisplit: one ballot per digit bit), and reorders it in shared
 // memory (sm.keys / sm.vals in digit order); sm.cnt = the tile's digit counts,
 // sm.local = their exclusive offsets.  Returns the number of valid keys.
+#if defined(GES_DS_TIMING) && GES_DS_TIMING == 3
+__device__ unsigned long long g_ds_t[8];
+#define DS_RMARK(k) do { __syncthreads(); if (blockIdx.x == 0 && threadIdx.x == 0 && shift == 9) { unsigned long long t_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_ds_t[k] = t_; } } while (0)
+#else
+#define DS_RMARK(k) do {} while (0)
+#endif
 __device__ uint32_t ds_tile_rank(DsSmem& sm, const uint32_t* kin, const uint32_t* vin, int64_t t0, int64_t r1,
                                  int shift, bool drop, uint32_t kmin) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    DS_RMARK(0);
     const uint32_t lt_mask = (1u << lane) - 1u;
     // warp-striped: item j of lane l of warp w is element t0 + w 256 + j 32 + l
     const int64_t wb = t0 + warp * (kDsItems * 32);
@@ -203,30 +211,65 @@ __device__ uint32_t ds_tile_rank(DsSmem& sm, const uint32_t* kin, const uint32_t
 #pragma unroll
     for (int j = 0; j < kDsDigits / 32; ++j) sm.whist[warp][j * 32 + lane] = 0;
     __syncwarp();
+#if defined(GES_DS_TIMING) && GES_DS_TIMING == 3
+    { uint32_t x = 0; for (int j = 0; j < kDsItems; ++j) x ^= k[j] ^ v[j]; if (x == 0x12345678u) sm.warp[0] = x; }
+    DS_RMARK(1);
+#endif
+#ifndef GES_DS_MATCH
+    // Stable ranks without MATCH or per-bit ballots (both issue far below the ALU rate):
+    // per item, rounds in which the lowest unranked lane of every digit (atomicMin on a
+    // per-warp owner slot) takes the digit's next count.  Rounds = the largest digit
+    // multiplicity among the warp's 32 keys (mostly 1-3).  The owner slots borrow
+    // sm.keys / sm.vals (free until the reorder below), 512 per warp, all ~0 between uses.
+    uint32_t* own = sm.keys + warp * kDsDigits;
+#pragma unroll
+    for (int j = 0; j < kDsDigits / 32; ++j) own[j * 32 + lane] = 0xffffffffu;
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < kDsItems; ++j) {
+        const uint32_t d = ds_digit(k[j], kmin, shift);
+        bool pending = (valid >> j) & 1u;
+        rank[j] = 0;
+        while (__any_sync(0xffffffffu, pending)) {
+            if (pending) atomicMin(&own[d], (uint32_t)lane);
+            __syncwarp();
+            const bool win = pending && own[d] == (uint32_t)lane;
+            __syncwarp();
+            if (win) {
+                const uint32_t c = sm.whist[warp][d];
+                rank[j] = c;
+                sm.whist[warp][d] = c + 1u;
+                own[d] = 0xffffffffu;
+                pending = false;
+            }
+            __syncwarp();
+        }
+    }
+#else
+    // the peers (lanes with the same digit) of all items first, then the serial
+    // per-warp counter updates
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    uint32_t peers[kDsItems];
 #pragma unroll
     for (int j = 0; j < kDsItems; ++j) {
         const bool ok = (valid >> j) & 1u;
         const uint32_t d = ds_digit(k[j], kmin, shift);
-#ifdef GES_DS_BALLOT
-        uint32_t peers = __ballot_sync(0xffffffffu, ok);
+        peers[j] = __match_any_sync(0xffffffffu, ok ? d : (uint32_t)kDsDigits);
+    }
 #pragma unroll
-        for (int b = 0; b < kDsBits; ++b) {
-            const uint32_t bit = (d >> b) & 1u;
-            const uint32_t bal = __ballot_sync(0xffffffffu, bit);
-            peers &= bit ? bal : ~bal;
-        }
-#else
-        // lanes with the same digit (invalid lanes share the out-of-range value 512)
-        const uint32_t peers = __match_any_sync(0xffffffffu, ok ? d : (uint32_t)kDsDigits);
-#endif
+    for (int j = 0; j < kDsItems; ++j) {
+        const bool ok = (valid >> j) & 1u;
+        const uint32_t d = ds_digit(k[j], kmin, shift);
         uint32_t cn = 0;
         if (ok) cn = sm.whist[warp][d];
         __syncwarp();
-        rank[j] = cn + __popc(peers & lt_mask);
-        if (ok && (peers >> lane) == 1u) sm.whist[warp][d] = cn + __popc(peers);
+        rank[j] = cn + __popc(peers[j] & lt_mask);
+        if (ok && (peers[j] >> lane) == 1u) sm.whist[warp][d] = cn + __popc(peers[j]);
         __syncwarp();
     }
+#endif
     __syncthreads();
+    DS_RMARK(2);
     // per digit: exclusive over warps, tile count, tile-local exclusive offsets
     uint32_t tc = 0;
     if (tid < kDsDigits) {
@@ -242,6 +285,7 @@ __device__ uint32_t ds_tile_rank(DsSmem& sm, const uint32_t* kin, const uint32_t
     const uint32_t loc = scan512<uint32_t>(tc, sm.warp, &nvalid);
     if (tid < kDsDigits) sm.local[tid] = loc;
     __syncthreads();
+    DS_RMARK(3);
 #pragma unroll
     for (int j = 0; j < kDsItems; ++j) {
         if ((valid >> j) & 1u) {
@@ -252,6 +296,7 @@ __device__ uint32_t ds_tile_rank(DsSmem& sm, const uint32_t* kin, const uint32_t
         }
     }
     __syncthreads();
+    DS_RMARK(4);
     return nvalid;
 }
 
@@ -422,6 +467,11 @@ __global__ void __launch_bounds__(kDsThreads, 1) depth_sort_kernel(DepthSortArgs
     }
 }
 
+#if defined(GES_DS_TIMING) && GES_DS_TIMING == 3
+}  // namespace ges
+extern "C" void ges_debug_ds_times(unsigned long long* out) { cudaMemcpyFromSymbol(out, ges::g_ds_t, 64); }
+namespace ges {
+#endif
 int depth_sort_grid() {
     static int grid[kMaxDevices] = {0};
     const int dev = current_device();
