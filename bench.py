@@ -472,9 +472,10 @@ def run_ours(args) -> None:
                        f"K6: {K6_OPS} FP32 instr x E_fwd = sum n_eval ({e_fwd})"),
         "preprocess": ("hbm", s1_bytes / (stage_ms[0] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s",
                        f"K1: 48 P + (12K + 56) V + 4 (P - V) = {s1_bytes} B"),
-        "sort": ("hbm", sort_algorithmic_bytes(P, V, int(cnt.pairs), depth_passes(frame))
+        "sort": ("hbm", sort_algorithmic_bytes(P, V, int(cnt.pairs), row_incidences(frame), depth_passes(frame))
                  / (stage_ms[1] / 1e3) / 1e9, peaks["hbm_gbs"], "GB/s",
-                 "K2-K5, bucket variant counting its own passes (depth radix over V, item scan, one list write)"),
+                 "K2-K5 counting their own passes: depth radix over V (item records in the last pass), "
+                 "row lists, column counts, tile lists (one write of the M entries)"),
         "backward_particles": ("hbm", particle_bwd_bytes(P, V, K) / (stage_ms[4] / 1e3) / 1e9,
                                peaks["hbm_gbs"], "GB/s",
                                "K8: parameters and 2-D record read for visible particles, every gradient written"),
@@ -548,8 +549,8 @@ K7_OPS = 45
 # useful work only: FP32 instructions the method needs per composited (pixel, entry)
 FWD_OPS = 20
 BWD_OPS = 38
-# kernels per step: preprocess, depth sort + item scan (one cooperative kernel), binning (count,
-# column scan + ranges, scatter), fwd, bwd tiles, particle bwd (+ the frame's zero-region memset)
+# kernels per step: preprocess, depth sort + item records (one cooperative kernel), binning (rows,
+# column counts, columns + ranges), fwd, bwd tiles, particle bwd (+ the frame's zero-region memset)
 LAUNCHES_PER_STEP = 1 + 1 + 3 + 1 + 1 + 1
 
 
@@ -597,6 +598,12 @@ def preprocess_bytes(P, V, deg):
     return P * (4 * 12 + 94) + V * 4 * 3 * K
 
 
+def row_incidences(frame):
+    """Row-list entries of the frame: sum over visible particles of their rect heights."""
+    import torch
+    return int(frame.view("row_count", torch.int32, frame.c.band_rows).sum().item())
+
+
 def depth_passes(frame):
     """Passes the depth sort ran: 9-bit digits over bits(max visible key - bits(near_z))."""
     import torch
@@ -605,16 +612,16 @@ def depth_passes(frame):
     return max(1, -(-span.bit_length() // 9))
 
 
-def sort_algorithmic_bytes(P, V, M, passes):
-    # depth sort: pass 0 reads the P keys twice (histogram, scatter); every later pass reads V keys
-    # (histogram) and V (key, id) (scatter); all but the last write V (key, id), the last writes
-    # the V ids and 16-B item records (gathering the 8-B rects)
-    depth = P * 4 * 2 + (passes - 1) * V * (4 + 8) + (passes - 1) * V * 8 + V * (4 + 16 + 8)
-    items = V * 16 * 2 + V * 8                 # item scan: records read twice, E + slot field written
-    # binning: count and scatter read the item records; the scatter writes the M list entries;
-    # the per-(chunk, tile) table and the ranges are O(chunks x tiles), small
-    binning = V * 16 * 2 + M * 4
-    return depth + items + binning
+def sort_algorithmic_bytes(P, V, M, I, passes):
+    # depth sort: phase H and pass 0 read the P keys (the ids are the indices); pass 0 writes V
+    # (key, id); every middle pass reads and writes V (key, id); the last reads V (key, id) and writes
+    # the V ids and 8-B item records, gathering the 8-B rects
+    depth = P * 4 * 2 + V * 8 + max(0, passes - 2) * V * 16 + (V * 8 if passes > 1 else 0) + V * (4 + 8 + 8)
+    # binning: the rows read the V item records and write the I row-list entries (8 B; I = sum of
+    # rect heights); the column counts and the column binning read them; the M list entries are
+    # written once.  Row counts, look-back words, tile counts and ranges are O(rows x tiles), small
+    binning = V * 8 + I * 8 * 3 + M * 4
+    return depth + binning
 
 
 def particle_bwd_bytes(P, V, K):

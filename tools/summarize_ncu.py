@@ -15,8 +15,8 @@ import sys
 
 
 # launches of each kernel in one bench step
-STEP = {"preprocess_tma_kernel<16>": 1, "depth_sort_kernel": 1, "bin_count_kernel": 1, "bin_colscan_kernel": 1,
-        "bin_scatter_kernel": 1, "render_fwd_kernel<2, 0, 0>": 1, "render_bwd_kernel<4, 0>": 1,
+STEP = {"preprocess_tma_kernel<16>": 1, "depth_sort_kernel": 1, "bin_rows_kernel<2>": 1, "bin_cols_count_kernel<3>": 1,
+        "bin_cols_kernel<3>": 1, "render_fwd_kernel<2, 0, 0>": 1, "render_bwd_kernel<4, 0>": 1,
         "particle_bwd_tma_kernel<16>": 1}
 
 
