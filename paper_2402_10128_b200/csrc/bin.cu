@@ -104,13 +104,13 @@ __device__ __forceinline__ int row_of(const uint32_t* first, int rows, uint32_t 
 // this chunk's vector; out (shared) = the sum over chunks < k.  Chunks are
 // claimed in order (tickets), so every awaited word has a running or finished
 // writer.
-__device__ void chunk_prefix(uint32_t* st, uint32_t* gt, int64_t k, int64_t nk, int n, const uint32_t* agg,
-                             uint32_t* out) {
+__device__ __forceinline__ void chunk_publish(uint32_t* st, int64_t k, int n, const uint32_t* agg) {
+    for (int i = threadIdx.x; i < n; i += kBinThreads) lb_store(st + k * n + i, kPub | agg[i]);
+}
+__device__ void chunk_wait(uint32_t* st, uint32_t* gt, int64_t k, int64_t nk, int n, const uint32_t* agg,
+                           uint32_t* out) {
     const int tid = threadIdx.x;
-    for (int i = tid; i < n; i += kBinThreads) {
-        lb_store(st + k * n + i, kPub | agg[i]);
-        out[i] = 0;
-    }
+    for (int i = tid; i < n; i += kBinThreads) out[i] = 0;
     __syncthreads();
     const int64_t first = k / kGroup * kGroup, glast = (first + kGroup < nk ? first + kGroup : nk) - 1;
     const int m = (int)(k - first);
@@ -127,6 +127,11 @@ __device__ void chunk_prefix(uint32_t* st, uint32_t* gt, int64_t k, int64_t nk, 
         atomicAdd(&out[i], lb_wait(gt + (int64_t)gg * kGroup * n + i));
     }
     __syncthreads();
+}
+__device__ void chunk_prefix(uint32_t* st, uint32_t* gt, int64_t k, int64_t nk, int n, const uint32_t* agg,
+                             uint32_t* out) {
+    chunk_publish(st, k, n, agg);
+    chunk_wait(st, gt, k, nk, n, agg, out);
 }
 
 // Per-warp bin counts of this lane's records (difference array in shared memory,
@@ -311,17 +316,25 @@ __global__ void __launch_bounds__(kBinThreads) bin_rows_kernel(BinArgs a) {
         s_agg[tid] = run;
     }
     __syncthreads();
-    chunk_prefix(a.lb_rows, a.lb_rows + a.row_chunks * rows, k, nk, rows, s_agg, s_excl);
-    if (warp == 0) {  // global first slot of this chunk's entries in each row
-        warp_excl<kScanRows>([&](int i) { return a.row_count[i]; }, s_gbase, rows);
-        __syncwarp();
-        for (int i = lane; i < rows; i += 32) s_gbase[i] += s_excl[i];
-    } else if (warp == 1) {  // staging offsets
-        warp_excl<BPL>([&](int i) { return s_agg[i]; }, s_lbase, rows);
-    }
+    // publish this chunk's row counts now; the prefix over the earlier chunks is awaited only
+    // after the emission into the stage (which needs the local offsets alone)
+    uint32_t* lbw = a.lb_rows;
+    uint32_t* lbg = a.lb_rows + a.row_chunks * rows;
+    chunk_publish(lbw, k, rows, s_agg);
+    if (warp == 1) warp_excl<BPL>([&](int i) { return s_agg[i]; }, s_lbase, rows);  // staging offsets
     __syncthreads();
     const uint32_t total = s_lbase[rows];
     const bool staged = total <= (uint32_t)kRowStage;
+    auto global_base = [&]() {  // global first slot of this chunk's entries in each row
+        chunk_wait(lbw, lbg, k, nk, rows, s_agg, s_excl);
+        if (warp == 0) {
+            warp_excl<kScanRows>([&](int i) { return a.row_count[i]; }, s_gbase, rows);
+            __syncwarp();
+            for (int i = lane; i < rows; i += 32) s_gbase[i] += s_excl[i];
+        }
+        __syncthreads();
+    };
+    if (!staged) global_base();
     uint32_t cur[BPL];
 #pragma unroll
     for (int j = 0; j < BPL; ++j) {
@@ -337,8 +350,10 @@ __global__ void __launch_bounds__(kBinThreads) bin_rows_kernel(BinArgs a) {
         else emit_group<BPL>(a.rowlist, m, cur, s_pay[warp]);
         __syncwarp();
     }
-    __syncthreads();
-    if (staged) copy_runs(s_rstage, a.rowlist, s_lbase, s_gbase, rows);
+    if (staged) {
+        global_base();  // (its barriers also order the emission before the copy)
+        copy_runs(s_rstage, a.rowlist, s_lbase, s_gbase, rows);
+    }
 }
 
 // Row scans shared by the column kernels: s_rb = first row-list entry of each
