@@ -888,7 +888,8 @@ def time_view_batch(G, cfg, dev, stream, steps, rank, world):
     return {"config": gi.CONFIG_NAMES[cfg], "views_per_iter": 8, "views_per_rank": len(mine), "ms_per_iter": ms,
             "ms_per_iter_direct_launches": ms_direct, "launch": "CUDA graph" if ms is ms_graph else "direct",
             "iters_per_s": 1e3 / ms, "value": 8 * W * H / (ms / 1e3) / 1e6, "unit": "Mpixel-frames/s (fwd+bwd)",
-            "scaling": "strong", "ms_without_collectives": ms_local, "exposed_comm_ms": ms - ms_local,
+            "scaling": "strong", "ms_without_collectives": ms_local if world > 1 else ms,
+            "exposed_comm_ms": (ms_direct - ms_local) if world > 1 else 0.0,  # (both direct launches at N > 1)
             "optimizer": "Adam (all LRs 0); N > 1: ZeRO-1 -- reduce-scatter of the gradients, each rank's 1/N range "
                          "updated, all-gather of the parameters (dist.ShardedAdam)",
             "gradient_bytes": 4 * n_el}
