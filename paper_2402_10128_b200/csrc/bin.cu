@@ -36,8 +36,14 @@ constexpr int kBinThreads = 512;
 constexpr int kBinWarps = kBinThreads / 32;
 constexpr int kRowItems = kRowChunk / kBinThreads;  // items per lane (4)
 constexpr int kColItems = kColChunk / kBinThreads;  // entries per lane (8)
-constexpr int kRowStage = 8192;   // staged row-list entries (8 B) per chunk
-constexpr int kColStage = 16384;  // staged list entries (4 B) per chunk
+#ifndef GES_ROW_STAGE
+#define GES_ROW_STAGE 8192
+#endif
+#ifndef GES_COL_STAGE
+#define GES_COL_STAGE 16384
+#endif
+constexpr int kRowStage = GES_ROW_STAGE;  // staged row-list entries (8 B) per chunk
+constexpr int kColStage = GES_COL_STAGE;  // staged list entries (4 B) per chunk
 constexpr uint32_t kPub = 0x80000000u;  // published word flag (values < 2^31)
 constexpr int kGroup = 16;
 constexpr int kScanRows = kMaxBandRows / 32;  // rows per lane of a one-warp row scan
@@ -211,6 +217,7 @@ __device__ __forceinline__ void group_masks(uint32_t* sx, bool valid, int lo, in
 // warp's largest popcount (one REDUX per j), the payloads come from shared memory.
 #ifdef GES_BIN_STATS
 __device__ unsigned long long g_bin_trips[2];  // emission loop trips: [0] rows, [1] columns
+__device__ unsigned long long g_bin_direct[4]; // chunks: [0] rows direct, [1] rows, [2] columns direct, [3] columns
 #endif
 template <int BPL, class T>
 __device__ __forceinline__ void emit_group(T* dst, const uint32_t (&m)[BPL], uint32_t (&cur)[BPL], const T* pay) {
@@ -325,6 +332,9 @@ __global__ void __launch_bounds__(kBinThreads) bin_rows_kernel(BinArgs a) {
     __syncthreads();
     const uint32_t total = s_lbase[rows];
     const bool staged = total <= (uint32_t)kRowStage;
+#ifdef GES_BIN_STATS
+    if (tid == 0) { atomicAdd(&g_bin_direct[0], staged ? 0ull : 1ull); atomicAdd(&g_bin_direct[1], 1ull); }
+#endif
     auto global_base = [&]() {  // global first slot of this chunk's entries in each row
         chunk_wait(lbw, lbg, k, nk, rows, s_agg, s_excl);
         if (warp == 0) {
@@ -525,6 +535,9 @@ __global__ void __launch_bounds__(kBinThreads) bin_cols_kernel(BinArgs a) {
         __syncthreads();
         const uint32_t total = s_lbase[tx];
         const bool staged = total <= (uint32_t)kColStage;
+#ifdef GES_BIN_STATS
+        if (tid == 0) { atomicAdd(&g_bin_direct[2], staged ? 0ull : 1ull); atomicAdd(&g_bin_direct[3], 1ull); }
+#endif
         uint32_t cur[BPL];
 #pragma unroll
         for (int j = 0; j < BPL; ++j) {
@@ -606,5 +619,6 @@ cudaError_t launch_bin(const BinArgs& a, cudaStream_t stream) {
 #ifdef GES_BIN_STATS
 extern "C" void ges_debug_bin_trips(unsigned long long* out) {
     cudaMemcpyFromSymbol(out, ges::g_bin_trips, sizeof(unsigned long long) * 2);
+    cudaMemcpyFromSymbol(out + 2, ges::g_bin_direct, sizeof(unsigned long long) * 4);
 }
 #endif

@@ -84,7 +84,10 @@ cudaError_t launch_reorder(const float* const* in, float* const* out, int n_buff
 
 // --- row-then-column binning (bin.cu) ----------------------------------------
 constexpr int kRowChunk = 2048;       // items per row-binning CTA
-constexpr int kColChunk = 4096;       // row-list entries per column-binning CTA
+#ifndef GES_COL_CHUNK
+#define GES_COL_CHUNK 3072
+#endif
+constexpr int kColChunk = GES_COL_CHUNK;  // row-list entries per column-binning CTA
 struct BinArgs {
     const uint2* items;               // [V] depth-ordered item records (sort.cu)
     const uint32_t* row_count;        // [rows] items covering each row (sort.cu)

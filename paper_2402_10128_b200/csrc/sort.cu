@@ -127,6 +127,14 @@ __device__ void ds_range_hist(const DepthSortArgs& a, DsSmem& sm, const uint32_t
     __syncthreads();
 }
 
+#if defined(GES_DS_TIMING) && GES_DS_TIMING == 3
+__device__ unsigned long long g_ds_t[8];
+__device__ long long g_ds_q[6];
+#define DS_RMARK(k) do { __syncthreads(); if (blockIdx.x == 0 && threadIdx.x == 0 && shift == 9) { unsigned long long t_; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_ds_t[k] = t_; } } while (0)
+#else
+#define DS_RMARK(k) do {} while (0)
+#endif
 // Publishes this CTA's digit counts of pass p, then finds the sums over the
 // CTAs before it without a grid barrier, in two levels of groups of kDsGroup
 // CTAs: the published words of the earlier CTAs of its group, plus the
@@ -162,12 +170,27 @@ __device__ void ds_prefix(const DepthSortArgs& a, DsSmem& sm, int p, bool publis
     // the pass's implicit barrier)
     const int ng = (G + kDsGroup - 1) / kDsGroup;
     uint32_t tot = 0;
+#if defined(GES_DS_TIMING) && GES_DS_TIMING == 3
+    long long q0 = clock64(), q1 = 0, q2 = 0, q3 = 0;
+#endif
     if (tid < kDsDigits) {
         const int d = tid;
         const uint32_t in = ds_sum_published<kDsGroup - 1>(stc + (size_t)first * kDsDigits + d, kDsDigits, c - first);
-        if (c == glast) st_volatile(gtc + (size_t)g * kDsDigits + d, kCntFlag | (in + sm.cnt[d]));
+        if (c == glast)  // + this CTA's own published count (sm.cnt may hold a tile's by now)
+            st_volatile(gtc + (size_t)g * kDsDigits + d,
+                        kCntFlag | (in + (ld_volatile(stc + (size_t)c * kDsDigits + d) & ~kCntFlag)));
+#if defined(GES_DS_TIMING) && GES_DS_TIMING == 3
+        q1 = clock64();
+#endif
         const uint32_t out = ds_sum_published<16>(gtc + d, kDsDigits, g);
+#if defined(GES_DS_TIMING) && GES_DS_TIMING == 3
+        q2 = clock64();
+#endif
         tot = out + ds_sum_published<16>(gtc + (size_t)g * kDsDigits + d, kDsDigits, ng - g);
+#if defined(GES_DS_TIMING) && GES_DS_TIMING == 3
+        q3 = clock64();
+        if (p == 1 && tid == 0 && (c == 0 || c == G - 1)) { g_ds_q[(c ? 3 : 0) + 0] = q1 - q0; g_ds_q[(c ? 3 : 0) + 1] = q2 - q1; g_ds_q[(c ? 3 : 0) + 2] = q3 - q2; }
+#endif
         sm.base[d] = in + out;
     }
     __syncthreads();
@@ -182,15 +205,8 @@ __device__ void ds_prefix(const DepthSortArgs& a, DsSmem& sm, int p, bool publis
 // digit (warp multisplit: one ballot per digit bit), and reorders it in shared
 // memory (sm.keys / sm.vals in digit order); sm.cnt = the tile's digit counts,
 // sm.local = their exclusive offsets.  Returns the number of valid keys.
-#if defined(GES_DS_TIMING) && GES_DS_TIMING == 3
-__device__ unsigned long long g_ds_t[8];
-#define DS_RMARK(k) do { __syncthreads(); if (blockIdx.x == 0 && threadIdx.x == 0 && shift == 9) { unsigned long long t_; \
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_ds_t[k] = t_; } } while (0)
-#else
-#define DS_RMARK(k) do {} while (0)
-#endif
 __device__ uint32_t ds_tile_rank(DsSmem& sm, const uint32_t* kin, const uint32_t* vin, int64_t t0, int64_t r1,
-                                 int shift, bool drop, uint32_t kmin) {
+                                 int shift, bool drop, uint32_t kmin, uint32_t* publish = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     DS_RMARK(0);
     const uint32_t lt_mask = (1u << lane) - 1u;
@@ -207,6 +223,16 @@ __device__ uint32_t ds_tile_rank(DsSmem& sm, const uint32_t* kin, const uint32_t
         const int64_t idx = wb + j * 32 + lane;
         v[j] = vin ? (idx < r1 ? __ldcg(vin + idx) : 0u) : (uint32_t)idx;
         if (idx < r1 && !(drop && k[j] == kInvalidKey)) valid |= 1u << j;
+    }
+    if (publish) {  // the tile is the CTA's whole range: publish its digit counts before ranking,
+                    // so that the pass prefix's loads find the other CTAs' words already set
+        if (tid < kDsDigits) sm.cnt[tid] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kDsItems; ++j)
+            if ((valid >> j) & 1u) atomicAdd(&sm.cnt[ds_digit(k[j], kmin, shift)], 1u);
+        __syncthreads();
+        if (tid < kDsDigits) st_volatile(publish + tid, kCntFlag | sm.cnt[tid]);
     }
 #pragma unroll
     for (int j = 0; j < kDsDigits / 32; ++j) sm.whist[warp][j * 32 + lane] = 0;
@@ -376,18 +402,22 @@ __device__ void ds_pass(const DepthSortArgs& a, DsSmem& sm, const uint32_t* kin,
         __syncthreads();
     }
     if (p > 0 && r1 - r0 <= kDsTile) {
-        const uint32_t nvalid = ds_tile_rank(sm, kin, vin, r0, r1, shift, drop, a.key_base);
+        uint32_t* pub = a.st_cnt + ((size_t)p * kDsMaxGrid + blockIdx.x) * kDsDigits;
+        const uint32_t nvalid = ds_tile_rank(sm, kin, vin, r0, r1, shift, drop, a.key_base, pub);
         if (last) ds_tile_rects(a, sm, nvalid);
-        ds_prefix(a, sm, p, true);
+        ds_prefix(a, sm, p, false);  // (published before the ranking)
         ds_tile_write(a, sm, nvalid, kout, vout, shift, last);
     } else {
         if (p > 0) ds_range_hist(a, sm, kin, r0, r1, shift, false);
-        ds_prefix(a, sm, p, p > 0);   // pass 0: counted and published by phase H
+        if (p > 0) ds_prefix(a, sm, p, true);
         for (int64_t t0 = r0; t0 < r1; t0 += kDsTile) {
             const uint32_t nvalid = ds_tile_rank(sm, kin, vin, t0, r1, shift, drop, a.key_base);
             if (last) ds_tile_rects(a, sm, nvalid);
+            // pass 0 (counted and published by phase H): the prefix after the first tile's ranking
+            if (p == 0 && t0 == r0) ds_prefix(a, sm, p, false);
             ds_tile_write(a, sm, nvalid, kout, vout, shift, last);
         }
+        if (p == 0 && r1 <= r0) ds_prefix(a, sm, p, false);  // (an empty range still takes part)
     }
     if (last) {  // the CTA's pair slots and row coverage
         uint32_t v = tid < a.rows ? (uint32_t)sm.rowd[tid] : 0u;
@@ -470,6 +500,7 @@ __global__ void __launch_bounds__(kDsThreads, 1) depth_sort_kernel(DepthSortArgs
 #if defined(GES_DS_TIMING) && GES_DS_TIMING == 3
 }  // namespace ges
 extern "C" void ges_debug_ds_times(unsigned long long* out) { cudaMemcpyFromSymbol(out, ges::g_ds_t, 64); }
+extern "C" void ges_debug_ds_q(long long* out) { cudaMemcpyFromSymbol(out, ges::g_ds_q, 48); }
 namespace ges {
 #endif
 int depth_sort_grid() {

@@ -10,7 +10,7 @@ r = G.Renderer(params.P, cam.width, cam.height)
 r.forward(params, cam, st); torch.cuda.synchronize()
 lib = L.load()
 if hasattr(lib, "ges_debug_bin_trips"):
-    out = (C.c_ulonglong * 2)()
+    out = (C.c_ulonglong * 6)()
     lib.ges_debug_bin_trips(out)
     a = list(out)
     G.ges_preprocess(params, cam, st, r.frame); G.ges_sort(r.frame); torch.cuda.synchronize()
@@ -18,6 +18,7 @@ if hasattr(lib, "ges_debug_bin_trips"):
     b = list(out)
     c = r.frame.counts()
     print("trips rows", b[0]-a[0], "cols", b[1]-a[1], "pairs", c.pairs, "pairs/trip", c.pairs/(b[1]-a[1]))
+    print("direct-path chunks: rows", b[2]-a[2], "of", b[3]-a[3], " cols", b[4]-a[4], "of", b[5]-a[5])
     sys.exit(0)
 import numpy as np
 t = (C.c_ulonglong * 512)(); n = C.c_int(0)
