@@ -83,7 +83,10 @@ cudaError_t launch_reorder(const float* const* in, float* const* out, int n_buff
                            uint32_t* perm, void* workspace, cudaStream_t stream);
 
 // --- row-then-column binning (bin.cu) ----------------------------------------
-constexpr int kRowChunk = 2048;       // items per row-binning CTA
+#ifndef GES_ROW_CHUNK
+#define GES_ROW_CHUNK 2048
+#endif
+constexpr int kRowChunk = GES_ROW_CHUNK;  // items per row-binning CTA
 #ifndef GES_COL_CHUNK
 #define GES_COL_CHUNK 3072
 #endif

@@ -304,23 +304,43 @@ def test_screen_tile_bands_match_full_frame(world):
         assert bad.sum() == 0, (n, int(bad.sum()))
 
 
-@pytest.mark.parametrize("case", ["cfg4_camera", "wide_4096"])
-def test_binning_over_several_tile_windows(case):
-    """The binning kernels walk the tile grid in windows of <= 6144 tiles (one
-    shared-memory cursor table each).  Frames with more tiles than
-    one window -- config 4's 1600x1064 camera (2 windows) and a 4096-wide frame
-    (3 windows of 24 tile rows) -- must give the same bit-exact lists, ranges and
-    images as the oracle, including tiles on the window seams."""
+@pytest.mark.parametrize("case", ["cfg4_camera", "wide_4096", "tall_4096"])
+def test_binning_frame_shapes(case):
+    """The row and column binnings keep per-lane bin masks for ceil(bins / 32) bins
+    per lane (instantiated for 1, 2, 3, 4 and 8): config 4's 1600x1064 camera (100
+    tile columns, 67 rows: 4 and 3 per lane), a 4096-wide frame (256 columns: 8 per
+    lane) and a 4096-tall frame (256 rows: 8 per lane) must give the same bit-exact
+    lists, ranges and images as the oracle."""
     if case == "cfg4_camera":
         sc = gi.make_config(4, P=150000, n_views=1)
         cam = sc.cameras[0]
     else:
         sc = gi.make_config(1, P=40000)
         c0 = sc.cameras[0]
-        cam = gi.Camera(4096, 1024, 900.0, 900.0, 2048.0, 512.0, 0.2, c0.R, c0.t)
+        cam = (gi.Camera(4096, 1024, 900.0, 900.0, 2048.0, 512.0, 0.2, c0.R, c0.t) if case == "wide_4096"
+               else gi.Camera(1024, 4096, 900.0, 900.0, 512.0, 2048.0, 0.2, c0.R, c0.t))
     gs, osx = settings_pair(rho=sc.rho)
-    assert ((cam.width + 15) // 16) * ((cam.height + 15) // 16) > 6144
     run_case(sc.particles, cam, gs, osx, gi.upstream_grad(sc.seed, 4, cam.width, cam.height), label=case)
+
+
+def test_binning_stage_overflow_writes_directly():
+    """A chunk whose row-list entries (rows) or pairs (columns) exceed its shared-memory
+    stage writes them straight to HBM instead of staging them (bin.cu).  Wide splats
+    (rects of ~20-40 tiles a side) push every chunk over its stage: S1 state, lists and
+    ranges bit-exact against the oracle, and the image within the north_star bar."""
+    sc = gi.random_small_scene(23, P=5000, W=1024, H=768, sh_degree=1, kappa_max=0.6, log_scale_mu=-0.8)
+    cam = sc.cameras[0]
+    gs, osx = settings_pair(rho=sc.rho)
+    out = gpu_forward(sc.particles, cam, gs)
+    pre = O.preprocess(sc.particles, cam, osx, "f32")
+    compare_preprocess(out, pre)
+    compare_sort(out, pre)
+    vis = pre["status"] == 0
+    h = (pre["rect"][3] - pre["rect"][1])[vis]
+    w = (pre["rect"][2] - pre["rect"][0])[vis]
+    assert np.median(h) * 2048 > 8192 and np.median(w) * 3072 > 16384  # every chunk overflows its stage
+    ref = O.render_fwd(pre, cam, osx, *O.tile_lists(pre))
+    compare_image(out, ref)
 
 
 def test_exact_kernel_bands_match_full_frame():
