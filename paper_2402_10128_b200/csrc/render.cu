@@ -454,6 +454,7 @@ static void launch_fwd_ppt(const RenderFwdArgs& a, int grid, bool diag, cudaStre
 cudaError_t launch_render_fwd(const RenderFwdArgs& a, cudaStream_t stream) {
     static const int ppt = ppt_from_env("GES_PPT_FWD", 2);
     const int grid = a.tiles_x * a.tiles_y;
+    if (grid == 0) return cudaSuccess;  // a band without tile rows renders nothing
     const bool diag = a.n_eval || a.n_comp;  // the counters cost issue slots: only when asked
     if (a.exact) {
         if (ppt == 4) launch_fwd_ppt<4, true>(a, grid, diag, stream);
@@ -728,6 +729,7 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads, PPT) render_bwd_kernel(Render
 cudaError_t launch_render_bwd(const RenderBwdArgs& a, cudaStream_t stream) {
     static const int ppt = ppt_from_env("GES_PPT_BWD", 4);
     const int grid = a.tiles_x * a.tiles_y;
+    if (grid == 0) return cudaSuccess;  // a band without tile rows: no 2-D gradients
     if (a.exact) {
         if (ppt == 4) render_bwd_kernel<4, true><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
         else render_bwd_kernel<2, true><<<grid, Layout<2>::kThreads, 0, stream>>>(a);

@@ -439,3 +439,29 @@ def test_equal_depth_ties_keep_index_order(P):
     for t in range(r.size - 1):
         seg = out["list"][r[t]:r[t + 1]]
         assert np.all(np.diff(seg) > 0), t
+
+
+def test_band_without_rows():
+    """A band that owns no tile row (N bands > tile rows, band b >= tiles_y) renders
+    nothing: every stage runs (no zero-size launch), no pairs, the image is untouched
+    and the gradients are zero."""
+    sc = gi.make_config(0)
+    cam = sc.cameras[0]
+    assert (cam.height + 15) // 16 == 16
+    gs = G.Settings(rho=0.1, tile_row_begin=17, tile_row_step=20)
+    params = G.PlanarParams.from_inputs(sc.particles)
+    r = G.Renderer(params.P, cam.width, cam.height)
+    img = torch.full((3, cam.height, cam.width), 7.0, device="cuda")
+    G.ges_preprocess(params, cam, gs, r.frame)
+    G.ges_sort(r.frame)
+    G.ges_render_fwd(r.frame, gs, img)
+    dL = torch.from_numpy(gi.upstream_grad(1, 0, cam.width, cam.height)).cuda()
+    grads = G.PlanarParams.zeros(params.P, params.sh_degree)
+    grads.flat.fill_(5.0)
+    G.ges_render_bwd(params, cam, gs, r.frame, dL, grads)
+    torch.cuda.synchronize()
+    c = r.frame.counts()
+    assert c.visible == 0 and c.pairs == 0 and not c.overflow
+    assert r.frame.c.band_rows == 0
+    assert bool((img == 7.0).all())
+    assert bool((grads.flat == 0.0).all())
