@@ -122,6 +122,9 @@ typedef enum { GES_KERNEL_PHI_GAUSS = 0, GES_KERNEL_EXACT_BETA = 1 } ges_kernel;
  * into the buffers (several views before one allreduce), 0 overwrites. */
 typedef struct {
     float *mean, *log_scale, *quat, *opacity_logit, *sh, *beta;
+    float *mean2d;          /* optional (NULL: not written): [2][P] dL/d(u, v), the gradient of
+                               the projected mean in pixels (the view-space gradient of 3DGS's
+                               densification; 0 for particles that are not visible) */
     int32_t accumulate;
     int32_t _pad;
 } ges_grads;
@@ -131,6 +134,9 @@ typedef struct {
     int64_t pairs;      /* M = (tile, particle) pairs in the per-tile lists          */
     int64_t slots;      /* sum over visible particles of their rect areas (>= M)     */
     int64_t capacity;   /* pair capacity of the frame                               */
+    int64_t culled_near;/* particles with status GES_CULL_NEAR                       */
+    int64_t degenerate; /* particles with status GES_DEGENERATE                      */
+    int64_t offscreen;  /* particles with status GES_OFFSCREEN                       */
     int32_t overflow;   /* 1 if slots > capacity: lists and images are invalid       */
     int32_t _pad;
 } ges_counts;
@@ -145,7 +151,10 @@ enum {
     GES_CTR_TICKET_COLS = 5, /* scratch: chunk tickets of the column counts         */
     GES_CTR_TICKET_EMIT = 6, /* scratch: chunk tickets of the column binning        */
     GES_CTR_KEYMAX = 7,   /* largest visible depth key (depth sort pass plan)       */
-    GES_CTR_N = 16
+    GES_CTR_CULLED_NEAR = 8, /* particles behind the near plane                      */
+    GES_CTR_DEGENERATE = 9,  /* non-finite / singular particles                      */
+    GES_CTR_OFFSCREEN = 10,  /* particles whose rect misses the frame (or band)      */
+    GES_CTR_N = 24           /* (slots 16-23: debug timers of instrumented builds)   */
 };
 
 /* A frame: every per-frame device array, carved by ges_frame_init out of ONE

@@ -21,7 +21,7 @@ GES_KERNEL_PHI_GAUSS, GES_KERNEL_EXACT_BETA = 0, 1
 GES_VISIBLE, GES_CULL_NEAR, GES_DEGENERATE, GES_OFFSCREEN = range(4)
 GES_CTR_VISIBLE, GES_CTR_PAIRS, GES_CTR_OVERFLOW, GES_CTR_SLOTS = 0, 1, 2, 3
 GES_CTR_TICKET, GES_CTR_TICKET_COLS, GES_CTR_TICKET_EMIT = 4, 5, 6
-GES_CTR_KEYMAX, GES_CTR_N = 7, 16
+GES_CTR_KEYMAX, GES_CTR_CULLED_NEAR, GES_CTR_DEGENERATE, GES_CTR_OFFSCREEN, GES_CTR_N = 7, 8, 9, 10, 24
 
 _fp = C.POINTER(C.c_float)
 _u32p = C.POINTER(C.c_uint32)
@@ -45,12 +45,13 @@ class ges_settings(C.Structure):
 
 
 class ges_grads(C.Structure):
-    _fields_ = [(n, C.c_void_p) for n in ("mean", "log_scale", "quat", "opacity_logit", "sh", "beta")] + [
+    _fields_ = [(n, C.c_void_p) for n in ("mean", "log_scale", "quat", "opacity_logit", "sh", "beta", "mean2d")] + [
         ("accumulate", C.c_int32), ("_pad", C.c_int32)]
 
 
 class ges_counts(C.Structure):
     _fields_ = [("visible", C.c_int64), ("pairs", C.c_int64), ("slots", C.c_int64), ("capacity", C.c_int64),
+                ("culled_near", C.c_int64), ("degenerate", C.c_int64), ("offscreen", C.c_int64),
                 ("overflow", C.c_int32), ("_pad", C.c_int32)]
 
 

@@ -85,10 +85,14 @@ class PlanarParams:
             setattr(p, n, getattr(self, n).data_ptr())
         return p
 
-    def c_grads(self, accumulate: bool) -> L.ges_grads:
+    def c_grads(self, accumulate: bool, mean2d: Optional[torch.Tensor] = None) -> L.ges_grads:
+        """mean2d (optional): a [2][P] fp32 device tensor for dL/d(u, v) (ges.h ges_grads)."""
         g = L.ges_grads()
         for n in PARAM_NAMES:
             setattr(g, n, getattr(self, n).data_ptr())
+        if mean2d is not None:
+            assert mean2d.dtype == torch.float32 and mean2d.is_contiguous() and mean2d.numel() == 2 * self.P
+            g.mean2d = mean2d.data_ptr()
         g.accumulate = 1 if accumulate else 0
         return g
 
@@ -204,9 +208,10 @@ def ges_render_fwd(frame: Frame, settings: Settings, image: torch.Tensor, n_eval
 
 
 def ges_render_bwd(particles: PlanarParams, camera, settings: Settings, frame: Frame, dL_dimage: torch.Tensor,
-                   grads: PlanarParams, accumulate: bool = False, stream=None) -> None:
+                   grads: PlanarParams, accumulate: bool = False, stream=None,
+                   mean2d: Optional[torch.Tensor] = None) -> None:
     assert dL_dimage.dtype == torch.float32 and dL_dimage.is_contiguous()
-    p, c, s, g = particles.c_particles(), c_camera(camera), settings.c(), grads.c_grads(accumulate)
+    p, c, s, g = particles.c_particles(), c_camera(camera), settings.c(), grads.c_grads(accumulate, mean2d)
     L.check(L.load().ges_render_bwd(C.byref(p), C.byref(c), C.byref(s), C.byref(frame.c),
                                     C.c_void_p(dL_dimage.data_ptr()), C.byref(g), C.c_void_p(_stream(stream))),
             "ges_render_bwd")
@@ -220,8 +225,8 @@ def ges_render_bwd_tiles(settings: Settings, frame: Frame, dL_dimage: torch.Tens
 
 
 def ges_backward_particles(particles: PlanarParams, camera, settings: Settings, frame: Frame, grads: PlanarParams,
-                           accumulate: bool = False, stream=None) -> None:
-    p, c, s, g = particles.c_particles(), c_camera(camera), settings.c(), grads.c_grads(accumulate)
+                           accumulate: bool = False, stream=None, mean2d: Optional[torch.Tensor] = None) -> None:
+    p, c, s, g = particles.c_particles(), c_camera(camera), settings.c(), grads.c_grads(accumulate, mean2d)
     L.check(L.load().ges_backward_particles(C.byref(p), C.byref(c), C.byref(s), C.byref(frame.c), C.byref(g),
                                             C.c_void_p(_stream(stream))), "ges_backward_particles")
 

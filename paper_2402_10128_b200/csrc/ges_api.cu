@@ -280,6 +280,7 @@ ges_status ges_backward_particles(const ges_particles* particles, const ges_came
     q.status = frame->status; q.flags = frame->flags; q.grad2d = frame->grad2d; q.drgb_ddir = frame->drgb_ddir;
     q.g_mean = grads->mean; q.g_log_scale = grads->log_scale; q.g_quat = grads->quat;
     q.g_opacity_logit = grads->opacity_logit; q.g_sh = grads->sh; q.g_beta = grads->beta;
+    q.g_mean2d = grads->mean2d;
     q.accumulate = grads->accumulate;
     return cuda_status(launch_particle_bwd(q, (cudaStream_t)stream));
 }
@@ -305,6 +306,9 @@ ges_status ges_counts_get(const ges_frame* frame, ges_counts* host_out, void* st
     host_out->pairs = (int64_t)c[GES_CTR_PAIRS];
     host_out->slots = (int64_t)c[GES_CTR_SLOTS];
     host_out->capacity = frame->pair_capacity;
+    host_out->culled_near = (int64_t)c[GES_CTR_CULLED_NEAR];
+    host_out->degenerate = (int64_t)c[GES_CTR_DEGENERATE];
+    host_out->offscreen = (int64_t)c[GES_CTR_OFFSCREEN];
     host_out->overflow = (int32_t)c[GES_CTR_OVERFLOW];
     host_out->_pad = 0;
     return GES_OK;

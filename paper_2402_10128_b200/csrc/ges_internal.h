@@ -164,6 +164,7 @@ struct ParticleBwdArgs {
     const float* drgb_ddir;           // [9][P] from S1
     float* grad2d;
     float *g_mean, *g_log_scale, *g_quat, *g_opacity_logit, *g_sh, *g_beta;
+    float* g_mean2d;                  // optional [2][P] dL/d(u, v)
     int accumulate;
 };
 cudaError_t launch_particle_bwd(const ParticleBwdArgs& a, cudaStream_t stream);

@@ -63,7 +63,7 @@ __device__ __forceinline__ void particle_bwd_one(const ParticleBwdArgs& a, int i
     // read-modify-write in DRAM.
     const bool vis = in.status == GES_VISIBLE;
     float o_mean[3] = {0.f, 0.f, 0.f}, o_ls[3] = {0.f, 0.f, 0.f}, o_q[4] = {0.f, 0.f, 0.f, 0.f};
-    float o_op = 0.f, o_beta = 0.f;
+    float o_op = 0.f, o_beta = 0.f, o_m2d[2] = {0.f, 0.f};
     float Y[16], drgb[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int k = 0; k < 16; ++k) Y[k] = 0.f;
@@ -144,6 +144,8 @@ __device__ __forceinline__ void particle_bwd_one(const ParticleBwdArgs& a, int i
         const float cA = (C * idet) * (-0.5f * kLog2e), cB = (-B * idet) * (-kLog2e), cC = (A * idet) * (-0.5f * kLog2e);
         const float E = kl * r0.x, F = kl * r0.y;
         const float du = 2.f * cA * E + cB * F, dv = cB * E + 2.f * cC * F;
+        o_m2d[0] = du;
+        o_m2d[1] = dv;
         const float da = (kl * r0.z) * (-0.5f * kLog2e);
         const float db = (kl * r0.w) * (-kLog2e);
         const float dc = (kl * r1.x) * (-0.5f * kLog2e);
@@ -258,6 +260,10 @@ __device__ __forceinline__ void particle_bwd_one(const ParticleBwdArgs& a, int i
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) put(a.g_sh, 3 * k + ch, Y[k] * drgb[ch]);
     put(a.g_beta, 0, o_beta);
+    if (a.g_mean2d) {
+        put(a.g_mean2d, 0, o_m2d[0]);
+        put(a.g_mean2d, 1, o_m2d[1]);
+    }
     // leave the 2-D record zeroed for the next backward (ges.h); every particle's
     // record is written so the 48-B records cover whole sectors
     float4* rec = reinterpret_cast<float4*>(a.grad2d) + (size_t)i * (kGrad2dStride / 4);

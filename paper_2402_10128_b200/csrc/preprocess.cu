@@ -226,6 +226,22 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
 
 constexpr int kPreThreads = 256;
 
+// Per-warp counts of the non-visible statuses (ges_counts: culled_near, degenerate,
+// offscreen); status -1 = no particle.
+struct StatusCounts {
+    uint32_t near = 0, degen = 0, off = 0;
+    __device__ __forceinline__ void add(int status) {
+        near += __popc(__ballot_sync(0xffffffffu, status == GES_CULL_NEAR));
+        degen += __popc(__ballot_sync(0xffffffffu, status == GES_DEGENERATE));
+        off += __popc(__ballot_sync(0xffffffffu, status == GES_OFFSCREEN));
+    }
+    __device__ __forceinline__ void flush(unsigned long long* ctr) const {
+        if (near) atomicAdd(&ctr[GES_CTR_CULLED_NEAR], (unsigned long long)near);
+        if (degen) atomicAdd(&ctr[GES_CTR_DEGENERATE], (unsigned long long)degen);
+        if (off) atomicAdd(&ctr[GES_CTR_OFFSCREEN], (unsigned long long)off);
+    }
+};
+
 // Writes particle i's S1 state and its sort key (fp32 depth bits, or 0xffffffff
 // when not visible -- dropped by depth pass 0, which thereby compacts the
 // visible set).  Returns visibility.
@@ -257,18 +273,23 @@ __global__ void __launch_bounds__(kPreThreads, GES_PRE_MINB) preprocess_kernel(P
     const int tid = threadIdx.x, lane = tid & 31;
     const CamDerived cd = derive_camera(a.cam);
     uint32_t nvis = 0, kmax = 0;  // visible count, largest visible depth key (depth sort pass plan)
+    StatusCounts sc;
     for (int base = blockIdx.x * kPreThreads; base < a.P; base += gridDim.x * kPreThreads) {
         const int i = base + tid;
         bool vis = false;
+        int status = -1;
         if (i < a.P) {
             const ParamIn in = load_params(a, i);
             const PreOut o = preprocess_one<K>(a, cd, i, in, a.sh + i, a.P);
             vis = store_out(a, i, o);
+            status = o.status;
         }
         nvis += __popc(__ballot_sync(0xffffffffu, vis));
+        sc.add(status);
         if (vis) kmax = max(kmax, a.vis_key[i]);
     }
     if (lane == 0 && nvis) atomicAdd(&a.counters[GES_CTR_VISIBLE], (unsigned long long)nvis);
+    if (lane == 0) sc.flush(a.counters);
     kmax = __reduce_max_sync(0xffffffffu, kmax);
     if (lane == 0 && kmax) atomicMax(&a.counters[GES_CTR_KEYMAX], (unsigned long long)kmax);
 }
@@ -360,6 +381,7 @@ __global__ void __launch_bounds__(kPreTmaThreads) preprocess_tma_kernel(Preproce
     }
     const CamDerived cd = derive_camera(a.cam);
     uint32_t nvis = 0, kmax = 0;  // visible count, largest visible depth key (depth sort pass plan)
+    StatusCounts sc;
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++it) {
         const int st = it % kPreStages;
@@ -377,20 +399,25 @@ __global__ void __launch_bounds__(kPreTmaThreads) preprocess_tma_kernel(Preproce
         if (lane == 0) mbar_arrive(&s_empty[st]);  // the warp is done reading the stage
         const bool vis = store_out(a, i, o);
         nvis += __popc(__ballot_sync(0xffffffffu, vis));
+        sc.add(o.status);
         if (vis) kmax = max(kmax, __float_as_uint(o.depth));
     }
     // the partial last tile, from global memory
     if (blockIdx.x == 0) {
         const int i = ntiles * kPreTile + tid;
         bool vis = false;
+        int status = -1;
         if (i < a.P) {
             const ParamIn in = load_params(a, i);
             const PreOut o = preprocess_one<K>(a, cd, i, in, a.sh + i, a.P);
             vis = store_out(a, i, o);
+            status = o.status;
             if (vis) kmax = max(kmax, __float_as_uint(o.depth));
         }
         nvis += __popc(__ballot_sync(0xffffffffu, vis));
+        sc.add(status);
     }
+    if (lane == 0) sc.flush(a.counters);
     if (lane == 0 && nvis) atomicAdd(&s_nvis, nvis);
     kmax = __reduce_max_sync(0xffffffffu, kmax);
     if (lane == 0 && kmax) atomicMax(&s_kmax, kmax);

@@ -427,13 +427,13 @@ __device__ void ds_pass(const DepthSortArgs& a, DsSmem& sm, const uint32_t* kin,
     }
 }
 
-// GES_DS_TIMING: CTA 0 records %globaltimer at phase boundaries in counters[8..15]
+// GES_DS_TIMING: CTA 0 records %globaltimer at phase boundaries in counters[16..23]
 __device__ __forceinline__ void ds_mark(const DepthSortArgs& a, int slot) {
 #ifdef GES_DS_TIMING
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        a.counters[8 + slot] = t;
+        a.counters[16 + slot] = t;
     }
 #endif
 }

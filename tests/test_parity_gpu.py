@@ -25,6 +25,9 @@ PRE_KEYS = ("depth", "uv", "conic", "kappa", "rgb", "radius", "rect", "status", 
 def compare_preprocess(out, pre):
     P = pre["status"].size
     assert np.array_equal(out["status"], pre["status"])
+    c = out["counts"]  # ges_counts: the status census of S1
+    assert (c.visible, c.culled_near, c.degenerate, c.offscreen) == tuple(
+        int((pre["status"] == k).sum()) for k in (0, 1, 2, 3))
     vis = pre["status"] == 0
     assert np.array_equal(out["depth"].view(np.uint32), pre["depth"].view(np.uint32))
     g_uv = out["pay0"][:, 0:2].T
@@ -465,3 +468,45 @@ def test_band_without_rows():
     assert r.frame.c.band_rows == 0
     assert bool((img == 7.0).all())
     assert bool((grads.flat == 0.0).all())
+
+
+@pytest.mark.parametrize("case", ["config0", "config1_beta2", "config0_exact"])
+def test_mean2d_gradient(case):
+    """ges_grads.mean2d (optional output): dL/d(u, v), the gradient of each visible
+    particle's projected mean in pixels, against the oracle's S5a du, dv (Eq. 3's
+    adjoint) at the north_star tolerance or the entry's R19 scale; exactly 0 for
+    particles that are not visible; accumulate adds."""
+    kernel = 1 if case.endswith("exact") else 0
+    sc = gi.make_config(1, beta_value=2.0, P=20000) if case == "config1_beta2" else gi.make_config(0)
+    cam = sc.cameras[0]
+    gs, osx = settings_pair(rho=0.1, kernel=kernel)
+    out = gpu_forward(sc.particles, cam, gs)
+    pre = O.preprocess(sc.particles, cam, osx, "f32")
+    offsets, lst = O.tile_lists(pre)
+    ref = O.render_fwd(pre, cam, osx, offsets, lst)
+    dL = masked_upstream(gi.upstream_grad(sc.seed, 3, cam.width, cam.height), ref["amb"])
+    g2d, mag = O.render_bwd(pre, cam, osx, offsets, lst, dL, with_abs=True)
+    P = sc.particles.P
+    m2d = torch.full((2, P), 3.0, device="cuda")
+    grads = G.PlanarParams.zeros(P, out["params"].sh_degree)
+    dLt = torch.from_numpy(np.ascontiguousarray(dL, np.float32)).cuda()
+    G.ges_render_bwd(out["params"], cam, gs, out["renderer"].frame, dLt, grads, mean2d=m2d)
+    torch.cuda.synchronize()
+    a = m2d.cpu().numpy().astype(np.float64)
+    vis = pre["status"] == 0
+    assert np.all(a[:, ~vis] == 0.0)
+    from gpu_helpers import EPS32, R19_C
+    for j in range(2):
+        r = g2d[j, vis]
+        bound = np.maximum(np.maximum(1e-3 * np.abs(r), 1e-6), R19_C * EPS32 * mag[j, vis] + mag[10 + j, vis])
+        bad = np.abs(a[j, vis] - r) > bound
+        assert bad.sum() == 0, (case, j, int(bad.sum()), int(vis.sum()))
+    print(f"[mean2d {case}] compared {int(vis.sum())} of {int(vis.sum())} visible particles")
+    # accumulate: a second view adds
+    G.ges_preprocess(out["params"], cam, gs, out["renderer"].frame)
+    G.ges_sort(out["renderer"].frame)
+    G.ges_render_fwd(out["renderer"].frame, gs, torch.empty(3, cam.height, cam.width, device="cuda"))
+    G.ges_render_bwd(out["params"], cam, gs, out["renderer"].frame, dLt, grads, accumulate=True, mean2d=m2d)
+    torch.cuda.synchronize()
+    b = m2d.cpu().numpy().astype(np.float64)
+    assert np.allclose(b, 2 * a, rtol=1e-4, atol=1e-6 * (1 + np.abs(a).max()))

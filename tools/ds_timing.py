@@ -20,8 +20,8 @@ for _ in range(5):
     G.ges_preprocess(params, cam, st, r.frame)
     G.ges_sort(r.frame)
 torch.cuda.synchronize()
-ctr = r.frame.view("counters", torch.int64, 16).cpu().tolist()
-t = ctr[8:16]
+ctr = r.frame.view("counters", torch.int64, 24).cpu().tolist()
+t = ctr[16:24]
 # slots: 0 start, 1 after phase H, 2 / 3 after passes 0 / 1 (non-last), 4 last pass hist done,
 # 5 last pass prefix done, 6 end
 names = [("phase H", 0, 1), ("pass 0", 1, 2), ("pass 1", 2, 3), ("last hist", 3, 4), ("last prefix", 4, 5),
