@@ -226,19 +226,23 @@ __device__ __forceinline__ PreOut preprocess_one(const PreprocessArgs& a, const 
 
 constexpr int kPreThreads = 256;
 
-// Per-warp counts of the non-visible statuses (ges_counts: culled_near, degenerate,
-// offscreen); status -1 = no particle.
+// Per-thread counts of the non-visible statuses (ges_counts: culled_near, degenerate,
+// offscreen), summed over the warp once at the end; status -1 = no particle.
 struct StatusCounts {
     uint32_t near = 0, degen = 0, off = 0;
     __device__ __forceinline__ void add(int status) {
-        near += __popc(__ballot_sync(0xffffffffu, status == GES_CULL_NEAR));
-        degen += __popc(__ballot_sync(0xffffffffu, status == GES_DEGENERATE));
-        off += __popc(__ballot_sync(0xffffffffu, status == GES_OFFSCREEN));
+        near += status == GES_CULL_NEAR;
+        degen += status == GES_DEGENERATE;
+        off += status == GES_OFFSCREEN;
     }
-    __device__ __forceinline__ void flush(unsigned long long* ctr) const {
-        if (near) atomicAdd(&ctr[GES_CTR_CULLED_NEAR], (unsigned long long)near);
-        if (degen) atomicAdd(&ctr[GES_CTR_DEGENERATE], (unsigned long long)degen);
-        if (off) atomicAdd(&ctr[GES_CTR_OFFSCREEN], (unsigned long long)off);
+    __device__ __forceinline__ void flush(unsigned long long* ctr) const {  // whole warp; lane 0 adds
+        const uint32_t n = __reduce_add_sync(0xffffffffu, near), d = __reduce_add_sync(0xffffffffu, degen),
+                       o = __reduce_add_sync(0xffffffffu, off);
+        if ((threadIdx.x & 31) == 0) {
+            if (n) atomicAdd(&ctr[GES_CTR_CULLED_NEAR], (unsigned long long)n);
+            if (d) atomicAdd(&ctr[GES_CTR_DEGENERATE], (unsigned long long)d);
+            if (o) atomicAdd(&ctr[GES_CTR_OFFSCREEN], (unsigned long long)o);
+        }
     }
 };
 
@@ -289,7 +293,7 @@ __global__ void __launch_bounds__(kPreThreads, GES_PRE_MINB) preprocess_kernel(P
         if (vis) kmax = max(kmax, a.vis_key[i]);
     }
     if (lane == 0 && nvis) atomicAdd(&a.counters[GES_CTR_VISIBLE], (unsigned long long)nvis);
-    if (lane == 0) sc.flush(a.counters);
+    sc.flush(a.counters);
     kmax = __reduce_max_sync(0xffffffffu, kmax);
     if (lane == 0 && kmax) atomicMax(&a.counters[GES_CTR_KEYMAX], (unsigned long long)kmax);
 }
@@ -417,7 +421,7 @@ __global__ void __launch_bounds__(kPreTmaThreads) preprocess_tma_kernel(Preproce
         nvis += __popc(__ballot_sync(0xffffffffu, vis));
         sc.add(status);
     }
-    if (lane == 0) sc.flush(a.counters);
+    sc.flush(a.counters);
     if (lane == 0 && nvis) atomicAdd(&s_nvis, nvis);
     kmax = __reduce_max_sync(0xffffffffu, kmax);
     if (lane == 0 && kmax) atomicMax(&s_kmax, kmax);
