@@ -60,7 +60,14 @@ struct DsSmem {
     int rowd[kMaxBandRows + 1];          // last pass: row difference counts of the CTA's items
     unsigned long long area;             // last pass: the CTA's pair slots
     uint32_t warp[kDsWarps + 1];
+    uint32_t hn;                         // phase H's compacted count (> kDsTile: did not fit)
+    // phase H keeps the visible keys of the CTA's range of the S1 keys (and their
+    // indices), compacted in index order, for pass 0 when they fit one tile -- over
+    // whist, which pass 0's ranking overwrites only after loading them
+    __device__ uint32_t* hkeys() { return &whist[0][0]; }
+    __device__ uint32_t* hvals() { return &whist[0][0] + kDsTile; }
 };
+static_assert(sizeof(uint32_t) * kDsWarps * kDsDigits >= sizeof(uint32_t) * 2 * kDsTile, "hkeys/hvals fit whist");
 
 __device__ __forceinline__ uint32_t ds_digit(uint32_t key, uint32_t kmin, int shift) {
     return ((key - kmin) >> shift) & (kDsDigits - 1);
@@ -205,6 +212,7 @@ __device__ void ds_prefix(const DepthSortArgs& a, DsSmem& sm, int p, bool publis
 // digit (warp multisplit: one ballot per digit bit), and reorders it in shared
 // memory (sm.keys / sm.vals in digit order); sm.cnt = the tile's digit counts,
 // sm.local = their exclusive offsets.  Returns the number of valid keys.
+template <bool SMEM_IN = false>  // the tile's keys / ids come from shared memory (phase H's compaction)
 __device__ uint32_t ds_tile_rank(DsSmem& sm, const uint32_t* kin, const uint32_t* vin, int64_t t0, int64_t r1,
                                  int shift, bool drop, uint32_t kmin, uint32_t* publish = nullptr) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -216,14 +224,15 @@ __device__ uint32_t ds_tile_rank(DsSmem& sm, const uint32_t* kin, const uint32_t
 #pragma unroll
     for (int j = 0; j < kDsItems; ++j) {
         const int64_t idx = wb + j * 32 + lane;
-        k[j] = idx < r1 ? __ldcg(kin + idx) : kInvalidKey;
+        k[j] = idx < r1 ? (SMEM_IN ? kin[idx] : __ldcg(kin + idx)) : kInvalidKey;
     }
 #pragma unroll
     for (int j = 0; j < kDsItems; ++j) {
         const int64_t idx = wb + j * 32 + lane;
-        v[j] = vin ? (idx < r1 ? __ldcg(vin + idx) : 0u) : (uint32_t)idx;
+        v[j] = vin ? (idx < r1 ? (SMEM_IN ? vin[idx] : __ldcg(vin + idx)) : 0u) : (uint32_t)idx;
         if (idx < r1 && !(drop && k[j] == kInvalidKey)) valid |= 1u << j;
     }
+    if (SMEM_IN) __syncthreads();  // the inputs alias whist: every thread has loaded them
     if (publish) {  // the tile is the CTA's whole range: publish its digit counts before ranking,
                     // so that the pass prefix's loads find the other CTAs' words already set
         if (tid < kDsDigits) sm.cnt[tid] = 0;
@@ -401,7 +410,13 @@ __device__ void ds_pass(const DepthSortArgs& a, DsSmem& sm, const uint32_t* kin,
         if (tid == 0) sm.area = 0;
         __syncthreads();
     }
-    if (p > 0 && r1 - r0 <= kDsTile) {
+    if (p == 0 && sm.hn <= (uint32_t)kDsTile) {
+        // pass 0 from phase H's compacted visible keys: one tile, counted and published there
+        const uint32_t nvalid = ds_tile_rank<true>(sm, sm.hkeys(), sm.hvals(), 0, sm.hn, shift, false, a.key_base);
+        if (last) ds_tile_rects(a, sm, nvalid);
+        ds_prefix(a, sm, p, false);
+        ds_tile_write(a, sm, nvalid, kout, vout, shift, last);
+    } else if (p > 0 && r1 - r0 <= kDsTile) {
         uint32_t* pub = a.st_cnt + ((size_t)p * kDsMaxGrid + blockIdx.x) * kDsDigits;
         const uint32_t nvalid = ds_tile_rank(sm, kin, vin, r0, r1, shift, drop, a.key_base, pub);
         if (last) ds_tile_rects(a, sm, nvalid);
@@ -461,18 +476,58 @@ __global__ void __launch_bounds__(kDsThreads, 1) depth_sort_kernel(DepthSortArgs
     }
     __syncthreads();
     {
+        // count pass 0's digits of the range and compact its visible keys (with their
+        // indices, in index order) into sm.hkeys / sm.hvals while they fit one tile
         const int64_t h0 = range_lo(P, c, G), h1 = range_lo(P, c + 1, G);
+        const int lane = tid & 31, warp = tid >> 5;
+        const uint32_t lt_mask = (1u << lane) - 1u;
+        uint32_t hn = 0;  // (uniform)
         for (int64_t t0 = h0; t0 < h1; t0 += kDsTile) {
-            uint32_t k[kDsItems];
+            // warp-striped as in ds_tile_rank: item j of lane l of warp w is t0 + w 256 + j 32 + l
+            const int64_t wb = t0 + warp * (kDsItems * 32);
+            uint32_t k[kDsItems], bal[kDsItems], wcnt = 0;
 #pragma unroll
             for (int j = 0; j < kDsItems; ++j) {
-                const int64_t idx = t0 + j * kDsThreads + tid;
+                const int64_t idx = wb + j * 32 + lane;
                 k[j] = idx < h1 ? __ldcg(a.key0 + idx) : kInvalidKey;
             }
 #pragma unroll
-            for (int j = 0; j < kDsItems; ++j)
+            for (int j = 0; j < kDsItems; ++j) {
+                bal[j] = __ballot_sync(0xffffffffu, k[j] != kInvalidKey);
+                wcnt += __popc(bal[j]);
                 if (k[j] != kInvalidKey) atomicAdd(&sm.cnt[ds_digit(k[j], kmin, 0)], 1u);
+            }
+            if (lane == 0) sm.warp[warp] = wcnt;
+            __syncthreads();
+            if (warp == 0) {  // exclusive scan of the 32 warp counts
+                const uint32_t x = sm.warp[lane];
+                uint32_t incl = x;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t nn = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += nn;
+                }
+                sm.warp[lane] = incl - x;
+                if (lane == 31) sm.warp[kDsWarps] = incl;
+            }
+            __syncthreads();
+            uint32_t pos = hn + sm.warp[warp];
+            const uint32_t tile_total = sm.warp[kDsWarps];
+#pragma unroll
+            for (int j = 0; j < kDsItems; ++j) {
+                if (k[j] != kInvalidKey) {
+                    const uint32_t q = pos + __popc(bal[j] & lt_mask);
+                    if (q < (uint32_t)kDsTile) {
+                        sm.hkeys()[q] = k[j];
+                        sm.hvals()[q] = (uint32_t)(wb + j * 32 + lane);
+                    }
+                }
+                pos += __popc(bal[j]);
+            }
+            hn += tile_total;
+            __syncthreads();  // (sm.warp is reused by the next tile)
         }
+        if (tid == 0) sm.hn = hn;
         __syncthreads();
     }
     if (tid < kDsDigits) a.st_cnt[(size_t)c * kDsDigits + tid] = kCntFlag | sm.cnt[tid];  // pass 0 counted
