@@ -1,5 +1,6 @@
-// sort.cu -- S2: depth radix sort of the visible particles
-// and the item scan that turns the depth-sorted particles into pair slots.
+// sort.cu -- S2: depth radix sort of the visible particles;
+// its last pass writes the depth-ordered item records the binning (bin.cu)
+// turns into the per-tile lists.
 //
 // Design: instead of a 64-bit LSD sort of
 // (tile_id << 32 | depth) keys over all pairs, the depth order is established
@@ -13,12 +14,15 @@
 // ONE persistent cooperative kernel (one 1024-thread CTA per SM): at V ~ 1e6
 // the passes are latency-bound, so every phase boundary that is not a true
 // data dependency is removed.
-//   phase H  CTA c zeroes its published words and counts pass 0's digits of
-//            its range [c P / G, (c+1) P / G) of the S1 keys.  Grid barrier.
+//   phase H  CTA c zeroes its published words, counts pass 0's digits of its
+//            range [c P / G, (c+1) P / G) of the S1 keys and compacts the
+//            visible ones (with their indices, in index order) into shared
+//            memory, from where pass 0 ranks them as one tile.  Grid barrier.
 //   pass p   CTA c owns [c n / G, (c+1) n / G) of the pass input (n = P for
 //            pass 0, then V): it ranks its keys stably by digit (a 8192-key
-//            tile: warp match_any multisplit, shared-memory reorder), publishes
-//            its digit counts (flagged words), and finds its starting position
+//            tile: stable warp ranks by owner-slot rounds, shared-memory
+//            reorder), publishes its digit counts (flagged words; a range of
+//            one tile before ranking), and finds its starting position
 //            per digit without a grid barrier, in two levels of 16-CTA groups
 //            (the earlier CTAs of its group + the earlier groups' totals, each
 //            group total published by the group's last CTA; the digit totals
@@ -209,7 +213,7 @@ __device__ void ds_prefix(const DepthSortArgs& a, DsSmem& sm, int p, bool publis
 
 // --- one 8192-key tile of a pass: rank, (last pass) areas, write -------------
 // ds_tile_rank: loads the tile [t0, min(t0 + kDsTile, r1)), ranks it stably by
-// digit (warp multisplit: one ballot per digit bit), and reorders it in shared
+// digit (per-warp counters, owner-slot rounds: below), and reorders it in shared
 // memory (sm.keys / sm.vals in digit order); sm.cnt = the tile's digit counts,
 // sm.local = their exclusive offsets.  Returns the number of valid keys.
 template <bool SMEM_IN = false>  // the tile's keys / ids come from shared memory (phase H's compaction)
