@@ -206,7 +206,7 @@ typedef struct {
     uint32_t *col_excl;    /* [col_chunks][tiles_x] offset of each column chunk inside
                               its tiles' lists                                        */
     int64_t row_chunks;    /* ceil(P / 2048): item chunks of the row binning           */
-    int64_t col_chunks;    /* ceil(cap / 4096) + tiles_y: row-list chunks (bound)      */
+    int64_t col_chunks;    /* ceil(cap / 3072) + tiles_y: row-list chunks (bound)      */
     uint32_t *list;        /* [cap] per-tile lists: tile t = list[ranges[t] .. ranges[t+1]) */
     uint32_t *ranges;      /* [T+1]                                               */
     uint64_t *counters;    /* [GES_CTR_N]                                         */
