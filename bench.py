@@ -1214,29 +1214,53 @@ def run_e2e_train(G, scene, cam, st, frame, dev, stream, steps, world):
     opt = G.Adam(params)
     host_loss = torch.empty(4, dtype=torch.float32).pin_memory()
 
-    def one():
-        gt.copy_(host_gt, non_blocking=True)
-        G.ges_preprocess(params, cam, st, frame, stream)
-        G.ges_sort(frame, stream)
-        G.ges_render_fwd(frame, st, img, None, stream)
-        loss.mask(gt, 0.75, mask, stream=stream)
-        out, _ = loss(img, gt, mask, dL, stream=stream)
-        G.ges_render_bwd(params, cam, st, frame, dL, grads, False, stream)
-        opt.step(params, grads, stream=stream)
-        host_loss.copy_(out, non_blocking=True)
+    def one(s=None):
+        s = stream if s is None else s
+        with torch.cuda.stream(s):
+            gt.copy_(host_gt, non_blocking=True)
+            G.ges_preprocess(params, cam, st, frame, s)
+            G.ges_sort(frame, s)
+            G.ges_render_fwd(frame, st, img, None, s)
+            loss.mask(gt, 0.75, mask, stream=s)
+            out, _ = loss(img, gt, mask, dL, stream=s)
+            G.ges_render_bwd(params, cam, st, frame, dL, grads, False, s)
+            opt.step(params, grads, stream=s)
+            host_loss.copy_(out, non_blocking=True)
 
     for _ in range(2):
         one()
     torch.cuda.synchronize()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(steps):
-        one()
-    b.record(stream)
-    b.synchronize()
-    ms = a.elapsed_time(b) / steps
+
+    def timed(fn):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            fn()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b) / steps
+
+    ms_direct = timed(one)
+    # the same iteration captured once as a CUDA graph (the copies are graph memcpy nodes
+    # from / to the pinned host buffers, so every replay still moves them)
+    ms_graph, launch = None, "direct launches"
+    if world == 1:
+        try:
+            g = torch.cuda.CUDAGraph()
+            cap = torch.cuda.Stream()
+            cap.wait_stream(stream)
+            with torch.cuda.graph(g, stream=cap):
+                one(cap)
+            stream.wait_stream(cap)
+            torch.cuda.synchronize()
+            ms_graph = timed(g.replay)
+            launch = "CUDA graph"
+        except Exception as e:  # noqa: BLE001 -- reported; the direct number stands
+            launch = f"direct launches (graph capture failed: {e})"
+    ms = ms_graph if ms_graph is not None else ms_direct
     return {"value": world * W * H / (ms / 1e3) / 1e6, "unit": "Mpixel-frames/s (fwd+loss+bwd+Adam)",
-            "ms_per_step": ms, "h2d_bytes_per_step": host_gt.numel() * 4, "d2h_bytes_per_step": host_loss.numel() * 4,
+            "ms_per_step": ms, "ms_per_step_direct_launches": ms_direct, "launch": launch,
+            "h2d_bytes_per_step": host_gt.numel() * 4, "d2h_bytes_per_step": host_loss.numel() * 4,
             "final_loss": float(host_loss[0]), "pair_overflow": bool(frame.counts().overflow),
             "path": "parameters resident; ground truth pinned host -> device, S1-S4, ges_loss_mask + ges_loss, "
                     "S5, ges_adam_step, loss -> host"}
