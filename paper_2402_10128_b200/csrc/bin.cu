@@ -32,10 +32,15 @@
 
 namespace ges {
 
-constexpr int kBinThreads = 512;
+constexpr int kBinThreads = 512;     // column kernels
 constexpr int kBinWarps = kBinThreads / 32;
-constexpr int kRowItems = kRowChunk / kBinThreads;  // items per lane (4)
-constexpr int kColItems = kColChunk / kBinThreads;  // entries per lane (8)
+#ifndef GES_ROW_THREADS
+#define GES_ROW_THREADS 512
+#endif
+constexpr int kRowThreads = GES_ROW_THREADS;  // row kernel
+constexpr int kRowWarps = kRowThreads / 32;
+constexpr int kRowItems = kRowChunk / kRowThreads;  // items per lane
+constexpr int kColItems = kColChunk / kBinThreads;  // entries per lane
 #ifndef GES_ROW_STAGE
 #define GES_ROW_STAGE 8192
 #endif
@@ -47,7 +52,7 @@ constexpr int kColStage = GES_COL_STAGE;  // staged list entries (4 B) per chunk
 constexpr uint32_t kPub = 0x80000000u;  // published word flag (values < 2^31)
 constexpr int kGroup = 16;
 constexpr int kScanRows = kMaxBandRows / 32;  // rows per lane of a one-warp row scan
-static_assert(kRowItems * kBinThreads == kRowChunk && kColItems * kBinThreads == kColChunk, "chunk sizes");
+static_assert(kRowItems * kRowThreads == kRowChunk && kColItems * kBinThreads == kColChunk, "chunk sizes");
 
 __device__ __forceinline__ uint32_t lb_load(const uint32_t* p) {
     uint32_t v;
@@ -111,24 +116,25 @@ __device__ __forceinline__ int row_of(const uint32_t* first, int rows, uint32_t 
 // claimed in order (tickets), so every awaited word has a running or finished
 // writer.
 __device__ __forceinline__ void chunk_publish(uint32_t* st, int64_t k, int n, const uint32_t* agg) {
-    for (int i = threadIdx.x; i < n; i += kBinThreads) lb_store(st + k * n + i, kPub | agg[i]);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) lb_store(st + k * n + i, kPub | agg[i]);
 }
 __device__ void chunk_wait(uint32_t* st, uint32_t* gt, int64_t k, int64_t nk, int n, const uint32_t* agg,
                            uint32_t* out) {
     const int tid = threadIdx.x;
-    for (int i = tid; i < n; i += kBinThreads) out[i] = 0;
+    const int nt = blockDim.x;
+    for (int i = tid; i < n; i += nt) out[i] = 0;
     __syncthreads();
     const int64_t first = k / kGroup * kGroup, glast = (first + kGroup < nk ? first + kGroup : nk) - 1;
     const int m = (int)(k - first);
-    for (int t = tid; t < n * m; t += kBinThreads) {
+    for (int t = tid; t < n * m; t += nt) {
         const int i = t % n, j = t / n;
         atomicAdd(&out[i], lb_wait(st + (first + j) * n + i));
     }
     __syncthreads();
     if (k == glast)
-        for (int i = tid; i < n; i += kBinThreads) lb_store(gt + first * n + i, kPub | (out[i] + agg[i]));
+        for (int i = tid; i < n; i += nt) lb_store(gt + first * n + i, kPub | (out[i] + agg[i]));
     const int ng = (int)(first / kGroup);
-    for (int t = tid; t < n * ng; t += kBinThreads) {
+    for (int t = tid; t < n * ng; t += nt) {
         const int i = t % n, gg = t / n;
         atomicAdd(&out[i], lb_wait(gt + (int64_t)gg * kGroup * n + i));
     }
@@ -264,7 +270,7 @@ __device__ __forceinline__ void emit_group_staged(T* stage, uint32_t spare, cons
 template <class T>
 __device__ __forceinline__ void copy_runs(const T* stage, T* out, const uint32_t* lbase, const uint32_t* gbase, int n) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int x = warp; x < n; x += kBinWarps) {
+    for (int x = warp; x < n; x += (int)(blockDim.x >> 5)) {
         const uint32_t l0 = lbase[x], len = lbase[x + 1] - l0, g0 = gbase[x];
         for (uint32_t i = lane; i < len; i += 32) out[g0 + i] = stage[l0 + i];
     }
@@ -272,12 +278,12 @@ __device__ __forceinline__ void copy_runs(const T* stage, T* out, const uint32_t
 
 // ---- rows: items -> per-row lists ------------------------------------------
 template <int BPL>
-__global__ void __launch_bounds__(kBinThreads) bin_rows_kernel(BinArgs a) {
+__global__ void __launch_bounds__(kRowThreads) bin_rows_kernel(BinArgs a) {
     constexpr int NB = 32 * BPL;
-    __shared__ uint32_t s_cnt[kBinWarps][NB + 1];
-    __shared__ uint32_t s_msk[kBinWarps][NB + 1];
+    __shared__ uint32_t s_cnt[kRowWarps][NB + 1];
+    __shared__ uint32_t s_msk[kRowWarps][NB + 1];
     __shared__ uint32_t s_agg[NB], s_excl[NB], s_lbase[NB + 1], s_gbase[kMaxBandRows + 1];
-    __shared__ uint2 s_pay[kBinWarps][32];
+    __shared__ uint2 s_pay[kRowWarps][32];
     __shared__ unsigned long long s_k;
     extern __shared__ __align__(16) uint2 s_rstage[];  // [kRowStage + 1] (+ the spare slot)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -288,7 +294,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_rows_kernel(BinArgs a) {
     }
     const int64_t V = (int64_t)a.counters[GES_CTR_VISIBLE];
     if (tid == 0) s_k = atomicAdd(&a.counters[GES_CTR_TICKET], 1ull);
-    for (int i = tid; i < kBinWarps * (NB + 1); i += kBinThreads) {
+    for (int i = tid; i < kRowWarps * (NB + 1); i += kRowThreads) {
         (&s_cnt[0][0])[i] = 0u;
         (&s_msk[0][0])[i] = 0u;
     }
@@ -315,7 +321,7 @@ __global__ void __launch_bounds__(kBinThreads) bin_rows_kernel(BinArgs a) {
     __syncthreads();
     if (tid < rows) {  // exclusive over the warps; the chunk's row counts
         uint32_t run = 0;
-        for (int w = 0; w < kBinWarps; ++w) {
+        for (int w = 0; w < kRowWarps; ++w) {
             const uint32_t x = s_cnt[w][tid];
             s_cnt[w][tid] = run;
             run += x;
@@ -574,7 +580,7 @@ static cudaError_t launch_rows(const BinArgs& a, cudaStream_t stream) {
     const int smem = (kRowStage + 1) * (int)sizeof(uint2);
     cudaError_t e = set_smem(bin_rows_kernel<BR>, smem, done);
     if (e != cudaSuccess) return e;
-    bin_rows_kernel<BR><<<(unsigned)std::max<int64_t>(1, a.row_chunks), kBinThreads, smem, stream>>>(a);
+    bin_rows_kernel<BR><<<(unsigned)std::max<int64_t>(1, a.row_chunks), kRowThreads, smem, stream>>>(a);
     return cudaGetLastError();
 }
 
