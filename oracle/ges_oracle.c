@@ -326,9 +326,21 @@ typedef struct {
  * Returns the number of composited entries written to rec (if rec != NULL).
  * amb: bit0 = a skip/stop decision lies within the fp32 error bound (the
  * image may legitimately differ), bit1 = a 0.99-clamp decision does. */
+/* flip_at >= 0 (R18, both branches): the flip_at-th ambiguous decision of the pixel
+ * (0-based, in list order) takes its other outcome; every other decision is made
+ * as usual.  Returns -1 (and leaves C untouched) if the pixel has no such decision. */
+static int composite_pixel_flip(const OrSplat2D *s, const int32_t *lst, int64_t n, double px, double py,
+                                double C[3], double *T_out, int32_t *n_contrib, int32_t *n_eval, uint8_t *amb,
+                                OrComp *rec, double *errT_out, int flip_at);
 static int composite_pixel(const OrSplat2D *s, const int32_t *lst, int64_t n, double px, double py,
                            double C[3], double *T_out, int32_t *n_contrib, int32_t *n_eval, uint8_t *amb,
                            OrComp *rec, double *errT_out) {
+    return composite_pixel_flip(s, lst, n, px, py, C, T_out, n_contrib, n_eval, amb, rec, errT_out, -1);
+}
+static int composite_pixel_flip(const OrSplat2D *s, const int32_t *lst, int64_t n, double px, double py,
+                                double C[3], double *T_out, int32_t *n_contrib, int32_t *n_eval, uint8_t *amb,
+                                OrComp *rec, double *errT_out, int flip_at) {
+    int na = 0, flipped = 0;  /* ambiguous decisions met so far; whether flip_at was reached */
     const int64_t P = s->P;
     double T = 1.0, errT = 0.0;
     int nrec = 0;
@@ -363,14 +375,26 @@ static int composite_pixel(const OrSplat2D *s, const int32_t *lst, int64_t n, do
         }
         const double G = exp(power);
         const double araw = s->kappa[i] * G;
-        const double alpha = araw < OR_ALPHA_MAX ? araw : OR_ALPHA_MAX;
-        if (fabs(araw - OR_ALPHA_MIN) <= erel * araw) a |= 1;
-        if (fabs(araw - OR_ALPHA_MAX) <= erel * araw) a |= 2;
-        if (alpha < OR_ALPHA_MIN) continue;
+        int clamp = !(araw < OR_ALPHA_MAX);
+        if (fabs(araw - OR_ALPHA_MAX) <= erel * araw) {
+            a |= 2;
+            if (na++ == flip_at) { clamp = !clamp; flipped = 1; }
+        }
+        const double alpha = clamp ? OR_ALPHA_MAX : araw;
+        int skip = alpha < OR_ALPHA_MIN;
+        if (fabs(araw - OR_ALPHA_MIN) <= erel * araw) {
+            a |= 1;
+            if (na++ == flip_at) { skip = !skip; flipped = 1; }
+        }
+        if (skip) continue;
         const double Tn = T * (1.0 - alpha);
         const double errTn = errT + erel * alpha / (1.0 - alpha) + 2.4e-7;
-        if (fabs(Tn - OR_T_MIN) <= OR_T_MIN * (errTn + 1e-6 + g_amb_margin)) a |= 1;
-        if (Tn < OR_T_MIN) { ne = (int32_t)(k + 1); break; }
+        int stop = Tn < OR_T_MIN;
+        if (fabs(Tn - OR_T_MIN) <= OR_T_MIN * (errTn + 1e-6 + g_amb_margin)) {
+            a |= 1;
+            if (na++ == flip_at) { stop = !stop; flipped = 1; }
+        }
+        if (stop) { ne = (int32_t)(k + 1); break; }
         for (int ch = 0; ch < 3; ++ch) C[ch] += s->rgb[(int64_t)ch * P + i] * alpha * T;
         if (rec) {
             OrComp *r = &rec[nrec];
@@ -389,7 +413,40 @@ static int composite_pixel(const OrSplat2D *s, const int32_t *lst, int64_t n, do
     *n_contrib = last;
     *n_eval = ne;
     *amb = a;
+    if (flip_at >= 0 && !flipped) return -1;
     return nrec;
+}
+
+/* R18 both branches: for every pixel with amb != 0, alt[f] = the image when the f-th
+ * ambiguous decision of the pixel (list order) takes its other outcome, f < n_alt;
+ * NaN where the pixel has fewer than f + 1 such decisions (or amb == 0). */
+int or_render_fwd_alternatives(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets, const int32_t *list,
+                               const uint8_t *amb_in, int n_alt, double *alt) {
+    const int W = sc->width, H = sc->height;
+    const int64_t T = (int64_t)sc->tiles_x * sc->tiles_y, HW = (int64_t)W * H;
+    for (int64_t q = 0; q < (int64_t)n_alt * 3 * HW; ++q) alt[q] = NAN;
+#pragma omp parallel for schedule(dynamic, 2)
+    for (int64_t t = 0; t < T; ++t) {
+        const int tx = (int)(t % sc->tiles_x), ty = (int)(t / sc->tiles_x);
+        const int32_t *lst = list + offsets[t];
+        const int64_t n = offsets[t + 1] - offsets[t];
+        for (int yy = 0; yy < 16; ++yy)
+            for (int xx = 0; xx < 16; ++xx) {
+                const int px = tx * 16 + xx, py = ty * 16 + yy;
+                if (px >= W || py >= H) continue;
+                const int64_t pix = (int64_t)py * W + px;
+                if (!amb_in[pix]) continue;
+                for (int f = 0; f < n_alt; ++f) {
+                    double C[3], Tf;
+                    int32_t nc, ne;
+                    uint8_t am;
+                    if (composite_pixel_flip(s, lst, n, px + 0.5, py + 0.5, C, &Tf, &nc, &ne, &am, NULL, NULL, f) < 0)
+                        break;
+                    for (int ch = 0; ch < 3; ++ch) alt[((int64_t)f * 3 + ch) * HW + pix] = C[ch] + Tf * sc->bg[ch];
+                }
+            }
+    }
+    return 0;
 }
 
 int or_render_fwd(const OrScreen *sc, const OrSplat2D *s, const int64_t *offsets, const int32_t *list,

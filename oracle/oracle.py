@@ -357,6 +357,24 @@ def render_fwd(pre, cam, st: Settings, offsets, lst, tile_mask=None) -> dict:
     return {"image": img, "final_T": fT, "n_contrib": nc, "n_eval": ne, "n_comp": ncomp, "amb": amb}
 
 
+def render_fwd_alternatives(pre, cam, st: Settings, offsets, lst, amb, n_alt: int = 4) -> np.ndarray:
+    """R18, both branches: for every pixel the oracle flags (amb != 0),
+    alt[f] = the image when the f-th threshold-ambiguous decision of the pixel (in
+    list order: a 0.99 clamp, a 1/255 skip or a T < 1e-4 stop) takes its other
+    outcome, every other decision as usual; NaN where the pixel has no f-th such
+    decision.  An fp32 implementation may land on either side of any of them."""
+    H, W = cam.height, cam.width
+    keep = _Keep()
+    sp = _splat(pre, keep)
+    alt = np.zeros((n_alt, 3, H, W), np.float64)
+    lst = keep(np.ascontiguousarray(lst if lst.size else np.zeros(1, np.int32), dtype=np.int32))
+    amb = keep(np.ascontiguousarray(amb, dtype=np.uint8))
+    lib().or_render_fwd_alternatives(C.byref(_screen(cam, st)), C.byref(sp), _ptr(offsets, C.c_int64),
+                                     _ptr(lst, C.c_int32), _ptr(amb, C.c_uint8), C.c_int(int(n_alt)),
+                                     _ptr(alt, C.c_double))
+    return alt
+
+
 def render_bwd(pre, cam, st: Settings, offsets, lst, dL_dimg, tile_mask=None, with_abs: bool = False):
     """S5a: per-particle 2D gradients g2d [10][P] = (du, dv, da, db, dc, dkappa, dr, dg, db, dbeta);
     dbeta (the exact GEF kernel's direct shape term) is 0 for the phi-bar Gaussian kernel.

@@ -646,3 +646,37 @@ def test_definitional_lists_on_sampled_tiles_match_the_c_enumeration():
         got = lst[off[t]:off[t + 1]]
         want = full_lst[full_off[t]:full_off[t + 1]] if mask[t] else full_lst[:0]
         assert np.array_equal(got, want), t
+
+
+def test_r18_both_branches_skip_decision_closed_form():
+    """R18: a splat centred on a pixel centre (d = 0, G = 1, alpha = kappa)
+    with kappa = 1/255 to fp32 rounding puts the pixel's skip decision inside the fp32
+    error bound: the oracle flags the pixel, and its both-branch alternative is the
+    other outcome in closed form -- one of (image, alternative) is the background
+    (skipped) and the other kappa c + (1 - kappa) bg (composited); a pixel with no
+    ambiguous decision has no alternative (NaN)."""
+    cam = cam_identity(W=32, H=32, f=30.0)
+    bg = (0.1, 0.2, 0.3)
+    bgc = np.array([np.float32(c) for c in bg], np.float64)
+    z = 4.0
+    x = (16.5 - 16.0) * z / 30.0
+    kappa = 1.0 / 255.0
+    sh = np.array([[0.9], [-0.6], [0.1]])
+    f32 = lambda a: np.ascontiguousarray(np.asarray(a, np.float64), np.float32)
+    parts = gi.Particles(f32([[x], [x], [z]]), f32(np.full((3, 1), -2.5)), f32([[1.0], [0], [0], [0]]),
+                         f32([math.log(kappa / (1 - kappa))]), f32(sh), f32([2.0]), 0)
+    st = O.Settings(background=bg)
+    pre = O.preprocess(parts, cam, st, "f32")
+    offsets, lst = O.tile_lists(pre)
+    ref = O.render_fwd(pre, cam, st, offsets, lst)
+    assert ref["amb"][16, 16] != 0
+    alt = O.render_fwd_alternatives(pre, cam, st, offsets, lst, ref["amb"], n_alt=2)
+    k = float(pre["kappa"][0])
+    assert abs(k - kappa) < 1e-6 * kappa
+    c = pre["rgb"][:, 0].astype(np.float64)
+    composited, skipped = k * c + (1 - k) * bgc, bgc
+    pair = [ref["image"][:, 16, 16], alt[0][:, 16, 16]]
+    assert any(np.allclose(pair[i], composited, rtol=0, atol=1e-12) and np.allclose(pair[1 - i], skipped, rtol=0,
+                                                                                       atol=1e-12) for i in (0, 1))
+    assert np.isnan(alt[1][:, 16, 16]).all()          # one ambiguous decision only
+    assert np.isnan(alt[0][:, 0, 0]).all() and ref["amb"][0, 0] == 0   # unflagged pixel
