@@ -5,6 +5,8 @@
 #include <cmath>
 #include <cstring>
 
+#include <nvtx3/nvToolsExt.h>  // header-only: the ranges cost nothing without a tool attached
+
 #include "ges_internal.h"
 #include "ges_scan.cuh"
 
@@ -134,6 +136,12 @@ bool camera_ok(const ges_camera* c, const ges_frame* f) {
 
 ges_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GES_OK : GES_ERR_CUDA; }
 
+// NVTX range around each entry point (nsys / ncu --nvtx timelines by stage).
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
+
 }  // namespace
 }  // namespace ges
 
@@ -167,6 +175,7 @@ ges_status ges_frame_init(void* workspace, size_t bytes, int64_t P, int32_t widt
 
 ges_status ges_preprocess(const ges_particles* particles, const ges_camera* camera, const ges_settings* settings,
                           ges_frame* frame, void* stream) {
+    Nvtx nvtx_("ges_preprocess");
     if (!frame || !settings || !particles_ok(particles) || !camera_ok(camera, frame) || particles->P != frame->P ||
         !(settings->rho >= 0.0f) || (settings->phi_mode != GES_PHI_SCALE && settings->phi_mode != GES_PHI_VARIANCE) ||
         (settings->kernel != GES_KERNEL_PHI_GAUSS && settings->kernel != GES_KERNEL_EXACT_BETA))
@@ -197,6 +206,7 @@ ges_status ges_preprocess(const ges_particles* particles, const ges_camera* came
 }
 
 ges_status ges_sort(ges_frame* frame, void* stream) {
+    Nvtx nvtx_("ges_sort");
     if (!frame) return GES_ERR_INVALID_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long* ctr = (unsigned long long*)frame->counters;
@@ -235,6 +245,7 @@ ges_status ges_sort(ges_frame* frame, void* stream) {
 
 ges_status ges_render_fwd(ges_frame* frame, const ges_settings* settings, float* image, uint32_t* n_eval,
                           uint32_t* n_comp, void* stream) {
+    Nvtx nvtx_("ges_render_fwd");
     if (!frame || !settings || !image || !band_matches(settings, frame)) return GES_ERR_INVALID_ARG;
     RenderFwdArgs a;
     a.pay0 = (const float4*)frame->pay0; a.pay1 = (const float4*)frame->pay1; a.pay2 = frame->pay2;
@@ -250,6 +261,7 @@ ges_status ges_render_fwd(ges_frame* frame, const ges_settings* settings, float*
 
 ges_status ges_render_bwd_tiles(const ges_settings* settings, ges_frame* frame, const float* dL_dimage,
                                 void* stream) {
+    Nvtx nvtx_("ges_render_bwd_tiles");
     if (!frame || !settings || !dL_dimage || !band_matches(settings, frame)) return GES_ERR_INVALID_ARG;
     RenderBwdArgs b;
     b.pay0 = (const float4*)frame->pay0; b.pay1 = (const float4*)frame->pay1; b.pay2 = frame->pay2;
@@ -266,6 +278,7 @@ ges_status ges_render_bwd_tiles(const ges_settings* settings, ges_frame* frame, 
 ges_status ges_backward_particles(const ges_particles* particles, const ges_camera* camera,
                                   const ges_settings* settings, ges_frame* frame, const ges_grads* grads,
                                   void* stream) {
+    Nvtx nvtx_("ges_backward_particles");
     if (!frame || !settings || !grads || !particles_ok(particles) || !camera_ok(camera, frame) ||
         particles->P != frame->P || !grads->mean || !grads->log_scale || !grads->quat || !grads->opacity_logit ||
         !grads->sh || !grads->beta)
@@ -369,6 +382,7 @@ size_t ges_loss_workspace_bytes(int32_t width, int32_t height, float downsample)
 
 ges_status ges_loss_mask(const float* gt, int32_t width, int32_t height, float omega, const ges_loss_settings* settings,
                          void* workspace, size_t workspace_bytes, uint8_t* mask_lo, void* stream) {
+    Nvtx nvtx_("ges_loss_mask");
     if (!gt || !mask_lo || !workspace || width < 1 || height < 1 || !loss_settings_ok(settings) ||
         !(omega >= 0.0f && omega <= 1.0f))
         return GES_ERR_INVALID_ARG;
@@ -392,6 +406,7 @@ ges_status ges_loss_mask(const float* gt, int32_t width, int32_t height, float o
 ges_status ges_loss(const float* image, const float* gt, const uint8_t* mask_lo, int32_t width, int32_t height,
                     const ges_loss_settings* settings, void* workspace, size_t workspace_bytes, float* dL_dimage,
                     float* loss_out, void* stream) {
+    Nvtx nvtx_("ges_loss");
     if (!image || !gt || !workspace || !dL_dimage || !loss_out || width < 1 || height < 1 ||
         !loss_settings_ok(settings))
         return GES_ERR_INVALID_ARG;
@@ -429,6 +444,7 @@ double ges_lr_position(int64_t step, double init, double final_, double delay_mu
 
 ges_status ges_adam_step(float* params, const float* grads, float* m, float* v, int64_t P, int32_t sh_degree,
                          const ges_adam_settings* s, void* stream) {
+    Nvtx nvtx_("ges_adam_step");
     if (!params || !grads || !m || !v || !s || P < 1 || sh_degree < 0 || sh_degree > 3 || s->step < 1)
         return GES_ERR_INVALID_ARG;
     const int K = (sh_degree + 1) * (sh_degree + 1);
@@ -445,6 +461,7 @@ ges_status ges_adam_step(float* params, const float* grads, float* m, float* v, 
 ges_status ges_adam_step_range(float* params, const float* grads_range, float* m, float* v, int64_t P,
                                int32_t sh_degree, const ges_adam_settings* s, int64_t begin, int64_t count,
                                void* stream) {
+    Nvtx nvtx_("ges_adam_step_range");
     const int K = (sh_degree + 1) * (sh_degree + 1);
     if (!params || !grads_range || !m || !v || !s || P < 1 || sh_degree < 0 || sh_degree > 3 || s->step < 1 ||
         begin < 0 || count < 0 || begin + count > (int64_t)(12 + 3 * K) * P)
@@ -464,6 +481,7 @@ size_t ges_reorder_workspace_bytes(int64_t P) { return P < 1 ? 0 : reorder_works
 ges_status ges_reorder(const float* params, float* params_out, const float* m, float* m_out, const float* v,
                        float* v_out, int64_t P, int32_t sh_degree, uint32_t* perm_out, void* workspace, size_t bytes,
                        void* stream) {
+    Nvtx nvtx_("ges_reorder");
     if (!params || !params_out || !perm_out || !workspace || P < 1 || P > 0x7fffffff || sh_degree < 0 ||
         sh_degree > 3 || (!m != !m_out) || (!v != !v_out) || params == params_out || (m && m == m_out) ||
         (v && v == v_out))
@@ -485,6 +503,7 @@ ges_status ges_reset(float* params, int64_t P, int32_t sh_degree, int32_t what, 
 }
 
 ges_status ges_densify_stats(const ges_frame* frame, float* accum, float* count, void* stream) {
+    Nvtx nvtx_("ges_densify_stats");
     if (!frame || !accum || !count) return GES_ERR_INVALID_ARG;
     DensifyStatsArgs a;
     a.status = frame->status; a.grad2d = frame->grad2d; a.accum = accum; a.count = count;
@@ -502,6 +521,7 @@ ges_status ges_densify_prune(const float* params, const float* m, const float* v
                              const float* count, int64_t P, int32_t sh_degree, const ges_density_settings* s,
                              float* params_out, float* m_out, float* v_out, int64_t capacity_out, void* workspace,
                              size_t workspace_bytes, int64_t* P_out, void* stream) {
+    Nvtx nvtx_("ges_densify_prune");
     if (!params || !m || !v || !accum || !count || !s || !params_out || !m_out || !v_out || !workspace || !P_out ||
         P < 1 || sh_degree < 0 || sh_degree > 3 || capacity_out < 2 * P)
         return GES_ERR_INVALID_ARG;
@@ -582,6 +602,7 @@ ges_status ges_probe_mufu(float* out, int32_t iters, int32_t blocks, void* strea
 
 // ---- view-DP gradient compaction -----------------------------
 ges_status ges_mask_visible(const ges_frame* frame, uint8_t* mask, void* stream) {
+    Nvtx nvtx_("ges_mask_visible");
     if (!frame || !mask) return GES_ERR_INVALID_ARG;
     return cuda_status(launch_mask_visible(frame->status, frame->P, mask, (cudaStream_t)stream));
 }
@@ -593,6 +614,7 @@ size_t ges_grad_pack_workspace_bytes(int64_t P) {
 
 ges_status ges_grad_index(int64_t P, const uint8_t* mask, void* workspace, size_t workspace_bytes, int32_t* idx,
                           int64_t* U, void* stream) {
+    Nvtx nvtx_("ges_grad_index");
     if (P < 1 || P > 0x7fffffff || !mask || !workspace || !idx || !U) return GES_ERR_INVALID_ARG;
     if (workspace_bytes < ges_grad_pack_workspace_bytes(P)) return GES_ERR_CAPACITY;
     return cuda_status(launch_grad_index(P, mask, (int*)workspace, idx, (long long*)U, (cudaStream_t)stream));
@@ -600,12 +622,14 @@ ges_status ges_grad_index(int64_t P, const uint8_t* mask, void* workspace, size_
 
 ges_status ges_grad_pack(const float* grads, int64_t P, int32_t C, const int32_t* idx, const int64_t* U,
                          float* packed, void* stream) {
+    Nvtx nvtx_("ges_grad_pack");
     if (!grads || P < 1 || P > 0x7fffffff || C < 1 || !idx || !U || !packed) return GES_ERR_INVALID_ARG;
     return cuda_status(launch_grad_pack(grads, P, C, idx, (const long long*)U, packed, (cudaStream_t)stream));
 }
 
 ges_status ges_grad_unpack(const float* packed, int64_t P, int32_t C, const int32_t* idx, const int64_t* U,
                            float* grads, void* stream) {
+    Nvtx nvtx_("ges_grad_unpack");
     if (!packed || P < 1 || P > 0x7fffffff || C < 1 || !idx || !U || !grads) return GES_ERR_INVALID_ARG;
     return cuda_status(launch_grad_unpack(packed, P, C, idx, (const long long*)U, grads, (cudaStream_t)stream));
 }
