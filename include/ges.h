@@ -470,6 +470,11 @@ ges_status ges_mix_fit(const ges_mix_run *runs, int32_t n_runs, float *params, f
 ges_status ges_theorem1_errors(const float *alpha, int32_t na, const float *beta, int32_t nb, float A, float L,
                                int32_t intervals, float *E, void *stream);
 
+/* Failure detection (debug): *count (device uint64, accumulated --
+ * zero it first) += the number of NaN / Inf values among x[0, n) (device fp32: an
+ * image, a gradient buffer, the parameters).  No synchronisation. */
+ges_status ges_count_nonfinite(const float *x, int64_t n, uint64_t *count, void *stream);
+
 /* ---- view data parallelism: visible-union compaction of the gradient allreduce
  * (SURVEY.md §8(e)).  A particle no view of any rank saw has a zero gradient on
  * every rank, so only the union of the ranks' visible sets is reduced:

@@ -114,7 +114,8 @@ EXPORTS = ["ges_workspace_bytes", "ges_frame_init", "ges_frame_layout", "ges_pre
            "ges_loss", "ges_lr_position", "ges_adam_step", "ges_adam_step_range", "ges_reset", "ges_densify_stats",
            "ges_densify_workspace_bytes", "ges_densify_prune", "ges_mix_signal", "ges_mix_eval", "ges_mix_fit",
            "ges_theorem1_errors", "ges_probe_mufu", "ges_mask_visible", "ges_grad_pack_workspace_bytes",
-           "ges_grad_index", "ges_grad_pack", "ges_grad_unpack", "ges_reorder_workspace_bytes", "ges_reorder"]
+           "ges_grad_index", "ges_grad_pack", "ges_grad_unpack", "ges_reorder_workspace_bytes", "ges_reorder",
+           "ges_count_nonfinite"]
 
 _lib = None
 
@@ -208,6 +209,8 @@ def load(build_if_missing: bool = True) -> C.CDLL:
                                           C.c_int32, C.c_void_p, C.c_void_p]
         L.ges_mask_visible.restype = C.c_int
         L.ges_mask_visible.argtypes = [C.POINTER(ges_frame), C.c_void_p, C.c_void_p]
+        L.ges_count_nonfinite.restype = C.c_int
+        L.ges_count_nonfinite.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
         L.ges_grad_pack_workspace_bytes.restype = C.c_size_t
         L.ges_grad_pack_workspace_bytes.argtypes = [C.c_int64]
         L.ges_grad_index.restype = C.c_int

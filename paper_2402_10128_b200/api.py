@@ -389,6 +389,17 @@ class Adam:
                 "ges_adam_step")
 
 
+def count_nonfinite(*tensors: torch.Tensor, stream=None) -> torch.Tensor:
+    """Failure detection (debug): the number of NaN / Inf values in fp32 device tensors,
+    as a device int64 scalar (no synchronisation; `.item()` reads it)."""
+    out = torch.zeros(1, dtype=torch.int64, device=tensors[0].device if tensors else "cuda")
+    for t in tensors:
+        assert t.dtype == torch.float32 and t.is_contiguous() and t.is_cuda
+        L.check(L.load().ges_count_nonfinite(C.c_void_p(t.data_ptr()), t.numel(), C.c_void_p(out.data_ptr()),
+                                             C.c_void_p(_stream(stream))), "ges_count_nonfinite")
+    return out[0]
+
+
 def reorder(params: PlanarParams, opt: Optional["Adam"] = None, stream=None):
     """Particle storage order (ges_reorder): a new PlanarParams in the Morton order of
     the means, and perm (int32 [P], perm[j] = old index of new particle j).  With an

@@ -601,6 +601,12 @@ ges_status ges_probe_mufu(float* out, int32_t iters, int32_t blocks, void* strea
 }
 
 // ---- view-DP gradient compaction -----------------------------
+ges_status ges_count_nonfinite(const float* x, int64_t n, uint64_t* count, void* stream) {
+    if (!x || !count || n < 0) return GES_ERR_INVALID_ARG;
+    if (n == 0) return GES_OK;
+    return cuda_status(launch_count_nonfinite(x, n, (unsigned long long*)count, (cudaStream_t)stream));
+}
+
 ges_status ges_mask_visible(const ges_frame* frame, uint8_t* mask, void* stream) {
     Nvtx nvtx_("ges_mask_visible");
     if (!frame || !mask) return GES_ERR_INVALID_ARG;

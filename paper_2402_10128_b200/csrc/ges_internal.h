@@ -108,6 +108,7 @@ struct BinArgs {
     int64_t row_chunks, col_chunks;   // capacities of the look-back words
 };
 cudaError_t launch_bin(const BinArgs& a, cudaStream_t stream);
+cudaError_t launch_count_nonfinite(const float* x, int64_t n, unsigned long long* count, cudaStream_t stream);
 
 // --- render ----------------------------------------------------------------
 constexpr int kGrad2dStride = 12;  // floats per particle in grad2d (3 x float4)

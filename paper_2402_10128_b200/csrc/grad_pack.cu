@@ -11,6 +11,8 @@
 //   ges_grad_unpack    grads[c][idx[k]] = packed[c][k]
 // Rows of `packed` are U apart, U read from device memory by the kernels, so
 // nothing here synchronises; the host reads U once to size the allreduce.
+#include <algorithm>
+
 #include "ges_internal.h"
 
 namespace ges {
@@ -124,6 +126,22 @@ __global__ void gp_move_kernel(float* grads, int64_t P, const int* idx, const lo
 }
 
 int64_t grad_pack_blocks(int64_t P) { return (P + kGpBlock - 1) / kGpBlock; }
+
+// Failure detection: *count += the number of NaN / Inf values among x[0, n).
+__global__ void count_nonfinite_kernel(const float* x, int64_t n, unsigned long long* count) {
+    uint32_t c = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        c += !isfinite(__ldg(x + i));
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(count, (unsigned long long)c);
+}
+
+cudaError_t launch_count_nonfinite(const float* x, int64_t n, unsigned long long* count, cudaStream_t stream) {
+    const int64_t want = (n + 255) / 256;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)num_sms() * 8));
+    count_nonfinite_kernel<<<grid, 256, 0, stream>>>(x, n, count);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_mask_visible(const uint8_t* status, int64_t P, uint8_t* mask, cudaStream_t stream) {
     mask_visible_kernel<<<(unsigned)((P + 255) / 256), 256, 0, stream>>>(status, P, mask);

@@ -524,3 +524,20 @@ def test_mean2d_gradient(case):
     torch.cuda.synchronize()
     b = m2d.cpu().numpy().astype(np.float64)
     assert np.allclose(b, 2 * a, rtol=1e-4, atol=1e-6 * (1 + np.abs(a).max()))
+
+
+def test_count_nonfinite():
+    """Failure detection (ges_count_nonfinite): counts NaN and +-Inf exactly, 0 on a
+    rendered frame and its gradients; accumulates over several buffers."""
+    x = torch.randn(1000003, device="cuda")
+    assert int(G.count_nonfinite(x).item()) == 0
+    x[[0, 17, 999999]] = float("nan")
+    x[[5, 1000002]] = float("inf")
+    x[123] = -float("inf")
+    assert int(G.count_nonfinite(x).item()) == 6
+    assert int(G.count_nonfinite(x, x[:10].contiguous()).item()) == 8
+    sc = gi.make_config(0)
+    out = gpu_forward(sc.particles, sc.cameras[0], G.Settings())
+    _, grads = gpu_backward(out, sc.cameras[0], G.Settings(), gi.upstream_grad(1, 0, 256, 256))
+    img = torch.from_numpy(out["image"]).cuda()
+    assert int(G.count_nonfinite(img, grads.flat).item()) == 0
