@@ -1297,9 +1297,12 @@ def main():
                     help="particle storage order of our arm (DESIGN.md 'Particle order')")
     ap.add_argument("--definitional-tiles", type=int, default=16,
                     help="tiles of the oracle's definitional-mode sample in cpu_baseline (0: skip)")
+    ap.add_argument("--config", type=int, choices=[0, 1, 2, 3, 4], default=3,
+                    help="scene of the headline step (BASELINE.json's metric is quoted on config 3)")
     args = ap.parse_args()
-    global ORDER
+    global ORDER, WORKLOAD_CFG
     ORDER = args.order
+    WORKLOAD_CFG = args.config
     if args.impl == "reference":
         run_reference(args)
     else:
