@@ -172,3 +172,28 @@ def test_backward_determinism_max_ulp(cfg):
         assert np.all(np.abs(a.astype(np.float64) - b) <= bound + 1e-30)
     print(f"[determinism config {cfg}] forward bit-identical over {len(outs)} runs; backward max ulp diff "
           f"{max(report):.0f} (median over entries {float(np.median(_ulps(outs[0][3], outs[1][3]))):.1f})")
+
+
+def test_sort_protocols_repeatable_under_load():
+    """The sort's and binning's cross-CTA protocols (chunk tickets, published words,
+    two-level look-backs) give the same lists and ranges frame after frame: 200
+    back-to-back frames of config 3 (10 compared bit for bit with the first)."""
+    sc = gi.make_config(3)
+    cam = sc.cameras[0]
+    params = G.PlanarParams.from_inputs(sc.particles)
+    st = G.Settings(rho=sc.rho)
+    r = G.Renderer(params.P, cam.width, cam.height)
+    r.forward(params, cam, st)
+    r.grow(int(r.frame.counts().slots))
+    G.ges_preprocess(params, cam, st, r.frame)
+    G.ges_sort(r.frame)
+    torch.cuda.synchronize()
+    M = int(r.frame.counts().pairs)
+    ref_list, ref_rng = r.frame.list(M).clone(), r.frame.ranges().clone()
+    for it in range(200):
+        G.ges_preprocess(params, cam, st, r.frame)
+        G.ges_sort(r.frame)
+        if it % 20 == 19:
+            torch.cuda.synchronize()
+            assert int(r.frame.counts().pairs) == M
+            assert torch.equal(r.frame.list(M), ref_list) and torch.equal(r.frame.ranges(), ref_rng), it
