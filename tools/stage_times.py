@@ -17,8 +17,9 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=3)
 ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--tag", default="")
+ap.add_argument("--P", type=int, default=None, help="particle count override (config 3's distributions)")
 args = ap.parse_args()
-sc = gi.make_config(args.config)
+sc = gi.make_config(args.config, **({"P": args.P} if args.P else {}))
 cam = sc.cameras[0]
 params = G.PlanarParams.from_inputs(sc.particles)
 st = G.Settings(rho=sc.rho)
