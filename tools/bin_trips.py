@@ -1,3 +1,5 @@
+"""Binning emission-trip counts and direct-path chunks (needs a GES_BIN_STATS=1 build; run with
+GES_LIB=paper_2402_10128_b200/build/variants/stats/libges.so)."""
 import ctypes as C, os, sys
 sys.path.insert(0, os.getcwd())
 import torch

@@ -1,3 +1,5 @@
+"""Depth-sort rank-phase timings (needs a GES_DS_TIMING=3 build: python paper_2402_10128_b200/_build.py
+--variant dst3 -DGES_DS_TIMING=3 [-DGES_DS_TIMING_SHIFT=18]; run with GES_LIB=.../dst3/libges.so)."""
 import ctypes as C, os, sys
 sys.path.insert(0, os.getcwd())
 import numpy as np, torch
