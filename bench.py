@@ -447,6 +447,7 @@ def run_ours(args) -> None:
                "cfg4": time_view_batch(G, 4, dev, stream, min(args.steps, 10), rank, world)}
     small = time_small_configs(G, dev, stream, min(args.steps, 50)) if world == 1 else None
     union = time_union_compaction(G, scene, dev, stream, min(args.steps, 20)) if world == 1 else None
+    shfac = time_sh_factorized(G, scene, dev, stream, min(args.steps, 20)) if world == 1 else None
 
     # ---- algorithmic work for the roofline (SURVEY.md §8(d) units) ----
     n_comp = torch.zeros(W * H, dtype=torch.int32, device=dev)
@@ -513,6 +514,7 @@ def run_ours(args) -> None:
             "view_batch_iters": batches,
             "small_configs": small,
             "allreduce_union_compaction": union,
+            "allreduce_sh_factorized": shfac,
             "loss_front_end": loss_line,
             "vs_gaussian_equivalent": {"ges_fwd_ms": fwd_ms, "gaussian_fwd_ms": g_ms, "ratio": g_ms / fwd_ms,
                                        "note": "same footprints: log_scale + ln(phi-bar), gaussian_only=1"},
@@ -994,6 +996,44 @@ def time_union_compaction(G, scene, dev, stream, steps):
             "index_ms": a.elapsed_time(b) / steps, "pack_unpack_ms": b.elapsed_time(c) / steps,
             "used_when": "union <= 0.5 P (VisibleUnionReducer.max_union); above it the dense allreduce runs",
             "note": "view-DP allreduce of only the union of the ranks' visible particles (one host read of U)"}
+
+def time_sh_factorized(G, scene, dev, stream, steps):
+    """DESIGN.md §8 SH-factorised view-DP exchange, measured on one GPU: the device time of
+    ges_sh_grad_from_colour rebuilding the 3K SH planes from 8 views' dL/drgb (what every
+    rank runs after the all-gather at N = 8, one view per rank), and the bytes each rank
+    receives in the exchange against the dense allreduce's (NVLS: ~ the buffer once)."""
+    import torch
+    params = G.PlanarParams.from_inputs(scene.particles, device=dev)
+    P, C, K = params.P, params.flat.shape[0], scene.particles.K
+    cams = G.camera_rows(scene.cameras[:8], device=dev)
+    n = cams.shape[0]
+    st = G.Settings(rho=scene.rho)
+    r = G.Renderer(P, scene.cameras[0].width, scene.cameras[0].height, device=dev)
+    grads = G.PlanarParams.zeros(P, params.sh_degree, dev)
+    drgb = torch.zeros((n, 3, P), dtype=torch.float32, device=dev)
+    for v, c in enumerate(scene.cameras[:n]):    # real per-view colour gradients (sparsity as in training)
+        r.forward(params, c, st)
+        dLv = torch.randn((3, c.height, c.width), device=dev)
+        r.backward(params, c, st, dLv, grads=grads, accumulate=v > 0, drgb=drgb[v])
+    out = torch.empty_like(params.sh)
+    G.sh_grad_from_colour(params, cams, drgb, out=out, stream=stream)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    a, b = ev(), ev()
+    a.record(stream)
+    for _ in range(steps):
+        G.sh_grad_from_colour(params, cams, drgb, out=out, stream=stream)
+    b.record(stream)
+    b.synchronize()
+    err = float(((out - grads.sh).abs().max() / (grads.sh.abs().max() + 1e-30)).item())
+    ms = a.elapsed_time(b) / steps
+    kbytes = 12 * P + 12 * n * P + 4 * 3 * K * P
+    return {"views": n, "sh_from_colour_ms": ms, "sh_from_colour_gbs": kbytes / (ms / 1e3) / 1e9,
+            "max_rel_diff_vs_accumulated_sh": err,
+            "exchange_bytes_per_rank_dense": 4 * C * P,
+            "exchange_bytes_per_rank_factorized": 4 * (C - 3 * K) * P + 4 * 3 * (n - 1) * P,
+            "note": "N = 8, one view per rank: allreduce of the 12 non-SH planes + all-gather of the "
+                    "other 7 views' 3-float dL/drgb, then this kernel on every rank"}
+
 
 def time_loss_front_end(G, params, cam, st, frame, grads, image, flush, stream, steps, dev):
     """Eq. 9's loss on the bench frame (mask M_omega at omega = 0.75, L1 + SSIM + L_omega and

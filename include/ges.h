@@ -125,6 +125,10 @@ typedef struct {
     float *mean2d;          /* optional (NULL: not written): [2][P] dL/d(u, v), the gradient of
                                the projected mean in pixels (the view-space gradient of 3DGS's
                                densification; 0 for particles that are not visible) */
+    float *drgb;            /* optional (NULL: not written): [3][P] dL/d rgb of the view (0 for a
+                               clamped channel or a particle that is not visible): with the camera
+                               it determines this view's SH gradient (ges_sh_grad_from_colour);
+                               = or += with accumulate like every other output */
     int32_t accumulate;
     int32_t _pad;
 } ges_grads;
@@ -469,6 +473,16 @@ ges_status ges_mix_fit(const ges_mix_run *runs, int32_t n_runs, float *params, f
  * alpha or beta give NaN. */
 ges_status ges_theorem1_errors(const float *alpha, int32_t na, const float *beta, int32_t nb, float A, float L,
                                int32_t intervals, float *E, void *stream);
+
+/* View data parallelism, SH-factorised exchange: the SH gradient of a
+ * view is Y_k(u) dL/drgb per particle (u the unit direction from the view's camera
+ * centre to the mean), so ranks can exchange the 3-float dL/drgb of their views
+ * (ges_grads.drgb) instead of reducing the 3K SH planes.  g_sh [3K][P] (=, or += with
+ * accumulate) <- sum over the n views of Y_k(u_v) drgb[v][ch] (drgb: device [n][3][P];
+ * cams: device [n][12] = R (world -> camera, row-major 3x3) then t, as ges_camera;
+ * mean: device [3][P]). */
+ges_status ges_sh_grad_from_colour(const float *mean, int64_t P, int32_t sh_degree, const float *cams,
+                                   int32_t n_views, const float *drgb, float *g_sh, int32_t accumulate, void *stream);
 
 /* Failure detection (debug): *count (device uint64, accumulated --
  * zero it first) += the number of NaN / Inf values among x[0, n) (device fp32: an

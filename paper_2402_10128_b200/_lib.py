@@ -45,7 +45,8 @@ class ges_settings(C.Structure):
 
 
 class ges_grads(C.Structure):
-    _fields_ = [(n, C.c_void_p) for n in ("mean", "log_scale", "quat", "opacity_logit", "sh", "beta", "mean2d")] + [
+    _fields_ = [(n, C.c_void_p) for n in ("mean", "log_scale", "quat", "opacity_logit", "sh", "beta", "mean2d",
+                                          "drgb")] + [
         ("accumulate", C.c_int32), ("_pad", C.c_int32)]
 
 
@@ -115,7 +116,7 @@ EXPORTS = ["ges_workspace_bytes", "ges_frame_init", "ges_frame_layout", "ges_pre
            "ges_densify_workspace_bytes", "ges_densify_prune", "ges_mix_signal", "ges_mix_eval", "ges_mix_fit",
            "ges_theorem1_errors", "ges_probe_mufu", "ges_mask_visible", "ges_grad_pack_workspace_bytes",
            "ges_grad_index", "ges_grad_pack", "ges_grad_unpack", "ges_reorder_workspace_bytes", "ges_reorder",
-           "ges_count_nonfinite"]
+           "ges_count_nonfinite", "ges_sh_grad_from_colour"]
 
 _lib = None
 
@@ -211,6 +212,9 @@ def load(build_if_missing: bool = True) -> C.CDLL:
         L.ges_mask_visible.argtypes = [C.POINTER(ges_frame), C.c_void_p, C.c_void_p]
         L.ges_count_nonfinite.restype = C.c_int
         L.ges_count_nonfinite.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        L.ges_sh_grad_from_colour.restype = C.c_int
+        L.ges_sh_grad_from_colour.argtypes = [C.c_void_p, C.c_int64, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p,
+                                              C.c_void_p, C.c_int32, C.c_void_p]
         L.ges_grad_pack_workspace_bytes.restype = C.c_size_t
         L.ges_grad_pack_workspace_bytes.argtypes = [C.c_int64]
         L.ges_grad_index.restype = C.c_int

@@ -85,14 +85,19 @@ class PlanarParams:
             setattr(p, n, getattr(self, n).data_ptr())
         return p
 
-    def c_grads(self, accumulate: bool, mean2d: Optional[torch.Tensor] = None) -> L.ges_grads:
-        """mean2d (optional): a [2][P] fp32 device tensor for dL/d(u, v) (ges.h ges_grads)."""
+    def c_grads(self, accumulate: bool, mean2d: Optional[torch.Tensor] = None,
+                drgb: Optional[torch.Tensor] = None) -> L.ges_grads:
+        """mean2d (optional): a [2][P] fp32 device tensor for dL/d(u, v); drgb (optional): a
+        [3][P] one for the view's dL/d rgb (ges.h ges_grads)."""
         g = L.ges_grads()
         for n in PARAM_NAMES:
             setattr(g, n, getattr(self, n).data_ptr())
         if mean2d is not None:
             assert mean2d.dtype == torch.float32 and mean2d.is_contiguous() and mean2d.numel() == 2 * self.P
             g.mean2d = mean2d.data_ptr()
+        if drgb is not None:
+            assert drgb.dtype == torch.float32 and drgb.is_contiguous() and drgb.numel() == 3 * self.P
+            g.drgb = drgb.data_ptr()
         g.accumulate = 1 if accumulate else 0
         return g
 
@@ -209,9 +214,9 @@ def ges_render_fwd(frame: Frame, settings: Settings, image: torch.Tensor, n_eval
 
 def ges_render_bwd(particles: PlanarParams, camera, settings: Settings, frame: Frame, dL_dimage: torch.Tensor,
                    grads: PlanarParams, accumulate: bool = False, stream=None,
-                   mean2d: Optional[torch.Tensor] = None) -> None:
+                   mean2d: Optional[torch.Tensor] = None, drgb: Optional[torch.Tensor] = None) -> None:
     assert dL_dimage.dtype == torch.float32 and dL_dimage.is_contiguous()
-    p, c, s, g = particles.c_particles(), c_camera(camera), settings.c(), grads.c_grads(accumulate, mean2d)
+    p, c, s, g = particles.c_particles(), c_camera(camera), settings.c(), grads.c_grads(accumulate, mean2d, drgb)
     L.check(L.load().ges_render_bwd(C.byref(p), C.byref(c), C.byref(s), C.byref(frame.c),
                                     C.c_void_p(dL_dimage.data_ptr()), C.byref(g), C.c_void_p(_stream(stream))),
             "ges_render_bwd")
@@ -225,8 +230,9 @@ def ges_render_bwd_tiles(settings: Settings, frame: Frame, dL_dimage: torch.Tens
 
 
 def ges_backward_particles(particles: PlanarParams, camera, settings: Settings, frame: Frame, grads: PlanarParams,
-                           accumulate: bool = False, stream=None, mean2d: Optional[torch.Tensor] = None) -> None:
-    p, c, s, g = particles.c_particles(), c_camera(camera), settings.c(), grads.c_grads(accumulate, mean2d)
+                           accumulate: bool = False, stream=None, mean2d: Optional[torch.Tensor] = None,
+                           drgb: Optional[torch.Tensor] = None) -> None:
+    p, c, s, g = particles.c_particles(), c_camera(camera), settings.c(), grads.c_grads(accumulate, mean2d, drgb)
     L.check(L.load().ges_backward_particles(C.byref(p), C.byref(c), C.byref(s), C.byref(frame.c), C.byref(g),
                                             C.c_void_p(_stream(stream))), "ges_backward_particles")
 
@@ -261,10 +267,11 @@ class Renderer:
         raise L.GESError("pair capacity still exceeded after regrowing the frame twice")
 
     def backward(self, particles: PlanarParams, camera, settings: Settings, dL_dimage: torch.Tensor,
-                 grads: Optional[PlanarParams] = None, accumulate: bool = False, stream=None) -> PlanarParams:
+                 grads: Optional[PlanarParams] = None, accumulate: bool = False, stream=None,
+                 drgb: Optional[torch.Tensor] = None) -> PlanarParams:
         if grads is None:
             grads = PlanarParams.zeros(particles.P, particles.sh_degree, self.device)
-        ges_render_bwd(particles, camera, settings, self.frame, dL_dimage, grads, accumulate, stream)
+        ges_render_bwd(particles, camera, settings, self.frame, dL_dimage, grads, accumulate, stream, drgb=drgb)
         return grads
 
 
@@ -387,6 +394,29 @@ class Adam:
                                        C.c_void_p(self.m.flat.data_ptr()), C.c_void_p(self.v.flat.data_ptr()),
                                        params.P, params.sh_degree, C.byref(s), C.c_void_p(_stream(stream))),
                 "ges_adam_step")
+
+
+def camera_rows(cameras, device="cuda") -> torch.Tensor:
+    """[n][12] fp32 (R row-major, then t) of camera objects, as ges_sh_grad_from_colour takes them."""
+    rows = [[float(x) for x in list(c.R.reshape(9))] + [float(x) for x in list(c.t.reshape(3))] for c in cameras]
+    return torch.tensor(rows, dtype=torch.float32).reshape(len(rows), 12).to(device)
+
+
+def sh_grad_from_colour(params: PlanarParams, cams: torch.Tensor, drgb: torch.Tensor,
+                        out: Optional[torch.Tensor] = None, accumulate: bool = False, stream=None) -> torch.Tensor:
+    """The SH gradient [3K][P] of n views from their cameras (cams: [n][12], camera_rows) and
+    their per-view dL/d rgb (drgb: [n][3][P], ges_grads.drgb) -- ges_sh_grad_from_colour."""
+    n = cams.shape[0]
+    assert cams.dtype == torch.float32 and cams.is_contiguous() and cams.shape == (n, 12)
+    assert drgb.dtype == torch.float32 and drgb.is_contiguous() and drgb.numel() == 3 * n * params.P
+    if out is None:
+        out = torch.empty_like(params.sh)
+    assert out.dtype == torch.float32 and out.is_contiguous() and out.shape == params.sh.shape
+    L.check(L.load().ges_sh_grad_from_colour(C.c_void_p(params.mean.data_ptr()), params.P, params.sh_degree,
+                                             C.c_void_p(cams.data_ptr()), n, C.c_void_p(drgb.data_ptr()),
+                                             C.c_void_p(out.data_ptr()), 1 if accumulate else 0,
+                                             C.c_void_p(_stream(stream))), "ges_sh_grad_from_colour")
+    return out
 
 
 def count_nonfinite(*tensors: torch.Tensor, stream=None) -> torch.Tensor:

@@ -294,6 +294,7 @@ ges_status ges_backward_particles(const ges_particles* particles, const ges_came
     q.g_mean = grads->mean; q.g_log_scale = grads->log_scale; q.g_quat = grads->quat;
     q.g_opacity_logit = grads->opacity_logit; q.g_sh = grads->sh; q.g_beta = grads->beta;
     q.g_mean2d = grads->mean2d;
+    q.g_drgb = grads->drgb;
     q.accumulate = grads->accumulate;
     return cuda_status(launch_particle_bwd(q, (cudaStream_t)stream));
 }
@@ -601,6 +602,16 @@ ges_status ges_probe_mufu(float* out, int32_t iters, int32_t blocks, void* strea
 }
 
 // ---- view-DP gradient compaction -----------------------------
+ges_status ges_sh_grad_from_colour(const float* mean, int64_t P, int32_t sh_degree, const float* cams,
+                                   int32_t n_views, const float* drgb, float* g_sh, int32_t accumulate, void* stream) {
+    Nvtx nvtx_("ges_sh_grad_from_colour");
+    if (!mean || !g_sh || P < 1 || P > 0x7fffffff || sh_degree < 0 || sh_degree > 3 || n_views < 0 ||
+        (n_views > 0 && (!cams || !drgb)))
+        return GES_ERR_INVALID_ARG;
+    return cuda_status(launch_sh_from_colour(mean, P, sh_degree, cams, n_views, drgb, g_sh, accumulate ? 1 : 0,
+                                             (cudaStream_t)stream));
+}
+
 ges_status ges_count_nonfinite(const float* x, int64_t n, uint64_t* count, void* stream) {
     if (!x || !count || n < 0) return GES_ERR_INVALID_ARG;
     if (n == 0) return GES_OK;

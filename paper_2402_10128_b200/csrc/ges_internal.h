@@ -166,9 +166,12 @@ struct ParticleBwdArgs {
     float* grad2d;
     float *g_mean, *g_log_scale, *g_quat, *g_opacity_logit, *g_sh, *g_beta;
     float* g_mean2d;                  // optional [2][P] dL/d(u, v)
+    float* g_drgb;                    // optional [3][P] dL/d rgb (clamped channels 0)
     int accumulate;
 };
 cudaError_t launch_particle_bwd(const ParticleBwdArgs& a, cudaStream_t stream);
+cudaError_t launch_sh_from_colour(const float* mean, int64_t P, int sh_degree, const float* cams, int n_views,
+                                  const float* drgb, float* g_sh, int accumulate, cudaStream_t stream);
 
 // --- loss front end (loss.cu) ------------------------
 struct LossArgs {

@@ -264,6 +264,10 @@ __device__ __forceinline__ void particle_bwd_one(const ParticleBwdArgs& a, int i
         put(a.g_mean2d, 0, o_m2d[0]);
         put(a.g_mean2d, 1, o_m2d[1]);
     }
+    if (a.g_drgb) {  // the per-view colour gradient the SH gradient factors through
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) put(a.g_drgb, ch, drgb[ch]);
+    }
     // leave the 2-D record zeroed for the next backward (ges.h); every particle's
     // record is written so the 48-B records cover whole sectors
     float4* rec = reinterpret_cast<float4*>(a.grad2d) + (size_t)i * (kGrad2dStride / 4);
@@ -411,6 +415,68 @@ static bool pb_aligned(const ParticleBwdArgs& a) {
     auto al = [](const void* p) { return ((uintptr_t)p & 15u) == 0; };
     return (a.P % 4) == 0 && a.P >= kPbTile && al(a.mean) && al(a.log_scale) && al(a.quat) &&
            al(a.opacity_logit) && al(a.beta) && al(a.drgb_ddir) && al(a.grad2d) && al(a.status) && al(a.flags);
+}
+
+// SH gradient from per-view colour gradients (view DP): S5b's SH term is
+// dL/dsh[3k + ch] = Y_k(u_v) dL/drgb_v[ch] per view v (u_v the unit direction from
+// view v's camera centre to the mean), so the SH gradient of any set of views follows
+// from their 3-float dL/drgb and their cameras -- the same expressions S5b evaluates.
+struct ShFromColourArgs {
+    const float* mean;       // [3][P]
+    int P;
+    const float* cams;       // [n][12]: R (9, world -> camera, row-major), t (3)
+    int n_views;
+    const float* drgb;       // [n][3][P]
+    float* g_sh;             // [3K][P]
+    int accumulate;
+};
+
+template <int K>
+__global__ void __launch_bounds__(128) sh_from_colour_kernel(ShFromColourArgs a) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= a.P) return;
+    const int P = a.P;
+    const float m0 = __ldg(a.mean + i), m1 = __ldg(a.mean + P + i), m2 = __ldg(a.mean + 2 * P + i);
+    float acc[3 * K];
+#pragma unroll
+    for (int q = 0; q < 3 * K; ++q) acc[q] = 0.f;
+    for (int v = 0; v < a.n_views; ++v) {
+        const float* dv = a.drgb + (size_t)v * 3 * P + i;
+        const float r[3] = {__ldg(dv), __ldg(dv + P), __ldg(dv + 2 * P)};
+        if (r[0] == 0.f && r[1] == 0.f && r[2] == 0.f) continue;  // not visible in view v
+        CamParams cam;
+        for (int k = 0; k < 9; ++k) cam.R[k] = __ldg(a.cams + 12 * v + k);
+        for (int k = 0; k < 3; ++k) cam.t[k] = __ldg(a.cams + 12 * v + 9 + k);
+        cam.W = cam.H = 1; cam.fx = cam.fy = 1.f;
+        const CamDerived cd = derive_camera(cam);
+        const float d0 = m0 - cd.c0, d1 = m1 - cd.c1, d2 = m2 - cd.c2;
+        const float dn = sqrtf(d0 * d0 + d1 * d1 + d2 * d2), idn = 1.f / dn;
+        float Y[16];
+        sh_basis<K>(d0 * idn, d1 * idn, d2 * idn, Y);
+#pragma unroll
+        for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) acc[3 * k + ch] += Y[k] * r[ch];
+    }
+#pragma unroll
+    for (int q = 0; q < 3 * K; ++q) {
+        float* o = a.g_sh + (size_t)q * P + i;
+        *o = a.accumulate ? *o + acc[q] : acc[q];
+    }
+}
+
+cudaError_t launch_sh_from_colour(const float* mean, int64_t P, int sh_degree, const float* cams, int n_views,
+                                  const float* drgb, float* g_sh, int accumulate, cudaStream_t stream) {
+    ShFromColourArgs a{mean, (int)P, cams, n_views, drgb, g_sh, accumulate};
+    const unsigned grid = (unsigned)((P + 127) / 128);
+    switch (sh_degree) {
+        case 0: sh_from_colour_kernel<1><<<grid, 128, 0, stream>>>(a); break;
+        case 1: sh_from_colour_kernel<4><<<grid, 128, 0, stream>>>(a); break;
+        case 2: sh_from_colour_kernel<9><<<grid, 128, 0, stream>>>(a); break;
+        case 3: sh_from_colour_kernel<16><<<grid, 128, 0, stream>>>(a); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_particle_bwd(const ParticleBwdArgs& a, cudaStream_t stream) {

@@ -24,7 +24,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib as L
-from .api import Frame, PlanarParams, Renderer, Settings, _stream
+from .api import Frame, PlanarParams, Renderer, Settings, _stream, sh_grad_from_colour
 
 TILE = 16
 
@@ -48,6 +48,43 @@ def allreduce_grads(flat: torch.Tensor, group=None) -> torch.Tensor:
     """Sum the flat [C][P] gradient buffer over the group in place (one call)."""
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=group)
+    return flat
+
+
+def sh_rows(sh_degree: int):
+    """Rows of the planar [C][P] buffer holding the SH planes (mean 3, log-scale 3, quat 4,
+    logit 1, then the 3K SH planes, then beta)."""
+    K = (sh_degree + 1) ** 2
+    return 11, 11 + 3 * K
+
+
+def allreduce_grads_sh_factorized(flat: torch.Tensor, sh_degree: int, drgb: torch.Tensor, cams: torch.Tensor,
+                                  sh_from_colour, group=None) -> torch.Tensor:
+    """View-DP gradient exchange with the SH gradient factorised.  The SH
+    gradient of a view is Y_k(u_v) dL/drgb_v per particle (S5b's own expression), so
+    instead of reducing the 3K SH planes each rank all-gathers the 3-float dL/drgb of its
+    views (drgb [V][3][P], ges_grads.drgb) and their cameras (cams [V][12]), reduces only
+    the 12 non-SH planes, and rebuilds the SH planes of the summed gradient locally with
+    sh_from_colour(drgb_all [n][3][P], cams_all [n][12], out_sh [3K][P]) (the GPU path:
+    ges_sh_grad_from_colour; the same call on every rank, so the result is identical on
+    all of them).  Bytes per particle received per rank: 4 (12 + 3 V (N - 1)) instead of
+    the 4 (12 + 3K) of the full buffer's reduction (N ranks, V views each)."""
+    lo, hi = sh_rows(sh_degree)
+    C = flat.shape[0]
+    world = dist.get_world_size(group) if (dist.is_available() and dist.is_initialized()) else 1
+    rest = torch.cat([flat[:lo], flat[hi:]]) if world > 1 else None
+    if world > 1:
+        dist.all_reduce(rest, op=dist.ReduceOp.SUM, group=group)
+        flat[:lo].copy_(rest[:lo])
+        flat[hi:].copy_(rest[lo:])
+        d_all = torch.empty((world * drgb.shape[0],) + tuple(drgb.shape[1:]), dtype=drgb.dtype, device=drgb.device)
+        c_all = torch.empty((world * cams.shape[0], cams.shape[1]), dtype=cams.dtype, device=cams.device)
+        dist.all_gather_into_tensor(d_all, drgb.contiguous(), group=group)
+        dist.all_gather_into_tensor(c_all, cams.contiguous(), group=group)
+    else:
+        d_all, c_all = drgb, cams
+    sh_from_colour(d_all.contiguous(), c_all.contiguous(), flat[lo:hi])
+    assert flat.shape[0] == C
     return flat
 
 
@@ -217,12 +254,27 @@ class ViewDataParallel:
     allreduced parameter gradients of sum_v <dL/dimage_v, image_v>."""
 
     def __init__(self, params: PlanarParams, cameras: Sequence, settings: Settings, rank: int, world: int,
-                 device="cuda", group=None, compact: bool = False):
+                 device="cuda", group=None, compact: bool = False, sh_factorized: bool = False):
         self.params, self.cameras, self.settings = params, list(cameras), settings
+        if compact and sh_factorized:
+            raise ValueError("compact and sh_factorized are alternative exchanges")
         # compact: reduce only the union of the ranks' visible particles (VisibleUnionReducer)
         self.reducer = VisibleUnionReducer(params.P, params.flat.shape[0], device) if compact else None
         self.views = views_for_rank(len(self.cameras), rank, world)
         self.group = group
+        # sh_factorized: all-gather each view's dL/drgb and rebuild the SH planes
+        # (allreduce_grads_sh_factorized); every rank gathers the same number of view
+        # slots (the most any rank has), unused slots hold zeros and contribute nothing
+        self.drgb = self.cams = None
+        if sh_factorized:
+            n_slots = -(-len(self.cameras) // max(world, 1))
+            self.drgb = torch.zeros((n_slots, 3, params.P), dtype=torch.float32, device=device)
+            rows = torch.zeros((n_slots, 12), dtype=torch.float32)
+            rows[:, 0] = rows[:, 4] = rows[:, 8] = 1.0
+            for j, v in enumerate(self.views):
+                c = self.cameras[v]
+                rows[j] = torch.tensor([float(x) for x in list(c.R.reshape(9)) + list(c.t.reshape(3))])
+            self.cams = rows.to(device)
         cam0 = self.cameras[0]
         self.renderers = {}
         for v in self.views:
@@ -241,17 +293,21 @@ class ViewDataParallel:
         if stream is not None and cur is not None:
             stream.wait_stream(cur)  # inputs produced on the current stream
         first = True
-        if self.reducer is not None:
+        if self.reducer is not None or self.drgb is not None:
             with torch.cuda.stream(stream) if stream is not None else _nullctx():
-                self.reducer.reset()
-        for v in self.views:
+                if self.reducer is not None:
+                    self.reducer.reset()
+                else:
+                    self.drgb.zero_()
+        for j, v in enumerate(self.views):
             cam = self.cameras[v]
             r = self.renderers[(cam.width, cam.height)]
             self.images[v] = r.forward(self.params, cam, self.settings, stream=stream)
             if self.reducer is not None:
                 self.reducer.add_view(r.frame, stream)
             r.backward(self.params, cam, self.settings, dL_dimages[v], grads=self.grads,
-                       accumulate=not first, stream=stream)
+                       accumulate=not first, stream=stream,
+                       drgb=self.drgb[j] if self.drgb is not None else None)
             first = False
         if first:  # no views on this rank: contribute zeros
             with torch.cuda.stream(stream) if stream is not None else _nullctx():
@@ -260,6 +316,11 @@ class ViewDataParallel:
             cur.wait_stream(stream)  # the masks and gradients are complete before any collective
         if self.reducer is not None:
             self.reducer.allreduce(self.grads.flat, self.group)
+        elif self.drgb is not None:
+            p = self.params
+            allreduce_grads_sh_factorized(
+                self.grads.flat, p.sh_degree, self.drgb, self.cams,
+                lambda d, c, o: sh_grad_from_colour(p, c, d, out=o), self.group)
         else:
             allreduce_grads(self.grads.flat, self.group)
         if stream is not None and cur is not None:

@@ -355,3 +355,64 @@ def test_zero1_sharded_update_world2(sh_degree, P):
     begin0, c0, shard = gdist.shard_range(C * P, 0, world)
     begin1, c1, _ = gdist.shard_range(C * P, 1, world)
     assert begin0 == 0 and begin1 == shard and c0 + c1 == C * P
+
+
+# --------------------------------------------------------------------------
+# SH-factorised exchange: all-gather the per-view dL/drgb, reduce
+# the 12 non-SH planes, rebuild the SH planes locally
+# --------------------------------------------------------------------------
+SHF_DEG, SHF_P, SHF_V = 2, 37, 3   # 3 views per rank
+
+
+def _fake_sh_from_colour(d_all, c_all, out):
+    """A stand-in for ges_sh_grad_from_colour with the same linear structure:
+    out[3k + ch] = sum_v basis(c_v)[k] drgb_v[ch] (basis: a fixed function of the view's camera row)."""
+    K = out.shape[0] // 3
+    out.zero_()
+    for v in range(d_all.shape[0]):
+        basis = torch.cos(c_all[v, :K] * 3.0 + torch.arange(K, dtype=torch.float32))
+        for k in range(K):
+            out[3 * k:3 * k + 3] += basis[k] * d_all[v]
+
+
+def _shf_rank_data(rank):
+    g = torch.Generator().manual_seed(100 + rank)
+    C = 3 + 3 + 4 + 1 + 3 * (SHF_DEG + 1) ** 2 + 1
+    flat = torch.randn((C, SHF_P), generator=g)
+    drgb = torch.randn((SHF_V, 3, SHF_P), generator=g)
+    drgb[:, :, ::5] = 0.0                       # particles a view did not see
+    cams = torch.randn((SHF_V, 12), generator=g)
+    lo, hi = gdist.sh_rows(SHF_DEG)
+    _fake_sh_from_colour(drgb, cams, flat[lo:hi])   # the rank's own SH planes (what S5b accumulates)
+    return flat, drgb, cams
+
+
+def _shf_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        flat, drgb, cams = _shf_rank_data(rank)
+        dense = flat.clone()
+        dist.all_reduce(dense)
+        gdist.allreduce_grads_sh_factorized(flat, SHF_DEG, drgb, cams,
+                                            lambda d, c, o: _fake_sh_from_colour(d, c, o))
+        out[rank] = (flat.numpy().copy(), dense.numpy().copy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sh_factorized_exchange_world2():
+    """The factorised exchange gives every rank the dense allreduce's sum: non-SH planes
+    reduced, SH planes rebuilt from the gathered per-view colour gradients (sum order
+    differs: fp32 tolerance), bit-identical across the ranks."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_shf_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        got, dense = out[r]
+        assert np.allclose(got, dense, rtol=1e-5, atol=1e-5)
+    assert np.array_equal(out[0][0], out[1][0])
+    lo, hi = gdist.sh_rows(SHF_DEG)
+    assert (lo, hi) == (11, 11 + 27)

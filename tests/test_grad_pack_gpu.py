@@ -75,3 +75,25 @@ def test_view_data_parallel_compact_equals_dense_single_rank():
     # the float atomics of S5a reordering between the two runs
     floor = 1e-6 + 1e-6 * np.abs(a).max()
     assert np.all(np.abs(a - b) <= np.maximum(1e-4 * np.abs(a), floor))
+
+
+def test_view_data_parallel_sh_factorized_equals_dense_single_rank():
+    """ViewDataParallel(sh_factorized=True): the SH planes rebuilt from the views' dL/drgb
+    (ges_sh_grad_from_colour) and the untouched non-SH planes equal the dense step's
+    gradient; two steps in a row (the drgb slots are re-zeroed)."""
+    sc = gi.make_config(2, P=20000, n_views=3)
+    cams = [_zoomed(c) for c in sc.cameras]
+    params = G.PlanarParams.from_inputs(sc.particles)
+    st = G.Settings(rho=sc.rho)
+    dLs = {v: torch.from_numpy(gi.upstream_grad(sc.seed, v, c.width, c.height)).cuda() for v, c in enumerate(cams)}
+    dense = gdist.ViewDataParallel(params, cams, st, 0, 1).step(dLs).flat.clone()
+    vdp = gdist.ViewDataParallel(params, cams, st, 0, 1, sh_factorized=True)
+    assert vdp.drgb.shape == (3, 3, params.P)
+    for _ in range(2):
+        fac = vdp.step(dLs).flat.clone()
+        torch.cuda.synchronize()
+        a, b = dense.cpu().numpy(), fac.cpu().numpy()
+        floor = 1e-6 + 1e-6 * np.abs(a).max()
+        assert np.all(np.abs(a - b) <= np.maximum(1e-4 * np.abs(a), floor))
+    with pytest.raises(ValueError):
+        gdist.ViewDataParallel(params, cams, st, 0, 1, compact=True, sh_factorized=True)

@@ -6,12 +6,15 @@ same seeded inputs.  Bars (BASELINE.json north_star):
   * gradients: |g_gpu - g_ref| <= max(1e-3 |g_ref|, 1e-6), except particles
     touching an ambiguous pixel (reported, bounded in number).
 """
+import ctypes as C
+
 import numpy as np
 import pytest
 import torch
 
 import ges_inputs as gi
 import paper_2402_10128_b200 as G
+from paper_2402_10128_b200 import _lib as L
 from oracle import oracle as O
 
 from gpu_helpers import (check_grads, gpu_backward, gpu_forward, gpu_keys, masked_upstream, oracle_grads,
@@ -541,3 +544,50 @@ def test_count_nonfinite():
     _, grads = gpu_backward(out, sc.cameras[0], G.Settings(), gi.upstream_grad(1, 0, 256, 256))
     img = torch.from_numpy(out["image"]).cuda()
     assert int(G.count_nonfinite(img, grads.flat).item()) == 0
+
+
+def test_sh_grad_from_colour_matches_accumulated_sh():
+    """SH-factorised view exchange: the SH gradient rebuilt from the
+    per-view dL/drgb (ges_grads.drgb) and the cameras by ges_sh_grad_from_colour equals
+    the SH planes S5b accumulates over the same views (same per-view products, the sum
+    order may differ by one rounding: rtol 1e-5 of the summed magnitudes).  A single
+    view in overwrite mode agrees to the same bound; invalid arguments are rejected."""
+    sc = gi.make_config(2, P=30000, n_views=4)
+    gs = G.Settings()
+    dev = G.PlanarParams.from_inputs(sc.particles)
+    P, V = dev.P, len(sc.cameras)
+    r = G.Renderer(P, sc.cameras[0].width, sc.cameras[0].height)
+    grads = G.PlanarParams.zeros(P, dev.sh_degree)
+    drgb = torch.zeros((V, 3, P), device="cuda")
+    one_sh = []
+    for v, cam in enumerate(sc.cameras):
+        r.forward(dev, cam, gs)
+        dL = torch.from_numpy(np.ascontiguousarray(gi.upstream_grad(sc.seed, v, cam.width, cam.height),
+                                                   np.float32)).cuda()
+        G.ges_render_bwd(dev, cam, gs, r.frame, dL, grads, accumulate=v > 0, drgb=drgb[v])
+        if v == 0:
+            one_sh.append(grads.sh.clone())
+    cams = G.camera_rows(sc.cameras)
+    torch.cuda.synchronize()
+    assert int((drgb.abs().sum(dim=1) > 0).sum().item()) > 0.1 * P * V
+    rebuilt = G.sh_grad_from_colour(dev, cams, drgb)
+    torch.cuda.synchronize()
+    # magnitude of the sum's terms: |Y_k| <= 1.1 at degree 3 -> bound by sum_v |drgb_v|
+    mag = drgb.abs().sum(dim=0).repeat(dev.sh.shape[0] // 3, 1)
+    assert torch.all((rebuilt - grads.sh).abs() <= 1e-5 * mag + 1e-12), float((rebuilt - grads.sh).abs().max())
+    one = G.sh_grad_from_colour(dev, cams[:1].contiguous(), drgb[:1].contiguous())
+    torch.cuda.synchronize()
+    assert torch.all((one - one_sh[0]).abs() <= 1e-6 * mag + 1e-12)
+    # accumulate adds; zero views leave an overwrite at 0
+    acc = rebuilt.clone()
+    G.sh_grad_from_colour(dev, cams, drgb, out=acc, accumulate=True)
+    assert torch.allclose(acc, 2 * rebuilt, rtol=1e-6, atol=0)
+    z = G.sh_grad_from_colour(dev, cams[:0].contiguous(), drgb[:0].contiguous())
+    assert int((z != 0).sum().item()) == 0
+    lib = L.load()
+    st = lib.ges_sh_grad_from_colour(C.c_void_p(dev.mean.data_ptr()), P, 4, C.c_void_p(cams.data_ptr()), V,
+                                     C.c_void_p(drgb.data_ptr()), C.c_void_p(rebuilt.data_ptr()), 0, None)
+    assert st == L.GES_ERR_INVALID_ARG
+    st = lib.ges_sh_grad_from_colour(C.c_void_p(dev.mean.data_ptr()), P, 3, None, V,
+                                     C.c_void_p(drgb.data_ptr()), C.c_void_p(rebuilt.data_ptr()), 0, None)
+    assert st == L.GES_ERR_INVALID_ARG
