@@ -203,6 +203,8 @@ typedef struct {
                               (particle, x0 | (x1-1) << 8)                            */
     uint32_t *tile_count;  /* [T] pairs per tile (zeroed per frame)                   */
     uint32_t *row_pairs;   /* [tiles_y] pairs per band row (zeroed per frame)         */
+    uint32_t *tile_bucket; /* [64] tiles per backward-cost bucket, appended by S4 (zeroed
+                              per frame; see tile_order)                             */
     uint32_t *lb_rows;     /* [2][row_chunks][tiles_y] published chunk / group words of
                               the row binning (zeroed per frame)                      */
     uint32_t *lb_cols;     /* [2][col_chunks][tiles_x] published words of the column
@@ -218,6 +220,14 @@ typedef struct {
     /* ---- S4 / S5 ---- */
     float *final_T;        /* [H*W] transmittance after the last composited particle   */
     uint32_t *n_contrib;   /* [H*W] list position of the last composited particle + 1  */
+    uint32_t *tile_order;  /* [64][T] S5a launch order: S4 appends each tile to the bucket
+                              of its backward cost (the longest backward walk: the tile's
+                              largest n_contrib, on a 4-per-octave log scale); S5a's
+                              CTA b takes the b-th tile of the
+                              buckets in descending cost (costliest first: a shorter tail),
+                              or tile b when the buckets do not hold exactly T tiles
+                              (S4 run twice on one frame).  Only an order: any permutation
+                              gives the same sums up to float atomics order             */
     float *grad2d;         /* [P][12] per-particle S5a record: raw moments over the
                               particle's composited pixels (dx = u - px, dy = v - py),
                               (sum m dx, sum m dy, sum m dx^2, sum m dx dy |

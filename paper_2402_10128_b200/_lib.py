@@ -67,11 +67,11 @@ class ges_frame(C.Structure):
         ("drgb_ddir", C.c_void_p),
         ("vis_key", C.c_void_p * 2), ("vis_val", C.c_void_p * 2), ("sorted_vis", C.c_void_p),
         ("radix_hist", C.c_void_p), ("items", C.c_void_p), ("row_count", C.c_void_p), ("rowlist", C.c_void_p),
-        ("tile_count", C.c_void_p), ("row_pairs", C.c_void_p), ("lb_rows", C.c_void_p), ("lb_cols", C.c_void_p),
+        ("tile_count", C.c_void_p), ("row_pairs", C.c_void_p), ("tile_bucket", C.c_void_p), ("lb_rows", C.c_void_p), ("lb_cols", C.c_void_p),
         ("col_excl", C.c_void_p), ("row_chunks", C.c_int64), ("col_chunks", C.c_int64),
         ("list", C.c_void_p), ("ranges", C.c_void_p),
         ("counters", C.c_void_p), ("zero_bytes", C.c_size_t),
-        ("final_T", C.c_void_p), ("n_contrib", C.c_void_p), ("grad2d", C.c_void_p),
+        ("final_T", C.c_void_p), ("n_contrib", C.c_void_p), ("tile_order", C.c_void_p), ("grad2d", C.c_void_p),
         ("workspace_bytes", C.c_size_t),
     ]
 

@@ -126,10 +126,10 @@ class Frame:
     """One frame workspace (a single torch uint8 allocation) and its C struct."""
 
     # the frame's sub-arrays in carving order (ges.h ges_frame_layout)
-    LAYOUT = ("counters", "row_count", "tile_count", "row_pairs", "lb_rows", "lb_cols", "depth", "pay0", "pay1",
-              "pay2", "pay3", "radius", "rect", "status", "flags", "drgb_ddir", "vis_key0", "vis_val0", "vis_key1",
-              "vis_val1", "sorted_vis", "radix_hist", "items", "rowlist", "col_excl", "list", "ranges", "final_T",
-              "n_contrib", "grad2d")
+    LAYOUT = ("counters", "row_count", "tile_count", "row_pairs", "tile_bucket", "lb_rows", "lb_cols", "depth",
+              "pay0", "pay1", "pay2", "pay3", "radius", "rect", "status", "flags", "drgb_ddir", "vis_key0",
+              "vis_val0", "vis_key1", "vis_val1", "sorted_vis", "radix_hist", "items", "rowlist", "col_excl", "list",
+              "ranges", "final_T", "n_contrib", "tile_order", "grad2d")
 
     def __init__(self, P: int, width: int, height: int, pair_capacity: int, device="cuda",
                  poison: Optional[int] = None, guard: int = 0):

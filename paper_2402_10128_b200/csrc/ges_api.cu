@@ -65,6 +65,7 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     g.row_count = (uint32_t*)take(sizeof(uint32_t) * ty);
     g.tile_count = (uint32_t*)take(sizeof(uint32_t) * (size_t)T);
     g.row_pairs = (uint32_t*)take(sizeof(uint32_t) * ty);
+    g.tile_bucket = (uint32_t*)take(sizeof(uint32_t) * kTileBuckets);
     g.lb_rows = (uint32_t*)take(sizeof(uint32_t) * 2 * (size_t)g.row_chunks * ty);
     g.lb_cols = (uint32_t*)take(sizeof(uint32_t) * 2 * (size_t)g.col_chunks * tx);
     g.zero_bytes = off;  // bytes of the zero region from the workspace base
@@ -94,6 +95,7 @@ size_t layout(char* base, int64_t P, int32_t W, int32_t H, int64_t cap, ges_fram
     g.ranges = (uint32_t*)take(sizeof(uint32_t) * (size_t)(T + 1));
     g.final_T = (float*)take(sizeof(float) * HW);
     g.n_contrib = (uint32_t*)take(sizeof(uint32_t) * HW);
+    g.tile_order = (uint32_t*)take(sizeof(uint32_t) * kTileBuckets * (size_t)T);
     g.grad2d = (float*)take(sizeof(float) * kGrad2dStride * (size_t)P);
     g.workspace_bytes = off;
     if (n_extents) *n_extents = ne;
@@ -256,6 +258,7 @@ ges_status ges_render_fwd(ges_frame* frame, const ges_settings* settings, float*
     for (int k = 0; k < 3; ++k) a.bg[k] = settings->background[k];
     a.image = image; a.final_T = frame->final_T; a.n_contrib = frame->n_contrib; a.n_eval = n_eval;
     a.n_comp = n_comp;
+    a.tile_bucket = frame->tile_bucket; a.tile_order = frame->tile_order;
     return cuda_status(launch_render_fwd(a, (cudaStream_t)stream));
 }
 
@@ -272,6 +275,7 @@ ges_status ges_render_bwd_tiles(const ges_settings* settings, ges_frame* frame, 
     for (int k = 0; k < 3; ++k) b.bg[k] = settings->background[k];
     b.final_T = frame->final_T; b.n_contrib = frame->n_contrib; b.dL_dimage = dL_dimage; b.grad2d = frame->grad2d;
     b.P = (int)frame->P;
+    b.tile_bucket = frame->tile_bucket; b.tile_order = frame->tile_order;
     return cuda_status(launch_render_bwd(b, (cudaStream_t)stream));
 }
 

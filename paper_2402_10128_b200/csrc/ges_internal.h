@@ -87,6 +87,7 @@ cudaError_t launch_reorder(const float* const* in, float* const* out, int n_buff
 #define GES_ROW_CHUNK 2048
 #endif
 constexpr int kRowChunk = GES_ROW_CHUNK;  // items per row-binning CTA
+constexpr int kTileBuckets = 64;          // S5a launch-order cost buckets (ges_frame.tile_order)
 #ifndef GES_COL_CHUNK
 #define GES_COL_CHUNK 3072
 #endif
@@ -129,6 +130,8 @@ struct RenderFwdArgs {
     uint32_t* n_contrib;
     uint32_t* n_eval;
     uint32_t* n_comp;
+    uint32_t* tile_bucket;            // [kTileBuckets] (ges_frame.tile_order)
+    uint32_t* tile_order;             // [kTileBuckets][gridDim]
 };
 cudaError_t launch_render_fwd(const RenderFwdArgs& a, cudaStream_t stream);
 
@@ -150,6 +153,9 @@ struct RenderBwdArgs {
     float* grad2d;  // [P][12]: du, dv, dA, dB | dC (pre-scaled conic), dkappa, dr, dg | db, dbeta*, 0, 0
                     // (* exact kernel: Eq. 2's direct dL/dbeta)
     int P;
+    const uint32_t* tile_bucket;      // S4's cost buckets: launch the costliest tiles first
+    const uint32_t* tile_order;
+    int use_order;
 };
 cudaError_t launch_render_bwd(const RenderBwdArgs& a, cudaStream_t stream);
 

@@ -30,6 +30,35 @@
 
 namespace ges {
 
+#ifdef GES_TILE_CLOCK
+// Debug (GES_TILE_CLOCK builds only): per tile, the first warp start and the last warp
+// end (%globaltimer ns) and the SM of the forward [0] and backward [1] kernels.
+__device__ unsigned long long g_tile_clk[2][16384][3];
+// and an optional launch order (block -> tile) per kernel, to measure schedules
+__device__ int g_tile_order[2][16384];
+__device__ int g_tile_order_on[2];
+struct TileClock {
+    unsigned long long* rec;
+    __device__ explicit TileClock(int which) {
+        rec = g_tile_clk[which][(g_tile_order_on[which] ? g_tile_order[which][blockIdx.x] : blockIdx.x) & 16383];
+        unsigned long long t, sm;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(*(unsigned*)&sm));
+        if ((threadIdx.x & 31) == 0) { atomicMin(rec, t); rec[2] = sm & 0xffffffffull; }
+    }
+    __device__ ~TileClock() {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if ((threadIdx.x & 31) == 0) atomicMax(rec + 1, t);
+    }
+};
+#define GES_CLOCK(which) TileClock tile_clock_(which)
+#define GES_TILE(which) (g_tile_order_on[which] ? g_tile_order[which][blockIdx.x] : (int)blockIdx.x)
+#else
+#define GES_CLOCK(which)
+#define GES_TILE(which) ((int)blockIdx.x)
+#endif
+
 #ifndef GES_BATCH
 #define GES_BATCH 256
 #endif
@@ -238,6 +267,44 @@ __device__ __forceinline__ void tile_origin(int tile, int tiles_x, int band_begi
     y0 = (band_begin + (tile / tiles_x) * band_step) * kTile;
 }
 
+// Bucket of a backward tile cost on a log scale, 4 buckets per octave (exact below 4),
+// saturating at kTileBuckets - 1.
+__device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
+    if (c < 4u) return c;
+    const int e = 31 - __clz(c);
+    return min((uint32_t)(kTileBuckets - 1), 4u * (uint32_t)(e - 1) + ((c >> (e - 2)) & 3u));
+}
+
+// S5a: the tile of CTA b in descending cost order (the forward's buckets), or b itself
+// when the buckets do not hold exactly gridDim.x tiles.  Every warp computes it.
+__device__ __forceinline__ int ordered_tile(const uint32_t* bucket, const uint32_t* order) {
+    static_assert(kTileBuckets == 64, "two buckets per lane");
+    const int lane = threadIdx.x & 31;
+    const uint32_t b = blockIdx.x, T = gridDim.x;
+    // lane l holds buckets 63 - l (first half) and 31 - l (second half): descending cost
+    const uint32_t c0 = bucket[63 - lane], c1 = bucket[31 - lane];
+    uint32_t i0 = c0, i1 = c1;  // inclusive scans of each half
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t x0 = __shfl_up_sync(0xffffffffu, i0, d), x1 = __shfl_up_sync(0xffffffffu, i1, d);
+        if (lane >= d) { i0 += x0; i1 += x1; }
+    }
+    const uint32_t h0 = __shfl_sync(0xffffffffu, i0, 31);
+    if (h0 + __shfl_sync(0xffffffffu, i1, 31) != T) return (int)b;
+    const unsigned m0 = __ballot_sync(0xffffffffu, i0 > b);
+    int q;
+    uint32_t excl;
+    if (m0) {
+        q = __ffs(m0) - 1;
+        excl = __shfl_sync(0xffffffffu, i0 - c0, q);
+        return (int)__ldg(order + (size_t)(63 - q) * T + (b - excl));
+    }
+    const unsigned m1 = __ballot_sync(0xffffffffu, h0 + i1 > b);
+    q = __ffs(m1) - 1;
+    excl = h0 + __shfl_sync(0xffffffffu, i1 - c1, q);
+    return (int)__ldg(order + (size_t)(31 - q) * T + (b - excl));
+}
+
 template <int PPT>
 __device__ __forceinline__ void pixel_base(int tile_x0, int tile_y0, int tid, int& px, int& py0) {
     const int warp = tid >> 5, lane = tid & 31;
@@ -300,6 +367,7 @@ struct RenderSmem {
     uint32_t ids[2][kBatch];  // list ids of this and the next batch
     uint8_t mask[kBatch];
     uint32_t max;
+    uint32_t wmax[Layout<PPT>::kWarps];  // forward: each warp's largest n_contrib (tile cost)
     static constexpr int kG1 = kBatch * 16, kB = kBatch * 32, kPid = kBatch * 36, kHb = kBatch * 40;
 };
 
@@ -308,9 +376,10 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
     using Lt = Layout<PPT>;
     using Sm = RenderSmem<PPT, EXACT>;
     __shared__ Sm S;
+    GES_CLOCK(0);
     static_assert(offsetof(Sm, g1) == Sm::kG1 && offsetof(Sm, b) == Sm::kB && offsetof(Sm, pid) == Sm::kPid &&
                   offsetof(Sm, hb) == Sm::kHb, "smem layout");
-    const int tile = blockIdx.x;
+    const int tile = GES_TILE(0);
     const int tid = threadIdx.x, warp = tid >> 5;
     int px, py0;
     int tile_x0, tile_y0;
@@ -409,6 +478,25 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
         }
     }
     wait_ids();  // no copy into shared memory outlives the CTA
+    {
+        // S5a's launch order (ges_frame.tile_order): a backward CTA lasts as long as its
+        // longer walk, so the tile's cost is its largest n_contrib (measured against the
+        // sum over the two backward warp regions and the list length: tools/tile_clock.py)
+        uint32_t m = 0;
+#pragma unroll
+        for (int k = 0; k < PPT; ++k) m = max(m, last[k]);
+        m = __reduce_max_sync(0xffffffffu, m);
+        if ((tid & 31) == 0) S.wmax[warp] = m;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t c = 0u;
+#pragma unroll
+            for (int w = 0; w < Lt::kWarps; ++w) c = max(c, S.wmax[w]);
+            const uint32_t b = cost_bucket(c);
+            const uint32_t slot = atomicAdd(a.tile_bucket + b, 1u);
+            a.tile_order[(size_t)b * gridDim.x + slot] = (uint32_t)tile;
+        }
+    }
     const int plane = a.W * a.H;
 #pragma unroll
     for (int k = 0; k < PPT; ++k) {
@@ -527,7 +615,12 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads, PPT) render_bwd_kernel(Render
     using Lt = Layout<PPT>;
     using Sm = RenderSmem<PPT, EXACT>;
     __shared__ Sm S;
-    const int tile = blockIdx.x;
+    GES_CLOCK(1);
+#ifdef GES_TILE_CLOCK
+    const int tile = g_tile_order_on[1] ? GES_TILE(1) : (a.use_order ? ordered_tile(a.tile_bucket, a.tile_order) : (int)blockIdx.x);
+#else
+    const int tile = a.use_order ? ordered_tile(a.tile_bucket, a.tile_order) : (int)blockIdx.x;
+#endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int px, py0;
     int tile_x0, tile_y0;
@@ -726,8 +819,15 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads, PPT) render_bwd_kernel(Render
     }
 }
 
-cudaError_t launch_render_bwd(const RenderBwdArgs& a, cudaStream_t stream) {
+cudaError_t launch_render_bwd(const RenderBwdArgs& args, cudaStream_t stream) {
     static const int ppt = ppt_from_env("GES_PPT_BWD", 4);
+    // experiment knob: GES_BWD_ORDER=0 launches the tiles in index order
+    static const int use_order = [] {
+        const char* e = getenv("GES_BWD_ORDER");
+        return e ? atoi(e) : 1;
+    }();
+    RenderBwdArgs a = args;
+    a.use_order = use_order && a.tile_bucket && a.tile_order;
     const int grid = a.tiles_x * a.tiles_y;
     if (grid == 0) return cudaSuccess;  // a band without tile rows: no 2-D gradients
     if (a.exact) {
@@ -745,3 +845,21 @@ cudaError_t launch_render_bwd(const RenderBwdArgs& a, cudaStream_t stream) {
 }
 
 }  // namespace ges
+
+#ifdef GES_TILE_CLOCK
+extern "C" void ges_debug_tile_order(int which, const int* order, int n) {  // n = 0: off
+    int on = n > 0;
+    if (on) cudaMemcpyToSymbol(ges::g_tile_order, order, sizeof(int) * n, sizeof(int) * 16384 * which);
+    cudaMemcpyToSymbol(ges::g_tile_order_on, &on, sizeof(int), sizeof(int) * which);
+}
+extern "C" void ges_debug_tile_clock(unsigned long long* out, int reset) {
+    if (reset) {
+        static unsigned long long init[2][16384][3];
+        for (int w = 0; w < 2; ++w)
+            for (int i = 0; i < 16384; ++i) { init[w][i][0] = ~0ull; init[w][i][1] = 0; init[w][i][2] = 0; }
+        cudaMemcpyToSymbol(ges::g_tile_clk, init, sizeof(init));
+    } else {
+        cudaMemcpyFromSymbol(out, ges::g_tile_clk, sizeof(unsigned long long) * 2 * 16384 * 3);
+    }
+}
+#endif

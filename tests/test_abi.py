@@ -69,8 +69,8 @@ def test_workspace_and_frame_carving_host_only():
     assert f.workspace_bytes == nbytes
     ptrs = [f.depth, f.pay0, f.pay1, f.pay2, f.pay3, f.radius, f.rect, f.status, f.flags, f.drgb_ddir, f.vis_key[0], f.vis_key[1],
             f.vis_val[0], f.vis_val[1], f.radix_hist, f.items, f.row_count, f.rowlist, f.tile_count, f.row_pairs,
-            f.lb_rows, f.lb_cols, f.col_excl, f.list, f.ranges, f.counters,
-            f.final_T, f.n_contrib, f.grad2d]
+            f.lb_rows, f.lb_cols, f.col_excl, f.list, f.ranges, f.counters, f.tile_bucket,
+            f.final_T, f.n_contrib, f.tile_order, f.grad2d]
     assert all(base <= p < base + nbytes and p % 256 == 0 for p in ptrs)
     assert len(set(ptrs)) == len(ptrs)
     # errors
@@ -94,15 +94,18 @@ def test_workspace_and_frame_carving_host_only():
     assert all(o % 256 == 0 for o, _ in pairs)
     assert all(o1 + s1 <= o2 for (o1, s1), (o2, _) in zip(pairs, pairs[1:]))
     assert pairs[-1][0] + pairs[-1][1] <= f2.workspace_bytes == nbytes
-    names = ("counters", "row_count", "tile_count", "row_pairs", "lb_rows", "lb_cols", "depth", "pay0", "pay1",
-             "pay2", "pay3", "radius", "rect", "status", "flags", "drgb_ddir", None, None, None, None, "sorted_vis",
-             "radix_hist", "items", "rowlist", "col_excl", "list", "ranges", "final_T", "n_contrib", "grad2d")
+    names = ("counters", "row_count", "tile_count", "row_pairs", "tile_bucket", "lb_rows", "lb_cols", "depth",
+             "pay0", "pay1", "pay2", "pay3", "radius", "rect", "status", "flags", "drgb_ddir", None, None, None, None,
+             "sorted_vis", "radix_hist", "items", "rowlist", "col_excl", "list", "ranges", "final_T", "n_contrib",
+             "tile_order", "grad2d")
     assert len(names) == n.value
     for (o, s), nm in zip(pairs, names):
         if nm:
             assert getattr(f2, nm) == base + o, nm
-    assert (f2.vis_key[0], f2.vis_val[0], f2.vis_key[1], f2.vis_val[1]) == tuple(base + pairs[k][0] for k in range(16, 20))
+    assert (f2.vis_key[0], f2.vis_val[0], f2.vis_key[1], f2.vis_val[1]) == tuple(base + pairs[k][0] for k in range(17, 21))
     assert pairs[names.index("depth")][1] == 4 * P and pairs[names.index("grad2d")][1] == 48 * P
+    assert pairs[names.index("tile_bucket")][1] == 4 * 64 and pairs[names.index("tile_order")][1] == 4 * 64 * 35
+    assert pairs[names.index("tile_bucket")][0] + 4 * 64 <= f2.zero_bytes  # zeroed per frame
     assert lib.ges_frame_layout(None, None, 0, C.byref(n)) == L.GES_ERR_INVALID_ARG
     assert lib.ges_sort(None, None) == L.GES_ERR_INVALID_ARG
     assert lib.ges_status_string(L.GES_ERR_CAPACITY).decode().startswith("workspace")

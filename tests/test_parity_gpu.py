@@ -7,6 +7,7 @@ same seeded inputs.  Bars (BASELINE.json north_star):
     touching an ambiguous pixel (reported, bounded in number).
 """
 import ctypes as C
+import dataclasses
 
 import numpy as np
 import pytest
@@ -591,3 +592,46 @@ def test_sh_grad_from_colour_matches_accumulated_sh():
     st = lib.ges_sh_grad_from_colour(C.c_void_p(dev.mean.data_ptr()), P, 3, None, V,
                                      C.c_void_p(drgb.data_ptr()), C.c_void_p(rebuilt.data_ptr()), 0, None)
     assert st == L.GES_ERR_INVALID_ARG
+
+
+def test_backward_launch_order():
+    """ges_frame.tile_order (S4 -> S5a launch order): after one forward the 64 buckets hold
+    every tile exactly once, in the bucket of the tile's largest n_contrib; S5a's gradients
+    equal those of the index-order fallback (a second S4 on the same frame doubles the
+    bucket counts) up to float-atomic order; band frames too."""
+    sc = gi.make_config(2, P=60000, n_views=1)
+    cam = sc.cameras[0]
+    gs = G.Settings(rho=sc.rho)
+    dev = G.PlanarParams.from_inputs(sc.particles)
+    dL = torch.from_numpy(np.ascontiguousarray(gi.upstream_grad(sc.seed, 0, cam.width, cam.height))).cuda()
+    for band in ((0, 1), (1, 3)):
+        s = dataclasses.replace(gs, tile_row_begin=band[0], tile_row_step=band[1])
+        r = G.Renderer(dev.P, cam.width, cam.height)
+        img = r.forward(dev, cam, s)
+        f = r.frame
+        T = f.c.tiles_x * f.c.band_rows
+        torch.cuda.synchronize()
+        counts = f.view("tile_bucket", torch.int32, 64).cpu().numpy()
+        assert counts.sum() == T
+        order = f.view("tile_order", torch.int32, 64 * T).cpu().numpy().reshape(64, T)
+        tiles = np.concatenate([order[b, :counts[b]] for b in range(64)])
+        assert np.array_equal(np.sort(tiles), np.arange(T))
+        # bucket = the 4-per-octave log bucket of the tile's largest n_contrib
+        H, W = cam.height, cam.width
+        nc = f.view("n_contrib", torch.int32, W * H).cpu().numpy().reshape(H, W).astype(np.int64)
+        rows = [band[0] + k * band[1] for k in range(f.c.band_rows)]
+        for b in range(64):
+            for t in order[b, :counts[b]]:
+                ty, tx = rows[t // f.c.tiles_x], t % f.c.tiles_x
+                c = int(nc[16 * ty:16 * ty + 16, 16 * tx:16 * tx + 16].max())
+                e = c.bit_length() - 1
+                want = c if c < 4 else min(63, 4 * (e - 1) + ((c >> (e - 2)) & 3))
+                assert b == want, (t, c, b, want)
+        g1 = r.backward(dev, cam, s, dL).flat.clone()
+        G.ges_render_fwd(f, s, img)               # second S4: counts 2T -> index order
+        torch.cuda.synchronize()
+        assert f.view("tile_bucket", torch.int32, 64).cpu().numpy().sum() == 2 * T
+        g2 = r.backward(dev, cam, s, dL).flat.clone()
+        torch.cuda.synchronize()
+        a, b2 = g1.cpu().numpy(), g2.cpu().numpy()
+        assert np.all(np.abs(a - b2) <= 1e-4 * np.abs(a) + 1e-6 * (1 + np.abs(a).max()))
