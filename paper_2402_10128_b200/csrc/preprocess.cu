@@ -312,6 +312,13 @@ __global__ void __launch_bounds__(kPreThreads, GES_PRE_MINB) preprocess_kernel(P
 #ifndef GES_PRE_STAGES
 #define GES_PRE_STAGES 2
 #endif
+// experiment knob GES_PRE_TMA_MINB: min blocks per SM (unset: no second launch-bounds
+// argument -- spelling out 1 lets ptxas take 121 registers instead of 96)
+#ifdef GES_PRE_TMA_MINB
+#define GES_PRE_TMA_LB __launch_bounds__(kPreTmaThreads, GES_PRE_TMA_MINB)
+#else
+#define GES_PRE_TMA_LB __launch_bounds__(kPreTmaThreads)
+#endif
 constexpr int kPreTile = GES_PRE_TILE;
 constexpr int kPreStages = GES_PRE_STAGES;
 constexpr int kPreTmaThreads = kPreTile + 32;
@@ -352,7 +359,7 @@ __device__ __forceinline__ const float* pre_plane(const PreprocessArgs& a, int p
 }
 
 template <int K>
-__global__ void __launch_bounds__(kPreTmaThreads) preprocess_tma_kernel(PreprocessArgs a) {
+__global__ void GES_PRE_TMA_LB preprocess_tma_kernel(PreprocessArgs a) {
     constexpr int NPL = 12 + 3 * K;
     extern __shared__ __align__(128) float s_st[];  // [kPreStages][NPL][kPreTile]
     __shared__ __align__(8) uint64_t s_full[kPreStages], s_empty[kPreStages];

@@ -401,8 +401,11 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
     }
     constexpr uint32_t kAll = (1u << PPT) - 1u;
     StagedBatch sb{S.g0, S.g1, S.b, nullptr, S.mask, S.hb};
-    const uint32_t sbase = smem_addr(&S);
-    const uint32_t a_list = smem_addr(S.list[warp]);
+    uint32_t sbase = smem_addr(&S);
+    uint32_t a_list = smem_addr(S.list[warp]);
+    // opaque: kept in registers instead of rebuilt from the CTA's shared window
+    // (S2UR SR_CgaCtaId + ULEA) in every iteration of the entry loop
+    asm volatile("" : "+r"(sbase), "+r"(a_list));
     if (start < end) prefetch_ids(S.ids[0], a.list, start, (int)min((uint32_t)kBatch, end - start));
     int buf = 0;
     for (uint32_t b0 = start; b0 < end; b0 += kBatch, buf ^= 1) {
@@ -663,8 +666,11 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads, PPT) render_bwd_kernel(Render
     uint32_t nxt = warp_max;
     const int red_comp = record_component<EXACT>(lane);
     StagedBatch sb{S.g0, S.g1, S.b, S.pid, S.mask, S.hb};
-    const uint32_t sbase = smem_addr(&S);
-    const uint32_t a_list = smem_addr(S.list[warp]);
+    uint32_t sbase = smem_addr(&S);
+    uint32_t a_list = smem_addr(S.list[warp]);
+    // opaque: kept in registers instead of rebuilt from the CTA's shared window
+    // (S2UR SR_CgaCtaId + ULEA) in every iteration of the entry loop
+    asm volatile("" : "+r"(sbase), "+r"(a_list));
     if (max_last > 0) {
         const int32_t b0 = max(0, (int32_t)max_last - kBatch);
         prefetch_ids(S.ids[0], a.list, start + (uint32_t)b0, (int)max_last - b0);

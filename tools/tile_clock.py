@@ -87,6 +87,13 @@ for w, name in enumerate(["render_fwd", "render_bwd"]):
                       ("max of the halves", nc_hmax)):
         print(f"  corr(duration, {pname}) {np.corrcoef(d, pv)[0, 1]:.3f}")
 d_f = a[0, :, 1] - a[0, :, 0]
+best_c, best_r = None, -2
+for c in (50, 100, 200, 300, 400, 600, 800, 1200, 1600):
+    rr = np.corrcoef(d_f, np.minimum(lens, c))[0, 1]
+    print(f"corr(fwd duration, min(list length, {c})) {rr:.3f}")
+    if rr > best_r:
+        best_c, best_r = c, rr
+capped = np.minimum(lens, best_c)
 d_b = a[1, :, 1] - a[1, :, 0]
 print(f"corr(fwd duration, bwd duration) {np.corrcoef(d_f, d_b)[0, 1]:.3f}")
 experiments = {
@@ -97,6 +104,7 @@ experiments = {
     "max of the halves": (np.argsort(-nc_hmax, kind="stable"), np.argsort(-nc_hmax, kind="stable")),
     "sum + max halves": (np.argsort(-(nc_wmax + nc_hmax), kind="stable"), np.argsort(-(nc_wmax + nc_hmax), kind="stable")),
     "bwd by fwd duration": (None, np.argsort(-d_f, kind="stable")),
+    "fwd by capped list length": (np.argsort(-capped, kind="stable"), None),
 }
 print(f"natural order: fwd {base[0]:.1f} us, bwd {base[1]:.1f} us")
 for k, (of, ob) in experiments.items():
