@@ -332,7 +332,13 @@ __device__ __forceinline__ void pb_bulk(void* dst, const void* src, uint32_t byt
 }
 
 template <int K>
-__global__ void __launch_bounds__(kPbThreads) particle_bwd_tma_kernel(ParticleBwdArgs a) {
+// experiment knob GES_PB_TMA_MINB: min resident CTAs per SM (register cap); unset = none
+#ifdef GES_PB_TMA_MINB
+#define GES_PB_TMA_LB __launch_bounds__(kPbThreads, GES_PB_TMA_MINB)
+#else
+#define GES_PB_TMA_LB __launch_bounds__(kPbThreads)
+#endif
+__global__ void GES_PB_TMA_LB particle_bwd_tma_kernel(ParticleBwdArgs a) {
     extern __shared__ __align__(128) unsigned char s_raw[];
     PbStage* stg = reinterpret_cast<PbStage*>(s_raw);
     __shared__ __align__(8) uint64_t s_full[kPbStages], s_empty[kPbStages];

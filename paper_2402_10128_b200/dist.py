@@ -24,7 +24,8 @@ import torch
 import torch.distributed as dist
 
 from . import _lib as L
-from .api import Frame, PlanarParams, Renderer, Settings, _stream, sh_grad_from_colour
+from .api import (Frame, PlanarParams, Renderer, Settings, _stream, ges_backward_particles,
+                  ges_render_bwd_tiles, sh_grad_from_colour)
 
 TILE = 16
 
@@ -254,10 +255,17 @@ class ViewDataParallel:
     allreduced parameter gradients of sum_v <dL/dimage_v, image_v>."""
 
     def __init__(self, params: PlanarParams, cameras: Sequence, settings: Settings, rank: int, world: int,
-                 device="cuda", group=None, compact: bool = False, sh_factorized: bool = False):
+                 device="cuda", group=None, compact: bool = False, sh_factorized: bool = False, streams: int = 1):
         self.params, self.cameras, self.settings = params, list(cameras), settings
         if compact and sh_factorized:
             raise ValueError("compact and sh_factorized are alternative exchanges")
+        # streams = 2: consecutive views alternate between two streams and two frames, so one
+        # view's latency-bound phases (sort, render tails) overlap the other's; the S5b
+        # accumulations into the one gradient buffer stay in view order (events)
+        if streams not in (1, 2) or (streams == 2 and compact):
+            raise ValueError("streams must be 1 or 2 (2 only without compact)")
+        self.n_streams = streams
+        self.side = torch.cuda.Stream(device=device) if streams == 2 else None
         # compact: reduce only the union of the ranks' visible particles (VisibleUnionReducer)
         self.reducer = VisibleUnionReducer(params.P, params.flat.shape[0], device) if compact else None
         self.views = views_for_rank(len(self.cameras), rank, world)
@@ -275,43 +283,87 @@ class ViewDataParallel:
                 c = self.cameras[v]
                 rows[j] = torch.tensor([float(x) for x in list(c.R.reshape(9)) + list(c.t.reshape(3))])
             self.cams = rows.to(device)
-        cam0 = self.cameras[0]
         self.renderers = {}
         for v in self.views:
             c = self.cameras[v]
             key = (c.width, c.height)
             if key not in self.renderers:
-                self.renderers[key] = Renderer(params.P, c.width, c.height, device=device)
+                self.renderers[key] = [Renderer(params.P, c.width, c.height, device=device) for _ in range(streams)]
         self.grads = PlanarParams.zeros(params.P, params.sh_degree, device)
         self.images = {}
+        # per view: the frame's (overflow, slots) counters after its forward, copied on the
+        # device; read once per step (one host sync instead of one per view)
+        self.status = torch.zeros((max(len(self.views), 1), 2), dtype=torch.int64, device=device)
+
+    def _views(self, dL_dimages: dict, main) -> bool:
+        """Every view of this rank fwd+bwd (views alternate between `main` and the side
+        stream when streams = 2); False (after growing the frames) if a frame overflowed."""
+        ctx = (lambda q: torch.cuda.stream(q)) if main is not None else (lambda q: _nullctx())
+        first = True
+        with ctx(main):
+            if self.reducer is not None:
+                self.reducer.reset()
+            elif self.drgb is not None:
+                self.drgb.zero_()
+        if self.side is not None:
+            self.side.wait_stream(main)
+        prev = None  # the previous view's S5b (streams = 2)
+        ovf = L.GES_CTR_OVERFLOW
+        for j, v in enumerate(self.views):
+            cam = self.cameras[v]
+            q = self.side if (self.side is not None and j % 2 == 1) else main
+            r = self.renderers[(cam.width, cam.height)][j % self.n_streams]
+            with ctx(q):
+                img = torch.empty((3, cam.height, cam.width), dtype=torch.float32, device=self.grads.flat.device)
+                r.forward(self.params, cam, self.settings, img, stream=q, check_overflow=False)
+                cnt = r.frame.view("counters", torch.int64, L.GES_CTR_N)
+                self.status[j, 0].copy_(cnt[ovf])
+                self.status[j, 1].copy_(cnt[L.GES_CTR_SLOTS])
+            self.images[v] = img
+            if self.reducer is not None:
+                self.reducer.add_view(r.frame, q)
+            drgb = self.drgb[j] if self.drgb is not None else None
+            if self.side is None:
+                r.backward(self.params, cam, self.settings, dL_dimages[v], grads=self.grads,
+                           accumulate=not first, stream=q, drgb=drgb)
+            else:
+                ges_render_bwd_tiles(self.settings, r.frame, dL_dimages[v], q)
+                if prev is not None:
+                    q.wait_event(prev)  # S5b accumulations in view order, never concurrent
+                ges_backward_particles(self.params, cam, self.settings, r.frame, self.grads,
+                                       accumulate=not first, stream=q, drgb=drgb)
+                prev = torch.cuda.Event()
+                prev.record(q)
+            first = False
+        if first:  # no views on this rank: contribute zeros
+            with ctx(main):
+                self.grads.flat.zero_()
+        if self.side is not None:
+            main.wait_stream(self.side)
+        if not self.views:
+            return True
+        st = self.status[:len(self.views)].cpu()  # one host sync per step
+        if not bool(st[:, 0].any()):
+            return True
+        keys = {(self.cameras[v].width, self.cameras[v].height) for j, v in enumerate(self.views) if st[j, 0]}
+        for key in keys:  # the exact slot count: the next attempt fits unless the scene changed
+            for r in self.renderers[key]:
+                r.grow(int(st[:, 1].max()))
+        return False
 
     def step(self, dL_dimages: dict, stream=None) -> PlanarParams:
         """dL_dimages: view -> [3][H][W] device tensor, for this rank's views.  Everything
         runs on `stream` (default: torch's current stream); the collectives are issued on
         torch's current stream after it waits for `stream`, and `stream` waits for them."""
         cur = torch.cuda.current_stream() if torch.cuda.is_available() else None
+        main = stream if stream is not None else cur
         if stream is not None and cur is not None:
             stream.wait_stream(cur)  # inputs produced on the current stream
-        first = True
-        if self.reducer is not None or self.drgb is not None:
-            with torch.cuda.stream(stream) if stream is not None else _nullctx():
-                if self.reducer is not None:
-                    self.reducer.reset()
-                else:
-                    self.drgb.zero_()
-        for j, v in enumerate(self.views):
-            cam = self.cameras[v]
-            r = self.renderers[(cam.width, cam.height)]
-            self.images[v] = r.forward(self.params, cam, self.settings, stream=stream)
-            if self.reducer is not None:
-                self.reducer.add_view(r.frame, stream)
-            r.backward(self.params, cam, self.settings, dL_dimages[v], grads=self.grads,
-                       accumulate=not first, stream=stream,
-                       drgb=self.drgb[j] if self.drgb is not None else None)
-            first = False
-        if first:  # no views on this rank: contribute zeros
-            with torch.cuda.stream(stream) if stream is not None else _nullctx():
-                self.grads.flat.zero_()
+        for attempt in range(3):
+            if self._views(dL_dimages, main):
+                break
+            if attempt == 2:
+                raise L.GESError("pair capacity still exceeded after regrowing the frames twice")
         if stream is not None and cur is not None:
             cur.wait_stream(stream)  # the masks and gradients are complete before any collective
         if self.reducer is not None:

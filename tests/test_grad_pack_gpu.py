@@ -97,3 +97,34 @@ def test_view_data_parallel_sh_factorized_equals_dense_single_rank():
         assert np.all(np.abs(a - b) <= np.maximum(1e-4 * np.abs(a), floor))
     with pytest.raises(ValueError):
         gdist.ViewDataParallel(params, cams, st, 0, 1, compact=True, sh_factorized=True)
+
+
+@pytest.mark.parametrize("sh_factorized", [False, True])
+def test_view_data_parallel_two_streams(sh_factorized):
+    """ViewDataParallel(streams=2): views alternate between two streams and two frames, the
+    S5b accumulations serialised in view order; the gradients and images equal the
+    one-stream step (float-atomic order aside); frames that overflow are regrown and the
+    step redone (one host read of the per-view counters)."""
+    sc = gi.make_config(2, P=40000, n_views=5)
+    cams = [_zoomed(c) for c in sc.cameras]
+    params = G.PlanarParams.from_inputs(sc.particles)
+    st = G.Settings(rho=sc.rho)
+    dLs = {v: torch.from_numpy(gi.upstream_grad(sc.seed, v, c.width, c.height)).cuda() for v, c in enumerate(cams)}
+    one = gdist.ViewDataParallel(params, cams, st, 0, 1, sh_factorized=sh_factorized)
+    a = one.step(dLs).flat.clone()
+    imgs = {v: one.images[v].clone() for v in one.views}
+    two = gdist.ViewDataParallel(params, cams, st, 0, 1, sh_factorized=sh_factorized, streams=2)
+    for rl in two.renderers.values():            # too small: the first step must regrow
+        for r in rl:
+            r.frame = G.Frame(params.P, r.width, r.height, 1024)
+    for _ in range(2):
+        b = two.step(dLs).flat.clone()
+        torch.cuda.synchronize()
+        x, y = a.cpu().numpy(), b.cpu().numpy()
+        floor = 1e-6 + 1e-6 * np.abs(x).max()
+        assert np.all(np.abs(x - y) <= np.maximum(1e-4 * np.abs(x), floor))
+        for v in one.views:
+            assert torch.equal(imgs[v], two.images[v])
+    assert all(r.frame.c.pair_capacity > 1024 for rl in two.renderers.values() for r in rl)
+    with pytest.raises(ValueError):
+        gdist.ViewDataParallel(params, cams, st, 0, 1, compact=True, streams=2)
