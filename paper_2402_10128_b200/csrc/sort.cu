@@ -141,10 +141,23 @@ __device__ void ds_range_hist(const DepthSortArgs& a, DsSmem& sm, const uint32_t
 #if defined(GES_DS_TIMING) && GES_DS_TIMING == 3
 __device__ unsigned long long g_ds_t[8];
 __device__ long long g_ds_q[6];
-#define DS_RMARK(k) do { __syncthreads(); if (blockIdx.x == 0 && threadIdx.x == 0 && shift == 9) { unsigned long long t_; \
+#ifndef GES_DS_TIMING_SHIFT
+#define GES_DS_TIMING_SHIFT 9  // the pass whose rank phases are timed (digit shift)
+#endif
+#define DS_RMARK(k) do { __syncthreads(); if (blockIdx.x == 0 && threadIdx.x == 0 && shift == GES_DS_TIMING_SHIFT) { unsigned long long t_; \
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); g_ds_t[k] = t_; } } while (0)
 #else
 #define DS_RMARK(k) do {} while (0)
+#endif
+#if defined(GES_DS_TIMING) && GES_DS_TIMING == 4
+// per pass p and phase k (0 start, 1 ranked, 2 prefix known, 3 written, 4 after the grid
+// barrier): %globaltimer of thread 0 of CTA 0 [0] and of the last CTA [1]
+__device__ unsigned long long g_ds_p[2][4][5];
+#define DS_PMARK(p, k) do { if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) && (p) < 4) { \
+    unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \
+    g_ds_p[blockIdx.x == 0 ? 0 : 1][p][k] = t_; } } while (0)
+#else
+#define DS_PMARK(p, k) do {} while (0)
 #endif
 // Publishes this CTA's digit counts of pass p, then finds the sums over the
 // CTAs before it without a grid barrier, in two levels of groups of kDsGroup
@@ -342,19 +355,33 @@ __device__ uint32_t ds_tile_rank(DsSmem& sm, const uint32_t* kin, const uint32_t
 // Last pass: the rect of every reordered key staged in shared memory (over the
 // free rank histograms); the tile's rect areas and row coverage accumulate into
 // sm.area and sm.rowd.
-__device__ void ds_tile_rects(const DepthSortArgs& a, DsSmem& sm, uint32_t nvalid) {
-    const int tid = threadIdx.x;
-    uint2* rs = reinterpret_cast<uint2*>(&sm.whist[0][0]);
-    const int s0 = tid * kDsItems;  // thread tid owns the positions [8 tid, 8 tid + 8)
-    uint2 rc[kDsItems];
+// Last pass: gathers the ranked tile's rects (8 B each) into shared memory over whist
+// (free once the tile is ranked) with cp.async, so that the gathers' latency overlaps the
+// prefix look-back that follows; ds_tile_rects consumes them.
+__device__ void ds_rect_prefetch(const DepthSortArgs& a, DsSmem& sm, uint32_t nvalid) {
+    const int s0 = threadIdx.x * kDsItems;  // thread tid owns the positions [8 tid, 8 tid + 8)
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&sm.whist[0][0]) + 8u * (uint32_t)s0;
+    const uint2* src = reinterpret_cast<const uint2*>(a.rect);
 #pragma unroll
     for (int j = 0; j < kDsItems; ++j)
-        rc[j] = s0 + j < (int)nvalid ? __ldg(reinterpret_cast<const uint2*>(a.rect) + sm.vals[s0 + j]) : make_uint2(0, 0);
+        if (s0 + j < (int)nvalid)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst + 8u * j), "l"(src + sm.vals[s0 + j])
+                         : "memory");
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
+__device__ void ds_tile_rects(const DepthSortArgs& a, DsSmem& sm, uint32_t nvalid) {
+    const int tid = threadIdx.x;
+    asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's gathers (ds_rect_prefetch)
+    uint2* rs = reinterpret_cast<uint2*>(&sm.whist[0][0]);
+    const int s0 = tid * kDsItems;
+    uint2 rc[kDsItems];
+#pragma unroll
+    for (int j = 0; j < kDsItems; ++j) rc[j] = s0 + j < (int)nvalid ? rs[s0 + j] : make_uint2(0, 0);
     unsigned long long ar = 0;
 #pragma unroll
     for (int j = 0; j < kDsItems; ++j) {
         if (s0 + j < (int)nvalid) {
-            rs[s0 + j] = rc[j];
             const uint32_t y0 = rc[j].x >> 16, y1 = rc[j].y >> 16;
             ar += (unsigned long long)((rc[j].y & 0xffffu) - (rc[j].x & 0xffffu)) * (y1 - y0);
             atomicAdd(&sm.rowd[y0], 1);
@@ -414,24 +441,36 @@ __device__ void ds_pass(const DepthSortArgs& a, DsSmem& sm, const uint32_t* kin,
         if (tid == 0) sm.area = 0;
         __syncthreads();
     }
+    DS_PMARK(p, 0);
     if (p == 0 && sm.hn <= (uint32_t)kDsTile) {
         // pass 0 from phase H's compacted visible keys: one tile, counted and published there
         const uint32_t nvalid = ds_tile_rank<true>(sm, sm.hkeys(), sm.hvals(), 0, sm.hn, shift, false, a.key_base);
-        if (last) ds_tile_rects(a, sm, nvalid);
+        if (last) ds_rect_prefetch(a, sm, nvalid);
+        DS_PMARK(p, 1);
         ds_prefix(a, sm, p, false);
+        if (last) ds_tile_rects(a, sm, nvalid);
+        DS_PMARK(p, 2);
         ds_tile_write(a, sm, nvalid, kout, vout, shift, last);
+        DS_PMARK(p, 3);
     } else if (p > 0 && r1 - r0 <= kDsTile) {
         uint32_t* pub = a.st_cnt + ((size_t)p * kDsMaxGrid + blockIdx.x) * kDsDigits;
         const uint32_t nvalid = ds_tile_rank(sm, kin, vin, r0, r1, shift, drop, a.key_base, pub);
-        if (last) ds_tile_rects(a, sm, nvalid);
+        if (last) ds_rect_prefetch(a, sm, nvalid);
+        DS_PMARK(p, 1);
         ds_prefix(a, sm, p, false);  // (published before the ranking)
+        if (last) ds_tile_rects(a, sm, nvalid);
+        DS_PMARK(p, 2);
         ds_tile_write(a, sm, nvalid, kout, vout, shift, last);
+        DS_PMARK(p, 3);
     } else {
         if (p > 0) ds_range_hist(a, sm, kin, r0, r1, shift, false);
         if (p > 0) ds_prefix(a, sm, p, true);
         for (int64_t t0 = r0; t0 < r1; t0 += kDsTile) {
             const uint32_t nvalid = ds_tile_rank(sm, kin, vin, t0, r1, shift, drop, a.key_base);
-            if (last) ds_tile_rects(a, sm, nvalid);
+            if (last) {
+                ds_rect_prefetch(a, sm, nvalid);
+                ds_tile_rects(a, sm, nvalid);
+            }
             // pass 0 (counted and published by phase H): the prefix after the first tile's ranking
             if (p == 0 && t0 == r0) ds_prefix(a, sm, p, false);
             ds_tile_write(a, sm, nvalid, kout, vout, shift, last);
@@ -549,6 +588,7 @@ __global__ void __launch_bounds__(kDsThreads, 1) depth_sort_kernel(DepthSortArgs
         uint32_t* vout = last ? a.sorted_vis : a.vals[p & 1];
         ds_pass(a, sm, kin, vin, kout, vout, r0, r1, p, last);
         if (!last) grid.sync();
+        DS_PMARK(p, 4);
         ds_mark(a, last ? 6 : 2 + p);
         kin = kout;
         vin = vout;
@@ -560,6 +600,11 @@ __global__ void __launch_bounds__(kDsThreads, 1) depth_sort_kernel(DepthSortArgs
 }  // namespace ges
 extern "C" void ges_debug_ds_times(unsigned long long* out) { cudaMemcpyFromSymbol(out, ges::g_ds_t, 64); }
 extern "C" void ges_debug_ds_q(long long* out) { cudaMemcpyFromSymbol(out, ges::g_ds_q, 48); }
+namespace ges {
+#endif
+#if defined(GES_DS_TIMING) && GES_DS_TIMING == 4
+}  // namespace ges
+extern "C" void ges_debug_ds_pass_times(unsigned long long* out) { cudaMemcpyFromSymbol(out, ges::g_ds_p, 320); }
 namespace ges {
 #endif
 int depth_sort_grid() {
