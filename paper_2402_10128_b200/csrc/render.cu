@@ -39,8 +39,8 @@ __device__ int g_tile_order[2][16384];
 __device__ int g_tile_order_on[2];
 struct TileClock {
     unsigned long long* rec;
-    __device__ explicit TileClock(int which) {
-        rec = g_tile_clk[which][(g_tile_order_on[which] ? g_tile_order[which][blockIdx.x] : blockIdx.x) & 16383];
+    __device__ TileClock(int which, int tile) {
+        rec = g_tile_clk[which][tile & 16383];
         unsigned long long t, sm;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         asm volatile("mov.u32 %0, %%smid;" : "=r"(*(unsigned*)&sm));
@@ -52,10 +52,10 @@ struct TileClock {
         if ((threadIdx.x & 31) == 0) atomicMax(rec + 1, t);
     }
 };
-#define GES_CLOCK(which) TileClock tile_clock_(which)
+#define GES_CLOCK(which, tile) TileClock tile_clock_(which, tile)
 #define GES_TILE(which) (g_tile_order_on[which] ? g_tile_order[which][blockIdx.x] : (int)blockIdx.x)
 #else
-#define GES_CLOCK(which)
+#define GES_CLOCK(which, tile)
 #define GES_TILE(which) ((int)blockIdx.x)
 #endif
 
@@ -376,10 +376,10 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
     using Lt = Layout<PPT>;
     using Sm = RenderSmem<PPT, EXACT>;
     __shared__ Sm S;
-    GES_CLOCK(0);
     static_assert(offsetof(Sm, g1) == Sm::kG1 && offsetof(Sm, b) == Sm::kB && offsetof(Sm, pid) == Sm::kPid &&
                   offsetof(Sm, hb) == Sm::kHb, "smem layout");
     const int tile = GES_TILE(0);
+    GES_CLOCK(0, tile);
     const int tid = threadIdx.x, warp = tid >> 5;
     int px, py0;
     int tile_x0, tile_y0;
@@ -618,12 +618,12 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads, PPT) render_bwd_kernel(Render
     using Lt = Layout<PPT>;
     using Sm = RenderSmem<PPT, EXACT>;
     __shared__ Sm S;
-    GES_CLOCK(1);
 #ifdef GES_TILE_CLOCK
     const int tile = g_tile_order_on[1] ? GES_TILE(1) : (a.use_order ? ordered_tile(a.tile_bucket, a.tile_order) : (int)blockIdx.x);
 #else
     const int tile = a.use_order ? ordered_tile(a.tile_bucket, a.tile_order) : (int)blockIdx.x;
 #endif
+    GES_CLOCK(1, tile);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     int px, py0;
     int tile_x0, tile_y0;
