@@ -9,7 +9,7 @@
 //
 // One CTA per tile, PPT pixels per thread (2 forward, 4 backward); warp w owns
 // the 8 x (4 PPT)-pixel region (x0 = 8 (w & 1), y0 = 4 PPT (w >> 1)) of the tile.
-// Each batch of kBatch (256) list entries is gathered once into shared memory
+// Each batch of kBatchFwd (128, S4) / kBatch (256, S5a) list entries is gathered once into shared memory
 // (its list ids prefetched one batch early by cp.async); while gathering, each
 // thread tests its entry against the warp regions with an exact lower bound of the
 // Mahalanobis form over the region (the minimum of a positive-definite
@@ -62,7 +62,11 @@ struct TileClock {
 #ifndef GES_BATCH
 #define GES_BATCH 256
 #endif
-constexpr int kBatch = GES_BATCH;  // list entries staged per barrier
+constexpr int kBatch = GES_BATCH;  // list entries staged per barrier (S5a)
+#ifndef GES_BATCH_FWD
+#define GES_BATCH_FWD 128
+#endif
+constexpr int kBatchFwd = GES_BATCH_FWD;  // (S4)
 // tuning knobs: min resident CTAs per SM (register cap); unset = ptxas's choice
 // forward: 9 resident CTAs per SM (PPT 2: 128 threads, a 56-register cap met
 // without spills) measured 2 % faster than ptxas's own 64 registers
@@ -78,6 +82,11 @@ constexpr int kBatch = GES_BATCH;  // list entries staged per barrier
 #define GES_RBWD_LB(t, ppt) __launch_bounds__(t, (ppt) == 4 ? 9 : 1)
 #endif
 constexpr float kCullMargin = 0.01f;      // log2 units (0.7% in alpha)
+#ifdef GES_BWD_HALF
+constexpr bool kBwdHalf = true;
+#else
+constexpr bool kBwdHalf = false;
+#endif
 
 struct Splat {
     float u, v, A, B, C, kappa, r, g, b;
@@ -143,7 +152,6 @@ struct Layout {
     static constexpr int kThreads = kBlock / PPT;
     static constexpr int kWarps = kThreads / 32;
     static constexpr int kRegionH = 4 * PPT;
-    static constexpr int kLoads = kBatch / kThreads;  // entries staged per thread
 };
 
 // Bit w set if some pixel of warp region w may get alpha >= 1/255 from s.
@@ -241,6 +249,7 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
 }
 
 // Per-warp compaction of the batch entries whose mask has this warp's bit.
+template <int NB = kBatch>
 __device__ __forceinline__ int compact_warp_list(const uint8_t* s_mask, int n, int warp, uint16_t* out) {
     const int lane = threadIdx.x & 31;
     int cnt = 0;
@@ -249,7 +258,7 @@ __device__ __forceinline__ int compact_warp_list(const uint8_t* s_mask, int n, i
     for (int c = 0; c < (n + 31) / 32; ++c) {
 #else
 #pragma unroll
-    for (int c = 0; c < kBatch / 32; ++c) {
+    for (int c = 0; c < NB / 32; ++c) {
 #endif
         const int j = c * 32 + lane;
         const bool bit = j < n && ((s_mask[j] >> warp) & 1u);
@@ -275,12 +284,11 @@ __device__ __forceinline__ uint32_t cost_bucket(uint32_t c) {
     return min((uint32_t)(kTileBuckets - 1), 4u * (uint32_t)(e - 1) + ((c >> (e - 2)) & 3u));
 }
 
-// S5a: the tile of CTA b in descending cost order (the forward's buckets), or b itself
-// when the buckets do not hold exactly gridDim.x tiles.  Every warp computes it.
-__device__ __forceinline__ int ordered_tile(const uint32_t* bucket, const uint32_t* order) {
+// S5a: tile number b (of T) in descending cost order (the forward's buckets), or b itself
+// when the buckets do not hold exactly T tiles.  Every warp computes it.
+__device__ __forceinline__ int ordered_tile(const uint32_t* bucket, const uint32_t* order, uint32_t b, uint32_t T) {
     static_assert(kTileBuckets == 64, "two buckets per lane");
     const int lane = threadIdx.x & 31;
-    const uint32_t b = blockIdx.x, T = gridDim.x;
     // lane l holds buckets 63 - l (first half) and 31 - l (second half): descending cost
     const uint32_t c0 = bucket[63 - lane], c1 = bucket[31 - lane];
     uint32_t i0 = c0, i1 = c1;  // inclusive scans of each half
@@ -332,14 +340,14 @@ __device__ __forceinline__ void prefetch_ids(uint32_t* dst, const uint32_t* list
 }
 __device__ __forceinline__ void wait_ids() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
-template <int PPT, bool EXACT>
+template <int PPT, bool EXACT, int NT = Layout<PPT>::kThreads, int NB = kBatch>
 __device__ __forceinline__ void stage_batch(const float4* pay0, const float4* pay1, const float* pay2,
                                             const float* pay3, const uint32_t* ids, int n,
                                             int tile_x0, int tile_y0, StagedBatch sb) {
-    using Lt = Layout<PPT>;
+    static_assert(NB % NT == 0 && NB % 32 == 0, "a batch is whole rounds of the CTA's threads");
 #pragma unroll
-    for (int h = 0; h < Lt::kLoads; ++h) {
-        const int q = threadIdx.x + h * Lt::kThreads;
+    for (int h = 0; h < NB / NT; ++h) {
+        const int q = threadIdx.x + h * NT;
         if (q < n) {
             const uint32_t p = ids[q];
             const Splat s = load_splat(pay0, pay1, pay2, p);
@@ -356,25 +364,25 @@ __device__ __forceinline__ void stage_batch(const float4* pay0, const float4* pa
 
 // One shared-memory block per CTA: the staged batch at compile-time offsets, so
 // an entry's fields are one base register + an immediate (ld.shared [r+imm]).
-template <int PPT, bool EXACT>
+template <int PPT, bool EXACT, int NB = kBatch>
 struct RenderSmem {
-    float4 g0[kBatch];  // u, v, A, B
-    float4 g1[kBatch];  // C, kappa, r, g
-    float b[kBatch];
-    uint32_t pid[kBatch];
-    float hb[EXACT ? kBatch : 1];
-    uint16_t list[Layout<PPT>::kWarps][kBatch];
-    uint32_t ids[2][kBatch];  // list ids of this and the next batch
-    uint8_t mask[kBatch];
+    float4 g0[NB];  // u, v, A, B
+    float4 g1[NB];  // C, kappa, r, g
+    float b[NB];
+    uint32_t pid[NB];
+    float hb[EXACT ? NB : 1];
+    uint16_t list[Layout<PPT>::kWarps][NB];
+    uint32_t ids[2][NB];  // list ids of this and the next batch
+    uint8_t mask[NB];
     uint32_t max;
     uint32_t wmax[Layout<PPT>::kWarps];  // forward: each warp's largest n_contrib (tile cost)
-    static constexpr int kG1 = kBatch * 16, kB = kBatch * 32, kPid = kBatch * 36, kHb = kBatch * 40;
+    static constexpr int kG1 = NB * 16, kB = NB * 32, kPid = NB * 36, kHb = NB * 40;
 };
 
 template <int PPT, bool DIAG, bool EXACT>
 __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdArgs a) {
     using Lt = Layout<PPT>;
-    using Sm = RenderSmem<PPT, EXACT>;
+    using Sm = RenderSmem<PPT, EXACT, kBatchFwd>;
     __shared__ Sm S;
     static_assert(offsetof(Sm, g1) == Sm::kG1 && offsetof(Sm, b) == Sm::kB && offsetof(Sm, pid) == Sm::kPid &&
                   offsetof(Sm, hb) == Sm::kHb, "smem layout");
@@ -406,17 +414,17 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
     // opaque: kept in registers instead of rebuilt from the CTA's shared window
     // (S2UR SR_CgaCtaId + ULEA) in every iteration of the entry loop
     asm volatile("" : "+r"(sbase), "+r"(a_list));
-    if (start < end) prefetch_ids(S.ids[0], a.list, start, (int)min((uint32_t)kBatch, end - start));
+    if (start < end) prefetch_ids(S.ids[0], a.list, start, (int)min((uint32_t)kBatchFwd, end - start));
     int buf = 0;
-    for (uint32_t b0 = start; b0 < end; b0 += kBatch, buf ^= 1) {
+    for (uint32_t b0 = start; b0 < end; b0 += kBatchFwd, buf ^= 1) {
         wait_ids();
         if (__syncthreads_count(done == kAll) == Lt::kThreads) break;
-        const int n = (int)min((uint32_t)kBatch, end - b0);
-        if (b0 + kBatch < end) prefetch_ids(S.ids[buf ^ 1], a.list, b0 + kBatch, (int)min((uint32_t)kBatch, end - b0 - kBatch));
-        stage_batch<PPT, EXACT>(a.pay0, a.pay1, a.pay2, a.pay3, S.ids[buf], n, tile_x0, tile_y0, sb);
+        const int n = (int)min((uint32_t)kBatchFwd, end - b0);
+        if (b0 + kBatchFwd < end) prefetch_ids(S.ids[buf ^ 1], a.list, b0 + kBatchFwd, (int)min((uint32_t)kBatchFwd, end - b0 - kBatchFwd));
+        stage_batch<PPT, EXACT, Lt::kThreads, kBatchFwd>(a.pay0, a.pay1, a.pay2, a.pay3, S.ids[buf], n, tile_x0, tile_y0, sb);
         __syncthreads();
         if (__all_sync(0xffffffffu, done == kAll)) continue;  // the barrier above retires the tile
-        const int nw = compact_warp_list(S.mask, n, warp, S.list[warp]);
+        const int nw = compact_warp_list<kBatchFwd>(S.mask, n, warp, S.list[warp]);
         for (int i = 0; i < nw; ++i) {
             const int j = (int)lds_u16(a_list + 2u * (uint32_t)i);
             const uint32_t r16 = sbase + 16u * (uint32_t)j, r4 = sbase + 4u * (uint32_t)j;
@@ -614,21 +622,24 @@ __device__ __forceinline__ void red_add(float* addr, float x) {
 }
 
 template <int PPT, bool EXACT>
-__global__ void GES_RBWD_LB(Layout<PPT>::kThreads, PPT) render_bwd_kernel(RenderBwdArgs a) {
-    using Lt = Layout<PPT>;
+__global__ void GES_RBWD_LB(kBwdHalf ? 32 : Layout<PPT>::kThreads, PPT) render_bwd_kernel(RenderBwdArgs a) {
     using Sm = RenderSmem<PPT, EXACT>;
+    // kBwdHalf (experiment): one warp per CTA, CTA 2b + h walks warp region h of tile b
+    constexpr int kNT = kBwdHalf ? 32 : Layout<PPT>::kThreads;
     __shared__ Sm S;
+    const uint32_t b_ = kBwdHalf ? blockIdx.x >> 1 : blockIdx.x, T_ = kBwdHalf ? gridDim.x >> 1 : gridDim.x;
 #ifdef GES_TILE_CLOCK
-    const int tile = g_tile_order_on[1] ? GES_TILE(1) : (a.use_order ? ordered_tile(a.tile_bucket, a.tile_order) : (int)blockIdx.x);
+    const int tile = g_tile_order_on[1] ? GES_TILE(1) : (a.use_order ? ordered_tile(a.tile_bucket, a.tile_order, b_, T_) : (int)b_);
 #else
-    const int tile = a.use_order ? ordered_tile(a.tile_bucket, a.tile_order) : (int)blockIdx.x;
+    const int tile = a.use_order ? ordered_tile(a.tile_bucket, a.tile_order, b_, T_) : (int)b_;
 #endif
     GES_CLOCK(1, tile);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int vw = kBwdHalf ? (int)(blockIdx.x & 1u) : warp;  // the warp region walked
     int px, py0;
     int tile_x0, tile_y0;
     tile_origin(tile, a.tiles_x, a.band_begin, a.band_step, tile_x0, tile_y0);
-    pixel_base<PPT>(tile_x0, tile_y0, tid, px, py0);
+    pixel_base<PPT>(tile_x0, tile_y0, vw * 32 + lane, px, py0);
     const float fpx = (float)px + 0.5f;
     const bool ovf = a.counters[GES_CTR_OVERFLOW] != 0;
     const uint32_t start = ovf ? 0u : a.ranges[tile];
@@ -685,11 +696,11 @@ __global__ void GES_RBWD_LB(Layout<PPT>::kThreads, PPT) render_bwd_kernel(Render
             const int32_t nb = max(0, b_begin - kBatch);
             prefetch_ids(S.ids[buf ^ 1], a.list, start + (uint32_t)nb, b_begin - nb);
         }
-        stage_batch<PPT, EXACT>(a.pay0, a.pay1, a.pay2, a.pay3, S.ids[buf], n, tile_x0, tile_y0, sb);
+        stage_batch<PPT, EXACT, kNT>(a.pay0, a.pay1, a.pay2, a.pay3, S.ids[buf], n, tile_x0, tile_y0, sb);
         __syncthreads();
         // this warp's pixels composite nothing at or behind list position warp_max
         const int nw_lim = (int)min((int64_t)n, max((int64_t)0, (int64_t)warp_max - b_begin));
-        const int nw = compact_warp_list(S.mask, nw_lim, warp, S.list[warp]);
+        const int nw = compact_warp_list(S.mask, nw_lim, vw, S.list[warp]);
         for (int i = nw - 1; i >= 0; --i) {
             const int j = (int)lds_u16(a_list + 2u * (uint32_t)i);
             const uint32_t pos = (uint32_t)(b_begin + j);
@@ -834,17 +845,17 @@ cudaError_t launch_render_bwd(const RenderBwdArgs& args, cudaStream_t stream) {
     }();
     RenderBwdArgs a = args;
     a.use_order = use_order && a.tile_bucket && a.tile_order;
-    const int grid = a.tiles_x * a.tiles_y;
+    const int grid = a.tiles_x * a.tiles_y * (kBwdHalf ? 2 : 1);
     if (grid == 0) return cudaSuccess;  // a band without tile rows: no 2-D gradients
     if (a.exact) {
-        if (ppt == 4) render_bwd_kernel<4, true><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
-        else render_bwd_kernel<2, true><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
+        if (ppt == 4) render_bwd_kernel<4, true><<<grid, kBwdHalf ? 32 : Layout<4>::kThreads, 0, stream>>>(a);
+        else render_bwd_kernel<2, true><<<grid, kBwdHalf ? 32 : Layout<2>::kThreads, 0, stream>>>(a);
     } else {
         if (ppt == 4) {
             apply_carveout(render_bwd_kernel<4, false>);
-            render_bwd_kernel<4, false><<<grid, Layout<4>::kThreads, 0, stream>>>(a);
+            render_bwd_kernel<4, false><<<grid, kBwdHalf ? 32 : Layout<4>::kThreads, 0, stream>>>(a);
         } else {
-            render_bwd_kernel<2, false><<<grid, Layout<2>::kThreads, 0, stream>>>(a);
+            render_bwd_kernel<2, false><<<grid, kBwdHalf ? 32 : Layout<2>::kThreads, 0, stream>>>(a);
         }
     }
     return cudaGetLastError();
