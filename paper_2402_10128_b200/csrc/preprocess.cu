@@ -249,6 +249,9 @@ struct StatusCounts {
 // Writes particle i's S1 state and its sort key (fp32 depth bits, or 0xffffffff
 // when not visible -- dropped by depth pass 0, which thereby compacts the
 // visible set).  Returns visibility.
+#ifndef GES_PRE_L2_KEEP
+#define GES_PRE_L2_KEEP 1
+#endif
 __device__ __forceinline__ bool store_out(const PreprocessArgs& a, int i, const PreOut& o) {
     a.depth[i] = o.depth;
     a.pay0[i] = make_float4(o.u, o.v, o.ca, o.cb);
@@ -256,7 +259,18 @@ __device__ __forceinline__ bool store_out(const PreprocessArgs& a, int i, const 
     a.pay2[i] = o.b;
     if (a.kernel == GES_KERNEL_EXACT_BETA) a.pay3[i] = o.hb;
     a.radius[i] = o.radius;
+#if GES_PRE_L2_KEEP
+    {   // the rects the depth sort's last pass gathers by particle: stored with an L2
+        // evict_last policy (measured: S5b -3 us, the rest unchanged)
+        uint64_t pol;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        const uint64_t r = (uint64_t)(uint16_t)o.x0 | ((uint64_t)(uint16_t)o.y0 << 16) |
+                           ((uint64_t)(uint16_t)o.x1 << 32) | ((uint64_t)(uint16_t)o.y1 << 48);
+        asm volatile("st.global.L2::cache_hint.b64 [%0], %1, %2;" ::"l"(a.rect + i), "l"(r), "l"(pol) : "memory");
+    }
+#else
     a.rect[i] = make_ushort4((uint16_t)o.x0, (uint16_t)o.y0, (uint16_t)o.x1, (uint16_t)o.y1);
+#endif
     a.status[i] = o.status;
     a.flags[i] = o.flags;
 #pragma unroll
