@@ -342,7 +342,8 @@ class ViewDataParallel:
             main.wait_stream(self.side)
         if not self.views:
             return True
-        st = self.status[:len(self.views)].cpu()  # one host sync per step
+        with ctx(main):  # (the copy is ordered after the views on `main`)
+            st = self.status[:len(self.views)].cpu()  # one host sync per step
         if not bool(st[:, 0].any()):
             return True
         keys = {(self.cameras[v].width, self.cameras[v].height) for j, v in enumerate(self.views) if st[j, 0]}
