@@ -635,3 +635,43 @@ def test_backward_launch_order():
         torch.cuda.synchronize()
         a, b2 = g1.cpu().numpy(), g2.cpu().numpy()
         assert np.all(np.abs(a - b2) <= 1e-4 * np.abs(a) + 1e-6 * (1 + np.abs(a).max()))
+
+
+@pytest.mark.parametrize("case", ["config0", "config1_beta2"])
+def test_drgb_output_parity(case):
+    """ges_grads.drgb (optional output, the per-view colour gradient of the SH-factorised
+    exchange): dL/d rgb of every visible particle against the oracle's S5a colour sums
+    (g2d rows 6-8) with the clamped channels zeroed (flags bits 0-2, R13), at the
+    north_star tolerance or the entry's R19 scale; exactly 0 for particles that are not
+    visible."""
+    sc = gi.make_config(1, beta_value=2.0, P=20000) if case == "config1_beta2" else gi.make_config(0)
+    cam = sc.cameras[0]
+    gs, osx = settings_pair(rho=0.1)
+    out = gpu_forward(sc.particles, cam, gs)
+    pre = O.preprocess(sc.particles, cam, osx, "f32")
+    offsets, lst = O.tile_lists(pre)
+    ref = O.render_fwd(pre, cam, osx, offsets, lst)
+    dL = masked_upstream(gi.upstream_grad(sc.seed, 5, cam.width, cam.height), ref["amb"])
+    g2d, mag = O.render_bwd(pre, cam, osx, offsets, lst, dL, with_abs=True)
+    P = sc.particles.P
+    drgb = torch.full((3, P), 7.0, device="cuda")
+    grads = G.PlanarParams.zeros(P, out["params"].sh_degree)
+    dLt = torch.from_numpy(np.ascontiguousarray(dL, np.float32)).cuda()
+    G.ges_render_bwd(out["params"], cam, gs, out["renderer"].frame, dLt, grads, drgb=drgb)
+    torch.cuda.synchronize()
+    a = drgb.cpu().numpy().astype(np.float64)
+    vis = pre["status"] == 0
+    assert np.all(a[:, ~vis] == 0.0)
+    from gpu_helpers import EPS32, R19_C
+    n_clamped = 0
+    for ch in range(3):
+        clamped = (pre["flags"][vis] >> ch) & 1 == 1
+        n_clamped += int(clamped.sum())
+        r = np.where(clamped, 0.0, g2d[6 + ch, vis])
+        bound = np.maximum(np.maximum(1e-3 * np.abs(r), 1e-6),
+                           R19_C * EPS32 * mag[6 + ch, vis] + mag[16 + ch, vis])
+        bad = np.abs(a[ch, vis] - r) > bound
+        assert bad.sum() == 0, (case, ch, int(bad.sum()), int(vis.sum()))
+        assert np.all(a[ch, vis][clamped] == 0.0)
+    print(f"[drgb {case}] compared {int(vis.sum())} of {int(vis.sum())} visible particles, "
+          f"{n_clamped} clamped channels")
