@@ -637,7 +637,7 @@ def test_backward_launch_order():
         assert np.all(np.abs(a - b2) <= 1e-4 * np.abs(a) + 1e-6 * (1 + np.abs(a).max()))
 
 
-@pytest.mark.parametrize("case", ["config0", "config1_beta2"])
+@pytest.mark.parametrize("case", ["config0", "config1_beta2", "config0_clamped"])
 def test_drgb_output_parity(case):
     """ges_grads.drgb (optional output, the per-view colour gradient of the SH-factorised
     exchange): dL/d rgb of every visible particle against the oracle's S5a colour sums
@@ -645,15 +645,20 @@ def test_drgb_output_parity(case):
     north_star tolerance or the entry's R19 scale; exactly 0 for particles that are not
     visible."""
     sc = gi.make_config(1, beta_value=2.0, P=20000) if case == "config1_beta2" else gi.make_config(0)
+    parts = sc.particles
+    if case.endswith("clamped"):  # a third of the particles with one or two channels below 0
+        parts = parts.subset(slice(None))
+        parts.sh[0, 0::3] = -3.0
+        parts.sh[2, 0::6] = -3.0
     cam = sc.cameras[0]
     gs, osx = settings_pair(rho=0.1)
-    out = gpu_forward(sc.particles, cam, gs)
-    pre = O.preprocess(sc.particles, cam, osx, "f32")
+    out = gpu_forward(parts, cam, gs)
+    pre = O.preprocess(parts, cam, osx, "f32")
     offsets, lst = O.tile_lists(pre)
     ref = O.render_fwd(pre, cam, osx, offsets, lst)
     dL = masked_upstream(gi.upstream_grad(sc.seed, 5, cam.width, cam.height), ref["amb"])
     g2d, mag = O.render_bwd(pre, cam, osx, offsets, lst, dL, with_abs=True)
-    P = sc.particles.P
+    P = parts.P
     drgb = torch.full((3, P), 7.0, device="cuda")
     grads = G.PlanarParams.zeros(P, out["params"].sh_degree)
     dLt = torch.from_numpy(np.ascontiguousarray(dL, np.float32)).cuda()
@@ -675,3 +680,5 @@ def test_drgb_output_parity(case):
         assert np.all(a[ch, vis][clamped] == 0.0)
     print(f"[drgb {case}] compared {int(vis.sum())} of {int(vis.sum())} visible particles, "
           f"{n_clamped} clamped channels")
+    if case.endswith("clamped"):
+        assert n_clamped > 100
