@@ -682,3 +682,38 @@ def test_drgb_output_parity(case):
           f"{n_clamped} clamped channels")
     if case.endswith("clamped"):
         assert n_clamped > 100
+
+
+def test_sh_grad_from_colour_against_oracle():
+    """ges_sh_grad_from_colour over several views against the oracle: the sum over the
+    views of the oracle's S5b SH gradient of each view (oracle S5a -> S5b, fp64), the
+    GPU side fed with the views' dL/drgb from ges_grads.drgb.  Tolerance: 1e-3 of the
+    summed magnitudes of the views' terms (grad_magnitude) + 1e-6."""
+    sc = gi.make_config(2, P=20000, n_views=3)
+    parts = sc.particles
+    gs, osx = settings_pair(rho=sc.rho)
+    dev = G.PlanarParams.from_inputs(parts)
+    P, V = dev.P, len(sc.cameras)
+    cam0 = sc.cameras[0]
+    r = G.Renderer(P, cam0.width, cam0.height)
+    grads = G.PlanarParams.zeros(P, dev.sh_degree)
+    drgb = torch.zeros((V, 3, P), device="cuda")
+    want = np.zeros((3 * parts.K, P))
+    mag = np.zeros((3 * parts.K, P))
+    for v, cam in enumerate(sc.cameras):
+        pre = O.preprocess(parts, cam, osx, "f32")
+        offsets, lst = O.tile_lists(pre)
+        ref = O.render_fwd(pre, cam, osx, offsets, lst)
+        dL = masked_upstream(gi.upstream_grad(sc.seed, v, cam.width, cam.height), ref["amb"])
+        g2d, gabs = O.render_bwd(pre, cam, osx, offsets, lst, dL, with_abs=True)
+        want += O.backward_particles(parts, cam, osx, g2d, pre["status"], pre["flags"])["sh"]
+        mag += O.grad_magnitude(parts, cam, osx, gabs, pre["status"], pre["flags"])["sh"]
+        r.forward(dev, cam, gs)
+        dLt = torch.from_numpy(np.ascontiguousarray(dL, np.float32)).cuda()
+        G.ges_render_bwd(dev, cam, gs, r.frame, dLt, grads, drgb=drgb[v])
+    got = G.sh_grad_from_colour(dev, G.camera_rows(sc.cameras), drgb).cpu().numpy().astype(np.float64)
+    bad = np.abs(got - want) > 1e-3 * mag + 1e-6
+    assert bad.sum() == 0, (int(bad.sum()), float(np.abs(got - want).max()))
+    nz = int((np.abs(want) > 0).any(axis=0).sum())
+    assert nz > 0.2 * P
+    print(f"[sh from colour] {V} views, {nz} particles with an SH gradient, all {3 * parts.K * P} entries compared")
