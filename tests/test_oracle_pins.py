@@ -680,3 +680,38 @@ def test_r18_both_branches_skip_decision_closed_form():
                                                                                        atol=1e-12) for i in (0, 1))
     assert np.isnan(alt[1][:, 16, 16]).all()          # one ambiguous decision only
     assert np.isnan(alt[0][:, 0, 0]).all() and ref["amb"][0, 0] == 0   # unflagged pixel
+
+
+def test_sh_gradient_factorises_per_view():
+    """The SH part of S5b is the outer product Y_k(u) * dL/drgb (zero through a clamped
+    channel, R13) per view -- the identity the SH-factorised view-DP exchange rests on
+    (DESIGN.md §8): the oracle's SH gradient against the pinned SH basis (orthonormal, above)
+    evaluated at u = (mean - camera centre) / |.|, times its own S5a colour sums, for each of
+    two views."""
+    sc = gi.make_config(2, P=300, n_views=2)
+    parts = sc.particles
+    st = O.Settings(rho=sc.rho)
+    K = parts.K
+    total = np.zeros((3 * K, parts.P))
+    for v, cam in enumerate(sc.cameras):
+        pre = O.preprocess(parts, cam, st, "f32")
+        offsets, lst = O.tile_lists(pre)
+        g = gi.upstream_grad(sc.seed, v, cam.width, cam.height).astype(np.float64)
+        g2d = O.render_bwd(pre, cam, st, offsets, lst, g)
+        sh = O.backward_particles(parts, cam, st, g2d, pre["status"], pre["flags"])["sh"]
+        total += sh
+        R = np.asarray(cam.R, np.float64).reshape(3, 3)
+        centre = -R.T @ np.asarray(cam.t, np.float64).reshape(3)
+        vis = np.nonzero(pre["status"] == 0)[0]
+        assert vis.size > 20
+        want = np.zeros_like(sh)
+        for i in vis:
+            d = parts.mean[:, i].astype(np.float64) - centre
+            Y = O.sh_basis(d / np.linalg.norm(d), K)
+            for ch in range(3):
+                if not (pre["flags"][i] >> ch) & 1:
+                    want[ch::3, i] = Y * g2d[6 + ch, i]
+        scale = np.abs(want).max()
+        assert np.abs(sh - want).max() <= 1e-9 * scale
+        assert np.all(sh[:, pre["status"] != 0] == 0.0)
+    assert np.count_nonzero(total) > 0
