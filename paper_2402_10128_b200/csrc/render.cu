@@ -25,6 +25,7 @@
 // (red.global.add.f32) into the particle's 12-float raw-moment record.
 #include <cstddef>
 #include <cstdlib>
+#include <type_traits>
 
 #include "ges_internal.h"
 
@@ -124,6 +125,56 @@ __device__ __forceinline__ float fast_rcp(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
+}
+
+// Two fp32 values in one 64-bit register pair, for the packed sm_100 instructions
+// (FADD2 / FMUL2 / FFMA2: one issue slot for two IEEE round-to-nearest operations, each
+// lane's result identical to the scalar instruction's).  A scalar operand broadcast with
+// f2_bc costs nothing: ptxas folds it into the instruction's .F32 operand form.
+typedef unsigned long long f2;
+#if !defined(GES_F32X2) && !defined(GES_NO_F32X2)
+#define GES_F32X2 1  // S5a's Gaussian entry loop on pixel pairs (GES_NO_F32X2: scalar)
+#endif
+#ifdef GES_F32X2
+constexpr bool kF32x2 = true;
+#else
+constexpr bool kF32x2 = false;
+#endif
+__device__ __forceinline__ f2 f2_pk(float a, float b) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2_bc(float a) { return f2_pk(a, a); }
+__device__ __forceinline__ float f2_lo(f2 r) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+    return a;
+}
+__device__ __forceinline__ float f2_hi(f2 r) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(r));
+    return b;
+}
+__device__ __forceinline__ f2 f2_add(f2 a, f2 b) {
+    f2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2_sub(f2 a, f2 b) {
+    f2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2_mul(f2 a, f2 b) {
+    f2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 f2_fma(f2 a, f2 b, f2 c) {
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
 }
 
 // Minimum of Q = a x^2 + b x y + c y^2 (a, c > 0, 4ac > b^2) over the box
@@ -666,6 +717,19 @@ __global__ void GES_RBWD_LB(kBwdHalf ? 32 : Layout<PPT>::kThreads, PPT) render_b
         U[k] = Tfin * (gr[k] * a.bg[0] + gg[k] * a.bg[1] + gb[k] * a.bg[2]);
         my_max = max(my_max, last[k]);
     }
+#ifdef GES_F32X2
+    // pixels 2h, 2h + 1 of the thread as register pairs (the Gaussian entry loop)
+    f2 Tp[PPT / 2], Up[PPT / 2], grp[PPT / 2], ggp[PPT / 2], gbp[PPT / 2], pyp[PPT / 2];
+#pragma unroll
+    for (int h = 0; h < PPT / 2; ++h) {
+        Tp[h] = f2_pk(T[2 * h], T[2 * h + 1]);
+        Up[h] = f2_pk(U[2 * h], U[2 * h + 1]);
+        grp[h] = f2_pk(gr[2 * h], gr[2 * h + 1]);
+        ggp[h] = f2_pk(gg[2 * h], gg[2 * h + 1]);
+        gbp[h] = f2_pk(gb[2 * h], gb[2 * h + 1]);
+        pyp[h] = f2_pk((float)(py0 + 8 * h) + 0.5f, (float)(py0 + 8 * h + 4) + 0.5f);
+    }
+#endif
     if (tid == 0) S.max = 0;
     __syncthreads();
     const uint32_t warp_max = __reduce_max_sync(0xffffffffu, my_max);
@@ -771,7 +835,67 @@ __global__ void GES_RBWD_LB(kBwdHalf ? 32 : Layout<PPT>::kThreads, PPT) render_b
             // The Gaussian path accumulates kappa q = alpha' dL/dalpha (kappa, a
             // per-particle constant, is divided out in S5b).
             float amax = 0.0f;
+#ifdef GES_F32X2
+            // the same per-pixel arithmetic on pixel pairs with FADD2 / FMUL2 / FFMA2 (the
+            // exponent, alpha and the skip decision bit-identical to the scalar form and the
+            // forward's); the sums accumulate per pair half and are added at the end
+            {
+                const f2 kap = f2_bc(g1.y), C2 = f2_bc(g1.x), c1 = f2_bc(ec.c1), c0 = f2_bc(ec.c0);
+                const f2 gy = f2_bc(g0.y), one = f2_bc(1.0f);
+                const f2 cz = f2_bc(g1.z), cw = f2_bc(g1.w), cb = f2_bc(rb);
+                f2 s0 = 0ull, s1 = 0ull, s2 = 0ull, sr = 0ull, sg = 0ull, sb = 0ull;
+                auto pairs = [&](auto clamp_tag) {
+                    constexpr bool CLAMP = decltype(clamp_tag)::value;
+#pragma unroll
+                    for (int h = 0; h < PPT / 2; ++h) {
+                        const f2 dy = f2_sub(gy, pyp[h]);
+                        const f2 p2 = f2_fma(dy, f2_fma(C2, dy, c1), c0);
+                        const f2 araw = f2_mul(kap, f2_pk(fast_exp2(f2_lo(p2)), fast_exp2(f2_hi(p2))));
+                        float a0 = f2_lo(araw), a1 = f2_hi(araw);
+                        if (CLAMP) { a0 = fminf(kAlphaMax, a0); a1 = fminf(kAlphaMax, a1); }
+                        a0 = a0 >= thr[2 * h] ? a0 : 0.0f;
+                        a1 = a1 >= thr[2 * h + 1] ? a1 : 0.0f;
+                        amax = fmaxf(amax, fmaxf(a0, a1));
+                        const f2 al = f2_pk(a0, a1);
+                        const f2 om = f2_sub(one, al);
+                        const f2 inv = f2_pk(fast_rcp(f2_lo(om)), fast_rcp(f2_hi(om)));
+                        const f2 Tk = f2_mul(Tp[h], inv);  // transmittance before this entry
+                        const f2 cg = f2_fma(cz, grp[h], f2_fma(cw, ggp[h], f2_mul(cb, gbp[h])));
+                        const f2 w = f2_mul(al, Tk);
+                        const f2 dal = f2_sub(f2_mul(Tk, cg), f2_mul(Up[h], inv));
+                        Up[h] = f2_fma(cg, w, Up[h]);
+                        sr = f2_fma(w, grp[h], sr);
+                        sg = f2_fma(w, ggp[h], sg);
+                        sb = f2_fma(w, gbp[h], sb);
+                        f2 q;
+                        if (CLAMP) {  // no gradient through the clamp (R13): q = araw dL/dalpha
+                            const f2 qr = f2_mul(araw, dal);
+                            const float q0 = (a0 > 0.0f && f2_lo(araw) < kAlphaMax) ? f2_lo(qr) : 0.0f;
+                            const float q1 = (a1 > 0.0f && f2_hi(araw) < kAlphaMax) ? f2_hi(qr) : 0.0f;
+                            q = f2_pk(q0, q1);
+                        } else {
+                            q = f2_mul(al, dal);  // kappa G dL/dalpha where composited
+                        }
+                        s0 = f2_add(s0, q);
+                        const f2 t = f2_mul(q, dy);
+                        s1 = f2_add(s1, t);
+                        s2 = f2_fma(t, dy, s2);
+                        Tp[h] = Tk;
+                    }
+                };
+                if (!(g1.y > kAlphaMax)) pairs(std::false_type{});  // warp-uniform
+                else pairs(std::true_type{});
+                S0 = f2_lo(s0) + f2_hi(s0);
+                S1 = f2_lo(s1) + f2_hi(s1);
+                S2 = f2_lo(s2) + f2_hi(s2);
+                dr = f2_lo(sr) + f2_hi(sr);
+                dgc = f2_lo(sg) + f2_hi(sg);
+                dbc = f2_lo(sb) + f2_hi(sb);
+            }
+            if (false) {
+#else
             if (!(g1.y > kAlphaMax)) {  // warp-uniform: alpha cannot reach the 0.99 clamp
+#endif
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) {
                     const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
@@ -795,7 +919,7 @@ __global__ void GES_RBWD_LB(kBwdHalf ? 32 : Layout<PPT>::kThreads, PPT) render_b
                     S2 += t * dy;
                     T[k] = Tk;
                 }
-            } else {  // alpha = min(0.99, kappa G): no gradient through the clamp (R13)
+            } else if (!kF32x2) {  // alpha = min(0.99, kappa G): no gradient through the clamp (R13)
 #pragma unroll
                 for (int k = 0; k < PPT; ++k) {
                     const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
