@@ -459,6 +459,11 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
         if (!(px < a.W && py0 + 4 * k < a.H)) { done |= 1u << k; thr[k] = 2.0f; }
     }
     constexpr uint32_t kAll = (1u << PPT) - 1u;
+    // the plain Gaussian instance runs a thread's two pixels as one register pair with the
+    // packed FP32 instructions (same per-lane results: the image is bit-identical)
+    constexpr bool kPk = kF32x2 && !EXACT && !DIAG && PPT == 2;
+    f2 Tp = f2_pk(T[0], T[PPT - 1]), crp = 0ull, cgp = 0ull, cbp = 0ull;
+    const f2 pyp = f2_pk((float)py0 + 0.5f, (float)(py0 + 4) + 0.5f);
     StagedBatch sb{S.g0, S.g1, S.b, nullptr, S.mask, S.hb};
     uint32_t sbase = smem_addr(&S);
     uint32_t a_list = smem_addr(S.list[warp]);
@@ -498,6 +503,40 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
             // clamped at 0: the form is >= 0 up to rounding, G exceeds 1 by <= 2^-22 -- R19b.)
             float al[PPT], w[PPT], Tn[PPT];
             float tmin = 1.0f;
+            if constexpr (kPk) {
+                const f2 dy = f2_sub(f2_bc(g0.y), pyp);
+                const f2 p2 = f2_fma(dy, f2_fma(f2_bc(g1.x), dy, f2_bc(ec.c1)), f2_bc(ec.c0));
+                const f2 araw = f2_mul(f2_bc(g1.y), f2_pk(fast_exp2(f2_lo(p2)), fast_exp2(f2_hi(p2))));
+                float a0 = f2_lo(araw), a1 = f2_hi(araw);
+                if (clampk) { a0 = fminf(kAlphaMax, a0); a1 = fminf(kAlphaMax, a1); }
+                al[0] = a0 >= thr[0] ? a0 : 0.0f;
+                al[1] = a1 >= thr[1] ? a1 : 0.0f;
+                const f2 wp = f2_mul(f2_pk(al[0], al[1]), Tp);
+                const f2 Tnp = f2_sub(Tp, wp);
+                tmin = fminf(tmin, fminf(f2_lo(Tnp), f2_hi(Tnp)));
+                if (!__any_sync(0xffffffffu, tmin < kTMin)) {
+                    crp = f2_fma(f2_bc(g1.z), wp, crp);
+                    cgp = f2_fma(f2_bc(g1.w), wp, cgp);
+                    cbp = f2_fma(f2_bc(gbl), wp, cbp);
+#pragma unroll
+                    for (int k = 0; k < PPT; ++k) last[k] = al[k] > 0.0f ? pos1 : last[k];
+                    Tp = Tnp;
+                } else {
+                    const bool st0 = f2_lo(Tnp) < kTMin, st1 = f2_hi(Tnp) < kTMin;
+                    const f2 wk = f2_pk(st0 ? 0.0f : f2_lo(wp), st1 ? 0.0f : f2_hi(wp));
+                    crp = f2_fma(f2_bc(g1.z), wk, crp);
+                    cgp = f2_fma(f2_bc(g1.w), wk, cgp);
+                    cbp = f2_fma(f2_bc(gbl), wk, cbp);
+                    last[0] = (!st0 && al[0] > 0.0f) ? pos1 : last[0];
+                    last[1] = (!st1 && al[1] > 0.0f) ? pos1 : last[1];
+                    Tp = f2_pk(st0 ? f2_lo(Tp) : f2_lo(Tnp), st1 ? f2_hi(Tp) : f2_hi(Tnp));
+                    thr[0] = st0 ? 2.0f : thr[0];
+                    thr[1] = st1 ? 2.0f : thr[1];
+                    done |= (st0 ? 1u : 0u) | (st1 ? 2u : 0u);
+                    if (__all_sync(0xffffffffu, done == kAll)) break;  // done changes only here
+                }
+                continue;
+            }
 #pragma unroll
             for (int k = 0; k < PPT; ++k) {
                 const float dy = __fsub_rn(g0.y, (float)(py0 + 4 * k) + 0.5f);
@@ -540,6 +579,12 @@ __global__ void GES_RFWD_LB(Layout<PPT>::kThreads) render_fwd_kernel(RenderFwdAr
         }
     }
     wait_ids();  // no copy into shared memory outlives the CTA
+    if constexpr (kPk) {
+        T[0] = f2_lo(Tp); T[PPT - 1] = f2_hi(Tp);
+        cr[0] = f2_lo(crp); cr[PPT - 1] = f2_hi(crp);
+        cg[0] = f2_lo(cgp); cg[PPT - 1] = f2_hi(cgp);
+        cb[0] = f2_lo(cbp); cb[PPT - 1] = f2_hi(cbp);
+    }
     {
         // S5a's launch order (ges_frame.tile_order): a backward CTA lasts as long as its
         // longer walk, so the tile's cost is its largest n_contrib (measured against the
